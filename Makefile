@@ -1,0 +1,19 @@
+# Build the sm_100a shared library (C ABI) and the CPU oracle.
+NVCC ?= nvcc
+ARCH := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -shared -Xptxas -v
+PKG := paper_2411_00033_b200
+SRCS := $(PKG)/csrc/lc_plan.cu $(PKG)/csrc/lc_exec.cu
+HDRS := $(PKG)/csrc/lc_internal.h include/legcheb.h
+
+all: $(PKG)/liblegcheb.so oracle/liboracle.so
+
+$(PKG)/liblegcheb.so: $(SRCS) $(HDRS)
+	$(NVCC) $(NVFLAGS) $(SRCS) -o $@ 2> build/ptxas.log || (cat build/ptxas.log; exit 1)
+
+oracle/liboracle.so: oracle/oracle.c
+	gcc -O2 -fno-fast-math -ffp-contract=off -fopenmp -shared -fPIC $< -o $@ -lm
+
+clean:
+	rm -f $(PKG)/liblegcheb.so oracle/liboracle.so
+.PHONY: all clean

@@ -1,0 +1,164 @@
+/*
+ * legcheb.h -- C ABI of the B200 (sm_100a) execution stage of the modal FMM
+ * Legendre<->Chebyshev coefficient transform of arXiv 2411.00033.
+ *
+ * Citations "PAPER.md:L" are lines of the paper's LaTeX source; equation and
+ * algorithm names are its LaTeX labels.
+ *
+ *   leg2cheb (L2C):  f_cheb = C^{-1} A f_leg                         PAPER.md:29-32 (eq:directmv)
+ *   cheb2leg (C2L):  f_leg  = A^{-1} C f_cheb                        PAPER.md:29-32 (eq:directmv)
+ *   a_{i,i+2k} = Lambda(k) Lambda(i+k),  Lambda(x) = Gamma(x+1/2)/Gamma(x+1)
+ *   C = diag(c_i pi/2), c_0 = 2, c_i = 1
+ *
+ * The transform is evaluated with the paper's O(N) algorithm (Alg. 4,
+ * alg:fastercomplete): leaf projection (step 1), upward
+ * modal transfer with the exact triangular B(l) (step 2, eq:wtk, Alg. a.1),
+ * low-rank M2L with the precomputed M x M Chebyshev coefficient matrices
+ * A_hat (step 3, eq:aklmore), the "faster downward spreading" B(p)^T
+ * (step 4), leaf evaluation (step 5), the direct near-diagonal band
+ * (step 6, Alg. 1 restricted to j < j_end(i) = min(N, 2s(floor(i/2s)+2))) and
+ * C^{-1} (step 7).  C2L uses the kernel L(x,y) of eq:Lxymod
+ * in the band and in A_hat.  Both parities share one A_hat.
+ *
+ * Conventions common to all entry points
+ * --------------------------------------
+ *  - All floating point data are IEEE fp64 (double).
+ *  - Device pointers are CUDA device addresses on the plan's device; host
+ *    pointers are ordinary (preferably page-locked) host addresses.
+ *  - Nothing here throws; every function returns an lc_status.  A CUDA
+ *    error detected during a call is returned as LC_ERR_CUDA; asynchronous
+ *    kernel faults surface at the caller's next synchronisation.
+ *  - Thread safety: a plan is immutable after lc_plan_create and may be
+ *    shared by threads; concurrent lc_execute calls on one plan need
+ *    distinct workspaces (a NULL workspace means the plan-owned one, which
+ *    serialises calls on one stream only).
+ */
+#ifndef LEGCHEB_H_
+#define LEGCHEB_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct lc_plan lc_plan; /* opaque; immutable after create */
+
+typedef enum { LC_LEG2CHEB = 0, LC_CHEB2LEG = 1 } lc_direction;
+
+/* Batch layouts of in/out.  VEC: in[v*ld + j] (vector-contiguous, default);
+ * BATCH: in[j*ld + v] (batch-contiguous, e.g. the second pass of a 2-D
+ * tensor-product transform). */
+typedef enum { LC_VEC_CONTIGUOUS = 0, LC_BATCH_CONTIGUOUS = 1 } lc_layout;
+
+typedef enum {
+  LC_OK = 0,
+  LC_ERR_INVALID_ARG = 1,
+  LC_ERR_UNSUPPORTED_DEVICE = 2,
+  LC_ERR_OUT_OF_MEMORY = 3,
+  LC_ERR_CUDA = 4,
+  LC_ERR_ALIASING = 5,
+  LC_ERR_INTERNAL = 6
+} lc_status;
+
+typedef struct {
+  int64_t s_hat;    /* preferred smallest-submatrix half size s_hat (eq:numlevels); 0 -> 32 */
+  int32_t M;        /* Chebyshev modes per axis; only 18 is supported; 0 -> 18 */
+  int32_t layout;   /* lc_layout of in/out */
+  int64_t ld_in;    /* leading dimension of in  (elements); 0 -> n (VEC) or batch (BATCH) */
+  int64_t ld_out;   /* leading dimension of out (elements); 0 -> n (VEC) or batch (BATCH) */
+  int32_t device;   /* CUDA device ordinal; -1 -> current device */
+  int32_t vt;       /* vectors per CTA tile; 0 -> automatic */
+  int32_t subtree;  /* subtree depth k of the execution kernels; 0 -> automatic */
+  int32_t stage_blocks; /* FMM blocks (3 A_hat each) per TMA bulk-copy stage; 0 -> automatic */
+  int32_t stages;   /* bulk-copy ring depth; 0 -> automatic */
+} lc_plan_opts;
+
+/* Geometry and algorithmic work of a plan (per vector unless stated). */
+typedef struct {
+  int64_t n;          /* user length */
+  int64_t N;          /* padded length s*2^(L+2)                 (eq:Ntot) */
+  int64_t L;          /* number of levels                          (eq:numlevels) */
+  int64_t s;          /* smallest half size h_{L-1} */
+  int64_t M;          /* modes per axis (18) */
+  int64_t batch;      /* vectors per execute */
+  int64_t nc;         /* number of A_hat matrices N_c = 3(N/2s-L-2) (eq:total_blocks_and_mats) */
+  int64_t direction;  /* lc_direction */
+  int64_t band_nnz;   /* nonzeros of A in the direct band (exact count) */
+  size_t plan_bytes;  /* device bytes owned by the plan (A_hat arena, tables) */
+  size_t workspace_bytes; /* bytes lc_execute needs as workspace */
+  double flops_alg;   /* algorithmic flops per vector: 2 nnz_band + 16 b_{L-1} s M + 4 N_c M^2 + 8(M^2+2M)(2^L-L-1) + n */
+  double bytes_alg;   /* algorithmic HBM bytes per execute: 16 n batch + 8 M^2 N_c + 8 N */
+  int32_t vt, subtree, stage_blocks, stages; /* chosen kernel configuration */
+  int32_t kernels_per_execute;               /* kernel launches per lc_execute */
+} lc_plan_desc;
+
+/* Host-only geometry (no GPU needed): fills n, N, L, s, M, nc, band_nnz,
+ * flops_alg (batch = 1), bytes_alg (batch = 1).  s_hat <= 0 -> 32.
+ * Errors: LC_ERR_INVALID_ARG if n < 1 or out == NULL. */
+lc_status lc_geometry(int64_t n, int64_t s_hat, lc_plan_desc* out);
+
+/* Create a plan: precomputes on the device lambda (and for C2L the band
+ * tables), the level/block hierarchy, B(0) (App. A3, exact), the
+ * finest-level Vandermonde T(sigma) (eq:Xs) and the N_c A_hat matrices
+ * (eq:aklmore, sampled at Chebyshev-Gauss points, 2-D DCT-II), level-major
+ * in (level, block, r) order (eq:cfrompq).  batch >= 1 vectors per execute.
+ * opts may be NULL (defaults).  Allocates a plan-owned workspace.
+ * Errors: INVALID_ARG (n < 1, batch < 1, M != 18, bad layout/ld),
+ * UNSUPPORTED_DEVICE (not compute capability 10.x), OUT_OF_MEMORY, CUDA. */
+lc_status lc_plan_create(lc_plan** out, int64_t n, lc_direction dir, int64_t batch, const lc_plan_opts* opts);
+
+lc_status lc_plan_describe(const lc_plan* p, lc_plan_desc* out);
+
+/* Bytes of workspace lc_execute needs. */
+size_t lc_workspace_bytes(const lc_plan* p);
+
+/* Zero-initialise a caller-owned workspace before its first use with any
+ * plan (enqueued on stream).  Plan-owned workspaces are initialised at create. */
+lc_status lc_workspace_init(const lc_plan* p, void* workspace, void* stream);
+
+/* Execute the transform of `batch` vectors: out = T(in), enqueue-only on
+ * `stream` (a cudaStream_t; NULL = legacy default stream).
+ *   in:  device, batch vectors of n doubles in the plan's layout; unmodified.
+ *   out: device, same shape; must not overlap in (LC_ERR_ALIASING).
+ *   workspace: device, >= lc_workspace_bytes(p), zero-initialised once, or
+ *              NULL for the plan-owned workspace.
+ * Outputs are the first n entries of the transform of the zero-padded input. */
+lc_status lc_execute(const lc_plan* p, const double* in, double* out, void* workspace, void* stream);
+
+/* As lc_execute, and records ev[0] before the first kernel, ev[i] after
+ * kernel i (i = 1..kernels_per_execute).  ev are cudaEvent_t handles; nev
+ * must be >= kernels_per_execute + 1.  Used by bench.py for per-kernel times. */
+lc_status lc_execute_timed(const lc_plan* p, const double* in, double* out, void* workspace, void* stream,
+                           void* const* ev, int32_t nev);
+
+/* End-to-end call with HOST buffers: copies h_in (batch vectors, layout and
+ * leading dimensions of the plan) to plan-owned device staging, executes,
+ * copies the result to h_out, all enqueued on stream (no host sync).  Host
+ * buffers should be page-locked for asynchronous copies. */
+lc_status lc_execute_host(const lc_plan* p, const double* h_in, double* h_out, void* stream);
+
+/* Copy plan data to host memory (synchronous; test/diagnostic use).
+ * what: 0 band table B (length N: lambda_m for L2C, rho_m for C2L),
+ *       1 band table A (length 2s: lambda_k for L2C, kappa_k for C2L),
+ *       2 A_hat arena (nc*M*M, row-major per matrix, level-major order),
+ *       3 B(0) (M*M row-major), 4 T(sigma) (2*s*M, [sigma][m][k]).
+ * count = number of doubles host_out can hold; returns INVALID_ARG if short. */
+lc_status lc_plan_export(const lc_plan* p, int32_t what, double* host_out, int64_t count);
+
+lc_status lc_plan_destroy(lc_plan* p);
+
+const char* lc_status_string(lc_status s);
+
+/* Version string of the library. */
+const char* lc_version(void);
+
+/* Name and description of the last CUDA error seen by this thread inside the
+ * library (for messages accompanying LC_ERR_CUDA / LC_ERR_OUT_OF_MEMORY). */
+const char* lc_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LEGCHEB_H_ */

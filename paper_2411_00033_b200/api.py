@@ -1,0 +1,176 @@
+"""Python API over the C ABI: plans and transforms on torch CUDA tensors.
+
+    plan = Plan(n, "leg2cheb", batch=V)          # lc_plan_create
+    z = plan.execute(x)                          # lc_execute on torch's current stream
+    leg2cheb(x), cheb2leg(x)                     # cached-plan conveniences
+
+PyTorch provides device memory and streams only; the transform itself is the
+sm_100a kernels of liblegcheb.so (Alg. 4, alg:fastercomplete).
+"""
+from __future__ import annotations
+
+import ctypes
+import threading
+
+import numpy as np
+import torch
+
+from . import _lib
+
+DIRECTIONS = {"leg2cheb": 0, "l2c": 0, 0: 0, "cheb2leg": 1, "c2l": 1, 1: 1}
+LAYOUTS = {"vec": 0, "batch": 1, 0: 0, 1: 1}
+EXPORTS = {"tabB": 0, "tabA": 1, "ahat": 2, "B": 3, "T": 4}
+
+
+def geometry(n: int, s_hat: int = 32) -> dict:
+    """Host-only decomposition (eq:numlevels, eq:Ntot, eq:total_blocks_and_mats) and work model."""
+    d = _lib.PlanDesc()
+    _lib.check("lc_geometry", _lib.load().lc_geometry(int(n), int(s_hat), ctypes.byref(d)))
+    return d.as_dict()
+
+
+def _stream_handle(stream) -> int:
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return int(stream.cuda_stream) if hasattr(stream, "cuda_stream") else int(stream)
+
+
+class Plan:
+    """A transform plan (immutable) for `batch` vectors of length n on one device."""
+
+    def __init__(self, n: int, direction="leg2cheb", batch: int = 1, device=None, s_hat: int = 32,
+                 layout="vec", ld_in: int = 0, ld_out: int = 0, vt: int = 0, subtree: int = 0,
+                 stage_blocks: int = 0, stages: int = 0):
+        lib = _lib.load()
+        if device is None:
+            device = torch.cuda.current_device()
+        device = torch.device("cuda", device) if isinstance(device, int) else torch.device(device)
+        self.device = device
+        self.n, self.batch = int(n), int(batch)
+        self.direction = DIRECTIONS[direction]
+        self.layout = LAYOUTS[layout]
+        opts = _lib.PlanOpts(s_hat=s_hat, M=18, layout=self.layout, ld_in=ld_in, ld_out=ld_out,
+                             device=device.index if device.index is not None else -1, vt=vt, subtree=subtree,
+                             stage_blocks=stage_blocks, stages=stages)
+        h = ctypes.c_void_p()
+        with torch.cuda.device(device):
+            _lib.check("lc_plan_create", lib.lc_plan_create(ctypes.byref(h), self.n, self.direction, self.batch,
+                                                            ctypes.byref(opts)))
+        self._h = h
+        self._lib = lib
+        d = _lib.PlanDesc()
+        _lib.check("lc_plan_describe", lib.lc_plan_describe(h, ctypes.byref(d)))
+        self.desc = d.as_dict()
+        self.ld_in = ld_in or (self.n if self.layout == 0 else self.batch)
+        self.ld_out = ld_out or (self.n if self.layout == 0 else self.batch)
+
+    # -- lifetime
+    def close(self):
+        if getattr(self, "_h", None) and self._h.value:
+            self._lib.lc_plan_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def handle(self):
+        return self._h
+
+    @property
+    def workspace_bytes(self) -> int:
+        return int(self._lib.lc_workspace_bytes(self._h))
+
+    @property
+    def kernels_per_execute(self) -> int:
+        return int(self.desc["kernels_per_execute"])
+
+    def _shape(self):
+        return (self.batch, self.ld_in) if self.layout == 0 else (self.n, self.ld_in)
+
+    def _check(self, x: torch.Tensor, what: str):
+        if x.device != self.device or x.dtype != torch.float64 or not x.is_contiguous():
+            raise ValueError(f"{what}: need a contiguous float64 tensor on {self.device}")
+
+    def new_workspace(self, stream=None) -> torch.Tensor:
+        ws = torch.empty(max(1, self.workspace_bytes), dtype=torch.uint8, device=self.device)
+        _lib.check("lc_workspace_init", self._lib.lc_workspace_init(self._h, ctypes.c_void_p(ws.data_ptr()),
+                                                                    ctypes.c_void_p(_stream_handle(stream))))
+        return ws
+
+    # -- execution
+    def execute(self, x: torch.Tensor, out: torch.Tensor | None = None, workspace: torch.Tensor | None = None,
+                stream=None) -> torch.Tensor:
+        """out = transform(x) on the device; x is [batch, n] (vec layout) or [n, batch] (batch layout)."""
+        self._check(x, "input")
+        if out is None:
+            out = torch.empty_like(x)
+        self._check(out, "output")
+        ws = ctypes.c_void_p(workspace.data_ptr()) if workspace is not None else ctypes.c_void_p()
+        _lib.check("lc_execute", self._lib.lc_execute(self._h, ctypes.c_void_p(x.data_ptr()),
+                                                      ctypes.c_void_p(out.data_ptr()), ws,
+                                                      ctypes.c_void_p(_stream_handle(stream))))
+        return out
+
+    def execute_timed(self, x: torch.Tensor, out: torch.Tensor, events, stream=None) -> None:
+        """lc_execute that records CUDA events around each kernel (events: list of torch.cuda.Event)."""
+        arr = (ctypes.c_void_p * len(events))(*[ctypes.c_void_p(e.cuda_event) for e in events])
+        _lib.check("lc_execute_timed", self._lib.lc_execute_timed(
+            self._h, ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(),
+            ctypes.c_void_p(_stream_handle(stream)), arr, len(events)))
+
+    def execute_host(self, h_in: torch.Tensor, h_out: torch.Tensor, stream=None) -> None:
+        """End-to-end call with HOST buffers (H2D, transform, D2H enqueued on stream; no sync)."""
+        for t in (h_in, h_out):
+            if t.device.type != "cpu" or t.dtype != torch.float64 or not t.is_contiguous():
+                raise ValueError("execute_host needs contiguous float64 host tensors")
+        _lib.check("lc_execute_host", self._lib.lc_execute_host(
+            self._h, ctypes.c_void_p(h_in.data_ptr()), ctypes.c_void_p(h_out.data_ptr()),
+            ctypes.c_void_p(_stream_handle(stream))))
+
+    def export(self, what: str) -> np.ndarray:
+        """Copy plan data to the host: tabB, tabA, ahat, B, T (tests/diagnostics)."""
+        lens = {"tabB": self.desc["N"], "tabA": 2 * self.desc["s"], "ahat": self.desc["nc"] * 324, "B": 324,
+                "T": 2 * self.desc["s"] * 18}
+        out = np.zeros(max(1, lens[what]), dtype=np.float64)
+        _lib.check("lc_plan_export", self._lib.lc_plan_export(
+            self._h, EXPORTS[what], out.ctypes.data_as(_lib.c_dp), out.size))
+        return out[: lens[what]]
+
+
+_cache: dict = {}
+_cache_lock = threading.Lock()
+
+
+def _cached(n, direction, batch, device) -> Plan:
+    key = (n, DIRECTIONS[direction], batch, str(device))
+    with _cache_lock:
+        p = _cache.get(key)
+        if p is None:
+            p = Plan(n, direction, batch, device)
+            _cache[key] = p
+        return p
+
+
+def _run(x: torch.Tensor, direction) -> torch.Tensor:
+    squeeze = x.dim() == 1
+    x2 = x.reshape(1, -1) if squeeze else x
+    if x2.dim() != 2:
+        raise ValueError("expected [n] or [batch, n]")
+    x2 = x2.contiguous()
+    p = _cached(x2.shape[1], direction, x2.shape[0], x2.device)
+    out = p.execute(x2)
+    return out.reshape(-1) if squeeze else out
+
+
+def leg2cheb(x: torch.Tensor) -> torch.Tensor:
+    """Chebyshev coefficients of the Legendre series x (last axis), f_cheb = C^{-1} A f_leg."""
+    return _run(x, "leg2cheb")
+
+
+def cheb2leg(x: torch.Tensor) -> torch.Tensor:
+    """Legendre coefficients of the Chebyshev series x (last axis), f_leg = A^{-1} C f_cheb."""
+    return _run(x, "cheb2leg")

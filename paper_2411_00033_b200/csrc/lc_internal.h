@@ -1,0 +1,137 @@
+// lc_internal.h -- internal definitions shared by the planner and the
+// execution kernels of the B200 Legendre<->Chebyshev library.
+//
+// Notation follows arXiv 2411.00033: levels g = 0..L-1, h_g =
+// s 2^(L-g-1), b_g = 2^(g+1)-1 blocks, three submatrices r = 0,1,2 per block
+// (eq:cfrompq), M = 18 Chebyshev modes.  DESIGN.md "Data layout" defines the
+// segment indexing used here: level g cuts the padded vector into 2^(g+2)
+// segments of length 2h_g; column block (g,b,q) is segment t = 2b+q+2
+// (eq:globalij), row block (g,b,p) is segment u = 2b+p; segment t of level g
+// is segments 2t, 2t+1 of level g+1 (eq:flevels, eq:zlevels).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/legcheb.h"
+
+namespace lc {
+
+constexpr int kM = 18;               // Chebyshev modes
+constexpr int kMM = kM * kM;
+constexpr int kThreads = 256;        // threads per CTA of the execution kernels
+constexpr int kMaxStages = 96;       // max bulk-copy stages per CTA (stage table size)
+
+// First A_hat index of level g in the level-major (g, b, r) arena:
+// 3 * sum_{g'<g} b_g' = 3 (2^(g+1) - 2 - g).
+__host__ __device__ inline int64_t ahat_level_offset(int g) {
+  return 3 * ((int64_t(2) << g) - 2 - g);
+}
+// Segments on level g (all of them; rows u < 2^(g+2)-2 carry M2L, columns t >= 2 carry w).
+__host__ __device__ inline int64_t nseg(int g) { return int64_t(4) << g; }
+// Offset (in units of VT*M doubles) of level g inside one vector tile of w:
+// sum_{g'<g} 2 * 2^(g'+2) = 2 (2^(g+2) - 4).
+__host__ __device__ inline int64_t w_level_offset_units(int g) { return 2 * ((int64_t(4) << g) - 4); }
+
+struct Geometry {
+  int64_t n, N, L, s, nc;
+};
+
+// eq:numlevels; L clamped at 0 (band only) for n <= 4 s_hat.
+inline Geometry geometry(int64_t n, int64_t s_hat) {
+  Geometry G{};
+  int64_t lp = 0;
+  while ((s_hat << lp) < n) ++lp;
+  G.L = lp >= 2 ? lp - 2 : 0;
+  G.n = n;
+  G.s = (n + (int64_t(1) << (G.L + 2)) - 1) >> (G.L + 2);
+  G.N = G.s << (G.L + 2);
+  G.nc = G.L > 0 ? 3 * ((G.N / (2 * G.s)) - G.L - 2) : 0;  // eq:total_blocks_and_mats
+  return G;
+}
+
+// Shared-memory layout of the down kernel (host computes the size, device the offsets).
+struct DownSmem {
+  int64_t Tt, Bs, cA, cB, wwin, anc, chain, uni, bars, stab, total;  // byte offsets
+  int64_t ring_bytes, leaf_bytes;
+};
+
+struct StageDesc {
+  int j;        // subtree-relative level
+  int b0;       // first block (level-local)
+  int nb;       // blocks in stage
+  int r0;       // first r of the first block (0 except the odd-root stage: 2)
+  int nmat;     // matrices in stage
+  int pad;
+  long long mat0;  // first global A_hat index
+};
+
+__host__ __device__ inline int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+__host__ __device__ inline DownSmem down_smem_layout(int VT, int k, int s, int bps, int nst, int gr) {
+  DownSmem L{};
+  int64_t o = 0;
+  const int64_t node = int64_t(2) * VT * kM * 8;  // one segment, both parities, VT vectors
+  L.Tt = o;    o = align_up(o + int64_t(2) * kM * s * 8, 128);
+  L.Bs = o;    o = align_up(o + int64_t(kMM) * 8, 128);
+  L.cA = o;    o = align_up(o + (int64_t(1) << k) * node, 128);
+  L.cB = o;    o = align_up(o + (int64_t(1) << k) * node, 128);
+  L.wwin = o;  o = align_up(o + ((int64_t(1) << k) + 2) * node, 128);
+  L.anc = o;   o = align_up(o + int64_t(gr > 0 ? gr : 1) * node, 128);
+  L.chain = o; o = align_up(o + 2 * node, 128);
+  L.ring_bytes = int64_t(nst) * bps * 3 * kMM * 8;
+  L.leaf_bytes = (int64_t(VT) + 1) * ((int64_t(1) << k) + 2) * 2 * s * 8 + int64_t(2) * s * 8;
+  L.uni = o;   o = align_up(o + (L.ring_bytes > L.leaf_bytes ? L.ring_bytes : L.leaf_bytes), 128);
+  L.bars = o;  o = align_up(o + int64_t(nst) * 8, 128);
+  L.stab = o;  o = align_up(o + int64_t(kMaxStages) * sizeof(StageDesc), 128);
+  L.total = o;
+  return L;
+}
+
+__host__ __device__ inline int64_t up_smem_bytes(int VT, int k, int s) {
+  int64_t o = 0;
+  o = align_up(o + int64_t(2) * s * kM * 8, 128);                 // T [2][s][M]
+  o = align_up(o + int64_t(kMM) * 8, 128);                        // B
+  o = align_up(o + int64_t(VT) * (int64_t(1) << k) * 2 * s * 8, 128);  // f tile
+  o = align_up(o + ((int64_t(2) << k) - 1) * 2 * VT * kM * 8, 128);    // w tree
+  o += 16;
+  return o;
+}
+
+}  // namespace lc
+
+struct lc_plan {
+  int64_t n, N, L, s, M, batch, nc;
+  int dir;
+  int layout;
+  int64_t ld_in, ld_out;
+  int device;
+  int sm_count;
+  // kernel configuration
+  int vt, k, gr, bps, nst, group;
+  int64_t ntiles;
+  int64_t w_tile_doubles, cnt_tile_ints;
+  size_t ws_bytes;
+  size_t smem_up, smem_down;
+  // device data (plan-owned)
+  double* d_A;      // nc * M * M
+  double* d_tabB;   // N    (L2C: lambda_m; C2L: rho_m = 1/(2m(2m+1) lambda_m), rho_0 = 0)
+  double* d_tabA;   // 2s   (L2C: lambda_k; C2L: kappa_k = lambda_k/(1-2k))
+  double* d_T;      // [2][s][M]
+  double* d_Tt;     // [2][M][s]
+  double* d_B;      // [M][M]
+  void* d_ws;       // plan-owned workspace
+  double* d_stage_in;   // lc_execute_host staging (lazy)
+  double* d_stage_out;
+  size_t stage_bytes;
+  int64_t band_nnz;
+  double flops_alg, bytes_alg;
+  size_t plan_bytes;
+};
+
+namespace lc {
+// remembers the last CUDA error (thread-local) for lc_last_error(); returns LC_ERR_CUDA or OUT_OF_MEMORY
+lc_status record_cuda_error(cudaError_t e);
+lc_status launch_execute(const lc_plan* p, const double* in, double* out, void* ws, cudaStream_t st,
+                         cudaEvent_t const* ev, int nev);
+int64_t band_nnz(int64_t N, int64_t s);
+}  // namespace lc
