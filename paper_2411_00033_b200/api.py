@@ -117,6 +117,9 @@ class Plan:
 
     def execute_timed(self, x: torch.Tensor, out: torch.Tensor, events, stream=None) -> None:
         """lc_execute that records CUDA events around each kernel (events: list of torch.cuda.Event)."""
+        for e in events:  # torch creates the underlying cudaEvent_t lazily, on first record
+            if not e.cuda_event:
+                e.record(torch.cuda.current_stream(self.device) if stream is None else stream)
         arr = (ctypes.c_void_p * len(events))(*[ctypes.c_void_p(e.cuda_event) for e in events])
         _lib.check("lc_execute_timed", self._lib.lc_execute_timed(
             self._h, ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(),

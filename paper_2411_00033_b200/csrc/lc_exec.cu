@@ -129,7 +129,23 @@ __device__ __forceinline__ double l2l_entry(const double* __restrict__ src, int 
   return p ? e - o : e + o;
 }
 
+// cp.async (LDGSTS): per-element asynchronous global->shared copies, used for
+// the small gathers (w windows, band tiles) whose shared-memory destinations
+// are padded or scattered; src_bytes = 0 zero-fills (padding beyond n).
+__device__ __forceinline__ void cp_async8(void* dst, const void* src, uint32_t src_bytes) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(src_bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
 // ============================================================== up kernel
+// Step 1 (eq:wMM) and step 2 (eq:wtk / Alg. a.1) for a subtree of 2^k leaf
+// segments, then the group continuation up to level 0.
 template <int VT>
 __global__ void __launch_bounds__(kThreads) lc_up_kernel(const UpParams P) {
   extern __shared__ __align__(128) unsigned char smem[];
@@ -148,34 +164,57 @@ __global__ void __launch_bounds__(kThreads) lc_up_kernel(const UpParams P) {
   const int64_t R = blockIdx.x;
   const int64_t tile = blockIdx.y;
   griddep_launch();
-  for (int i = tid; i < 2 * s * kM; i += blockDim.x) Ts[i] = P.T[i];
-  for (int i = tid; i < kMM; i += blockDim.x) Bs[i] = P.B[i];
-  griddep_wait();  // input f may be produced by the preceding kernel
+  for (int i = tid; i < 2 * s * kM; i += blockDim.x) Ts[i] = __ldg(P.T + i);
+  for (int i = tid; i < kMM; i += blockDim.x) Bs[i] = __ldg(P.B + i);
+  griddep_wait();  // the input may be produced by the preceding kernel
 
   // stage the leaf range [R 2^k, (R+1) 2^k) of segments, zero padding beyond n
   const int64_t j0 = R * tlen;
-  for (int64_t idx = tid; idx < VT * tlen; idx += blockDim.x) {
-    const int64_t v = idx / tlen, jj = idx - v * tlen;
-    const int64_t gv = tile * VT + v, j = j0 + jj;
-    fs[idx] = (gv < P.batch && j < P.n) ? P.in[vaddr(P.layout, P.ld_in, gv, j)] : 0.0;
+  if (P.layout == LC_VEC_CONTIGUOUS) {
+    for (int64_t idx = tid; idx < VT * tlen; idx += blockDim.x) {
+      const int64_t v = idx / tlen, jj = idx - v * tlen;
+      const int64_t gv = tile * VT + v, j = j0 + jj;
+      const bool ok = gv < P.batch && j < P.n;
+      cp_async8(fs + idx, ok ? P.in + gv * P.ld_in + j : P.in, ok ? 8u : 0u);
+    }
+  } else {
+    for (int64_t idx = tid; idx < VT * tlen; idx += blockDim.x) {
+      const int64_t jj = idx / VT, v = idx - jj * VT;  // v fastest: coalesced in the batch layout
+      const int64_t gv = tile * VT + v, j = j0 + jj;
+      const bool ok = gv < P.batch && j < P.n;
+      cp_async8(fs + v * tlen + jj, ok ? P.in + j * P.ld_in + gv : P.in, ok ? 8u : 0u);
+    }
   }
+  cp_async_commit();
+  cp_async_wait<0>();
   __syncthreads();
 
-  // step 1: w(L-1)[t] = sum_m f[2s t + 2m + sigma] T(sigma)[m][.]   (eq:wMM)
+  // step 1: w(L-1)[t][k] = sum_m f[2s t + 2m + sigma] T(sigma)[m][k]   (eq:wMM)
+  // item = (v, seg, sigma, group of 6 modes); 3 lanes share each f value.
   {
     double* leaf = tree + tree_off(k);
-    const int items = nleaf * 2 * VT * kM;
+    const int items = nleaf * 2 * VT * 3;
     for (int it = tid; it < items; it += blockDim.x) {
-      const int kk = it % kM;
-      int r = it / kM;
-      const int v = r % VT;
-      r /= VT;
-      const int sg = r & 1, seg = r >> 1;
+      const int kg = it % 3;
+      int r = it / 3;
+      const int sg = r & 1;
+      r >>= 1;
+      const int seg = r % nleaf;
+      const int v = r / nleaf;
       const double* fp = fs + v * tlen + seg * seglen + sg;
-      const double* tp = Ts + sg * s * kM + kk;
-      double acc = 0.0;
-      for (int m = 0; m < s; ++m) acc = fma(fp[2 * m], tp[m * kM], acc);
-      leaf[((sg * nleaf + seg) * VT + v) * kM + kk] = acc;
+      const double* tp = Ts + sg * s * kM + 6 * kg;
+      double a0 = 0, a1 = 0, a2 = 0, a3 = 0, a4 = 0, a5 = 0;
+      for (int m = 0; m < s; ++m) {
+        const double f = fp[2 * m];
+        const double2 t01 = *reinterpret_cast<const double2*>(tp + m * kM);
+        const double2 t23 = *reinterpret_cast<const double2*>(tp + m * kM + 2);
+        const double2 t45 = *reinterpret_cast<const double2*>(tp + m * kM + 4);
+        a0 = fma(f, t01.x, a0); a1 = fma(f, t01.y, a1);
+        a2 = fma(f, t23.x, a2); a3 = fma(f, t23.y, a3);
+        a4 = fma(f, t45.x, a4); a5 = fma(f, t45.y, a5);
+      }
+      double* o = leaf + ((sg * nleaf + seg) * VT + v) * kM + 6 * kg;
+      o[0] = a0; o[1] = a1; o[2] = a2; o[3] = a3; o[4] = a4; o[5] = a5;
     }
   }
   __syncthreads();
@@ -190,14 +229,14 @@ __global__ void __launch_bounds__(kThreads) lc_up_kernel(const UpParams P) {
     const int g = P.gr + j;
     const int64_t cntd = (int64_t(1) << j) * VM;
     for (int sg = 0; sg < 2; ++sg) {
-      double* dst = wt + (w_level_offset_units(g) + sg * nseg(g) + (R << j)) * VM;
-      const double* src = tree + tree_off(j) + sg * (int64_t(1) << j) * VM;
-      for (int64_t i = tid; i < cntd; i += blockDim.x) dst[i] = src[i];
+      double2* dst = reinterpret_cast<double2*>(wt + (w_level_offset_units(g) + sg * nseg(g) + (R << j)) * VM);
+      const double2* src = reinterpret_cast<const double2*>(tree + tree_off(j) + sg * (int64_t(1) << j) * VM);
+      for (int64_t i = tid; i < cntd / 2; i += blockDim.x) dst[i] = src[i];
     }
   }
 
-  // upward continuation above the subtree roots: last arriver of each group of
-  // 2^G nodes merges them G levels up (threadfence-reduction pattern).
+  // upward continuation above the subtree roots: the last arriver of each
+  // group of 2^G nodes merges them G levels up (threadfence-reduction pattern).
   int g = P.gr;
   int64_t node = R;
   while (g > 0) {
@@ -241,8 +280,9 @@ __global__ void __launch_bounds__(kThreads) lc_up_kernel(const UpParams P) {
 }
 
 // ============================================================== down kernel
+// One CTA per (subtree of 2^k leaf row segments, tile of VT vectors).
 template <int VT, int DIR>
-__global__ void __launch_bounds__(kThreads) lc_down_kernel(const DownParams P) {
+__global__ void __launch_bounds__(kThreads, 2) lc_down_kernel(const DownParams P) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ int s_nstages;
   const int s = P.s, k = P.k, gr = P.gr, L = P.L;
@@ -250,20 +290,29 @@ __global__ void __launch_bounds__(kThreads) lc_down_kernel(const DownParams P) {
   const DownSmem SL = down_smem_layout(VT, k, s, P.bps, P.nst, gr);
   double* Tt = reinterpret_cast<double*>(smem + SL.Tt);
   double* Bs = reinterpret_cast<double*>(smem + SL.Bs);
+  double* ta = reinterpret_cast<double*>(smem + SL.ta);
   double* cA = reinterpret_cast<double*>(smem + SL.cA);
   double* cB = reinterpret_cast<double*>(smem + SL.cB);
-  double* wwin = reinterpret_cast<double*>(smem + SL.wwin);
+  double* wall = reinterpret_cast<double*>(smem + SL.wall);
   double* anc = reinterpret_cast<double*>(smem + SL.anc);
   double* chain = reinterpret_cast<double*>(smem + SL.chain);
-  double* uni = reinterpret_cast<double*>(smem + SL.uni);
+  double* ring = reinterpret_cast<double*>(smem + SL.ring);
+  double* gt = reinterpret_cast<double*>(smem + SL.gt);
+  double* tb = reinterpret_cast<double*>(smem + SL.tb);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SL.bars);
   StageDesc* stab = reinterpret_cast<StageDesc*>(smem + SL.stab);
+  const int64_t tp = SL.tp;
 
   const int64_t R = blockIdx.x;
   const int64_t tile = blockIdx.y;
   const int64_t VM = int64_t(VT) * kM;
-  const int nwmax = (1 << k) + 2;
   const int64_t slot_doubles = int64_t(P.bps) * 3 * kMM;
+  const int nleaf = 1 << k;
+  const int64_t seglen = 2 * s;
+  const int64_t U0 = R << k;
+  const int64_t i0 = U0 * seglen;
+  const int64_t rows = nleaf * seglen;
+  const int64_t tcols = (nleaf + 2) * seglen;
 
   // ---- stage table of this CTA's A_hat stream (level-major arena, contiguous per level)
   if (tid == 0) {
@@ -283,10 +332,12 @@ __global__ void __launch_bounds__(kThreads) lc_down_kernel(const DownParams P) {
           }
         } else {
           const int64_t bb0 = R << (j - 1);
-          const int64_t bend = (bb0 + (int64_t(1) << (j - 1))) < bg ? (bb0 + (int64_t(1) << (j - 1))) : bg;
+          const int64_t lim = bb0 + (int64_t(1) << (j - 1));
+          const int64_t bend = lim < bg ? lim : bg;
           for (int64_t b = bb0; b < bend; b += P.bps) {
             StageDesc d;
-            d.j = j; d.b0 = int(b); d.nb = int((bend - b) < P.bps ? (bend - b) : P.bps); d.r0 = 0; d.nmat = 3 * d.nb; d.pad = 0;
+            d.j = j; d.b0 = int(b); d.nb = int((bend - b) < P.bps ? (bend - b) : P.bps); d.r0 = 0;
+            d.nmat = 3 * d.nb; d.pad = 0;
             d.mat0 = abase + 3 * b;
             stab[ns++] = d;
           }
@@ -306,22 +357,55 @@ __global__ void __launch_bounds__(kThreads) lc_down_kernel(const DownParams P) {
     const uint32_t bytes = uint32_t(d.nmat) * kMM * 8u;
     fence_proxy_async();
     mbar_expect_tx(&bars[slot], bytes);
-    bulk_g2s(uni + slot * slot_doubles, P.A + d.mat0 * kMM, bytes, &bars[slot], pol);
+    bulk_g2s(ring + slot * slot_doubles, P.A + d.mat0 * kMM, bytes, &bars[slot], pol);
   };
   if (tid == 0 && nstages > 0) {
     pol = policy_evict_first();
     for (int st = 0; st < min(P.nst, nstages); ++st) issue(st);
   }
-  for (int i = tid; i < 2 * s * kM; i += blockDim.x) Tt[i] = P.Tt[i];
-  for (int i = tid; i < kMM; i += blockDim.x) Bs[i] = P.B[i];
+  // ---- plan constants (cp.async group 0): T(sigma)^T, B(0), band tables
+  for (int i = tid; i < 2 * s * kM / 2; i += blockDim.x) cp_async16(Tt + 2 * i, P.Tt + 2 * i);
+  for (int i = tid; i < kMM / 2; i += blockDim.x) cp_async16(Bs + 2 * i, P.B + 2 * i);
+  for (int x = tid; x < 2 * s + 2 * kBandR; x += blockDim.x)
+    cp_async8(ta + x, x < 2 * s ? P.tabA + x : P.tabA, x < 2 * s ? 8u : 0u);
+  for (int64_t x = tid; x < tcols + 2 * kBandR; x += blockDim.x) {
+    const bool ok = x < tcols && i0 + x < P.N;
+    cp_async8(tb + pidx(x), ok ? P.tabB + i0 + x : P.tabB, ok ? 8u : 0u);
+  }
+  cp_async_commit();
   griddep_launch();
   griddep_wait();  // w (up kernel) and the input are ready past this point
-  __syncthreads();
+
+  // ---- data of this CTA (cp.async group 1): w windows of every subtree level, input tile
+  const double* wt = P.w + tile * P.w_tile;
+  if (L > 0) {
+    for (int j = 0; j <= k; ++j) {
+      const int g = gr + j;
+      const int64_t nodes = int64_t(1) << j;
+      const int64_t tw0 = (R << j) + 2;
+      const int64_t nw = nodes > 2 ? nodes : 2;
+      const int64_t twe = (tw0 + nw) < nseg(g) ? (tw0 + nw) : nseg(g);
+      if (twe <= tw0) continue;
+      const int64_t cnt2 = (twe - tw0) * VM / 2;
+      for (int sg = 0; sg < 2; ++sg) {
+        const double* src = wt + (w_level_offset_units(g) + sg * nseg(g) + tw0) * VM;
+        double* dst = wall + (wall_nodes_before(j) * 2 + sg * nw) * VM;
+        for (int64_t i = tid; i < cnt2; i += blockDim.x) cp_async16(dst + 2 * i, src + 2 * i);
+      }
+    }
+  }
+  for (int64_t idx = tid; idx < VT * (tcols + 2 * kBandR); idx += blockDim.x) {
+    const int64_t v = idx / (tcols + 2 * kBandR), x = idx - v * (tcols + 2 * kBandR);
+    const int64_t gv = tile * VT + v, j = i0 + x;
+    const bool ok = x < tcols && gv < P.batch && j < P.n;
+    const double* src = ok ? P.in + vaddr(P.layout, P.ld_in, gv, j) : P.in;
+    cp_async8(gt + v * tp + pidx(x), src, ok ? 8u : 0u);
+  }
+  cp_async_commit();
 
   const double* cfin = cA;
   if (L > 0) {
-    const double* wt = P.w + tile * P.w_tile;
-    // ---- ancestor chain: M2L of every ancestor of the subtree root, in parallel
+    // ---- ancestor chain: M2L of every ancestor of the subtree root, all in parallel (L2-resident A_hat)
     const double* chain_final = chain;
     if (gr > 0) {
       for (int it = tid; it < gr * kM; it += blockDim.x) {
@@ -339,18 +423,27 @@ __global__ void __launch_bounds__(kThreads) lc_down_kernel(const DownParams P) {
           for (int mi = 0; mi < nmat; ++mi) {
             const int r = (a & 1) ? 2 : mi;
             const int64_t t = (a & 1) ? a + 2 : a + 2 + mi;  // r=0: t=a+2, r=1: t=a+3; r=2 (odd a): t=a+2
-            const double* arow = P.A + (abase + 3 * b + r) * kMM + kk * kM;
+            const double2* arow = reinterpret_cast<const double2*>(P.A + (abase + 3 * b + r) * kMM + kk * kM);
             double ar[kM];
 #pragma unroll
-            for (int l = 0; l < kM; ++l) ar[l] = __ldg(arow + l);
+            for (int l = 0; l < kM / 2; ++l) {
+              const double2 a2 = __ldg(arow + l);
+              ar[2 * l] = a2.x;
+              ar[2 * l + 1] = a2.y;
+            }
 #pragma unroll
             for (int sg = 0; sg < 2; ++sg)
 #pragma unroll
               for (int v = 0; v < VT; ++v) {
-                const double* wp = wt + (w_level_offset_units(g) + sg * nseg(g) + t) * VM + v * kM;
+                const double2* wp =
+                    reinterpret_cast<const double2*>(wt + (w_level_offset_units(g) + sg * nseg(g) + t) * VM + v * kM);
                 double sacc = 0.0;
 #pragma unroll
-                for (int l = 0; l < kM; ++l) sacc = fma(ar[l], wp[l], sacc);
+                for (int l = 0; l < kM / 2; ++l) {
+                  const double2 w2 = __ldcg(wp + l);
+                  sacc = fma(ar[2 * l], w2.x, sacc);
+                  sacc = fma(ar[2 * l + 1], w2.y, sacc);
+                }
                 acc[sg][v] += sacc;
               }
           }
@@ -360,7 +453,10 @@ __global__ void __launch_bounds__(kThreads) lc_down_kernel(const DownParams P) {
 #pragma unroll
           for (int v = 0; v < VT; ++v) anc[((g * 2 + sg) * VT + v) * kM + kk] = acc[sg][v];
       }
-      __syncthreads();
+    }
+    cp_async_wait<1>();  // constants (B) have landed
+    __syncthreads();
+    if (gr > 0) {
       // Horner chain of step 4 down to level gr-1
       double* cb0 = chain;
       double* cb1 = chain + 2 * VM;
@@ -378,13 +474,17 @@ __global__ void __launch_bounds__(kThreads) lc_down_kernel(const DownParams P) {
       }
       chain_final = cb0;
     }
+    cp_async_wait<0>();  // w windows and the input tile
+    __syncthreads();
 
     // ---- the subtree, level by level: step 4 push then step 3 M2L (streamed A_hat)
     int st = 0;
     for (int j = 0; j <= k; ++j) {
-      const int g = gr + j;
       const int nodes = 1 << j;
       const int64_t u0 = R << j;
+      const int64_t tw0 = u0 + 2;
+      const int nw = nodes > 2 ? nodes : 2;
+      const double* wwin = wall + wall_nodes_before(j) * 2 * VM;
       double* cur = (j & 1) ? cB : cA;
       const double* par = (j & 1) ? cA : cB;
       {
@@ -406,23 +506,12 @@ __global__ void __launch_bounds__(kThreads) lc_down_kernel(const DownParams P) {
           cur[((sg * nodes + node) * VT + v) * kM + kk] = val;
         }
       }
-      // w window: columns [u0+2, u0+2+max(nodes,2)) of level g
-      const int64_t tw0 = u0 + 2;
-      const int64_t twe = min(tw0 + max(nodes, 2), nseg(g));
-      if (twe > tw0) {
-        const int64_t cntd = (twe - tw0) * VM;
-        for (int sg = 0; sg < 2; ++sg) {
-          const double* src = wt + (w_level_offset_units(g) + sg * nseg(g) + tw0) * VM;
-          double* dst = wwin + sg * nwmax * VM;
-          for (int64_t i = tid; i < cntd; i += blockDim.x) dst[i] = src[i];
-        }
-      }
       __syncthreads();
       while (st < nstages && stab[st].j == j) {
         const StageDesc d = stab[st];
         const int slot = st % P.nst;
         mbar_wait(&bars[slot], uint32_t((st / P.nst) & 1));
-        const double* As = uni + slot * slot_doubles;
+        const double* As = ring + slot * slot_doubles;
         const int nrows = (j == 0) ? 1 : 2 * d.nb;
         for (int it = tid; it < nrows * kM; it += blockDim.x) {
           const int ri = it / kM, kk = it % kM;
@@ -449,7 +538,7 @@ __global__ void __launch_bounds__(kThreads) lc_down_kernel(const DownParams P) {
             for (int sg = 0; sg < 2; ++sg)
 #pragma unroll
               for (int v = 0; v < VT; ++v) {
-                const double* wp = wwin + (sg * nwmax + (t - tw0)) * VM + v * kM;
+                const double* wp = wwin + (sg * nw + (t - tw0)) * VM + v * kM;
                 double sacc = 0.0;
 #pragma unroll
                 for (int l = 0; l < kM; ++l) sacc = fma(ar[l], wp[l], sacc);
@@ -465,61 +554,99 @@ __global__ void __launch_bounds__(kThreads) lc_down_kernel(const DownParams P) {
         if (tid == 0 && st + P.nst < nstages) issue(st + P.nst);
         ++st;
       }
-      __syncthreads();
     }
     cfin = (k & 1) ? cB : cA;
+  } else {
+    cp_async_wait<0>();
+    __syncthreads();
   }
 
-  // ---- epilogue: step 5 (leaf evaluation), step 6 (direct band), step 7 (C^{-1}), store
-  const int nleaf = 1 << k;
-  const int64_t seglen = 2 * s;
-  const int64_t U0 = R << k;
-  const int64_t i0 = U0 * seglen;
-  const int64_t rows = nleaf * seglen;
-  const int64_t tcols = (nleaf + 2) * seglen;
-  double* gt = uni;                 // [VT][tcols]  g_j = f_j (L2C) or j f_j (C2L)
-  double* tb = uni + VT * tcols;    // tabB[i0 .. i0+tcols)
-  double* ta = tb + tcols;          // tabA[0 .. 2s)
-  for (int64_t idx = tid; idx < VT * tcols; idx += blockDim.x) {
-    const int64_t v = idx / tcols, x = idx - v * tcols;
-    const int64_t gv = tile * VT + v, j = i0 + x;
-    const double fv = (gv < P.batch && j < P.n) ? P.in[vaddr(P.layout, P.ld_in, gv, j)] : 0.0;
-    gt[idx] = DIR == 0 ? fv : double(j) * fv;
-  }
-  for (int64_t x = tid; x < tcols; x += blockDim.x) tb[x] = (i0 + x < P.N) ? P.tabB[i0 + x] : 0.0;
-  for (int x = tid; x < 2 * s; x += blockDim.x) ta[x] = P.tabA[x];
-  __syncthreads();
+  // ---- epilogue: step 5 (eq:step5), step 6 (direct band, register-blocked), step 7 (C^{-1})
+  // item = (v, segment u, parity sigma, block t of kBandR same-parity rows m = kBandR t + r).
+  // Band for row i' = i + 2r (i the block's first row): sum_c a[c-r] b[i+r+c] g[i+2c], c >= r,
+  // i + 2c < j_end; a[.] = tabA, b[.] = tabB, g = f (L2C) or j f_j (C2L).  Sliding windows of a
+  // and b are kept in registers (slots rotate with c), so each step loads 3 values for kBandR rows.
+  double* zst = ring;  // [VT][rows] staging for a coalesced store
   const double inv_pi = 0.318309886183790671537767526745028724;
-  for (int64_t it = tid; it < VT * rows; it += blockDim.x) {
-    const int v = int(it / rows);
-    const int64_t ii = it - int64_t(v) * rows;
+  const int ntb = (s + kBandR - 1) / kBandR;
+  const int items = VT * nleaf * 2 * ntb;
+  for (int it = tid; it < items; it += blockDim.x) {
+    const int tb_i = it % ntb;
+    int r_ = it / ntb;
+    const int sg = r_ & 1;
+    r_ >>= 1;
+    const int u = r_ % nleaf;
+    const int v = r_ / nleaf;
+    const int m0 = kBandR * tb_i;
+    const int64_t ii = int64_t(u) * seglen + sg + 2 * m0;  // tile-local first row
     const int64_t i = i0 + ii;
-    const int64_t gv = tile * VT + v;
-    const int u = int(ii / seglen);
-    const int rr = int(ii - int64_t(u) * seglen);
-    const int sg = rr & 1, m = rr >> 1;
-    double acc = 0.0;
-    if (L > 0) {  // step 5: z^sigma = c(L-1) T(sigma)^T   (eq:step5)
-      const double* cp = cfin + ((sg * nleaf + u) * VT + v) * kM;
-      const double* tp = Tt + sg * kM * s + m;
+    const int64_t je = (seglen * (U0 + u + 2)) < P.N ? seglen * (U0 + u + 2) : P.N;
+    const int cmax = int((je - i - 1) >> 1);
+    const double* gv_t = gt + v * tp;
+    double acc[kBandR], aw[kBandR], bw[kBandR];
 #pragma unroll
-      for (int kk = 0; kk < kM; ++kk) acc = fma(cp[kk], tp[kk * s], acc);
+    for (int r = 0; r < kBandR; ++r) {
+      acc[r] = 0.0;
+      aw[r] = 0.0;
+      bw[r] = tb[pidx(ii + r)];
     }
-    // step 6: sum_{i <= j < j_end(i), j-i even} a_k b_{i+k} g_j, j = i+2k
-    const int64_t je = min(P.N, seglen * (U0 + u + 2));
-    const int nk = int((je - i + 1) >> 1);
-    const double* gp = gt + v * tcols + ii;
-    const double* bp = tb + ii;
-    double bs = 0.0;
-    for (int q = 0; q < nk; ++q) bs = fma(ta[q] * bp[q], gp[2 * q], bs);
-    double z;
-    if (DIR == 0) {
-      z = (acc + bs) * (i == 0 ? inv_pi : 2.0 * inv_pi);  // step 7: C^{-1}
-    } else {
-      z = acc + double(2 * i + 1) * bs;
-      if (i == 0 && gv < P.batch) z += P.in[vaddr(P.layout, P.ld_in, gv, 0)];  // entry (0,0) = 1
+    for (int c0 = 0; c0 <= cmax; c0 += kBandR) {
+#pragma unroll
+      for (int uu = 0; uu < kBandR; ++uu) {
+        const int c = c0 + uu;
+        if (c <= cmax) {
+          aw[uu] = ta[c];
+          if (c >= 1) bw[(uu + kBandR - 1) % kBandR] = tb[pidx(ii + kBandR - 1 + c)];
+          double gval = gv_t[pidx(ii + 2 * c)];
+          if (DIR == 1) gval *= double(i + 2 * c);
+#pragma unroll
+          for (int r = 0; r < kBandR; ++r)
+            acc[r] = fma(aw[(uu - r + kBandR) % kBandR] * bw[(r + uu) % kBandR], gval, acc[r]);
+        }
+      }
     }
-    if (gv < P.batch && i < P.n) P.out[vaddr(P.layout, P.ld_out, gv, i)] = z;
+    // step 5: z^sigma = c(L-1) T(sigma)^T
+    double t5[kBandR];
+#pragma unroll
+    for (int r = 0; r < kBandR; ++r) t5[r] = 0.0;
+    if (L > 0) {
+      const double* cp = cfin + ((sg * nleaf + u) * VT + v) * kM;
+      const double* tq = Tt + sg * kM * s + m0;
+#pragma unroll
+      for (int kk = 0; kk < kM; ++kk) {
+        const double cv = cp[kk];
+#pragma unroll
+        for (int r = 0; r < kBandR; ++r) t5[r] = fma(cv, tq[kk * s + r], t5[r]);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < kBandR; ++r) {
+      if (m0 + r < s) {
+        const int64_t ir = i + 2 * r;
+        double z;
+        if (DIR == 0) {
+          z = (t5[r] + acc[r]) * (ir == 0 ? inv_pi : 2.0 * inv_pi);  // step 7: C^{-1}
+        } else {
+          z = t5[r] + double(2 * ir + 1) * acc[r];
+          if (ir == 0) z += gv_t[pidx(0)];  // entry (0,0) of A^{-1}C is 1 (reading R2)
+        }
+        zst[v * rows + ii + 2 * r] = z;
+      }
+    }
+  }
+  __syncthreads();
+  if (P.layout == LC_VEC_CONTIGUOUS) {
+    for (int64_t idx = tid; idx < VT * rows; idx += blockDim.x) {
+      const int64_t v = idx / rows, ii = idx - v * rows;
+      const int64_t gv = tile * VT + v, i = i0 + ii;
+      if (gv < P.batch && i < P.n) P.out[gv * P.ld_out + i] = zst[idx];
+    }
+  } else {
+    for (int64_t idx = tid; idx < VT * rows; idx += blockDim.x) {
+      const int64_t ii = idx / VT, v = idx - ii * VT;
+      const int64_t gv = tile * VT + v, i = i0 + ii;
+      if (gv < P.batch && i < P.n) P.out[i * P.ld_out + gv] = zst[v * rows + ii];
+    }
   }
 }
 
@@ -550,13 +677,13 @@ lc_status configure_kernels(lc_plan* p) {
   if (ea != cudaSuccess) return record_cuda_error(ea);
   smax -= 256;  // static shared memory of the kernels
 
-  const int64_t budget = 110 * 1024;  // two CTAs per SM
+  const int64_t budget = 113 * 1024;  // two CTAs per SM (228 KB minus 1 KB reserved per CTA)
   int vt = p->vt;
   if (vt <= 0) vt = p->batch >= 2 ? 2 : 1;
   if (vt != 1 && vt != 2 && vt != 4 && vt != 8) return LC_ERR_INVALID_ARG;
   const bool user_k = p->k > 0;
   int k = user_k ? p->k : 4;
-  int bps = p->bps > 0 ? p->bps : 4;
+  int bps = p->bps > 0 ? p->bps : 2;
   int nst = p->nst > 0 ? p->nst : 3;
   if (p->L == 0) {
     k = 1;
@@ -568,15 +695,20 @@ lc_status configure_kernels(lc_plan* p) {
     return down_smem_layout(vt_, k_, int(p->s), bps, nst, gr_).total;
   };
   if (!user_k) {
-    while ((down_bytes(vt, k) > budget || up_smem_bytes(vt, k, int(p->s)) > budget) && p->L > 0 && k > 1) --k;
+    while (down_bytes(vt, k) > budget && p->L > 0 && k > 1) --k;
   }
-  if (down_bytes(vt, k) > smax || up_smem_bytes(vt, k, int(p->s)) > smax) return LC_ERR_INVALID_ARG;
+  if (down_bytes(vt, k) > smax) return LC_ERR_INVALID_ARG;
+  // up kernel: deeper subtrees (its shared memory is small); continuation step = its depth
+  int kup = p->L > 0 ? int(std::min<int64_t>(5, p->L - 1)) : 0;
+  while (kup > 0 && up_smem_bytes(vt, kup, int(p->s)) > budget) --kup;
   p->vt = vt;
   p->k = k;
   p->bps = bps;
   p->nst = nst;
   p->gr = p->L > 0 ? int(p->L - 1 - k) : 0;
-  p->group = std::max(k, 1);
+  p->kup = kup;
+  p->grup = p->L > 0 ? int(p->L - 1 - kup) : 0;
+  p->group = std::max(kup, 1);
   p->ntiles = (p->batch + vt - 1) / vt;
   // stage-table capacity
   if (p->L > 0) {
@@ -585,7 +717,7 @@ lc_status configure_kernels(lc_plan* p) {
     if (ns > kMaxStages) return LC_ERR_INVALID_ARG;
   }
   p->smem_down = size_t(down_bytes(vt, k));
-  p->smem_up = size_t(up_smem_bytes(vt, k, int(p->s)));
+  p->smem_up = size_t(up_smem_bytes(vt, kup, int(p->s)));
   if (p->L > 0) {
     p->w_tile_doubles = int64_t(vt) * kM * 2 * ((int64_t(4) << p->L) - 4);
     p->cnt_tile_ints = int64_t(4) << p->L;
@@ -599,8 +731,8 @@ lc_status configure_kernels(lc_plan* p) {
 }
 
 template <int VT>
-static cudaError_t launch_vt(const lc_plan* p, const UpParams& up, const DownParams& dp, dim3 grid, cudaStream_t st,
-                             cudaEvent_t const* ev, int nev) {
+static cudaError_t launch_vt(const lc_plan* p, const UpParams& up, const DownParams& dp, dim3 grid_up, dim3 grid,
+                             cudaStream_t st, cudaEvent_t const* ev, int nev) {
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
@@ -613,7 +745,7 @@ static cudaError_t launch_vt(const lc_plan* p, const UpParams& up, const DownPar
   int evi = 0;
   if (ev && nev > 0) cudaEventRecord(ev[evi++], st);
   if (p->L > 0) {
-    cfg.gridDim = grid;
+    cfg.gridDim = grid_up;
     cfg.dynamicSmemBytes = p->smem_up;
     e = cudaLaunchKernelEx(&cfg, lc_up_kernel<VT>, up);
     if (e != cudaSuccess) return e;
@@ -653,7 +785,7 @@ lc_status launch_execute(const lc_plan* p, const double* in, double* out, void* 
                                     align_up(p->ntiles * p->w_tile_doubles * 8, 256));
   UpParams up{};
   up.in = in; up.ld_in = p->ld_in; up.n = p->n; up.N = p->N; up.batch = p->batch;
-  up.layout = p->layout; up.L = int(p->L); up.s = int(p->s); up.k = p->k; up.gr = p->gr; up.G = p->group;
+  up.layout = p->layout; up.L = int(p->L); up.s = int(p->s); up.k = p->kup; up.gr = p->grup; up.G = p->group;
   up.T = p->d_T; up.B = p->d_B; up.w = w; up.cnt = cnt; up.w_tile = p->w_tile_doubles; up.cnt_tile = p->cnt_tile_ints;
   DownParams dp{};
   dp.in = in; dp.out = out; dp.ld_in = p->ld_in; dp.ld_out = p->ld_out; dp.n = p->n; dp.N = p->N;
@@ -666,12 +798,13 @@ lc_status launch_execute(const lc_plan* p, const double* in, double* out, void* 
     return LC_ERR_INVALID_ARG;
   }
   const dim3 grid(unsigned(nsub), unsigned(p->ntiles));
+  const dim3 grid_up(unsigned(p->L > 0 ? (int64_t(4) << p->grup) : 1), unsigned(p->ntiles));
   cudaError_t e;
   switch (p->vt) {
-    case 1: e = launch_vt<1>(p, up, dp, grid, st, ev, nev); break;
-    case 2: e = launch_vt<2>(p, up, dp, grid, st, ev, nev); break;
-    case 4: e = launch_vt<4>(p, up, dp, grid, st, ev, nev); break;
-    case 8: e = launch_vt<8>(p, up, dp, grid, st, ev, nev); break;
+    case 1: e = launch_vt<1>(p, up, dp, grid_up, grid, st, ev, nev); break;
+    case 2: e = launch_vt<2>(p, up, dp, grid_up, grid, st, ev, nev); break;
+    case 4: e = launch_vt<4>(p, up, dp, grid_up, grid, st, ev, nev); break;
+    case 8: e = launch_vt<8>(p, up, dp, grid_up, grid, st, ev, nev); break;
     default: e = cudaErrorInvalidValue;
   }
   if (prev != p->device) cudaSetDevice(prev);

@@ -49,10 +49,18 @@ inline Geometry geometry(int64_t n, int64_t s_hat) {
   return G;
 }
 
+constexpr int kBandR = 8;            // rows per thread in the register-blocked band (step 6)
+
+// Padded index of the band tiles: one pad double every 16, so that threads
+// whose rows are 2*kBandR apart hit distinct shared-memory banks.
+__host__ __device__ inline int64_t pidx(int64_t x) { return x + (x >> 4); }
+
+__host__ __device__ inline int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
 // Shared-memory layout of the down kernel (host computes the size, device the offsets).
 struct DownSmem {
-  int64_t Tt, Bs, cA, cB, wwin, anc, chain, uni, bars, stab, total;  // byte offsets
-  int64_t ring_bytes, leaf_bytes;
+  int64_t Tt, Bs, ta, cA, cB, wall, anc, chain, ring, gt, tb, bars, stab, total;  // byte offsets
+  int64_t tp;  // padded band-tile length (doubles)
 };
 
 struct StageDesc {
@@ -65,22 +73,33 @@ struct StageDesc {
   long long mat0;  // first global A_hat index
 };
 
-__host__ __device__ inline int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+// w windows of all subtree levels: level j needs max(2^j, 2) column segments.
+__host__ __device__ inline int64_t wall_nodes_before(int j) {
+  int64_t t = 0;
+  for (int jj = 0; jj < j; ++jj) t += (1 << jj) > 2 ? (1 << jj) : 2;
+  return t;
+}
 
 __host__ __device__ inline DownSmem down_smem_layout(int VT, int k, int s, int bps, int nst, int gr) {
   DownSmem L{};
   int64_t o = 0;
   const int64_t node = int64_t(2) * VT * kM * 8;  // one segment, both parities, VT vectors
-  L.Tt = o;    o = align_up(o + int64_t(2) * kM * s * 8, 128);
+  const int64_t nleaf = int64_t(1) << k;
+  const int64_t tcols = (nleaf + 2) * 2 * s;
+  L.tp = pidx(tcols + 2 * kBandR) + 2;
+  L.Tt = o;    o = align_up(o + int64_t(2) * kM * s * 8 + 2 * kBandR * 8, 128);
   L.Bs = o;    o = align_up(o + int64_t(kMM) * 8, 128);
-  L.cA = o;    o = align_up(o + (int64_t(1) << k) * node, 128);
-  L.cB = o;    o = align_up(o + (int64_t(1) << k) * node, 128);
-  L.wwin = o;  o = align_up(o + ((int64_t(1) << k) + 2) * node, 128);
+  L.ta = o;    o = align_up(o + (int64_t(2) * s + 2 * kBandR) * 8, 128);
+  L.cA = o;    o = align_up(o + nleaf * node, 128);
+  L.cB = o;    o = align_up(o + nleaf * node, 128);
+  L.wall = o;  o = align_up(o + wall_nodes_before(k + 1) * node, 128);
   L.anc = o;   o = align_up(o + int64_t(gr > 0 ? gr : 1) * node, 128);
   L.chain = o; o = align_up(o + 2 * node, 128);
-  L.ring_bytes = int64_t(nst) * bps * 3 * kMM * 8;
-  L.leaf_bytes = (int64_t(VT) + 1) * ((int64_t(1) << k) + 2) * 2 * s * 8 + int64_t(2) * s * 8;
-  L.uni = o;   o = align_up(o + (L.ring_bytes > L.leaf_bytes ? L.ring_bytes : L.leaf_bytes), 128);
+  const int64_t ring = int64_t(nst) * bps * 3 * kMM * 8;
+  const int64_t zst = int64_t(VT) * nleaf * 2 * s * 8;  // z staging reuses the ring
+  L.ring = o;  o = align_up(o + (ring > zst ? ring : zst), 128);
+  L.gt = o;    o = align_up(o + int64_t(VT) * L.tp * 8, 128);
+  L.tb = o;    o = align_up(o + L.tp * 8, 128);
   L.bars = o;  o = align_up(o + int64_t(nst) * 8, 128);
   L.stab = o;  o = align_up(o + int64_t(kMaxStages) * sizeof(StageDesc), 128);
   L.total = o;
@@ -107,7 +126,7 @@ struct lc_plan {
   int device;
   int sm_count;
   // kernel configuration
-  int vt, k, gr, bps, nst, group;
+  int vt, k, gr, bps, nst, group, kup, grup;
   int64_t ntiles;
   int64_t w_tile_doubles, cnt_tile_ints;
   size_t ws_bytes;
