@@ -242,12 +242,20 @@ def run_gpu(args, world, rank, local):
         for d, ev in enumerate((evs, evc)):
             for i in range(kpe):
                 per_kernel[d][i] += ev[i].elapsed_time(ev[i + 1]) / ksteps
-    down_ms = 0.5 * (per_kernel[0][-1] + per_kernel[1][-1])
     hbm, hbm_src = peaks()
     dl = pl.desc
-    down_bytes = dl["bytes_alg"]  # 8 M^2 N_c (A_hat) + 16 n V (f in, z out) + 8 N (lambda): all read/written by the down kernel
+    names = ["lc_up_kernel", "lc_m2l_kernel", "lc_down_kernel"] if kpe == 3 else ["lc_down_kernel"]
+    # algorithmic bytes per launch (f in, z out, A_hat once, lambda once; work arrays excluded)
+    alg = {"lc_up_kernel": 8.0 * n * V, "lc_m2l_kernel": 8.0 * 324 * dl["nc"],
+           "lc_down_kernel": 16.0 * n * V + 8.0 * dl["N"]}
+    if kpe == 1:
+        alg["lc_down_kernel"] = dl["bytes_alg"]
+    avg_ms = {nm: 0.5 * (per_kernel[0][i] + per_kernel[1][i]) for i, nm in enumerate(names)}
+    dom = max(avg_ms, key=avg_ms.get)
+    down_ms = avg_ms[dom]
+    down_bytes = alg[dom]
     achieved = down_bytes / (down_ms * 1e-3) / 1e9
-    traffic = load_traffic(args.config, n)
+    traffic = load_traffic(args.config, dom)
     # transform-level roofline (slower of fp64 flops at the measured DFMA peak and bytes at HBM peak)
     t_roof = max(dl["flops_alg"] * V / (FP64_PEAK_TFLOPS * 1e12), dl["bytes_alg"] / (hbm * 1e9))
     t_meas = ms_local / args.steps / 2 * 1e-3
@@ -292,15 +300,16 @@ def run_gpu(args, world, rank, local):
                          f"{3 * bytes_vec / 1e6:.0f} MB of vectors vs 126 MB L2" if dl["nc"] > 0 else "small",
                    "graph": graph is not None, "kernel_cfg": {k: dl[k] for k in ("vt", "subtree", "stage_blocks",
                                                                                  "stages")}},
-        "roofline": {"bound": "hbm", "kernel": "lc_down_kernel", "achieved": achieved, "peak": hbm,
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm,
                      "unit": "GB/s", "frac": achieved / hbm, "traffic": traffic,
                      "algorithmic_bytes_per_launch": down_bytes, "avg_launch_ms": down_ms,
                      "peak_source": hbm_src},
         "roofline_transform": {"t_roof_us": t_roof * 1e6, "t_measured_us": t_meas * 1e6,
                                "frac": t_roof / t_meas, "fp64_peak_tflops": FP64_PEAK_TFLOPS,
                                "flops_alg_per_vector": dl["flops_alg"], "bytes_alg": dl["bytes_alg"]},
-        "kernel_ms": {"leg2cheb": per_kernel[0], "cheb2leg": per_kernel[1],
-                      "names": (["lc_up_kernel"] if kpe == 2 else []) + ["lc_down_kernel"]},
+        "kernel_ms": {"leg2cheb": per_kernel[0], "cheb2leg": per_kernel[1], "names": names,
+                      "algorithmic_bytes": [alg[nm] for nm in names],
+                      "achieved_gbs": [alg[nm] / (avg_ms[nm] * 1e-3) / 1e9 for nm in names]},
         "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": 2 * bytes_vec,
                 "d2h_bytes_per_step": 2 * bytes_vec, "steps": e2e_steps, "ms_per_step": e2e_ms / e2e_steps,
                 "path": "lc_execute_host (C ABI, pinned host buffers) x2 per step"},
@@ -321,14 +330,15 @@ def allreduce_sum(x: float, world: int) -> float:
     return float(t.item())
 
 
-def load_traffic(config, n):
+def load_traffic(config, kernel):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel` from the committed
+    ncu --set full capture (profiles/ncu_traffic.json, written from the .ncu-rep), or None."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if not os.path.exists(p):
         return None
     try:
         d = json.load(open(p))
-        e = d.get(config)
-        return None if e is None else e.get("down_dram_bytes_per_launch")
+        return d.get(config, {}).get(kernel)
     except Exception:
         return None
 

@@ -19,7 +19,6 @@ namespace lc {
 constexpr int kM = 18;               // Chebyshev modes
 constexpr int kMM = kM * kM;
 constexpr int kThreads = 256;        // threads per CTA of the execution kernels
-constexpr int kMaxStages = 96;       // max bulk-copy stages per CTA (stage table size)
 
 // First A_hat index of level g in the level-major (g, b, r) arena:
 // 3 * sum_{g'<g} b_g' = 3 (2^(g+1) - 2 - g).
@@ -49,7 +48,7 @@ inline Geometry geometry(int64_t n, int64_t s_hat) {
   return G;
 }
 
-constexpr int kBandR = 8;            // rows per thread in the register-blocked band (step 6)
+constexpr int kBandR = 4;            // rows per thread in the register-blocked band (step 6)
 
 // Padded index of the band tiles: one pad double every 16, so that threads
 // whose rows are 2*kBandR apart hit distinct shared-memory banks.
@@ -59,57 +58,45 @@ __host__ __device__ inline int64_t align_up(int64_t x, int64_t a) { return (x + 
 
 // Shared-memory layout of the down kernel (host computes the size, device the offsets).
 struct DownSmem {
-  int64_t Tt, Bs, ta, cA, cB, wall, anc, chain, ring, gt, tb, bars, stab, total;  // byte offsets
-  int64_t tp;  // padded band-tile length (doubles)
+  int64_t Bs, Tt, ta, tb, gt, zst, cm, chw, total;  // byte offsets
+  int64_t tp;                              // padded band-tile length (doubles)
 };
 
-struct StageDesc {
-  int j;        // subtree-relative level
-  int b0;       // first block (level-local)
-  int nb;       // blocks in stage
-  int r0;       // first r of the first block (0 except the odd-root stage: 2)
-  int nmat;     // matrices in stage
-  int pad;
-  long long mat0;  // first global A_hat index
-};
+// c_m2l nodes staged by the down kernel: gr ancestors + the 2^(k+1)-1 subtree nodes.
+__host__ __device__ inline int64_t down_cm_nodes(int k, int gr) { return int64_t(gr) + ((int64_t(2) << k) - 1); }
 
-// w windows of all subtree levels: level j needs max(2^j, 2) column segments.
-__host__ __device__ inline int64_t wall_nodes_before(int j) {
-  int64_t t = 0;
-  for (int jj = 0; jj < j; ++jj) t += (1 << jj) > 2 ? (1 << jj) : 2;
-  return t;
-}
-
-__host__ __device__ inline DownSmem down_smem_layout(int VT, int k, int s, int bps, int nst, int gr) {
+__host__ __device__ inline DownSmem down_smem_layout(int VT, int k, int s, int gr) {
   DownSmem L{};
   int64_t o = 0;
   const int64_t node = int64_t(2) * VT * kM * 8;  // one segment, both parities, VT vectors
   const int64_t nleaf = int64_t(1) << k;
   const int64_t tcols = (nleaf + 2) * 2 * s;
   L.tp = pidx(tcols + 2 * kBandR) + 2;
-  L.Tt = o;    o = align_up(o + int64_t(2) * kM * s * 8 + 2 * kBandR * 8, 128);
   L.Bs = o;    o = align_up(o + int64_t(kMM) * 8, 128);
+  L.Tt = o;    o = align_up(o + int64_t(2) * kM * s * 8 + 2 * kBandR * 8, 128);
   L.ta = o;    o = align_up(o + (int64_t(2) * s + 2 * kBandR) * 8, 128);
-  L.cA = o;    o = align_up(o + nleaf * node, 128);
-  L.cB = o;    o = align_up(o + nleaf * node, 128);
-  L.wall = o;  o = align_up(o + wall_nodes_before(k + 1) * node, 128);
-  L.anc = o;   o = align_up(o + int64_t(gr > 0 ? gr : 1) * node, 128);
-  L.chain = o; o = align_up(o + 2 * node, 128);
-  const int64_t ring = int64_t(nst) * bps * 3 * kMM * 8;
-  const int64_t zst = int64_t(VT) * nleaf * 2 * s * 8;  // z staging reuses the ring
-  L.ring = o;  o = align_up(o + (ring > zst ? ring : zst), 128);
-  L.gt = o;    o = align_up(o + int64_t(VT) * L.tp * 8, 128);
   L.tb = o;    o = align_up(o + L.tp * 8, 128);
-  L.bars = o;  o = align_up(o + int64_t(nst) * 8, 128);
-  L.stab = o;  o = align_up(o + int64_t(kMaxStages) * sizeof(StageDesc), 128);
+  L.gt = o;    o = align_up(o + int64_t(VT) * L.tp * 8, 128);
+  L.zst = o;   o = align_up(o + int64_t(VT) * nleaf * 2 * s * 8, 128);
+  L.cm = o;    o = align_up(o + down_cm_nodes(k, gr) * node, 128);
+  L.chw = o;   o = align_up(o + int64_t(2) * VT * 32 * 8, 128);  // ancestor-chain exchange (per chain: 32 doubles)
   L.total = o;
   return L;
+}
+
+// M2L streaming kernel: per ring slot, the A_hat of `cb` blocks plus the w window
+// (2 cb column segments, both parities, VT vectors).
+__host__ __device__ inline int64_t m2l_slot_bytes(int VT, int cb) {
+  return align_up(int64_t(cb) * 3 * kMM * 8, 128) + align_up(int64_t(2) * (2 * cb) * VT * kM * 8, 128);
+}
+__host__ __device__ inline int64_t m2l_smem_bytes(int VT, int cb, int nst) {
+  return int64_t(nst) * m2l_slot_bytes(VT, cb) + align_up(int64_t(2) * nst * 8, 128);  // + full/empty barriers
 }
 
 __host__ __device__ inline int64_t up_smem_bytes(int VT, int k, int s) {
   int64_t o = 0;
   o = align_up(o + int64_t(2) * s * kM * 8, 128);                 // T [2][s][M]
-  o = align_up(o + int64_t(kMM) * 8, 128);                        // B
+  o = align_up(o + int64_t(kMM) * 8, 128);                        // B(0)^T
   o = align_up(o + int64_t(VT) * (int64_t(1) << k) * 2 * s * 8, 128);  // f tile
   o = align_up(o + ((int64_t(2) << k) - 1) * 2 * VT * kM * 8, 128);    // w tree
   o += 16;
@@ -127,6 +114,8 @@ struct lc_plan {
   int sm_count;
   // kernel configuration
   int vt, k, gr, bps, nst, group, kup, grup;
+  int64_t m2l_units;  // (chunk, tile) work units of the M2L kernel
+  int m2l_grid;
   int64_t ntiles;
   int64_t w_tile_doubles, cnt_tile_ints;
   size_t ws_bytes;
