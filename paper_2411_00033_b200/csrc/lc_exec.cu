@@ -106,6 +106,7 @@ struct UpParams {
   const double* B;  // B(0) [M][M]
   double* w;
   int* cnt;
+  int* flags;
   int64_t w_tile, cnt_tile;
 };
 
@@ -113,6 +114,8 @@ struct M2lParams {
   const double* A;
   const double* w;
   double* c;
+  int* flags;
+  int gr_up;  // levels >= gr_up are written by the up kernel's main phase
   int64_t w_tile;  // doubles per vector tile (w and c share the layout)
   int64_t ntiles, nunits;
   int L, cb, nst;
@@ -132,38 +135,71 @@ struct DownParams {
 };
 
 // ============================================================== up kernel
-// Alg. a.1 for a whole tree level in shared memory, one thread per output mode n:
+// B(0) (App. A3) is a universal constant for M = 18: in constant memory the fully unrolled
+// triangular products below take it as a uniform DFMA operand (no shared-memory traffic).
+__constant__ double c_B0[kMM];
+
+// Alg. a.1 for one parent node, 18 outputs per thread:
 // parent[n] = sum_{k<=n} b_nk (x0_k + (-1)^(n-k) x1_k)  (B(1) = B(0) with odd diagonals
-// negated, App. A3).  Bt = B(0)^T so that lanes with consecutive n read consecutive words.
-template <int VT>
-__device__ __forceinline__ void m2m_level(const double* __restrict__ ch, double* __restrict__ pa, int nparent,
-                                          const double* __restrict__ Bt) {
-  const int items = 2 * nparent * VT * kM;
-  for (int it = threadIdx.x; it < items; it += blockDim.x) {
-    const int n = it % kM;
-    const int r = it / kM;  // (sigma * nparent + P) * VT + v
-    const int v = r % VT;
-    const int sp = r / VT;
-    const int P = sp % nparent;
-    const int sg = sp / nparent;
-    const double* x0 = ch + ((sg * 2 * nparent + 2 * P) * VT + v) * kM;
-    const double* x1 = x0 + VT * kM;
-    double ae = 0.0, ao = 0.0;  // even / odd diagonals
-    for (int k = n; k >= 0; k -= 2) ae = fma(Bt[k * kM + n], x0[k] + x1[k], ae);
-    for (int k = n - 1; k >= 0; k -= 2) ao = fma(Bt[k * kM + n], x0[k] - x1[k], ao);
-    pa[r * kM + n] = ae + ao;
+// negated, App. A3); written to shared memory in pairs as soon as formed.
+__device__ __forceinline__ void m2m18(const double* __restrict__ x0p, const double* __restrict__ x1p,
+                                      double* __restrict__ out) {
+  double zp[kM], zm[kM];
+#pragma unroll
+  for (int k = 0; k < kM; k += 2) {
+    const double2 a = *reinterpret_cast<const double2*>(x0p + k);
+    const double2 b = *reinterpret_cast<const double2*>(x1p + k);
+    zp[k] = a.x + b.x;
+    zm[k] = a.x - b.x;
+    zp[k + 1] = a.y + b.y;
+    zm[k + 1] = a.y - b.y;
+  }
+#pragma unroll
+  for (int n = 0; n < kM; n += 2) {
+    double a = 0.0, b = 0.0;
+#pragma unroll
+    for (int k = 0; k <= n; ++k) a = fma(c_B0[n * kM + k], ((n - k) & 1) ? zm[k] : zp[k], a);
+#pragma unroll
+    for (int k = 0; k <= n + 1; ++k) b = fma(c_B0[(n + 1) * kM + k], ((n + 1 - k) & 1) ? zm[k] : zp[k], b);
+    *reinterpret_cast<double2*>(out + n) = make_double2(a, b);
   }
 }
 
+// one tree level in shared memory ([sigma][node][v][M]); item = (sigma, parent, v); nparent = 2^lp
 template <int VT>
-__global__ void __launch_bounds__(kThreads, 2) lc_up_kernel(const UpParams P) {
+__device__ __forceinline__ void m2m_level(const double* __restrict__ ch, double* __restrict__ pa, int lp) {
+  const int nparent = 1 << lp;
+  const int items = 2 * nparent * VT;
+  for (int it = threadIdx.x; it < items; it += blockDim.x) {
+    const int v = it % VT;
+    const int sp = it / VT;
+    const int P = sp & (nparent - 1);
+    const int sg = sp >> lp;
+    const double* x0 = ch + ((sg * 2 * nparent + 2 * P) * VT + v) * kM;
+    m2m18(x0, x0 + VT * kM, pa + it * kM);
+  }
+}
+
+// release/acquire helpers for the readiness flags (gpu scope)
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// flags (workspace): [0] main-phase arrivals, [1] fine levels ready, [2] finished continuations,
+// [3] coarse levels ready, [4] finished M2L CTAs.  Self-resetting.
+template <int VT>
+__global__ void __launch_bounds__(kThreads, 1) lc_up_kernel(const UpParams P) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ int s_last;
   const int s = P.s, k = P.k;
   const int tid = threadIdx.x;
   double* Ts = reinterpret_cast<double*>(smem);
-  double* Bt = reinterpret_cast<double*>(smem + align_up(int64_t(2) * s * kM * 8, 128));
-  double* fs = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(Bt) + align_up(int64_t(kMM) * 8, 128));
+  double* fs = reinterpret_cast<double*>(smem + align_up(int64_t(2) * s * kM * 8, 128) + align_up(int64_t(kMM) * 8, 128));
   const int nleaf = 1 << k;
   const int64_t seglen = 2 * s;
   const int64_t tlen = nleaf * seglen;
@@ -173,7 +209,6 @@ __global__ void __launch_bounds__(kThreads, 2) lc_up_kernel(const UpParams P) {
   const int64_t R = blockIdx.x;
   const int64_t tile = blockIdx.y;
   for (int i = tid; i < s * kM; i += blockDim.x) cp_async16(Ts + 2 * i, P.T + 2 * i);
-  for (int i = tid; i < kMM; i += blockDim.x) Bt[(i % kM) * kM + i / kM] = __ldg(P.B + i);
   cp_async_commit();
   griddep_launch();
   griddep_wait();  // the input may be produced by the preceding kernel
@@ -214,8 +249,8 @@ __global__ void __launch_bounds__(kThreads, 2) lc_up_kernel(const UpParams P) {
       int r = it / 3;
       const int sg = r & 1;
       r >>= 1;
-      const int seg = r % nleaf;
-      const int v = r / nleaf;
+      const int seg = r & (nleaf - 1);
+      const int v = r >> k;
       const double* fp = fs + v * tlen + seg * seglen + sg;
       const double* tp = Ts + sg * s * kM + 6 * kg;
       double a0 = 0, a1 = 0, a2 = 0, a3 = 0, a4 = 0, a5 = 0;
@@ -238,18 +273,30 @@ __global__ void __launch_bounds__(kThreads, 2) lc_up_kernel(const UpParams P) {
   __syncthreads();
   // step 2 inside the subtree
   for (int j = k; j >= 1; --j) {
-    m2m_level<VT>(tree + tree_off(j), tree + tree_off(j - 1), 1 << (j - 1), Bt);
+    m2m_level<VT>(tree + tree_off(j), tree + tree_off(j - 1), j - 1);
     __syncthreads();
   }
   double* wt = P.w + tile * P.w_tile;
   const int64_t VM = int64_t(VT) * kM;
   for (int j = 0; j <= k; ++j) {
     const int g = P.gr + j;
-    const int64_t cntd = (int64_t(1) << j) * VM;
+    const int cnt2 = int((int64_t(1) << j) * VM / 2);
     for (int sg = 0; sg < 2; ++sg) {
       double2* dst = reinterpret_cast<double2*>(wt + (w_level_offset_units(g) + sg * nseg(g) + (R << j)) * VM);
       const double2* src = reinterpret_cast<const double2*>(tree + tree_off(j) + sg * (int64_t(1) << j) * VM);
-      for (int64_t i = tid; i < cntd / 2; i += blockDim.x) dst[i] = src[i];
+      for (int i = tid; i < cnt2; i += blockDim.x) dst[i] = src[i];
+    }
+  }
+  // the fine levels (gr..L-1) of the whole batch are ready once every CTA got here
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) {
+    const int total = int(gridDim.x * gridDim.y);
+    if (atomicAdd(&P.flags[0], 1) == total - 1) {
+      atomicExch(&P.flags[0], 0);
+      __threadfence();
+      st_release(&P.flags[1], 1);
+      if (P.gr == 0) st_release(&P.flags[3], 1);
     }
   }
 
@@ -260,7 +307,6 @@ __global__ void __launch_bounds__(kThreads, 2) lc_up_kernel(const UpParams P) {
   while (g > 0) {
     const int ge = min(P.G, g);
     const int64_t grp = node >> ge;
-    __threadfence();
     __syncthreads();
     if (tid == 0) {
       int* c = P.cnt + tile * P.cnt_tile + (nseg(g) - 4) + grp;
@@ -272,36 +318,49 @@ __global__ void __launch_bounds__(kThreads, 2) lc_up_kernel(const UpParams P) {
     __syncthreads();
     if (!s_last) return;
     __threadfence();
-    const int64_t cntd = (int64_t(1) << ge) * VM;
+    const int cnt2 = int((int64_t(1) << ge) * VM / 2);
     for (int sg = 0; sg < 2; ++sg) {
       const double2* src =
           reinterpret_cast<const double2*>(wt + (w_level_offset_units(g) + sg * nseg(g) + (grp << ge)) * VM);
-      double2* dst = reinterpret_cast<double2*>(tree + tree_off(ge) + sg * cntd);
-      for (int64_t i = tid; i < cntd / 2; i += blockDim.x) dst[i] = __ldcg(src + i);
+      double2* dst = reinterpret_cast<double2*>(tree + tree_off(ge) + sg * 2 * cnt2);
+      for (int i = tid; i < cnt2; i += blockDim.x) dst[i] = __ldcg(src + i);
     }
     __syncthreads();
     for (int j = ge; j >= 1; --j) {
-      m2m_level<VT>(tree + tree_off(j), tree + tree_off(j - 1), 1 << (j - 1), Bt);
+      m2m_level<VT>(tree + tree_off(j), tree + tree_off(j - 1), j - 1);
       __syncthreads();
     }
     for (int j = 0; j < ge; ++j) {
       const int gg = g - ge + j;
-      const int64_t cj = (int64_t(1) << j) * VM;
+      const int cj2 = int((int64_t(1) << j) * VM / 2);
       for (int sg = 0; sg < 2; ++sg) {
         double2* dst = reinterpret_cast<double2*>(wt + (w_level_offset_units(gg) + sg * nseg(gg) + (grp << j)) * VM);
-        const double2* src = reinterpret_cast<const double2*>(tree + tree_off(j) + sg * cj);
-        for (int64_t i = tid; i < cj / 2; i += blockDim.x) dst[i] = src[i];
+        const double2* src = reinterpret_cast<const double2*>(tree + tree_off(j) + sg * 2 * cj2);
+        for (int i = tid; i < cj2; i += blockDim.x) dst[i] = src[i];
       }
     }
+    __threadfence();
     g -= ge;
     node = grp;
+  }
+  if (P.gr > 0) {  // this CTA produced one of the 4 level-0 nodes of its vector tile
+    __syncthreads();
+    if (tid == 0) {
+      const int total = 4 * int(gridDim.y);
+      if (atomicAdd(&P.flags[2], 1) == total - 1) {
+        atomicExch(&P.flags[2], 0);
+        __threadfence();
+        st_release(&P.flags[3], 1);
+      }
+    }
   }
 }
 
 // ============================================================== M2L kernel
-// Work unit q = (chunk, tile): chunk = (level g, blocks [b0, b0+nb)), nb <= cb,
-// enumerated level-major; tiles innermost so concurrent CTAs share A_hat in L2.
-// cstart[g] = first chunk of level g (shared-memory table, 32-bit arithmetic only).
+// Work unit q = (chunk, tile): chunk = (level g, blocks [b0, b0+nb)), nb <= cb, enumerated
+// from the finest level down to level 0 (the coarse w are produced last by the up kernel's
+// continuation); tiles innermost so concurrent CTAs share A_hat in L2.
+// cstart[o] = first chunk of level L-1-o (shared-memory table, 32-bit arithmetic only).
 __device__ __forceinline__ void m2l_unit(int q, int ntiles, int L, int cb, const int* cstart, int& g, int& b0,
                                          int& nb, int& tile) {
   int ch = q;
@@ -310,9 +369,10 @@ __device__ __forceinline__ void m2l_unit(int q, int ntiles, int L, int cb, const
     ch = q / ntiles;
     tile = q - ch * ntiles;
   }
-  g = 0;
-  while (g + 1 < L && cstart[g + 1] <= ch) ++g;
-  b0 = (ch - cstart[g]) * cb;
+  int o = 0;
+  while (o + 1 < L && cstart[o + 1] <= ch) ++o;
+  g = L - 1 - o;
+  b0 = (ch - cstart[o]) * cb;
   const int bg = (2 << g) - 1;
   nb = (bg - b0) < cb ? (bg - b0) : cb;
 }
@@ -342,8 +402,9 @@ __global__ void __launch_bounds__(kM2lThreads) lc_m2l_kernel(const M2lParams P) 
   const int nmine = nunits > int(blockIdx.x) ? (nunits - int(blockIdx.x) + int(gridDim.x) - 1) / int(gridDim.x) : 0;
   if (tid == 0) {
     int acc = 0;
-    for (int g = 0; g < P.L && g < 32; ++g) {
-      cstart[g] = acc;
+    for (int o = 0; o < P.L && o < 32; ++o) {
+      cstart[o] = acc;
+      const int g = P.L - 1 - o;
       acc += ((2 << g) - 1 + cb - 1) / cb;
     }
     for (int i = 0; i < nst; ++i) {
@@ -355,10 +416,12 @@ __global__ void __launch_bounds__(kM2lThreads) lc_m2l_kernel(const M2lParams P) 
   __syncthreads();
   const int ntiles = int(P.ntiles);
 
+  griddep_launch();
   if (tid < 32) {
     // ------------------------------------------------ producer warp
     if (tid == 0) {
       const uint64_t pol = policy_evict_first();
+      bool fine_ok = false, coarse_ok = false;
       auto issue = [&](int i, bool with_a, bool with_w) {
         int g, nb, b0, tile;
         m2l_unit(int(blockIdx.x) + i * int(gridDim.x), ntiles, P.L, cb, cstart, g, b0, nb, tile);
@@ -372,6 +435,15 @@ __global__ void __launch_bounds__(kM2lThreads) lc_m2l_kernel(const M2lParams P) 
           bulk_g2s(base, P.A + (ahat_level_offset(g) + 3 * int64_t(b0)) * kMM, abytes, &full[slot], pol);
         }
         if (with_w) {
+          // w of level g is ready: fine levels after the up kernel's main phase, coarse ones after
+          // its continuation (flags set with release semantics by the up kernel)
+          bool& ok = g >= P.gr_up ? fine_ok : coarse_ok;
+          if (!ok) {
+            const int* f = &P.flags[g >= P.gr_up ? 1 : 3];
+            while (ld_acquire(f) == 0) __nanosleep(64);
+            asm volatile("fence.proxy.async.global;" ::: "memory");  // order the bulk reads after the acquire
+            ok = true;
+          }
           double* wwin = reinterpret_cast<double*>(base + a_bytes);
           const double* wt = P.w + int64_t(tile) * P.w_tile;
           for (int sg = 0; sg < 2; ++sg)
@@ -380,21 +452,17 @@ __global__ void __launch_bounds__(kM2lThreads) lc_m2l_kernel(const M2lParams P) 
         }
       };
       const int npre = nmine < nst ? nmine : nst;
-      for (int i = 0; i < npre; ++i) issue(i, true, false);  // A_hat is plan data: before the dependency wait
-      griddep_launch();
-      griddep_wait();  // w (up kernel) is ready past this point
+      for (int i = 0; i < npre; ++i) issue(i, true, false);  // A_hat is plan data: issued immediately
       for (int i = 0; i < npre; ++i) issue(i, false, true);
       for (int i = nst; i < nmine; ++i) {
         mbar_wait(&empty[i % nst], uint32_t(((i / nst) - 1) & 1));
         issue(i, true, true);
       }
     }
-    return;
   }
   // -------------------------------------------------- consumer warps
-  griddep_launch();
   const int ctid = tid - 32;
-  for (int i = 0; i < nmine; ++i) {
+  for (int i = 0; i < nmine && tid >= 32; ++i) {
     int g, nb, b0, tile;
     m2l_unit(int(blockIdx.x) + i * int(gridDim.x), ntiles, P.L, cb, cstart, g, b0, nb, tile);
     const int slot = i % nst;
@@ -436,6 +504,15 @@ __global__ void __launch_bounds__(kM2lThreads) lc_m2l_kernel(const M2lParams P) 
     }
     __syncwarp();
     if ((tid & 31) == 0) mbar_arrive(&empty[slot]);  // this warp is done with the slot
+  }
+  __syncthreads();
+  if (tid == 0) {  // the last CTA to finish re-arms the readiness flags for the next execution
+    if (atomicAdd(&P.flags[4], 1) == int(gridDim.x) - 1) {
+      P.flags[1] = 0;
+      P.flags[3] = 0;
+      __threadfence();
+      atomicExch(&P.flags[4], 0);
+    }
   }
 }
 
@@ -726,6 +803,11 @@ lc_status configure_kernels(lc_plan* p) {
     if (ea == cudaSuccess) ea = set_attrs_vt<2>(smax);
     if (ea == cudaSuccess) ea = set_attrs_vt<4>(smax);
     if (ea == cudaSuccess) ea = set_attrs_vt<8>(smax);
+    if (ea == cudaSuccess) {
+      double B[kMM];
+      ea = cudaMemcpy(B, p->d_B, sizeof(B), cudaMemcpyDeviceToHost);
+      if (ea == cudaSuccess) ea = cudaMemcpyToSymbol(c_B0, B, sizeof(B));
+    }
     if (ea != cudaSuccess) return record_cuda_error(ea);
     g_device_ready[p->device] = true;
   }
@@ -792,9 +874,9 @@ lc_status configure_kernels(lc_plan* p) {
     p->w_tile_doubles = 0;
     p->cnt_tile_ints = 0;
   }
-  // workspace: w | c_m2l | arrival counters (c_m2l rows without a submatrix stay zero from init)
+  // workspace: w | c_m2l | flags (64 ints) | arrival counters (c_m2l rows without a submatrix stay zero)
   const size_t wb = size_t(align_up(p->ntiles * p->w_tile_doubles * 8, 256));
-  p->ws_bytes = 2 * wb + size_t(p->ntiles * p->cnt_tile_ints) * sizeof(int);
+  p->ws_bytes = 2 * wb + 256 + size_t(p->ntiles * p->cnt_tile_ints) * sizeof(int);
   return LC_OK;
 }
 
@@ -858,13 +940,14 @@ lc_status launch_execute(const lc_plan* p, const double* in, double* out, void* 
   const size_t wb = size_t(align_up(p->ntiles * p->w_tile_doubles * 8, 256));
   double* w = reinterpret_cast<double*>(ws);
   double* c = reinterpret_cast<double*>(reinterpret_cast<char*>(ws) + wb);
-  int* cnt = reinterpret_cast<int*>(reinterpret_cast<char*>(ws) + 2 * wb);
+  int* flags = reinterpret_cast<int*>(reinterpret_cast<char*>(ws) + 2 * wb);
+  int* cnt = flags + 64;
   UpParams up{};
   up.in = in; up.ld_in = p->ld_in; up.n = p->n; up.N = p->N; up.batch = p->batch;
   up.layout = p->layout; up.L = int(p->L); up.s = int(p->s); up.k = p->kup; up.gr = p->grup; up.G = p->group;
-  up.T = p->d_T; up.B = p->d_B; up.w = w; up.cnt = cnt; up.w_tile = p->w_tile_doubles; up.cnt_tile = p->cnt_tile_ints;
+  up.T = p->d_T; up.B = p->d_B; up.w = w; up.cnt = cnt; up.flags = flags; up.w_tile = p->w_tile_doubles; up.cnt_tile = p->cnt_tile_ints;
   M2lParams mp{};
-  mp.A = p->d_A; mp.w = w; mp.c = c; mp.w_tile = p->w_tile_doubles; mp.ntiles = p->ntiles;
+  mp.A = p->d_A; mp.w = w; mp.c = c; mp.flags = flags; mp.gr_up = p->grup; mp.w_tile = p->w_tile_doubles; mp.ntiles = p->ntiles;
   mp.nunits = p->m2l_units; mp.L = int(p->L); mp.cb = p->bps; mp.nst = p->nst;
   DownParams dp{};
   dp.in = in; dp.out = out; dp.ld_in = p->ld_in; dp.ld_out = p->ld_out; dp.n = p->n; dp.N = p->N;
