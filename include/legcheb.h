@@ -73,6 +73,7 @@ typedef struct {
   int32_t subtree;  /* subtree depth k of the execution kernels; 0 -> automatic */
   int32_t stage_blocks; /* FMM blocks (3 A_hat each) per TMA bulk-copy stage; 0 -> automatic */
   int32_t stages;   /* bulk-copy ring depth; 0 -> automatic */
+  int32_t up_subtree; /* subtree depth of the upward (leaf projection + M2M) kernel; 0 -> automatic */
 } lc_plan_opts;
 
 /* Geometry and algorithmic work of a plan (per vector unless stated). */

@@ -40,7 +40,7 @@ class Plan:
 
     def __init__(self, n: int, direction="leg2cheb", batch: int = 1, device=None, s_hat: int = 32,
                  layout="vec", ld_in: int = 0, ld_out: int = 0, vt: int = 0, subtree: int = 0,
-                 stage_blocks: int = 0, stages: int = 0):
+                 stage_blocks: int = 0, stages: int = 0, up_subtree: int = 0):
         lib = _lib.load()
         if device is None:
             device = torch.cuda.current_device()
@@ -51,7 +51,7 @@ class Plan:
         self.layout = LAYOUTS[layout]
         opts = _lib.PlanOpts(s_hat=s_hat, M=18, layout=self.layout, ld_in=ld_in, ld_out=ld_out,
                              device=device.index if device.index is not None else -1, vt=vt, subtree=subtree,
-                             stage_blocks=stage_blocks, stages=stages)
+                             stage_blocks=stage_blocks, stages=stages, up_subtree=up_subtree)
         h = ctypes.c_void_p()
         with torch.cuda.device(device):
             _lib.check("lc_plan_create", lib.lc_plan_create(ctypes.byref(h), self.n, self.direction, self.batch,

@@ -79,6 +79,22 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
+// Phase timestamps for the debug build (-DLC_PHASE_TIMING): %globaltimer (ns) per CTA and phase.
+#ifdef LC_PHASE_TIMING
+__device__ unsigned long long g_lc_ts[3][1 << 20];
+__device__ __forceinline__ void lc_ts(int kern, int slot) {
+  if (threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    const unsigned cta = blockIdx.y * gridDim.x + blockIdx.x;
+    if (cta * 8 + slot < (1u << 20)) g_lc_ts[kern][cta * 8 + slot] = t;
+  }
+}
+#define LC_TS(k, s) lc_ts(k, s)
+#else
+#define LC_TS(k, s) ((void)0)
+#endif
+
 __device__ __forceinline__ int64_t vaddr(int layout, int64_t ld, int64_t v, int64_t j) {
   return layout == LC_VEC_CONTIGUOUS ? v * ld + j : j * ld + v;
 }
@@ -165,6 +181,25 @@ __device__ __forceinline__ void m2m18(const double* __restrict__ x0p, const doub
   }
 }
 
+// Step 4: dst += B(p)^T src with (B(p)^T c)_k = sum_{n>=k} b_nk (-1)^{p(n-k)} c_n
+// = (-1)^{pk} sum_n b_nk c'_n, c'_n = (-1)^{pn} c_n: B(1) is B(0) with the odd diagonals negated
+// ("faster downward spreading").  src/dst in shared memory, B(0) constant,
+// 18 accumulators live (src streamed one value at a time keeps register pressure low).
+__device__ __forceinline__ void l2l18_smem(const double* __restrict__ src, int p, double* __restrict__ dst) {
+  double acc[kM];
+#pragma unroll
+  for (int k = 0; k < kM; ++k) acc[k] = 0.0;
+#pragma unroll
+  for (int n = 0; n < kM; ++n) {
+    double cn = src[n];
+    if ((n & 1) && p) cn = -cn;
+#pragma unroll
+    for (int k = 0; k <= n; ++k) acc[k] = fma(c_B0[n * kM + k], cn, acc[k]);
+  }
+#pragma unroll
+  for (int k = 0; k < kM; ++k) dst[k] += ((k & 1) && p) ? -acc[k] : acc[k];
+}
+
 // one tree level in shared memory ([sigma][node][v][M]); item = (sigma, parent, v); nparent = 2^lp
 template <int VT>
 __device__ __forceinline__ void m2m_level(const double* __restrict__ ch, double* __restrict__ pa, int lp) {
@@ -208,6 +243,7 @@ __global__ void __launch_bounds__(kThreads, 1) lc_up_kernel(const UpParams P) {
 
   const int64_t R = blockIdx.x;
   const int64_t tile = blockIdx.y;
+  LC_TS(0, 0);
   for (int i = tid; i < s * kM; i += blockDim.x) cp_async16(Ts + 2 * i, P.T + 2 * i);
   cp_async_commit();
   griddep_launch();
@@ -238,6 +274,7 @@ __global__ void __launch_bounds__(kThreads, 1) lc_up_kernel(const UpParams P) {
   cp_async_commit();
   cp_async_wait<0>();
   __syncthreads();
+  LC_TS(0, 1);
 
   // step 1: w(L-1)[t][k] = sum_m f[2s t + 2m + sigma] T(sigma)[m][k]   (eq:wMM)
   // item = (v, seg, sigma, group of 6 modes); 3 lanes share each f value.
@@ -271,11 +308,13 @@ __global__ void __launch_bounds__(kThreads, 1) lc_up_kernel(const UpParams P) {
     }
   }
   __syncthreads();
+  LC_TS(0, 2);
   // step 2 inside the subtree
   for (int j = k; j >= 1; --j) {
     m2m_level<VT>(tree + tree_off(j), tree + tree_off(j - 1), j - 1);
     __syncthreads();
   }
+  LC_TS(0, 3);
   double* wt = P.w + tile * P.w_tile;
   const int64_t VM = int64_t(VT) * kM;
   for (int j = 0; j <= k; ++j) {
@@ -290,6 +329,7 @@ __global__ void __launch_bounds__(kThreads, 1) lc_up_kernel(const UpParams P) {
   // the fine levels (gr..L-1) of the whole batch are ready once every CTA got here
   __threadfence();
   __syncthreads();
+  LC_TS(0, 4);
   if (tid == 0) {
     const int total = int(gridDim.x * gridDim.y);
     if (atomicAdd(&P.flags[0], 1) == total - 1) {
@@ -317,6 +357,7 @@ __global__ void __launch_bounds__(kThreads, 1) lc_up_kernel(const UpParams P) {
     }
     __syncthreads();
     if (!s_last) return;
+    LC_TS(0, 5);
     __threadfence();
     const int cnt2 = int((int64_t(1) << ge) * VM / 2);
     for (int sg = 0; sg < 2; ++sg) {
@@ -342,6 +383,7 @@ __global__ void __launch_bounds__(kThreads, 1) lc_up_kernel(const UpParams P) {
     __threadfence();
     g -= ge;
     node = grp;
+    LC_TS(0, 6);
   }
   if (P.gr > 0) {  // this CTA produced one of the 4 level-0 nodes of its vector tile
     __syncthreads();
@@ -415,6 +457,7 @@ __global__ void __launch_bounds__(kM2lThreads) lc_m2l_kernel(const M2lParams P) 
   }
   __syncthreads();
   const int ntiles = int(P.ntiles);
+  LC_TS(1, 0);
 
   griddep_launch();
   if (tid < 32) {
@@ -506,6 +549,7 @@ __global__ void __launch_bounds__(kM2lThreads) lc_m2l_kernel(const M2lParams P) 
     if ((tid & 31) == 0) mbar_arrive(&empty[slot]);  // this warp is done with the slot
   }
   __syncthreads();
+  LC_TS(1, 1);
   if (tid == 0) {  // the last CTA to finish re-arms the readiness flags for the next execution
     if (atomicAdd(&P.flags[4], 1) == int(gridDim.x) - 1) {
       P.flags[1] = 0;
@@ -556,6 +600,7 @@ __global__ void __launch_bounds__(kThreads, 2) lc_down_kernel(const DownParams P
   auto cm_anc = [&](int g) { return cm + int64_t(g) * 2 * VM; };
   auto cm_lvl = [&](int j) { return cm + (int64_t(gr) + (1 << j) - 1) * 2 * VM; };
 
+  LC_TS(2, 0);
   // ---- phase 1a: plan constants (cp.async group 0)
   for (int i = tid; i < kMM / 2; i += blockDim.x) cp_async16(Bs + 2 * i, P.B + 2 * i);
   for (int i = tid; i < s * kM; i += blockDim.x) cp_async16(Tt + 2 * i, P.Tt + 2 * i);
@@ -571,6 +616,7 @@ __global__ void __launch_bounds__(kThreads, 2) lc_down_kernel(const DownParams P
   if (tid == 0) s_work = 0;
   griddep_launch();
   griddep_wait();  // c_m2l (M2L kernel) and the input are ready past this point
+  LC_TS(2, 1);
 
   // ---- phase 1b: data of this CTA (cp.async group 1)
   const double* ct = P.c + tile * P.w_tile;
@@ -615,40 +661,15 @@ __global__ void __launch_bounds__(kThreads, 2) lc_down_kernel(const DownParams P
   cp_async_commit();
   cp_async_wait<0>();
   __syncthreads();
+  LC_TS(2, 2);
 
-  // ---- phase 2a: step 4 along the ancestor chain, warp w < 2VT handles chain (sigma, v) = w,
-  // lane kk < M owns mode kk; the chain vector is exchanged through shared memory.
+  // ---- phase 2a: step 4 along the ancestor chain, one thread per (sigma, v) (registers only);
+  // the band below does not depend on it and keeps the other warps busy meanwhile.
   const int nchain = (L > 0) ? 2 * VT : 0;
-  for (int chn = warp; chn < nchain; chn += kThreads / 32) {
-    double* xc = chw + chn * 32;  // chain vector (kM used)
-    const int kk = lane < kM ? lane : kM - 1;
-    double c = 0.0;
-    for (int g = 0; g < gr; ++g) {
-      const int p = int((R >> (gr - g)) & 1);  // child index of ancestor a_g under a_{g-1}
-      double m = cm_anc(g)[chn * kM + kk];
-      if (g > 0) {
-        double e = 0.0, o = 0.0;
-        for (int n = kk; n < kM; n += 2) e = fma(Bs[n * kM + kk], xc[n], e);
-        for (int n = kk + 1; n < kM; n += 2) o = fma(Bs[n * kM + kk], xc[n], o);
-        m += p ? e - o : e + o;
-      }
-      c = m;
-      __syncwarp();
-      if (lane < kM) xc[lane] = c;
-      __syncwarp();
-    }
-    if (lane < kM) {
-      double* root = cm_lvl(0) + chn * kM;  // [sigma][node 0][v] == chn
-      double m = root[lane];
-      if (gr > 0) {
-        const int p = int(R & 1);
-        double e = 0.0, o = 0.0;
-        for (int n = lane; n < kM; n += 2) e = fma(Bs[n * kM + lane], xc[n], e);
-        for (int n = lane + 1; n < kM; n += 2) o = fma(Bs[n * kM + lane], xc[n], o);
-        m += p ? e - o : e + o;
-      }
-      root[lane] = m;
-    }
+  if (tid < nchain) {
+    // running chain vector c(a_g) in the chain scratch; cm_anc(g) += B(p)^T c(a_{g-1})
+    for (int g = 1; g < gr; ++g) l2l18_smem(cm_anc(g - 1) + tid * kM, int((R >> (gr - g)) & 1), cm_anc(g) + tid * kM);
+    if (gr > 0) l2l18_smem(cm_anc(gr - 1) + tid * kM, int(R & 1), cm_lvl(0) + tid * kM);  // [sigma][node 0][v] == tid
   }
 
   // ---- phase 2b: step 6, the direct band (independent of c), dynamically shared by all warps.
@@ -684,21 +705,37 @@ __global__ void __launch_bounds__(kThreads, 2) lc_down_kernel(const DownParams P
       for (int r = 0; r < kBandR; ++r) {
         acc[r] = 0.0;
         aw[r] = 0.0;
-        bw[r] = tb[pidx(ii + r)];
+        bw[r] = tb[(ii + r) + ((ii + r) >> 4)];
       }
-      for (int c0 = 0; c0 <= cmax; c0 += kBandR) {
+      // (re-loading b[ii+R-1] at c = 0 is harmless: it is the value already in that slot)
+      const int ngrp = (cmax + 1) / kBandR;
+      int c0 = 0;
+      for (int gi = 0; gi < ngrp; ++gi, c0 += kBandR) {
 #pragma unroll
         for (int uu = 0; uu < kBandR; ++uu) {
           const int c = c0 + uu;
-          if (c <= cmax) {
-            aw[uu] = ta[c];
-            if (c >= 1) bw[(uu + kBandR - 1) % kBandR] = tb[pidx(ii + kBandR - 1 + c)];
-            double gval = gv_t[pidx(ii + 2 * c)];
-            if (DIR == 1) gval *= double(i + 2 * c);
+          aw[uu] = ta[c];
+          const int xb = ii + kBandR - 1 + c, xg = ii + 2 * c;
+          bw[(uu + kBandR - 1) % kBandR] = tb[xb + (xb >> 4)];
+          double gval = gv_t[xg + (xg >> 4)];
+          if (DIR == 1) gval *= double(i + 2 * c);
 #pragma unroll
-            for (int r = 0; r < kBandR; ++r)
-              acc[r] = fma(aw[(uu - r + kBandR) % kBandR] * bw[(r + uu) % kBandR], gval, acc[r]);
-          }
+          for (int r = 0; r < kBandR; ++r)
+            acc[r] = fma(aw[(uu - r + kBandR) % kBandR] * bw[(r + uu) % kBandR], gval, acc[r]);
+        }
+      }
+#pragma unroll
+      for (int uu = 0; uu < kBandR; ++uu) {  // remainder, c = c0 + uu <= cmax
+        const int c = c0 + uu;
+        if (c <= cmax) {
+          aw[uu] = ta[c];
+          const int xb = ii + kBandR - 1 + c, xg = ii + 2 * c;
+          bw[(uu + kBandR - 1) % kBandR] = tb[xb + (xb >> 4)];
+          double gval = gv_t[xg + (xg >> 4)];
+          if (DIR == 1) gval *= double(i + 2 * c);
+#pragma unroll
+          for (int r = 0; r < kBandR; ++r)
+            acc[r] = fma(aw[(uu - r + kBandR) % kBandR] * bw[(r + uu) % kBandR], gval, acc[r]);
         }
       }
 #pragma unroll
@@ -716,31 +753,28 @@ __global__ void __launch_bounds__(kThreads, 2) lc_down_kernel(const DownParams P
     }
   }
   __syncthreads();
+  LC_TS(2, 3);
 
-  // ---- phase 3: step 4 down the subtree, one thread per output mode: c(j) = B(p)^T c(j-1) + c_m2l(j)
+  // ---- phase 3: step 4 down the subtree, one thread per (sigma, node, v):
+  // c(j) = B(p)^T c(j-1) + c_m2l(j), in place, B(0) from constant memory
   if (L > 0) {
     for (int j = 1; j <= k; ++j) {
       const int nodes = 1 << j;
       const double* par = cm_lvl(j - 1);
       double* cur = cm_lvl(j);
-      const int items = 2 * nodes * VT * kM;
+      const int items = 2 * nodes * VT;
       for (int it = tid; it < items; it += blockDim.x) {
-        const int kk = it % kM;
-        const int r = it / kM;  // (sigma * nodes + node) * VT + v
-        const int v = r % VT;
-        const int sn = r / VT;
-        const int node = sn % nodes;
-        const int sg = sn / nodes;
-        const double* src = par + ((sg * (nodes >> 1) + (node >> 1)) * VT + v) * kM;
-        double e = 0.0, o = 0.0;
-        for (int n = kk; n < kM; n += 2) e = fma(Bs[n * kM + kk], src[n], e);
-        for (int n = kk + 1; n < kM; n += 2) o = fma(Bs[n * kM + kk], src[n], o);
-        cur[r * kM + kk] += (node & 1) ? e - o : e + o;
+        const int v = it % VT;
+        const int sn = it / VT;
+        const int node = sn & (nodes - 1);
+        const int sg = sn >> j;
+        l2l18_smem(par + ((sg * (nodes >> 1) + (node >> 1)) * VT + v) * kM, node & 1, cur + it * kM);
       }
       __syncthreads();
     }
   }
   const double* cfin = cm_lvl(k);
+  LC_TS(2, 4);
 
   // ---- phase 4: step 5 (z^sigma += c(L-1) T(sigma)^T, eq:step5), step 7 (C^{-1}), store
   const double inv_pi = 0.318309886183790671537767526745028724;
@@ -769,6 +803,8 @@ __global__ void __launch_bounds__(kThreads, 2) lc_down_kernel(const DownParams P
     else
       P.out[i * P.ld_out + gv] = z;
   }
+  __syncthreads();
+  LC_TS(2, 5);
 }
 
 // ============================================================== host side
@@ -837,8 +873,10 @@ lc_status configure_kernels(lc_plan* p) {
   while (m2l_smem_bytes(vt, cb, nst) > budget && cb > 1) --cb;
   if (m2l_smem_bytes(vt, cb, nst) > smax) return LC_ERR_INVALID_ARG;
   // up kernel: deeper subtrees (its shared memory is small); continuation step = its depth
-  int kup = p->L > 0 ? int(std::min<int64_t>(5, p->L - 1)) : 0;
-  while (kup > 0 && up_smem_bytes(vt, kup, int(p->s)) > budget) --kup;
+  const bool user_kup = p->kup > 0;
+  int kup = p->L > 0 ? int(std::min<int64_t>(user_kup ? p->kup : 5, p->L - 1)) : 0;
+  while (!user_kup && kup > 0 && up_smem_bytes(vt, kup, int(p->s)) > budget) --kup;
+  if (up_smem_bytes(vt, kup, int(p->s)) > smax) return LC_ERR_INVALID_ARG;
   p->vt = vt;
   p->k = k;
   p->bps = cb;
@@ -1016,3 +1054,11 @@ extern "C" lc_status lc_execute_host(const lc_plan* p_, const double* h_in, doub
   cudaSetDevice(prev);
   return rc;
 }
+
+#ifdef LC_PHASE_TIMING
+extern "C" int lc_debug_timestamps(int kern, unsigned long long* host_out, long long count) {
+  if (kern < 0 || kern > 2 || count > (1 << 20)) return 1;
+  return cudaMemcpyFromSymbol(host_out, lc::g_lc_ts, sizeof(unsigned long long) * count,
+                              sizeof(unsigned long long) * (size_t(kern) << 20)) == cudaSuccess ? 0 : 1;
+}
+#endif

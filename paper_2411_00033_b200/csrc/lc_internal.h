@@ -48,7 +48,7 @@ inline Geometry geometry(int64_t n, int64_t s_hat) {
   return G;
 }
 
-constexpr int kBandR = 4;            // rows per thread in the register-blocked band (step 6)
+constexpr int kBandR = 8;            // rows per thread in the register-blocked band (step 6)
 
 // Padded index of the band tiles: one pad double every 16, so that threads
 // whose rows are 2*kBandR apart hit distinct shared-memory banks.

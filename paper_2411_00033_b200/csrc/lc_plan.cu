@@ -300,7 +300,7 @@ extern "C" lc_status lc_plan_create(lc_plan** out, int64_t n, lc_direction dir, 
   p->n = n; p->N = G.N; p->L = G.L; p->s = G.s; p->M = kM; p->batch = batch; p->nc = G.nc;
   p->dir = int(dir); p->layout = o.layout; p->ld_in = o.ld_in; p->ld_out = o.ld_out;
   p->device = dev; p->sm_count = prop.multiProcessorCount;
-  p->vt = o.vt; p->k = o.subtree; p->bps = o.stage_blocks; p->nst = o.stages;
+  p->vt = o.vt; p->k = o.subtree; p->bps = o.stage_blocks; p->nst = o.stages; p->kup = o.up_subtree;
 
   auto fail = [&](lc_status st) {
     lc_plan_destroy(p);
