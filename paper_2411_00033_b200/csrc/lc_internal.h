@@ -58,8 +58,7 @@ __host__ __device__ inline int64_t align_up(int64_t x, int64_t a) { return (x + 
 
 // Shared-memory layout of the down kernel (host computes the size, device the offsets).
 struct DownSmem {
-  int64_t Bs, Tt, ta, tb, gt, zst, cm, chw, total;  // byte offsets
-  int64_t tp;                              // padded band-tile length (doubles)
+  int64_t Tt, zb, cm, total;  // byte offsets
 };
 
 // c_m2l nodes staged by the down kernel: gr ancestors + the 2^(k+1)-1 subtree nodes.
@@ -70,33 +69,40 @@ __host__ __device__ inline DownSmem down_smem_layout(int VT, int k, int s, int g
   int64_t o = 0;
   const int64_t node = int64_t(2) * VT * kM * 8;  // one segment, both parities, VT vectors
   const int64_t nleaf = int64_t(1) << k;
-  const int64_t tcols = (nleaf + 2) * 2 * s;
-  L.tp = pidx(tcols + 2 * kBandR) + 2;
-  L.Bs = o;    o = align_up(o + int64_t(kMM) * 8, 128);
-  L.Tt = o;    o = align_up(o + int64_t(2) * kM * s * 8 + 2 * kBandR * 8, 128);
-  L.ta = o;    o = align_up(o + (int64_t(2) * s + 2 * kBandR) * 8, 128);
-  L.tb = o;    o = align_up(o + L.tp * 8, 128);
-  L.gt = o;    o = align_up(o + int64_t(VT) * L.tp * 8, 128);
-  L.zst = o;   o = align_up(o + int64_t(VT) * nleaf * 2 * s * 8, 128);
+  L.Tt = o;    o = align_up(o + int64_t(2) * kM * s * 8, 128);
+  L.zb = o;    o = align_up(o + int64_t(VT) * nleaf * 2 * s * 8, 128);
   L.cm = o;    o = align_up(o + down_cm_nodes(k, gr) * node, 128);
-  L.chw = o;   o = align_up(o + int64_t(2) * VT * 32 * 8, 128);  // ancestor-chain exchange (per chain: 32 doubles)
   L.total = o;
   return L;
 }
 
-// M2L streaming kernel: per ring slot, the A_hat of `cb` blocks plus the w window
-// (2 cb column segments, both parities, VT vectors).
-__host__ __device__ inline int64_t m2l_slot_bytes(int VT, int cb) {
-  return align_up(int64_t(cb) * 3 * kMM * 8, 128) + align_up(int64_t(2) * (2 * cb) * VT * kM * 8, 128);
-}
-__host__ __device__ inline int64_t m2l_smem_bytes(int VT, int cb, int nst) {
-  return int64_t(nst) * m2l_slot_bytes(VT, cb) + align_up(int64_t(2) * nst * 8, 128);  // + full/empty barriers
+// Streaming kernel: a ring of nst slots, each with the A_hat of `cb` blocks plus the w window
+// (2 cb column segments, both parities, VT vectors); and the band region for a band unit of
+// 2^kb leaf segments: tabA, padded tabB and input tiles, and the z staging tile.
+struct StreamSmem {
+  int64_t slot, ring, ta, tb, gt, zst, bars, total;
+  int64_t tp;  // padded band-tile length (doubles)
+};
+__host__ __device__ inline StreamSmem stream_smem_layout(int VT, int cb, int nst, int kb, int s) {
+  StreamSmem L{};
+  L.slot = align_up(int64_t(cb) * 3 * kMM * 8, 128) + align_up(int64_t(2) * (2 * cb) * VT * kM * 8, 128);
+  int64_t o = 0;
+  L.ring = o;  o += int64_t(nst) * L.slot;
+  const int64_t nleaf = int64_t(1) << kb;
+  const int64_t tcols = (nleaf + 2) * 2 * s;
+  L.tp = pidx(tcols + 2 * kBandR) + 2;
+  L.ta = o;    o = align_up(o + (int64_t(2) * s + 2 * kBandR) * 8, 128);
+  L.tb = o;    o = align_up(o + L.tp * 8, 128);
+  L.gt = o;    o = align_up(o + int64_t(VT) * L.tp * 8, 128);
+  L.zst = o;   o = align_up(o + int64_t(VT) * nleaf * 2 * s * 8, 128);
+  L.bars = o;  o = align_up(o + int64_t(2) * nst * 8, 128);
+  L.total = o;
+  return L;
 }
 
 __host__ __device__ inline int64_t up_smem_bytes(int VT, int k, int s) {
   int64_t o = 0;
   o = align_up(o + int64_t(2) * s * kM * 8, 128);                 // T [2][s][M]
-  o = align_up(o + int64_t(kMM) * 8, 128);                        // B(0)^T
   o = align_up(o + int64_t(VT) * (int64_t(1) << k) * 2 * s * 8, 128);  // f tile
   o = align_up(o + ((int64_t(2) << k) - 1) * 2 * VT * kM * 8, 128);    // w tree
   o += 16;
@@ -113,9 +119,11 @@ struct lc_plan {
   int device;
   int sm_count;
   // kernel configuration
-  int vt, k, gr, bps, nst, group, kup, grup;
-  int64_t m2l_units;  // (chunk, tile) work units of the M2L kernel
-  int m2l_grid;
+  int vt, k, gr, bps, nst, group, kup, grup, kb;
+  int64_t m2l_units;   // (chunk, tile) M2L work units of the streaming kernel
+  int64_t band_units;  // (leaf range, tile) band work units of the streaming kernel
+  int stream_grid;
+  size_t smem_stream;
   int64_t ntiles;
   int64_t w_tile_doubles, cnt_tile_ints;
   size_t ws_bytes;
