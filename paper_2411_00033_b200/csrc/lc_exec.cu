@@ -224,7 +224,7 @@ struct UpParams {
   double* w;
   int* cnt;
   int* flags;
-  int64_t w_tile, cnt_tile;
+  int64_t w_tile, cnt_tile, ntiles;
 };
 
 struct StreamParams {
@@ -272,22 +272,53 @@ __device__ __forceinline__ void m2m_level(const double* __restrict__ ch, double*
   }
 }
 
+// Persistent: grid <= one CTA per SM (so that a streaming CTA fits beside it); task t =
+// (subtree R, vector tile) for t = blockIdx.x + i * gridDim.x.  The input tile of the next task
+// is prefetched (cp.async, double buffer) while the current one is processed.
+template <int VT>
+__device__ __forceinline__ void up_stage_input(const UpParams& P, double* fs, int64_t R, int64_t tile, int tlen) {
+  const int64_t j0 = R * tlen;
+  if (P.layout == LC_VEC_CONTIGUOUS) {
+#pragma unroll 1
+    for (int v = 0; v < VT; ++v) {
+      const int64_t gv = tile * VT + v;
+      const double* src = P.in + gv * P.ld_in + j0;
+      const int64_t lim = gv < P.batch ? P.n - j0 : 0;  // valid elements of this vector in the tile
+      for (int jj = threadIdx.x; jj < tlen; jj += blockDim.x) {
+        const bool ok = jj < lim;
+        cp_async8(fs + v * tlen + jj, ok ? src + jj : P.in, ok ? 8u : 0u);
+      }
+    }
+  } else {
+    for (int idx = threadIdx.x; idx < VT * tlen; idx += blockDim.x) {
+      const int jj = idx / VT, v = idx - jj * VT;  // v fastest: coalesced in the batch layout
+      const int64_t gv = tile * VT + v, j = j0 + jj;
+      const bool ok = gv < P.batch && j < P.n;
+      cp_async8(fs + v * tlen + jj, ok ? P.in + j * P.ld_in + gv : P.in, ok ? 8u : 0u);
+    }
+  }
+  cp_async_commit();
+}
+
 template <int VT>
 __global__ void __launch_bounds__(kThreads, 2) lc_up_kernel(const UpParams P) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ int s_last;
   const int s = P.s, k = P.k;
   const int tid = threadIdx.x;
-  double* Ts = reinterpret_cast<double*>(smem);
-  double* fs = reinterpret_cast<double*>(smem + align_up(int64_t(2) * s * kM * 8, 128));
   const int nleaf = 1 << k;
   const int seglen = 2 * s;
   const int tlen = nleaf * seglen;
-  double* tree = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(fs) + align_up(int64_t(VT) * tlen * 8, 128));
+  double* Ts = reinterpret_cast<double*>(smem);
+  double* fbuf[2];
+  fbuf[0] = reinterpret_cast<double*>(smem + align_up(int64_t(2) * s * kM * 8, 128));
+  fbuf[1] = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(fbuf[0]) + align_up(int64_t(VT) * tlen * 8, 128));
+  double* tree = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(fbuf[1]) + align_up(int64_t(VT) * tlen * 8, 128));
   auto tree_off = [&](int j) { return ((1 << j) - 1) * 2 * VT * kM; };
+  const int64_t nsub = int64_t(4) << P.gr;
+  const int64_t ntasks = nsub * P.ntiles;
+  const int64_t VM = int64_t(VT) * kM;
 
-  const int64_t R = blockIdx.x;
-  const int64_t tile = blockIdx.y;
   LC_TS(0, 0);
   BRow br;
   load_brow(br, P.B, tid & 31);
@@ -299,89 +330,79 @@ __global__ void __launch_bounds__(kThreads, 2) lc_up_kernel(const UpParams P) {
   griddep_launch();
   if (tid == 0) st_release(&P.flags[5], 1);  // predecessor complete: the streaming kernel may read the input
 
-  // stage the leaf range [R 2^k, (R+1) 2^k) of segments, zero padding beyond n
-  const int64_t j0 = R * tlen;
-  if (P.layout == LC_VEC_CONTIGUOUS) {
-#pragma unroll 1
-    for (int v = 0; v < VT; ++v) {
-      const int64_t gv = tile * VT + v;
-      const double* src = P.in + gv * P.ld_in + j0;
-      const int64_t lim = gv < P.batch ? P.n - j0 : 0;  // valid elements of this vector in the tile
-      for (int jj = tid; jj < tlen; jj += blockDim.x) {
-        const bool ok = jj < lim;
-        cp_async8(fs + v * tlen + jj, ok ? src + jj : P.in, ok ? 8u : 0u);
-      }
+  int64_t t = blockIdx.x;
+  if (t < ntasks) up_stage_input<VT>(P, fbuf[0], t % nsub, t / nsub, tlen);
+  int buf = 0;
+  for (; t < ntasks; t += gridDim.x, buf ^= 1) {
+    const int64_t R = t % nsub, tile = t / nsub;
+    const int64_t tn = t + gridDim.x;
+    if (tn < ntasks) {
+      up_stage_input<VT>(P, fbuf[buf ^ 1], tn % nsub, tn / nsub, tlen);  // prefetch the next task
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
     }
-  } else {
-    for (int idx = tid; idx < VT * tlen; idx += blockDim.x) {
-      const int jj = idx / VT, v = idx - jj * VT;  // v fastest: coalesced in the batch layout
-      const int64_t gv = tile * VT + v, j = j0 + jj;
-      const bool ok = gv < P.batch && j < P.n;
-      cp_async8(fs + v * tlen + jj, ok ? P.in + j * P.ld_in + gv : P.in, ok ? 8u : 0u);
-    }
-  }
-  cp_async_commit();
-  cp_async_wait<0>();
-  __syncthreads();
-  LC_TS(0, 1);
-
-  // step 1: w(L-1)[t][k] = sum_m f[2s t + 2m + sigma] T(sigma)[m][k]   (eq:wMM)
-  // item = (v, seg, sigma, group of 6 modes); 3 lanes share each f value.
-  {
-    double* leaf = tree + tree_off(k);
-    const int items = nleaf * 2 * VT * 3;
-    for (int it = tid; it < items; it += blockDim.x) {
-      const int kg = it % 3;
-      int r = it / 3;
-      const int sg = r & 1;
-      r >>= 1;
-      const int seg = r & (nleaf - 1);
-      const int v = r >> k;
-      const double* fp = fs + v * tlen + seg * seglen + sg;
-      const double* tp = Ts + sg * s * kM + 6 * kg;
-      double a0 = 0, a1 = 0, a2 = 0, a3 = 0, a4 = 0, a5 = 0;
-#pragma unroll 4
-      for (int m = 0; m < s; ++m) {
-        const double f = fp[2 * m];
-        const double2 t01 = *reinterpret_cast<const double2*>(tp + m * kM);
-        const double2 t23 = *reinterpret_cast<const double2*>(tp + m * kM + 2);
-        const double2 t45 = *reinterpret_cast<const double2*>(tp + m * kM + 4);
-        a0 = fma(f, t01.x, a0); a1 = fma(f, t01.y, a1);
-        a2 = fma(f, t23.x, a2); a3 = fma(f, t23.y, a3);
-        a4 = fma(f, t45.x, a4); a5 = fma(f, t45.y, a5);
-      }
-      double* o = leaf + ((sg * nleaf + seg) * VT + v) * kM + 6 * kg;
-      *reinterpret_cast<double2*>(o) = make_double2(a0, a1);
-      *reinterpret_cast<double2*>(o + 2) = make_double2(a2, a3);
-      *reinterpret_cast<double2*>(o + 4) = make_double2(a4, a5);
-    }
-  }
-  __syncthreads();
-  LC_TS(0, 2);
-  // step 2 inside the subtree
-  for (int j = k; j >= 1; --j) {
-    m2m_level<VT>(tree + tree_off(j), tree + tree_off(j - 1), j - 1, br);
     __syncthreads();
-  }
-  LC_TS(0, 3);
-  double* wt = P.w + tile * P.w_tile;
-  const int64_t VM = int64_t(VT) * kM;
-  for (int j = 0; j <= k; ++j) {
-    const int g = P.gr + j;
-    const int cnt2 = int((int64_t(1) << j) * VM / 2);
-    for (int sg = 0; sg < 2; ++sg) {
-      double2* dst = reinterpret_cast<double2*>(wt + (w_level_offset_units(g) + sg * nseg(g) + (R << j)) * VM);
-      const double2* src = reinterpret_cast<const double2*>(tree + tree_off(j) + sg * (int64_t(1) << j) * VM);
-      for (int i = tid; i < cnt2; i += blockDim.x) dst[i] = src[i];
+    LC_TS(0, 1);
+    const double* fs = fbuf[buf];
+    // step 1: w(L-1)[t][k] = sum_m f[2s t + 2m + sigma] T(sigma)[m][k]   (eq:wMM)
+    // item = (v, seg, sigma, group of 6 modes); 3 lanes share each f value.
+    {
+      double* leaf = tree + tree_off(k);
+      const int items = nleaf * 2 * VT * 3;
+      for (int it = tid; it < items; it += blockDim.x) {
+        const int kg = it % 3;
+        int r = it / 3;
+        const int sg = r & 1;
+        r >>= 1;
+        const int seg = r & (nleaf - 1);
+        const int v = r >> k;
+        const double* fp = fs + v * tlen + seg * seglen + sg;
+        const double* tp = Ts + sg * s * kM + 6 * kg;
+        double a0 = 0, a1 = 0, a2 = 0, a3 = 0, a4 = 0, a5 = 0;
+#pragma unroll 4
+        for (int m = 0; m < s; ++m) {
+          const double f = fp[2 * m];
+          const double2 t01 = *reinterpret_cast<const double2*>(tp + m * kM);
+          const double2 t23 = *reinterpret_cast<const double2*>(tp + m * kM + 2);
+          const double2 t45 = *reinterpret_cast<const double2*>(tp + m * kM + 4);
+          a0 = fma(f, t01.x, a0); a1 = fma(f, t01.y, a1);
+          a2 = fma(f, t23.x, a2); a3 = fma(f, t23.y, a3);
+          a4 = fma(f, t45.x, a4); a5 = fma(f, t45.y, a5);
+        }
+        double* o = leaf + ((sg * nleaf + seg) * VT + v) * kM + 6 * kg;
+        *reinterpret_cast<double2*>(o) = make_double2(a0, a1);
+        *reinterpret_cast<double2*>(o + 2) = make_double2(a2, a3);
+        *reinterpret_cast<double2*>(o + 4) = make_double2(a4, a5);
+      }
     }
+    __syncthreads();
+    LC_TS(0, 2);
+    // step 2 inside the subtree
+    for (int j = k; j >= 1; --j) {
+      m2m_level<VT>(tree + tree_off(j), tree + tree_off(j - 1), j - 1, br);
+      __syncthreads();
+    }
+    LC_TS(0, 3);
+    double* wt = P.w + tile * P.w_tile;
+    for (int j = 0; j <= k; ++j) {
+      const int g = P.gr + j;
+      const int cnt2 = int((int64_t(1) << j) * VM / 2);
+      for (int sg = 0; sg < 2; ++sg) {
+        double2* dst = reinterpret_cast<double2*>(wt + (w_level_offset_units(g) + sg * nseg(g) + (R << j)) * VM);
+        const double2* src = reinterpret_cast<const double2*>(tree + tree_off(j) + sg * (int64_t(1) << j) * VM);
+        for (int i = tid; i < cnt2; i += blockDim.x) dst[i] = src[i];
+      }
+    }
+    __syncthreads();  // the tree is rebuilt by the next task
   }
-  // the fine levels (gr..L-1) of the whole batch are ready once every CTA got here
+  // the fine levels (gr..L-1) of the whole batch are ready once every task is written
   __threadfence();
   __syncthreads();
   LC_TS(0, 4);
-  if (tid == 0) {
-    const int total = int(gridDim.x * gridDim.y);
-    if (atomicAdd(&P.flags[0], 1) == total - 1) {
+  const int64_t nmine = ntasks > int64_t(blockIdx.x) ? (ntasks - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  if (tid == 0 && nmine > 0) {
+    if (atomicAdd(&P.flags[0], int(nmine)) == int(ntasks - nmine)) {
       atomicExch(&P.flags[0], 0);
       __threadfence();
       st_release(&P.flags[1], 1);
@@ -389,59 +410,63 @@ __global__ void __launch_bounds__(kThreads, 2) lc_up_kernel(const UpParams P) {
     }
   }
 
-  // upward continuation above the subtree roots: the last arriver of each
-  // group of 2^G nodes merges them G levels up (threadfence-reduction pattern).
-  int g = P.gr;
-  int64_t node = R;
-  while (g > 0) {
-    const int ge = min(P.G, g);
-    const int64_t grp = node >> ge;
-    __syncthreads();
-    if (tid == 0) {
-      int* c = P.cnt + tile * P.cnt_tile + (nseg(g) - 4) + grp;
-      const int old = atomicAdd(c, 1);
-      const int last = (old == (1 << ge) - 1);
-      if (last) atomicExch(c, 0);  // self-reset for the next launch
-      s_last = last;
-    }
-    __syncthreads();
-    if (!s_last) return;
-    LC_TS(0, 5);
-    __threadfence();
-    const int cnt2 = int((int64_t(1) << ge) * VM / 2);
-    for (int sg = 0; sg < 2; ++sg) {
-      const double2* src =
-          reinterpret_cast<const double2*>(wt + (w_level_offset_units(g) + sg * nseg(g) + (grp << ge)) * VM);
-      double2* dst = reinterpret_cast<double2*>(tree + tree_off(ge) + sg * 2 * cnt2);
-      for (int i = tid; i < cnt2; i += blockDim.x) dst[i] = __ldcg(src + i);
-    }
-    __syncthreads();
-    for (int j = ge; j >= 1; --j) {
-      m2m_level<VT>(tree + tree_off(j), tree + tree_off(j - 1), j - 1, br);
+  // upward continuation above the subtree roots: for each task of this CTA, the last arriver of
+  // each group of 2^G nodes merges them G levels up (threadfence-reduction pattern).
+  for (int64_t t0 = blockIdx.x; t0 < ntasks; t0 += gridDim.x) {
+    const int64_t tile = t0 / nsub;
+    double* wt = P.w + tile * P.w_tile;
+    int g = P.gr;
+    int64_t node = t0 % nsub;
+    while (g > 0) {
+      const int ge = min(P.G, g);
+      const int64_t grp = node >> ge;
       __syncthreads();
-    }
-    for (int j = 0; j < ge; ++j) {
-      const int gg = g - ge + j;
-      const int cj2 = int((int64_t(1) << j) * VM / 2);
-      for (int sg = 0; sg < 2; ++sg) {
-        double2* dst = reinterpret_cast<double2*>(wt + (w_level_offset_units(gg) + sg * nseg(gg) + (grp << j)) * VM);
-        const double2* src = reinterpret_cast<const double2*>(tree + tree_off(j) + sg * 2 * cj2);
-        for (int i = tid; i < cj2; i += blockDim.x) dst[i] = src[i];
+      if (tid == 0) {
+        int* c = P.cnt + tile * P.cnt_tile + (nseg(g) - 4) + grp;
+        const int old = atomicAdd(c, 1);
+        const int last = (old == (1 << ge) - 1);
+        if (last) atomicExch(c, 0);  // self-reset for the next launch
+        s_last = last;
       }
-    }
-    __threadfence();
-    g -= ge;
-    node = grp;
-    LC_TS(0, 6);
-  }
-  if (P.gr > 0) {  // this CTA produced one of the 4 level-0 nodes of its vector tile
-    __syncthreads();
-    if (tid == 0) {
-      const int total = 4 * int(gridDim.y);
-      if (atomicAdd(&P.flags[2], 1) == total - 1) {
-        atomicExch(&P.flags[2], 0);
-        __threadfence();
-        st_release(&P.flags[3], 1);
+      __syncthreads();
+      if (!s_last) break;
+      LC_TS(0, 5);
+      __threadfence();
+      const int cnt2 = int((int64_t(1) << ge) * VM / 2);
+      for (int sg = 0; sg < 2; ++sg) {
+        const double2* src =
+            reinterpret_cast<const double2*>(wt + (w_level_offset_units(g) + sg * nseg(g) + (grp << ge)) * VM);
+        double2* dst = reinterpret_cast<double2*>(tree + tree_off(ge) + sg * 2 * cnt2);
+        for (int i = tid; i < cnt2; i += blockDim.x) dst[i] = __ldcg(src + i);
+      }
+      __syncthreads();
+      for (int j = ge; j >= 1; --j) {
+        m2m_level<VT>(tree + tree_off(j), tree + tree_off(j - 1), j - 1, br);
+        __syncthreads();
+      }
+      for (int j = 0; j < ge; ++j) {
+        const int gg = g - ge + j;
+        const int cj2 = int((int64_t(1) << j) * VM / 2);
+        for (int sg = 0; sg < 2; ++sg) {
+          double2* dst = reinterpret_cast<double2*>(wt + (w_level_offset_units(gg) + sg * nseg(gg) + (grp << j)) * VM);
+          const double2* src = reinterpret_cast<const double2*>(tree + tree_off(j) + sg * 2 * cj2);
+          for (int i = tid; i < cj2; i += blockDim.x) dst[i] = src[i];
+        }
+      }
+      __threadfence();
+      g -= ge;
+      node = grp;
+      LC_TS(0, 6);
+      if (g == 0) {  // this CTA produced one of the 4 level-0 nodes of the vector tile
+        __syncthreads();
+        if (tid == 0) {
+          const int total = 4 * int(P.ntiles);
+          if (atomicAdd(&P.flags[2], 1) == total - 1) {
+            atomicExch(&P.flags[2], 0);
+            __threadfence();
+            st_release(&P.flags[3], 1);
+          }
+        }
       }
     }
   }
@@ -902,30 +927,53 @@ __global__ void __launch_bounds__(kThreads, 2) lc_down_kernel(const DownParams P
   LC_TS(2, 4);
   const double* cfin = cm_lvl(k);
 
-  // step 5: z^sigma += c(L-1) T(sigma)^T (eq:step5); step 7: C^{-1} (L2C); coalesced store
-  const double inv_pi = 0.318309886183790671537767526745028724;
-  for (int idx = tid; idx < VT * rows; idx += blockDim.x) {
-    const int v = idx / rows;
-    const int ii = idx - v * rows;
-    const int64_t gv = tile * VT + v;
-    if (ii >= olim || gv >= P.batch) continue;
-    const int u = ii / seglen;
-    const int rr = ii - u * seglen;
-    const int sg = rr & 1, m = rr >> 1;
-    double t5 = 0.0;
-    if (L > 0) {
+  // step 5: z^sigma += c(L-1) T(sigma)^T (eq:step5), 4 same-parity rows per thread (c kept in
+  // registers), accumulated into the band result in shared memory
+  if (L > 0) {
+    constexpr int R5 = 4;
+    const int nb5 = (s + R5 - 1) / R5;
+    const int items = VT * nleaf * 2 * nb5;
+    for (int it = tid; it < items; it += blockDim.x) {
+      const int mb = it % nb5;
+      int r_ = it / nb5;
+      const int sg = r_ & 1;
+      r_ >>= 1;
+      const int u = r_ & (nleaf - 1);
+      const int v = r_ >> k;
+      const int m0 = R5 * mb;
       const double* cp = cfin + ((sg * nleaf + u) * VT + v) * kM;
-      const double* tq = Tt + sg * kM * s + m;
+      const double* tq = Tt + sg * kM * s + m0;
+      double t5[R5];
 #pragma unroll
-      for (int kk = 0; kk < kM; ++kk) t5 = fma(cp[kk], tq[kk * s], t5);
+      for (int r = 0; r < R5; ++r) t5[r] = 0.0;
+#pragma unroll
+      for (int kk = 0; kk < kM; ++kk) {
+        const double cv = cp[kk];
+#pragma unroll
+        for (int r = 0; r < R5; ++r) t5[r] = fma(cv, tq[kk * s + r], t5[r]);  // (tq beyond s: padding, unused)
+      }
+      double* zr = zb + v * rows + u * seglen + sg + 2 * m0;
+#pragma unroll
+      for (int r = 0; r < R5; ++r)
+        if (m0 + r < s) zr[2 * r] += t5[r];
     }
-    const int64_t i = i0 + ii;
-    double z = zb[idx] + t5;
-    if (DIR == 0) z *= (i == 0 ? inv_pi : 2.0 * inv_pi);  // step 7: C^{-1}
-    if (P.layout == LC_VEC_CONTIGUOUS)
-      P.out[gv * P.ld_out + i] = z;
-    else
-      P.out[i * P.ld_out + gv] = z;
+    __syncthreads();
+  }
+  // step 7: C^{-1} (L2C); coalesced store
+  const double inv_pi = 0.318309886183790671537767526745028724;
+#pragma unroll 1
+  for (int v = 0; v < VT; ++v) {
+    const int64_t gv = tile * VT + v;
+    if (gv >= P.batch) break;
+    for (int ii = tid; ii < olim; ii += blockDim.x) {
+      const int64_t i = i0 + ii;
+      double z = zb[v * rows + ii];
+      if (DIR == 0) z *= (i == 0 ? inv_pi : 2.0 * inv_pi);
+      if (P.layout == LC_VEC_CONTIGUOUS)
+        P.out[gv * P.ld_out + i] = z;
+      else
+        P.out[i * P.ld_out + gv] = z;
+    }
   }
   __syncthreads();
   LC_TS(2, 5);
@@ -992,7 +1040,7 @@ lc_status configure_kernels(lc_plan* p) {
   const bool user_k = p->k > 0;
   int k = user_k ? p->k : 4;
   int cb = p->bps > 0 ? p->bps : 3;
-  int nst = p->nst > 0 ? p->nst : 3;
+  int nst = p->nst > 0 ? p->nst : 4;
   if (nst > 8) return LC_ERR_INVALID_ARG;
   const int64_t nleaf_total = p->L > 0 ? (int64_t(2) << p->L) : 2;  // leaf segments (L = 0: the two halves)
   int lnleaf = 0;
@@ -1013,13 +1061,15 @@ lc_status configure_kernels(lc_plan* p) {
   // streaming kernel: band units of 2^kb leaf segments
   int kb = std::min(4, lnleaf);  // 2^kb segments x 2 parities x ceil(s/R) blocks = one item per band thread
   auto stream_bytes = [&](int cb_, int kb_) { return stream_smem_layout(vt, cb_, nst, kb_, int(p->s)).total; };
-  while (stream_bytes(cb, kb) > budget2 && kb > 1) --kb;
-  while (stream_bytes(cb, kb) > budget2 && cb > 1) --cb;
+  const int64_t budget_stream = 150 * 1024;  // leaves room for one up-kernel CTA on the same SM
+  while (stream_bytes(cb, kb) > budget_stream && kb > 1) --kb;
+  while (stream_bytes(cb, kb) > budget_stream && nst > 2) --nst;
+  while (stream_bytes(cb, kb) > budget_stream && cb > 1) --cb;
   if (stream_bytes(cb, kb) > smax) return LC_ERR_INVALID_ARG;
   // up kernel: deeper subtrees (its shared memory is small); continuation step = its depth
   const bool user_kup = p->kup > 0;
   int kup = p->L > 0 ? int(std::min<int64_t>(user_kup ? p->kup : 5, p->L - 1)) : 0;
-  while (!user_kup && kup > 0 && up_smem_bytes(vt, kup, int(p->s)) > budget2) --kup;
+  while (!user_kup && kup > 0 && up_smem_bytes(vt, kup, int(p->s)) > 74 * 1024) --kup;
   if (up_smem_bytes(vt, kup, int(p->s)) > smax) return LC_ERR_INVALID_ARG;
   p->vt = vt;
   p->k = k;
@@ -1048,9 +1098,9 @@ lc_status configure_kernels(lc_plan* p) {
       default: occ = stream_occupancy<8>(p->dir, p->smem_stream); break;
     }
     if (occ < 1) return LC_ERR_INVALID_ARG;
-    // persistent grid: every CTA co-resident (the producer may wait on flags raised by other grids)
-    const int64_t g = int64_t(occ) * p->sm_count;
-    p->stream_grid = int(std::max<int64_t>(1, std::min<int64_t>(g, p->m2l_units + p->band_units)));
+    // persistent grid, one CTA per SM (a single deep TMA ring per SM streams fastest; the up
+    // kernel's CTA fits beside it)
+    p->stream_grid = int(std::max<int64_t>(1, std::min<int64_t>(p->sm_count, p->m2l_units + p->band_units)));
   }
   if (p->L > 0) {
     p->w_tile_doubles = int64_t(vt) * kM * 2 * ((int64_t(4) << p->L) - 4);
@@ -1128,7 +1178,7 @@ lc_status launch_execute(const lc_plan* p, const double* in, double* out, void* 
   up.in = in; up.ld_in = p->ld_in; up.n = p->n; up.N = p->N; up.batch = p->batch;
   up.layout = p->layout; up.L = int(p->L); up.s = int(p->s); up.k = p->kup; up.gr = p->grup; up.G = p->group;
   up.T = p->d_T; up.B = p->d_B; up.w = w; up.cnt = cnt; up.flags = flags; up.w_tile = p->w_tile_doubles;
-  up.cnt_tile = p->cnt_tile_ints;
+  up.cnt_tile = p->cnt_tile_ints; up.ntiles = p->ntiles;
   StreamParams sp{};
   sp.A = p->d_A; sp.w = w; sp.c = c; sp.in = in; sp.out = out; sp.tabA = p->d_tabA; sp.tabB = p->d_tabB;
   sp.flags = flags; sp.w_tile = p->w_tile_doubles; sp.ld_in = p->ld_in; sp.ld_out = p->ld_out; sp.n = p->n;
@@ -1145,7 +1195,7 @@ lc_status launch_execute(const lc_plan* p, const double* in, double* out, void* 
     return LC_ERR_INVALID_ARG;
   }
   const dim3 grid(unsigned(nsub), unsigned(p->ntiles));
-  const dim3 grid_up(unsigned(p->L > 0 ? (int64_t(4) << p->grup) : 1), unsigned(p->ntiles));
+  const dim3 grid_up(unsigned(p->L > 0 ? std::min<int64_t>((int64_t(4) << p->grup) * p->ntiles, p->sm_count) : 1), 1);
   cudaError_t e;
   const int key = p->vt * 2 + p->dir;
   switch (key) {

@@ -69,7 +69,7 @@ __host__ __device__ inline DownSmem down_smem_layout(int VT, int k, int s, int g
   int64_t o = 0;
   const int64_t node = int64_t(2) * VT * kM * 8;  // one segment, both parities, VT vectors
   const int64_t nleaf = int64_t(1) << k;
-  L.Tt = o;    o = align_up(o + int64_t(2) * kM * s * 8, 128);
+  L.Tt = o;    o = align_up(o + int64_t(2) * kM * s * 8 + 8 * 8, 128);  // + padding read by blocked step 5
   L.zb = o;    o = align_up(o + int64_t(VT) * nleaf * 2 * s * 8, 128);
   L.cm = o;    o = align_up(o + down_cm_nodes(k, gr) * node, 128);
   L.total = o;
@@ -104,6 +104,7 @@ __host__ __device__ inline int64_t up_smem_bytes(int VT, int k, int s) {
   int64_t o = 0;
   o = align_up(o + int64_t(2) * s * kM * 8, 128);                 // T [2][s][M]
   o = align_up(o + int64_t(VT) * (int64_t(1) << k) * 2 * s * 8, 128);  // f tile
+  o = align_up(o + int64_t(VT) * (int64_t(1) << k) * 2 * s * 8, 128);  // f tile (prefetch buffer)
   o = align_up(o + ((int64_t(2) << k) - 1) * 2 * VT * kM * 8, 128);    // w tree
   o += 16;
   return o;

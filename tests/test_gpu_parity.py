@@ -131,3 +131,21 @@ def test_plan_tables_pinned():
     refb = oracle.lam(big.size)
     idx = np.r_[0:1000, np.arange(1000, big.size, 997)]
     assert np.max(np.abs(big[idx] - refb[idx]) / refb[idx]) < 1e-15
+
+
+@pytest.mark.parametrize("direction", ["leg2cheb", "cheb2leg"])
+def test_back_to_back_same_plan_different_inputs(direction):
+    # executions of one plan enqueued back to back (no host sync) must not observe each other's
+    # readiness flags or work arrays
+    dev = _dev()
+    n = 300000
+    p = _plan(n, direction, device=dev)
+    xs = [torch.from_numpy(vector("uniform_r0.5", n, seed=sd)).reshape(1, -1).to(dev) for sd in (21, 22, 23)]
+    outs = [p.execute(x) for x in xs for _ in range(2)]
+    torch.cuda.synchronize()
+    rows = np.r_[0:200, np.linspace(200, n - 1, 300).astype(np.int64)]
+    for q, x in enumerate(xs):
+        ref = _ref(direction, x.cpu().numpy()[0], rows)
+        for rep in range(2):
+            z = outs[2 * q + rep].cpu().numpy()[0][rows]
+            assert oracle.einf(z, ref) <= GATE, (q, rep)
