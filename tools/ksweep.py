@@ -1,6 +1,17 @@
 """Sweep execution-kernel configurations for one workload; per-kernel CUDA-event times (no graph)."""
 import itertools, json, sys
 import torch
+
+
+def gpu_warmup(seconds=1.0):
+    """Run dense work for `seconds` so the SM clock ramps up from idle before timing."""
+    import time
+    a = torch.randn(4096, 4096, device="cuda")
+    t = time.time()
+    while time.time() - t < seconds:
+        a = a @ a
+        a /= a.norm()
+    torch.cuda.synchronize()
 sys.path.insert(0, '.')
 from lc_inputs import vector
 from paper_2411_00033_b200 import Plan
@@ -12,7 +23,7 @@ def run(n, d, V=1, reps=30, **opts):
     p = Plan(n, d, batch=V, device=dev, **opts)
     kpe = p.kernels_per_execute
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(kpe + 1)]
-    for _ in range(3):
+    for _ in range(200):
         p.execute(x, y)
     acc = [0.0] * kpe
     for _ in range(reps):
@@ -33,8 +44,9 @@ def run(n, d, V=1, reps=30, **opts):
     p.close()
 
 if __name__ == "__main__":
+    gpu_warmup(1.5)
     n = int(sys.argv[1]) if len(sys.argv) > 1 else 1000000
-    for kup in (3, 4, 5, 6, 7):
+    for kup in (3, 4, 5, 6):
         run(n, "leg2cheb", up_subtree=kup)
     for k in (2, 3, 4, 5):
         run(n, "leg2cheb", subtree=k)

@@ -2,6 +2,17 @@
 import ctypes, sys
 import numpy as np
 import torch
+
+
+def gpu_warmup(seconds=1.0):
+    """Run dense work for `seconds` so the SM clock ramps up from idle before timing."""
+    import time
+    a = torch.randn(4096, 4096, device="cuda")
+    t = time.time()
+    while time.time() - t < seconds:
+        a = a @ a
+        a /= a.norm()
+    torch.cuda.synchronize()
 sys.path.insert(0, '.')
 from paper_2411_00033_b200 import _lib
 _lib.LIB_PATH = _lib.LIB_PATH.replace("liblegcheb.so", "liblegcheb_dbg.so")
@@ -17,7 +28,8 @@ x = torch.from_numpy(vector("sign_over_j1", n, 0, 0)).reshape(1, -1).to(dev)
 p = Plan(n, d, device=dev, **opts)
 lib = _lib.load()
 lib.lc_debug_timestamps.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_ulonglong), ctypes.c_longlong]
-for _ in range(3):
+gpu_warmup(1.5)
+for _ in range(200):
     y = p.execute(x)
 torch.cuda.synchronize()
 # clear, run once
@@ -28,13 +40,19 @@ zero = np.zeros(1 << 20, dtype=np.uint64)
 y = p.execute(x)
 torch.cuda.synchronize()
 t0 = None
-for kern, name in enumerate(["up", "m2l", "down"]):
+for kern, name in enumerate(["up", "fmm", "down"]):
     lib.lc_debug_timestamps(kern, buf.ctypes.data_as(ctypes.POINTER(ctypes.c_ulonglong)), buf.size)
     a = buf.reshape(-1, 8).astype(np.int64).copy()
     a = a[a[:, 0] > 0]
-    ts[name] = a
-t0 = min(ts[k][:, 0].min() for k in ts)
+    if len(a):
+        ts[name] = a
+t0 = min(ts[k][:, 0].min() for k in ts if k != "up")
 print("config", p.desc["vt"], p.desc["subtree"], p.desc["stage_blocks"], p.desc["stages"])
+if "up" in ts:  # up-role task 0: slots 0 (input ready) 1 (step 1) 2 (merges) 3 (writes) 4 (fence)
+    a = ts.pop("up")
+    d = np.diff(a[:, :5], axis=1) / 1e3
+    print("up task0 phase durations med (us): step1 %.2f merges %.2f write %.2f fence %.2f; input ready at %.2f us"
+          % tuple(list(np.median(d, axis=0)) + [np.median((a[:, 0] - t0) / 1e3)]))
 for name, a in ts.items():
     start = (a[:, 0] - t0) / 1e3
     print(f"{name}: CTAs {len(a)}  first start {start.min():.1f} us  last start {start.max():.1f} us")
