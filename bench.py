@@ -244,12 +244,16 @@ def run_gpu(args, world, rank, local):
                 per_kernel[d][i] += ev[i].elapsed_time(ev[i + 1]) / ksteps
     hbm, hbm_src = peaks()
     dl = pl.desc
-    names = ["lc_fmm_kernel", "lc_down_kernel"]
+    names = (["lc_up_kernel"] if kpe == 3 else []) + ["lc_stream_kernel", "lc_down_kernel"]
     # algorithmic bytes per launch (f in, z out, A_hat once, lambda once; work arrays excluded):
-    # the fused kernel reads A_hat, f and lambda; the down kernel writes z
-    alg = {"lc_fmm_kernel": 8.0 * 324 * dl["nc"] + 8.0 * n * V + 8.0 * dl["N"], "lc_down_kernel": 8.0 * n * V}
+    # the up kernel reads f, the streaming kernel reads A_hat and lambda (and f again for the band),
+    # the down kernel writes z
+    alg = {"lc_up_kernel": 8.0 * n * V, "lc_stream_kernel": 8.0 * 324 * dl["nc"] + 8.0 * dl["N"],
+           "lc_down_kernel": 8.0 * n * V}
+    if kpe == 2:
+        alg["lc_stream_kernel"] += 8.0 * n * V
     avg_ms = {nm: 0.5 * (per_kernel[0][i] + per_kernel[1][i]) for i, nm in enumerate(names)}
-    dom = "lc_fmm_kernel"  # the A_hat stream: the HBM-dominant kernel
+    dom = "lc_stream_kernel"  # the A_hat stream: the HBM-dominant kernel
     down_ms = avg_ms[dom]
     down_bytes = alg[dom]
     achieved = down_bytes / (down_ms * 1e-3) / 1e9

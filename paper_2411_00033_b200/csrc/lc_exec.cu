@@ -88,6 +88,10 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+// named barrier among the consumer warps of the streaming kernel (the producer warp does not join)
+__device__ __forceinline__ void consumer_sync(int nthreads) {
+  asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");  // barrier 1: the band warps
+}
 // release/acquire helpers for the readiness flags (gpu scope)
 __device__ __forceinline__ void st_release(int* p, int v) {
   asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
@@ -211,46 +215,31 @@ __device__ __forceinline__ double l2l_warp(const BCol& cb, const double* __restr
 // flags (workspace ints): [0] up main-phase arrivals, [1] fine levels of w ready,
 // [2] finished level-0 continuations, [3] coarse levels of w ready, [4] finished
 // streaming CTAs, [5] predecessor complete (input readable).  Self-resetting.
-// Work split of the fused kernel (one CTA per SM, persistent):
-//   warp 0            TMA producer (one lane): A_hat chunks + w windows into the ring
-//   warps 1..4        M2L consumers (step 3)
-//   warps 5..16       compute role: the upward pass (steps 1-2) over subtree tasks, the
-//                     continuation arrivals, then the direct band (step 6) units
-constexpr int kM2lWarps = 4;
-constexpr int kCompWarps = 12;
-constexpr int kM2lBase = 32;
-constexpr int kCompBase = kM2lBase + 32 * kM2lWarps;
-constexpr int kFusedThreads = kCompBase + 32 * kCompWarps;
-constexpr int kBandThreads = 32 * kCompWarps;
-constexpr int kUpThreads = 32 * kCompWarps;
-
-__device__ __forceinline__ void band_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kBandThreads) : "memory"); }
-__device__ __forceinline__ void up_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kUpThreads) : "memory"); }
-
-// flags (workspace ints): [2] finished level-0 continuations, [3] coarse levels of w ready,
-// [4] finished CTAs; ready[t] = subtree task t written (fine levels).  Reset by the last CTA.
-struct FmmParams {
+struct UpParams {
   const double* in;
-  double* out;
-  int64_t ld_in, ld_out, n, N, batch, ntiles;
-  int layout, L, s;
-  int* flags;
-  int* ready;
-  int64_t w_tile;
-  // upward pass
+  int64_t ld_in, n, N, batch;
+  int layout, L, s, k, gr, G;
   const double* T;  // [2][s][M]
-  const double* B;  // B(0)
+  const double* B;  // B(0) [M][M]
   double* w;
   int* cnt;
-  int64_t cnt_tile;
-  int kup, grup, G;
-  // streaming
+  int* flags;
+  int64_t w_tile, cnt_tile;
+};
+
+struct StreamParams {
   const double* A;
+  const double* w;
   double* c;
+  const double* in;
+  double* out;
   const double* tabA;
   const double* tabB;
-  int64_t nm2l, nband;
-  int cb, nst, kb;
+  int* flags;
+  int64_t w_tile;  // doubles per vector tile (w and c share the layout)
+  int64_t ld_in, ld_out, n, N, batch;
+  int64_t ntiles, nm2l, nband;
+  int layout, L, s, cb, nst, kb, gr_up;
 };
 
 struct DownParams {
@@ -263,15 +252,15 @@ struct DownParams {
   int64_t w_tile;
 };
 
-// ============================================================== upward pass (role)
+// ============================================================== up kernel
 // one tree level in shared memory ([sigma][node][v][M]); item = (sigma, parent, v) handled by
-// one warp of the role (lane = output mode); nparent = 2^lp
+// one warp (lane = output mode); nparent = 2^lp
 template <int VT>
 __device__ __forceinline__ void m2m_level(const double* __restrict__ ch, double* __restrict__ pa, int lp,
-                                          const BRow& br, int rtid, int rthreads) {
+                                          const BRow& br) {
   const int nparent = 1 << lp;
   const int items = 2 * nparent * VT;
-  const int lane = rtid & 31, warp = rtid >> 5, nwarps = rthreads >> 5;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   for (int it = warp; it < items; it += nwarps) {
     const int v = it % VT;
     const int sp = it / VT;
@@ -284,8 +273,33 @@ __device__ __forceinline__ void m2m_level(const double* __restrict__ ch, double*
 }
 
 template <int VT>
-__device__ __forceinline__ void up_stage_input(const FmmParams& P, double* fs, int64_t R, int64_t tile, int tlen,
-                                               int utid) {
+__global__ void __launch_bounds__(kThreads, 2) lc_up_kernel(const UpParams P) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ int s_last;
+  const int s = P.s, k = P.k;
+  const int tid = threadIdx.x;
+  double* Ts = reinterpret_cast<double*>(smem);
+  double* fs = reinterpret_cast<double*>(smem + align_up(int64_t(2) * s * kM * 8, 128));
+  const int nleaf = 1 << k;
+  const int seglen = 2 * s;
+  const int tlen = nleaf * seglen;
+  double* tree = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(fs) + align_up(int64_t(VT) * tlen * 8, 128));
+  auto tree_off = [&](int j) { return ((1 << j) - 1) * 2 * VT * kM; };
+
+  const int64_t R = blockIdx.x;
+  const int64_t tile = blockIdx.y;
+  LC_TS(0, 0);
+  BRow br;
+  load_brow(br, P.B, tid & 31);
+  for (int i = tid; i < s * kM; i += blockDim.x) cp_async16(Ts + 2 * i, P.T + 2 * i);
+  cp_async_commit();
+  griddep_wait();  // the input may be produced by the preceding kernel
+  // Trigger the dependent (streaming) launch only now: every streaming CTA then starts after the
+  // whole previous execution completed, so it can never observe flags of that execution.
+  griddep_launch();
+  if (tid == 0) st_release(&P.flags[5], 1);  // predecessor complete: the streaming kernel may read the input
+
+  // stage the leaf range [R 2^k, (R+1) 2^k) of segments, zero padding beyond n
   const int64_t j0 = R * tlen;
   if (P.layout == LC_VEC_CONTIGUOUS) {
 #pragma unroll 1
@@ -293,13 +307,13 @@ __device__ __forceinline__ void up_stage_input(const FmmParams& P, double* fs, i
       const int64_t gv = tile * VT + v;
       const double* src = P.in + gv * P.ld_in + j0;
       const int64_t lim = gv < P.batch ? P.n - j0 : 0;  // valid elements of this vector in the tile
-      for (int jj = utid; jj < tlen; jj += kUpThreads) {
+      for (int jj = tid; jj < tlen; jj += blockDim.x) {
         const bool ok = jj < lim;
         cp_async8(fs + v * tlen + jj, ok ? src + jj : P.in, ok ? 8u : 0u);
       }
     }
   } else {
-    for (int idx = utid; idx < VT * tlen; idx += kUpThreads) {
+    for (int idx = tid; idx < VT * tlen; idx += blockDim.x) {
       const int jj = idx / VT, v = idx - jj * VT;  // v fastest: coalesced in the batch layout
       const int64_t gv = tile * VT + v, j = j0 + jj;
       const bool ok = gv < P.batch && j < P.n;
@@ -307,180 +321,138 @@ __device__ __forceinline__ void up_stage_input(const FmmParams& P, double* fs, i
     }
   }
   cp_async_commit();
-}
+  cp_async_wait<0>();
+  __syncthreads();
+  LC_TS(0, 1);
 
-// Steps 1 (eq:wMM) and 2 (eq:wtk, Alg. a.1) over the subtree tasks t = blockIdx.x + i gridDim.x
-// (subtree R = t mod nsub of 2^kup leaf segments, vector tile t / nsub); the next task's input is
-// prefetched while the current one is processed.  Each task raises ready[t] once its w(g >= grup)
-// are written; the last arriver of each group of 2^G subtree roots continues upwards (coarse w).
-template <int VT>
-__device__ __forceinline__ void up_role(const FmmParams& P, unsigned char* usm, int utid, int* s_last) {
-  const int s = P.s, k = P.kup;
-  const int nleaf = 1 << k;
-  const int seglen = 2 * s;
-  const int tlen = nleaf * seglen;
-  double* Ts = reinterpret_cast<double*>(usm);
-  double* fbuf[2];
-  fbuf[0] = reinterpret_cast<double*>(usm + align_up(int64_t(2) * s * kM * 8, 128));
-  fbuf[1] = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(fbuf[0]) + align_up(int64_t(VT) * tlen * 8, 128));
-  double* tree = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(fbuf[1]) + align_up(int64_t(VT) * tlen * 8, 128));
-  auto tree_off = [&](int j) { return ((1 << j) - 1) * 2 * VT * kM; };
-  const int64_t nsub = int64_t(4) << P.grup;
-  const int64_t ntasks = nsub * P.ntiles;
-  const int64_t VM = int64_t(VT) * kM;
-  BRow br;
-  load_brow(br, P.B, utid & 31);
-  for (int i = utid; i < s * kM; i += kUpThreads) cp_async16(Ts + 2 * i, P.T + 2 * i);
-  cp_async_commit();
-
-  int64_t t = blockIdx.x;
-  if (t < ntasks) up_stage_input<VT>(P, fbuf[0], t % nsub, t / nsub, tlen, utid);
-  int buf = 0;
-  for (; t < ntasks; t += gridDim.x, buf ^= 1) {
-    const int64_t R = t % nsub, tile = t / nsub;
-    const int64_t tn = t + gridDim.x;
-    if (tn < ntasks) {
-      up_stage_input<VT>(P, fbuf[buf ^ 1], tn % nsub, tn / nsub, tlen, utid);  // prefetch the next task
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
-    up_sync();
-#ifdef LC_PHASE_TIMING
-    if (utid == 0 && t == blockIdx.x) { lc_ts_any(0, 0); }
-#endif
-    const double* fs = fbuf[buf];
-    // step 1: w(L-1)[t][k] = sum_m f[2s t + 2m + sigma] T(sigma)[m][k]   (eq:wMM)
-    // item = (v, seg, sigma, group of 6 modes); 3 lanes share each f value.
-    {
-      double* leaf = tree + tree_off(k);
-      const int items = nleaf * 2 * VT * 3;
-      for (int it = utid; it < items; it += kUpThreads) {
-        const int kg = it % 3;
-        int r = it / 3;
-        const int sg = r & 1;
-        r >>= 1;
-        const int seg = r & (nleaf - 1);
-        const int v = r >> k;
-        const double* fp = fs + v * tlen + seg * seglen + sg;
-        const double* tp = Ts + sg * s * kM + 6 * kg;
-        double a0 = 0, a1 = 0, a2 = 0, a3 = 0, a4 = 0, a5 = 0;
+  // step 1: w(L-1)[t][k] = sum_m f[2s t + 2m + sigma] T(sigma)[m][k]   (eq:wMM)
+  // item = (v, seg, sigma, group of 6 modes); 3 lanes share each f value.
+  {
+    double* leaf = tree + tree_off(k);
+    const int items = nleaf * 2 * VT * 3;
+    for (int it = tid; it < items; it += blockDim.x) {
+      const int kg = it % 3;
+      int r = it / 3;
+      const int sg = r & 1;
+      r >>= 1;
+      const int seg = r & (nleaf - 1);
+      const int v = r >> k;
+      const double* fp = fs + v * tlen + seg * seglen + sg;
+      const double* tp = Ts + sg * s * kM + 6 * kg;
+      double a0 = 0, a1 = 0, a2 = 0, a3 = 0, a4 = 0, a5 = 0;
 #pragma unroll 4
-        for (int m = 0; m < s; ++m) {
-          const double f = fp[2 * m];
-          const double2 t01 = *reinterpret_cast<const double2*>(tp + m * kM);
-          const double2 t23 = *reinterpret_cast<const double2*>(tp + m * kM + 2);
-          const double2 t45 = *reinterpret_cast<const double2*>(tp + m * kM + 4);
-          a0 = fma(f, t01.x, a0); a1 = fma(f, t01.y, a1);
-          a2 = fma(f, t23.x, a2); a3 = fma(f, t23.y, a3);
-          a4 = fma(f, t45.x, a4); a5 = fma(f, t45.y, a5);
-        }
-        double* o = leaf + ((sg * nleaf + seg) * VT + v) * kM + 6 * kg;
-        *reinterpret_cast<double2*>(o) = make_double2(a0, a1);
-        *reinterpret_cast<double2*>(o + 2) = make_double2(a2, a3);
-        *reinterpret_cast<double2*>(o + 4) = make_double2(a4, a5);
+      for (int m = 0; m < s; ++m) {
+        const double f = fp[2 * m];
+        const double2 t01 = *reinterpret_cast<const double2*>(tp + m * kM);
+        const double2 t23 = *reinterpret_cast<const double2*>(tp + m * kM + 2);
+        const double2 t45 = *reinterpret_cast<const double2*>(tp + m * kM + 4);
+        a0 = fma(f, t01.x, a0); a1 = fma(f, t01.y, a1);
+        a2 = fma(f, t23.x, a2); a3 = fma(f, t23.y, a3);
+        a4 = fma(f, t45.x, a4); a5 = fma(f, t45.y, a5);
       }
+      double* o = leaf + ((sg * nleaf + seg) * VT + v) * kM + 6 * kg;
+      *reinterpret_cast<double2*>(o) = make_double2(a0, a1);
+      *reinterpret_cast<double2*>(o + 2) = make_double2(a2, a3);
+      *reinterpret_cast<double2*>(o + 4) = make_double2(a4, a5);
     }
-    up_sync();
-#ifdef LC_PHASE_TIMING
-    if (utid == 0 && t == blockIdx.x) { lc_ts_any(0, 1); }
-#endif
-    // step 2 inside the subtree
-    for (int j = k; j >= 1; --j) {
-      m2m_level<VT>(tree + tree_off(j), tree + tree_off(j - 1), j - 1, br, utid, kUpThreads);
-      up_sync();
+  }
+  __syncthreads();
+  LC_TS(0, 2);
+  // step 2 inside the subtree
+  for (int j = k; j >= 1; --j) {
+    m2m_level<VT>(tree + tree_off(j), tree + tree_off(j - 1), j - 1, br);
+    __syncthreads();
+  }
+  LC_TS(0, 3);
+  double* wt = P.w + tile * P.w_tile;
+  const int64_t VM = int64_t(VT) * kM;
+  for (int j = 0; j <= k; ++j) {
+    const int g = P.gr + j;
+    const int cnt2 = int((int64_t(1) << j) * VM / 2);
+    for (int sg = 0; sg < 2; ++sg) {
+      double2* dst = reinterpret_cast<double2*>(wt + (w_level_offset_units(g) + sg * nseg(g) + (R << j)) * VM);
+      const double2* src = reinterpret_cast<const double2*>(tree + tree_off(j) + sg * (int64_t(1) << j) * VM);
+      for (int i = tid; i < cnt2; i += blockDim.x) dst[i] = src[i];
     }
-#ifdef LC_PHASE_TIMING
-    if (utid == 0 && t == blockIdx.x) { lc_ts_any(0, 2); }
-#endif
-    double* wt = P.w + tile * P.w_tile;
-    for (int j = 0; j <= k; ++j) {
-      const int g = P.grup + j;
-      const int cnt2 = int((int64_t(1) << j) * VM / 2);
-      for (int sg = 0; sg < 2; ++sg) {
-        double2* dst = reinterpret_cast<double2*>(wt + (w_level_offset_units(g) + sg * nseg(g) + (R << j)) * VM);
-        const double2* src = reinterpret_cast<const double2*>(tree + tree_off(j) + sg * (int64_t(1) << j) * VM);
-        for (int i = utid; i < cnt2; i += kUpThreads) dst[i] = src[i];
-      }
+  }
+  // the fine levels (gr..L-1) of the whole batch are ready once every CTA got here
+  __threadfence();
+  __syncthreads();
+  LC_TS(0, 4);
+  if (tid == 0) {
+    const int total = int(gridDim.x * gridDim.y);
+    if (atomicAdd(&P.flags[0], 1) == total - 1) {
+      atomicExch(&P.flags[0], 0);
+      __threadfence();
+      st_release(&P.flags[1], 1);
+      if (P.gr == 0) st_release(&P.flags[3], 1);
     }
-#ifdef LC_PHASE_TIMING
-    if (utid == 0 && t == blockIdx.x) { lc_ts_any(0, 3); }
-#endif
-    __threadfence();
-    up_sync();  // also: the tree is rebuilt by the next task
-#ifdef LC_PHASE_TIMING
-    if (utid == 0 && t == blockIdx.x) { lc_ts_any(0, 4); }
-#endif
-    if (utid == 0) st_release(&P.ready[t], 1);  // fine levels of subtree R ready for the M2L stream
   }
 
-#ifdef LC_PHASE_TIMING
-  if (utid == 0) lc_ts_any(1, 4);
-#endif
-  // upward continuation above the subtree roots: for each task of this CTA, the last arriver of
-  // each group of 2^G nodes merges them G levels up (threadfence-reduction pattern).
-  for (int64_t t0 = blockIdx.x; t0 < ntasks; t0 += gridDim.x) {
-    const int64_t tile = t0 / nsub;
-    double* wt = P.w + tile * P.w_tile;
-    int g = P.grup;
-    int64_t node = t0 % nsub;
-    while (g > 0) {
-      const int ge = min(P.G, g);
-      const int64_t grp = node >> ge;
-      up_sync();
-      if (utid == 0) {
-        int* c = P.cnt + tile * P.cnt_tile + (nseg(g) - 4) + grp;
-        const int old = atomicAdd(c, 1);
-        const int last = (old == (1 << ge) - 1);
-        if (last) atomicExch(c, 0);  // self-reset for the next launch
-        *s_last = last;
-      }
-      up_sync();
-      if (!*s_last) break;
-      __threadfence();
-      const int cnt2 = int((int64_t(1) << ge) * VM / 2);
+  // upward continuation above the subtree roots: the last arriver of each
+  // group of 2^G nodes merges them G levels up (threadfence-reduction pattern).
+  int g = P.gr;
+  int64_t node = R;
+  while (g > 0) {
+    const int ge = min(P.G, g);
+    const int64_t grp = node >> ge;
+    __syncthreads();
+    if (tid == 0) {
+      int* c = P.cnt + tile * P.cnt_tile + (nseg(g) - 4) + grp;
+      const int old = atomicAdd(c, 1);
+      const int last = (old == (1 << ge) - 1);
+      if (last) atomicExch(c, 0);  // self-reset for the next launch
+      s_last = last;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    LC_TS(0, 5);
+    __threadfence();
+    const int cnt2 = int((int64_t(1) << ge) * VM / 2);
+    for (int sg = 0; sg < 2; ++sg) {
+      const double2* src =
+          reinterpret_cast<const double2*>(wt + (w_level_offset_units(g) + sg * nseg(g) + (grp << ge)) * VM);
+      double2* dst = reinterpret_cast<double2*>(tree + tree_off(ge) + sg * 2 * cnt2);
+      for (int i = tid; i < cnt2; i += blockDim.x) dst[i] = __ldcg(src + i);
+    }
+    __syncthreads();
+    for (int j = ge; j >= 1; --j) {
+      m2m_level<VT>(tree + tree_off(j), tree + tree_off(j - 1), j - 1, br);
+      __syncthreads();
+    }
+    for (int j = 0; j < ge; ++j) {
+      const int gg = g - ge + j;
+      const int cj2 = int((int64_t(1) << j) * VM / 2);
       for (int sg = 0; sg < 2; ++sg) {
-        const double2* src =
-            reinterpret_cast<const double2*>(wt + (w_level_offset_units(g) + sg * nseg(g) + (grp << ge)) * VM);
-        double2* dst = reinterpret_cast<double2*>(tree + tree_off(ge) + sg * 2 * cnt2);
-        for (int i = utid; i < cnt2; i += kUpThreads) dst[i] = __ldcg(src + i);
+        double2* dst = reinterpret_cast<double2*>(wt + (w_level_offset_units(gg) + sg * nseg(gg) + (grp << j)) * VM);
+        const double2* src = reinterpret_cast<const double2*>(tree + tree_off(j) + sg * 2 * cj2);
+        for (int i = tid; i < cj2; i += blockDim.x) dst[i] = src[i];
       }
-      up_sync();
-      for (int j = ge; j >= 1; --j) {
-        m2m_level<VT>(tree + tree_off(j), tree + tree_off(j - 1), j - 1, br, utid, kUpThreads);
-        up_sync();
-      }
-      for (int j = 0; j < ge; ++j) {
-        const int gg = g - ge + j;
-        const int cj2 = int((int64_t(1) << j) * VM / 2);
-        for (int sg = 0; sg < 2; ++sg) {
-          double2* dst = reinterpret_cast<double2*>(wt + (w_level_offset_units(gg) + sg * nseg(gg) + (grp << j)) * VM);
-          const double2* src = reinterpret_cast<const double2*>(tree + tree_off(j) + sg * 2 * cj2);
-          for (int i = utid; i < cj2; i += kUpThreads) dst[i] = src[i];
-        }
-      }
-      __threadfence();
-      g -= ge;
-      node = grp;
-#ifdef LC_PHASE_TIMING
-      if (utid == 0) lc_ts_any(1, 6);
-#endif
-      if (g == 0) {  // this CTA produced one of the 4 level-0 nodes of the vector tile
-        up_sync();
-        if (utid == 0) {
-          const int total = 4 * int(P.ntiles);
-          if (atomicAdd(&P.flags[2], 1) == total - 1) {
-            atomicExch(&P.flags[2], 0);
-            __threadfence();
-            st_release(&P.flags[3], 1);
-          }
-        }
+    }
+    __threadfence();
+    g -= ge;
+    node = grp;
+    LC_TS(0, 6);
+  }
+  if (P.gr > 0) {  // this CTA produced one of the 4 level-0 nodes of its vector tile
+    __syncthreads();
+    if (tid == 0) {
+      const int total = 4 * int(gridDim.y);
+      if (atomicAdd(&P.flags[2], 1) == total - 1) {
+        atomicExch(&P.flags[2], 0);
+        __threadfence();
+        st_release(&P.flags[3], 1);
       }
     }
   }
 }
 
-// ============================================================== M2L unit decoding
+// ============================================================== streaming kernel
+constexpr int kM2lWarps = 4;   // consumer warps applying M2L to the A_hat ring
+constexpr int kBandWarps = 4;  // consumer warps computing the direct band (independent pipeline)
+constexpr int kStreamThreads = 32 * (1 + kM2lWarps + kBandWarps);
+constexpr int kBandThreads = 32 * kBandWarps;
+
 // M2L unit q (< nm2l) = (chunk, tile): chunk = (level g, blocks [b0, b0+nb)), nb <= cb, the
 // finest level first; tiles innermost so concurrent CTAs share A_hat in L2.
 // cstart[o] = first chunk of level L-1-o (shared-memory table, 32-bit arithmetic only).
@@ -500,14 +472,12 @@ __device__ __forceinline__ void m2l_unit(int q, int ntiles, int L, int cb, const
   nb = (bg - b0) < cb ? (bg - b0) : cb;
 }
 
-// ============================================================== fused kernel
-// Streaming units of the CTA: u = blockIdx.x + i * gridDim.x over [0, nband + nm2l); units below
+// Work units of the CTA: u = blockIdx.x + i * gridDim.x over [0, nband + nm2l); units below
 // nband are band units (leaf range of 2^kb segments x vector tile), the rest M2L units.
 template <int VT, int DIR>
-__global__ void __launch_bounds__(kFusedThreads, 1) lc_fmm_kernel(const FmmParams P) {
+__global__ void __launch_bounds__(kStreamThreads, 2) lc_stream_kernel(const StreamParams P) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ int cstart[32];
-  __shared__ int s_last;
   const int tid = threadIdx.x;
   const int s = P.s, cb = P.cb, nst = P.nst, kb = P.kb;
   const int64_t VM = int64_t(VT) * kM;
@@ -519,9 +489,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) lc_fmm_kernel(const FmmParam
   double* tb = reinterpret_cast<double*>(smem + SL.tb);
   double* gt = reinterpret_cast<double*>(smem + SL.gt);
   double* zst = reinterpret_cast<double*>(smem + SL.zst);
-  unsigned char* usm = smem + SL.total;  // upward-pass region
   const int tp = int(SL.tp);
-  const int64_t nsub = P.L > 0 ? (int64_t(4) << P.grup) : 0;
 
   const int nband = int(P.nband), nm2l = int(P.nm2l);
   const int nunits = nband + nm2l;
@@ -542,12 +510,13 @@ __global__ void __launch_bounds__(kFusedThreads, 1) lc_fmm_kernel(const FmmParam
   __syncthreads();
   const int ntiles = int(P.ntiles);
   LC_TS(1, 0);
+  griddep_launch();
 
-  if (tid < kM2lBase) {
+  if (tid < 32) {
     // ------------------------------------------------ producer warp: the A_hat / w stream
     if (tid == 0) {
       const uint64_t pol = policy_evict_first();
-      bool coarse_ok = false;
+      bool fine_ok = false, coarse_ok = false;
       auto issue = [&](int q, int j, bool with_a, bool with_w) {  // M2L unit q, ring use j
         int g, nb, b0, tile;
         m2l_unit(q, ntiles, P.L, cb, cstart, g, b0, nb, tile);
@@ -561,18 +530,14 @@ __global__ void __launch_bounds__(kFusedThreads, 1) lc_fmm_kernel(const FmmParam
           bulk_g2s(base, P.A + (ahat_level_offset(g) + 3 * int64_t(b0)) * kMM, abytes, &full[slot], pol);
         }
         if (with_w) {
-          // w of level g: fine levels once the subtree tasks holding columns [2b0+2, 2b0+2nb+2)
-          // are written, coarse levels after the continuation (release/acquire flags)
-          if (g >= P.grup) {
-            const int sh = g - P.grup;
-            const int64_t r0 = (2 * int64_t(b0) + 2) >> sh, r1 = (2 * int64_t(b0) + 2 * nb + 1) >> sh;
-            for (int64_t r = r0; r <= r1; ++r) wait_flag(&P.ready[int64_t(tile) * nsub + r]);
-          } else if (!coarse_ok) {
-            wait_flag(&P.flags[3]);
-            LC_TS(1, 5);
-            coarse_ok = true;
+          // w of level g: fine levels after the up kernel's main phase, coarse ones after its continuation
+          bool& ok = g >= P.gr_up ? fine_ok : coarse_ok;
+          if (!ok) {
+            wait_flag(&P.flags[g >= P.gr_up ? 1 : 3]);
+            LC_TS(1, g >= P.gr_up ? 4 : 5);
+            asm volatile("fence.proxy.async.global;" ::: "memory");  // order the bulk reads after the acquire
+            ok = true;
           }
-          asm volatile("fence.proxy.async.global;" ::: "memory");  // order the bulk reads after the acquire
           double* wwin = reinterpret_cast<double*>(base + a_bytes);
           const double* wt = P.w + int64_t(tile) * P.w_tile;
           for (int sg = 0; sg < 2; ++sg)
@@ -580,7 +545,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) lc_fmm_kernel(const FmmParam
                      wbytes, &full[slot], pol);
         }
       };
-      // the A_hat of the first nst M2L units is plan data: issue it before the dependency wait
+      // the A_hat of the first nst M2L units is plan data: issue it before any dependency
       int j = 0;
       int firstq[8];
       for (int i = 0; i < nmine && j < nst && j < 8; ++i) {
@@ -590,7 +555,6 @@ __global__ void __launch_bounds__(kFusedThreads, 1) lc_fmm_kernel(const FmmParam
         issue(firstq[j], j, true, false);
         ++j;
       }
-      griddep_wait();
       const int npre = j;
       for (int jj = 0; jj < npre; ++jj) issue(firstq[jj], jj, false, true);
       j = 0;
@@ -604,75 +568,76 @@ __global__ void __launch_bounds__(kFusedThreads, 1) lc_fmm_kernel(const FmmParam
         ++j;
       }
     }
-  } else if (tid < kCompBase) {
+  } else if (tid < 32 * (1 + kM2lWarps)) {
     // ------------------------------------------------ M2L consumer warps
-    const int ctid = tid - kM2lBase;
+    const int ctid = tid - 32;
     int j = 0;  // M2L ring use counter
     for (int i = 0; i < nmine; ++i) {
       const int u = int(blockIdx.x) + i * int(gridDim.x);
       if (u < nband) continue;
-      int g, nb, b0, tile;
-      m2l_unit(u - nband, ntiles, P.L, cb, cstart, g, b0, nb, tile);
-      const int slot = j % nst;
+      {
+        // ---------------- M2L unit: step 3 on a chunk of blocks of one level
+          int g, nb, b0, tile;
+          m2l_unit(u - nband, ntiles, P.L, cb, cstart, g, b0, nb, tile);
+          const int slot = j % nst;
 #ifdef LC_PHASE_TIMING
-      if (j == 0 && ctid == 0) lc_ts_any(1, 2);
+          if (j == 0 && ctid == 0) lc_ts_any(1, 2);
 #endif
-      mbar_wait(&full[slot], uint32_t((j / nst) & 1));
+          mbar_wait(&full[slot], uint32_t((j / nst) & 1));
 #ifdef LC_PHASE_TIMING
-      if (j == 0 && ctid == 0) lc_ts_any(1, 3);
+          if (j == 0 && ctid == 0) lc_ts_any(1, 3);
 #endif
-      const double* As = reinterpret_cast<const double*>(smem + SL.ring + slot * SL.slot);
-      const double* wwin = reinterpret_cast<const double*>(smem + SL.ring + slot * SL.slot + a_bytes);
-      double* ct = P.c + int64_t(tile) * P.w_tile + (w_level_offset_units(g) + 2 * int64_t(b0)) * VM;
-      const int64_t sgstride = nseg(g) * VM;
-      const int nrows = 2 * nb;
-      for (int it = ctid; it < nrows * kM; it += 32 * kM2lWarps) {
-        const int ri = it / kM, kk = it % kM;  // row u = 2 b0 + ri
-        double acc[2][VT];
+          const double* As = reinterpret_cast<const double*>(smem + SL.ring + slot * SL.slot);
+          const double* wwin = reinterpret_cast<const double*>(smem + SL.ring + slot * SL.slot + a_bytes);
+          double* ct = P.c + int64_t(tile) * P.w_tile + (w_level_offset_units(g) + 2 * int64_t(b0)) * VM;
+          const int64_t sgstride = nseg(g) * VM;
+          const int nrows = 2 * nb;
+          for (int it = ctid; it < nrows * kM; it += 32 * kM2lWarps) {
+            const int ri = it / kM, kk = it % kM;  // row u = 2 b0 + ri
+            double acc[2][VT];
 #pragma unroll
-        for (int sg = 0; sg < 2; ++sg)
+            for (int sg = 0; sg < 2; ++sg)
 #pragma unroll
-          for (int v = 0; v < VT; ++v) acc[sg][v] = 0.0;
-        // even row (p=0): r=0 with column t=u+2 and r=1 with t=u+3; odd row (p=1): r=2 with t=u+2
-        const int nmat = (ri & 1) ? 1 : 2;
-        for (int mi = 0; mi < nmat; ++mi) {
-          const int r = (ri & 1) ? 2 : mi;
-          const int tloc = (ri & 1) ? ri : ri + mi;  // t - (2 b0 + 2)
-          const double* arow = As + (3 * (ri >> 1) + r) * kMM + kk * kM;
-          double ar[kM];
+              for (int v = 0; v < VT; ++v) acc[sg][v] = 0.0;
+            // even row (p=0): r=0 with column t=u+2 and r=1 with t=u+3; odd row (p=1): r=2 with t=u+2
+            const int nmat = (ri & 1) ? 1 : 2;
+            for (int mi = 0; mi < nmat; ++mi) {
+              const int r = (ri & 1) ? 2 : mi;
+              const int tloc = (ri & 1) ? ri : ri + mi;  // t - (2 b0 + 2)
+              const double* arow = As + (3 * (ri >> 1) + r) * kMM + kk * kM;
+              double ar[kM];
 #pragma unroll
-          for (int l = 0; l < kM; l += 2) {
-            const double2 t2 = *reinterpret_cast<const double2*>(arow + l);
-            ar[l] = t2.x;
-            ar[l + 1] = t2.y;
-          }
+              for (int l = 0; l < kM; l += 2) {
+                const double2 t2 = *reinterpret_cast<const double2*>(arow + l);
+                ar[l] = t2.x;
+                ar[l + 1] = t2.y;
+              }
 #pragma unroll
-          for (int sg = 0; sg < 2; ++sg)
+              for (int sg = 0; sg < 2; ++sg)
 #pragma unroll
-            for (int v = 0; v < VT; ++v) {
-              const double* wp = wwin + (sg * 2 * cb + tloc) * VM + v * kM;
-              double sacc = 0.0;
+                for (int v = 0; v < VT; ++v) {
+                  const double* wp = wwin + (sg * 2 * cb + tloc) * VM + v * kM;
+                  double sacc = 0.0;
 #pragma unroll
-              for (int l = 0; l < kM; ++l) sacc = fma(ar[l], wp[l], sacc);
-              acc[sg][v] += sacc;
+                  for (int l = 0; l < kM; ++l) sacc = fma(ar[l], wp[l], sacc);
+                  acc[sg][v] += sacc;
+                }
             }
-        }
 #pragma unroll
-        for (int sg = 0; sg < 2; ++sg)
+            for (int sg = 0; sg < 2; ++sg)
 #pragma unroll
-          for (int v = 0; v < VT; ++v) ct[sg * sgstride + ri * VM + v * kM + kk] = acc[sg][v];
+              for (int v = 0; v < VT; ++v) ct[sg * sgstride + ri * VM + v * kM + kk] = acc[sg][v];
+          }
+          __syncwarp();
+          if ((tid & 31) == 0) mbar_arrive(&empty[slot]);  // this warp is done with the slot
+        ++j;
       }
-      __syncwarp();
-      if ((tid & 31) == 0) mbar_arrive(&empty[slot]);  // this warp is done with the slot
-      ++j;
     }
   } else {
-    // ------------------------------------------------ compute warps
-    const int btid = tid - kCompBase;
+    // ------------------------------------------------ band consumer warps
+    const int btid = tid - 32 * (1 + kM2lWarps);
+    bool input_ok = false;
     for (int x = btid; x < 2 * s + 2 * kBandR; x += kBandThreads) ta[x] = x < 2 * s ? P.tabA[x] : 0.0;
-    griddep_wait();  // the input may be produced by the preceding kernel
-    if (P.L > 0) up_role<VT>(P, usm, btid, &s_last);
-    band_sync();
     for (int i = 0; i < nmine; ++i) {
       const int u = int(blockIdx.x) + i * int(gridDim.x);
       if (u >= nband) continue;
@@ -680,6 +645,15 @@ __global__ void __launch_bounds__(kFusedThreads, 1) lc_fmm_kernel(const FmmParam
         // ---------------- band unit: step 6 for rows of 2^kb leaf segments of one vector tile
         const int tile = ntiles > 1 ? u % ntiles : 0;
         const int lr = ntiles > 1 ? u / ntiles : u;
+        if (!input_ok) {  // the input is readable once the predecessor of the up kernel completed
+          if (P.L > 0) {
+            if (btid == 0) wait_flag(&P.flags[5]);
+          } else {
+            griddep_wait();
+          }
+          consumer_sync(kBandThreads);
+          input_ok = true;
+        }
         const int nleaf = 1 << kb;
         const int seglen = 2 * s;
         const int64_t U0 = int64_t(lr) << kb;
@@ -712,7 +686,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) lc_fmm_kernel(const FmmParam
         }
         cp_async_commit();
         cp_async_wait<0>();
-        band_sync();
+        consumer_sync(kBandThreads);
         // item = (v, segment uu, parity sigma, block of kBandR same-parity rows m = kBandR t + r).
         // Band of row i' = i + 2r (i the block's first row): sum_c a[c-r] b[i+r+c] g[i+2c], c >= r,
         // i + 2c < j_end; a = tabA, b = tabB, g = f (L2C) or j f_j (C2L).  Sliding windows of a and
@@ -783,7 +757,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) lc_fmm_kernel(const FmmParam
             }
           }
         }
-        band_sync();
+        consumer_sync(kBandThreads);
         // coalesced store of the band result (step 5 and step 7 are added by the down kernel)
         const int olim = int((P.n - i0) < rows ? (P.n - i0) : rows);
 #pragma unroll 1
@@ -797,26 +771,19 @@ __global__ void __launch_bounds__(kFusedThreads, 1) lc_fmm_kernel(const FmmParam
             for (int x = btid; x < olim; x += kBandThreads) P.out[(i0 + x) * P.ld_out + gv] = zst[v * rows + x];
           }
         }
-        band_sync();  // tiles are reused by the next band unit
+        consumer_sync(kBandThreads);  // tiles are reused by the next band unit
       }
     }
-#ifdef LC_PHASE_TIMING
-    if (btid == 0) lc_ts_any(1, 7);
-#endif
   }
-  griddep_launch();
   __syncthreads();
   LC_TS(1, 1);
   if (tid == 0) {  // the last CTA to finish re-arms the readiness flags for the next execution
-    s_last = (atomicAdd(&P.flags[4], 1) == int(gridDim.x) - 1);
-  }
-  __syncthreads();
-  if (s_last) {
-    const int64_t ntasks = nsub * P.ntiles;
-    for (int64_t t = tid; t < ntasks; t += blockDim.x) P.ready[t] = 0;
-    if (tid == 0) {
+    if (atomicAdd(&P.flags[4], 1) == int(gridDim.x) - 1) {
+      P.flags[1] = 0;
       P.flags[3] = 0;
-      P.flags[4] = 0;
+      P.flags[5] = 0;
+      __threadfence();
+      atomicExch(&P.flags[4], 0);
     }
   }
 }
@@ -1000,14 +967,25 @@ static cudaError_t set_max_dyn_smem(K kernel, int smax) {
 }
 template <int VT>
 static cudaError_t set_attrs_vt(int smax) {
-  cudaError_t e = set_max_dyn_smem(lc_fmm_kernel<VT, 0>, smax);
-  if (e == cudaSuccess) e = set_max_dyn_smem(lc_fmm_kernel<VT, 1>, smax);
+  cudaError_t e = set_max_dyn_smem(lc_up_kernel<VT>, smax);
+  if (e == cudaSuccess) e = set_max_dyn_smem(lc_stream_kernel<VT, 0>, smax);
+  if (e == cudaSuccess) e = set_max_dyn_smem(lc_stream_kernel<VT, 1>, smax);
   if (e == cudaSuccess) e = set_max_dyn_smem(lc_down_kernel<VT, 0>, smax);
   if (e == cudaSuccess) e = set_max_dyn_smem(lc_down_kernel<VT, 1>, smax);
   return e;
 }
 
 static bool g_device_ready[64] = {false};
+
+template <int VT>
+static int stream_occupancy(int dir, size_t smem) {
+  int occ = 0;
+  if (dir == 0)
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, lc_stream_kernel<VT, 0>, kStreamThreads, smem);
+  else
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, lc_stream_kernel<VT, 1>, kStreamThreads, smem);
+  return occ;
+}
 
 lc_status configure_kernels(lc_plan* p) {
   int smax = 0;
@@ -1019,19 +997,25 @@ lc_status configure_kernels(lc_plan* p) {
     if (ea == cudaSuccess) ea = set_attrs_vt<2>(smax);
     if (ea == cudaSuccess) ea = set_attrs_vt<4>(smax);
     if (ea == cudaSuccess) ea = set_attrs_vt<8>(smax);
+    if (ea == cudaSuccess) {
+      double B[kMM];
+      ea = cudaMemcpy(B, p->d_B, sizeof(B), cudaMemcpyDeviceToHost);
+      if (ea == cudaSuccess) ea = cudaMemcpyToSymbol(c_B0, B, sizeof(B));
+    }
     if (ea != cudaSuccess) return record_cuda_error(ea);
     g_device_ready[p->device] = true;
   }
   smax -= 256;  // static shared memory of the kernels
 
-  const int64_t budget3 = 74 * 1024;  // down kernel: three CTAs per SM
+  const int64_t budget2 = 113 * 1024;  // two CTAs per SM (228 KB minus 1 KB reserved per CTA)
+  const int64_t budget3 = 74 * 1024;   // three CTAs per SM
   int vt = p->vt;
   if (vt <= 0) vt = p->batch >= 2 ? 2 : 1;
   if (vt != 1 && vt != 2 && vt != 4 && vt != 8) return LC_ERR_INVALID_ARG;
   const bool user_k = p->k > 0;
   int k = user_k ? p->k : 4;
   int cb = p->bps > 0 ? p->bps : 3;
-  int nst = p->nst > 0 ? p->nst : 4;
+  int nst = p->nst > 0 ? p->nst : 3;
   if (nst > 8) return LC_ERR_INVALID_ARG;
   const int64_t nleaf_total = p->L > 0 ? (int64_t(2) << p->L) : 2;  // leaf segments (L = 0: the two halves)
   int lnleaf = 0;
@@ -1049,19 +1033,17 @@ lc_status configure_kernels(lc_plan* p) {
     while (down_bytes(vt, k) > budget3 && p->L > 0 && k > 1) --k;
   }
   if (down_bytes(vt, k) > smax) return LC_ERR_INVALID_ARG;
-  // fused kernel: streaming region (ring + band tiles of 2^kb segments) + upward-pass region
-  int kb = std::min(5, lnleaf);  // 2^kb segments x 2 parities x ceil(s/R) blocks of band items per unit
+  // streaming kernel: band units of 2^kb leaf segments
+  int kb = std::min(4, lnleaf);  // 2^kb segments x 2 parities x ceil(s/R) blocks = one item per band thread
+  auto stream_bytes = [&](int cb_, int kb_) { return stream_smem_layout(vt, cb_, nst, kb_, int(p->s)).total; };
+  while (stream_bytes(cb, kb) > budget2 && kb > 1) --kb;
+  while (stream_bytes(cb, kb) > budget2 && cb > 1) --cb;
+  if (stream_bytes(cb, kb) > smax) return LC_ERR_INVALID_ARG;
+  // up kernel: deeper subtrees (its shared memory is small); continuation step = its depth
   const bool user_kup = p->kup > 0;
   int kup = p->L > 0 ? int(std::min<int64_t>(user_kup ? p->kup : 5, p->L - 1)) : 0;
-  auto fused_bytes = [&](int cb_, int nst_, int kb_, int kup_) {
-    return stream_smem_layout(vt, cb_, nst_, kb_, int(p->s)).total +
-           (p->L > 0 ? up_smem_bytes(vt, kup_, int(p->s)) : 0);
-  };
-  while (fused_bytes(cb, nst, kb, kup) > smax && !user_kup && kup > 1) --kup;
-  while (fused_bytes(cb, nst, kb, kup) > smax && kb > 1) --kb;
-  while (fused_bytes(cb, nst, kb, kup) > smax && nst > 2) --nst;
-  while (fused_bytes(cb, nst, kb, kup) > smax && cb > 1) --cb;
-  if (fused_bytes(cb, nst, kb, kup) > smax) return LC_ERR_INVALID_ARG;
+  while (!user_kup && kup > 0 && up_smem_bytes(vt, kup, int(p->s)) > budget2) --kup;
+  if (up_smem_bytes(vt, kup, int(p->s)) > smax) return LC_ERR_INVALID_ARG;
   p->vt = vt;
   p->k = k;
   p->bps = cb;
@@ -1073,16 +1055,26 @@ lc_status configure_kernels(lc_plan* p) {
   p->group = std::max(kup, 1);
   p->ntiles = (p->batch + vt - 1) / vt;
   p->smem_down = size_t(down_bytes(vt, k));
-  p->smem_stream = size_t(fused_bytes(cb, nst, kb, kup));
+  p->smem_up = size_t(up_smem_bytes(vt, kup, int(p->s)));
+  p->smem_stream = size_t(stream_bytes(cb, kb));
   int64_t nchunks = 0;
   for (int g = 0; g < p->L; ++g) nchunks += (((int64_t(2) << g) - 1) + cb - 1) / cb;
   p->m2l_units = nchunks * p->ntiles;
   p->band_units = (nleaf_total >> kb) * p->ntiles;
   if (p->m2l_units + p->band_units > 0x7fffffff) return LC_ERR_INVALID_ARG;
-  const int64_t ntasks = p->L > 0 ? (int64_t(4) << p->grup) * p->ntiles : 0;
-  // persistent grid, one CTA per SM (all CTAs co-resident)
-  p->stream_grid = int(std::max<int64_t>(
-      1, std::min<int64_t>(p->sm_count, std::max<int64_t>(ntasks, p->m2l_units + p->band_units))));
+  {
+    int occ = 0;
+    switch (vt) {
+      case 1: occ = stream_occupancy<1>(p->dir, p->smem_stream); break;
+      case 2: occ = stream_occupancy<2>(p->dir, p->smem_stream); break;
+      case 4: occ = stream_occupancy<4>(p->dir, p->smem_stream); break;
+      default: occ = stream_occupancy<8>(p->dir, p->smem_stream); break;
+    }
+    if (occ < 1) return LC_ERR_INVALID_ARG;
+    // persistent grid: every CTA co-resident (the producer may wait on flags raised by other grids)
+    const int64_t g = int64_t(occ) * p->sm_count;
+    p->stream_grid = int(std::max<int64_t>(1, std::min<int64_t>(g, p->m2l_units + p->band_units)));
+  }
   if (p->L > 0) {
     p->w_tile_doubles = int64_t(vt) * kM * 2 * ((int64_t(4) << p->L) - 4);
     p->cnt_tile_ints = int64_t(4) << p->L;
@@ -1090,16 +1082,15 @@ lc_status configure_kernels(lc_plan* p) {
     p->w_tile_doubles = 0;
     p->cnt_tile_ints = 0;
   }
-  // workspace: w | c_m2l | flags (64 ints) | ready (ntasks ints) | arrival counters
-  // (c_m2l rows without a submatrix stay zero from the initialisation)
+  // workspace: w | c_m2l | flags (64 ints) | arrival counters (c_m2l rows without a submatrix stay zero)
   const size_t wb = size_t(align_up(p->ntiles * p->w_tile_doubles * 8, 256));
-  p->ws_bytes = 2 * wb + 256 + size_t(align_up(ntasks * 4, 256)) + size_t(p->ntiles * p->cnt_tile_ints) * sizeof(int);
+  p->ws_bytes = 2 * wb + 256 + size_t(p->ntiles * p->cnt_tile_ints) * sizeof(int);
   return LC_OK;
 }
 
 template <int VT, int DIR>
-static cudaError_t launch_vt(const lc_plan* p, const FmmParams& fp, const DownParams& dp, dim3 grid,
-                             cudaStream_t st, cudaEvent_t const* ev, int nev) {
+static cudaError_t launch_vt(const lc_plan* p, const UpParams& up, const StreamParams& sp, const DownParams& dp,
+                             dim3 grid_up, dim3 grid, cudaStream_t st, cudaEvent_t const* ev, int nev) {
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
@@ -1110,10 +1101,18 @@ static cudaError_t launch_vt(const lc_plan* p, const FmmParams& fp, const DownPa
   cudaError_t e = cudaSuccess;
   int evi = 0;
   if (ev && nev > 0) cudaEventRecord(ev[evi++], st);
+  if (p->L > 0) {
+    cfg.gridDim = grid_up;
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = p->smem_up;
+    e = cudaLaunchKernelEx(&cfg, lc_up_kernel<VT>, up);
+    if (e != cudaSuccess) return e;
+    if (ev && evi < nev) cudaEventRecord(ev[evi++], st);
+  }
   cfg.gridDim = dim3(unsigned(p->stream_grid));
-  cfg.blockDim = dim3(kFusedThreads);
+  cfg.blockDim = dim3(kStreamThreads);
   cfg.dynamicSmemBytes = p->smem_stream;
-  e = cudaLaunchKernelEx(&cfg, lc_fmm_kernel<VT, DIR>, fp);
+  e = cudaLaunchKernelEx(&cfg, lc_stream_kernel<VT, DIR>, sp);
   if (e != cudaSuccess) return e;
   if (ev && evi < nev) cudaEventRecord(ev[evi++], st);
   cfg.gridDim = p->L > 0 ? grid : dim3(1, grid.y);
@@ -1144,20 +1143,21 @@ lc_status launch_execute(const lc_plan* p, const double* in, double* out, void* 
   cudaGetDevice(&prev);
   if (prev != p->device) cudaSetDevice(p->device);
   const size_t wb = size_t(align_up(p->ntiles * p->w_tile_doubles * 8, 256));
-  const int64_t ntasks = p->L > 0 ? (int64_t(4) << p->grup) * p->ntiles : 0;
   double* w = reinterpret_cast<double*>(ws);
   double* c = reinterpret_cast<double*>(reinterpret_cast<char*>(ws) + wb);
   int* flags = reinterpret_cast<int*>(reinterpret_cast<char*>(ws) + 2 * wb);
-  int* ready = flags + 64;
-  int* cnt = reinterpret_cast<int*>(reinterpret_cast<char*>(ready) + align_up(ntasks * 4, 256));
-  FmmParams fp{};
-  fp.in = in; fp.out = out; fp.ld_in = p->ld_in; fp.ld_out = p->ld_out; fp.n = p->n; fp.N = p->N;
-  fp.batch = p->batch; fp.ntiles = p->ntiles; fp.layout = p->layout; fp.L = int(p->L); fp.s = int(p->s);
-  fp.flags = flags; fp.ready = ready; fp.w_tile = p->w_tile_doubles;
-  fp.T = p->d_T; fp.B = p->d_B; fp.w = w; fp.cnt = cnt; fp.cnt_tile = p->cnt_tile_ints;
-  fp.kup = p->kup; fp.grup = p->grup; fp.G = p->group;
-  fp.A = p->d_A; fp.c = c; fp.tabA = p->d_tabA; fp.tabB = p->d_tabB; fp.nm2l = p->m2l_units;
-  fp.nband = p->band_units; fp.cb = p->bps; fp.nst = p->nst; fp.kb = p->kb;
+  int* cnt = flags + 64;
+  UpParams up{};
+  up.in = in; up.ld_in = p->ld_in; up.n = p->n; up.N = p->N; up.batch = p->batch;
+  up.layout = p->layout; up.L = int(p->L); up.s = int(p->s); up.k = p->kup; up.gr = p->grup; up.G = p->group;
+  up.T = p->d_T; up.B = p->d_B; up.w = w; up.cnt = cnt; up.flags = flags; up.w_tile = p->w_tile_doubles;
+  up.cnt_tile = p->cnt_tile_ints;
+  StreamParams sp{};
+  sp.A = p->d_A; sp.w = w; sp.c = c; sp.in = in; sp.out = out; sp.tabA = p->d_tabA; sp.tabB = p->d_tabB;
+  sp.flags = flags; sp.w_tile = p->w_tile_doubles; sp.ld_in = p->ld_in; sp.ld_out = p->ld_out; sp.n = p->n;
+  sp.N = p->N; sp.batch = p->batch; sp.ntiles = p->ntiles; sp.nm2l = p->m2l_units; sp.nband = p->band_units;
+  sp.layout = p->layout; sp.L = int(p->L); sp.s = int(p->s); sp.cb = p->bps; sp.nst = p->nst; sp.kb = p->kb;
+  sp.gr_up = p->grup;
   DownParams dp{};
   dp.out = out; dp.ld_out = p->ld_out; dp.n = p->n; dp.N = p->N; dp.batch = p->batch; dp.layout = p->layout;
   dp.L = int(p->L); dp.s = int(p->s); dp.k = p->k; dp.gr = p->gr; dp.Tt = p->d_Tt; dp.B = p->d_B; dp.c = c;
@@ -1168,17 +1168,18 @@ lc_status launch_execute(const lc_plan* p, const double* in, double* out, void* 
     return LC_ERR_INVALID_ARG;
   }
   const dim3 grid(unsigned(nsub), unsigned(p->ntiles));
+  const dim3 grid_up(unsigned(p->L > 0 ? (int64_t(4) << p->grup) : 1), unsigned(p->ntiles));
   cudaError_t e;
   const int key = p->vt * 2 + p->dir;
   switch (key) {
-    case 2: e = launch_vt<1, 0>(p, fp, dp, grid, st, ev, nev); break;
-    case 3: e = launch_vt<1, 1>(p, fp, dp, grid, st, ev, nev); break;
-    case 4: e = launch_vt<2, 0>(p, fp, dp, grid, st, ev, nev); break;
-    case 5: e = launch_vt<2, 1>(p, fp, dp, grid, st, ev, nev); break;
-    case 8: e = launch_vt<4, 0>(p, fp, dp, grid, st, ev, nev); break;
-    case 9: e = launch_vt<4, 1>(p, fp, dp, grid, st, ev, nev); break;
-    case 16: e = launch_vt<8, 0>(p, fp, dp, grid, st, ev, nev); break;
-    case 17: e = launch_vt<8, 1>(p, fp, dp, grid, st, ev, nev); break;
+    case 2: e = launch_vt<1, 0>(p, up, sp, dp, grid_up, grid, st, ev, nev); break;
+    case 3: e = launch_vt<1, 1>(p, up, sp, dp, grid_up, grid, st, ev, nev); break;
+    case 4: e = launch_vt<2, 0>(p, up, sp, dp, grid_up, grid, st, ev, nev); break;
+    case 5: e = launch_vt<2, 1>(p, up, sp, dp, grid_up, grid, st, ev, nev); break;
+    case 8: e = launch_vt<4, 0>(p, up, sp, dp, grid_up, grid, st, ev, nev); break;
+    case 9: e = launch_vt<4, 1>(p, up, sp, dp, grid_up, grid, st, ev, nev); break;
+    case 16: e = launch_vt<8, 0>(p, up, sp, dp, grid_up, grid, st, ev, nev); break;
+    case 17: e = launch_vt<8, 1>(p, up, sp, dp, grid_up, grid, st, ev, nev); break;
     default: e = cudaErrorInvalidValue;
   }
   if (prev != p->device) cudaSetDevice(prev);
@@ -1193,7 +1194,7 @@ extern "C" lc_status lc_execute(const lc_plan* p, const double* in, double* out,
 
 extern "C" lc_status lc_execute_timed(const lc_plan* p, const double* in, double* out, void* ws, void* stream,
                                       void* const* ev, int32_t nev) {
-  if (!p || !ev || nev < 3) return LC_ERR_INVALID_ARG;
+  if (!p || !ev || nev < (p->L > 0 ? 4 : 3)) return LC_ERR_INVALID_ARG;
   return lc::launch_execute(p, in, out, ws, (cudaStream_t)stream, reinterpret_cast<cudaEvent_t const*>(ev), nev);
 }
 

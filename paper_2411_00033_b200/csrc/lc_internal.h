@@ -104,7 +104,6 @@ __host__ __device__ inline int64_t up_smem_bytes(int VT, int k, int s) {
   int64_t o = 0;
   o = align_up(o + int64_t(2) * s * kM * 8, 128);                 // T [2][s][M]
   o = align_up(o + int64_t(VT) * (int64_t(1) << k) * 2 * s * 8, 128);  // f tile
-  o = align_up(o + int64_t(VT) * (int64_t(1) << k) * 2 * s * 8, 128);  // f tile (prefetch buffer)
   o = align_up(o + ((int64_t(2) << k) - 1) * 2 * VT * kM * 8, 128);    // w tree
   o += 16;
   return o;

@@ -399,7 +399,7 @@ extern "C" lc_status lc_plan_describe(const lc_plan* p, lc_plan_desc* d) {
   d->plan_bytes = p->plan_bytes; d->workspace_bytes = p->ws_bytes;
   d->flops_alg = p->flops_alg; d->bytes_alg = p->bytes_alg;
   d->vt = p->vt; d->subtree = p->k; d->stage_blocks = p->bps; d->stages = p->nst;
-  d->kernels_per_execute = 2;
+  d->kernels_per_execute = p->L > 0 ? 3 : 2;
   return LC_OK;
 }
 

@@ -46,9 +46,10 @@ def run(n, d, V=1, reps=30, **opts):
 if __name__ == "__main__":
     gpu_warmup(1.5)
     n = int(sys.argv[1]) if len(sys.argv) > 1 else 1000000
-    for kup in (3, 4, 5, 6):
+    import itertools
+    for kup in (4, 5, 6):
         run(n, "leg2cheb", up_subtree=kup)
-    for k in (2, 3, 4, 5):
+    for k in (3, 4, 5):
         run(n, "leg2cheb", subtree=k)
-    for cb, nst in ((2, 4), (3, 3), (4, 2), (6, 2), (3, 4), (8, 2)):
+    for cb, nst in ((3, 2), (3, 3), (3, 4), (2, 6), (4, 3), (6, 2)):
         run(n, "leg2cheb", stage_blocks=cb, stages=nst)
