@@ -1,0 +1,114 @@
+"""Multi-GPU drivers over torch.distributed (one process per GPU; NCCL over NVLink).
+
+Two partitionings:
+
+* batch sharding (cfg3, cfg4): independent vectors are split contiguously over the ranks; every rank
+  holds the full plan (replicated) and transforms its own slice -- there is no collective on the data
+  path (`shard_range`, `BatchedTransform`).
+* 2-D tensor-product transform (cfg5): an n0 x n1 array partitioned by rows.  Pass 1 transforms along
+  axis 1 (each local row is one vector); an all-to-all transposes the row slabs into column slabs;
+  pass 2 transforms along axis 0 with the batch-contiguous layout (LC_BATCH_CONTIGUOUS), so no local
+  transpose is needed after the exchange (`tensor_product_2d`).
+
+The per-pass transform is injectable (`row_fn`, `col_fn`) so that the index algebra can be tested on
+CPU ranks with gloo; the default is the sm_100a library through `Plan`.
+"""
+from __future__ import annotations
+
+from typing import Callable, Optional
+
+import torch
+import torch.distributed as dist
+
+
+def shard_range(total: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous [start, stop) of `total` items owned by `rank` (the first total % world ranks get one more)."""
+    base, rem = divmod(total, world)
+    start = rank * base + min(rank, rem)
+    return start, start + base + (1 if rank < rem else 0)
+
+
+class BatchedTransform:
+    """Transform of this rank's contiguous slice of a batch of vectors (no communication)."""
+
+    def __init__(self, n: int, direction: str, total_batch: int, group=None, device=None, **opts):
+        from .api import Plan
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.start, self.stop = shard_range(total_batch, self.world, self.rank)
+        self.plan = Plan(n, direction, batch=max(1, self.stop - self.start), device=device, **opts)
+
+    def __call__(self, x_local: torch.Tensor, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+        if x_local.shape[0] != self.stop - self.start:
+            raise ValueError(f"rank {self.rank} owns vectors [{self.start}, {self.stop})")
+        return self.plan.execute(x_local, out)
+
+
+def pack_for_transpose(y_rows: torch.Tensor, world: int) -> torch.Tensor:
+    """[R, n1] row slab -> [world, R, C] with block d = columns [d C, (d+1) C) (C = n1 / world)."""
+    R, n1 = y_rows.shape
+    C = n1 // world
+    return y_rows.reshape(R, world, C).permute(1, 0, 2).contiguous()
+
+
+def transpose_rows_to_cols(y_rows: torch.Tensor, group=None) -> torch.Tensor:
+    """All-to-all: row slab [R, n1] of every rank -> column slab [n0, C] (row-major, C = n1 / world).
+
+    Rank r sends block (its rows) x (columns of rank d) to rank d; stacking the received blocks over
+    the source ranks gives rows in global order, i.e. the column slab in the batch-contiguous layout."""
+    world = dist.get_world_size(group)
+    R, n1 = y_rows.shape
+    if n1 % world:
+        raise ValueError("n1 must be divisible by the number of ranks")
+    send = pack_for_transpose(y_rows, world)
+    recv = torch.empty_like(send)
+    dist.all_to_all_single(recv.view(-1), send.view(-1), group=group)
+    return recv.reshape(world * R, n1 // world)
+
+
+def transpose_cols_to_rows(z_cols: torch.Tensor, group=None) -> torch.Tensor:
+    """Inverse exchange: column slab [n0, C] -> row slab [R, n1] (R = n0 / world)."""
+    world = dist.get_world_size(group)
+    n0, C = z_cols.shape
+    send = z_cols.reshape(world, n0 // world, C).contiguous()
+    recv = torch.empty_like(send)
+    dist.all_to_all_single(recv.view(-1), send.view(-1), group=group)
+    return recv.permute(1, 0, 2).reshape(n0 // world, world * C)
+
+
+def tensor_product_2d(x_rows: torch.Tensor, group=None, row_fn: Optional[Callable] = None,
+                      col_fn: Optional[Callable] = None, direction: str = "leg2cheb",
+                      restore_rows: bool = False, timing: Optional[dict] = None) -> torch.Tensor:
+    """2-D transform of an n0 x n1 array partitioned by rows (this rank: [n0/world, n1]).
+
+    Pass 1 along axis 1 on the row slab, all-to-all, pass 2 along axis 0 on the column slab
+    ([n0, n1/world], batch-contiguous).  Returns the column slab, or the row slab if restore_rows."""
+    world = dist.get_world_size(group)
+    R, n1 = x_rows.shape
+    n0 = R * world
+    C = n1 // world
+    if row_fn is None or col_fn is None:
+        from .api import Plan
+        if row_fn is None:
+            prow = Plan(n1, direction, batch=R, device=x_rows.device)
+            row_fn = prow.execute
+        if col_fn is None:
+            pcol = Plan(n0, direction, batch=C, device=x_rows.device, layout="batch")
+            col_fn = pcol.execute
+    ev = None
+    if timing is not None and x_rows.is_cuda:
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        ev[0].record()
+    y = row_fn(x_rows)
+    if ev:
+        ev[1].record()
+    yc = transpose_rows_to_cols(y, group)
+    if ev:
+        ev[2].record()
+    z = col_fn(yc)
+    if ev:
+        ev[3].record()
+        torch.cuda.synchronize()
+        timing.update(pass1_ms=ev[0].elapsed_time(ev[1]), alltoall_ms=ev[1].elapsed_time(ev[2]),
+                      pass2_ms=ev[2].elapsed_time(ev[3]))
+    return transpose_cols_to_rows(z, group) if restore_rows else z

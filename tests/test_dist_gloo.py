@@ -1,0 +1,119 @@
+"""World-size-2 (and 3) gloo tests of the multi-GPU host logic on CPU ranks: batch sharding index maps
+and the 2-D tensor-product transform with its all-to-all transposes.  The per-pass transform is the
+CPU oracle (a test stand-in; the product path never imports it)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2411_00033_b200.dist import (pack_for_transpose, shard_range, tensor_product_2d,
+                                        transpose_cols_to_rows, transpose_rows_to_cols)
+
+
+def test_shard_range_covers_exactly():
+    for total in (1, 7, 64, 4096, 4097):
+        for world in (1, 2, 3, 4, 8):
+            spans = [shard_range(total, world, r) for r in range(world)]
+            assert spans[0][0] == 0 and spans[-1][1] == total
+            assert all(spans[i][1] == spans[i + 1][0] for i in range(world - 1))
+            sizes = [b - a for a, b in spans]
+            assert max(sizes) - min(sizes) <= 1
+
+
+def test_pack_for_transpose_blocks():
+    y = torch.arange(4 * 6, dtype=torch.float64).reshape(4, 6)
+    p = pack_for_transpose(y, 3)
+    for d in range(3):
+        assert torch.equal(p[d], y[:, 2 * d:2 * d + 2])
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _oracle_rows(x):  # transform each row (a vector) with the oracle: stand-in for the GPU plan
+    import oracle
+    return torch.from_numpy(np.stack([oracle.l2c(r.numpy()).astype(np.float64) for r in x]))
+
+
+def _oracle_cols_batch_layout(x):  # x: [n0, C] batch-contiguous columns
+    import oracle
+    cols = [oracle.l2c(x[:, j].numpy()).astype(np.float64) for j in range(x.shape[1])]
+    return torch.from_numpy(np.stack(cols, axis=1))
+
+
+def _worker(rank, world, port, n0, n1, results):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        g = torch.Generator().manual_seed(5)
+        full = torch.randn(n0, n1, generator=g, dtype=torch.float64)
+        full /= torch.outer(torch.arange(1, n0 + 1, dtype=torch.float64), torch.arange(1, n1 + 1, dtype=torch.float64))
+        R = n0 // world
+        mine = full[rank * R:(rank + 1) * R].contiguous()
+        # the exchange alone round-trips
+        back = transpose_cols_to_rows(transpose_rows_to_cols(mine), None)
+        ok_roundtrip = torch.equal(back, mine)
+        # the column slab after the exchange holds columns [rank C, (rank+1) C) of the full array
+        C = n1 // world
+        cols = transpose_rows_to_cols(mine)
+        ok_cols = torch.equal(cols, full[:, rank * C:(rank + 1) * C])
+        z = tensor_product_2d(mine, None, row_fn=_oracle_rows, col_fn=_oracle_cols_batch_layout)
+        zr = tensor_product_2d(mine, None, row_fn=_oracle_rows, col_fn=_oracle_cols_batch_layout,
+                               restore_rows=True)
+        results[rank] = (ok_roundtrip, ok_cols, z.numpy().copy(), zr.numpy().copy())
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n0,n1", [(2, 40, 24), (3, 33, 27)])
+def test_tensor_product_2d_gloo(world, n0, n1):
+    import oracle
+    mgr = mp.Manager()
+    results = mgr.dict()
+    port = _free_port()
+    mp.spawn(_worker, args=(world, port, n0, n1, results), nprocs=world, join=True)
+    g = torch.Generator().manual_seed(5)
+    full = torch.randn(n0, n1, generator=g, dtype=torch.float64)
+    full /= torch.outer(torch.arange(1, n0 + 1, dtype=torch.float64), torch.arange(1, n1 + 1, dtype=torch.float64))
+    # reference: L2C along axis 1 then axis 0 (separable 2-D transform, SURVEY C-4 for cfg5)
+    ref = np.stack([oracle.l2c(r).astype(np.float64) for r in full.numpy()])
+    ref = np.stack([oracle.l2c(ref[:, j]).astype(np.float64) for j in range(n1)], axis=1)
+    C = n1 // world
+    R = n0 // world
+    for r in range(world):
+        ok_rt, ok_cols, z, zr = results[r]
+        assert ok_rt and ok_cols
+        assert np.max(np.abs(z - ref[:, r * C:(r + 1) * C])) <= 1e-15 * np.max(np.abs(ref))
+        assert np.max(np.abs(zr - ref[r * R:(r + 1) * R])) <= 1e-15 * np.max(np.abs(ref))
+
+
+def _batch_worker(rank, world, port, total, results):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        a, b = shard_range(total, world, rank)
+        t = torch.tensor([b - a], dtype=torch.int64)
+        dist.all_reduce(t)
+        mx = torch.tensor([float(rank + 1)], dtype=torch.float64)
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)  # bench.py's max-over-ranks timing reduction
+        results[rank] = (a, b, int(t.item()), float(mx.item()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_batch_sharding_gloo():
+    world, total = 2, 4097
+    mgr = mp.Manager()
+    results = mgr.dict()
+    mp.spawn(_batch_worker, args=(world, _free_port(), total, results), nprocs=world, join=True)
+    assert results[0][:2] == (0, 2049) and results[1][:2] == (2049, 4097)
+    assert all(results[r][2] == total and results[r][3] == float(world) for r in range(world))
