@@ -163,6 +163,7 @@ def make_input(kind, n, V, v0, pin):
 # --------------------------------------------------------------------------- our arm
 def run_gpu(args, world, rank, local):
     from paper_2411_00033_b200 import Plan
+    from paper_2411_00033_b200.dist import tensor_product_2d
     dev = torch.device("cuda", local)
     n, V, kind, v0, scaling = workload(args.config, world, rank)
     xh = make_input(kind, n, V, v0, pin=True)
@@ -170,13 +171,26 @@ def run_gpu(args, world, rank, local):
     tmp = torch.empty_like(x)
     y = torch.empty_like(x)
     opts = dict(vt=args.vt, subtree=args.subtree, stage_blocks=args.stage_blocks, stages=args.stages)
-    pl = Plan(n, "leg2cheb", batch=V, device=dev, **opts)
-    pc = Plan(n, "cheb2leg", batch=V, device=dev, **opts)
     stream = torch.cuda.current_stream(dev)
+    two_d = args.config == "cfg5"
+    if two_d:
+        # rows [v0, v0+V) of the n x n array on this rank; pass 1 along axis 1 (V row vectors), all-to-all,
+        # pass 2 along axis 0 (n/world column vectors, batch-contiguous)
+        scaling = "strong"
+        C = n // world
+        pl = Plan(n, "leg2cheb", batch=V, device=dev, **opts)
+        pc = Plan(n, "leg2cheb", batch=C, device=dev, layout="batch", **opts)
+        ycol = torch.empty((n, C), dtype=torch.float64, device=dev)
 
-    def step():
-        pl.execute(x, tmp)
-        pc.execute(tmp, y)
+        def step():
+            tensor_product_2d(x, row_fn=lambda a: pl.execute(a, tmp), col_fn=lambda a: pc.execute(a, ycol))
+    else:
+        pl = Plan(n, "leg2cheb", batch=V, device=dev, **opts)
+        pc = Plan(n, "cheb2leg", batch=V, device=dev, **opts)
+
+        def step():
+            pl.execute(x, tmp)
+            pc.execute(tmp, y)
 
     for _ in range(args.warmup):
         step()
@@ -227,7 +241,7 @@ def run_gpu(args, world, rank, local):
     value = total_coeffs * args.steps / (ms / 1e3)
 
     # correctness of what was timed: round trip back to the input (gate 1e-12 for n <= 1e6)
-    rt = float((y - x).abs().max() / x.abs().max())
+    rt = None if two_d else float((y - x).abs().max() / x.abs().max())
 
     # ---- per-kernel durations (events around each kernel, same stream) for the roofline
     kpe = pl.kernels_per_execute
@@ -237,7 +251,10 @@ def run_gpu(args, world, rank, local):
     per_kernel = [[0.0] * kpe, [0.0] * kpe]
     for _ in range(ksteps):
         pl.execute_timed(x, tmp, evs)
-        pc.execute_timed(tmp, y, evc)
+        if two_d:
+            pl.execute_timed(x, tmp, evc)
+        else:
+            pc.execute_timed(tmp, y, evc)
         torch.cuda.synchronize()
         for d, ev in enumerate((evs, evc)):
             for i in range(kpe):
@@ -264,11 +281,23 @@ def run_gpu(args, world, rank, local):
 
     # ---- e2e through the C ABI with HOST buffers (lc_execute_host: H2D, kernels, D2H per transform)
     hz = torch.empty_like(xh).pin_memory()
-    hy = torch.empty_like(xh).pin_memory()
+    hy = torch.empty_like(xh).pin_memory() if not two_d else torch.empty((n, n // world), dtype=torch.float64).pin_memory()
     e2e_steps = max(3, min(args.steps, args.e2e_steps))
+
+    def host_step():
+        if two_d and world == 1:
+            pl.execute_host(xh, hz)
+            pc.execute_host(hz.view(n, n), hy)
+        elif two_d:
+            xd = xh.to(dev, non_blocking=True)
+            zc = tensor_product_2d(xd, row_fn=lambda a: pl.execute(a, tmp), col_fn=lambda a: pc.execute(a, ycol))
+            hy.copy_(zc, non_blocking=True)
+        else:
+            pl.execute_host(xh, hz)
+            pc.execute_host(hz, hy)
+
     for _ in range(2):
-        pl.execute_host(xh, hz)
-        pc.execute_host(hz, hy)
+        host_step()
     torch.cuda.synchronize()
     barrier(world)
     torch.cuda.synchronize()
@@ -276,15 +305,18 @@ def run_gpu(args, world, rank, local):
     h1 = torch.cuda.Event(enable_timing=True)
     h0.record(stream)
     for _ in range(e2e_steps):
-        pl.execute_host(xh, hz)
-        pc.execute_host(hz, hy)
+        host_step()
     h1.record(stream)
     torch.cuda.synchronize()
     barrier(world)
     e2e_ms = allreduce_max(h0.elapsed_time(h1), world)
     e2e_val = total_coeffs * e2e_steps / (e2e_ms / 1e3)
-    rt_host = float((hy - xh).abs().max() / xh.abs().max())
+    rt_host = None if two_d else float((hy - xh).abs().max() / xh.abs().max())
     bytes_vec = 8 * n * V
+    h2d = bytes_vec * (1 if (two_d and world > 1) else 2)
+    d2h = 8 * hy.numel() if two_d else 2 * bytes_vec
+    if two_d and world == 1:
+        h2d, d2h = 2 * bytes_vec, 2 * bytes_vec
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
@@ -294,8 +326,10 @@ def run_gpu(args, world, rank, local):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": scaling,
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE.json recipe)",
-        "config": {"workload": f"{args.config}: leg2cheb then cheb2leg (round trip) of {V} fp64 vector(s) "
-                               f"of n={n} per GPU", "n": n, "vectors_per_gpu": V, "N_padded": dl["N"],
+        "config": {"workload": (f"{args.config}: leg2cheb then cheb2leg (round trip) of {V} fp64 vector(s) "
+                                f"of n={n} per GPU") if not two_d else
+                               (f"cfg5: 2-D leg2cheb of an {n}x{n} fp64 array (axis 1, all-to-all, axis 0), "
+                                f"{V} rows per GPU"), "n": n, "vectors_per_gpu": V, "N_padded": dl["N"],
                    "L": dl["L"], "s": dl["s"], "M": 18, "s_hat": 32, "transforms_per_step": 2,
                    "input_kind": kind,
                    "l2": f"no flush: per-step working set {2 * 8 * 324 * dl['nc'] / 1e6:.0f} MB of A_hat + "
@@ -312,9 +346,10 @@ def run_gpu(args, world, rank, local):
         "kernel_ms": {"leg2cheb": per_kernel[0], "cheb2leg": per_kernel[1], "names": names,
                       "algorithmic_bytes": [alg[nm] for nm in names],
                       "achieved_gbs": [alg[nm] / (avg_ms[nm] * 1e-3) / 1e9 for nm in names]},
-        "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": 2 * bytes_vec,
-                "d2h_bytes_per_step": 2 * bytes_vec, "steps": e2e_steps, "ms_per_step": e2e_ms / e2e_steps,
-                "path": "lc_execute_host (C ABI, pinned host buffers) x2 per step"},
+        "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "steps": e2e_steps, "ms_per_step": e2e_ms / e2e_steps,
+                "path": "lc_execute_host (C ABI, pinned host buffers) x2 per step" if not (two_d and world > 1)
+                        else "H2D + tensor_product_2d (NCCL all-to-all) + D2H"},
         "gpu_launches": kpe * 2 * args.steps,
         "clocks": clk,
         "round_trip_einf": {"device": rt, "host_path": rt_host},

@@ -83,7 +83,7 @@ def tensor_product_2d(x_rows: torch.Tensor, group=None, row_fn: Optional[Callabl
 
     Pass 1 along axis 1 on the row slab, all-to-all, pass 2 along axis 0 on the column slab
     ([n0, n1/world], batch-contiguous).  Returns the column slab, or the row slab if restore_rows."""
-    world = dist.get_world_size(group)
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
     R, n1 = x_rows.shape
     n0 = R * world
     C = n1 // world
@@ -102,7 +102,8 @@ def tensor_product_2d(x_rows: torch.Tensor, group=None, row_fn: Optional[Callabl
     y = row_fn(x_rows)
     if ev:
         ev[1].record()
-    yc = transpose_rows_to_cols(y, group)
+    # one rank: the row-major [n0, n1] result already is the batch-contiguous column layout
+    yc = transpose_rows_to_cols(y, group) if world > 1 else y
     if ev:
         ev[2].record()
     z = col_fn(yc)
@@ -111,4 +112,4 @@ def tensor_product_2d(x_rows: torch.Tensor, group=None, row_fn: Optional[Callabl
         torch.cuda.synchronize()
         timing.update(pass1_ms=ev[0].elapsed_time(ev[1]), alltoall_ms=ev[1].elapsed_time(ev[2]),
                       pass2_ms=ev[2].elapsed_time(ev[3]))
-    return transpose_cols_to_rows(z, group) if restore_rows else z
+    return transpose_cols_to_rows(z, group) if (restore_rows and world > 1) else z
