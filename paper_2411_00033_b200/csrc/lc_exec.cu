@@ -405,7 +405,10 @@ __global__ void __launch_bounds__(kThreads, 2) lc_up_kernel(const UpParams P) {
       s_last = last;
     }
     __syncthreads();
-    if (!s_last) return;
+    if (!s_last) {
+      LC_TS(0, 7);
+      return;
+    }
     LC_TS(0, 5);
     __threadfence();
     const int cnt2 = int((int64_t(1) << ge) * VM / 2);
@@ -445,6 +448,7 @@ __global__ void __launch_bounds__(kThreads, 2) lc_up_kernel(const UpParams P) {
       }
     }
   }
+  LC_TS(0, 7);
 }
 
 // ============================================================== streaming kernel
@@ -1232,6 +1236,12 @@ extern "C" lc_status lc_execute_host(const lc_plan* p_, const double* h_in, doub
 }
 
 #ifdef LC_PHASE_TIMING
+extern "C" int lc_debug_clear() {
+  static unsigned long long zero[1 << 16];
+  for (int k = 0; k < 3 * 16; ++k)
+    if (cudaMemcpyToSymbol(lc::g_lc_ts, zero, sizeof(zero), sizeof(zero) * size_t(k)) != cudaSuccess) return 1;
+  return 0;
+}
 extern "C" int lc_debug_timestamps(int kern, unsigned long long* host_out, long long count) {
   if (kern < 0 || kern > 2 || count > (1 << 20)) return 1;
   return cudaMemcpyFromSymbol(host_out, lc::g_lc_ts, sizeof(unsigned long long) * count,
