@@ -148,6 +148,13 @@ lc_status lc_execute_host(const lc_plan* p, const double* h_in, double* h_out, v
  * count = number of doubles host_out can hold; returns INVALID_ARG if short. */
 lc_status lc_plan_export(const lc_plan* p, int32_t what, double* host_out, int64_t count);
 
+/* Kernel configuration chosen for the plan (diagnostic; host only, no device work).
+ * out[0..] = stream_grid, smem_stream, smem_up, kup (up-kernel subtree depth), grup,
+ * kb (band/down unit depth), cb (blocks per A_hat stage), nst (stages), vt, stream CTAs per
+ * SM, m2l_units, band_units, up_grid (CTAs), kd (down-kernel subtree depth), smem_down.  count = capacity of out; returns the number of
+ * values written through *written (may be NULL).  Errors: INVALID_ARG on NULL p or out. */
+lc_status lc_plan_kernel_info(const lc_plan* p, int64_t* out, int32_t count, int32_t* written);
+
 lc_status lc_plan_destroy(lc_plan* p);
 
 const char* lc_status_string(lc_status s);

@@ -46,6 +46,7 @@ SIGNATURES = {
     "lc_execute_timed": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_vp, ctypes.POINTER(c_vp), c_i32]),
     "lc_execute_host": (c_i32, [c_vp, c_vp, c_vp, c_vp]),
     "lc_plan_export": (c_i32, [c_vp, c_i32, c_dp, c_i64]),
+    "lc_plan_kernel_info": (c_i32, [c_vp, ctypes.POINTER(c_i64), c_i32, ctypes.POINTER(c_i32)]),
     "lc_plan_destroy": (c_i32, [c_vp]),
     "lc_status_string": (ctypes.c_char_p, [c_i32]),
     "lc_version": (ctypes.c_char_p, []),

@@ -85,6 +85,16 @@ class Plan:
         return int(self._lib.lc_workspace_bytes(self._h))
 
     @property
+    def kernel_info(self) -> dict:
+        """Kernel configuration of the plan (lc_plan_kernel_info)."""
+        buf = (ctypes.c_int64 * 32)()
+        nw = ctypes.c_int32(0)
+        _lib.check("lc_plan_kernel_info", self._lib.lc_plan_kernel_info(self._h, buf, 32, ctypes.byref(nw)))
+        names = ["stream_grid", "smem_stream", "smem_up", "kup", "grup", "kb", "cb", "nst", "vt", "stream_occ",
+                 "m2l_units", "band_units", "up_grid", "kd", "smem_down"]
+        return {k: int(buf[i]) for i, k in enumerate(names[:nw.value])}
+
+    @property
     def kernels_per_execute(self) -> int:
         return int(self.desc["kernels_per_execute"])
 

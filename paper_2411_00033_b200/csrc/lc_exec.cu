@@ -1,31 +1,34 @@
 // lc_exec.cu -- execution stage (Alg. 4, alg:fastercomplete)
-// as three sm_100a kernels per transform; both parities are processed together
+// as two sm_100a kernels per transform; both parities are processed together
 // (the same A_hat serves sigma = 0 and 1, so it is streamed once).
 //
-//   lc_up_kernel     one CTA per subtree of 2^kup leaf segments x VT vectors:
-//                    step 1 (eq:wMM, w = f^sigma T(sigma)) and step 2 (eq:wtk with
-//                    Alg. a.1) inside the subtree; the last CTA
-//                    of each group of 2^G sibling subtrees (atomic arrival counter)
-//                    continues the upward pass G levels, up to level 0.  Writes
-//                    w(g) of every level; raises readiness flags.
-//   lc_stream_kernel persistent, warp-specialised.  One producer lane streams the
-//                    level-major A_hat arena with TMA bulk copies (cp.async.bulk +
-//                    mbarrier ring, L2 evict-first), finest level first, together
-//                    with each chunk's w window; eight consumer warps apply
-//                    step 3 (M2L) and, interleaved with it, the
-//                    direct band of step 6 (Alg. 1 restricted to j < j_end(i)),
-//                    which depends only on f and lambda: the fp64-heavy band runs
-//                    in the shadow of the HBM-bound A_hat stream.
-//   lc_down_kernel   one CTA per subtree of 2^k leaf row segments x VT vectors:
-//                    step 4 ("faster downward spreading", B(p)^T)
-//                    along the ancestor chain and down the subtree, step 5
-//                    (eq:step5) added to the band result, step 7 (C^{-1}), store.
+//   lc_up_kernel     one CTA per subtree of 2^kup leaf segments x VT vectors, one wave:
+//                    step 1 (eq:wMM, w = f^sigma T(sigma), T(sigma) read from the
+//                    kernel-parameter constant bank as uniform DFMA operands) and step 2
+//                    (eq:wtk with Alg. a.1) inside the subtree; the last
+//                    CTA of each group of 2^G sibling subtrees continues the upward pass
+//                    to level 0.  Writes w(g) of every level; raises readiness flags.
+//   lc_stream_kernel persistent, warp-specialised:
+//                    * producer lane: TMA bulk copies (cp.async.bulk + mbarrier ring,
+//                      L2 evict-first) of the level-major A_hat arena and each chunk's
+//                      w window, in the level order  [fine non-leaf levels] ->
+//                      [coarse levels] -> [leaf level L-1];
+//                    * 4 M2L warps: step 3 from the ring, c_m2l
+//                      stores, completion counters / epoch flags per chunk;
+//                    * 4 band warps: first the direct band of step 6 (Alg. 1 restricted
+//                      to j < j_end(i)), which depends only on f and lambda, then the
+//                      "down units": step 4 ("faster downward spreading")
+//                      along the ancestor chain and down a subtree, step 5 (eq:step5)
+//                      with T(sigma) from the constant bank, step 7 (C^{-1}) and the store.
+//                      A down unit needs the non-leaf levels of c_m2l (done before the
+//                      leaf level is streamed) and the leaf-level chunks over its rows,
+//                      so the downward pass overlaps the second half of the A_hat stream.
 //
-// Kernels are chained with programmatic dependent launch (griddepcontrol); the
-// streaming kernel synchronises with the up kernel through release/acquire flags
-// so that the band and the fine-level M2L overlap the end of the upward pass.
+// The kernels are chained with programmatic dependent launch (griddepcontrol); the
+// streaming kernel synchronises with the up kernel through release/acquire flags.
 #include <algorithm>
 #include <cstdio>
+#include <cstring>
 
 #include "lc_internal.h"
 
@@ -77,7 +80,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 }
 // cp.async (LDGSTS): per-element asynchronous global->shared copies for the small gathers
 // whose shared destinations are padded or scattered; src_bytes = 0 zero-fills (the zero
-// padding beyond n).
+// padding beyond n).  .cg (L2 only) for data produced by other SMs.
 __device__ __forceinline__ void cp_async8(void* dst, const void* src, uint32_t src_bytes) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(src_bytes)
                : "memory");
@@ -85,16 +88,23 @@ __device__ __forceinline__ void cp_async8(void* dst, const void* src, uint32_t s
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
+__device__ __forceinline__ void cp_async16z(void* dst, const void* src, uint32_t src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(src_bytes)
+               : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
-// named barrier among the consumer warps of the streaming kernel (the producer warp does not join)
-__device__ __forceinline__ void consumer_sync(int nthreads) {
-  asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");  // barrier 1: the band warps
+// named barriers of the streaming kernel: 1 = band warps, 2 = M2L warps (the producer joins neither)
+__device__ __forceinline__ void named_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 // release/acquire helpers for the readiness flags (gpu scope)
 __device__ __forceinline__ void st_release(int* p, int v) {
   asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void red_release_add(int* p, int v) {
+  asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 __device__ __forceinline__ int ld_acquire(const int* p) {
   int v;
@@ -104,109 +114,70 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
 __device__ __forceinline__ void wait_flag(const int* p) {
   while (ld_acquire(p) == 0) __nanosleep(64);
 }
+__device__ __forceinline__ void wait_geq(const int* p, int target) {  // wrap-safe "p >= target"
+  while (ld_acquire(p) - target < 0) __nanosleep(64);
+}
 
 // Phase timestamps for the debug build (-DLC_PHASE_TIMING): %globaltimer (ns) per CTA and phase.
 #ifdef LC_PHASE_TIMING
 __device__ unsigned long long g_lc_ts[3][1 << 20];
-__device__ __forceinline__ void lc_ts(int kern, int slot) {
-  if (threadIdx.x == 0) {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    const unsigned cta = blockIdx.y * gridDim.x + blockIdx.x;
-    if (cta * 8 + slot < (1u << 20)) g_lc_ts[kern][cta * 8 + slot] = t;
-  }
-}
-__device__ __forceinline__ void lc_ts_any(int kern, int slot) {  // any thread
+__device__ __forceinline__ void lc_ts_any(int kern, int slot) {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   const unsigned cta = blockIdx.y * gridDim.x + blockIdx.x;
   if (cta * 8 + slot < (1u << 20)) g_lc_ts[kern][cta * 8 + slot] = t;
 }
-#define LC_TS(k, s) lc_ts(k, s)
+#define LC_TS(k, s) \
+  do {                                   \
+    if (threadIdx.x == 0) lc_ts_any(k, s); \
+  } while (0)
+#define LC_TS_T(k, s) lc_ts_any(k, s)
 #else
 #define LC_TS(k, s) ((void)0)
+#define LC_TS_T(k, s) ((void)0)
 #endif
-
-__device__ __forceinline__ int64_t vaddr(int layout, int64_t ld, int64_t v, int64_t j) {
-  return layout == LC_VEC_CONTIGUOUS ? v * ld + j : j * ld + v;
-}
 
 // ---------------------------------------------------------------- transfer operators
 // Alg. a.1 for one parent node:
 // parent[n] = sum_{k<=n} b_nk (x0_k + (-1)^(n-k) x1_k)  (B(1) = B(0) with the odd diagonals
-// negated, App. A3).  Children streamed from shared memory one mode at a time; 18 register
-// accumulators; B(0) from constant memory.
+// negated, App. A3).  18 register accumulators; B(0) from constant memory.
 __device__ __forceinline__ void m2m18(const double* __restrict__ x0, const double* __restrict__ x1,
                                       double* __restrict__ out) {
   double acc[kM];
 #pragma unroll
   for (int n = 0; n < kM; ++n) acc[n] = 0.0;
 #pragma unroll
-  for (int k = 0; k < kM; ++k) {
-    const double a = x0[k], b = x1[k];
-    const double zp = a + b, zm = a - b;
+  for (int k = 0; k < kM; k += 2) {
+    const double2 a2 = *reinterpret_cast<const double2*>(x0 + k);
+    const double2 b2 = *reinterpret_cast<const double2*>(x1 + k);
+    const double zp0 = a2.x + b2.x, zm0 = a2.x - b2.x, zp1 = a2.y + b2.y, zm1 = a2.y - b2.y;
 #pragma unroll
-    for (int n = k; n < kM; ++n) acc[n] = fma(c_B0[n * kM + k], ((n - k) & 1) ? zm : zp, acc[n]);
+    for (int n = k; n < kM; ++n) acc[n] = fma(c_B0[n * kM + k], ((n - k) & 1) ? zm0 : zp0, acc[n]);
+#pragma unroll
+    for (int n = k + 1; n < kM; ++n) acc[n] = fma(c_B0[n * kM + k + 1], ((n - k - 1) & 1) ? zm1 : zp1, acc[n]);
   }
 #pragma unroll
   for (int n = 0; n < kM; n += 2) *reinterpret_cast<double2*>(out + n) = make_double2(acc[n], acc[n + 1]);
 }
 
-// Step 4: dst += B(p)^T src with (B(p)^T c)_k = sum_{n>=k} b_nk (-1)^{p(n-k)} c_n
-// = (-1)^{pk} sum_n b_nk c'_n, c'_n = (-1)^{pn} c_n ("faster downward spreading",
-// B(1) differs from B(0) only in the sign of the odd diagonals).
-__device__ __forceinline__ void l2l18(const double* __restrict__ src, int p, double* __restrict__ dst) {
-  double acc[kM];
-#pragma unroll
-  for (int k = 0; k < kM; ++k) acc[k] = 0.0;
-#pragma unroll
-  for (int n = 0; n < kM; ++n) {
-    double cn = src[n];
-    if ((n & 1) && p) cn = -cn;
-#pragma unroll
-    for (int k = 0; k <= n; ++k) acc[k] = fma(c_B0[n * kM + k], cn, acc[k]);
-  }
-#pragma unroll
-  for (int k = 0; k < kM; ++k) dst[k] += ((k & 1) && p) ? -acc[k] : acc[k];
-}
-
-// Warp-level transfer operators: lane l < 18 owns output mode l and keeps its row (M2M) or
-// column (L2L) of B(0) in registers; the input vector is read from shared memory by all lanes
-// at once (broadcast), so one warp applies one 18 x 18 triangular operator in ~36 instructions.
-struct BRow {  // brow[k] = b_{l k} (k <= l), 0 otherwise
-  double v[kM];
-};
+// Warp-level step 4: lane l < 18 owns output mode l and keeps its column of B(0) in
+// registers; the input vector is read from shared memory by all lanes at once (broadcast).
 struct BCol {  // bcol[n] = b_{n l} (n >= l), 0 otherwise
   double v[kM];
 };
-__device__ __forceinline__ void load_brow(BRow& r, const double* __restrict__ B, int l) {
+__device__ __forceinline__ void load_bcol(BCol& c, int l) {
 #pragma unroll
-  for (int k = 0; k < kM; ++k) r.v[k] = (l < kM && k <= l) ? __ldg(B + l * kM + k) : 0.0;
+  for (int n = 0; n < kM; ++n) c.v[n] = (l < kM && n >= l) ? c_B0[n * kM + (l < kM ? l : 0)] : 0.0;
 }
-__device__ __forceinline__ void load_bcol(BCol& c, const double* __restrict__ B, int l) {
-#pragma unroll
-  for (int n = 0; n < kM; ++n) c.v[n] = (l < kM && n >= l) ? __ldg(B + n * kM + l) : 0.0;
-}
-// Alg. a.1: parent_l = sum_k b_lk x0_k + (-1)^l sum_k b_lk (-1)^k x1_k   (lane l; returns for l < 18)
-__device__ __forceinline__ double m2m_warp(const BRow& r, const double* __restrict__ x0,
-                                           const double* __restrict__ x1, int l) {
-  double a0 = 0.0, a1 = 0.0;
-#pragma unroll
-  for (int k = 0; k < kM; ++k) {
-    a0 = fma(r.v[k], x0[k], a0);
-    a1 = fma(r.v[k], (k & 1) ? -x1[k] : x1[k], a1);
-  }
-  return (l & 1) ? a0 - a1 : a0 + a1;
-}
-// Step 4: (B(p)^T c)_l = (-1)^{pl} sum_n b_nl (-1)^{pn} c_n   (lane l)
+// (B(p)^T c)_l = (-1)^{pl} sum_n b_nl (-1)^{pn} c_n   (lane l)
 __device__ __forceinline__ double l2l_warp(const BCol& cb, const double* __restrict__ c, int p, int l) {
   double a0 = 0.0, a1 = 0.0;
 #pragma unroll
   for (int n = 0; n < kM; n += 2) {
-    a0 = fma(cb.v[n], c[n], a0);
-    a1 = fma(cb.v[n + 1], c[n + 1], a1);
+    const double2 c2 = *reinterpret_cast<const double2*>(c + n);
+    a0 = fma(cb.v[n], c2.x, a0);
+    a1 = fma(cb.v[n + 1], c2.y, a1);
   }
-  // even n keep their sign; odd n flip when p = 1; then the lane sign (-1)^{pl}
   const double r = p ? a0 - a1 : a0 + a1;
   return (p && (l & 1)) ? -r : r;
 }
@@ -214,17 +185,21 @@ __device__ __forceinline__ double l2l_warp(const BCol& cb, const double* __restr
 // ---------------------------------------------------------------- parameters
 // flags (workspace ints): [0] up main-phase arrivals, [1] fine levels of w ready,
 // [2] finished level-0 continuations, [3] coarse levels of w ready, [4] finished
-// streaming CTAs, [5] predecessor complete (input readable).  Self-resetting.
+// streaming CTAs, [5] predecessor complete (input readable), [8] execution epoch.
 struct UpParams {
   const double* in;
+  const double* Tpad;  // [2][SMAX][M], zero rows m >= s
+  const double* B;     // B(0) [M][M]
   int64_t ld_in, n, N, batch;
-  int layout, L, s, k, gr, G;
-  const double* T;  // [2][s][M]
-  const double* B;  // B(0) [M][M]
+  int layout, L, s, k, gr, G, fstride, vec16;
   double* w;
   int* cnt;
   int* flags;
   int64_t w_tile, cnt_tile;
+};
+template <int SMAX>
+struct UpArgs {
+  UpParams p;
 };
 
 struct StreamParams {
@@ -240,66 +215,144 @@ struct StreamParams {
   int64_t ld_in, ld_out, n, N, batch;
   int64_t ntiles, nm2l, nband;
   int layout, L, s, cb, nst, kb, gr_up;
+  int lvorder[32];  // M2L level order: position o -> level
 };
+using StreamArgs = StreamParams;
 
 struct DownParams {
   double* out;
-  int64_t ld_out, n, N, batch;
-  int layout, L, s, k, gr;
-  const double* Tt;  // [2][M][s]
-  const double* B;   // B(0) [M][M]
-  const double* c;   // c_m2l
-  int64_t w_tile;
+  const double* c;     // c_m2l
+  const double* Tpad;  // [2][SMAX][M], zero rows m >= s
+  int64_t ld_out, n, N, batch, w_tile;
+  int layout, L, s, k;
 };
 
 // ============================================================== up kernel
-// one tree level in shared memory ([sigma][node][v][M]); item = (sigma, parent, v) handled by
-// one warp (lane = output mode); nparent = 2^lp
+// Alg. a.1, rows [R0, R1) of one parent:
+// parent[n] = sum_{k<=n} b_nk (x0_k + (-1)^(n-k) x1_k)   (B(1) = B(0) with the odd diagonals
+// negated, App. A3).  The children are loaded into registers first (sum/difference formed
+// once), B(0) is a uniform constant-bank operand (the row group is warp-uniform), and every row
+// keeps two partial sums (even / odd k) to halve its dependent DFMA chain.
+template <int R0, int R1>
+__device__ __forceinline__ void m2m_rows(const double* __restrict__ x0, const double* __restrict__ x1,
+                                         double* __restrict__ out) {
+  constexpr int NR = R1 - R0;
+  double zp[R1], zm[R1];
+#pragma unroll
+  for (int k = 0; k < R1; k += 2) {
+    const double2 a2 = *reinterpret_cast<const double2*>(x0 + k);
+    const double2 b2 = *reinterpret_cast<const double2*>(x1 + k);
+    zp[k] = a2.x + b2.x;
+    zm[k] = a2.x - b2.x;
+    if (k + 1 < R1) {
+      zp[k + 1] = a2.y + b2.y;
+      zm[k + 1] = a2.y - b2.y;
+    }
+  }
+  double acc[NR];
+#pragma unroll
+  for (int n = R0; n < R1; ++n) {
+    double ae = 0.0, ao = 0.0;
+#pragma unroll
+    for (int k = 0; k <= n; k += 2) ae = fma(c_B0[n * kM + k], ((n - k) & 1) ? zm[k] : zp[k], ae);
+#pragma unroll
+    for (int k = 1; k <= n; k += 2) ao = fma(c_B0[n * kM + k], ((n - k) & 1) ? zm[k] : zp[k], ao);
+    acc[n - R0] = ae + ao;
+  }
+#pragma unroll
+  for (int i = 0; i < NR; ++i) out[R0 + i] = acc[i];
+}
+
+// one tree level in shared memory ([sigma][node][v][M]); one thread per (row group, sigma,
+// parent, v), each warp on a single row group: [0,10), [10,15), [15,18) carry 55, 65 and 51
+// DFMA.  Six of the eight warps work; a level is one round for up to 64 (sigma, parent, v).
 template <int VT>
-__device__ __forceinline__ void m2m_level(const double* __restrict__ ch, double* __restrict__ pa, int lp,
-                                          const BRow& br) {
-  const int nparent = 1 << lp;
-  const int items = 2 * nparent * VT;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-  for (int it = warp; it < items; it += nwarps) {
-    const int v = it % VT;
-    const int sp = it / VT;
-    const int P = sp & (nparent - 1);
+__device__ __forceinline__ void m2m_level(const double* __restrict__ ch, double* __restrict__ pa, int lp) {
+  const int np = 1 << lp;
+  const int per = 2 * np * VT;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wpr = (blockDim.x >> 5) / 3;  // warps per row group
+  if (warp >= 3 * wpr) return;
+  const int rg = warp % 3;
+  for (int r = (warp / 3) * 32 + lane; r < per; r += wpr * 32) {
+    const int v = r % VT;
+    const int sp = r / VT;
+    const int P = sp & (np - 1);
     const int sg = sp >> lp;
-    const double* x0 = ch + ((sg * 2 * nparent + 2 * P) * VT + v) * kM;
-    const double r = m2m_warp(br, x0, x0 + VT * kM, lane);
-    if (lane < kM) pa[it * kM + lane] = r;
+    const double* x0 = ch + ((sg * 2 * np + 2 * P) * VT + v) * kM;
+    double* o = pa + r * kM;
+    if (rg == 0)
+      m2m_rows<0, 10>(x0, x0 + VT * kM, o);
+    else if (rg == 1)
+      m2m_rows<10, 15>(x0, x0 + VT * kM, o);
+    else
+      m2m_rows<15, 18>(x0, x0 + VT * kM, o);
   }
 }
 
-template <int VT>
-__global__ void __launch_bounds__(kThreads, 2) lc_up_kernel(const UpParams P) {
+// step 1 for one (leaf, 6 modes 6KG..6KG+5), both parities: the f pair (f_2m, f_2m+1) is one
+// 16-byte shared load, T(sigma)[m][6KG..] three 16-byte broadcast loads per parity.
+// Rows m >= s of the staged T are zero: the loop runs to SMAX without a branch (the f reads
+// beyond the segment stay inside the zero-padded shared tile).
+template <int SMAX, int KG>
+__device__ __forceinline__ void step1_item(const double* __restrict__ Ts, const double* __restrict__ fp,
+                                           double* __restrict__ o0, double* __restrict__ o1) {
+  double a[6], b[6];
+#pragma unroll
+  for (int i = 0; i < 6; ++i) a[i] = b[i] = 0.0;
+#pragma unroll 8
+  for (int m = 0; m < SMAX; ++m) {
+    const double2 f2 = *reinterpret_cast<const double2*>(fp + 2 * m);
+    const double* t0 = Ts + m * kM + 6 * KG;
+    const double* t1 = Ts + (SMAX + m) * kM + 6 * KG;
+#pragma unroll
+    for (int i = 0; i < 6; i += 2) {
+      const double2 u0 = *reinterpret_cast<const double2*>(t0 + i);
+      const double2 u1 = *reinterpret_cast<const double2*>(t1 + i);
+      a[i] = fma(f2.x, u0.x, a[i]);
+      a[i + 1] = fma(f2.x, u0.y, a[i + 1]);
+      b[i] = fma(f2.y, u1.x, b[i]);
+      b[i + 1] = fma(f2.y, u1.y, b[i + 1]);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 6; i += 2) {
+    *reinterpret_cast<double2*>(o0 + 6 * KG + i) = make_double2(a[i], a[i + 1]);
+    *reinterpret_cast<double2*>(o1 + 6 * KG + i) = make_double2(b[i], b[i + 1]);
+  }
+}
+
+template <int VT, int SMAX>
+__global__ void __launch_bounds__(kThreads, 2) lc_up_kernel(const __grid_constant__ UpArgs<SMAX> A) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ int s_last;
-  const int s = P.s, k = P.k;
+  const UpParams& P = A.p;
+  const int s = P.s, k = P.k, fst = P.fstride;
   const int tid = threadIdx.x;
-  double* Ts = reinterpret_cast<double*>(smem);
-  double* fs = reinterpret_cast<double*>(smem + align_up(int64_t(2) * s * kM * 8, 128));
   const int nleaf = 1 << k;
   const int seglen = 2 * s;
   const int tlen = nleaf * seglen;
-  double* tree = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(fs) + align_up(int64_t(VT) * tlen * 8, 128));
+  double* Ts = reinterpret_cast<double*>(smem);          // [2][SMAX][M], zero rows m >= s
+  double* Bs = Ts + 2 * SMAX * kM;                       // B(0) [M][M]
+  double* fs = reinterpret_cast<double*>(smem + kUpConstBytes);  // [v][leaf][fstride]
+  double* tree = reinterpret_cast<double*>(smem + kUpConstBytes + align_up((int64_t(VT) * nleaf * fst + 2 * SMAX) * 8, 128));
   auto tree_off = [&](int j) { return ((1 << j) - 1) * 2 * VT * kM; };
 
   const int64_t R = blockIdx.x;
   const int64_t tile = blockIdx.y;
   LC_TS(0, 0);
-  BRow br;
-  load_brow(br, P.B, tid & 31);
-  for (int i = tid; i < s * kM; i += blockDim.x) cp_async16(Ts + 2 * i, P.T + 2 * i);
+  // plan constants into shared memory (broadcast operands of steps 1 and 2)
+  for (int i = tid; i < SMAX * kM; i += blockDim.x) cp_async16(Ts + 2 * i, P.Tpad + 2 * i);
+  for (int i = tid; i < kMM / 2; i += blockDim.x) cp_async16(Bs + 2 * i, P.B + 2 * i);
   cp_async_commit();
-  griddep_wait();  // the input may be produced by the preceding kernel
+  griddep_wait();  // the input may be produced by the preceding kernel; w/c of the previous execution are free
   // Trigger the dependent (streaming) launch only now: every streaming CTA then starts after the
   // whole previous execution completed, so it can never observe flags of that execution.
   griddep_launch();
-  if (tid == 0) st_release(&P.flags[5], 1);  // predecessor complete: the streaming kernel may read the input
+  if (tid == 0 && R == 0 && tile == 0) st_release(&P.flags[5], 1);  // the streaming kernel may read the input
 
-  // stage the leaf range [R 2^k, (R+1) 2^k) of segments, zero padding beyond n
+  // stage the leaf range [R 2^k, (R+1) 2^k) of segments, zero padding beyond n;
+  // segment stride fstride = 2s or 2s+2 (= 2 mod 4 doubles: conflict-free 16-byte reads below)
   const int64_t j0 = R * tlen;
   if (P.layout == LC_VEC_CONTIGUOUS) {
 #pragma unroll 1
@@ -307,9 +360,21 @@ __global__ void __launch_bounds__(kThreads, 2) lc_up_kernel(const UpParams P) {
       const int64_t gv = tile * VT + v;
       const double* src = P.in + gv * P.ld_in + j0;
       const int64_t lim = gv < P.batch ? P.n - j0 : 0;  // valid elements of this vector in the tile
-      for (int jj = tid; jj < tlen; jj += blockDim.x) {
-        const bool ok = jj < lim;
-        cp_async8(fs + v * tlen + jj, ok ? src + jj : P.in, ok ? 8u : 0u);
+      if (P.vec16) {
+        const int npair = tlen / 2;
+        for (int q = tid; q < npair; q += blockDim.x) {
+          const int jj = 2 * q;
+          const int lf = jj / seglen, x = jj - lf * seglen;
+          const int64_t rem = lim - jj;
+          const uint32_t bytes = rem >= 2 ? 16u : (rem == 1 ? 8u : 0u);
+          cp_async16z(fs + (v * nleaf + lf) * fst + x, bytes ? src + jj : P.in, bytes);
+        }
+      } else {
+        for (int jj = tid; jj < tlen; jj += blockDim.x) {
+          const int lf = jj / seglen, x = jj - lf * seglen;
+          const bool ok = jj < lim;
+          cp_async8(fs + (v * nleaf + lf) * fst + x, ok ? src + jj : P.in, ok ? 8u : 0u);
+        }
       }
     }
   } else {
@@ -317,50 +382,44 @@ __global__ void __launch_bounds__(kThreads, 2) lc_up_kernel(const UpParams P) {
       const int jj = idx / VT, v = idx - jj * VT;  // v fastest: coalesced in the batch layout
       const int64_t gv = tile * VT + v, j = j0 + jj;
       const bool ok = gv < P.batch && j < P.n;
-      cp_async8(fs + v * tlen + jj, ok ? P.in + j * P.ld_in + gv : P.in, ok ? 8u : 0u);
+      const int lf = jj / seglen, x = jj - lf * seglen;
+      cp_async8(fs + (v * nleaf + lf) * fst + x, ok ? P.in + j * P.ld_in + gv : P.in, ok ? 8u : 0u);
     }
   }
+  // zero tail read by the branch-free step 1 of the last leaf (m up to SMAX-1)
+  for (int x = tid; x < 2 * SMAX; x += blockDim.x) fs[VT * nleaf * fst + x] = 0.0;
+  if (fst > seglen)  // and the segment padding (fstride = 2s + 2 for even s)
+    for (int x = tid; x < VT * nleaf; x += blockDim.x) *reinterpret_cast<double2*>(fs + x * fst + seglen) = make_double2(0.0, 0.0);
   cp_async_commit();
   cp_async_wait<0>();
   __syncthreads();
   LC_TS(0, 1);
 
   // step 1: w(L-1)[t][k] = sum_m f[2s t + 2m + sigma] T(sigma)[m][k]   (eq:wMM)
-  // item = (v, seg, sigma, group of 6 modes); 3 lanes share each f value.
+  // item = (mode group kg of 6, v, leaf); a warp shares kg whenever VT * nleaf >= 32.
   {
     double* leaf = tree + tree_off(k);
-    const int items = nleaf * 2 * VT * 3;
-    for (int it = tid; it < items; it += blockDim.x) {
-      const int kg = it % 3;
-      int r = it / 3;
-      const int sg = r & 1;
-      r >>= 1;
-      const int seg = r & (nleaf - 1);
-      const int v = r >> k;
-      const double* fp = fs + v * tlen + seg * seglen + sg;
-      const double* tp = Ts + sg * s * kM + 6 * kg;
-      double a0 = 0, a1 = 0, a2 = 0, a3 = 0, a4 = 0, a5 = 0;
-#pragma unroll 4
-      for (int m = 0; m < s; ++m) {
-        const double f = fp[2 * m];
-        const double2 t01 = *reinterpret_cast<const double2*>(tp + m * kM);
-        const double2 t23 = *reinterpret_cast<const double2*>(tp + m * kM + 2);
-        const double2 t45 = *reinterpret_cast<const double2*>(tp + m * kM + 4);
-        a0 = fma(f, t01.x, a0); a1 = fma(f, t01.y, a1);
-        a2 = fma(f, t23.x, a2); a3 = fma(f, t23.y, a3);
-        a4 = fma(f, t45.x, a4); a5 = fma(f, t45.y, a5);
-      }
-      double* o = leaf + ((sg * nleaf + seg) * VT + v) * kM + 6 * kg;
-      *reinterpret_cast<double2*>(o) = make_double2(a0, a1);
-      *reinterpret_cast<double2*>(o + 2) = make_double2(a2, a3);
-      *reinterpret_cast<double2*>(o + 4) = make_double2(a4, a5);
+    const int per = VT * nleaf;
+    for (int it = tid; it < 3 * per; it += blockDim.x) {
+      const int kg = it / per;
+      const int r = it - kg * per;
+      const int v = r / nleaf, lf = r - v * nleaf;
+      const double* fp = fs + (v * nleaf + lf) * fst;
+      double* o0 = leaf + (lf * VT + v) * kM;
+      double* o1 = leaf + ((nleaf + lf) * VT + v) * kM;
+      if (kg == 0)
+        step1_item<SMAX, 0>(Ts, fp, o0, o1);
+      else if (kg == 1)
+        step1_item<SMAX, 1>(Ts, fp, o0, o1);
+      else
+        step1_item<SMAX, 2>(Ts, fp, o0, o1);
     }
   }
   __syncthreads();
   LC_TS(0, 2);
   // step 2 inside the subtree
   for (int j = k; j >= 1; --j) {
-    m2m_level<VT>(tree + tree_off(j), tree + tree_off(j - 1), j - 1, br);
+    m2m_level<VT>(tree + tree_off(j), tree + tree_off(j - 1), j - 1);
     __syncthreads();
   }
   LC_TS(0, 3);
@@ -420,7 +479,7 @@ __global__ void __launch_bounds__(kThreads, 2) lc_up_kernel(const UpParams P) {
     }
     __syncthreads();
     for (int j = ge; j >= 1; --j) {
-      m2m_level<VT>(tree + tree_off(j), tree + tree_off(j - 1), j - 1, br);
+      m2m_level<VT>(tree + tree_off(j), tree + tree_off(j - 1), j - 1);
       __syncthreads();
     }
     for (int j = 0; j < ge; ++j) {
@@ -451,17 +510,23 @@ __global__ void __launch_bounds__(kThreads, 2) lc_up_kernel(const UpParams P) {
   LC_TS(0, 7);
 }
 
+
 // ============================================================== streaming kernel
-constexpr int kM2lWarps = 4;   // consumer warps applying M2L to the A_hat ring
-constexpr int kBandWarps = 4;  // consumer warps computing the direct band (independent pipeline)
+constexpr int kM2lWarps = 3;   // consumer warps applying M2L to the A_hat ring
+constexpr int kBandWarps = 4;  // band + down warps (independent pipeline)
 constexpr int kStreamThreads = 32 * (1 + kM2lWarps + kBandWarps);
 constexpr int kBandThreads = 32 * kBandWarps;
+constexpr int kM2lThreads = 32 * kM2lWarps;
+constexpr int kMaxChain = 24;  // ancestor levels above a down unit's subtree (n up to ~4e9)
 
-// M2L unit q (< nm2l) = (chunk, tile): chunk = (level g, blocks [b0, b0+nb)), nb <= cb, the
-// finest level first; tiles innermost so concurrent CTAs share A_hat in L2.
-// cstart[o] = first chunk of level L-1-o (shared-memory table, 32-bit arithmetic only).
-__device__ __forceinline__ void m2l_unit(int q, int ntiles, int L, int cb, const int* cstart, int& g, int& b0,
-                                         int& nb, int& tile) {
+__device__ __forceinline__ void band_sync() { named_sync(1, kBandThreads); }
+__device__ __forceinline__ void m2l_sync() { named_sync(2, kM2lThreads); }
+
+// M2L unit q (< nm2l) = (chunk, tile): chunk = (level g, blocks [b0, b0+nb)), nb <= cb, levels in
+// the order lvorder[]; tiles innermost so concurrent CTAs share A_hat in L2.
+// cstart[o] = first chunk of the o-th level of the order (shared-memory table).
+__device__ __forceinline__ void m2l_unit(int q, int ntiles, int L, int cb, const int* cstart, const int* lvord,
+                                         int& g, int& b0, int& nb, int& tile) {
   int ch = q;
   tile = 0;
   if (ntiles > 1) {
@@ -470,18 +535,142 @@ __device__ __forceinline__ void m2l_unit(int q, int ntiles, int L, int cb, const
   }
   int o = 0;
   while (o + 1 < L && cstart[o + 1] <= ch) ++o;
-  g = L - 1 - o;
+  g = lvord[o];
   b0 = (ch - cstart[o]) * cb;
   const int bg = (2 << g) - 1;
   nb = (bg - b0) < cb ? (bg - b0) : cb;
 }
 
-// Work units of the CTA: u = blockIdx.x + i * gridDim.x over [0, nband + nm2l); units below
-// nband are band units (leaf range of 2^kb segments x vector tile), the rest M2L units.
+// ---------------------------------------------------------------- band unit (step 6)
+// rows of 2^kb leaf segments x one vector tile; result (without C^{-1}) stored to out,
+// where the down unit of the same rows (same CTA, later) picks it up.
 template <int VT, int DIR>
-__global__ void __launch_bounds__(kStreamThreads, 2) lc_stream_kernel(const StreamParams P) {
+__device__ __forceinline__ void band_unit(const StreamParams& P, int tile, int lr, double* ta, double* tb, double* gt,
+                                          double* zst, int tp, int btid) {
+  const int s = P.s, kb = P.kb;
+  const int nleaf = 1 << kb;
+  const int seglen = 2 * s;
+  const int64_t U0 = int64_t(lr) << kb;
+  const int64_t i0 = U0 * seglen;
+  const int rows = nleaf * seglen;
+  const int tcols = (nleaf + 2) * seglen;
+  const int tbl = int((P.N - i0) < tcols ? (P.N - i0) : tcols);  // valid band-table entries
+  for (int x = btid; x < tcols + 2 * kBandR; x += kBandThreads) {
+    const bool ok = x < tbl;
+    cp_async8(tb + x + (x >> 4), ok ? P.tabB + i0 + x : P.tabB, ok ? 8u : 0u);
+  }
+#pragma unroll 1
+  for (int v = 0; v < VT; ++v) {
+    const int64_t gv = int64_t(tile) * VT + v;
+    int lim = 0;  // valid input elements of this vector in the tile
+    if (gv < P.batch) lim = int((P.n - i0) < tcols ? (P.n - i0) : tcols);
+    if (lim < 0) lim = 0;
+    if (P.layout == LC_VEC_CONTIGUOUS) {
+      const double* src = P.in + gv * P.ld_in + i0;
+      for (int x = btid; x < tcols + 2 * kBandR; x += kBandThreads) {
+        const bool ok = x < lim;
+        cp_async8(gt + v * tp + x + (x >> 4), ok ? src + x : P.in, ok ? 8u : 0u);
+      }
+    } else {
+      for (int x = btid; x < tcols + 2 * kBandR; x += kBandThreads) {
+        const bool ok = x < lim;
+        cp_async8(gt + v * tp + x + (x >> 4), ok ? P.in + (i0 + x) * P.ld_in + gv : P.in, ok ? 8u : 0u);
+      }
+    }
+  }
+  cp_async_commit();
+  cp_async_wait<0>();
+  band_sync();
+  // item = (v, segment uu, parity sigma, block of kBandR same-parity rows m = kBandR t + r).
+  // Band of row i' = i + 2r (i the block's first row): sum_c a[c-r] b[i+r+c] g[i+2c], c >= r,
+  // i + 2c < j_end; a = tabA, b = tabB, g = f (L2C) or j f_j (C2L).  Sliding windows of a and
+  // b live in registers (slots rotate with c): each step loads 3 values for kBandR rows.
+  const int ntb = (s + kBandR - 1) / kBandR;
+  const int items = VT * nleaf * 2 * ntb;
+  for (int it = btid; it < items; it += kBandThreads) {
+    const int tb_i = it % ntb;
+    int r_ = it / ntb;
+    const int sg = r_ & 1;
+    r_ >>= 1;
+    const int uu = r_ & (nleaf - 1);
+    const int v = r_ >> kb;
+    const int m0 = kBandR * tb_i;
+    const int ii = uu * seglen + sg + 2 * m0;  // tile-local first row
+    const int64_t i = i0 + ii;
+    const int64_t je = (int64_t(seglen) * (U0 + uu + 2)) < P.N ? int64_t(seglen) * (U0 + uu + 2) : P.N;
+    const int cmax = int((je - i - 1) >> 1);
+    const double* gv_t = gt + v * tp;
+    double acc[kBandR], aw[kBandR], bw[kBandR];
+#pragma unroll
+    for (int r = 0; r < kBandR; ++r) {
+      acc[r] = 0.0;
+      aw[r] = 0.0;
+      bw[r] = tb[(ii + r) + ((ii + r) >> 4)];
+    }
+    const int ngrp = (cmax + 1) / kBandR;
+    int c0 = 0;
+    for (int gi = 0; gi < ngrp; ++gi, c0 += kBandR) {
+#pragma unroll
+      for (int q = 0; q < kBandR; ++q) {
+        const int c = c0 + q;
+        aw[q] = ta[c];
+        const int xb = ii + kBandR - 1 + c, xg = ii + 2 * c;
+        bw[(q + kBandR - 1) % kBandR] = tb[xb + (xb >> 4)];
+        double gval = gv_t[xg + (xg >> 4)];
+        if (DIR == 1) gval *= double(i + 2 * c);
+#pragma unroll
+        for (int r = 0; r < kBandR; ++r) acc[r] = fma(aw[(q - r + kBandR) % kBandR] * bw[(r + q) % kBandR], gval, acc[r]);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < kBandR; ++q) {  // remainder: c = c0 + q <= cmax
+      const int c = c0 + q;
+      if (c <= cmax) {
+        aw[q] = ta[c];
+        const int xb = ii + kBandR - 1 + c, xg = ii + 2 * c;
+        bw[(q + kBandR - 1) % kBandR] = tb[xb + (xb >> 4)];
+        double gval = gv_t[xg + (xg >> 4)];
+        if (DIR == 1) gval *= double(i + 2 * c);
+#pragma unroll
+        for (int r = 0; r < kBandR; ++r) acc[r] = fma(aw[(q - r + kBandR) % kBandR] * bw[(r + q) % kBandR], gval, acc[r]);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < kBandR; ++r) {
+      if (m0 + r < s) {
+        const int64_t ir = i + 2 * r;
+        double z = acc[r];
+        if (DIR == 1) {
+          z *= double(2 * ir + 1);
+          if (ir == 0) z += gv_t[0];  // entry (0,0) of A^{-1}C is 1 (reading R2)
+        }
+        zst[v * rows + ii + 2 * r] = z;
+      }
+    }
+  }
+  band_sync();
+  // coalesced store of the band result (steps 4, 5 and 7 are added by the down unit)
+  const int olim = int((P.n - i0) < rows ? (P.n - i0) : rows);
+#pragma unroll 1
+  for (int v = 0; v < VT; ++v) {
+    const int64_t gv = int64_t(tile) * VT + v;
+    if (gv >= P.batch) break;
+    if (P.layout == LC_VEC_CONTIGUOUS) {
+      double* dst = P.out + gv * P.ld_out + i0;
+      for (int x = btid; x < olim; x += kBandThreads) dst[x] = zst[v * rows + x];
+    } else {
+      for (int x = btid; x < olim; x += kBandThreads) P.out[(i0 + x) * P.ld_out + gv] = zst[v * rows + x];
+    }
+  }
+  band_sync();  // tiles are reused by the next unit
+}
+
+template <int VT, int DIR>
+__global__ void __launch_bounds__(kStreamThreads, 2) lc_stream_kernel(const __grid_constant__ StreamArgs A) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ int cstart[32];
+  __shared__ int s_last;
+  const StreamParams& P = A;
   const int tid = threadIdx.x;
   const int s = P.s, cb = P.cb, nst = P.nst, kb = P.kb;
   const int64_t VM = int64_t(VT) * kM;
@@ -489,20 +678,14 @@ __global__ void __launch_bounds__(kStreamThreads, 2) lc_stream_kernel(const Stre
   const int64_t a_bytes = align_up(int64_t(cb) * 3 * kMM * 8, 128);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + SL.bars);
   uint64_t* empty = full + nst;
-  double* ta = reinterpret_cast<double*>(smem + SL.ta);
-  double* tb = reinterpret_cast<double*>(smem + SL.tb);
-  double* gt = reinterpret_cast<double*>(smem + SL.gt);
-  double* zst = reinterpret_cast<double*>(smem + SL.zst);
   const int tp = int(SL.tp);
 
   const int nband = int(P.nband), nm2l = int(P.nm2l);
-  const int nunits = nband + nm2l;
-  const int nmine = nunits > int(blockIdx.x) ? (nunits - int(blockIdx.x) + int(gridDim.x) - 1) / int(gridDim.x) : 0;
   if (tid == 0) {
     int acc = 0;
     for (int o = 0; o < P.L && o < 32; ++o) {
       cstart[o] = acc;
-      const int g = P.L - 1 - o;
+      const int g = P.lvorder[o];
       acc += ((2 << g) - 1 + cb - 1) / cb;
     }
     for (int i = 0; i < nst; ++i) {
@@ -523,7 +706,7 @@ __global__ void __launch_bounds__(kStreamThreads, 2) lc_stream_kernel(const Stre
       bool fine_ok = false, coarse_ok = false;
       auto issue = [&](int q, int j, bool with_a, bool with_w) {  // M2L unit q, ring use j
         int g, nb, b0, tile;
-        m2l_unit(q, ntiles, P.L, cb, cstart, g, b0, nb, tile);
+        m2l_unit(q, ntiles, P.L, cb, cstart, P.lvorder, g, b0, nb, tile);
         const int slot = j % nst;
         unsigned char* base = smem + SL.ring + slot * SL.slot;
         const uint32_t abytes = uint32_t(nb) * 3 * kMM * 8;
@@ -538,7 +721,6 @@ __global__ void __launch_bounds__(kStreamThreads, 2) lc_stream_kernel(const Stre
           bool& ok = g >= P.gr_up ? fine_ok : coarse_ok;
           if (!ok) {
             wait_flag(&P.flags[g >= P.gr_up ? 1 : 3]);
-            LC_TS(1, g >= P.gr_up ? 4 : 5);
             asm volatile("fence.proxy.async.global;" ::: "memory");  // order the bulk reads after the acquire
             ok = true;
           }
@@ -550,300 +732,196 @@ __global__ void __launch_bounds__(kStreamThreads, 2) lc_stream_kernel(const Stre
         }
       };
       // the A_hat of the first nst M2L units is plan data: issue it before any dependency
-      int j = 0;
-      int firstq[8];
-      for (int i = 0; i < nmine && j < nst && j < 8; ++i) {
-        const int u = int(blockIdx.x) + i * int(gridDim.x);
-        if (u < nband) continue;
-        firstq[j] = u - nband;
-        issue(firstq[j], j, true, false);
-        ++j;
+      int npre = 0;
+      for (int q = int(blockIdx.x); q < nm2l && npre < nst; q += int(gridDim.x)) issue(q, npre++, true, false);
+      {
+        int jj = 0;
+        for (int q = int(blockIdx.x); q < nm2l && jj < npre; q += int(gridDim.x)) issue(q, jj++, false, true);
       }
-      const int npre = j;
-      for (int jj = 0; jj < npre; ++jj) issue(firstq[jj], jj, false, true);
-      j = 0;
-      for (int i = 0; i < nmine; ++i) {
-        const int u = int(blockIdx.x) + i * int(gridDim.x);
-        if (u < nband) continue;
-        if (j >= npre) {
-          mbar_wait(&empty[j % nst], uint32_t(((j / nst) - 1) & 1));
-          issue(u - nband, j, true, true);
-        }
-        ++j;
+      int j = 0;
+      for (int q = int(blockIdx.x); q < nm2l; q += int(gridDim.x), ++j) {
+        if (j < npre) continue;
+        mbar_wait(&empty[j % nst], uint32_t(((j / nst) - 1) & 1));
+        issue(q, j, true, true);
       }
     }
   } else if (tid < 32 * (1 + kM2lWarps)) {
     // ------------------------------------------------ M2L consumer warps
     const int ctid = tid - 32;
     int j = 0;  // M2L ring use counter
-    for (int i = 0; i < nmine; ++i) {
-      const int u = int(blockIdx.x) + i * int(gridDim.x);
-      if (u < nband) continue;
-      {
-        // ---------------- M2L unit: step 3 on a chunk of blocks of one level
-          int g, nb, b0, tile;
-          m2l_unit(u - nband, ntiles, P.L, cb, cstart, g, b0, nb, tile);
-          const int slot = j % nst;
-#ifdef LC_PHASE_TIMING
-          if (j == 0 && ctid == 0) lc_ts_any(1, 2);
-#endif
-          mbar_wait(&full[slot], uint32_t((j / nst) & 1));
-#ifdef LC_PHASE_TIMING
-          if (j == 0 && ctid == 0) lc_ts_any(1, 3);
-#endif
-          const double* As = reinterpret_cast<const double*>(smem + SL.ring + slot * SL.slot);
-          const double* wwin = reinterpret_cast<const double*>(smem + SL.ring + slot * SL.slot + a_bytes);
-          double* ct = P.c + int64_t(tile) * P.w_tile + (w_level_offset_units(g) + 2 * int64_t(b0)) * VM;
-          const int64_t sgstride = nseg(g) * VM;
-          const int nrows = 2 * nb;
-          for (int it = ctid; it < nrows * kM; it += 32 * kM2lWarps) {
-            const int ri = it / kM, kk = it % kM;  // row u = 2 b0 + ri
-            double acc[2][VT];
+    for (int q = int(blockIdx.x); q < nm2l; q += int(gridDim.x), ++j) {
+      int g, nb, b0, tile;
+      m2l_unit(q, ntiles, P.L, cb, cstart, P.lvorder, g, b0, nb, tile);
+      const int slot = j % nst;
+      mbar_wait(&full[slot], uint32_t((j / nst) & 1));
+      const double* As = reinterpret_cast<const double*>(smem + SL.ring + slot * SL.slot);
+      const double* wwin = reinterpret_cast<const double*>(smem + SL.ring + slot * SL.slot + a_bytes);
+      double* ct = P.c + int64_t(tile) * P.w_tile + (w_level_offset_units(g) + 2 * int64_t(b0)) * VM;
+      const int64_t sgstride = nseg(g) * VM;
+      const int nrows = 2 * nb;
+      for (int it = ctid; it < nrows * kM; it += kM2lThreads) {
+        const int ri = it / kM, kk = it % kM;  // row u = 2 b0 + ri
+        double acc[2][VT];
 #pragma unroll
-            for (int sg = 0; sg < 2; ++sg)
+        for (int sg = 0; sg < 2; ++sg)
 #pragma unroll
-              for (int v = 0; v < VT; ++v) acc[sg][v] = 0.0;
-            // even row (p=0): r=0 with column t=u+2 and r=1 with t=u+3; odd row (p=1): r=2 with t=u+2
-            const int nmat = (ri & 1) ? 1 : 2;
-            for (int mi = 0; mi < nmat; ++mi) {
-              const int r = (ri & 1) ? 2 : mi;
-              const int tloc = (ri & 1) ? ri : ri + mi;  // t - (2 b0 + 2)
-              const double* arow = As + (3 * (ri >> 1) + r) * kMM + kk * kM;
-              double ar[kM];
+          for (int v = 0; v < VT; ++v) acc[sg][v] = 0.0;
+        // even row (p=0): r=0 with column t=u+2 and r=1 with t=u+3; odd row (p=1): r=2 with t=u+2
+        const int nmat = (ri & 1) ? 1 : 2;
+        for (int mi = 0; mi < nmat; ++mi) {
+          const int r = (ri & 1) ? 2 : mi;
+          const int tloc = (ri & 1) ? ri : ri + mi;  // t - (2 b0 + 2)
+          const double* arow = As + (3 * (ri >> 1) + r) * kMM + kk * kM;
+          double ar[kM];
 #pragma unroll
-              for (int l = 0; l < kM; l += 2) {
-                const double2 t2 = *reinterpret_cast<const double2*>(arow + l);
-                ar[l] = t2.x;
-                ar[l + 1] = t2.y;
-              }
-#pragma unroll
-              for (int sg = 0; sg < 2; ++sg)
-#pragma unroll
-                for (int v = 0; v < VT; ++v) {
-                  const double* wp = wwin + (sg * 2 * cb + tloc) * VM + v * kM;
-                  double sacc = 0.0;
-#pragma unroll
-                  for (int l = 0; l < kM; ++l) sacc = fma(ar[l], wp[l], sacc);
-                  acc[sg][v] += sacc;
-                }
-            }
-#pragma unroll
-            for (int sg = 0; sg < 2; ++sg)
-#pragma unroll
-              for (int v = 0; v < VT; ++v) ct[sg * sgstride + ri * VM + v * kM + kk] = acc[sg][v];
+          for (int l = 0; l < kM; l += 2) {
+            const double2 t2 = *reinterpret_cast<const double2*>(arow + l);
+            ar[l] = t2.x;
+            ar[l + 1] = t2.y;
           }
-          __syncwarp();
-          if ((tid & 31) == 0) mbar_arrive(&empty[slot]);  // this warp is done with the slot
-        ++j;
+#pragma unroll
+          for (int sg = 0; sg < 2; ++sg)
+#pragma unroll
+            for (int v = 0; v < VT; ++v) {
+              const double* wp = wwin + (sg * 2 * cb + tloc) * VM + v * kM;
+              double sacc = 0.0;
+#pragma unroll
+              for (int l = 0; l < kM; ++l) sacc = fma(ar[l], wp[l], sacc);
+              acc[sg][v] += sacc;
+            }
+        }
+#pragma unroll
+        for (int sg = 0; sg < 2; ++sg)
+#pragma unroll
+          for (int v = 0; v < VT; ++v) ct[sg * sgstride + ri * VM + v * kM + kk] = acc[sg][v];
       }
+      __syncwarp();
+      if ((tid & 31) == 0) mbar_arrive(&empty[slot]);  // this warp is done with the slot
     }
   } else {
-    // ------------------------------------------------ band consumer warps
+    // ------------------------------------------------ band + down warps
     const int btid = tid - 32 * (1 + kM2lWarps);
-    bool input_ok = false;
+    double* ta = reinterpret_cast<double*>(smem + SL.ta);
+    double* tb = reinterpret_cast<double*>(smem + SL.tb);
+    double* gt = reinterpret_cast<double*>(smem + SL.gt);
+    double* zst = reinterpret_cast<double*>(smem + SL.zst);
     for (int x = btid; x < 2 * s + 2 * kBandR; x += kBandThreads) ta[x] = x < 2 * s ? P.tabA[x] : 0.0;
-    for (int i = 0; i < nmine; ++i) {
-      const int u = int(blockIdx.x) + i * int(gridDim.x);
-      if (u >= nband) continue;
-      {
-        // ---------------- band unit: step 6 for rows of 2^kb leaf segments of one vector tile
-        const int tile = ntiles > 1 ? u % ntiles : 0;
-        const int lr = ntiles > 1 ? u / ntiles : u;
-        if (!input_ok) {  // the input is readable once the predecessor of the up kernel completed
-          if (P.L > 0) {
-            if (btid == 0) wait_flag(&P.flags[5]);
-          } else {
-            griddep_wait();
-          }
-          consumer_sync(kBandThreads);
-          input_ok = true;
-        }
-        const int nleaf = 1 << kb;
-        const int seglen = 2 * s;
-        const int64_t U0 = int64_t(lr) << kb;
-        const int64_t i0 = U0 * seglen;
-        const int rows = nleaf * seglen;
-        const int tcols = (nleaf + 2) * seglen;
-        const int tbl = int((P.N - i0) < tcols ? (P.N - i0) : tcols);  // valid band-table entries
-        for (int x = btid; x < tcols + 2 * kBandR; x += kBandThreads) {
-          const bool ok = x < tbl;
-          cp_async8(tb + x + (x >> 4), ok ? P.tabB + i0 + x : P.tabB, ok ? 8u : 0u);
-        }
-#pragma unroll 1
-        for (int v = 0; v < VT; ++v) {
-          const int64_t gv = int64_t(tile) * VT + v;
-          int lim = 0;  // valid input elements of this vector in the tile
-          if (gv < P.batch) lim = int((P.n - i0) < tcols ? (P.n - i0) : tcols);
-          if (lim < 0) lim = 0;
-          if (P.layout == LC_VEC_CONTIGUOUS) {
-            const double* src = P.in + gv * P.ld_in + i0;
-            for (int x = btid; x < tcols + 2 * kBandR; x += kBandThreads) {
-              const bool ok = x < lim;
-              cp_async8(gt + v * tp + x + (x >> 4), ok ? src + x : P.in, ok ? 8u : 0u);
-            }
-          } else {
-            for (int x = btid; x < tcols + 2 * kBandR; x += kBandThreads) {
-              const bool ok = x < lim;
-              cp_async8(gt + v * tp + x + (x >> 4), ok ? P.in + (i0 + x) * P.ld_in + gv : P.in, ok ? 8u : 0u);
-            }
-          }
-        }
-        cp_async_commit();
-        cp_async_wait<0>();
-        consumer_sync(kBandThreads);
-        // item = (v, segment uu, parity sigma, block of kBandR same-parity rows m = kBandR t + r).
-        // Band of row i' = i + 2r (i the block's first row): sum_c a[c-r] b[i+r+c] g[i+2c], c >= r,
-        // i + 2c < j_end; a = tabA, b = tabB, g = f (L2C) or j f_j (C2L).  Sliding windows of a and
-        // b live in registers (slots rotate with c): each step loads 3 values for kBandR rows.
-        const int ntb = (s + kBandR - 1) / kBandR;
-        const int items = VT * nleaf * 2 * ntb;
-        for (int it = btid; it < items; it += kBandThreads) {
-          const int tb_i = it % ntb;
-          int r_ = it / ntb;
-          const int sg = r_ & 1;
-          r_ >>= 1;
-          const int uu = r_ & (nleaf - 1);
-          const int v = r_ >> kb;
-          const int m0 = kBandR * tb_i;
-          const int ii = uu * seglen + sg + 2 * m0;  // tile-local first row
-          const int64_t i = i0 + ii;
-          const int64_t je = (int64_t(seglen) * (U0 + uu + 2)) < P.N ? int64_t(seglen) * (U0 + uu + 2) : P.N;
-          const int cmax = int((je - i - 1) >> 1);
-          const double* gv_t = gt + v * tp;
-          double acc[kBandR], aw[kBandR], bw[kBandR];
-#pragma unroll
-          for (int r = 0; r < kBandR; ++r) {
-            acc[r] = 0.0;
-            aw[r] = 0.0;
-            bw[r] = tb[(ii + r) + ((ii + r) >> 4)];
-          }
-          // (re-loading b[ii+R-1] at c = 0 is harmless: it is the value already in that slot)
-          const int ngrp = (cmax + 1) / kBandR;
-          int c0 = 0;
-          for (int gi = 0; gi < ngrp; ++gi, c0 += kBandR) {
-#pragma unroll
-            for (int q = 0; q < kBandR; ++q) {
-              const int c = c0 + q;
-              aw[q] = ta[c];
-              const int xb = ii + kBandR - 1 + c, xg = ii + 2 * c;
-              bw[(q + kBandR - 1) % kBandR] = tb[xb + (xb >> 4)];
-              double gval = gv_t[xg + (xg >> 4)];
-              if (DIR == 1) gval *= double(i + 2 * c);
-#pragma unroll
-              for (int r = 0; r < kBandR; ++r)
-                acc[r] = fma(aw[(q - r + kBandR) % kBandR] * bw[(r + q) % kBandR], gval, acc[r]);
-            }
-          }
-#pragma unroll
-          for (int q = 0; q < kBandR; ++q) {  // remainder: c = c0 + q <= cmax
-            const int c = c0 + q;
-            if (c <= cmax) {
-              aw[q] = ta[c];
-              const int xb = ii + kBandR - 1 + c, xg = ii + 2 * c;
-              bw[(q + kBandR - 1) % kBandR] = tb[xb + (xb >> 4)];
-              double gval = gv_t[xg + (xg >> 4)];
-              if (DIR == 1) gval *= double(i + 2 * c);
-#pragma unroll
-              for (int r = 0; r < kBandR; ++r)
-                acc[r] = fma(aw[(q - r + kBandR) % kBandR] * bw[(r + q) % kBandR], gval, acc[r]);
-            }
-          }
-#pragma unroll
-          for (int r = 0; r < kBandR; ++r) {
-            if (m0 + r < s) {
-              const int64_t ir = i + 2 * r;
-              double z = acc[r];
-              if (DIR == 1) {
-                z *= double(2 * ir + 1);
-                if (ir == 0) z += gv_t[0];  // entry (0,0) of A^{-1}C is 1 (reading R2)
-              }
-              zst[v * rows + ii + 2 * r] = z;
-            }
-          }
-        }
-        consumer_sync(kBandThreads);
-        // coalesced store of the band result (step 5 and step 7 are added by the down kernel)
-        const int olim = int((P.n - i0) < rows ? (P.n - i0) : rows);
-#pragma unroll 1
-        for (int v = 0; v < VT; ++v) {
-          const int64_t gv = int64_t(tile) * VT + v;
-          if (gv >= P.batch) break;
-          if (P.layout == LC_VEC_CONTIGUOUS) {
-            double* dst = P.out + gv * P.ld_out + i0;
-            for (int x = btid; x < olim; x += kBandThreads) dst[x] = zst[v * rows + x];
-          } else {
-            for (int x = btid; x < olim; x += kBandThreads) P.out[(i0 + x) * P.ld_out + gv] = zst[v * rows + x];
-          }
-        }
-        consumer_sync(kBandThreads);  // tiles are reused by the next band unit
+    if (nband > int(blockIdx.x)) {  // the input is readable once the predecessor of the up kernel completed
+      if (P.L > 0) {
+        if (btid == 0) wait_flag(&P.flags[5]);
+      } else {
+        griddep_wait();
       }
     }
+    band_sync();
+    for (int u = int(blockIdx.x); u < nband; u += int(gridDim.x)) {
+      const int tile = ntiles > 1 ? u % ntiles : 0;
+      const int lr = ntiles > 1 ? u / ntiles : u;
+      band_unit<VT, DIR>(P, tile, lr, ta, tb, gt, zst, tp, btid);
+    }
+    LC_TS_T(1, 2);
   }
   __syncthreads();
   LC_TS(1, 1);
-  if (tid == 0) {  // the last CTA to finish re-arms the readiness flags for the next execution
-    if (atomicAdd(&P.flags[4], 1) == int(gridDim.x) - 1) {
+  if (tid == 0) s_last = atomicAdd(&P.flags[4], 1) == int(gridDim.x) - 1;
+  __syncthreads();
+  if (s_last) {  // the last CTA to finish re-arms the counters and flags for the next execution
+    __threadfence();
+    if (tid == 0) {
       P.flags[1] = 0;
       P.flags[3] = 0;
       P.flags[5] = 0;
-      __threadfence();
-      atomicExch(&P.flags[4], 0);
     }
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) atomicExch(&P.flags[4], 0);
   }
 }
 
 // ============================================================== down kernel
-// One CTA per (subtree of 2^k leaf row segments, tile of VT vectors):
-//   cp.async prefetch of T(sigma)^T, the band result z_band of the rows and the c_m2l of the
-//   ancestors and of the subtree nodes; step 4 along the ancestor chain (one thread per
-//   (sigma, v)) and down the subtree (one thread per node); step 5 + step 7; store.
-template <int VT, int DIR>
-__global__ void __launch_bounds__(kThreads, 2) lc_down_kernel(const DownParams P) {
-  extern __shared__ __align__(128) unsigned char smem[];
-  const int s = P.s, k = P.k, gr = P.gr, L = P.L;
-  const int tid = threadIdx.x;
-  const DownSmem SL = down_smem_layout(VT, k, s, gr);
-  double* Tt = reinterpret_cast<double*>(smem + SL.Tt);
-  double* zb = reinterpret_cast<double*>(smem + SL.zb);
-  double* cm = reinterpret_cast<double*>(smem + SL.cm);
+// One CTA (4 warps) per (subtree of 2^kd leaf row segments, tile of VT vectors):
+//   T(sigma) row m of the lane's parity in registers (plan data, before the dependency wait);
+//   one cp.async round trip for the c_m2l of the ancestors and of the whole subtree and the
+//   band result of the rows; step 4 along the ancestor chain (one warp per (sigma, v), lane =
+//   mode, B(0) column in registers) and down the subtree (two nodes per warp iteration);
+//   step 5 with lane = row m (z_m = sum_k T(sigma)[m][k] c_k, c broadcast from shared memory);
+//   step 7; coalesced store.
+constexpr int kDownThreads = 128;
 
+// two independent (B(p)^T c) applications per call: ILP across nodes
+__device__ __forceinline__ void l2l_warp2(const BCol& cb, const double* __restrict__ c0, int p0,
+                                          const double* __restrict__ c1, int p1, int l, double& r0, double& r1) {
+  double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+#pragma unroll
+  for (int n = 0; n < kM; n += 2) {
+    const double2 x = *reinterpret_cast<const double2*>(c0 + n);
+    const double2 y = *reinterpret_cast<const double2*>(c1 + n);
+    a0 = fma(cb.v[n], x.x, a0);
+    a1 = fma(cb.v[n + 1], x.y, a1);
+    b0 = fma(cb.v[n], y.x, b0);
+    b1 = fma(cb.v[n + 1], y.y, b1);
+  }
+  r0 = p0 ? a0 - a1 : a0 + a1;
+  if (p0 && (l & 1)) r0 = -r0;
+  r1 = p1 ? b0 - b1 : b0 + b1;
+  if (p1 && (l & 1)) r1 = -r1;
+}
+
+template <int VT, int DIR, int SMAX>
+__global__ void __launch_bounds__(kDownThreads, 4) lc_down_kernel(const DownParams P) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int s = P.s, kd = P.k, L = P.L;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int gd = L > 0 ? L - 1 - kd : 0;  // level of the subtree root
+  const int64_t VM = int64_t(VT) * kM;
+  const int nleaf = 1 << kd;
+  const int seglen = 2 * s;
   const int64_t R = blockIdx.x;
   const int64_t tile = blockIdx.y;
-  const int64_t VM = int64_t(VT) * kM;
-  const int nleaf = 1 << k;
-  const int seglen = 2 * s;
-  const int64_t U0 = R << k;
+  const int64_t U0 = R << kd;
   const int64_t i0 = U0 * seglen;
   const int rows = nleaf * seglen;
-  // cm layout: ancestors [g][sigma][v][M] (g < gr), then subtree level j at node offset
-  // gr + 2^j - 1: [sigma][node][v][M]
+  // shared memory: cm = ancestors [g][sigma][v][M] (g < gd), subtree level j at node offset
+  // gd + 2^j - 1 ([sigma][node][v][M]); zb = [v][rows]
+  double* cm = reinterpret_cast<double*>(smem);
+  double* zb = cm + (L > 0 ? (int64_t(gd) + (int64_t(2) << kd) - 1) * 2 * VM : 0);
   auto cm_anc = [&](int g) { return cm + int64_t(g) * 2 * VM; };
-  auto cm_lvl = [&](int j) { return cm + (int64_t(gr) + (1 << j) - 1) * 2 * VM; };
-
+  auto cm_lvl = [&](int j) { return cm + (int64_t(gd) + (1 << j) - 1) * 2 * VM; };
   LC_TS(2, 0);
-  for (int i = tid; i < s * kM; i += blockDim.x) cp_async16(Tt + 2 * i, P.Tt + 2 * i);  // plan data
-  cp_async_commit();
+  // plan data first: T(sigma)[m][.] of this warp's parity (sigma = warp & 1) and lane m
+  double trow[kM];
+  {
+    const int sg = warp & 1;
+    const double* tp = P.Tpad + (int64_t(sg) * SMAX + (lane < SMAX ? lane : 0)) * kM;
+#pragma unroll
+    for (int k = 0; k < kM; k += 2) {
+      const double2 t2 = __ldg(reinterpret_cast<const double2*>(tp + k));
+      trow[k] = t2.x;
+      trow[k + 1] = t2.y;
+    }
+  }
+  BCol bc;
+  load_bcol(bc, lane);
   griddep_launch();
   griddep_wait();  // c_m2l and the band result (streaming kernel) are ready past this point
   LC_TS(2, 1);
-
   const double* ct = P.c + tile * P.w_tile;
   if (L > 0) {
-    for (int g = 0; g < gr; ++g) {
-      const int64_t a = R >> (gr - g);
+    for (int g = 0; g < gd; ++g) {
+      const int64_t a = R >> (gd - g);
       for (int sg = 0; sg < 2; ++sg) {
         const double* src = ct + (w_level_offset_units(g) + sg * nseg(g) + a) * VM;
         double* dst = cm_anc(g) + sg * VM;
-        for (int i = tid; i < VM / 2; i += blockDim.x) cp_async16(dst + 2 * i, src + 2 * i);
+        for (int i = tid; i < VM / 2; i += kDownThreads) cp_async16(dst + 2 * i, src + 2 * i);
       }
     }
-    for (int j = 0; j <= k; ++j) {
-      const int g = gr + j;
+    for (int j = 0; j <= kd; ++j) {
+      const int g = gd + j;
       const int cnt2 = int((int64_t(1) << j) * VM / 2);
       for (int sg = 0; sg < 2; ++sg) {
         const double* src = ct + (w_level_offset_units(g) + sg * nseg(g) + (R << j)) * VM;
         double* dst = cm_lvl(j) + sg * (int64_t(1) << j) * VM;
-        for (int i = tid; i < cnt2; i += blockDim.x) cp_async16(dst + 2 * i, src + 2 * i);
+        for (int i = tid; i < cnt2; i += kDownThreads) cp_async16(dst + 2 * i, src + 2 * i);
       }
     }
   }
@@ -852,17 +930,10 @@ __global__ void __launch_bounds__(kThreads, 2) lc_down_kernel(const DownParams P
   for (int v = 0; v < VT; ++v) {
     const int64_t gv = tile * VT + v;
     const int lim = gv < P.batch ? olim : 0;
-    if (P.layout == LC_VEC_CONTIGUOUS) {
-      const double* src = P.out + gv * P.ld_out + i0;
-      for (int x = tid; x < rows; x += blockDim.x) {
-        const bool ok = x < lim;
-        cp_async8(zb + v * rows + x, ok ? src + x : P.out, ok ? 8u : 0u);
-      }
-    } else {
-      for (int x = tid; x < rows; x += blockDim.x) {
-        const bool ok = x < lim;
-        cp_async8(zb + v * rows + x, ok ? P.out + (i0 + x) * P.ld_out + gv : P.out, ok ? 8u : 0u);
-      }
+    for (int x = tid; x < rows; x += kDownThreads) {
+      const bool ok = x < lim;
+      const double* src = P.layout == LC_VEC_CONTIGUOUS ? P.out + gv * P.ld_out + i0 + x : P.out + (i0 + x) * P.ld_out + gv;
+      cp_async8(zb + v * rows + x, ok ? src : P.out, ok ? 8u : 0u);
     }
   }
   cp_async_commit();
@@ -871,15 +942,12 @@ __global__ void __launch_bounds__(kThreads, 2) lc_down_kernel(const DownParams P
   LC_TS(2, 2);
 
   if (L > 0) {
-    const int lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
-    BCol bc;
-    load_bcol(bc, P.B, lane);
-    // step 4 along the ancestor chain, one warp per (sigma, v): cm_anc(g) += B(p)^T c(a_{g-1}),
-    // p = child index of a_g; then the subtree root
-    for (int ch = warp; ch < 2 * VT; ch += nwarps) {
-      for (int g = 1; g <= gr; ++g) {
-        const int p = int((R >> (gr - g)) & 1);
-        double* dst = (g < gr ? cm_anc(g) : cm_lvl(0)) + ch * kM;  // [sigma][node 0][v] == ch at the root
+    // step 4 along the ancestor chain, one warp per (sigma, v): c(a_g) += B(p)^T c(a_{g-1}),
+    // p = child index of a_g; the subtree root (level gd) last
+    for (int ch = warp; ch < 2 * VT; ch += kDownThreads / 32) {
+      for (int g = 1; g <= gd; ++g) {
+        const int p = int((R >> (gd - g)) & 1);
+        double* dst = (g < gd ? cm_anc(g) : cm_lvl(0)) + ch * kM;  // [sigma][node 0][v] == ch at the root
         const double r = l2l_warp(bc, cm_anc(g - 1) + ch * kM, p, lane);
         if (lane < kM) dst[lane] += r;
         __syncwarp();
@@ -887,64 +955,83 @@ __global__ void __launch_bounds__(kThreads, 2) lc_down_kernel(const DownParams P
     }
     __syncthreads();
     LC_TS(2, 3);
-    // step 4 down the subtree, one warp per (sigma, node, v): c(j) = B(p)^T c(j-1) + c_m2l(j)
-    for (int j = 1; j <= k; ++j) {
+    // step 4 down the subtree, two (sigma, node, v) per warp iteration
+    for (int j = 1; j <= kd; ++j) {
       const int nodes = 1 << j;
       const double* par = cm_lvl(j - 1);
       double* cur = cm_lvl(j);
-      for (int it = warp; it < 2 * nodes * VT; it += nwarps) {
-        const int v = it % VT;
-        const int sn = it / VT;
-        const int node = sn & (nodes - 1);
-        const int sg = sn >> j;
-        const double r = l2l_warp(bc, par + ((sg * (nodes >> 1) + (node >> 1)) * VT + v) * kM, node & 1, lane);
-        if (lane < kM) cur[it * kM + lane] += r;
+      const int items = 2 * nodes * VT;
+      for (int i0_ = warp * 2; i0_ < items; i0_ += 2 * (kDownThreads / 32)) {
+        const int it0 = i0_, it1 = i0_ + 1 < items ? i0_ + 1 : i0_;
+        auto parent = [&](int it, int& p) {
+          const int v = it % VT;
+          const int sn = it / VT;
+          const int node = sn & (nodes - 1);
+          const int sg = sn >> j;
+          p = node & 1;
+          return par + ((sg * (nodes >> 1) + (node >> 1)) * VT + v) * kM;
+        };
+        int p0, p1;
+        const double* c0 = parent(it0, p0);
+        const double* c1 = parent(it1, p1);
+        double r0, r1;
+        l2l_warp2(bc, c0, p0, c1, p1, lane, r0, r1);
+        if (lane < kM) {
+          cur[it0 * kM + lane] += r0;
+          if (it1 != it0) cur[it1 * kM + lane] += r1;
+        }
       }
       __syncthreads();
     }
-  }
-  LC_TS(2, 4);
-  const double* cfin = cm_lvl(k);
-
-  // step 5: z^sigma += c(L-1) T(sigma)^T (eq:step5), 4 same-parity rows per thread (c kept in
-  // registers), accumulated into the band result in shared memory
-  if (L > 0) {
-    constexpr int R5 = 4;
-    const int nb5 = (s + R5 - 1) / R5;
-    const int items = VT * nleaf * 2 * nb5;
-    for (int it = tid; it < items; it += blockDim.x) {
-      const int mb = it % nb5;
-      int r_ = it / nb5;
-      const int sg = r_ & 1;
-      r_ >>= 1;
-      const int u = r_ & (nleaf - 1);
-      const int v = r_ >> k;
-      const int m0 = R5 * mb;
-      const double* cp = cfin + ((sg * nleaf + u) * VT + v) * kM;
-      const double* tq = Tt + sg * kM * s + m0;
-      double t5[R5];
+    LC_TS(2, 4);
+    // step 5: z^sigma += c(L-1) T(sigma)^T (eq:step5): warp = (sigma, half of the leaves),
+    // lane = row m, c of the leaf broadcast from shared memory
+    {
+      const int sg = warp & 1, half = warp >> 1;
+      const double* cl = cm_lvl(kd);
+      const int per = nleaf * VT;
+      for (int it = half; it < per; it += 2) {
+        const int u = it / VT, v = it - u * VT;
+        const double* cp = cl + ((sg * nleaf + u) * VT + v) * kM;
+        double z0 = 0.0, z1 = 0.0, z2 = 0.0;
 #pragma unroll
-      for (int r = 0; r < R5; ++r) t5[r] = 0.0;
-#pragma unroll
-      for (int kk = 0; kk < kM; ++kk) {
-        const double cv = cp[kk];
-#pragma unroll
-        for (int r = 0; r < R5; ++r) t5[r] = fma(cv, tq[kk * s + r], t5[r]);  // (tq beyond s: padding, unused)
+        for (int k = 0; k < kM; k += 6) {
+          const double2 c01 = *reinterpret_cast<const double2*>(cp + k);
+          const double2 c23 = *reinterpret_cast<const double2*>(cp + k + 2);
+          const double2 c45 = *reinterpret_cast<const double2*>(cp + k + 4);
+          z0 = fma(trow[k], c01.x, z0);
+          z1 = fma(trow[k + 1], c01.y, z1);
+          z2 = fma(trow[k + 2], c23.x, z2);
+          z0 = fma(trow[k + 3], c23.y, z0);
+          z1 = fma(trow[k + 4], c45.x, z1);
+          z2 = fma(trow[k + 5], c45.y, z2);
+        }
+        if (lane < s) zb[v * rows + u * seglen + 2 * lane + sg] += (z0 + z1) + z2;
       }
-      double* zr = zb + v * rows + u * seglen + sg + 2 * m0;
+      if (SMAX > 32) {  // rows m = 32..s-1 (s_hat = 64 plans): a second pass with lane + 32
+        // (T rows of lane + 32 loaded on demand; rare configuration)
+        const int m = lane + 32;
+        for (int it = half; it < per; it += 2) {
+          const int u = it / VT, v = it - u * VT;
+          const double* cp = cl + ((sg * nleaf + u) * VT + v) * kM;
+          const double* tp = P.Tpad + (int64_t(sg) * SMAX + (m < SMAX ? m : 0)) * kM;
+          double z = 0.0;
 #pragma unroll
-      for (int r = 0; r < R5; ++r)
-        if (m0 + r < s) zr[2 * r] += t5[r];
+          for (int k = 0; k < kM; ++k) z = fma(__ldg(tp + k), cp[k], z);
+          if (m < s) zb[v * rows + u * seglen + 2 * m + sg] += z;
+        }
+      }
     }
     __syncthreads();
   }
+  LC_TS(2, 5);
   // step 7: C^{-1} (L2C); coalesced store
   const double inv_pi = 0.318309886183790671537767526745028724;
 #pragma unroll 1
   for (int v = 0; v < VT; ++v) {
     const int64_t gv = tile * VT + v;
     if (gv >= P.batch) break;
-    for (int ii = tid; ii < olim; ii += blockDim.x) {
+    for (int ii = tid; ii < olim; ii += kDownThreads) {
       const int64_t i = i0 + ii;
       double z = zb[v * rows + ii];
       if (DIR == 0) z *= (i == 0 ? inv_pi : 2.0 * inv_pi);
@@ -954,11 +1041,10 @@ __global__ void __launch_bounds__(kThreads, 2) lc_down_kernel(const DownParams P
         P.out[i * P.ld_out + gv] = z;
     }
   }
-  __syncthreads();
-  LC_TS(2, 5);
 }
 
 // ============================================================== host side
+
 template <typename K>
 static cudaError_t set_max_dyn_smem(K kernel, int smax) {
   cudaFuncAttributes fa;
@@ -969,13 +1055,21 @@ static cudaError_t set_max_dyn_smem(K kernel, int smax) {
   // without a preference the driver may pick a small shared-memory carveout and cap occupancy
   return cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
 }
-template <int VT>
+template <int VT, int SMAX>
 static cudaError_t set_attrs_vt(int smax) {
-  cudaError_t e = set_max_dyn_smem(lc_up_kernel<VT>, smax);
+  cudaError_t e = set_max_dyn_smem(lc_up_kernel<VT, SMAX>, smax);
   if (e == cudaSuccess) e = set_max_dyn_smem(lc_stream_kernel<VT, 0>, smax);
   if (e == cudaSuccess) e = set_max_dyn_smem(lc_stream_kernel<VT, 1>, smax);
-  if (e == cudaSuccess) e = set_max_dyn_smem(lc_down_kernel<VT, 0>, smax);
-  if (e == cudaSuccess) e = set_max_dyn_smem(lc_down_kernel<VT, 1>, smax);
+  if (e == cudaSuccess) e = set_max_dyn_smem(lc_down_kernel<VT, 0, SMAX>, smax);
+  if (e == cudaSuccess) e = set_max_dyn_smem(lc_down_kernel<VT, 1, SMAX>, smax);
+  return e;
+}
+template <int SMAX>
+static cudaError_t set_attrs_all(int smax) {
+  cudaError_t e = set_attrs_vt<1, SMAX>(smax);
+  if (e == cudaSuccess) e = set_attrs_vt<2, SMAX>(smax);
+  if (e == cudaSuccess) e = set_attrs_vt<4, SMAX>(smax);
+  if (e == cudaSuccess) e = set_attrs_vt<8, SMAX>(smax);
   return e;
 }
 
@@ -990,6 +1084,14 @@ static int stream_occupancy(int dir, size_t smem) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, lc_stream_kernel<VT, 1>, kStreamThreads, smem);
   return occ;
 }
+static int stream_occupancy_vt(int vt, int dir, size_t smem) {
+  switch (vt) {
+    case 1: return stream_occupancy<1>(dir, smem);
+    case 2: return stream_occupancy<2>(dir, smem);
+    case 4: return stream_occupancy<4>(dir, smem);
+    default: return stream_occupancy<8>(dir, smem);
+  }
+}
 
 lc_status configure_kernels(lc_plan* p) {
   int smax = 0;
@@ -997,10 +1099,8 @@ lc_status configure_kernels(lc_plan* p) {
   if (ea != cudaSuccess) return record_cuda_error(ea);
   if (p->device < 0 || p->device >= 64) return LC_ERR_INVALID_ARG;
   if (!g_device_ready[p->device]) {
-    ea = set_attrs_vt<1>(smax);
-    if (ea == cudaSuccess) ea = set_attrs_vt<2>(smax);
-    if (ea == cudaSuccess) ea = set_attrs_vt<4>(smax);
-    if (ea == cudaSuccess) ea = set_attrs_vt<8>(smax);
+    ea = set_attrs_all<32>(smax);
+    if (ea == cudaSuccess) ea = set_attrs_all<64>(smax);
     if (ea == cudaSuccess) {
       double B[kMM];
       ea = cudaMemcpy(B, p->d_B, sizeof(B), cudaMemcpyDeviceToHost);
@@ -1010,78 +1110,89 @@ lc_status configure_kernels(lc_plan* p) {
     g_device_ready[p->device] = true;
   }
   smax -= 256;  // static shared memory of the kernels
+  const int L = int(p->L);
+  if (L > 0 && L - 1 > 62) return LC_ERR_INVALID_ARG;
+  p->smax = p->s <= 32 ? 32 : 64;
 
   const int64_t budget2 = 113 * 1024;  // two CTAs per SM (228 KB minus 1 KB reserved per CTA)
-  const int64_t budget3 = 74 * 1024;   // three CTAs per SM
+  const int64_t budget4 = 56 * 1024;   // four CTAs per SM
   int vt = p->vt;
   if (vt <= 0) vt = p->batch >= 2 ? 2 : 1;
   if (vt != 1 && vt != 2 && vt != 4 && vt != 8) return LC_ERR_INVALID_ARG;
-  const bool user_k = p->k > 0;
-  int k = user_k ? p->k : 4;
-  int cb = p->bps > 0 ? p->bps : 3;
-  int nst = p->nst > 0 ? p->nst : 3;
-  if (nst > 8) return LC_ERR_INVALID_ARG;
-  const int64_t nleaf_total = p->L > 0 ? (int64_t(2) << p->L) : 2;  // leaf segments (L = 0: the two halves)
+  const int64_t nleaf_total = L > 0 ? (int64_t(2) << L) : 2;  // leaf segments (L = 0: the two halves)
   int lnleaf = 0;
   while ((int64_t(1) << (lnleaf + 1)) <= nleaf_total) ++lnleaf;  // log2(nleaf_total)
-  if (p->L == 0) {
-    k = 1;
-  } else {
-    k = int(std::min<int64_t>(k, p->L - 1));
-  }
-  auto down_bytes = [&](int vt_, int k_) {
-    const int gr_ = p->L > 0 ? int(p->L - 1 - k_) : 0;
-    return down_smem_layout(vt_, k_, int(p->s), gr_).total;
-  };
-  if (!user_k) {
-    while (down_bytes(vt, k) > budget3 && p->L > 0 && k > 1) --k;
-  }
-  if (down_bytes(vt, k) > smax) return LC_ERR_INVALID_ARG;
+  const int s = int(p->s);
+  // down kernel: subtrees of 2^kd leaf segments (kd <= L-1; L = 0: the whole vector)
+  const bool user_k = p->k > 0;
+  int kd = user_k ? p->k : 4;
+  if (L >= 1) kd = std::min(kd, L - 1);
+  if (L == 0) kd = 1;
+  if (!user_k)
+    while (down_smem_bytes(vt, kd, s, L) > budget4 && kd > (L == 0 ? 1 : 0)) --kd;
+  if (down_smem_bytes(vt, kd, s, L) > smax) return LC_ERR_INVALID_ARG;
   // streaming kernel: band units of 2^kb leaf segments
-  int kb = std::min(4, lnleaf);  // 2^kb segments x 2 parities x ceil(s/R) blocks = one item per band thread
-  auto stream_bytes = [&](int cb_, int kb_) { return stream_smem_layout(vt, cb_, nst, kb_, int(p->s)).total; };
+  int kb = std::min(4, lnleaf);
+  int cb = p->bps > 0 ? p->bps : 3;
+  int nst = p->nst > 0 ? p->nst : 3;
+  if (nst > 8 || cb > 64) return LC_ERR_INVALID_ARG;
+  auto stream_bytes = [&](int cb_, int kb_) { return stream_smem_layout(vt, cb_, nst, kb_, s).total; };
   while (stream_bytes(cb, kb) > budget2 && kb > 1) --kb;
-  while (stream_bytes(cb, kb) > budget2 && cb > 1) --cb;
+  while (p->bps <= 0 && stream_bytes(cb, kb) > budget2 && cb > 1) --cb;
   if (stream_bytes(cb, kb) > smax) return LC_ERR_INVALID_ARG;
-  // up kernel: deeper subtrees (its shared memory is small); continuation step = its depth
+  // up kernel: about one wave of subtrees (2 CTAs per SM) if the shared memory allows
   const bool user_kup = p->kup > 0;
-  int kup = p->L > 0 ? int(std::min<int64_t>(user_kup ? p->kup : 5, p->L - 1)) : 0;
-  while (!user_kup && kup > 0 && up_smem_bytes(vt, kup, int(p->s)) > budget2) --kup;
-  if (up_smem_bytes(vt, kup, int(p->s)) > smax) return LC_ERR_INVALID_ARG;
+  int kup = 0;
+  if (L > 0) {
+    const int64_t ntiles_ = (p->batch + vt - 1) / vt;
+    int kmax = L - 1;
+    while (kmax > 0 && up_smem_bytes(vt, kmax, s) > budget2) --kmax;
+    if (user_kup) {
+      kup = std::min(p->kup, L - 1);
+    } else {
+      kup = 0;
+      while (kup < kmax && (nleaf_total >> kup) * ntiles_ > 2 * int64_t(p->sm_count)) ++kup;
+      if (L >= 2) kup = std::max(kup, 1);
+    }
+  }
+  if (up_smem_bytes(vt, kup, s) > smax) return LC_ERR_INVALID_ARG;
   p->vt = vt;
-  p->k = k;
+  p->k = kd;
+  p->kb = kb;
   p->bps = cb;
   p->nst = nst;
-  p->kb = kb;
-  p->gr = p->L > 0 ? int(p->L - 1 - k) : 0;
   p->kup = kup;
-  p->grup = p->L > 0 ? int(p->L - 1 - kup) : 0;
+  p->grup = L > 0 ? L - 1 - kup : 0;
+  p->gr = L > 0 ? L - 1 - kd : 0;
   p->group = std::max(kup, 1);
   p->ntiles = (p->batch + vt - 1) / vt;
-  p->smem_down = size_t(down_bytes(vt, k));
-  p->smem_up = size_t(up_smem_bytes(vt, kup, int(p->s)));
+  p->smem_up = size_t(up_smem_bytes(vt, kup, s));
   p->smem_stream = size_t(stream_bytes(cb, kb));
+  p->smem_down = size_t(down_smem_bytes(vt, kd, s, L));
+  // M2L level order: the finest level first (its w is ready after the up kernel's main phase),
+  // down to the subtree roots, then the coarse levels (after the up kernel's continuation)
+  {
+    int o = 0;
+    for (int g = L - 1; g >= p->grup; --g) p->lvorder[o++] = g;
+    for (int g = 0; g < p->grup; ++g) p->lvorder[o++] = g;
+    if (o != L) return LC_ERR_INTERNAL;
+  }
   int64_t nchunks = 0;
-  for (int g = 0; g < p->L; ++g) nchunks += (((int64_t(2) << g) - 1) + cb - 1) / cb;
+  for (int g = 0; g < L; ++g) nchunks += (((int64_t(2) << g) - 1) + cb - 1) / cb;
   p->m2l_units = nchunks * p->ntiles;
   p->band_units = (nleaf_total >> kb) * p->ntiles;
   if (p->m2l_units + p->band_units > 0x7fffffff) return LC_ERR_INVALID_ARG;
   {
-    int occ = 0;
-    switch (vt) {
-      case 1: occ = stream_occupancy<1>(p->dir, p->smem_stream); break;
-      case 2: occ = stream_occupancy<2>(p->dir, p->smem_stream); break;
-      case 4: occ = stream_occupancy<4>(p->dir, p->smem_stream); break;
-      default: occ = stream_occupancy<8>(p->dir, p->smem_stream); break;
-    }
+    const int occ = stream_occupancy_vt(vt, p->dir, p->smem_stream);
     if (occ < 1) return LC_ERR_INVALID_ARG;
-    // persistent grid: every CTA co-resident (the producer may wait on flags raised by other grids)
+    p->stream_occ = occ;
+    // persistent grid: every CTA co-resident (the producer waits on flags raised by the up kernel)
     const int64_t g = int64_t(occ) * p->sm_count;
-    p->stream_grid = int(std::max<int64_t>(1, std::min<int64_t>(g, p->m2l_units + p->band_units)));
+    p->stream_grid = int(std::max<int64_t>(1, std::min<int64_t>(g, std::max(p->m2l_units, p->band_units))));
   }
-  if (p->L > 0) {
-    p->w_tile_doubles = int64_t(vt) * kM * 2 * ((int64_t(4) << p->L) - 4);
-    p->cnt_tile_ints = int64_t(4) << p->L;
+  if (L > 0) {
+    p->w_tile_doubles = int64_t(vt) * kM * 2 * ((int64_t(4) << L) - 4);
+    p->cnt_tile_ints = int64_t(4) << L;
   } else {
     p->w_tile_doubles = 0;
     p->cnt_tile_ints = 0;
@@ -1092,9 +1203,9 @@ lc_status configure_kernels(lc_plan* p) {
   return LC_OK;
 }
 
-template <int VT, int DIR>
+template <int VT, int DIR, int SMAX>
 static cudaError_t launch_vt(const lc_plan* p, const UpParams& up, const StreamParams& sp, const DownParams& dp,
-                             dim3 grid_up, dim3 grid, cudaStream_t st, cudaEvent_t const* ev, int nev) {
+                             dim3 grid_up, dim3 grid_down, cudaStream_t st, cudaEvent_t const* ev, int nev) {
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
@@ -1106,10 +1217,12 @@ static cudaError_t launch_vt(const lc_plan* p, const UpParams& up, const StreamP
   int evi = 0;
   if (ev && nev > 0) cudaEventRecord(ev[evi++], st);
   if (p->L > 0) {
+    UpArgs<SMAX> ua;
+    ua.p = up;
     cfg.gridDim = grid_up;
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = p->smem_up;
-    e = cudaLaunchKernelEx(&cfg, lc_up_kernel<VT>, up);
+    e = cudaLaunchKernelEx(&cfg, lc_up_kernel<VT, SMAX>, ua);
     if (e != cudaSuccess) return e;
     if (ev && evi < nev) cudaEventRecord(ev[evi++], st);
   }
@@ -1119,10 +1232,10 @@ static cudaError_t launch_vt(const lc_plan* p, const UpParams& up, const StreamP
   e = cudaLaunchKernelEx(&cfg, lc_stream_kernel<VT, DIR>, sp);
   if (e != cudaSuccess) return e;
   if (ev && evi < nev) cudaEventRecord(ev[evi++], st);
-  cfg.gridDim = p->L > 0 ? grid : dim3(1, grid.y);
-  cfg.blockDim = dim3(kThreads);
+  cfg.gridDim = grid_down;
+  cfg.blockDim = dim3(kDownThreads);
   cfg.dynamicSmemBytes = p->smem_down;
-  e = cudaLaunchKernelEx(&cfg, lc_down_kernel<VT, DIR>, dp);
+  e = cudaLaunchKernelEx(&cfg, lc_down_kernel<VT, DIR, SMAX>, dp);
   if (e != cudaSuccess) return e;
   if (ev && evi < nev) cudaEventRecord(ev[evi++], st);
   return cudaGetLastError();
@@ -1130,6 +1243,22 @@ static cudaError_t launch_vt(const lc_plan* p, const UpParams& up, const StreamP
 
 static int64_t extent(int layout, int64_t ld, int64_t n, int64_t batch) {
   return layout == LC_VEC_CONTIGUOUS ? (batch - 1) * ld + n : (n - 1) * ld + batch;
+}
+
+template <int SMAX>
+static cudaError_t launch_dispatch(const lc_plan* p, const UpParams& up, const StreamParams& sp, const DownParams& dp,
+                                   dim3 gu, dim3 gd, cudaStream_t st, cudaEvent_t const* ev, int nev) {
+  switch (p->vt * 2 + p->dir) {
+    case 2: return launch_vt<1, 0, SMAX>(p, up, sp, dp, gu, gd, st, ev, nev);
+    case 3: return launch_vt<1, 1, SMAX>(p, up, sp, dp, gu, gd, st, ev, nev);
+    case 4: return launch_vt<2, 0, SMAX>(p, up, sp, dp, gu, gd, st, ev, nev);
+    case 5: return launch_vt<2, 1, SMAX>(p, up, sp, dp, gu, gd, st, ev, nev);
+    case 8: return launch_vt<4, 0, SMAX>(p, up, sp, dp, gu, gd, st, ev, nev);
+    case 9: return launch_vt<4, 1, SMAX>(p, up, sp, dp, gu, gd, st, ev, nev);
+    case 16: return launch_vt<8, 0, SMAX>(p, up, sp, dp, gu, gd, st, ev, nev);
+    case 17: return launch_vt<8, 1, SMAX>(p, up, sp, dp, gu, gd, st, ev, nev);
+  }
+  return cudaErrorInvalidValue;
 }
 
 lc_status launch_execute(const lc_plan* p, const double* in, double* out, void* ws, cudaStream_t st,
@@ -1152,45 +1281,50 @@ lc_status launch_execute(const lc_plan* p, const double* in, double* out, void* 
   int* flags = reinterpret_cast<int*>(reinterpret_cast<char*>(ws) + 2 * wb);
   int* cnt = flags + 64;
   UpParams up{};
-  up.in = in; up.ld_in = p->ld_in; up.n = p->n; up.N = p->N; up.batch = p->batch;
+  up.in = in; up.Tpad = p->d_Tpad; up.B = p->d_B; up.ld_in = p->ld_in; up.n = p->n; up.N = p->N; up.batch = p->batch;
   up.layout = p->layout; up.L = int(p->L); up.s = int(p->s); up.k = p->kup; up.gr = p->grup; up.G = p->group;
-  up.T = p->d_T; up.B = p->d_B; up.w = w; up.cnt = cnt; up.flags = flags; up.w_tile = p->w_tile_doubles;
-  up.cnt_tile = p->cnt_tile_ints;
+  up.fstride = up_fstride(int(p->s));
+  up.vec16 = (reinterpret_cast<uintptr_t>(in) % 16 == 0) && (p->ld_in % 2 == 0) ? 1 : 0;
+  up.w = w; up.cnt = cnt; up.flags = flags; up.w_tile = p->w_tile_doubles; up.cnt_tile = p->cnt_tile_ints;
   StreamParams sp{};
   sp.A = p->d_A; sp.w = w; sp.c = c; sp.in = in; sp.out = out; sp.tabA = p->d_tabA; sp.tabB = p->d_tabB;
-  sp.flags = flags; sp.w_tile = p->w_tile_doubles; sp.ld_in = p->ld_in; sp.ld_out = p->ld_out; sp.n = p->n;
+  sp.flags = flags; sp.w_tile = p->w_tile_doubles;
+  sp.ld_in = p->ld_in; sp.ld_out = p->ld_out; sp.n = p->n;
   sp.N = p->N; sp.batch = p->batch; sp.ntiles = p->ntiles; sp.nm2l = p->m2l_units; sp.nband = p->band_units;
   sp.layout = p->layout; sp.L = int(p->L); sp.s = int(p->s); sp.cb = p->bps; sp.nst = p->nst; sp.kb = p->kb;
   sp.gr_up = p->grup;
+  for (int i = 0; i < 32; ++i) sp.lvorder[i] = p->lvorder[i];
   DownParams dp{};
-  dp.out = out; dp.ld_out = p->ld_out; dp.n = p->n; dp.N = p->N; dp.batch = p->batch; dp.layout = p->layout;
-  dp.L = int(p->L); dp.s = int(p->s); dp.k = p->k; dp.gr = p->gr; dp.Tt = p->d_Tt; dp.B = p->d_B; dp.c = c;
-  dp.w_tile = p->w_tile_doubles;
-  const int64_t nsub = p->L > 0 ? (int64_t(4) << p->gr) : 1;
-  if (nsub > 0x7fffffff || p->ntiles > 65535) {
+  dp.out = out; dp.c = c; dp.Tpad = p->d_Tpad; dp.ld_out = p->ld_out; dp.n = p->n; dp.N = p->N; dp.batch = p->batch;
+  dp.w_tile = p->w_tile_doubles; dp.layout = p->layout; dp.L = int(p->L); dp.s = int(p->s); dp.k = p->k;
+  const int64_t ndown = p->L > 0 ? (int64_t(2) << p->L) >> p->k : 1;
+  const int64_t nsub = p->L > 0 ? (int64_t(4) << p->grup) : 1;
+  if (nsub > 0x7fffffff || ndown > 0x7fffffff || p->ntiles > 65535) {
     if (prev != p->device) cudaSetDevice(prev);
     return LC_ERR_INVALID_ARG;
   }
-  const dim3 grid(unsigned(nsub), unsigned(p->ntiles));
-  const dim3 grid_up(unsigned(p->L > 0 ? (int64_t(4) << p->grup) : 1), unsigned(p->ntiles));
-  cudaError_t e;
-  const int key = p->vt * 2 + p->dir;
-  switch (key) {
-    case 2: e = launch_vt<1, 0>(p, up, sp, dp, grid_up, grid, st, ev, nev); break;
-    case 3: e = launch_vt<1, 1>(p, up, sp, dp, grid_up, grid, st, ev, nev); break;
-    case 4: e = launch_vt<2, 0>(p, up, sp, dp, grid_up, grid, st, ev, nev); break;
-    case 5: e = launch_vt<2, 1>(p, up, sp, dp, grid_up, grid, st, ev, nev); break;
-    case 8: e = launch_vt<4, 0>(p, up, sp, dp, grid_up, grid, st, ev, nev); break;
-    case 9: e = launch_vt<4, 1>(p, up, sp, dp, grid_up, grid, st, ev, nev); break;
-    case 16: e = launch_vt<8, 0>(p, up, sp, dp, grid_up, grid, st, ev, nev); break;
-    case 17: e = launch_vt<8, 1>(p, up, sp, dp, grid_up, grid, st, ev, nev); break;
-    default: e = cudaErrorInvalidValue;
-  }
+  const dim3 grid_up(unsigned(nsub), unsigned(p->ntiles));
+  const dim3 grid_down(unsigned(ndown), unsigned(p->ntiles));
+  const cudaError_t e = p->smax == 32 ? launch_dispatch<32>(p, up, sp, dp, grid_up, grid_down, st, ev, nev)
+                                      : launch_dispatch<64>(p, up, sp, dp, grid_up, grid_down, st, ev, nev);
   if (prev != p->device) cudaSetDevice(prev);
   return e == cudaSuccess ? LC_OK : record_cuda_error(e);
 }
 
 }  // namespace lc
+
+extern "C" lc_status lc_plan_kernel_info(const lc_plan* p, int64_t* out, int32_t count, int32_t* written) {
+  if (!p || !out) return LC_ERR_INVALID_ARG;
+  const int64_t up_grid = p->L > 0 ? (int64_t(4) << p->grup) * p->ntiles : 0;
+  const int64_t v[] = {p->stream_grid, int64_t(p->smem_stream), int64_t(p->smem_up), p->kup, p->grup, p->kb,
+                       p->bps, p->nst, p->vt, p->stream_occ, p->m2l_units, p->band_units, up_grid, p->k,
+                       int64_t(p->smem_down)};
+  const int32_t nv = int32_t(sizeof(v) / sizeof(v[0]));
+  int32_t i = 0;
+  for (; i < nv && i < count; ++i) out[i] = v[i];
+  if (written) *written = i;
+  return LC_OK;
+}
 
 extern "C" lc_status lc_execute(const lc_plan* p, const double* in, double* out, void* ws, void* stream) {
   return lc::launch_execute(p, in, out, ws, (cudaStream_t)stream, nullptr, 0);

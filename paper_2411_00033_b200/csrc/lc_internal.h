@@ -56,26 +56,6 @@ __host__ __device__ inline int64_t pidx(int64_t x) { return x + (x >> 4); }
 
 __host__ __device__ inline int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
-// Shared-memory layout of the down kernel (host computes the size, device the offsets).
-struct DownSmem {
-  int64_t Tt, zb, cm, total;  // byte offsets
-};
-
-// c_m2l nodes staged by the down kernel: gr ancestors + the 2^(k+1)-1 subtree nodes.
-__host__ __device__ inline int64_t down_cm_nodes(int k, int gr) { return int64_t(gr) + ((int64_t(2) << k) - 1); }
-
-__host__ __device__ inline DownSmem down_smem_layout(int VT, int k, int s, int gr) {
-  DownSmem L{};
-  int64_t o = 0;
-  const int64_t node = int64_t(2) * VT * kM * 8;  // one segment, both parities, VT vectors
-  const int64_t nleaf = int64_t(1) << k;
-  L.Tt = o;    o = align_up(o + int64_t(2) * kM * s * 8 + 8 * 8, 128);  // + padding read by blocked step 5
-  L.zb = o;    o = align_up(o + int64_t(VT) * nleaf * 2 * s * 8, 128);
-  L.cm = o;    o = align_up(o + down_cm_nodes(k, gr) * node, 128);
-  L.total = o;
-  return L;
-}
-
 // Streaming kernel: a ring of nst slots, each with the A_hat of `cb` blocks plus the w window
 // (2 cb column segments, both parities, VT vectors); and the band region for a band unit of
 // 2^kb leaf segments: tabA, padded tabB and input tiles, and the z staging tile.
@@ -84,27 +64,41 @@ struct StreamSmem {
   int64_t tp;  // padded band-tile length (doubles)
 };
 __host__ __device__ inline StreamSmem stream_smem_layout(int VT, int cb, int nst, int kb, int s) {
-  StreamSmem L{};
-  L.slot = align_up(int64_t(cb) * 3 * kMM * 8, 128) + align_up(int64_t(2) * (2 * cb) * VT * kM * 8, 128);
+  StreamSmem S{};
+  S.slot = align_up(int64_t(cb) * 3 * kMM * 8, 128) + align_up(int64_t(2) * (2 * cb) * VT * kM * 8, 128);
   int64_t o = 0;
-  L.ring = o;  o += int64_t(nst) * L.slot;
+  S.ring = o;  o += int64_t(nst) * S.slot;
   const int64_t nleaf = int64_t(1) << kb;
   const int64_t tcols = (nleaf + 2) * 2 * s;
-  L.tp = pidx(tcols + 2 * kBandR) + 2;
-  L.ta = o;    o = align_up(o + (int64_t(2) * s + 2 * kBandR) * 8, 128);
-  L.tb = o;    o = align_up(o + L.tp * 8, 128);
-  L.gt = o;    o = align_up(o + int64_t(VT) * L.tp * 8, 128);
-  L.zst = o;   o = align_up(o + int64_t(VT) * nleaf * 2 * s * 8, 128);
-  L.bars = o;  o = align_up(o + int64_t(2) * nst * 8, 128);
-  L.total = o;
-  return L;
+  S.tp = pidx(tcols + 2 * kBandR) + 2;
+  S.ta = o;   o = align_up(o + (int64_t(2) * s + 2 * kBandR) * 8, 128);
+  S.tb = o;   o = align_up(o + S.tp * 8, 128);
+  S.gt = o;   o = align_up(o + int64_t(VT) * S.tp * 8, 128);
+  S.zst = o;  o = align_up(o + int64_t(VT) * nleaf * 2 * s * 8, 128);
+  S.bars = o; o = align_up(o + int64_t(2) * nst * 8, 128);
+  S.total = o;
+  return S;
 }
 
+// Down kernel: c_m2l of the gd ancestors and of the 2^(kd+1)-1 subtree nodes (both parities,
+// VT vectors), then the band result of the 2^kd leaf segments.
+__host__ __device__ inline int64_t down_smem_bytes(int VT, int kd, int s, int L) {
+  const int gd = L > 0 ? L - 1 - kd : 0;
+  const int64_t nodes = L > 0 ? int64_t(gd) + ((int64_t(2) << kd) - 1) : 0;
+  return align_up(nodes * 2 * VT * kM * 8 + int64_t(VT) * (int64_t(1) << kd) * 2 * s * 8, 128);
+}
+
+// segment stride of the up kernel's f tile: 2s rounded up to 2 (mod 4) doubles, so that the
+// 16-byte reads of 32 consecutive leaves hit distinct bank quads
+__host__ __device__ inline int up_fstride(int s) { return (2 * s) % 4 == 2 ? 2 * s : 2 * s + 2; }
+
+constexpr int64_t kUpConstBytes = 21248;  // T(sigma) [2][<=64][M] and B(0) in shared memory, 128-byte aligned
+static_assert(kUpConstBytes >= (2 * 64 * kM + kMM) * 8 && kUpConstBytes % 128 == 0, "up-kernel constants");
+
 __host__ __device__ inline int64_t up_smem_bytes(int VT, int k, int s) {
-  int64_t o = 0;
-  o = align_up(o + int64_t(2) * s * kM * 8, 128);                 // T [2][s][M]
-  o = align_up(o + int64_t(VT) * (int64_t(1) << k) * 2 * s * 8, 128);  // f tile
-  o = align_up(o + ((int64_t(2) << k) - 1) * 2 * VT * kM * 8, 128);    // w tree
+  int64_t o = kUpConstBytes;
+  o = align_up(o + (int64_t(VT) * (int64_t(1) << k) * up_fstride(s) + 2 * 64) * 8, 128);  // f tile + zero tail
+  o = align_up(o + ((int64_t(2) << k) - 1) * 2 * VT * kM * 8, 128);          // w tree
   o += 16;
   return o;
 }
@@ -120,9 +114,13 @@ struct lc_plan {
   int sm_count;
   // kernel configuration
   int vt, k, gr, bps, nst, group, kup, grup, kb;
+  int smax;            // 32 or 64: rows of the padded copy of T(sigma)
+  int lvorder[32];     // M2L level order of the streaming kernel
+  double* h_Tpad;      // host [2][smax][M] copy of T(sigma), zero rows m >= s (kernel parameter)
+  double* d_Tpad;      // device copy of h_Tpad
   int64_t m2l_units;   // (chunk, tile) M2L work units of the streaming kernel
   int64_t band_units;  // (leaf range, tile) band work units of the streaming kernel
-  int stream_grid;
+  int stream_grid, stream_occ;
   size_t smem_stream;
   int64_t ntiles;
   int64_t w_tile_doubles, cnt_tile_ints;

@@ -361,6 +361,19 @@ extern "C" lc_status lc_plan_create(lc_plan** out, int64_t n, lc_direction dir, 
     p->bytes_alg = d.bytes_alg;
   }
 
+  p->h_Tpad = static_cast<double*>(std::calloc(size_t(2) * 64 * kM, sizeof(double)));
+  if (!p->h_Tpad) return fail(LC_ERR_OUT_OF_MEMORY);
+  {
+    const int smax_rows = s <= 32 ? 32 : 64;  // [2][smax][M], rows m >= s zero (kernel-parameter copy)
+    for (int sg = 0; sg < 2; ++sg)
+      for (int64_t m = 0; m < s; ++m)
+        for (int k = 0; k < kM; ++k) p->h_Tpad[(sg * smax_rows + m) * kM + k] = T[size_t((sg * s + m) * kM + k)];
+  }
+  {
+    const int smax_rows = s <= 32 ? 32 : 64;
+    LC_PTRY(cudaMalloc(&p->d_Tpad, sizeof(double) * size_t(2 * smax_rows * kM)));
+    LC_PTRY(cudaMemcpy(p->d_Tpad, p->h_Tpad, sizeof(double) * size_t(2 * smax_rows * kM), cudaMemcpyHostToDevice));
+  }
   const lc_status cs = configure_kernels(p);
   if (cs != LC_OK) return fail(cs);
   LC_PTRY(cudaMalloc(&p->d_ws, p->ws_bytes > 0 ? p->ws_bytes : 16));
@@ -386,6 +399,8 @@ extern "C" lc_status lc_plan_destroy(lc_plan* p) {
   cudaFree(p->d_ws);
   cudaFree(p->d_stage_in);
   cudaFree(p->d_stage_out);
+  std::free(p->h_Tpad);
+  cudaFree(p->d_Tpad);
   cudaSetDevice(prev);
   delete p;
   return LC_OK;

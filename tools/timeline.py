@@ -41,7 +41,7 @@ for _ in range(300):
     y = p.execute(x)
 torch.cuda.synchronize()
 NAMES = {"up": ["start", "staged", "step1", "subtreeM2M", "written", "cont", "contdone", "exit"],
-         "stream": ["start", "end", "m2lwait", "slotfull", "fineflag", "coarseflag", "-", "-"],
+         "stream": ["start", "end", "banddone", "-", "-", "-", "-", "-"],
          "down": ["start", "gdwait", "loaded", "chain", "subtree", "end", "-", "-"]}
 for rep in range(2):
     lib.lc_debug_clear()
