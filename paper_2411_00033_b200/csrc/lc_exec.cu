@@ -185,7 +185,8 @@ __device__ __forceinline__ double l2l_warp(const BCol& cb, const double* __restr
 // ---------------------------------------------------------------- parameters
 // flags (workspace ints): [0] up main-phase arrivals, [1] fine levels of w ready,
 // [2] finished level-0 continuations, [3] coarse levels of w ready, [4] finished
-// streaming CTAs, [5] predecessor complete (input readable), [8] execution epoch.
+// streaming CTAs, [5] predecessor complete (input readable), [10] next M2L unit,
+// [11] next band unit (dynamic schedule of the streaming kernel).
 struct UpParams {
   const double* in;
   const double* Tpad;  // [2][SMAX][M], zero rows m >= s
@@ -223,6 +224,7 @@ struct DownParams {
   double* out;
   const double* c;     // c_m2l
   const double* Tpad;  // [2][SMAX][M], zero rows m >= s
+  const double* B;     // B(0) [M][M]
   int64_t ld_out, n, N, batch, w_tile;
   int layout, L, s, k;
 };
@@ -669,7 +671,8 @@ template <int VT, int DIR>
 __global__ void __launch_bounds__(kStreamThreads, 2) lc_stream_kernel(const __grid_constant__ StreamArgs A) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ int cstart[32];
-  __shared__ int s_last;
+  __shared__ int slotq[8];  // M2L unit of each ring slot (-1: end of work)
+  __shared__ int s_last, s_band;
   const StreamParams& P = A;
   const int tid = threadIdx.x;
   const int s = P.s, cb = P.cb, nst = P.nst, kb = P.kb;
@@ -731,29 +734,45 @@ __global__ void __launch_bounds__(kStreamThreads, 2) lc_stream_kernel(const __gr
                      wbytes, &full[slot], pol);
         }
       };
-      // the A_hat of the first nst M2L units is plan data: issue it before any dependency
+      // dynamic schedule: units are taken from a global counter (flags[10]) in the level order,
+      // so CTAs that start late (SMs still busy with the up kernel) simply take fewer.  The unit
+      // of each ring slot is published to the consumers in slotq[] before the slot's arrive.
+      // The A_hat of the first nst units is plan data: issued before any dependency.
+      int qs[8];
       int npre = 0;
-      for (int q = int(blockIdx.x); q < nm2l && npre < nst; q += int(gridDim.x)) issue(q, npre++, true, false);
-      {
-        int jj = 0;
-        for (int q = int(blockIdx.x); q < nm2l && jj < npre; q += int(gridDim.x)) issue(q, jj++, false, true);
+      for (; npre < nst; ++npre) {
+        const int q = atomicAdd(&P.flags[10], 1);
+        if (q >= nm2l) break;
+        qs[npre] = q;
+        slotq[npre] = q;
+        issue(q, npre, true, false);
       }
-      int j = 0;
-      for (int q = int(blockIdx.x); q < nm2l; q += int(gridDim.x), ++j) {
-        if (j < npre) continue;
-        mbar_wait(&empty[j % nst], uint32_t(((j / nst) - 1) & 1));
-        issue(q, j, true, true);
+      for (int jj = 0; jj < npre; ++jj) issue(qs[jj], jj, false, true);
+      int j = npre;
+      if (npre == nst) {
+        int qn = atomicAdd(&P.flags[10], 1);
+        for (;; ++j) {
+          mbar_wait(&empty[j % nst], uint32_t(((j / nst) - 1) & 1));
+          if (qn >= nm2l) break;
+          const int q = qn;
+          qn = atomicAdd(&P.flags[10], 1);  // next unit, resolved while this one streams
+          slotq[j % nst] = q;
+          issue(q, j, true, true);
+        }
       }
+      slotq[j % nst] = -1;  // end of work: an arrive without transaction bytes
+      mbar_arrive(&full[j % nst]);
     }
   } else if (tid < 32 * (1 + kM2lWarps)) {
     // ------------------------------------------------ M2L consumer warps
     const int ctid = tid - 32;
-    int j = 0;  // M2L ring use counter
-    for (int q = int(blockIdx.x); q < nm2l; q += int(gridDim.x), ++j) {
-      int g, nb, b0, tile;
-      m2l_unit(q, ntiles, P.L, cb, cstart, P.lvorder, g, b0, nb, tile);
+    for (int j = 0;; ++j) {  // j: M2L ring use counter
       const int slot = j % nst;
       mbar_wait(&full[slot], uint32_t((j / nst) & 1));
+      const int q = slotq[slot];
+      if (q < 0) break;
+      int g, nb, b0, tile;
+      m2l_unit(q, ntiles, P.L, cb, cstart, P.lvorder, g, b0, nb, tile);
       const double* As = reinterpret_cast<const double*>(smem + SL.ring + slot * SL.slot);
       const double* wwin = reinterpret_cast<const double*>(smem + SL.ring + slot * SL.slot + a_bytes);
       double* ct = P.c + int64_t(tile) * P.w_tile + (w_level_offset_units(g) + 2 * int64_t(b0)) * VM;
@@ -806,7 +825,7 @@ __global__ void __launch_bounds__(kStreamThreads, 2) lc_stream_kernel(const __gr
     double* gt = reinterpret_cast<double*>(smem + SL.gt);
     double* zst = reinterpret_cast<double*>(smem + SL.zst);
     for (int x = btid; x < 2 * s + 2 * kBandR; x += kBandThreads) ta[x] = x < 2 * s ? P.tabA[x] : 0.0;
-    if (nband > int(blockIdx.x)) {  // the input is readable once the predecessor of the up kernel completed
+    {  // the input is readable once the predecessor of the up kernel completed
       if (P.L > 0) {
         if (btid == 0) wait_flag(&P.flags[5]);
       } else {
@@ -814,7 +833,12 @@ __global__ void __launch_bounds__(kStreamThreads, 2) lc_stream_kernel(const __gr
       }
     }
     band_sync();
-    for (int u = int(blockIdx.x); u < nband; u += int(gridDim.x)) {
+    for (;;) {  // dynamic schedule of the band units (flags[11])
+      if (btid == 0) s_band = atomicAdd(&P.flags[11], 1);
+      band_sync();
+      const int u = s_band;
+      band_sync();
+      if (u >= nband) break;
       const int tile = ntiles > 1 ? u % ntiles : 0;
       const int lr = ntiles > 1 ? u / ntiles : u;
       band_unit<VT, DIR>(P, tile, lr, ta, tb, gt, zst, tp, btid);
@@ -831,6 +855,8 @@ __global__ void __launch_bounds__(kStreamThreads, 2) lc_stream_kernel(const __gr
       P.flags[1] = 0;
       P.flags[3] = 0;
       P.flags[5] = 0;
+      P.flags[10] = 0;
+      P.flags[11] = 0;
     }
     __threadfence();
     __syncthreads();
@@ -839,41 +865,80 @@ __global__ void __launch_bounds__(kStreamThreads, 2) lc_stream_kernel(const __gr
 }
 
 // ============================================================== down kernel
-// One CTA (4 warps) per (subtree of 2^kd leaf row segments, tile of VT vectors):
-//   T(sigma) row m of the lane's parity in registers (plan data, before the dependency wait);
-//   one cp.async round trip for the c_m2l of the ancestors and of the whole subtree and the
-//   band result of the rows; step 4 along the ancestor chain (one warp per (sigma, v), lane =
-//   mode, B(0) column in registers) and down the subtree (two nodes per warp iteration);
-//   step 5 with lane = row m (z_m = sum_k T(sigma)[m][k] c_k, c broadcast from shared memory);
-//   step 7; coalesced store.
-constexpr int kDownThreads = 128;
+// One CTA (8 warps) per (subtree of 2^kd leaf row segments, tile of VT vectors), about one
+// wave.  Every dependent step is a warp-level operator with lane = Chebyshev mode:
+//   * one cp.async round trip brings the c_m2l of the ancestors and of the whole subtree and
+//     the band result of the rows into shared memory;
+//   * step 4 along the ancestor chain (Horner: c(g) = B(p_g)^T c(g-1) + c_m2l(g); one warp per
+//     (sigma, v)), then down the subtree level by level;
+//   * step 5 with lane = row m: z_m = sum_k T(sigma)[m][k] c_k, the T row in registers;
+//   * step 7 and a coalesced store.
+// Operator inputs are loaded into registers before the arithmetic and every dot product runs
+// as four partial sums, so a level costs one shared-memory round trip plus a 5-deep DFMA chain.
+constexpr int kDownThreads = 256;
+constexpr int kDownWarps = kDownThreads / 32;
 
-// two independent (B(p)^T c) applications per call: ILP across nodes
-__device__ __forceinline__ void l2l_warp2(const BCol& cb, const double* __restrict__ c0, int p0,
-                                          const double* __restrict__ c1, int p1, int l, double& r0, double& r1) {
-  double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+// (B(p)^T c)_l = (-1)^{pl} sum_n b_nl (-1)^{pn} c_n   (lane l); column l of
+// B(0) from shared memory (consecutive lanes, conflict-free), c broadcast.
+__device__ __forceinline__ double l2l_lane(const double* __restrict__ Bs, const double* __restrict__ c, int p, int l) {
+  const int lc = l < kM ? l : 0;
+  double x[kM], b[kM];
 #pragma unroll
   for (int n = 0; n < kM; n += 2) {
-    const double2 x = *reinterpret_cast<const double2*>(c0 + n);
-    const double2 y = *reinterpret_cast<const double2*>(c1 + n);
-    a0 = fma(cb.v[n], x.x, a0);
-    a1 = fma(cb.v[n + 1], x.y, a1);
-    b0 = fma(cb.v[n], y.x, b0);
-    b1 = fma(cb.v[n + 1], y.y, b1);
+    const double2 t = *reinterpret_cast<const double2*>(c + n);
+    x[n] = t.x;
+    x[n + 1] = t.y;
   }
-  r0 = p0 ? a0 - a1 : a0 + a1;
-  if (p0 && (l & 1)) r0 = -r0;
-  r1 = p1 ? b0 - b1 : b0 + b1;
-  if (p1 && (l & 1)) r1 = -r1;
+#pragma unroll
+  for (int n = 0; n < kM; ++n) b[n] = Bs[n * kM + lc];  // b_{n l} (zero above the diagonal)
+  double e0 = 0.0, e1 = 0.0, o0 = 0.0, o1 = 0.0;
+#pragma unroll
+  for (int n = 0; n < kM; n += 4) {
+    e0 = fma(b[n], x[n], e0);
+    o0 = fma(b[n + 1], x[n + 1], o0);
+    if (n + 2 < kM) e1 = fma(b[n + 2], x[n + 2], e1);
+    if (n + 3 < kM) o1 = fma(b[n + 3], x[n + 3], o1);
+  }
+  const double e = e0 + e1, o = o0 + o1;
+  const double r = p ? e - o : e + o;
+  return (p && (l & 1)) ? -r : r;
+}
+
+// Step 4 for outputs k in [K0, K1) of one node by one thread:
+// dst[k] += (B(p)^T c)_k = (-1)^{pk} sum_{n>=k} b_nk (-1)^{pn} c_n.
+// BT = B(0)^T in shared memory (row k = column k of B(0)), broadcast 16-byte loads; two partial
+// sums per output.  Groups [0,4), [4,9), [9,18) carry 66, 60 and 45 DFMA.
+template <int K0, int K1>
+__device__ __forceinline__ void l2l_rows(const double* __restrict__ BT, const double* __restrict__ c, int p,
+                                         double* __restrict__ dst) {
+  double x[kM];
+#pragma unroll
+  for (int n = K0 & ~1; n < kM; n += 2) {
+    const double2 t = *reinterpret_cast<const double2*>(c + n);
+    x[n] = t.x;
+    x[n + 1] = p ? -t.y : t.y;  // (-1)^{pn}
+  }
+#pragma unroll
+  for (int k = K0; k < K1; ++k) {
+    double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+    for (int n = k & ~1; n < kM; n += 2) {
+      const double2 b = *reinterpret_cast<const double2*>(BT + k * kM + n);  // b_{n k}, b_{n+1 k}
+      if (n >= k) a0 = fma(b.x, x[n], a0);
+      a1 = fma(b.y, x[n + 1], a1);
+    }
+    const double r = a0 + a1;
+    dst[k] += (p && (k & 1)) ? -r : r;  // (-1)^{pk}
+  }
 }
 
 template <int VT, int DIR, int SMAX>
-__global__ void __launch_bounds__(kDownThreads, 4) lc_down_kernel(const DownParams P) {
+__global__ void __launch_bounds__(kDownThreads, 2) lc_down_kernel(const DownParams P) {
   extern __shared__ __align__(128) unsigned char smem[];
   const int s = P.s, kd = P.k, L = P.L;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int gd = L > 0 ? L - 1 - kd : 0;  // level of the subtree root
-  const int64_t VM = int64_t(VT) * kM;
+  const int VM = VT * kM;
   const int nleaf = 1 << kd;
   const int seglen = 2 * s;
   const int64_t R = blockIdx.x;
@@ -881,27 +946,20 @@ __global__ void __launch_bounds__(kDownThreads, 4) lc_down_kernel(const DownPara
   const int64_t U0 = R << kd;
   const int64_t i0 = U0 * seglen;
   const int rows = nleaf * seglen;
-  // shared memory: cm = ancestors [g][sigma][v][M] (g < gd), subtree level j at node offset
-  // gd + 2^j - 1 ([sigma][node][v][M]); zb = [v][rows]
-  double* cm = reinterpret_cast<double*>(smem);
+  // shared memory: B(0), T(sigma), cm = ancestors [g][sigma][v][M] (g < gd), subtree level j
+  // at node offset gd + 2^j - 1 ([sigma][node][v][M]); zb = [v][rows]
+  double* Bsh = reinterpret_cast<double*>(smem);  // B(0) [M][M]
+  double* BTsh = Bsh + kMM + 4;                    // B(0)^T [M][M] (16-byte aligned)
+  double* Tsh = BTsh + kMM + 4;                    // T(sigma) [2][SMAX][M]
+  double* cm = Tsh + 2 * SMAX * kM;
   double* zb = cm + (L > 0 ? (int64_t(gd) + (int64_t(2) << kd) - 1) * 2 * VM : 0);
-  auto cm_anc = [&](int g) { return cm + int64_t(g) * 2 * VM; };
-  auto cm_lvl = [&](int j) { return cm + (int64_t(gd) + (1 << j) - 1) * 2 * VM; };
+  auto cm_anc = [&](int g) { return cm + g * 2 * VM; };
+  auto cm_lvl = [&](int j) { return cm + (gd + (1 << j) - 1) * 2 * VM; };
   LC_TS(2, 0);
-  // plan data first: T(sigma)[m][.] of this warp's parity (sigma = warp & 1) and lane m
-  double trow[kM];
-  {
-    const int sg = warp & 1;
-    const double* tp = P.Tpad + (int64_t(sg) * SMAX + (lane < SMAX ? lane : 0)) * kM;
-#pragma unroll
-    for (int k = 0; k < kM; k += 2) {
-      const double2 t2 = __ldg(reinterpret_cast<const double2*>(tp + k));
-      trow[k] = t2.x;
-      trow[k + 1] = t2.y;
-    }
-  }
-  BCol bc;
-  load_bcol(bc, lane);
+  // plan data first: B(0) and T(sigma) (padded to SMAX rows) into shared memory
+  for (int i = tid; i < kMM / 2; i += kDownThreads) cp_async16(Bsh + 2 * i, P.B + 2 * i);
+  for (int i = tid; i < SMAX * kM; i += kDownThreads) cp_async16(Tsh + 2 * i, P.Tpad + 2 * i);
+  for (int i = tid; i < kMM; i += kDownThreads) BTsh[(i % kM) * kM + i / kM] = __ldg(P.B + i);
   griddep_launch();
   griddep_wait();  // c_m2l and the band result (streaming kernel) are ready past this point
   LC_TS(2, 1);
@@ -917,10 +975,10 @@ __global__ void __launch_bounds__(kDownThreads, 4) lc_down_kernel(const DownPara
     }
     for (int j = 0; j <= kd; ++j) {
       const int g = gd + j;
-      const int cnt2 = int((int64_t(1) << j) * VM / 2);
+      const int cnt2 = (1 << j) * VM / 2;
       for (int sg = 0; sg < 2; ++sg) {
         const double* src = ct + (w_level_offset_units(g) + sg * nseg(g) + (R << j)) * VM;
-        double* dst = cm_lvl(j) + sg * (int64_t(1) << j) * VM;
+        double* dst = cm_lvl(j) + sg * (1 << j) * VM;
         for (int i = tid; i < cnt2; i += kDownThreads) cp_async16(dst + 2 * i, src + 2 * i);
       }
     }
@@ -942,82 +1000,106 @@ __global__ void __launch_bounds__(kDownThreads, 4) lc_down_kernel(const DownPara
   LC_TS(2, 2);
 
   if (L > 0) {
-    // step 4 along the ancestor chain, one warp per (sigma, v): c(a_g) += B(p)^T c(a_{g-1}),
-    // p = child index of a_g; the subtree root (level gd) last
-    for (int ch = warp; ch < 2 * VT; ch += kDownThreads / 32) {
-      for (int g = 1; g <= gd; ++g) {
-        const int p = int((R >> (gd - g)) & 1);
-        double* dst = (g < gd ? cm_anc(g) : cm_lvl(0)) + ch * kM;  // [sigma][node 0][v] == ch at the root
-        const double r = l2l_warp(bc, cm_anc(g - 1) + ch * kM, p, lane);
-        if (lane < kM) dst[lane] += r;
-        __syncwarp();
+    // step 4 along the ancestor chain (Horner), one warp per (sigma, v), then the subtree root
+    if (gd > 0) {
+      for (int ch = warp; ch < 2 * VT; ch += kDownWarps) {
+        double acc = lane < kM ? cm_anc(0)[ch * kM + lane] : 0.0;
+        double* scr = cm_anc(0) + ch * kM;  // the running vector is kept in place of c_m2l(0)
+        for (int g = 1; g <= gd; ++g) {
+          const double own = lane < kM ? (g < gd ? cm_anc(g) : cm_lvl(0))[ch * kM + lane] : 0.0;
+          const int p = int((R >> (gd - g)) & 1);
+          const double r = l2l_lane(Bsh, scr, p, lane);
+          acc = r + own;
+          __syncwarp();
+          scr = (g < gd ? cm_anc(g) : cm_lvl(0)) + ch * kM;
+          if (lane < kM) scr[lane] = acc;
+          __syncwarp();
+        }
       }
+      __syncthreads();
     }
-    __syncthreads();
     LC_TS(2, 3);
-    // step 4 down the subtree, two (sigma, node, v) per warp iteration
+    // step 4 down the subtree, level by level.  Narrow levels: one warp per (sigma, node, v),
+    // lane = mode (short dependent chain).  Wide levels: one thread per (sigma, node, v) with
+    // all 18 outputs (the fp64 pipe is the limit there: 171 DFMA on 32 busy lanes instead of
+    // 324 lane-slots of a warp item), B(0) rows broadcast from shared memory.
     for (int j = 1; j <= kd; ++j) {
       const int nodes = 1 << j;
       const double* par = cm_lvl(j - 1);
       double* cur = cm_lvl(j);
       const int items = 2 * nodes * VT;
-      for (int i0_ = warp * 2; i0_ < items; i0_ += 2 * (kDownThreads / 32)) {
-        const int it0 = i0_, it1 = i0_ + 1 < items ? i0_ + 1 : i0_;
-        auto parent = [&](int it, int& p) {
+      if (items <= 2 * kDownWarps) {
+        for (int it = warp; it < items; it += kDownWarps) {
           const int v = it % VT;
           const int sn = it / VT;
           const int node = sn & (nodes - 1);
           const int sg = sn >> j;
-          p = node & 1;
-          return par + ((sg * (nodes >> 1) + (node >> 1)) * VT + v) * kM;
-        };
-        int p0, p1;
-        const double* c0 = parent(it0, p0);
-        const double* c1 = parent(it1, p1);
-        double r0, r1;
-        l2l_warp2(bc, c0, p0, c1, p1, lane, r0, r1);
-        if (lane < kM) {
-          cur[it0 * kM + lane] += r0;
-          if (it1 != it0) cur[it1 * kM + lane] += r1;
+          const double own = lane < kM ? cur[it * kM + lane] : 0.0;
+          const double r = l2l_lane(Bsh, par + ((sg * (nodes >> 1) + (node >> 1)) * VT + v) * kM, node & 1, lane);
+          if (lane < kM) cur[it * kM + lane] = own + r;
+        }
+      } else {
+        // item = (group, sigma, node, v); warps of a round share the group when items >= 32
+        for (int q = tid; q < 3 * items; q += kDownThreads) {
+          const int grp = q / items;
+          const int it = q - grp * items;
+          const int v = it % VT;
+          const int sn = it / VT;
+          const int node = sn & (nodes - 1);
+          const int sg = sn >> j;
+          const double* cpar = par + ((sg * (nodes >> 1) + (node >> 1)) * VT + v) * kM;
+          if (grp == 0)
+            l2l_rows<0, 4>(BTsh, cpar, node & 1, cur + it * kM);
+          else if (grp == 1)
+            l2l_rows<4, 9>(BTsh, cpar, node & 1, cur + it * kM);
+          else
+            l2l_rows<9, 18>(BTsh, cpar, node & 1, cur + it * kM);
         }
       }
       __syncthreads();
     }
     LC_TS(2, 4);
-    // step 5: z^sigma += c(L-1) T(sigma)^T (eq:step5): warp = (sigma, half of the leaves),
+    // step 5: z^sigma += c(L-1) T(sigma)^T (eq:step5): warp = (sigma = warp & 1, leaf group),
     // lane = row m, c of the leaf broadcast from shared memory
     {
-      const int sg = warp & 1, half = warp >> 1;
+      const int sg = warp & 1;
+      double trow[kM];  // T(sigma)[m][.] of this lane's row m
+#pragma unroll
+      for (int k = 0; k < kM; k += 2) {
+        const double2 t2 = *reinterpret_cast<const double2*>(Tsh + (sg * SMAX + (lane < SMAX ? lane : 0)) * kM + k);
+        trow[k] = t2.x;
+        trow[k + 1] = t2.y;
+      }
       const double* cl = cm_lvl(kd);
       const int per = nleaf * VT;
-      for (int it = half; it < per; it += 2) {
+      for (int it = warp >> 1; it < per; it += kDownWarps / 2) {
         const int u = it / VT, v = it - u * VT;
         const double* cp = cl + ((sg * nleaf + u) * VT + v) * kM;
+        double c[kM];
+#pragma unroll
+        for (int k = 0; k < kM; k += 2) {
+          const double2 t = *reinterpret_cast<const double2*>(cp + k);
+          c[k] = t.x;
+          c[k + 1] = t.y;
+        }
         double z0 = 0.0, z1 = 0.0, z2 = 0.0;
 #pragma unroll
-        for (int k = 0; k < kM; k += 6) {
-          const double2 c01 = *reinterpret_cast<const double2*>(cp + k);
-          const double2 c23 = *reinterpret_cast<const double2*>(cp + k + 2);
-          const double2 c45 = *reinterpret_cast<const double2*>(cp + k + 4);
-          z0 = fma(trow[k], c01.x, z0);
-          z1 = fma(trow[k + 1], c01.y, z1);
-          z2 = fma(trow[k + 2], c23.x, z2);
-          z0 = fma(trow[k + 3], c23.y, z0);
-          z1 = fma(trow[k + 4], c45.x, z1);
-          z2 = fma(trow[k + 5], c45.y, z2);
+        for (int k = 0; k < kM; k += 3) {
+          z0 = fma(trow[k], c[k], z0);
+          z1 = fma(trow[k + 1], c[k + 1], z1);
+          z2 = fma(trow[k + 2], c[k + 2], z2);
         }
         if (lane < s) zb[v * rows + u * seglen + 2 * lane + sg] += (z0 + z1) + z2;
       }
-      if (SMAX > 32) {  // rows m = 32..s-1 (s_hat = 64 plans): a second pass with lane + 32
-        // (T rows of lane + 32 loaded on demand; rare configuration)
+      if (SMAX > 32) {  // rows m = 32..s-1 (s_hat = 64 plans): T rows of lane + 32 from global
         const int m = lane + 32;
-        for (int it = half; it < per; it += 2) {
+        for (int it = warp >> 1; it < per; it += kDownWarps / 2) {
           const int u = it / VT, v = it - u * VT;
           const double* cp = cl + ((sg * nleaf + u) * VT + v) * kM;
-          const double* tp = P.Tpad + (int64_t(sg) * SMAX + (m < SMAX ? m : 0)) * kM;
+          const double* tp = Tsh + (sg * SMAX + (m < SMAX ? m : 0)) * kM;
           double z = 0.0;
 #pragma unroll
-          for (int k = 0; k < kM; ++k) z = fma(__ldg(tp + k), cp[k], z);
+          for (int k = 0; k < kM; ++k) z = fma(tp[k], cp[k], z);
           if (m < s) zb[v * rows + u * seglen + 2 * m + sg] += z;
         }
       }
@@ -1115,7 +1197,6 @@ lc_status configure_kernels(lc_plan* p) {
   p->smax = p->s <= 32 ? 32 : 64;
 
   const int64_t budget2 = 113 * 1024;  // two CTAs per SM (228 KB minus 1 KB reserved per CTA)
-  const int64_t budget4 = 56 * 1024;   // four CTAs per SM
   int vt = p->vt;
   if (vt <= 0) vt = p->batch >= 2 ? 2 : 1;
   if (vt != 1 && vt != 2 && vt != 4 && vt != 8) return LC_ERR_INVALID_ARG;
@@ -1123,13 +1204,18 @@ lc_status configure_kernels(lc_plan* p) {
   int lnleaf = 0;
   while ((int64_t(1) << (lnleaf + 1)) <= nleaf_total) ++lnleaf;  // log2(nleaf_total)
   const int s = int(p->s);
-  // down kernel: subtrees of 2^kd leaf segments (kd <= L-1; L = 0: the whole vector)
+  // down kernel: subtrees of 2^kd leaf segments (kd <= L-1; L = 0: the whole vector), about
+  // one wave of 8-warp CTAs at two per SM when the shared memory allows
   const bool user_k = p->k > 0;
-  int kd = user_k ? p->k : 4;
-  if (L >= 1) kd = std::min(kd, L - 1);
-  if (L == 0) kd = 1;
-  if (!user_k)
-    while (down_smem_bytes(vt, kd, s, L) > budget4 && kd > (L == 0 ? 1 : 0)) --kd;
+  int kd = 1;
+  if (L >= 1) {
+    const int64_t ntiles_ = (p->batch + vt - 1) / vt;
+    kd = 0;
+    while (kd < L - 1 && (nleaf_total >> kd) * ntiles_ > 2 * int64_t(p->sm_count) &&
+           down_smem_bytes(vt, kd + 1, s, L) <= budget2)
+      ++kd;
+    if (user_k) kd = std::min(p->k, L - 1);
+  }
   if (down_smem_bytes(vt, kd, s, L) > smax) return LC_ERR_INVALID_ARG;
   // streaming kernel: band units of 2^kb leaf segments
   int kb = std::min(4, lnleaf);
@@ -1295,7 +1381,7 @@ lc_status launch_execute(const lc_plan* p, const double* in, double* out, void* 
   sp.gr_up = p->grup;
   for (int i = 0; i < 32; ++i) sp.lvorder[i] = p->lvorder[i];
   DownParams dp{};
-  dp.out = out; dp.c = c; dp.Tpad = p->d_Tpad; dp.ld_out = p->ld_out; dp.n = p->n; dp.N = p->N; dp.batch = p->batch;
+  dp.out = out; dp.c = c; dp.Tpad = p->d_Tpad; dp.B = p->d_B; dp.ld_out = p->ld_out; dp.n = p->n; dp.N = p->N; dp.batch = p->batch;
   dp.w_tile = p->w_tile_doubles; dp.layout = p->layout; dp.L = int(p->L); dp.s = int(p->s); dp.k = p->k;
   const int64_t ndown = p->L > 0 ? (int64_t(2) << p->L) >> p->k : 1;
   const int64_t nsub = p->L > 0 ? (int64_t(4) << p->grup) : 1;

@@ -85,7 +85,9 @@ __host__ __device__ inline StreamSmem stream_smem_layout(int VT, int cb, int nst
 __host__ __device__ inline int64_t down_smem_bytes(int VT, int kd, int s, int L) {
   const int gd = L > 0 ? L - 1 - kd : 0;
   const int64_t nodes = L > 0 ? int64_t(gd) + ((int64_t(2) << kd) - 1) : 0;
-  return align_up(nodes * 2 * VT * kM * 8 + int64_t(VT) * (int64_t(1) << kd) * 2 * s * 8, 128);
+  const int64_t smax = s <= 32 ? 32 : 64;
+  return align_up((2 * (kMM + 4) + 2 * smax * kM) * 8 + nodes * 2 * VT * kM * 8 + int64_t(VT) * (int64_t(1) << kd) * 2 * s * 8,
+                  128);
 }
 
 // segment stride of the up kernel's f tile: 2s rounded up to 2 (mod 4) doubles, so that the
