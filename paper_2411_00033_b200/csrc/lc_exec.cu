@@ -236,8 +236,8 @@ struct DownParams {
 // once), B(0) is a uniform constant-bank operand (the row group is warp-uniform), and every row
 // keeps two partial sums (even / odd k) to halve its dependent DFMA chain.
 template <int R0, int R1>
-__device__ __forceinline__ void m2m_rows(const double* __restrict__ x0, const double* __restrict__ x1,
-                                         double* __restrict__ out) {
+__device__ __forceinline__ void m2m_rows(const double* __restrict__ Bs, const double* __restrict__ x0,
+                                         const double* __restrict__ x1, double* __restrict__ out) {
   constexpr int NR = R1 - R0;
   double zp[R1], zm[R1];
 #pragma unroll
@@ -256,9 +256,15 @@ __device__ __forceinline__ void m2m_rows(const double* __restrict__ x0, const do
   for (int n = R0; n < R1; ++n) {
     double ae = 0.0, ao = 0.0;
 #pragma unroll
-    for (int k = 0; k <= n; k += 2) ae = fma(c_B0[n * kM + k], ((n - k) & 1) ? zm[k] : zp[k], ae);
-#pragma unroll
-    for (int k = 1; k <= n; k += 2) ao = fma(c_B0[n * kM + k], ((n - k) & 1) ? zm[k] : zp[k], ao);
+    for (int k = 0; k <= n; k += 2) {
+      if (k + 1 <= n) {  // b_{n k}, b_{n k+1}: one broadcast 16-byte load
+        const double2 b = *reinterpret_cast<const double2*>(Bs + n * kM + k);
+        ae = fma(b.x, ((n - k) & 1) ? zm[k] : zp[k], ae);
+        ao = fma(b.y, ((n - k - 1) & 1) ? zm[k + 1] : zp[k + 1], ao);
+      } else {
+        ae = fma(Bs[n * kM + k], zp[k], ae);
+      }
+    }
     acc[n - R0] = ae + ao;
   }
 #pragma unroll
@@ -269,7 +275,8 @@ __device__ __forceinline__ void m2m_rows(const double* __restrict__ x0, const do
 // parent, v), each warp on a single row group: [0,10), [10,15), [15,18) carry 55, 65 and 51
 // DFMA.  Six of the eight warps work; a level is one round for up to 64 (sigma, parent, v).
 template <int VT>
-__device__ __forceinline__ void m2m_level(const double* __restrict__ ch, double* __restrict__ pa, int lp) {
+__device__ __forceinline__ void m2m_level(const double* __restrict__ Bs, const double* __restrict__ ch,
+                                          double* __restrict__ pa, int lp) {
   const int np = 1 << lp;
   const int per = 2 * np * VT;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -284,11 +291,11 @@ __device__ __forceinline__ void m2m_level(const double* __restrict__ ch, double*
     const double* x0 = ch + ((sg * 2 * np + 2 * P) * VT + v) * kM;
     double* o = pa + r * kM;
     if (rg == 0)
-      m2m_rows<0, 10>(x0, x0 + VT * kM, o);
+      m2m_rows<0, 10>(Bs, x0, x0 + VT * kM, o);
     else if (rg == 1)
-      m2m_rows<10, 15>(x0, x0 + VT * kM, o);
+      m2m_rows<10, 15>(Bs, x0, x0 + VT * kM, o);
     else
-      m2m_rows<15, 18>(x0, x0 + VT * kM, o);
+      m2m_rows<15, 18>(Bs, x0, x0 + VT * kM, o);
   }
 }
 
@@ -421,7 +428,7 @@ __global__ void __launch_bounds__(kThreads, 2) lc_up_kernel(const __grid_constan
   LC_TS(0, 2);
   // step 2 inside the subtree
   for (int j = k; j >= 1; --j) {
-    m2m_level<VT>(tree + tree_off(j), tree + tree_off(j - 1), j - 1);
+    m2m_level<VT>(Bs, tree + tree_off(j), tree + tree_off(j - 1), j - 1);
     __syncthreads();
   }
   LC_TS(0, 3);
@@ -481,7 +488,7 @@ __global__ void __launch_bounds__(kThreads, 2) lc_up_kernel(const __grid_constan
     }
     __syncthreads();
     for (int j = ge; j >= 1; --j) {
-      m2m_level<VT>(tree + tree_off(j), tree + tree_off(j - 1), j - 1);
+      m2m_level<VT>(Bs, tree + tree_off(j), tree + tree_off(j - 1), j - 1);
       __syncthreads();
     }
     for (int j = 0; j < ge; ++j) {
@@ -777,8 +784,60 @@ __global__ void __launch_bounds__(kStreamThreads, 2) lc_stream_kernel(const __gr
       const double* wwin = reinterpret_cast<const double*>(smem + SL.ring + slot * SL.slot + a_bytes);
       double* ct = P.c + int64_t(tile) * P.w_tile + (w_level_offset_units(g) + 2 * int64_t(b0)) * VM;
       const int64_t sgstride = nseg(g) * VM;
-      const int nrows = 2 * nb;
-      for (int it = ctid; it < nrows * kM; it += kM2lThreads) {
+      // item = (block b, mode kk): the even row u = 2b (r = 0 with column t = u+2, r = 1 with
+      // t = u+3) and the odd row u+1 (r = 2 with t = u+3), both parities, all VT vectors:
+      // 3 A_hat rows x 2 x VT dot products of length 18, each as two partial sums.
+      if (VT <= 2) {
+      for (int it = ctid; it < nb * kM; it += kM2lThreads) {
+        const int bl = it / kM, kk = it - bl * kM;
+        double e0[2][VT], e1[2][VT], o0[2][VT], o1[2][VT];  // even row / odd row partial sums
+#pragma unroll
+        for (int sg = 0; sg < 2; ++sg)
+#pragma unroll
+          for (int v = 0; v < VT; ++v) e0[sg][v] = e1[sg][v] = o0[sg][v] = o1[sg][v] = 0.0;
+#pragma unroll
+        for (int r = 0; r < 3; ++r) {
+          const int tloc = 2 * bl + (r == 0 ? 0 : 1);  // t - (2 b0 + 2)
+          const double* arow = As + (3 * bl + r) * kMM + kk * kM;
+          double ar[kM];
+#pragma unroll
+          for (int l = 0; l < kM; l += 2) {
+            const double2 t2 = *reinterpret_cast<const double2*>(arow + l);
+            ar[l] = t2.x;
+            ar[l + 1] = t2.y;
+          }
+#pragma unroll
+          for (int sg = 0; sg < 2; ++sg)
+#pragma unroll
+            for (int v = 0; v < VT; ++v) {
+              const double* wp = wwin + (sg * 2 * cb + tloc) * VM + v * kM;
+              double p0 = 0.0, p1 = 0.0;
+#pragma unroll
+              for (int l = 0; l < kM; l += 2) {
+                const double2 w2 = *reinterpret_cast<const double2*>(wp + l);
+                p0 = fma(ar[l], w2.x, p0);
+                p1 = fma(ar[l + 1], w2.y, p1);
+              }
+              if (r < 2) {
+                e0[sg][v] += p0;
+                e1[sg][v] += p1;
+              } else {
+                o0[sg][v] = p0;
+                o1[sg][v] = p1;
+              }
+            }
+        }
+#pragma unroll
+        for (int sg = 0; sg < 2; ++sg)
+#pragma unroll
+          for (int v = 0; v < VT; ++v) {
+            ct[sg * sgstride + (2 * bl) * VM + v * kM + kk] = e0[sg][v] + e1[sg][v];
+            ct[sg * sgstride + (2 * bl + 1) * VM + v * kM + kk] = o0[sg][v] + o1[sg][v];
+          }
+      }
+      } else {  // wide vector tiles: one (row, mode) per thread, one A_hat row at a time
+        const int nrows = 2 * nb;
+        for (int it = ctid; it < nrows * kM; it += kM2lThreads) {
         const int ri = it / kM, kk = it % kM;  // row u = 2 b0 + ri
         double acc[2][VT];
 #pragma unroll
@@ -813,6 +872,7 @@ __global__ void __launch_bounds__(kStreamThreads, 2) lc_stream_kernel(const __gr
         for (int sg = 0; sg < 2; ++sg)
 #pragma unroll
           for (int v = 0; v < VT; ++v) ct[sg * sgstride + ri * VM + v * kM + kk] = acc[sg][v];
+      }
       }
       __syncwarp();
       if ((tid & 31) == 0) mbar_arrive(&empty[slot]);  // this warp is done with the slot
@@ -904,20 +964,13 @@ __device__ __forceinline__ double l2l_lane(const double* __restrict__ Bs, const 
   return (p && (l & 1)) ? -r : r;
 }
 
-// Step 4 for outputs k in [K0, K1) of one node by one thread:
-// dst[k] += (B(p)^T c)_k = (-1)^{pk} sum_{n>=k} b_nk (-1)^{pn} c_n.
-// BT = B(0)^T in shared memory (row k = column k of B(0)), broadcast 16-byte loads; two partial
-// sums per output.  Groups [0,4), [4,9), [9,18) carry 66, 60 and 45 DFMA.
+// Step 4 for one node by one thread: dst[k] += (B(p)^T c)_k = (-1)^{pk} sum_{n>=k} b_nk (-1)^{pn} c_n
+// (PAPER.md:383-384).  BT = B(0)^T in shared memory (row k = column k of B(0)), broadcast 16-byte
+// loads; two partial sums per output.  The outputs are produced in three groups separated by
+// compiler barriers so that the B loads of a group are not hoisted (register pressure).
 template <int K0, int K1>
-__device__ __forceinline__ void l2l_rows(const double* __restrict__ BT, const double* __restrict__ c, int p,
-                                         double* __restrict__ dst) {
-  double x[kM];
-#pragma unroll
-  for (int n = K0 & ~1; n < kM; n += 2) {
-    const double2 t = *reinterpret_cast<const double2*>(c + n);
-    x[n] = t.x;
-    x[n + 1] = p ? -t.y : t.y;  // (-1)^{pn}
-  }
+__device__ __forceinline__ void l2l_group(const double* __restrict__ BT, const double (&x)[kM], int p,
+                                          double* __restrict__ dst) {
 #pragma unroll
   for (int k = K0; k < K1; ++k) {
     double a0 = 0.0, a1 = 0.0;
@@ -929,7 +982,23 @@ __device__ __forceinline__ void l2l_rows(const double* __restrict__ BT, const do
     }
     const double r = a0 + a1;
     dst[k] += (p && (k & 1)) ? -r : r;  // (-1)^{pk}
+    if (k & 1) asm volatile("" ::: "memory");  // at most two outputs' B loads in flight
   }
+}
+__device__ __forceinline__ void l2l_node(const double* __restrict__ BT, const double* __restrict__ c, int p,
+                                         double* __restrict__ dst) {
+  double x[kM];
+#pragma unroll
+  for (int n = 0; n < kM; n += 2) {
+    const double2 t = *reinterpret_cast<const double2*>(c + n);
+    x[n] = t.x;
+    x[n + 1] = p ? -t.y : t.y;  // (-1)^{pn}
+  }
+  l2l_group<0, 4>(BT, x, p, dst);
+  asm volatile("" ::: "memory");
+  l2l_group<4, 9>(BT, x, p, dst);
+  asm volatile("" ::: "memory");
+  l2l_group<9, 18>(BT, x, p, dst);
 }
 
 template <int VT, int DIR, int SMAX>
@@ -1039,21 +1108,13 @@ __global__ void __launch_bounds__(kDownThreads, 2) lc_down_kernel(const DownPara
           if (lane < kM) cur[it * kM + lane] = own + r;
         }
       } else {
-        // item = (group, sigma, node, v); warps of a round share the group when items >= 32
-        for (int q = tid; q < 3 * items; q += kDownThreads) {
-          const int grp = q / items;
-          const int it = q - grp * items;
+        // one thread per (sigma, node, v), all 18 outputs (B(0)^T rows broadcast)
+        for (int it = tid; it < items; it += kDownThreads) {
           const int v = it % VT;
           const int sn = it / VT;
           const int node = sn & (nodes - 1);
           const int sg = sn >> j;
-          const double* cpar = par + ((sg * (nodes >> 1) + (node >> 1)) * VT + v) * kM;
-          if (grp == 0)
-            l2l_rows<0, 4>(BTsh, cpar, node & 1, cur + it * kM);
-          else if (grp == 1)
-            l2l_rows<4, 9>(BTsh, cpar, node & 1, cur + it * kM);
-          else
-            l2l_rows<9, 18>(BTsh, cpar, node & 1, cur + it * kM);
+          l2l_node(BTsh, par + ((sg * (nodes >> 1) + (node >> 1)) * VT + v) * kM, node & 1, cur + it * kM);
         }
       }
       __syncthreads();
