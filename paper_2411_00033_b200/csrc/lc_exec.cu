@@ -186,7 +186,8 @@ __device__ __forceinline__ double l2l_warp(const BCol& cb, const double* __restr
 // flags (workspace ints): [0] up main-phase arrivals, [1] fine levels of w ready,
 // [2] finished level-0 continuations, [3] coarse levels of w ready, [4] finished
 // streaming CTAs, [5] predecessor complete (input readable), [10] next M2L unit,
-// [11] next band unit (dynamic schedule of the streaming kernel).
+// [11] next band unit (dynamic schedule of the streaming kernel), [12] streaming kernel
+// complete (for the down kernel), [13] down CTAs past that flag.
 struct UpParams {
   const double* in;
   const double* Tpad;  // [2][SMAX][M], zero rows m >= s
@@ -222,6 +223,7 @@ using StreamArgs = StreamParams;
 
 struct DownParams {
   double* out;
+  int* flags;
   const double* c;     // c_m2l
   const double* Tpad;  // [2][SMAX][M], zero rows m >= s
   const double* B;     // B(0) [M][M]
@@ -907,20 +909,20 @@ __global__ void __launch_bounds__(kStreamThreads, 2) lc_stream_kernel(const __gr
   }
   __syncthreads();
   LC_TS(1, 1);
-  if (tid == 0) s_last = atomicAdd(&P.flags[4], 1) == int(gridDim.x) - 1;
+  if (tid == 0) {
+    __threadfence();  // this CTA's c_m2l and band stores before its arrival
+    s_last = atomicAdd(&P.flags[4], 1) == int(gridDim.x) - 1;
+  }
   __syncthreads();
-  if (s_last) {  // the last CTA to finish re-arms the counters and flags for the next execution
+  if (s_last && tid == 0) {  // the last CTA re-arms the counters and releases the down kernel
     __threadfence();
-    if (tid == 0) {
-      P.flags[1] = 0;
-      P.flags[3] = 0;
-      P.flags[5] = 0;
-      P.flags[10] = 0;
-      P.flags[11] = 0;
-    }
-    __threadfence();
-    __syncthreads();
-    if (tid == 0) atomicExch(&P.flags[4], 0);
+    P.flags[1] = 0;
+    P.flags[3] = 0;
+    P.flags[5] = 0;
+    P.flags[10] = 0;
+    P.flags[11] = 0;
+    P.flags[4] = 0;
+    st_release(&P.flags[12], 1);  // streaming complete (read by lc_down_kernel instead of a grid wait)
   }
 }
 
@@ -1030,7 +1032,16 @@ __global__ void __launch_bounds__(kDownThreads, 2) lc_down_kernel(const DownPara
   for (int i = tid; i < SMAX * kM; i += kDownThreads) cp_async16(Tsh + 2 * i, P.Tpad + 2 * i);
   for (int i = tid; i < kMM; i += kDownThreads) BTsh[(i % kM) * kM + i / kM] = __ldg(P.B + i);
   griddep_launch();
-  griddep_wait();  // c_m2l and the band result (streaming kernel) are ready past this point
+  // c_m2l and the band result are complete once the streaming kernel's last CTA released
+  // flags[12] (cheaper than waiting for the grid to retire); the last down CTA to pass re-arms it
+  if (tid == 0) {
+    wait_flag(&P.flags[12]);
+    if (atomicAdd(&P.flags[13], 1) == int(gridDim.x * gridDim.y) - 1) {
+      P.flags[13] = 0;
+      P.flags[12] = 0;
+    }
+  }
+  __syncthreads();
   LC_TS(2, 1);
   const double* ct = P.c + tile * P.w_tile;
   if (L > 0) {
@@ -1442,7 +1453,7 @@ lc_status launch_execute(const lc_plan* p, const double* in, double* out, void* 
   sp.gr_up = p->grup;
   for (int i = 0; i < 32; ++i) sp.lvorder[i] = p->lvorder[i];
   DownParams dp{};
-  dp.out = out; dp.c = c; dp.Tpad = p->d_Tpad; dp.B = p->d_B; dp.ld_out = p->ld_out; dp.n = p->n; dp.N = p->N; dp.batch = p->batch;
+  dp.out = out; dp.flags = flags; dp.c = c; dp.Tpad = p->d_Tpad; dp.B = p->d_B; dp.ld_out = p->ld_out; dp.n = p->n; dp.N = p->N; dp.batch = p->batch;
   dp.w_tile = p->w_tile_doubles; dp.layout = p->layout; dp.L = int(p->L); dp.s = int(p->s); dp.k = p->k;
   const int64_t ndown = p->L > 0 ? (int64_t(2) << p->L) >> p->k : 1;
   const int64_t nsub = p->L > 0 ? (int64_t(4) << p->grup) : 1;
