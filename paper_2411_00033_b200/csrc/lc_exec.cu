@@ -1003,11 +1003,12 @@ __device__ __forceinline__ void l2l_node(const double* __restrict__ BT, const do
   l2l_group<9, 18>(BT, x, p, dst);
 }
 
-template <int VT, int DIR, int SMAX>
-__global__ void __launch_bounds__(kDownThreads, 2) lc_down_kernel(const DownParams P) {
+template <int VT, int DIR, int SMAX, int NT>
+__global__ void __launch_bounds__(NT, 512 / NT) lc_down_kernel(const DownParams P) {
   extern __shared__ __align__(128) unsigned char smem[];
   const int s = P.s, kd = P.k, L = P.L;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int nthr = NT, nwarps = NT / 32;  // 256, or 128 for many small vector tiles
   const int gd = L > 0 ? L - 1 - kd : 0;  // level of the subtree root
   const int VM = VT * kM;
   const int nleaf = 1 << kd;
@@ -1028,9 +1029,9 @@ __global__ void __launch_bounds__(kDownThreads, 2) lc_down_kernel(const DownPara
   auto cm_lvl = [&](int j) { return cm + (gd + (1 << j) - 1) * 2 * VM; };
   LC_TS(2, 0);
   // plan data first: B(0) and T(sigma) (padded to SMAX rows) into shared memory
-  for (int i = tid; i < kMM / 2; i += kDownThreads) cp_async16(Bsh + 2 * i, P.B + 2 * i);
-  for (int i = tid; i < SMAX * kM; i += kDownThreads) cp_async16(Tsh + 2 * i, P.Tpad + 2 * i);
-  for (int i = tid; i < kMM; i += kDownThreads) BTsh[(i % kM) * kM + i / kM] = __ldg(P.B + i);
+  for (int i = tid; i < kMM / 2; i += nthr) cp_async16(Bsh + 2 * i, P.B + 2 * i);
+  for (int i = tid; i < SMAX * kM; i += nthr) cp_async16(Tsh + 2 * i, P.Tpad + 2 * i);
+  for (int i = tid; i < kMM; i += nthr) BTsh[(i % kM) * kM + i / kM] = __ldg(P.B + i);
   griddep_launch();
   // c_m2l and the band result are complete once the streaming kernel's last CTA released
   // flags[12] (cheaper than waiting for the grid to retire); the last down CTA to pass re-arms it
@@ -1050,7 +1051,7 @@ __global__ void __launch_bounds__(kDownThreads, 2) lc_down_kernel(const DownPara
       for (int sg = 0; sg < 2; ++sg) {
         const double* src = ct + (w_level_offset_units(g) + sg * nseg(g) + a) * VM;
         double* dst = cm_anc(g) + sg * VM;
-        for (int i = tid; i < VM / 2; i += kDownThreads) cp_async16(dst + 2 * i, src + 2 * i);
+        for (int i = tid; i < VM / 2; i += nthr) cp_async16(dst + 2 * i, src + 2 * i);
       }
     }
     for (int j = 0; j <= kd; ++j) {
@@ -1059,7 +1060,7 @@ __global__ void __launch_bounds__(kDownThreads, 2) lc_down_kernel(const DownPara
       for (int sg = 0; sg < 2; ++sg) {
         const double* src = ct + (w_level_offset_units(g) + sg * nseg(g) + (R << j)) * VM;
         double* dst = cm_lvl(j) + sg * (1 << j) * VM;
-        for (int i = tid; i < cnt2; i += kDownThreads) cp_async16(dst + 2 * i, src + 2 * i);
+        for (int i = tid; i < cnt2; i += nthr) cp_async16(dst + 2 * i, src + 2 * i);
       }
     }
   }
@@ -1068,7 +1069,7 @@ __global__ void __launch_bounds__(kDownThreads, 2) lc_down_kernel(const DownPara
   for (int v = 0; v < VT; ++v) {
     const int64_t gv = tile * VT + v;
     const int lim = gv < P.batch ? olim : 0;
-    for (int x = tid; x < rows; x += kDownThreads) {
+    for (int x = tid; x < rows; x += nthr) {
       const bool ok = x < lim;
       const double* src = P.layout == LC_VEC_CONTIGUOUS ? P.out + gv * P.ld_out + i0 + x : P.out + (i0 + x) * P.ld_out + gv;
       cp_async8(zb + v * rows + x, ok ? src : P.out, ok ? 8u : 0u);
@@ -1082,7 +1083,7 @@ __global__ void __launch_bounds__(kDownThreads, 2) lc_down_kernel(const DownPara
   if (L > 0) {
     // step 4 along the ancestor chain (Horner), one warp per (sigma, v), then the subtree root
     if (gd > 0) {
-      for (int ch = warp; ch < 2 * VT; ch += kDownWarps) {
+      for (int ch = warp; ch < 2 * VT; ch += nwarps) {
         double acc = lane < kM ? cm_anc(0)[ch * kM + lane] : 0.0;
         double* scr = cm_anc(0) + ch * kM;  // the running vector is kept in place of c_m2l(0)
         for (int g = 1; g <= gd; ++g) {
@@ -1108,8 +1109,8 @@ __global__ void __launch_bounds__(kDownThreads, 2) lc_down_kernel(const DownPara
       const double* par = cm_lvl(j - 1);
       double* cur = cm_lvl(j);
       const int items = 2 * nodes * VT;
-      if (items <= 2 * kDownWarps) {
-        for (int it = warp; it < items; it += kDownWarps) {
+      if (items <= 2 * nwarps) {
+        for (int it = warp; it < items; it += nwarps) {
           const int v = it % VT;
           const int sn = it / VT;
           const int node = sn & (nodes - 1);
@@ -1120,7 +1121,7 @@ __global__ void __launch_bounds__(kDownThreads, 2) lc_down_kernel(const DownPara
         }
       } else {
         // one thread per (sigma, node, v), all 18 outputs (B(0)^T rows broadcast)
-        for (int it = tid; it < items; it += kDownThreads) {
+        for (int it = tid; it < items; it += nthr) {
           const int v = it % VT;
           const int sn = it / VT;
           const int node = sn & (nodes - 1);
@@ -1144,7 +1145,7 @@ __global__ void __launch_bounds__(kDownThreads, 2) lc_down_kernel(const DownPara
       }
       const double* cl = cm_lvl(kd);
       const int per = nleaf * VT;
-      for (int it = warp >> 1; it < per; it += kDownWarps / 2) {
+      for (int it = warp >> 1; it < per; it += (nwarps / 2)) {
         const int u = it / VT, v = it - u * VT;
         const double* cp = cl + ((sg * nleaf + u) * VT + v) * kM;
         double c[kM];
@@ -1165,7 +1166,7 @@ __global__ void __launch_bounds__(kDownThreads, 2) lc_down_kernel(const DownPara
       }
       if (SMAX > 32) {  // rows m = 32..s-1 (s_hat = 64 plans): T rows of lane + 32 from global
         const int m = lane + 32;
-        for (int it = warp >> 1; it < per; it += kDownWarps / 2) {
+        for (int it = warp >> 1; it < per; it += (nwarps / 2)) {
           const int u = it / VT, v = it - u * VT;
           const double* cp = cl + ((sg * nleaf + u) * VT + v) * kM;
           const double* tp = Tsh + (sg * SMAX + (m < SMAX ? m : 0)) * kM;
@@ -1185,7 +1186,7 @@ __global__ void __launch_bounds__(kDownThreads, 2) lc_down_kernel(const DownPara
   for (int v = 0; v < VT; ++v) {
     const int64_t gv = tile * VT + v;
     if (gv >= P.batch) break;
-    for (int ii = tid; ii < olim; ii += kDownThreads) {
+    for (int ii = tid; ii < olim; ii += nthr) {
       const int64_t i = i0 + ii;
       double z = zb[v * rows + ii];
       if (DIR == 0) z *= (i == 0 ? inv_pi : 2.0 * inv_pi);
@@ -1214,8 +1215,10 @@ static cudaError_t set_attrs_vt(int smax) {
   cudaError_t e = set_max_dyn_smem(lc_up_kernel<VT, SMAX>, smax);
   if (e == cudaSuccess) e = set_max_dyn_smem(lc_stream_kernel<VT, 0>, smax);
   if (e == cudaSuccess) e = set_max_dyn_smem(lc_stream_kernel<VT, 1>, smax);
-  if (e == cudaSuccess) e = set_max_dyn_smem(lc_down_kernel<VT, 0, SMAX>, smax);
-  if (e == cudaSuccess) e = set_max_dyn_smem(lc_down_kernel<VT, 1, SMAX>, smax);
+  if (e == cudaSuccess) e = set_max_dyn_smem(lc_down_kernel<VT, 0, SMAX, kDownThreads>, smax);
+  if (e == cudaSuccess) e = set_max_dyn_smem(lc_down_kernel<VT, 1, SMAX, kDownThreads>, smax);
+  if (e == cudaSuccess) e = set_max_dyn_smem(lc_down_kernel<VT, 0, SMAX, kDownThreads / 2>, smax);
+  if (e == cudaSuccess) e = set_max_dyn_smem(lc_down_kernel<VT, 1, SMAX, kDownThreads / 2>, smax);
   return e;
 }
 template <int SMAX>
@@ -1378,7 +1381,8 @@ static cudaError_t launch_vt(const lc_plan* p, const UpParams& up, const StreamP
     UpArgs<SMAX> ua;
     ua.p = up;
     cfg.gridDim = grid_up;
-    cfg.blockDim = dim3(kThreads);
+    // many small vector tiles: 128-thread CTAs (four per SM) overlap their latency-bound phases
+    cfg.blockDim = dim3(p->ntiles >= 64 ? kThreads / 2 : kThreads);
     cfg.dynamicSmemBytes = p->smem_up;
     e = cudaLaunchKernelEx(&cfg, lc_up_kernel<VT, SMAX>, ua);
     if (e != cudaSuccess) return e;
@@ -1391,9 +1395,14 @@ static cudaError_t launch_vt(const lc_plan* p, const UpParams& up, const StreamP
   if (e != cudaSuccess) return e;
   if (ev && evi < nev) cudaEventRecord(ev[evi++], st);
   cfg.gridDim = grid_down;
-  cfg.blockDim = dim3(kDownThreads);
   cfg.dynamicSmemBytes = p->smem_down;
-  e = cudaLaunchKernelEx(&cfg, lc_down_kernel<VT, DIR, SMAX>, dp);
+  if (p->ntiles >= 64) {  // many small vector tiles: 4-warp CTAs, four per SM
+    cfg.blockDim = dim3(kDownThreads / 2);
+    e = cudaLaunchKernelEx(&cfg, lc_down_kernel<VT, DIR, SMAX, kDownThreads / 2>, dp);
+  } else {
+    cfg.blockDim = dim3(kDownThreads);
+    e = cudaLaunchKernelEx(&cfg, lc_down_kernel<VT, DIR, SMAX, kDownThreads>, dp);
+  }
   if (e != cudaSuccess) return e;
   if (ev && evi < nev) cudaEventRecord(ev[evi++], st);
   return cudaGetLastError();
