@@ -1381,8 +1381,10 @@ static cudaError_t launch_vt(const lc_plan* p, const UpParams& up, const StreamP
     UpArgs<SMAX> ua;
     ua.p = up;
     cfg.gridDim = grid_up;
-    // many small vector tiles: 128-thread CTAs (four per SM) overlap their latency-bound phases
-    cfg.blockDim = dim3(p->ntiles >= 64 ? kThreads / 2 : kThreads);
+    // many CTAs (small vector tiles or deep trees): 128-thread CTAs (four per SM) overlap their
+    // latency-bound phases
+    const bool small_up = int64_t(grid_up.x) * grid_up.y > 8 * p->sm_count && p->smem_up <= 56 * 1024;
+    cfg.blockDim = dim3(small_up ? kThreads / 2 : kThreads);
     cfg.dynamicSmemBytes = p->smem_up;
     e = cudaLaunchKernelEx(&cfg, lc_up_kernel<VT, SMAX>, ua);
     if (e != cudaSuccess) return e;
@@ -1396,7 +1398,8 @@ static cudaError_t launch_vt(const lc_plan* p, const UpParams& up, const StreamP
   if (ev && evi < nev) cudaEventRecord(ev[evi++], st);
   cfg.gridDim = grid_down;
   cfg.dynamicSmemBytes = p->smem_down;
-  if (p->ntiles >= 64) {  // many small vector tiles: 4-warp CTAs, four per SM
+  if (int64_t(grid_down.x) * grid_down.y > 8 * p->sm_count && p->smem_down <= 56 * 1024) {
+    // many small CTAs: 4-warp CTAs, four per SM
     cfg.blockDim = dim3(kDownThreads / 2);
     e = cudaLaunchKernelEx(&cfg, lc_down_kernel<VT, DIR, SMAX, kDownThreads / 2>, dp);
   } else {
