@@ -149,3 +149,56 @@ def test_back_to_back_same_plan_different_inputs(direction):
         for rep in range(2):
             z = outs[2 * q + rep].cpu().numpy()[0][rows]
             assert oracle.einf(z, ref) <= GATE, (q, rep)
+
+
+def test_two_plans_share_one_workspace():
+    # leg2cheb and cheb2leg plans of one length alternate on one caller-owned workspace (the flags
+    # and counters it holds are re-armed by the kernels that consume them)
+    dev = _dev()
+    n = 250000
+    pl, pc = _plan(n, "leg2cheb", device=dev), _plan(n, "cheb2leg", device=dev)
+    assert pl.workspace_bytes == pc.workspace_bytes
+    ws = pl.new_workspace()
+    x = torch.from_numpy(vector("uniform_r0.5", n, seed=31)).reshape(1, -1).to(dev)
+    ys, zs = [], []
+    for _ in range(3):
+        y = pl.execute(x, workspace=ws)
+        ys.append(y)
+        zs.append(pc.execute(y, workspace=ws))
+    torch.cuda.synchronize()
+    rows = np.r_[0:100, np.linspace(100, n - 1, 200).astype(np.int64)]
+    ref = _ref("leg2cheb", x.cpu().numpy()[0], rows)
+    for y, z in zip(ys, zs):
+        assert oracle.einf(y.cpu().numpy()[0][rows], ref) <= GATE
+        assert float((z - x).abs().max() / x.abs().max()) <= 2e-14  # round trip (SPEC acceptance 2)
+
+
+def test_concurrent_streams_distinct_workspaces():
+    # one plan executed concurrently on two streams with distinct workspaces (legcheb.h contract)
+    dev = _dev()
+    n = 200000
+    p = _plan(n, "leg2cheb", device=dev)
+    ws = [p.new_workspace(), p.new_workspace()]
+    xs = [torch.from_numpy(vector("uniform_r0.5", n, seed=sd)).reshape(1, -1).to(dev) for sd in (41, 42)]
+    st = [torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)]
+    torch.cuda.synchronize()
+    outs = [None, None]
+    for _ in range(3):
+        for i in range(2):
+            with torch.cuda.stream(st[i]):
+                outs[i] = p.execute(xs[i], workspace=ws[i], stream=st[i])
+    torch.cuda.synchronize()
+    rows = np.r_[0:100, np.linspace(100, n - 1, 200).astype(np.int64)]
+    for i in range(2):
+        ref = _ref("leg2cheb", xs[i].cpu().numpy()[0], rows)
+        assert oracle.einf(outs[i].cpu().numpy()[0][rows], ref) <= GATE
+
+
+def test_kernel_info_consistent():
+    dev = _dev()
+    p = _plan(1_000_000, "leg2cheb", device=dev)
+    ki = p.kernel_info
+    d = p.desc
+    assert ki["vt"] == d["vt"] and ki["kd"] == d["subtree"] and ki["cb"] == d["stage_blocks"]
+    assert ki["stream_grid"] <= ki["stream_occ"] * torch.cuda.get_device_properties(dev).multi_processor_count
+    assert ki["m2l_units"] > 0 and ki["band_units"] > 0 and p.kernels_per_execute == 3
