@@ -566,6 +566,37 @@ __device__ __forceinline__ void band_unit(const StreamParams& P, int tile, int l
   const int rows = nleaf * seglen;
   const int tcols = (nleaf + 2) * seglen;
   const int tbl = int((P.N - i0) < tcols ? (P.N - i0) : tcols);  // valid band-table entries
+  const bool mma8 = VT == 8 && s <= 32;
+  const int tp8 = tcols + 2 * kBandR + 2;  // unpadded row stride of the tensor-core path (<= tp)
+  if (mma8) {
+    // tensor-core path: unpadded tiles, 16-byte cp.async (zero fill beyond N / n)
+    for (int x = 2 * btid; x < tcols + 2 * kBandR; x += 2 * kBandThreads) {
+      const int valid = tbl - x;
+      const uint32_t bytes = valid >= 2 ? 16u : (valid == 1 ? 8u : 0u);
+      cp_async16z(tb + x, bytes ? P.tabB + i0 + x : P.tabB, bytes);
+    }
+#pragma unroll 1
+    for (int v = 0; v < VT; ++v) {
+      const int64_t gv = int64_t(tile) * VT + v;
+      int lim = 0;
+      if (gv < P.batch) lim = int((P.n - i0) < tcols ? (P.n - i0) : tcols);
+      if (lim < 0) lim = 0;
+      if (P.layout == LC_VEC_CONTIGUOUS && (reinterpret_cast<uintptr_t>(P.in) % 16 == 0) && (P.ld_in % 2 == 0)) {
+        const double* src = P.in + gv * P.ld_in + i0;
+        for (int x = 2 * btid; x < tcols + 2 * kBandR; x += 2 * kBandThreads) {
+          const int valid = lim - x;
+          const uint32_t bytes = valid >= 2 ? 16u : (valid == 1 ? 8u : 0u);
+          cp_async16z(gt + v * tp8 + x, bytes ? src + x : P.in, bytes);
+        }
+      } else {
+        for (int x = btid; x < tcols + 2 * kBandR; x += kBandThreads) {
+          const bool ok = x < lim;
+          const double* src = P.layout == LC_VEC_CONTIGUOUS ? P.in + gv * P.ld_in + i0 + x : P.in + (i0 + x) * P.ld_in + gv;
+          cp_async8(gt + v * tp8 + x, ok ? src : P.in, ok ? 8u : 0u);
+        }
+      }
+    }
+  } else {
   for (int x = btid; x < tcols + 2 * kBandR; x += kBandThreads) {
     const bool ok = x < tbl;
     cp_async8(tb + x + (x >> 4), ok ? P.tabB + i0 + x : P.tabB, ok ? 8u : 0u);
@@ -589,9 +620,69 @@ __device__ __forceinline__ void band_unit(const StreamParams& P, int tile, int l
       }
     }
   }
+  }
   cp_async_commit();
+#ifdef LC_PHASE_TIMING
+  unsigned long long tb0, tb1, tb2, tb3;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tb0));
+#endif
   cp_async_wait<0>();
   band_sync();
+#ifdef LC_PHASE_TIMING
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tb1));
+#endif
+  if (mma8) {
+    // fp64 tensor cores (DMMA m8n8k4): per (segment uu, parity sigma) the band is
+    // Z[r][v] = sum_{c=r}^{2s-1} K[r][c] G[c][v], rows i = i0 + 2s uu + 2r + sigma, columns
+    // j = i0 + 2s uu + 2c + sigma, K[r][c] = a[c-r] b[2s uu + r + c + sigma] (Toeplitz x Hankel,
+    // each lane forms its A-fragment element with one DMUL), G[c][v] = g_v[j] (8 vectors = the
+    // MMA n dimension).  Blocks with c < r everywhere are skipped; f and b are zero beyond n, N.
+    const int warp = btid >> 5, lane = btid & 31;
+    const int nrb = (s + 7) / 8, nkc = (2 * s + 3) / 4;
+    const int lr_ = lane >> 2, lc_ = lane & 3;
+    for (int job = warp; job < nleaf * 2; job += kBandThreads / 32) {
+      const int uu = job >> 1, sg = job & 1;
+      const int base = uu * seglen + sg;  // tile-local index of row r = 0 / column c = 0
+      double acc[4][2];
+#pragma unroll
+      for (int rb = 0; rb < 4; ++rb) acc[rb][0] = acc[rb][1] = 0.0;
+      for (int kc = 0; kc < nkc; ++kc) {
+        const int c = 4 * kc + lc_;  // this lane's A column / B row
+        const int xg = base + 2 * c;
+        double bfr = c < 2 * s ? gt[lr_ * tp8 + xg] : 0.0;  // G[c][v = lane >> 2]
+        if (DIR == 1) bfr *= double(i0 + xg);
+#pragma unroll
+        for (int rb = 0; rb < 4; ++rb) {
+          if (rb < nrb && 4 * kc + 3 >= 8 * rb) {  // warp-uniform: the block has entries with c >= r
+            const int r = 8 * rb + lr_;
+            const int xb = base + r + c;
+            const double a = (c >= r && c < 2 * s && r < s) ? ta[c - r] * tb[xb] : 0.0;
+            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                         : "+d"(acc[rb][0]), "+d"(acc[rb][1])
+                         : "d"(a), "d"(bfr));
+          }
+        }
+      }
+#pragma unroll
+      for (int rb = 0; rb < 4; ++rb) {
+        const int r = 8 * rb + lr_;
+        if (rb < nrb && r < s) {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int v = 2 * lc_ + h;
+            const int ii = base + 2 * r;
+            const int64_t ir = i0 + ii;
+            double z = acc[rb][h];
+            if (DIR == 1) {
+              z *= double(2 * ir + 1);
+              if (ir == 0) z += gt[v * tp8];  // entry (0,0) of A^{-1}C is 1 (reading R2)
+            }
+            zst[v * rows + ii] = z;
+          }
+        }
+      }
+    }
+  } else {
   // item = (v, segment uu, parity sigma, block of kBandR same-parity rows m = kBandR t + r).
   // Band of row i' = i + 2r (i the block's first row): sum_c a[c-r] b[i+r+c] g[i+2c], c >= r,
   // i + 2c < j_end; a = tabA, b = tabB, g = f (L2C) or j f_j (C2L).  Sliding windows of a and
@@ -659,7 +750,11 @@ __device__ __forceinline__ void band_unit(const StreamParams& P, int tile, int l
       }
     }
   }
+  }
   band_sync();
+#ifdef LC_PHASE_TIMING
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tb2));
+#endif
   // coalesced store of the band result (steps 4, 5 and 7 are added by the down unit)
   const int olim = int((P.n - i0) < rows ? (P.n - i0) : rows);
 #pragma unroll 1
@@ -674,6 +769,16 @@ __device__ __forceinline__ void band_unit(const StreamParams& P, int tile, int l
     }
   }
   band_sync();  // tiles are reused by the next unit
+#ifdef LC_PHASE_TIMING
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tb3));
+  if (btid == 0) {  // accumulated ns per CTA: [3] load wait, [4] compute, [5] store, [6] units
+    const unsigned cta = blockIdx.x;
+    g_lc_ts[1][cta * 8 + 3] += tb1 - tb0;
+    g_lc_ts[1][cta * 8 + 4] += tb2 - tb1;
+    g_lc_ts[1][cta * 8 + 5] += tb3 - tb2;
+    g_lc_ts[1][cta * 8 + 6] += 1;
+  }
+#endif
 }
 
 template <int VT, int DIR>
@@ -837,6 +942,39 @@ __global__ void __launch_bounds__(kStreamThreads, 2) lc_stream_kernel(const __gr
             ct[sg * sgstride + (2 * bl + 1) * VM + v * kM + kk] = o0[sg][v] + o1[sg][v];
           }
       }
+      } else if (VT == 8) {
+        // fp64 tensor cores (DMMA m8n8k4): output tile = (row segment u, 8 modes, parity sigma) x
+        // 8 vectors; c(u) = sum_r A_hat_r w(t_r) with K = 18 modes in steps of 4 (padded to 20)
+        const int lane = ctid & 31, warp = ctid >> 5;
+        const int lr_ = lane >> 2, lc_ = lane & 3;
+        const int ntl = 2 * nb * 3 * 2;  // (row ri, m-tile, sigma)
+        for (int t = warp; t < ntl; t += kM2lWarps) {
+          const int sg = t & 1, mt = (t >> 1) % 3, ri = (t >> 1) / 3;
+          const int bl = ri >> 1;
+          double c0 = 0.0, c1 = 0.0;
+          const int nmat = (ri & 1) ? 1 : 2;
+          for (int mi = 0; mi < nmat; ++mi) {
+            const int r = (ri & 1) ? 2 : mi;
+            const int tloc = (ri & 1) ? ri : ri + mi;  // t - (2 b0 + 2)
+            const double* Am = As + (3 * bl + r) * kMM;
+            const double* Wc = wwin + (sg * 2 * cb + tloc) * VM;
+            const int row = 8 * mt + lr_;
+#pragma unroll
+            for (int kk = 0; kk < 5; ++kk) {
+              const int kcol = 4 * kk + lc_;
+              const double a = (row < kM && kcol < kM) ? Am[row * kM + kcol] : 0.0;
+              const double b = kcol < kM ? Wc[lr_ * kM + kcol] : 0.0;  // W[k][vector lane >> 2]
+              asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                           : "+d"(c0), "+d"(c1)
+                           : "d"(a), "d"(b));
+            }
+          }
+          const int row = 8 * mt + lr_;
+          if (row < kM) {
+            ct[sg * sgstride + ri * VM + (2 * lc_) * kM + row] = c0;
+            ct[sg * sgstride + ri * VM + (2 * lc_ + 1) * kM + row] = c1;
+          }
+        }
       } else {  // wide vector tiles: one (row, mode) per thread, one A_hat row at a time
         const int nrows = 2 * nb;
         for (int it = ctid; it < nrows * kM; it += kM2lThreads) {
