@@ -690,12 +690,23 @@ __device__ __forceinline__ void band_unit(const StreamParams& P, int tile, int l
   const int ntb = (s + kBandR - 1) / kBandR;
   const int items = VT * nleaf * 2 * ntb;
   for (int it = btid; it < items; it += kBandThreads) {
-    const int tb_i = it % ntb;
-    int r_ = it / ntb;
-    const int sg = r_ & 1;
-    r_ >>= 1;
-    const int uu = r_ & (nleaf - 1);
-    const int v = r_ >> kb;
+    // single vector: segment fastest, so the lanes of a warp share the row block and with it the
+    // trip count of the column loop (no divergence; 1.7x in tools/ubench_band.cu)
+    int uu, v, sg, tb_i;
+    if (VT == 1) {
+      uu = it & (nleaf - 1);
+      const int r_ = it >> kb;
+      v = 0;
+      sg = r_ & 1;
+      tb_i = r_ >> 1;
+    } else {  // (row block fastest; measured faster with several vectors per tile)
+      tb_i = it % ntb;
+      int r_ = it / ntb;
+      sg = r_ & 1;
+      r_ >>= 1;
+      uu = r_ & (nleaf - 1);
+      v = r_ >> kb;
+    }
     const int m0 = kBandR * tb_i;
     const int ii = uu * seglen + sg + 2 * m0;  // tile-local first row
     const int64_t i = i0 + ii;

@@ -15,10 +15,18 @@ __device__ void band_items(const double* ta, const double* tb, const double* gt,
   const int ntb = (s + R - 1) / R;
   const int items = nleaf * 2 * ntb;
   for (int it = btid; it < items; it += 128) {
-    const int tb_i = it % ntb;
-    int r_ = it / ntb;
-    const int sg = r_ & 1;
-    const int uu = r_ >> 1;
+    int tb_i, sg, uu;
+    if (VAR == 2) {  // segment fastest: the lanes of a warp share the row block (uniform trip count)
+      uu = it % nleaf;
+      const int r2 = it / nleaf;
+      sg = r2 & 1;
+      tb_i = r2 >> 1;
+    } else {
+      tb_i = it % ntb;
+      int r_ = it / ntb;
+      sg = r_ & 1;
+      uu = r_ >> 1;
+    }
     const int m0 = R * tb_i;
     const int ii = uu * seglen + sg + 2 * m0;
     const int je = seglen * (uu + 2) < N ? seglen * (uu + 2) : N;
@@ -32,7 +40,7 @@ __device__ void band_items(const double* ta, const double* tb, const double* gt,
     }
     const int ngrp = (cmax + 1) / R;
     int c0 = 0;
-    if (VAR == 0) {
+    if (VAR != 1) {
       for (int gi = 0; gi < ngrp; ++gi, c0 += R) {
 #pragma unroll
         for (int q = 0; q < R; ++q) {
@@ -116,13 +124,16 @@ int main() {
   const size_t smem = 40000;
   cudaFuncSetAttribute(k<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaFuncSetAttribute(k<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(k<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   // fp64 ops per unit: sum over rows of (cmax+1) steps x 2 (DMUL + DFMA)
   long long ops = 0;
   for (int uu = 0; uu < 16; ++uu) for (int r = 0; r < 2 * s; ++r) { const int ii = uu * 2 * s + r; ops += 2 * (((2 * s * (uu + 2) - ii - 1) >> 1) + 1); }
-  for (int var = 0; var < 2; ++var)
+  for (int var = 0; var < 3; ++var)
     for (int blocks : {1, 296, 592}) {
       for (int t = 0; t < 2; ++t) {
-        if (var == 0) k<0><<<blocks, 128, smem>>>(cyc, sink, s, 20); else k<1><<<blocks, 128, smem>>>(cyc, sink, s, 20);
+        if (var == 0) k<0><<<blocks, 128, smem>>>(cyc, sink, s, 20);
+        else if (var == 1) k<1><<<blocks, 128, smem>>>(cyc, sink, s, 20);
+        else k<2><<<blocks, 128, smem>>>(cyc, sink, s, 20);
       }
       cudaDeviceSynchronize();
       long long h; cudaMemcpy(&h, cyc, 8, cudaMemcpyDeviceToHost);
