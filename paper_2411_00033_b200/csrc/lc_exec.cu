@@ -118,6 +118,14 @@ __device__ __forceinline__ void wait_geq(const int* p, int target) {  // wrap-sa
   while (ld_acquire(p) - target < 0) __nanosleep(64);
 }
 
+// fp64 tensor-core MMA (DMMA m8n8k4, row.col): lane l holds A[l>>2][l&3], B[l&3][l>>2] and
+// C[l>>2][2(l&3)], C[l>>2][2(l&3)+1]; d += A B.
+__device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+
 // Phase timestamps for the debug build (-DLC_PHASE_TIMING): %globaltimer (ns) per CTA and phase.
 #ifdef LC_PHASE_TIMING
 __device__ unsigned long long g_lc_ts[3][1 << 20];
@@ -301,38 +309,6 @@ __device__ __forceinline__ void m2m_level(const double* __restrict__ Bs, const d
   }
 }
 
-// step 1 for one (leaf, 6 modes 6KG..6KG+5), both parities: the f pair (f_2m, f_2m+1) is one
-// 16-byte shared load, T(sigma)[m][6KG..] three 16-byte broadcast loads per parity.
-// Rows m >= s of the staged T are zero: the loop runs to SMAX without a branch (the f reads
-// beyond the segment stay inside the zero-padded shared tile).
-template <int SMAX, int KG>
-__device__ __forceinline__ void step1_item(const double* __restrict__ Ts, const double* __restrict__ fp,
-                                           double* __restrict__ o0, double* __restrict__ o1) {
-  double a[6], b[6];
-#pragma unroll
-  for (int i = 0; i < 6; ++i) a[i] = b[i] = 0.0;
-#pragma unroll 8
-  for (int m = 0; m < SMAX; ++m) {
-    const double2 f2 = *reinterpret_cast<const double2*>(fp + 2 * m);
-    const double* t0 = Ts + m * kM + 6 * KG;
-    const double* t1 = Ts + (SMAX + m) * kM + 6 * KG;
-#pragma unroll
-    for (int i = 0; i < 6; i += 2) {
-      const double2 u0 = *reinterpret_cast<const double2*>(t0 + i);
-      const double2 u1 = *reinterpret_cast<const double2*>(t1 + i);
-      a[i] = fma(f2.x, u0.x, a[i]);
-      a[i + 1] = fma(f2.x, u0.y, a[i + 1]);
-      b[i] = fma(f2.y, u1.x, b[i]);
-      b[i + 1] = fma(f2.y, u1.y, b[i + 1]);
-    }
-  }
-#pragma unroll
-  for (int i = 0; i < 6; i += 2) {
-    *reinterpret_cast<double2*>(o0 + 6 * KG + i) = make_double2(a[i], a[i + 1]);
-    *reinterpret_cast<double2*>(o1 + 6 * KG + i) = make_double2(b[i], b[i + 1]);
-  }
-}
-
 template <int VT, int SMAX>
 __global__ void __launch_bounds__(kThreads, 2) lc_up_kernel(const __grid_constant__ UpArgs<SMAX> A) {
   extern __shared__ __align__(128) unsigned char smem[];
@@ -406,24 +382,46 @@ __global__ void __launch_bounds__(kThreads, 2) lc_up_kernel(const __grid_constan
   __syncthreads();
   LC_TS(0, 1);
 
-  // step 1: w(L-1)[t][k] = sum_m f[2s t + 2m + sigma] T(sigma)[m][k]   (eq:wMM)
-  // item = (mode group kg of 6, v, leaf); a warp shares kg whenever VT * nleaf >= 32.
+  // step 1: w(L-1)[t][k] = sum_m f[2s t + 2m + sigma] T(sigma)[m][k]   (eq:wMM), on the fp64
+  // tensor cores: one warp item = (vector v, 8 leaves); A = T(sigma)^T (modes padded to 24 = 3
+  // row tiles), B[m][leaf] = f[2s leaf + 2m + sigma] (one 16-byte load feeds both parities),
+  // K = SMAX rows of T (rows m >= s are zero, so the reads past a segment contribute nothing).
   {
     double* leaf = tree + tree_off(k);
-    const int per = VT * nleaf;
-    for (int it = tid; it < 3 * per; it += blockDim.x) {
-      const int kg = it / per;
-      const int r = it - kg * per;
-      const int v = r / nleaf, lf = r - v * nleaf;
-      const double* fp = fs + (v * nleaf + lf) * fst;
-      double* o0 = leaf + (lf * VT + v) * kM;
-      double* o1 = leaf + ((nleaf + lf) * VT + v) * kM;
-      if (kg == 0)
-        step1_item<SMAX, 0>(Ts, fp, o0, o1);
-      else if (kg == 1)
-        step1_item<SMAX, 1>(Ts, fp, o0, o1);
-      else
-        step1_item<SMAX, 2>(Ts, fp, o0, o1);
+    const int warp = tid >> 5, lane = tid & 31, nw = blockDim.x >> 5;
+    const int lr = lane >> 2, lc = lane & 3;
+    const int ngrp = (nleaf + 7) >> 3;
+    for (int item = warp; item < VT * ngrp; item += nw) {
+      const int v = item / ngrp, lf0 = (item - v * ngrp) * 8;
+      const bool okb = lf0 + lr < nleaf;  // this lane's B column
+      const double* fp = fs + (v * nleaf + (okb ? lf0 + lr : 0)) * fst + 2 * lc;
+      const double* tq = Ts + lc * kM + lr;
+      double acc[2][3][2];
+#pragma unroll
+      for (int mt = 0; mt < 3; ++mt) acc[0][mt][0] = acc[0][mt][1] = acc[1][mt][0] = acc[1][mt][1] = 0.0;
+#pragma unroll 4
+      for (int kk = 0; kk < SMAX / 4; ++kk) {
+        double2 f2 = *reinterpret_cast<const double2*>(fp + 8 * kk);  // f[2m], f[2m+1], m = 4kk + lc
+        if (!okb) f2 = make_double2(0.0, 0.0);
+        const double* t0 = tq + 4 * kk * kM;  // T(0)[m][8 mt + lr]
+#pragma unroll
+        for (int mt = 0; mt < 3; ++mt) {
+          const bool okm = 8 * mt + lr < kM;
+          const double a0 = okm ? t0[8 * mt] : 0.0;
+          const double a1 = okm ? t0[SMAX * kM + 8 * mt] : 0.0;
+          dmma(acc[0][mt], a0, f2.x);
+          dmma(acc[1][mt], a1, f2.y);
+        }
+      }
+#pragma unroll
+      for (int sg = 0; sg < 2; ++sg)
+#pragma unroll
+        for (int mt = 0; mt < 3; ++mt)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int lf = lf0 + 2 * lc + h, mode = 8 * mt + lr;
+            if (lf < nleaf && mode < kM) leaf[((sg * nleaf + lf) * VT + v) * kM + mode] = acc[sg][mt][h];
+          }
     }
   }
   __syncthreads();
@@ -1281,49 +1279,40 @@ __global__ void __launch_bounds__(NT, 512 / NT) lc_down_kernel(const DownParams 
       __syncthreads();
     }
     LC_TS(2, 4);
-    // step 5: z^sigma += c(L-1) T(sigma)^T (eq:step5): warp = (sigma = warp & 1, leaf group),
-    // lane = row m, c of the leaf broadcast from shared memory
+    // step 5: z^sigma += c(L-1) T(sigma)^T (eq:step5) on the fp64 tensor cores: warp item =
+    // (sigma, v, 8 leaves); A = T(sigma) (SMAX/8 row tiles of m, K = 18 modes padded to 20),
+    // B[k][leaf] = c(L-1)[leaf][k]; the result is added to the band result in zb.
     {
-      const int sg = warp & 1;
-      double trow[kM];  // T(sigma)[m][.] of this lane's row m
-#pragma unroll
-      for (int k = 0; k < kM; k += 2) {
-        const double2 t2 = *reinterpret_cast<const double2*>(Tsh + (sg * SMAX + (lane < SMAX ? lane : 0)) * kM + k);
-        trow[k] = t2.x;
-        trow[k + 1] = t2.y;
-      }
+      const int lr = lane >> 2, lc = lane & 3;
       const double* cl = cm_lvl(kd);
-      const int per = nleaf * VT;
-      for (int it = warp >> 1; it < per; it += (nwarps / 2)) {
-        const int u = it / VT, v = it - u * VT;
-        const double* cp = cl + ((sg * nleaf + u) * VT + v) * kM;
-        double c[kM];
+      const int ngrp = (nleaf + 7) >> 3;
+      for (int item = warp; item < 2 * VT * ngrp; item += nwarps) {
+        const int sg = item & 1, r_ = item >> 1;
+        const int v = r_ / ngrp, lf0 = (r_ - v * ngrp) * 8;
+        const bool okb = lf0 + lr < nleaf;
+        const double* cp = cl + ((sg * nleaf + (okb ? lf0 + lr : 0)) * VT + v) * kM;
+        const double* tq = Tsh + (sg * SMAX + lr) * kM;
+        double acc[SMAX / 8][2];
 #pragma unroll
-        for (int k = 0; k < kM; k += 2) {
-          const double2 t = *reinterpret_cast<const double2*>(cp + k);
-          c[k] = t.x;
-          c[k + 1] = t.y;
-        }
-        double z0 = 0.0, z1 = 0.0, z2 = 0.0;
+        for (int mt = 0; mt < SMAX / 8; ++mt) acc[mt][0] = acc[mt][1] = 0.0;
 #pragma unroll
-        for (int k = 0; k < kM; k += 3) {
-          z0 = fma(trow[k], c[k], z0);
-          z1 = fma(trow[k + 1], c[k + 1], z1);
-          z2 = fma(trow[k + 2], c[k + 2], z2);
-        }
-        if (lane < s) zb[v * rows + u * seglen + 2 * lane + sg] += (z0 + z1) + z2;
-      }
-      if (SMAX > 32) {  // rows m = 32..s-1 (s_hat = 64 plans): T rows of lane + 32 from global
-        const int m = lane + 32;
-        for (int it = warp >> 1; it < per; it += (nwarps / 2)) {
-          const int u = it / VT, v = it - u * VT;
-          const double* cp = cl + ((sg * nleaf + u) * VT + v) * kM;
-          const double* tp = Tsh + (sg * SMAX + (m < SMAX ? m : 0)) * kM;
-          double z = 0.0;
+        for (int kk = 0; kk < (kM + 3) / 4; ++kk) {
+          const int kx = 4 * kk + lc;
+          const bool okk = kx < kM;
+          const double b = (okb && okk) ? cp[kx] : 0.0;
 #pragma unroll
-          for (int k = 0; k < kM; ++k) z = fma(tp[k], cp[k], z);
-          if (m < s) zb[v * rows + u * seglen + 2 * m + sg] += z;
+          for (int mt = 0; mt < SMAX / 8; ++mt) {
+            const double a = okk ? tq[8 * mt * kM + kx] : 0.0;
+            dmma(acc[mt], a, b);
+          }
         }
+#pragma unroll
+        for (int mt = 0; mt < SMAX / 8; ++mt)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int m = 8 * mt + lr, lf = lf0 + 2 * lc + h;
+            if (m < s && lf < nleaf) zb[v * rows + lf * seglen + 2 * m + sg] += acc[mt][h];
+          }
       }
     }
     __syncthreads();
