@@ -526,7 +526,6 @@ constexpr int kBandWarps = 4;  // band + down warps (independent pipeline)
 constexpr int kStreamThreads = 32 * (1 + kM2lWarps + kBandWarps);
 constexpr int kBandThreads = 32 * kBandWarps;
 constexpr int kM2lThreads = 32 * kM2lWarps;
-constexpr int kMaxChain = 24;  // ancestor levels above a down unit's subtree (n up to ~4e9)
 
 __device__ __forceinline__ void band_sync() { named_sync(1, kBandThreads); }
 __device__ __forceinline__ void m2l_sync() { named_sync(2, kM2lThreads); }
@@ -1085,7 +1084,6 @@ __global__ void __launch_bounds__(kStreamThreads, 2) lc_stream_kernel(const __gr
 // Operator inputs are loaded into registers before the arithmetic and every dot product runs
 // as four partial sums, so a level costs one shared-memory round trip plus a 5-deep DFMA chain.
 constexpr int kDownThreads = 256;
-constexpr int kDownWarps = kDownThreads / 32;
 
 // (B(p)^T c)_l = (-1)^{pl} sum_n b_nl (-1)^{pn} c_n   (lane l); column l of
 // B(0) from shared memory (consecutive lanes, conflict-free), c broadcast.
@@ -1111,43 +1109,6 @@ __device__ __forceinline__ double l2l_lane(const double* __restrict__ Bs, const 
   const double e = e0 + e1, o = o0 + o1;
   const double r = p ? e - o : e + o;
   return (p && (l & 1)) ? -r : r;
-}
-
-// Step 4 for one node by one thread: dst[k] += (B(p)^T c)_k = (-1)^{pk} sum_{n>=k} b_nk (-1)^{pn} c_n
-// (PAPER.md:383-384).  BT = B(0)^T in shared memory (row k = column k of B(0)), broadcast 16-byte
-// loads; two partial sums per output.  The outputs are produced in three groups separated by
-// compiler barriers so that the B loads of a group are not hoisted (register pressure).
-template <int K0, int K1>
-__device__ __forceinline__ void l2l_group(const double* __restrict__ BT, const double (&x)[kM], int p,
-                                          double* __restrict__ dst) {
-#pragma unroll
-  for (int k = K0; k < K1; ++k) {
-    double a0 = 0.0, a1 = 0.0;
-#pragma unroll
-    for (int n = k & ~1; n < kM; n += 2) {
-      const double2 b = *reinterpret_cast<const double2*>(BT + k * kM + n);  // b_{n k}, b_{n+1 k}
-      if (n >= k) a0 = fma(b.x, x[n], a0);
-      a1 = fma(b.y, x[n + 1], a1);
-    }
-    const double r = a0 + a1;
-    dst[k] += (p && (k & 1)) ? -r : r;  // (-1)^{pk}
-    if (k & 1) asm volatile("" ::: "memory");  // at most two outputs' B loads in flight
-  }
-}
-__device__ __forceinline__ void l2l_node(const double* __restrict__ BT, const double* __restrict__ c, int p,
-                                         double* __restrict__ dst) {
-  double x[kM];
-#pragma unroll
-  for (int n = 0; n < kM; n += 2) {
-    const double2 t = *reinterpret_cast<const double2*>(c + n);
-    x[n] = t.x;
-    x[n + 1] = p ? -t.y : t.y;  // (-1)^{pn}
-  }
-  l2l_group<0, 4>(BT, x, p, dst);
-  asm volatile("" ::: "memory");
-  l2l_group<4, 9>(BT, x, p, dst);
-  asm volatile("" ::: "memory");
-  l2l_group<9, 18>(BT, x, p, dst);
 }
 
 template <int VT, int DIR, int SMAX, int NT>
@@ -1251,30 +1212,50 @@ __global__ void __launch_bounds__(NT, 512 / NT) lc_down_kernel(const DownParams 
     // lane = mode (short dependent chain).  Wide levels: one thread per (sigma, node, v) with
     // all 18 outputs (the fp64 pipe is the limit there: 171 DFMA on 32 busy lanes instead of
     // 324 lane-slots of a warp item), B(0) rows broadcast from shared memory.
+    // On the fp64 tensor cores: warp item = 8 parent columns (sigma, P, v); for child parity p,
+    // A_p[k][n] = (-1)^(p(k+n)) b_nk (rows k padded to 24, K = n padded to 20; blocks with
+    // n < k everywhere skipped), and the children 2P+p accumulate A_p c_parent.
     for (int j = 1; j <= kd; ++j) {
-      const int nodes = 1 << j;
+      const int nodes = 1 << j, half = nodes >> 1;
       const double* par = cm_lvl(j - 1);
       double* cur = cm_lvl(j);
-      const int items = 2 * nodes * VT;
-      if (items <= 2 * nwarps) {
-        for (int it = warp; it < items; it += nwarps) {
-          const int v = it % VT;
-          const int sn = it / VT;
-          const int node = sn & (nodes - 1);
-          const int sg = sn >> j;
-          const double own = lane < kM ? cur[it * kM + lane] : 0.0;
-          const double r = l2l_lane(Bsh, par + ((sg * (nodes >> 1) + (node >> 1)) * VT + v) * kM, node & 1, lane);
-          if (lane < kM) cur[it * kM + lane] = own + r;
+      const int ncol = nodes * VT;  // parent columns, both parities
+      const int lr = lane >> 2, lc = lane & 3;
+      for (int c0 = warp * 8; c0 < ncol; c0 += nwarps * 8) {
+        const int col = c0 + lr;
+        const bool okc = col < ncol;
+        const double* xp = par + (okc ? col : 0) * kM;
+        double acc[2][3][2];
+#pragma unroll
+        for (int mt = 0; mt < 3; ++mt)
+          acc[0][mt][0] = acc[0][mt][1] = acc[1][mt][0] = acc[1][mt][1] = 0.0;
+#pragma unroll
+        for (int kk = 0; kk < (kM + 3) / 4; ++kk) {
+          const int n = 4 * kk + lc;
+          const double b = (okc && n < kM) ? xp[n] : 0.0;
+#pragma unroll
+          for (int mt = 0; mt < 3; ++mt) {
+            if (4 * kk + 3 < 8 * mt) continue;  // n < k for the whole block
+            const int k = 8 * mt + lr;
+            const double a0 = (k < kM && n < kM) ? BTsh[k * kM + n] : 0.0;  // b_nk (zero for n < k)
+            const double a1 = ((k + n) & 1) ? -a0 : a0;
+            dmma(acc[0][mt], a0, b);
+            dmma(acc[1][mt], a1, b);
+          }
         }
-      } else {
-        // one thread per (sigma, node, v), all 18 outputs (B(0)^T rows broadcast)
-        for (int it = tid; it < items; it += nthr) {
-          const int v = it % VT;
-          const int sn = it / VT;
-          const int node = sn & (nodes - 1);
-          const int sg = sn >> j;
-          l2l_node(BTsh, par + ((sg * (nodes >> 1) + (node >> 1)) * VT + v) * kM, node & 1, cur + it * kM);
-        }
+#pragma unroll
+        for (int mt = 0; mt < 3; ++mt)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int k = 8 * mt + lr, co = c0 + 2 * lc + h;
+            if (k < kM && co < ncol) {
+              const int v = co % VT, sp = co / VT;
+              const int P = sp & (half - 1), sg = sp >> (j - 1);
+              double* d0 = cur + ((sg * nodes + 2 * P) * VT + v) * kM + k;
+              d0[0] += acc[0][mt][h];
+              d0[VT * kM] += acc[1][mt][h];
+            }
+          }
       }
       __syncthreads();
     }
