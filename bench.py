@@ -47,6 +47,7 @@ def peaks():
 
 
 FP64_PEAK_TFLOPS = 34.2  # profiles/r1_fp64_peak.txt: DFMA microbenchmark on this pool's B200 at 1965 MHz
+DMMA_PEAK_TFLOPS = 37.0  # profiles/r1_dmma_peak.txt: fp64 tensor-core MMA (m8n8k4) microbenchmark
 
 
 class ClockSampler:
@@ -170,7 +171,8 @@ def run_gpu(args, world, rank, local):
     x = xh.to(dev)
     tmp = torch.empty_like(x)
     y = torch.empty_like(x)
-    opts = dict(vt=args.vt, subtree=args.subtree, stage_blocks=args.stage_blocks, stages=args.stages)
+    opts = dict(vt=args.vt, subtree=args.subtree, stage_blocks=args.stage_blocks, stages=args.stages,
+                engine=args.engine)
     stream = torch.cuda.current_stream(dev)
     two_d = args.config == "cfg5"
     if two_d:
@@ -261,7 +263,8 @@ def run_gpu(args, world, rank, local):
                 per_kernel[d][i] += ev[i].elapsed_time(ev[i + 1]) / ksteps
     hbm, hbm_src = peaks()
     dl = pl.desc
-    names = (["lc_up_kernel"] if kpe == 3 else []) + ["lc_stream_kernel", "lc_down_kernel"]
+    names = ["lc_tile_kernel"] if kpe == 1 else (["lc_up_kernel"] if kpe == 3 else []) + ["lc_stream_kernel",
+                                                                                         "lc_down_kernel"]
     # algorithmic bytes per launch (f in, z out, A_hat once, lambda once; work arrays excluded):
     # the up kernel reads f, the streaming kernel reads A_hat and lambda (and f again for the band),
     # the down kernel writes z
@@ -269,12 +272,27 @@ def run_gpu(args, world, rank, local):
            "lc_down_kernel": 8.0 * n * V}
     if kpe == 2:
         alg["lc_stream_kernel"] += 8.0 * n * V
+    # the per-tile kernel (engine 2) is the whole transform: f in, z out, A_hat and lambda once
+    alg["lc_tile_kernel"] = 16.0 * n * V + 8.0 * 324 * dl["nc"] + 8.0 * dl["N"]
     avg_ms = {nm: 0.5 * (per_kernel[0][i] + per_kernel[1][i]) for i, nm in enumerate(names)}
-    dom = "lc_stream_kernel"  # the A_hat stream: the HBM-dominant kernel
+    dom = "lc_tile_kernel" if kpe == 1 else "lc_stream_kernel"  # the A_hat stream: the HBM-dominant kernel
     down_ms = avg_ms[dom]
     down_bytes = alg[dom]
     achieved = down_bytes / (down_ms * 1e-3) / 1e9
     traffic = load_traffic(args.config, dom)
+    if kpe == 1:
+        # fp64 tensor-core bound: algorithmic flops of one transform over the kernel time, against the
+        # measured DMMA peak (the higher of the two fp64 peaks, so the fraction is conservative)
+        tf = dl["flops_alg"] * V / (down_ms * 1e-3) / 1e12
+        roof = {"bound": "tensor", "kernel": dom, "achieved": tf, "peak": DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
+                "frac": tf / DMMA_PEAK_TFLOPS, "traffic": traffic, "algorithmic_flops_per_launch": dl["flops_alg"] * V,
+                "algorithmic_bytes_per_launch": down_bytes, "achieved_hbm_gbs": achieved, "avg_launch_ms": down_ms,
+                "peak_source": "measured fp64 DMMA m8n8k4 (profiles/r1_dmma_peak.txt)"}
+    else:
+        roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm,
+                "unit": "GB/s", "frac": achieved / hbm, "traffic": traffic,
+                "algorithmic_bytes_per_launch": down_bytes, "avg_launch_ms": down_ms,
+                "peak_source": hbm_src}
     # transform-level roofline (slower of fp64 flops at the measured DFMA peak and bytes at HBM peak)
     t_roof = max(dl["flops_alg"] * V / (FP64_PEAK_TFLOPS * 1e12), dl["bytes_alg"] / (hbm * 1e9))
     t_meas = ms_local / args.steps / 2 * 1e-3
@@ -334,12 +352,10 @@ def run_gpu(args, world, rank, local):
                    "input_kind": kind,
                    "l2": f"no flush: per-step working set {2 * 8 * 324 * dl['nc'] / 1e6:.0f} MB of A_hat + "
                          f"{3 * bytes_vec / 1e6:.0f} MB of vectors vs 126 MB L2" if dl["nc"] > 0 else "small",
-                   "graph": graph is not None, "kernel_cfg": {k: dl[k] for k in ("vt", "subtree", "stage_blocks",
-                                                                                 "stages")}},
-        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm,
-                     "unit": "GB/s", "frac": achieved / hbm, "traffic": traffic,
-                     "algorithmic_bytes_per_launch": down_bytes, "avg_launch_ms": down_ms,
-                     "peak_source": hbm_src},
+                   "graph": graph is not None, "kernel_cfg": {**{k: dl[k] for k in ("vt", "subtree", "stage_blocks",
+                                                                                    "stages")},
+                                                                 "engine": pl.kernel_info.get("engine", 1)}},
+        "roofline": roof,
         "roofline_transform": {"t_roof_us": t_roof * 1e6, "t_measured_us": t_meas * 1e6,
                                "frac": t_roof / t_meas, "fp64_peak_tflops": FP64_PEAK_TFLOPS,
                                "flops_alg_per_vector": dl["flops_alg"], "bytes_alg": dl["bytes_alg"]},
@@ -452,6 +468,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg2", choices=["cfg1", "cfg2", "cfg2b", "cfg3", "cfg4", "cfg5"])
     ap.add_argument("--vt", type=int, default=0)
+    ap.add_argument("--engine", type=int, default=0, help="0 automatic, 1 level-pipelined kernels, 2 per-tile kernel")
     ap.add_argument("--subtree", type=int, default=0)
     ap.add_argument("--stage-blocks", type=int, default=0)
     ap.add_argument("--stages", type=int, default=0)

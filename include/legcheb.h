@@ -74,6 +74,9 @@ typedef struct {
   int32_t stage_blocks; /* FMM blocks (3 A_hat each) per TMA bulk-copy stage; 0 -> automatic */
   int32_t stages;   /* bulk-copy ring depth; 0 -> automatic */
   int32_t up_subtree; /* subtree depth of the upward (leaf projection + M2M) kernel; 0 -> automatic */
+  int32_t engine;   /* 0 -> automatic; 1 -> level-pipelined kernels (up / streaming / down);
+                       2 -> per-tile streaming kernel (one CTA per 8-vector tile, whole Alg. 4 on chip;
+                       needs L >= 1 and s <= 32; automatic choice when there are >= 2 tiles per SM) */
 } lc_plan_opts;
 
 /* Geometry and algorithmic work of a plan (per vector unless stated). */
@@ -151,7 +154,8 @@ lc_status lc_plan_export(const lc_plan* p, int32_t what, double* host_out, int64
 /* Kernel configuration chosen for the plan (diagnostic; host only, no device work).
  * out[0..] = stream_grid, smem_stream, smem_up, kup (up-kernel subtree depth), grup,
  * kb (band/down unit depth), cb (blocks per A_hat stage), nst (stages), vt, stream CTAs per
- * SM, m2l_units, band_units, up_grid (CTAs), kd (down-kernel subtree depth), smem_down.  count = capacity of out; returns the number of
+ * SM, m2l_units, band_units, up_grid (CTAs), kd (down-kernel subtree depth), smem_down, engine (1 or 2),
+ * tile_grid and smem_tile (per-tile kernel, engine 2).  count = capacity of out; returns the number of
  * values written through *written (may be NULL).  Errors: INVALID_ARG on NULL p or out. */
 lc_status lc_plan_kernel_info(const lc_plan* p, int64_t* out, int32_t count, int32_t* written);
 

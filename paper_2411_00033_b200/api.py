@@ -40,7 +40,8 @@ class Plan:
 
     def __init__(self, n: int, direction="leg2cheb", batch: int = 1, device=None, s_hat: int = 32,
                  layout="vec", ld_in: int = 0, ld_out: int = 0, vt: int = 0, subtree: int = 0,
-                 stage_blocks: int = 0, stages: int = 0, up_subtree: int = 0):
+                 stage_blocks: int = 0, stages: int = 0, up_subtree: int = 0,
+                 engine: int = 0):
         lib = _lib.load()
         if device is None:
             device = torch.cuda.current_device()
@@ -51,7 +52,8 @@ class Plan:
         self.layout = LAYOUTS[layout]
         opts = _lib.PlanOpts(s_hat=s_hat, M=18, layout=self.layout, ld_in=ld_in, ld_out=ld_out,
                              device=device.index if device.index is not None else -1, vt=vt, subtree=subtree,
-                             stage_blocks=stage_blocks, stages=stages, up_subtree=up_subtree)
+                             stage_blocks=stage_blocks, stages=stages, up_subtree=up_subtree,
+                             engine=engine)
         h = ctypes.c_void_p()
         with torch.cuda.device(device):
             _lib.check("lc_plan_create", lib.lc_plan_create(ctypes.byref(h), self.n, self.direction, self.batch,
@@ -91,7 +93,7 @@ class Plan:
         nw = ctypes.c_int32(0)
         _lib.check("lc_plan_kernel_info", self._lib.lc_plan_kernel_info(self._h, buf, 32, ctypes.byref(nw)))
         names = ["stream_grid", "smem_stream", "smem_up", "kup", "grup", "kb", "cb", "nst", "vt", "stream_occ",
-                 "m2l_units", "band_units", "up_grid", "kd", "smem_down"]
+                 "m2l_units", "band_units", "up_grid", "kd", "smem_down", "engine", "tile_grid", "smem_tile"]
         return {k: int(buf[i]) for i, k in enumerate(names[:nw.value])}
 
     @property

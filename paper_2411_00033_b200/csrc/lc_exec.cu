@@ -1025,6 +1025,7 @@ __global__ void __launch_bounds__(kStreamThreads, 2) lc_stream_kernel(const __gr
       __syncwarp();
       if ((tid & 31) == 0) mbar_arrive(&empty[slot]);  // this warp is done with the slot
     }
+    if (tid == 32) LC_TS_T(1, 7);
   } else {
     // ------------------------------------------------ band + down warps
     const int btid = tid - 32 * (1 + kM2lWarps);
@@ -1317,6 +1318,340 @@ __global__ void __launch_bounds__(NT, 512 / NT) lc_down_kernel(const DownParams 
   }
 }
 
+// ============================================================== per-tile streaming kernel
+// Batched transforms of short vectors (many vector tiles): one CTA runs the whole of Alg. 4 for a
+// tile of 8 vectors in ONE right-to-left pass over the leaf segments U = 2^(L+1)-1 .. 0, keeping
+// every intermediate on chip (no w / c_m2l round trip through HBM, no inter-CTA flags).
+// The pass order works because A is upper triangular and every interaction is local:
+//   * row segment u of level g takes the M2L of column segments t = u+2 (and u+3 for even u)
+//     (eq:globalij: block b has rows 2b, 2b+1 and columns 2b+2, 2b+3), which lie to its right;
+//   * the band of leaf row segment U reaches the end of segment U+1 (j_end, R4);
+//   * c of a segment is its M2L plus the L2L of its parent's c (step 4), and a parent is
+//     entered (at its rightmost leaf) no later than its children.
+// So when leaf U is reached, all w(g, t) for columns right of U are complete.  Per leaf step:
+//   phase A  [chain]  c(g, u_g) += B(p)^T c(g-1, u_g/2) for the levels entered at U (step 4)
+//            [M2L]    c_m2l(g, u') for the levels the NEXT leaf U-1 enters (step 3)
+//            [step 1] w(L-1, U) = f_U^sigma T(sigma)
+//            [band]   z(U) = direct band of rows U (step 6)
+//   phase B  [M2M]    w(g-1, u/2) = B(0) w(g, u) + B(1) w(g, u+1) while u is a left child (step 2)
+//            [step 5] z(U) += T(sigma) c(L-1, U); the store (with C^{-1}, step 7) happens in the
+//                     next step's phase A.
+// All contractions run on the fp64 tensor cores (DMMA m8n8k4) with the 8 vectors of the tile as
+// the n dimension.  State per CTA (doubles): w ring [L][3][2][8][18] (live columns u+1..u+3 of
+// every level), c slots [L][2][2][8][18] (by segment parity), an f/lambda ring of 4 leaf
+// segments (prefetched two steps ahead with cp.async), z stage [2][8][2s+4], T, B(0), tabA.
+constexpr int kTileThreads = 256;
+constexpr int kTileV = 8;                  // vectors per tile (= DMMA n)
+constexpr int kTS = kTileV * kM;           // doubles per (segment, sigma) state
+__host__ __device__ inline int tile_fst(int s) { int f = 4; while (f < s) f += 16; return f; }
+__host__ __device__ inline int64_t tile_smem_doubles(int L, int s) {
+  const int fst = tile_fst(s);
+  return 2 * 32 * kM + (kMM + 4) + 80 + 4 * 2 * kTileV * fst + 4 * 2 * s + int64_t(L) * 3 * 2 * kTS +
+         int64_t(L) * 2 * 2 * kTS + 2 * kTileV * (2 * s + 4);
+}
+
+struct TileParams {
+  const double* in;
+  double* out;
+  const double* A;     // A_hat arena
+  const double* tabA;  // 2s
+  const double* tabB;  // N
+  const double* Tpad;  // [2][32][M]
+  const double* B;     // B(0)
+  int64_t ld_in, ld_out, n, N, batch, ntiles;
+  int layout, L, s;
+};
+
+template <int DIR>
+__global__ void __launch_bounds__(kTileThreads, 2) lc_tile_kernel(const __grid_constant__ TileParams P) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int nwarps = kTileThreads / 32;
+  const int lr = lane >> 2, lc = lane & 3;
+  const int s = P.s, L = P.L, seglen = 2 * s;
+  const int fst = tile_fst(s), zst_ = 2 * s + 4;
+  const int nls = 2 << L;  // leaf segments
+  double* Tq = reinterpret_cast<double*>(smem);  // [2][32][M]
+  double* Bq = Tq + 2 * 32 * kM;                  // B(0) [M][M]
+  double* taq = Bq + kMM + 4;                     // tabA [80]
+  double* fr = taq + 80;                          // [4][2][8][fst]
+  double* tbr = fr + 4 * 2 * kTileV * fst;        // [4][2s]
+  double* wr = tbr + 4 * seglen;                  // [L][3][2][8][M]
+  double* cs = wr + L * 3 * 2 * kTS;              // [L][2][2][8][M]
+  double* zs = cs + L * 2 * 2 * kTS;              // [2][8][2s+4]
+  auto fslot = [&](int U) { return fr + (U & 3) * 2 * kTileV * fst; };
+  auto tbslot = [&](int U) { return tbr + (U & 3) * seglen; };
+  auto wslot = [&](int g, int t) { return wr + (g * 3 + t % 3) * 2 * kTS; };
+  auto cslot = [&](int g, int u) { return cs + (g * 2 + (u & 1)) * 2 * kTS; };
+  auto zbuf = [&](int U) { return zs + (U & 1) * kTileV * zst_; };
+
+  for (int i = tid; i < 2 * 32 * kM / 2; i += kTileThreads) cp_async16(Tq + 2 * i, P.Tpad + 2 * i);
+  for (int i = tid; i < kMM / 2; i += kTileThreads) cp_async16(Bq + 2 * i, P.B + 2 * i);
+  for (int i = tid; i < 80; i += kTileThreads) taq[i] = i < seglen ? P.tabA[i] : 0.0;
+  // rows m in [s, fst) of every f slot stay zero (read by the K = 4 ceil(s/4) steps of step 1)
+  for (int i = tid; i < 4 * 2 * kTileV * fst; i += kTileThreads) fr[i] = 0.0;
+  cp_async_commit();
+  griddep_wait();  // the input may be produced by the preceding kernel
+  griddep_launch();
+
+  // stage leaf segment U of the tile: f de-interleaved by parity, lambda (tabB) as is
+  auto stage = [&](int64_t tile, int U) {
+    double* fd = fslot(U);
+    double* td = tbslot(U);
+    const int64_t j0 = int64_t(U) * seglen;
+    for (int idx = tid; idx < kTileV * seglen; idx += kTileThreads) {
+      int v, x;
+      if (P.layout == LC_VEC_CONTIGUOUS) { v = idx / seglen; x = idx - v * seglen; }
+      else { x = idx / kTileV; v = idx - x * kTileV; }
+      const int64_t gv = tile * kTileV + v, j = j0 + x;
+      const bool ok = gv < P.batch && j < P.n;
+      const double* src = P.layout == LC_VEC_CONTIGUOUS ? P.in + gv * P.ld_in + j : P.in + j * P.ld_in + gv;
+      cp_async8(fd + ((x & 1) * kTileV + v) * fst + (x >> 1), ok ? src : P.in, ok ? 8u : 0u);
+    }
+    for (int x = tid; x < seglen; x += kTileThreads) {
+      const bool ok = j0 + x < P.N;
+      cp_async8(td + x, ok ? P.tabB + j0 + x : P.tabB, ok ? 8u : 0u);
+    }
+  };
+  // coalesced store of z(U) with C^{-1} (L2C, step 7)
+  auto store = [&](int64_t tile, int U) {
+    const double* zb = zbuf(U);
+    const int64_t j0 = int64_t(U) * seglen;
+    const double inv_pi = 0.318309886183790671537767526745028724;
+    for (int idx = tid; idx < kTileV * seglen; idx += kTileThreads) {
+      int v, x;
+      if (P.layout == LC_VEC_CONTIGUOUS) { v = idx / seglen; x = idx - v * seglen; }
+      else { x = idx / kTileV; v = idx - x * kTileV; }
+      const int64_t gv = tile * kTileV + v, i = j0 + x;
+      if (gv >= P.batch || i >= P.n) continue;
+      double z = zb[v * zst_ + x];
+      if (DIR == 0) z *= (i == 0 ? inv_pi : 2.0 * inv_pi);
+      if (P.layout == LC_VEC_CONTIGUOUS) P.out[gv * P.ld_out + i] = z;
+      else P.out[i * P.ld_out + gv] = z;
+    }
+  };
+  // first level entered at leaf U (U is the rightmost leaf of its segments on levels >= gmin)
+  auto gmin_of = [&](int U) {
+    const int ones = __ffs(~U) - 1;  // trailing one bits
+    const int g = L - 1 - ones;
+    return g < 0 ? 0 : g;
+  };
+
+  for (int64_t tile = blockIdx.x; tile < P.ntiles; tile += gridDim.x) {
+    for (int i = tid; i < L * 2 * 2 * kTS; i += kTileThreads) cs[i] = 0.0;  // c_m2l of rows without M2L stay 0
+    {
+      double* fz = fslot(nls);  // the segment past the end reads as zero
+      for (int i = tid; i < 2 * kTileV * fst; i += kTileThreads) fz[i] = 0.0;
+      for (int i = tid; i < seglen; i += kTileThreads) tbslot(nls)[i] = 0.0;
+    }
+    stage(tile, nls - 1);
+    cp_async_commit();
+    stage(tile, nls - 2);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+
+    for (int U = nls - 1; U >= 0; --U) {
+      if (U >= 2) stage(tile, U - 2);
+      cp_async_commit();
+      if (U + 1 < nls) store(tile, U + 1);
+      // ------------------------------------------------------------ phase A
+      const int gA = gmin_of(U);
+      const int gN = U >= 1 ? gmin_of(U - 1) : L;  // levels the next leaf enters: gN..L-1
+      const int nm2l = (L - gN) * 6;
+      const int njobs = 2 + nm2l + 6 + 8;
+      for (int job = warp; job < njobs; job += nwarps) {
+        if (job < 2) {
+          // step 4 chain (sigma = job) over the levels entered at U, coarse to fine
+          const int sg = job;
+          for (int g = (gA > 0 ? gA : 1); g < L; ++g) {
+            const int u = U >> (L - 1 - g);
+            const int p = u & 1;
+            const double* par = cslot(g - 1, u >> 1) + sg * kTS;
+            double* dst = cslot(g, u) + sg * kTS;
+#pragma unroll
+            for (int mt = 0; mt < 3; ++mt) {
+              double acc[2] = {0.0, 0.0};
+#pragma unroll
+              for (int kk = 0; kk < 5; ++kk) {
+                if (4 * kk + 3 < 8 * mt) continue;  // n < k everywhere
+                const int nn = 4 * kk + lc, k = 8 * mt + lr;
+                const double b = nn < kM ? par[lr * kM + nn] : 0.0;
+                double a = (k < kM && nn < kM) ? Bq[nn * kM + k] : 0.0;  // b_{n k}
+                if (p && ((k + nn) & 1)) a = -a;
+                dmma(acc, a, b);
+              }
+              const int k = 8 * mt + lr;
+              if (k < kM) {
+                dst[(2 * lc) * kM + k] += acc[0];
+                dst[(2 * lc + 1) * kM + k] += acc[1];
+              }
+            }
+            __syncwarp();
+          }
+        } else if (job < 2 + nm2l) {
+          // step 3 for the row the next leaf enters on level g: c(u') = sum_r A_hat w(t_r)
+          const int jj = job - 2;
+          const int g = gN + jj / 6, sg = (jj % 6) & 1, mt = (jj % 6) >> 1;
+          const int u = (U - 1) >> (L - 1 - g);
+          double acc[2] = {0.0, 0.0};
+          if (u < (4 << g) - 2) {
+            const int b = u >> 1, p = u & 1;
+            const int mode = 8 * mt + lr;
+            for (int mi = 0; mi < (p ? 1 : 2); ++mi) {
+              const int r = p ? 2 : mi;
+              const int t = u + 2 + (p ? 0 : mi);
+              const double* Am = P.A + (ahat_level_offset(g) + 3 * int64_t(b) + r) * kMM;
+              const double* W = wslot(g, t) + sg * kTS;
+              double av[5];
+#pragma unroll
+              for (int kk = 0; kk < 5; ++kk) {
+                const int k = 4 * kk + lc;
+                av[kk] = (mode < kM && k < kM) ? __ldg(Am + mode * kM + k) : 0.0;
+              }
+#pragma unroll
+              for (int kk = 0; kk < 5; ++kk) {
+                const int k = 4 * kk + lc;
+                const double bb = k < kM ? W[lr * kM + k] : 0.0;
+                dmma(acc, av[kk], bb);
+              }
+            }
+          }
+          const int mode = 8 * mt + lr;
+          if (mode < kM) {
+            double* dst = cslot(g, u) + sg * kTS;
+            dst[(2 * lc) * kM + mode] = acc[0];
+            dst[(2 * lc + 1) * kM + mode] = acc[1];
+          }
+        } else if (job < 2 + nm2l + 6) {
+          // step 1: w(L-1, U)[sigma][v][mode] = sum_m T(sigma)[m][mode] f_v[2sU + 2m + sigma]
+          const int jj = job - 2 - nm2l;
+          const int sg = jj & 1, mt = jj >> 1;
+          const int mode = 8 * mt + lr;
+          const double* fv = fslot(U) + (sg * kTileV + lr) * fst;
+          const double* Tm = Tq + sg * 32 * kM;
+          double acc[2] = {0.0, 0.0};
+          const int nks = (s + 3) >> 2;
+          for (int kk = 0; kk < nks; ++kk) {
+            const int m = 4 * kk + lc;
+            const double a = mode < kM ? Tm[m * kM + mode] : 0.0;
+            dmma(acc, a, fv[m]);
+          }
+          if (mode < kM) {
+            double* dst = wslot(L - 1, U) + sg * kTS;
+            dst[(2 * lc) * kM + mode] = acc[0];
+            dst[(2 * lc + 1) * kM + mode] = acc[1];
+          }
+        } else {
+          // step 6: rows i = 2sU + 2r + sigma, columns j = 2sU + 2c + sigma (c >= r, j < j_end),
+          // K[r][c] = a[c-r] b[(i+j)/2] formed per lane, G[c][v] = f_v[j] (C2L: j f_j)
+          const int jj = job - 2 - nm2l - 6;
+          const int sg = jj & 1, rb = jj >> 1;
+          if (8 * rb < s) {
+            const int r = 8 * rb + lr;
+            const double* f0 = fslot(U) + (sg * kTileV + lr) * fst;
+            const double* f1 = fslot(U + 1) + (sg * kTileV + lr) * fst;
+            const double* t0 = tbslot(U);
+            const double* t1 = tbslot(U + 1);
+            const int64_t i0 = int64_t(U) * seglen;
+            double acc[2] = {0.0, 0.0};
+            const int nkc = (seglen + 3) >> 2;
+            for (int kc = 2 * rb; kc < nkc; ++kc) {
+              const int c = 4 * kc + lc;
+              double b = c < s ? f0[c] : (c < seglen ? f1[c - s] : 0.0);
+              if (DIR == 1) b *= double(i0 + 2 * c + sg);
+              const int x = r + c + sg;  // (i + j)/2 - 2sU
+              const double lam = x < seglen ? t0[x] : t1[x - seglen];
+              const double a = (c >= r && c < seglen && r < s) ? taq[c - r] * lam : 0.0;
+              dmma(acc, a, b);
+            }
+            if (r < s) {
+              double* zb = zbuf(U);
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                const int v = 2 * lc + h;
+                double z = acc[h];
+                if (DIR == 1) {
+                  const int64_t ir = i0 + 2 * r + sg;
+                  z *= double(2 * ir + 1);
+                  if (ir == 0) z += fslot(U)[v * fst];  // entry (0,0) of A^{-1}C is 1 (R2)
+                }
+                zb[v * zst_ + 2 * r + sg] = z;
+              }
+            }
+          }
+        }
+      }
+      cp_async_wait<1>();  // f(U-1) landed
+      __syncthreads();
+      // ------------------------------------------------------------ phase B
+      const int ncas = (U & 1) == 0 ? 2 : 0;
+      for (int job = warp; job < ncas + 8; job += nwarps) {
+        if (job < ncas) {
+          // step 2 cascade (sigma = job) while the completed segment is a left child
+          const int sg = job;
+          int g = L - 1, u = U;
+          while (g > 0 && (u & 1) == 0) {
+            const double* x0 = wslot(g, u) + sg * kTS;
+            const double* x1 = wslot(g, u + 1) + sg * kTS;
+            double* o = wslot(g - 1, u >> 1) + sg * kTS;
+#pragma unroll
+            for (int mt = 0; mt < 3; ++mt) {
+              double acc[2] = {0.0, 0.0};
+#pragma unroll
+              for (int kk = 0; kk < 9; ++kk) {
+                if (mt == 0 && (kk == 2 || kk == 3 || kk == 7 || kk == 8)) continue;  // k >= 8 > n
+                const int kap = 4 * kk + lc;
+                const int child = kap >= kM ? 1 : 0;
+                const int kx = kap - child * kM;
+                const double b = (child ? x1 : x0)[lr * kM + kx];
+                const int nn = 8 * mt + lr;
+                double a = nn < kM ? Bq[nn * kM + kx] : 0.0;
+                if (child && ((nn - kx) & 1)) a = -a;
+                dmma(acc, a, b);
+              }
+              const int nn = 8 * mt + lr;
+              if (nn < kM) {
+                o[(2 * lc) * kM + nn] = acc[0];
+                o[(2 * lc + 1) * kM + nn] = acc[1];
+              }
+            }
+            __syncwarp();
+            --g;
+            u >>= 1;
+          }
+        } else {
+          // step 5: z(U)[v][2m + sigma] += sum_k T(sigma)[m][k] c(L-1, U)[sigma][v][k]
+          const int jj = job - ncas;
+          const int sg = jj & 1, mt = jj >> 1;
+          if (8 * mt < s) {
+            const double* cc = cslot(L - 1, U) + sg * kTS;
+            const int m = 8 * mt + lr;
+            const double* Tm = Tq + (sg * 32 + m) * kM;
+            double acc[2] = {0.0, 0.0};
+#pragma unroll
+            for (int kk = 0; kk < 5; ++kk) {
+              const int k = 4 * kk + lc;
+              const double a = k < kM ? Tm[k] : 0.0;
+              const double b = k < kM ? cc[lr * kM + k] : 0.0;
+              dmma(acc, a, b);
+            }
+            if (m < s) {
+              double* zb = zbuf(U);
+              zb[(2 * lc) * zst_ + 2 * m + sg] += acc[0];
+              zb[(2 * lc + 1) * zst_ + 2 * m + sg] += acc[1];
+            }
+          }
+        }
+      }
+      __syncthreads();
+    }
+    store(tile, 0);
+    cp_async_wait<0>();
+    __syncthreads();
+  }
+}
+
 // ============================================================== host side
 
 template <typename K>
@@ -1377,6 +1712,8 @@ lc_status configure_kernels(lc_plan* p) {
   if (!g_device_ready[p->device]) {
     ea = set_attrs_all<32>(smax);
     if (ea == cudaSuccess) ea = set_attrs_all<64>(smax);
+    if (ea == cudaSuccess) ea = set_max_dyn_smem(lc_tile_kernel<0>, smax);
+    if (ea == cudaSuccess) ea = set_max_dyn_smem(lc_tile_kernel<1>, smax);
     if (ea == cudaSuccess) {
       double B[kMM];
       ea = cudaMemcpy(B, p->d_B, sizeof(B), cudaMemcpyDeviceToHost);
@@ -1480,6 +1817,25 @@ lc_status configure_kernels(lc_plan* p) {
   // workspace: w | c_m2l | flags (64 ints) | arrival counters (c_m2l rows without a submatrix stay zero)
   const size_t wb = size_t(align_up(p->ntiles * p->w_tile_doubles * 8, 256));
   p->ws_bytes = 2 * wb + 256 + size_t(p->ntiles * p->cnt_tile_ints) * sizeof(int);
+  // per-tile streaming kernel (engine 2): many 8-vector tiles of short vectors
+  {
+    const int64_t ntiles8 = (p->batch + kTileV - 1) / kTileV;
+    const int64_t tsm = L >= 1 ? tile_smem_doubles(L, s) * 8 : 0;
+    const bool tile_ok = L >= 1 && s <= 32 && tsm <= smax;
+    if (p->engine == 2 && !tile_ok) return LC_ERR_INVALID_ARG;
+    if (p->engine == 0) p->engine = (tile_ok && ntiles8 >= 2 * int64_t(p->sm_count)) ? 2 : 1;
+    if (p->engine == 2) {
+      int occ = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, p->dir == 0 ? lc_tile_kernel<0> : lc_tile_kernel<1>,
+                                                    kTileThreads, size_t(tsm));
+      if (occ < 1) return LC_ERR_INVALID_ARG;
+      p->smem_tile = size_t(tsm);
+      p->tile_grid = int(std::min<int64_t>(ntiles8, int64_t(occ) * p->sm_count));
+      p->vt = kTileV;
+      p->ntiles = ntiles8;
+      p->ws_bytes = 256;
+    }
+  }
   return LC_OK;
 }
 
@@ -1564,6 +1920,28 @@ lc_status launch_execute(const lc_plan* p, const double* in, double* out, void* 
   int prev = 0;
   cudaGetDevice(&prev);
   if (prev != p->device) cudaSetDevice(p->device);
+  if (p->engine == 2) {
+    TileParams tp{};
+    tp.in = in; tp.out = out; tp.A = p->d_A; tp.tabA = p->d_tabA; tp.tabB = p->d_tabB; tp.Tpad = p->d_Tpad;
+    tp.B = p->d_B; tp.ld_in = p->ld_in; tp.ld_out = p->ld_out; tp.n = p->n; tp.N = p->N; tp.batch = p->batch;
+    tp.ntiles = p->ntiles; tp.layout = p->layout; tp.L = int(p->L); tp.s = int(p->s);
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.stream = st;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cfg.gridDim = dim3(unsigned(p->tile_grid));
+    cfg.blockDim = dim3(kTileThreads);
+    cfg.dynamicSmemBytes = p->smem_tile;
+    if (ev && nev > 0) cudaEventRecord(ev[0], st);
+    cudaError_t e = p->dir == 0 ? cudaLaunchKernelEx(&cfg, lc_tile_kernel<0>, tp) : cudaLaunchKernelEx(&cfg, lc_tile_kernel<1>, tp);
+    if (e == cudaSuccess && ev && nev > 1) cudaEventRecord(ev[1], st);
+    if (e == cudaSuccess) e = cudaGetLastError();
+    if (prev != p->device) cudaSetDevice(prev);
+    return e == cudaSuccess ? LC_OK : record_cuda_error(e);
+  }
   const size_t wb = size_t(align_up(p->ntiles * p->w_tile_doubles * 8, 256));
   double* w = reinterpret_cast<double*>(ws);
   double* c = reinterpret_cast<double*>(reinterpret_cast<char*>(ws) + wb);
@@ -1607,7 +1985,7 @@ extern "C" lc_status lc_plan_kernel_info(const lc_plan* p, int64_t* out, int32_t
   const int64_t up_grid = p->L > 0 ? (int64_t(4) << p->grup) * p->ntiles : 0;
   const int64_t v[] = {p->stream_grid, int64_t(p->smem_stream), int64_t(p->smem_up), p->kup, p->grup, p->kb,
                        p->bps, p->nst, p->vt, p->stream_occ, p->m2l_units, p->band_units, up_grid, p->k,
-                       int64_t(p->smem_down)};
+                       int64_t(p->smem_down), p->engine, p->tile_grid, int64_t(p->smem_tile)};
   const int32_t nv = int32_t(sizeof(v) / sizeof(v[0]));
   int32_t i = 0;
   for (; i < nv && i < count; ++i) out[i] = v[i];
@@ -1621,7 +1999,7 @@ extern "C" lc_status lc_execute(const lc_plan* p, const double* in, double* out,
 
 extern "C" lc_status lc_execute_timed(const lc_plan* p, const double* in, double* out, void* ws, void* stream,
                                       void* const* ev, int32_t nev) {
-  if (!p || !ev || nev < (p->L > 0 ? 4 : 3)) return LC_ERR_INVALID_ARG;
+  if (!p || !ev || nev < (p->engine == 2 ? 2 : (p->L > 0 ? 4 : 3))) return LC_ERR_INVALID_ARG;
   return lc::launch_execute(p, in, out, ws, (cudaStream_t)stream, reinterpret_cast<cudaEvent_t const*>(ev), nev);
 }
 

@@ -123,6 +123,9 @@ struct lc_plan {
   int64_t m2l_units;   // (chunk, tile) M2L work units of the streaming kernel
   int64_t band_units;  // (leaf range, tile) band work units of the streaming kernel
   int stream_grid, stream_occ;
+  int engine;          // 1 = up / stream / down kernels, 2 = per-tile streaming kernel
+  int tile_grid;       // CTAs of the per-tile kernel (engine 2)
+  size_t smem_tile;
   size_t smem_stream;
   int64_t ntiles;
   int64_t w_tile_doubles, cnt_tile_ints;

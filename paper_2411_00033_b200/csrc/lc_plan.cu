@@ -279,6 +279,7 @@ extern "C" lc_status lc_plan_create(lc_plan** out, int64_t n, lc_direction dir, 
   if (o.s_hat <= 0) o.s_hat = 32;
   if (o.M <= 0) o.M = kM;
   if (o.M != kM || o.s_hat < 2 || o.s_hat > 64) return LC_ERR_INVALID_ARG;
+  if (o.engine < 0 || o.engine > 2) return LC_ERR_INVALID_ARG;
   if (o.layout != LC_VEC_CONTIGUOUS && o.layout != LC_BATCH_CONTIGUOUS) return LC_ERR_INVALID_ARG;
   const int64_t def_ld = o.layout == LC_VEC_CONTIGUOUS ? n : batch;
   if (o.ld_in == 0) o.ld_in = def_ld;
@@ -301,6 +302,7 @@ extern "C" lc_status lc_plan_create(lc_plan** out, int64_t n, lc_direction dir, 
   p->dir = int(dir); p->layout = o.layout; p->ld_in = o.ld_in; p->ld_out = o.ld_out;
   p->device = dev; p->sm_count = prop.multiProcessorCount;
   p->vt = o.vt; p->k = o.subtree; p->bps = o.stage_blocks; p->nst = o.stages; p->kup = o.up_subtree;
+  p->engine = o.engine;
 
   auto fail = [&](lc_status st) {
     lc_plan_destroy(p);
@@ -414,7 +416,7 @@ extern "C" lc_status lc_plan_describe(const lc_plan* p, lc_plan_desc* d) {
   d->plan_bytes = p->plan_bytes; d->workspace_bytes = p->ws_bytes;
   d->flops_alg = p->flops_alg; d->bytes_alg = p->bytes_alg;
   d->vt = p->vt; d->subtree = p->k; d->stage_blocks = p->bps; d->stages = p->nst;
-  d->kernels_per_execute = p->L > 0 ? 3 : 2;
+  d->kernels_per_execute = p->engine == 2 ? 1 : (p->L > 0 ? 3 : 2);
   return LC_OK;
 }
 

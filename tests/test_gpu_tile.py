@@ -1,0 +1,115 @@
+"""GPU parity of the per-tile streaming kernel (engine 2: one CTA per 8-vector tile runs the whole
+of Alg. 4 in one right-to-left pass over the leaf segments) against the CPU oracle.
+
+Cases span L = 1 .. 8, odd and even s, ragged batches (not a multiple of the 8-vector tile), both
+layouts, both directions and round trips; the gate is the north-star 1e-12 relative max norm.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from lc_inputs import batch
+
+pytestmark = pytest.mark.gpu
+
+GATE = 1e-12
+
+
+def _dev():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch.device("cuda", 0)
+
+
+def _plan(*a, **k):
+    from paper_2411_00033_b200 import Plan
+    return Plan(*a, **k)
+
+
+# (n, V): n = 129 -> L = 1; 1500 -> s = 24, L = 4; 3900 -> s = 31 (odd); 4096 -> L = 5, s = 32;
+# 5000 -> L = 6, s = 20; 8192 -> L = 6; 20000 -> L = 8, s = 20
+CASES = [(129, 8), (200, 13), (1000, 9), (1500, 3), (3900, 17), (4096, 8), (5000, 11), (8192, 10), (20000, 5)]
+
+
+@pytest.mark.parametrize("direction", ["leg2cheb", "cheb2leg"])
+@pytest.mark.parametrize("n,V", CASES)
+def test_tile_engine_vs_oracle(direction, n, V):
+    dev = _dev()
+    x = batch("normal_exp1000", n, V, seed=11)
+    p = _plan(n, direction, batch=V, device=dev, engine=2)
+    assert p.kernel_info["engine"] == 2 and p.kernels_per_execute == 1
+    z = p.execute(x.to(dev)).cpu().numpy()
+    for v in range(V):
+        e = oracle.einf(z[v], oracle.transform_rows(direction, x[v].numpy()))
+        assert e <= GATE, (n, V, v, direction, e, p.desc)
+
+
+@pytest.mark.parametrize("direction", ["leg2cheb", "cheb2leg"])
+def test_tile_engine_batch_layout_and_ld(direction):
+    dev = _dev()
+    n, V = 3000, 12
+    x = batch("normal", n, V, seed=5)
+    pv = _plan(n, direction, batch=V, device=dev, engine=2)
+    pb = _plan(n, direction, batch=V, device=dev, layout="batch", engine=2)
+    zv = pv.execute(x.to(dev))
+    zb = pb.execute(x.t().contiguous().to(dev))
+    assert torch.equal(zv, zb.t().contiguous())  # same arithmetic, only the addressing differs
+    # padded leading dimensions (VEC layout): ld_in = n + 7, ld_out = n + 3
+    xin = torch.zeros(V, n + 7, dtype=torch.float64)
+    xin[:, :n] = x
+    pl = _plan(n, direction, batch=V, device=dev, engine=2, ld_in=n + 7, ld_out=n + 3)
+    out = torch.full((V, n + 3), 7.0, dtype=torch.float64, device=dev)
+    pl.execute(xin.to(dev), out=out)
+    assert torch.equal(out[:, :n], zv)
+    assert torch.all(out[:, n:] == 7.0)  # nothing written past n
+
+
+def test_tile_engine_matches_level_pipeline():
+    dev = _dev()
+    n, V = 4096, 24
+    x = batch("normal_exp1000", n, V, seed=6).to(dev)
+    for direction in ("leg2cheb", "cheb2leg"):
+        z1 = _plan(n, direction, batch=V, device=dev, engine=1).execute(x)
+        z2 = _plan(n, direction, batch=V, device=dev, engine=2).execute(x)
+        e = (z1 - z2).abs().max().item() / z1.abs().max().item()
+        assert e <= 1e-13, (direction, e)
+
+
+@pytest.mark.parametrize("n", [1000, 4096])
+def test_tile_engine_round_trip(n):
+    dev = _dev()
+    V = 16
+    x = batch("normal_exp1000", n, V, seed=7).to(dev)
+    a = _plan(n, "leg2cheb", batch=V, device=dev, engine=2)
+    b = _plan(n, "cheb2leg", batch=V, device=dev, engine=2)
+    back = b.execute(a.execute(x)).cpu().numpy()
+    xs = x.cpu().numpy()
+    for v in range(V):
+        assert oracle.einf(back[v], xs[v]) <= GATE
+
+
+def test_tile_engine_automatic_choice():
+    dev = _dev()
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    big = _plan(4096, "leg2cheb", batch=4096, device=dev)  # cfg3: 512 tiles >= 2 per SM
+    assert big.kernel_info["engine"] == 2 and big.kernel_info["tile_grid"] <= 512
+    assert big.kernel_info["tile_grid"] <= 2 * sms * 2
+    few = _plan(4096, "leg2cheb", batch=16, device=dev)  # 2 tiles: level-pipelined kernels
+    assert few.kernel_info["engine"] == 1 and few.kernels_per_execute == 3
+    with pytest.raises(RuntimeError):
+        _plan(100, "leg2cheb", batch=8, device=dev, engine=2)  # L = 0: no hierarchy to stream
+
+
+def test_tile_engine_back_to_back_and_zero_vectors():
+    dev = _dev()
+    n, V = 2000, 20
+    p = _plan(n, "leg2cheb", batch=V, device=dev, engine=2)
+    x1 = batch("normal", n, V, seed=8).to(dev)
+    x2 = torch.zeros_like(x1)
+    z1a = p.execute(x1)
+    z2 = p.execute(x2)
+    z1b = p.execute(x1)
+    assert torch.equal(z1a, z1b)
+    assert torch.count_nonzero(z2) == 0
+    np.testing.assert_array_equal(z1a.cpu().numpy()[3], p.execute(x1).cpu().numpy()[3])

@@ -41,7 +41,7 @@ for _ in range(300):
     y = p.execute(x)
 torch.cuda.synchronize()
 NAMES = {"up": ["start", "staged", "step1", "subtreeM2M", "written", "cont", "contdone", "exit"],
-         "stream": ["start", "end", "banddone", "-", "-", "-", "-", "-"],
+         "stream": ["start", "end", "banddone", "-", "-", "-", "-", "m2ldone"],
          "down": ["start", "gdwait", "loaded", "chain", "subtree", "end", "-", "-"]}
 for rep in range(2):
     lib.lc_debug_clear()
@@ -65,6 +65,8 @@ for rep in range(2):
         st = (a[:, 0] - t0) / 1e3
         print(f"{name:6s}: CTAs {len(a):5d}  start min {st.min():7.2f} med {np.median(st):7.2f} max {st.max():7.2f} us")
         for ph in range(1, 8):
+            if NAMES[name][ph] == "-":
+                continue
             m = a[:, ph] > 0
             if m.sum() == 0:
                 continue
