@@ -1328,26 +1328,28 @@ __global__ void __launch_bounds__(NT, 512 / NT) lc_down_kernel(const DownParams 
 //   * the band of leaf row segment U reaches the end of segment U+1 (j_end, R4);
 //   * c of a segment is its M2L plus the L2L of its parent's c (step 4), and a parent is
 //     entered (at its rightmost leaf) no later than its children.
-// So when leaf U is reached, all w(g, t) for columns right of U are complete.  Per leaf step:
-//   phase A  [chain]  c(g, u_g) += B(p)^T c(g-1, u_g/2) for the levels entered at U (step 4)
-//            [M2L]    c_m2l(g, u') for the levels the NEXT leaf U-1 enters (step 3)
-//            [step 1] w(L-1, U) = f_U^sigma T(sigma)
-//            [band]   z(U) = direct band of rows U (step 6)
-//   phase B  [M2M]    w(g-1, u/2) = B(0) w(g, u) + B(1) w(g, u+1) while u is a left child (step 2)
-//            [step 5] z(U) += T(sigma) c(L-1, U); the store (with C^{-1}, step 7) happens in the
-//                     next step's phase A.
-// All contractions run on the fp64 tensor cores (DMMA m8n8k4) with the 8 vectors of the tile as
-// the n dimension.  State per CTA (doubles): w ring [L][3][2][8][18] (live columns u+1..u+3 of
-// every level), c slots [L][2][2][8][18] (by segment parity), an f/lambda ring of 4 leaf
-// segments (prefetched two steps ahead with cp.async), z stage [2][8][2s+4], T, B(0), tabA.
+// Leaf step U (one CTA barrier per step; a three-stage software pipeline over the leaves):
+//   [band]   z(U) = direct band of rows U (step 6)                        warps 0-3
+//   [eval]   z(U+1) += T(sigma) c(L-1, U+1) (step 5), C^{-1} (step 7), store      warps 0-3
+//   [step 1] w(L-1, U) = f_U^sigma T(sigma)                                warps 4-5
+//   [M2M]    w(g-1, u/2) = B(0) w(g, u) + B(1) w(g, u+1) while the segment u completed at leaf
+//            U+1 is a left child (step 2)                                  warps 4-5
+//   [chain]  c(g, u_g) += B(p)^T c(g-1, u_g/2) for the levels entered at U (step 4)  warps 6-7
+//   [M2L]    c_m2l(g, u') for the levels the next leaf U-1 enters (step 3)           warps 4-7
+// and the cp.async prefetch of leaf U-2.  Slots are chosen so that nothing a step writes is read
+// in the same step: w ring of 3 per level, c by segment parity (mod 3 on the leaf level), z by
+// leaf parity, f / lambda ring of 4 leaves.  All contractions run on the fp64 tensor cores (DMMA
+// m8n8k4) with the 8 vectors of the tile as the n dimension, 2-3 accumulator chains per warp.
 constexpr int kTileThreads = 256;
 constexpr int kTileV = 8;                  // vectors per tile (= DMMA n)
 constexpr int kTS = kTileV * kM;           // doubles per (segment, sigma) state
 __host__ __device__ inline int tile_fst(int s) { int f = 4; while (f < s) f += 16; return f; }
+// T [2][32][M] | B(0) [M][M]+4 | tabA [80] | f ring [4][2][8][fst] | lambda ring [4][4s] |
+// w ring [L][3][2][8][M] | c: levels < L-1 [2][2][8][M], level L-1 [3][2][8][M] | z [2][8][2s+4]
 __host__ __device__ inline int64_t tile_smem_doubles(int L, int s) {
   const int fst = tile_fst(s);
-  return 2 * 32 * kM + (kMM + 4) + 80 + 4 * 2 * kTileV * fst + 4 * 2 * s + int64_t(L) * 3 * 2 * kTS +
-         int64_t(L) * 2 * 2 * kTS + 2 * kTileV * (2 * s + 4);
+  return 2 * 32 * kM + (kMM + 4) + 80 + 4 * 2 * kTileV * fst + 4 * 4 * s + int64_t(L) * 3 * 2 * kTS +
+         int64_t(2 * L + 1) * 2 * kTS + 2 * kTileV * (2 * s + 4);
 }
 
 struct TileParams {
@@ -1366,7 +1368,6 @@ template <int DIR>
 __global__ void __launch_bounds__(kTileThreads, 2) lc_tile_kernel(const __grid_constant__ TileParams P) {
   extern __shared__ __align__(128) unsigned char smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  constexpr int nwarps = kTileThreads / 32;
   const int lr = lane >> 2, lc = lane & 3;
   const int s = P.s, L = P.L, seglen = 2 * s;
   const int fst = tile_fst(s), zst_ = 2 * s + 4;
@@ -1375,14 +1376,16 @@ __global__ void __launch_bounds__(kTileThreads, 2) lc_tile_kernel(const __grid_c
   double* Bq = Tq + 2 * 32 * kM;                  // B(0) [M][M]
   double* taq = Bq + kMM + 4;                     // tabA [80]
   double* fr = taq + 80;                          // [4][2][8][fst]
-  double* tbr = fr + 4 * 2 * kTileV * fst;        // [4][2s]
-  double* wr = tbr + 4 * seglen;                  // [L][3][2][8][M]
-  double* cs = wr + L * 3 * 2 * kTS;              // [L][2][2][8][M]
-  double* zs = cs + L * 2 * 2 * kTS;              // [2][8][2s+4]
+  double* lmr = fr + 4 * 2 * kTileV * fst;        // [4][4s]
+  double* wr = lmr + 4 * 4 * s;                   // [L][3][2][8][M]
+  double* cs = wr + L * 3 * 2 * kTS;              // [L-1][2][2][8][M] then [3][2][8][M]
+  double* zs = cs + (2 * L + 1) * 2 * kTS;        // [2][8][2s+4]
   auto fslot = [&](int U) { return fr + (U & 3) * 2 * kTileV * fst; };
-  auto tbslot = [&](int U) { return tbr + (U & 3) * seglen; };
+  auto lslot = [&](int U) { return lmr + (U & 3) * 4 * s; };
   auto wslot = [&](int g, int t) { return wr + (g * 3 + t % 3) * 2 * kTS; };
-  auto cslot = [&](int g, int u) { return cs + (g * 2 + (u & 1)) * 2 * kTS; };
+  auto cslot = [&](int g, int u) {
+    return g == L - 1 ? cs + (2 * (L - 1) + u % 3) * 2 * kTS : cs + (g * 2 + (u & 1)) * 2 * kTS;
+  };
   auto zbuf = [&](int U) { return zs + (U & 1) * kTileV * zst_; };
 
   for (int i = tid; i < 2 * 32 * kM / 2; i += kTileThreads) cp_async16(Tq + 2 * i, P.Tpad + 2 * i);
@@ -1394,40 +1397,31 @@ __global__ void __launch_bounds__(kTileThreads, 2) lc_tile_kernel(const __grid_c
   griddep_wait();  // the input may be produced by the preceding kernel
   griddep_launch();
 
-  // stage leaf segment U of the tile: f de-interleaved by parity, lambda (tabB) as is
+  // stage leaf segment U of the tile: f de-interleaved by parity ([sigma][v][m]), and the lambda
+  // (tabB) window [2sU, 2sU + 4s) that the band of rows U reads; zero beyond n / N
   auto stage = [&](int64_t tile, int U) {
     double* fd = fslot(U);
-    double* td = tbslot(U);
     const int64_t j0 = int64_t(U) * seglen;
-    for (int idx = tid; idx < kTileV * seglen; idx += kTileThreads) {
-      int v, x;
-      if (P.layout == LC_VEC_CONTIGUOUS) { v = idx / seglen; x = idx - v * seglen; }
-      else { x = idx / kTileV; v = idx - x * kTileV; }
-      const int64_t gv = tile * kTileV + v, j = j0 + x;
-      const bool ok = gv < P.batch && j < P.n;
-      const double* src = P.layout == LC_VEC_CONTIGUOUS ? P.in + gv * P.ld_in + j : P.in + j * P.ld_in + gv;
-      cp_async8(fd + ((x & 1) * kTileV + v) * fst + (x >> 1), ok ? src : P.in, ok ? 8u : 0u);
+    if (P.layout == LC_VEC_CONTIGUOUS) {  // warp = vector, lanes along the segment
+      const int64_t gv = tile * kTileV + warp;
+      const double* src = P.in + gv * P.ld_in + j0;
+      const int64_t lim = gv < P.batch ? P.n - j0 : 0;
+      for (int x = lane; x < seglen; x += 32) {
+        const bool ok = x < lim;
+        cp_async8(fd + ((x & 1) * kTileV + warp) * fst + (x >> 1), ok ? src + x : P.in, ok ? 8u : 0u);
+      }
+    } else {  // vectors fastest
+      for (int idx = tid; idx < kTileV * seglen; idx += kTileThreads) {
+        const int x = idx >> 3, v = idx & 7;
+        const int64_t gv = tile * kTileV + v, j = j0 + x;
+        const bool ok = gv < P.batch && j < P.n;
+        cp_async8(fd + ((x & 1) * kTileV + v) * fst + (x >> 1), ok ? P.in + j * P.ld_in + gv : P.in, ok ? 8u : 0u);
+      }
     }
-    for (int x = tid; x < seglen; x += kTileThreads) {
+    double* ld = lslot(U);
+    for (int x = tid; x < 2 * seglen; x += kTileThreads) {
       const bool ok = j0 + x < P.N;
-      cp_async8(td + x, ok ? P.tabB + j0 + x : P.tabB, ok ? 8u : 0u);
-    }
-  };
-  // coalesced store of z(U) with C^{-1} (L2C, step 7)
-  auto store = [&](int64_t tile, int U) {
-    const double* zb = zbuf(U);
-    const int64_t j0 = int64_t(U) * seglen;
-    const double inv_pi = 0.318309886183790671537767526745028724;
-    for (int idx = tid; idx < kTileV * seglen; idx += kTileThreads) {
-      int v, x;
-      if (P.layout == LC_VEC_CONTIGUOUS) { v = idx / seglen; x = idx - v * seglen; }
-      else { x = idx / kTileV; v = idx - x * kTileV; }
-      const int64_t gv = tile * kTileV + v, i = j0 + x;
-      if (gv >= P.batch || i >= P.n) continue;
-      double z = zb[v * zst_ + x];
-      if (DIR == 0) z *= (i == 0 ? inv_pi : 2.0 * inv_pi);
-      if (P.layout == LC_VEC_CONTIGUOUS) P.out[gv * P.ld_out + i] = z;
-      else P.out[i * P.ld_out + gv] = z;
+      cp_async8(ld + x, ok ? P.tabB + j0 + x : P.tabB, ok ? 8u : 0u);
     }
   };
   // first level entered at leaf U (U is the rightmost leaf of its segments on levels >= gmin)
@@ -1436,13 +1430,13 @@ __global__ void __launch_bounds__(kTileThreads, 2) lc_tile_kernel(const __grid_c
     const int g = L - 1 - ones;
     return g < 0 ? 0 : g;
   };
+  const double inv_pi = 0.318309886183790671537767526745028724;
 
   for (int64_t tile = blockIdx.x; tile < P.ntiles; tile += gridDim.x) {
-    for (int i = tid; i < L * 2 * 2 * kTS; i += kTileThreads) cs[i] = 0.0;  // c_m2l of rows without M2L stay 0
+    for (int i = tid; i < (2 * L + 1) * 2 * kTS; i += kTileThreads) cs[i] = 0.0;  // rows without M2L stay 0
     {
       double* fz = fslot(nls);  // the segment past the end reads as zero
       for (int i = tid; i < 2 * kTileV * fst; i += kTileThreads) fz[i] = 0.0;
-      for (int i = tid; i < seglen; i += kTileThreads) tbslot(nls)[i] = 0.0;
     }
     stage(tile, nls - 1);
     cp_async_commit();
@@ -1451,126 +1445,71 @@ __global__ void __launch_bounds__(kTileThreads, 2) lc_tile_kernel(const __grid_c
     cp_async_wait<1>();
     __syncthreads();
 
-    for (int U = nls - 1; U >= 0; --U) {
+    for (int U = nls - 1; U >= -1; --U) {
       if (U >= 2) stage(tile, U - 2);
       cp_async_commit();
-      if (U + 1 < nls) store(tile, U + 1);
-      // ------------------------------------------------------------ phase A
-      const int gA = gmin_of(U);
-      const int gN = U >= 1 ? gmin_of(U - 1) : L;  // levels the next leaf enters: gN..L-1
-      const int nm2l = (L - gN) * 6;
-      const int njobs = 2 + nm2l + 6 + 8;
-      for (int job = warp; job < njobs; job += nwarps) {
-        if (job < 2) {
-          // step 4 chain (sigma = job) over the levels entered at U, coarse to fine
-          const int sg = job;
-          for (int g = (gA > 0 ? gA : 1); g < L; ++g) {
-            const int u = U >> (L - 1 - g);
-            const int p = u & 1;
-            const double* par = cslot(g - 1, u >> 1) + sg * kTS;
-            double* dst = cslot(g, u) + sg * kTS;
-#pragma unroll
-            for (int mt = 0; mt < 3; ++mt) {
-              double acc[2] = {0.0, 0.0};
-#pragma unroll
-              for (int kk = 0; kk < 5; ++kk) {
-                if (4 * kk + 3 < 8 * mt) continue;  // n < k everywhere
-                const int nn = 4 * kk + lc, k = 8 * mt + lr;
-                const double b = nn < kM ? par[lr * kM + nn] : 0.0;
-                double a = (k < kM && nn < kM) ? Bq[nn * kM + k] : 0.0;  // b_{n k}
-                if (p && ((k + nn) & 1)) a = -a;
-                dmma(acc, a, b);
-              }
-              const int k = 8 * mt + lr;
-              if (k < kM) {
-                dst[(2 * lc) * kM + k] += acc[0];
-                dst[(2 * lc + 1) * kM + k] += acc[1];
-              }
-            }
-            __syncwarp();
-          }
-        } else if (job < 2 + nm2l) {
-          // step 3 for the row the next leaf enters on level g: c(u') = sum_r A_hat w(t_r)
-          const int jj = job - 2;
-          const int g = gN + jj / 6, sg = (jj % 6) & 1, mt = (jj % 6) >> 1;
-          const int u = (U - 1) >> (L - 1 - g);
-          double acc[2] = {0.0, 0.0};
-          if (u < (4 << g) - 2) {
-            const int b = u >> 1, p = u & 1;
-            const int mode = 8 * mt + lr;
-            for (int mi = 0; mi < (p ? 1 : 2); ++mi) {
-              const int r = p ? 2 : mi;
-              const int t = u + 2 + (p ? 0 : mi);
-              const double* Am = P.A + (ahat_level_offset(g) + 3 * int64_t(b) + r) * kMM;
-              const double* W = wslot(g, t) + sg * kTS;
-              double av[5];
-#pragma unroll
-              for (int kk = 0; kk < 5; ++kk) {
-                const int k = 4 * kk + lc;
-                av[kk] = (mode < kM && k < kM) ? __ldg(Am + mode * kM + k) : 0.0;
-              }
-#pragma unroll
-              for (int kk = 0; kk < 5; ++kk) {
-                const int k = 4 * kk + lc;
-                const double bb = k < kM ? W[lr * kM + k] : 0.0;
-                dmma(acc, av[kk], bb);
-              }
-            }
-          }
-          const int mode = 8 * mt + lr;
-          if (mode < kM) {
-            double* dst = cslot(g, u) + sg * kTS;
-            dst[(2 * lc) * kM + mode] = acc[0];
-            dst[(2 * lc + 1) * kM + mode] = acc[1];
-          }
-        } else if (job < 2 + nm2l + 6) {
-          // step 1: w(L-1, U)[sigma][v][mode] = sum_m T(sigma)[m][mode] f_v[2sU + 2m + sigma]
-          const int jj = job - 2 - nm2l;
-          const int sg = jj & 1, mt = jj >> 1;
-          const int mode = 8 * mt + lr;
-          const double* fv = fslot(U) + (sg * kTileV + lr) * fst;
-          const double* Tm = Tq + sg * 32 * kM;
-          double acc[2] = {0.0, 0.0};
-          const int nks = (s + 3) >> 2;
-          for (int kk = 0; kk < nks; ++kk) {
-            const int m = 4 * kk + lc;
-            const double a = mode < kM ? Tm[m * kM + mode] : 0.0;
-            dmma(acc, a, fv[m]);
-          }
-          if (mode < kM) {
-            double* dst = wslot(L - 1, U) + sg * kTS;
-            dst[(2 * lc) * kM + mode] = acc[0];
-            dst[(2 * lc + 1) * kM + mode] = acc[1];
-          }
-        } else {
-          // step 6: rows i = 2sU + 2r + sigma, columns j = 2sU + 2c + sigma (c >= r, j < j_end),
-          // K[r][c] = a[c-r] b[(i+j)/2] formed per lane, G[c][v] = f_v[j] (C2L: j f_j)
-          const int jj = job - 2 - nm2l - 6;
-          const int sg = jj & 1, rb = jj >> 1;
-          if (8 * rb < s) {
-            const int r = 8 * rb + lr;
-            const double* f0 = fslot(U) + (sg * kTileV + lr) * fst;
-            const double* f1 = fslot(U + 1) + (sg * kTileV + lr) * fst;
-            const double* t0 = tbslot(U);
-            const double* t1 = tbslot(U + 1);
-            const int64_t i0 = int64_t(U) * seglen;
-            double acc[2] = {0.0, 0.0};
-            const int nkc = (seglen + 3) >> 2;
-            for (int kc = 2 * rb; kc < nkc; ++kc) {
+      const int V1 = U + 1;  // the leaf whose step 5 / step 2 run in this step
+      if (warp < 4) {
+        if (U >= 0 && 8 * ((warp >> 1) ? 1 : 0) < s) {
+          // ---- step 6: rows i = 2sU + 2r + sigma, columns j = 2sU + 2c + sigma (c >= r, j < j_end),
+          // K[r][c] = a[c-r] b[(i+j)/2] formed per lane, G[c][v] = f_v[j] (C2L: j f_j); row tiles
+          // {0,3} or {1,2} per warp (two accumulator chains)
+          const int sg = warp & 1;
+          const int rlo = (warp >> 1) ? 1 : 0, rhi = (warp >> 1) ? 2 : 3;
+          const bool hion = 8 * rhi < s;
+          const double* fU = fslot(U) + (sg * kTileV + lr) * fst;
+          const double* fU1 = fslot(U + 1) + (sg * kTileV + lr) * fst;
+          const double* lw = lslot(U);
+          const int64_t i0 = int64_t(U) * seglen;
+          double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+          if ((s & 7) == 0) {  // fast path: row tiles full, chunk boundary = segment boundary
+            const double* lamw = lw + sg + lr + lc;  // lambda[(i+j)/2 - 2sU] = lamw[8 rb + 4 kc]
+            const double* tap = taq + lc - lr;       // a[c - r] = tap[4 kc - 8 rb]
+            const int nkc = seglen >> 2, s4 = s >> 2;
+            for (int kc = 2 * rlo; kc < nkc; ++kc) {
               const int c = 4 * kc + lc;
-              double b = c < s ? f0[c] : (c < seglen ? f1[c - s] : 0.0);
+              double b = kc < s4 ? fU[c] : fU1[c - s];
               if (DIR == 1) b *= double(i0 + 2 * c + sg);
-              const int x = r + c + sg;  // (i + j)/2 - 2sU
-              const double lam = x < seglen ? t0[x] : t1[x - seglen];
-              const double a = (c >= r && c < seglen && r < s) ? taq[c - r] * lam : 0.0;
-              dmma(acc, a, b);
+              {
+                const int d = 4 * kc - 8 * rlo;
+                double a = tap[d] * lamw[8 * rlo + 4 * kc];
+                if (d < 8 && lc + d < lr) a = 0.0;  // c < r inside the diagonal block
+                dmma(acc[0], a, b);
+              }
+              if (hion && kc >= 2 * rhi) {
+                const int d = 4 * kc - 8 * rhi;
+                double a = tap[d] * lamw[8 * rhi + 4 * kc];
+                if (d < 8 && lc + d < lr) a = 0.0;
+                dmma(acc[1], a, b);
+              }
             }
+          } else {  // general s: masks on rows, columns and the segment boundary
+            const int nkc = (seglen + 3) >> 2;
+            for (int kc = 2 * rlo; kc < nkc; ++kc) {
+              const int c = 4 * kc + lc;
+              double b = c < s ? fU[c] : (c < seglen ? fU1[c - s] : 0.0);
+              if (DIR == 1) b *= double(i0 + 2 * c + sg);
+#pragma unroll
+              for (int q = 0; q < 2; ++q) {
+                const int rb = q ? rhi : rlo;
+                if (8 * rb < s && kc >= 2 * rb) {
+                  const int r = 8 * rb + lr;
+                  const double lam = lw[r + c + sg];
+                  const double a = (c >= r && c < seglen && r < s) ? taq[c >= r ? c - r : 0] * lam : 0.0;
+                  dmma(acc[q], a, b);
+                }
+              }
+            }
+          }
+          double* zb = zbuf(U);
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            const int r = 8 * (q ? rhi : rlo) + lr;
             if (r < s) {
-              double* zb = zbuf(U);
 #pragma unroll
               for (int h = 0; h < 2; ++h) {
                 const int v = 2 * lc + h;
-                double z = acc[h];
+                double z = acc[q][h];
                 if (DIR == 1) {
                   const int64_t ir = i0 + 2 * r + sg;
                   z *= double(2 * ir + 1);
@@ -1581,72 +1520,189 @@ __global__ void __launch_bounds__(kTileThreads, 2) lc_tile_kernel(const __grid_c
             }
           }
         }
-      }
-      cp_async_wait<1>();  // f(U-1) landed
-      __syncthreads();
-      // ------------------------------------------------------------ phase B
-      const int ncas = (U & 1) == 0 ? 2 : 0;
-      for (int job = warp; job < ncas + 8; job += nwarps) {
-        if (job < ncas) {
-          // step 2 cascade (sigma = job) while the completed segment is a left child
-          const int sg = job;
-          int g = L - 1, u = U;
-          while (g > 0 && (u & 1) == 0) {
-            const double* x0 = wslot(g, u) + sg * kTS;
-            const double* x1 = wslot(g, u + 1) + sg * kTS;
-            double* o = wslot(g - 1, u >> 1) + sg * kTS;
+        if (V1 < nls && 16 * (warp >> 1) < s) {
+          // ---- step 5 of leaf V1: z[v][2m + sigma] += sum_k T(sigma)[m][k] c(L-1, V1)[sigma][v][k],
+          // row tiles {2h, 2h+1}; then C^{-1} (step 7) and the store of those rows
+          const int sg = warp & 1, mt0 = 2 * (warp >> 1);
+          const double* cc = cslot(L - 1, V1) + sg * kTS;
+          double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+          for (int kk = 0; kk < 5; ++kk) {
+            const int k = 4 * kk + lc;
+            const double bb = k < kM ? cc[lr * kM + k] : 0.0;
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+              const int m = 8 * (mt0 + q) + lr;
+              const double a = k < kM ? Tq[(sg * 32 + m) * kM + k] : 0.0;
+              dmma(acc[q], a, bb);
+            }
+          }
+          const double* zb = zbuf(V1);
+          const int64_t i0 = int64_t(V1) * seglen;
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            const int m = 8 * (mt0 + q) + lr;
+            if (m < s) {
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                const int v = 2 * lc + h;
+                const int64_t gv = tile * kTileV + v, i = i0 + 2 * m + sg;
+                double z = zb[v * zst_ + 2 * m + sg] + acc[q][h];
+                if (DIR == 0) z *= (i == 0 ? inv_pi : 2.0 * inv_pi);
+                if (gv < P.batch && i < P.n) {
+                  if (P.layout == LC_VEC_CONTIGUOUS) P.out[gv * P.ld_out + i] = z;
+                  else P.out[i * P.ld_out + gv] = z;
+                }
+              }
+            }
+          }
+        }
+      } else {
+        const int sg = warp & 1;
+        if (warp < 6) {
+          if (U >= 0) {
+            // ---- step 1: w(L-1, U)[sigma][v][mode] = sum_m T(sigma)[m][mode] f_v[2sU + 2m + sigma]
+            const double* fv = fslot(U) + (sg * kTileV + lr) * fst;
+            const double* Tm = Tq + sg * 32 * kM;
+            double acc[3][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+            const int nks = (s + 3) >> 2;
+            for (int kk = 0; kk < nks; ++kk) {
+              const int m = 4 * kk + lc;
+              const double bb = fv[m];
+#pragma unroll
+              for (int mt = 0; mt < 3; ++mt) {
+                const int mode = 8 * mt + lr;
+                dmma(acc[mt], mode < kM ? Tm[m * kM + mode] : 0.0, bb);
+              }
+            }
+            double* dst = wslot(L - 1, U) + sg * kTS;
 #pragma unroll
             for (int mt = 0; mt < 3; ++mt) {
-              double acc[2] = {0.0, 0.0};
+              const int mode = 8 * mt + lr;
+              if (mode < kM) {
+                dst[(2 * lc) * kM + mode] = acc[mt][0];
+                dst[(2 * lc + 1) * kM + mode] = acc[mt][1];
+              }
+            }
+          }
+          // ---- step 2 cascade from leaf V1 (complete since the last step) while it is a left child
+          // (w(g, 0) feeds no M2L: the cascade of leaf 0 is skipped)
+          if (V1 >= 2 && V1 < nls && (V1 & 1) == 0) {
+            int g = L - 1, u = V1;
+            while (g > 0 && (u & 1) == 0) {
+              const double* x0 = wslot(g, u) + sg * kTS;
+              const double* x1 = wslot(g, u + 1) + sg * kTS;
+              double* o = wslot(g - 1, u >> 1) + sg * kTS;
+              double acc[3][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
 #pragma unroll
               for (int kk = 0; kk < 9; ++kk) {
-                if (mt == 0 && (kk == 2 || kk == 3 || kk == 7 || kk == 8)) continue;  // k >= 8 > n
                 const int kap = 4 * kk + lc;
                 const int child = kap >= kM ? 1 : 0;
                 const int kx = kap - child * kM;
-                const double b = (child ? x1 : x0)[lr * kM + kx];
-                const int nn = 8 * mt + lr;
-                double a = nn < kM ? Bq[nn * kM + kx] : 0.0;
-                if (child && ((nn - kx) & 1)) a = -a;
-                dmma(acc, a, b);
+                const double bb = (child ? x1 : x0)[lr * kM + kx];
+#pragma unroll
+                for (int mt = 0; mt < 3; ++mt) {
+                  if (mt == 0 && (kk == 2 || kk == 3 || kk == 7 || kk == 8)) continue;  // k >= 8 > n
+                  const int nn = 8 * mt + lr;
+                  double a = nn < kM ? Bq[nn * kM + kx] : 0.0;
+                  if (child && ((nn - kx) & 1)) a = -a;
+                  dmma(acc[mt], a, bb);
+                }
               }
-              const int nn = 8 * mt + lr;
-              if (nn < kM) {
-                o[(2 * lc) * kM + nn] = acc[0];
-                o[(2 * lc + 1) * kM + nn] = acc[1];
+#pragma unroll
+              for (int mt = 0; mt < 3; ++mt) {
+                const int nn = 8 * mt + lr;
+                if (nn < kM) {
+                  o[(2 * lc) * kM + nn] = acc[mt][0];
+                  o[(2 * lc + 1) * kM + nn] = acc[mt][1];
+                }
+              }
+              __syncwarp();
+              --g;
+              u >>= 1;
+            }
+          }
+        } else if (U >= 0) {
+          // ---- step 4 chain (sigma) over the levels entered at U, coarse to fine
+          const int gA = gmin_of(U);
+          for (int g = (gA > 0 ? gA : 1); g < L; ++g) {
+            const int u = U >> (L - 1 - g);
+            const int p = u & 1;
+            const double* par = cslot(g - 1, u >> 1) + sg * kTS;
+            double* dst = cslot(g, u) + sg * kTS;
+            double acc[3][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+            for (int kk = 0; kk < 5; ++kk) {
+              const int nn = 4 * kk + lc;
+              const double bb = nn < kM ? par[lr * kM + nn] : 0.0;
+#pragma unroll
+              for (int mt = 0; mt < 3; ++mt) {
+                if (4 * kk + 3 < 8 * mt) continue;  // n < k everywhere
+                const int k = 8 * mt + lr;
+                double a = (k < kM && nn < kM) ? Bq[nn * kM + k] : 0.0;  // b_{n k}
+                if (p && ((k + nn) & 1)) a = -a;
+                dmma(acc[mt], a, bb);
+              }
+            }
+#pragma unroll
+            for (int mt = 0; mt < 3; ++mt) {
+              const int k = 8 * mt + lr;
+              if (k < kM) {
+                dst[(2 * lc) * kM + k] += acc[mt][0];
+                dst[(2 * lc + 1) * kM + k] += acc[mt][1];
               }
             }
             __syncwarp();
-            --g;
-            u >>= 1;
           }
-        } else {
-          // step 5: z(U)[v][2m + sigma] += sum_k T(sigma)[m][k] c(L-1, U)[sigma][v][k]
-          const int jj = job - ncas;
-          const int sg = jj & 1, mt = jj >> 1;
-          if (8 * mt < s) {
-            const double* cc = cslot(L - 1, U) + sg * kTS;
-            const int m = 8 * mt + lr;
-            const double* Tm = Tq + (sg * 32 + m) * kM;
-            double acc[2] = {0.0, 0.0};
+        }
+        // ---- step 3 for the rows the next leaf enters: job k = (level gN + k/2, sigma k&1) on warp
+        // 6, 7, 4, 5, 6, ...: c(u') = sum_r A_hat_r w(t_r)
+        if (U >= 1) {
+          const int gN = gmin_of(U - 1);
+          const int nm2l = (L - gN) * 2;
+          for (int k = (warp - 6) & 3; k < nm2l; k += 4) {
+            const int g = gN + (k >> 1), sgk = k & 1;
+            const int u = (U - 1) >> (L - 1 - g);
+            double acc[3][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+            if (u < (4 << g) - 2) {
+              const int b = u >> 1, p = u & 1;
+              for (int mi = 0; mi < (p ? 1 : 2); ++mi) {
+                const int r = p ? 2 : mi;
+                const int t = u + 2 + (p ? 0 : mi);
+                const double* Am = P.A + (ahat_level_offset(g) + 3 * int64_t(b) + r) * kMM;
+                const double* W = wslot(g, t) + sgk * kTS;
+                double av[3][5];
 #pragma unroll
-            for (int kk = 0; kk < 5; ++kk) {
-              const int k = 4 * kk + lc;
-              const double a = k < kM ? Tm[k] : 0.0;
-              const double b = k < kM ? cc[lr * kM + k] : 0.0;
-              dmma(acc, a, b);
+                for (int mt = 0; mt < 3; ++mt)
+#pragma unroll
+                  for (int kk = 0; kk < 5; ++kk) {
+                    const int kx = 4 * kk + lc, mode = 8 * mt + lr;
+                    av[mt][kk] = (mode < kM && kx < kM) ? __ldg(Am + mode * kM + kx) : 0.0;
+                  }
+#pragma unroll
+                for (int kk = 0; kk < 5; ++kk) {
+                  const int kx = 4 * kk + lc;
+                  const double bb = kx < kM ? W[lr * kM + kx] : 0.0;
+#pragma unroll
+                  for (int mt = 0; mt < 3; ++mt) dmma(acc[mt], av[mt][kk], bb);
+                }
+              }
             }
-            if (m < s) {
-              double* zb = zbuf(U);
-              zb[(2 * lc) * zst_ + 2 * m + sg] += acc[0];
-              zb[(2 * lc + 1) * zst_ + 2 * m + sg] += acc[1];
+            double* dst = cslot(g, u) + sgk * kTS;
+#pragma unroll
+            for (int mt = 0; mt < 3; ++mt) {
+              const int mode = 8 * mt + lr;
+              if (mode < kM) {
+                dst[(2 * lc) * kM + mode] = acc[mt][0];
+                dst[(2 * lc + 1) * kM + mode] = acc[mt][1];
+              }
             }
           }
         }
       }
+      cp_async_wait<1>();  // f(U-1) landed
       __syncthreads();
     }
-    store(tile, 0);
     cp_async_wait<0>();
     __syncthreads();
   }
