@@ -1364,6 +1364,52 @@ struct TileParams {
   int layout, L, s;
 };
 
+// debug build: per (CTA, warp) cycle accounting of the tile kernel in g_lc_ts[0]:
+// [0] band / step 1 / chain, [1] eval / cascade, [2] M2L jobs, [3] end of step, [4] steps
+#ifdef LC_PHASE_TIMING
+#define TP_DECL long long tp_t0 = clock64();
+#define TP_MARK(slot)                                                                           \
+  do {                                                                                          \
+    const long long tp_t1 = clock64();                                                          \
+    if (lane == 0 && blockIdx.x < 4096)                                                         \
+      g_lc_ts[0][(blockIdx.x * 8 + warp) * 8 + (slot)] += (unsigned long long)(tp_t1 - tp_t0);  \
+    tp_t0 = tp_t1;                                                                              \
+  } while (0)
+#define TP_COUNT(slot, v) \
+  do { if (lane == 0 && blockIdx.x < 4096) g_lc_ts[0][(blockIdx.x * 8 + warp) * 8 + (slot)] += (v); } while (0)
+#else
+#define TP_DECL
+#define TP_MARK(slot) ((void)0)
+#define TP_COUNT(slot, v) ((void)0)
+#endif
+
+// Step 6 of one leaf for s = 32, row tiles RLO < RHI, everything unrolled at compile time:
+// K[r][c] = a[c-r] lambda[(i+j)/2] (per lane, one DMUL), G[c][v] = f_v[j] (C2L: j f_j).  Pointers are
+// pre-offset by the lane: fU/fU1 -> f[sigma][v = lr][lc], lamw -> lambda window + sigma + lr + lc,
+// tap -> a + lc - lr; the c >= r mask only exists in the two diagonal chunks of each row tile.
+template <int DIR, int RLO, int RHI>
+__device__ __forceinline__ void band32(const double* __restrict__ fU, const double* __restrict__ fU1,
+                                       const double* __restrict__ lamw, const double* __restrict__ tap,
+                                       int64_t i0, int sg, int lc, int lr, double (&acc)[2][2]) {
+#pragma unroll
+  for (int kc = 2 * RLO; kc < 16; ++kc) {
+    double b = kc < 8 ? fU[4 * kc] : fU1[4 * kc - 32];
+    if (DIR == 1) b *= double(i0 + 2 * (4 * kc + lc) + sg);
+    {
+      constexpr int dummy = 0;
+      (void)dummy;
+      double a = tap[4 * kc - 8 * RLO] * lamw[8 * RLO + 4 * kc];
+      if (kc < 2 * RLO + 2 && lc + 4 * (kc - 2 * RLO) < lr) a = 0.0;
+      dmma(acc[0], a, b);
+    }
+    if (kc >= 2 * RHI) {
+      double a = tap[4 * kc - 8 * RHI] * lamw[8 * RHI + 4 * kc];
+      if (kc < 2 * RHI + 2 && lc + 4 * (kc - 2 * RHI) < lr) a = 0.0;
+      dmma(acc[1], a, b);
+    }
+  }
+}
+
 template <int DIR>
 __global__ void __launch_bounds__(kTileThreads, 2) lc_tile_kernel(const __grid_constant__ TileParams P) {
   extern __shared__ __align__(128) unsigned char smem[];
@@ -1445,6 +1491,7 @@ __global__ void __launch_bounds__(kTileThreads, 2) lc_tile_kernel(const __grid_c
     cp_async_wait<1>();
     __syncthreads();
 
+    TP_DECL
     for (int U = nls - 1; U >= -1; --U) {
       if (U >= 2) stage(tile, U - 2);
       cp_async_commit();
@@ -1462,7 +1509,16 @@ __global__ void __launch_bounds__(kTileThreads, 2) lc_tile_kernel(const __grid_c
           const double* lw = lslot(U);
           const int64_t i0 = int64_t(U) * seglen;
           double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
-          if ((s & 7) == 0) {  // fast path: row tiles full, chunk boundary = segment boundary
+          if (s == 32) {
+            const double* fa = fU + lc;
+            const double* fb = fU1 + lc;
+            const double* lamw = lw + sg + lr + lc;
+            const double* tap = taq + lc - lr;
+            if (rlo == 0)
+              band32<DIR, 0, 3>(fa, fb, lamw, tap, i0, sg, lc, lr, acc);
+            else
+              band32<DIR, 1, 2>(fa, fb, lamw, tap, i0, sg, lc, lr, acc);
+          } else if ((s & 7) == 0) {  // fast path: row tiles full, chunk boundary = segment boundary
             const double* lamw = lw + sg + lr + lc;  // lambda[(i+j)/2 - 2sU] = lamw[8 rb + 4 kc]
             const double* tap = taq + lc - lr;       // a[c - r] = tap[4 kc - 8 rb]
             const int nkc = seglen >> 2, s4 = s >> 2;
@@ -1520,6 +1576,7 @@ __global__ void __launch_bounds__(kTileThreads, 2) lc_tile_kernel(const __grid_c
             }
           }
         }
+        TP_MARK(0);
         if (V1 < nls && 16 * (warp >> 1) < s) {
           // ---- step 5 of leaf V1: z[v][2m + sigma] += sum_k T(sigma)[m][k] c(L-1, V1)[sigma][v][k],
           // row tiles {2h, 2h+1}; then C^{-1} (step 7) and the store of those rows
@@ -1565,14 +1622,26 @@ __global__ void __launch_bounds__(kTileThreads, 2) lc_tile_kernel(const __grid_c
             const double* fv = fslot(U) + (sg * kTileV + lr) * fst;
             const double* Tm = Tq + sg * 32 * kM;
             double acc[3][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
-            const int nks = (s + 3) >> 2;
-            for (int kk = 0; kk < nks; ++kk) {
-              const int m = 4 * kk + lc;
-              const double bb = fv[m];
+            if (s == 32) {  // compile-time K: immediate offsets, no loop control
+              const double* fq = fv + lc;
+              const double* tq = Tm + lc * kM + lr;
 #pragma unroll
-              for (int mt = 0; mt < 3; ++mt) {
-                const int mode = 8 * mt + lr;
-                dmma(acc[mt], mode < kM ? Tm[m * kM + mode] : 0.0, bb);
+              for (int kk = 0; kk < 8; ++kk) {
+                const double bb = fq[4 * kk];
+#pragma unroll
+                for (int mt = 0; mt < 3; ++mt)
+                  dmma(acc[mt], (mt < 2 || lr < 2) ? tq[4 * kk * kM + 8 * mt] : 0.0, bb);
+              }
+            } else {
+              const int nks = (s + 3) >> 2;
+              for (int kk = 0; kk < nks; ++kk) {
+                const int m = 4 * kk + lc;
+                const double bb = fv[m];
+#pragma unroll
+                for (int mt = 0; mt < 3; ++mt) {
+                  const int mode = 8 * mt + lr;
+                  dmma(acc[mt], mode < kM ? Tm[m * kM + mode] : 0.0, bb);
+                }
               }
             }
             double* dst = wslot(L - 1, U) + sg * kTS;
@@ -1585,6 +1654,7 @@ __global__ void __launch_bounds__(kTileThreads, 2) lc_tile_kernel(const __grid_c
               }
             }
           }
+          TP_MARK(0);
           // ---- step 2 cascade from leaf V1 (complete since the last step) while it is a left child
           // (w(g, 0) feeds no M2L: the cascade of leaf 0 is skipped)
           if (V1 >= 2 && V1 < nls && (V1 & 1) == 0) {
@@ -1655,6 +1725,7 @@ __global__ void __launch_bounds__(kTileThreads, 2) lc_tile_kernel(const __grid_c
             __syncwarp();
           }
         }
+        TP_MARK(1);
         // ---- step 3 for the rows the next leaf enters: job k = (level gN + k/2, sigma k&1) on warp
         // 6, 7, 4, 5, 6, ...: c(u') = sum_r A_hat_r w(t_r)
         if (U >= 1) {
@@ -1700,8 +1771,11 @@ __global__ void __launch_bounds__(kTileThreads, 2) lc_tile_kernel(const __grid_c
           }
         }
       }
+      TP_MARK(2);
       cp_async_wait<1>();  // f(U-1) landed
       __syncthreads();
+      TP_MARK(3);
+      TP_COUNT(4, 1);
     }
     cp_async_wait<0>();
     __syncthreads();

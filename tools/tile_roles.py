@@ -28,9 +28,9 @@ buf = np.zeros(1 << 20, dtype=np.uint64)
 lib.lc_debug_timestamps(0, buf.ctypes.data_as(ctypes.POINTER(ctypes.c_ulonglong)), buf.size)
 grid = p.kernel_info["tile_grid"]
 a = buf[: grid * 64].reshape(grid, 8, 8).astype(np.float64)
-steps = a[:, :, 3].sum(axis=0)
+steps = a[:, :, 4].sum(axis=0)
 print(f"n={n} batch={V} grid={grid}; cycles per leaf step, mean over CTAs")
 for w in range(8):
     st = max(steps[w], 1)
-    print(f"warp {w}: band {a[:, w, 5].sum() / st:8.0f}  work {a[:, w, 0].sum() / st:8.0f}  m2l {a[:, w, 1].sum() / st:8.0f}  "
-          f"end(wait+barrier) {a[:, w, 2].sum() / st:8.0f}  m2l jobs/step {a[:, w, 4].sum() / st:5.2f}")
+    print(f"warp {w}: role-a {a[:, w, 0].sum() / st:7.0f}  role-b {a[:, w, 1].sum() / st:7.0f}  "
+          f"m2l {a[:, w, 2].sum() / st:7.0f}  end {a[:, w, 3].sum() / st:7.0f}")
