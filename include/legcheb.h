@@ -159,6 +159,8 @@ lc_status lc_plan_export(const lc_plan* p, int32_t what, double* host_out, int64
  * values written through *written (may be NULL).  Errors: INVALID_ARG on NULL p or out. */
 lc_status lc_plan_kernel_info(const lc_plan* p, int64_t* out, int32_t count, int32_t* written);
 
+/* Frees the plan's device arrays and its own workspace after synchronizing the plan's device
+ * (executions still in flight may read them).  Errors: INVALID_ARG on NULL p. */
 lc_status lc_plan_destroy(lc_plan* p);
 
 const char* lc_status_string(lc_status s);

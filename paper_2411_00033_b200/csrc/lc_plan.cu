@@ -392,6 +392,9 @@ extern "C" lc_status lc_plan_destroy(lc_plan* p) {
   int prev = 0;
   cudaGetDevice(&prev);
   cudaSetDevice(p->device);
+  // executions still in flight on any stream may read the plan's arrays and workspace: finish them
+  // before the memory can be handed to another allocation
+  cudaDeviceSynchronize();
   cudaFree(p->d_A);
   cudaFree(p->d_tabB);
   cudaFree(p->d_tabA);
