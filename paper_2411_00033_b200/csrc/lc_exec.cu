@@ -1440,6 +1440,7 @@ __global__ void __launch_bounds__(kTileThreads, 2) lc_tile_kernel(const __grid_c
   // rows m in [s, fst) of every f slot stay zero (read by the K = 4 ceil(s/4) steps of step 1)
   for (int i = tid; i < 4 * 2 * kTileV * fst; i += kTileThreads) fr[i] = 0.0;
   cp_async_commit();
+  __syncthreads();  // the zero fill precedes every cp.async into the ring (other threads' elements)
   griddep_wait();  // the input may be produced by the preceding kernel
   griddep_launch();
 
