@@ -1367,20 +1367,26 @@ struct TileParams {
 // debug build: per (CTA, warp) cycle accounting of the tile kernel in g_lc_ts[0]:
 // [0] band / step 1 / chain, [1] eval / cascade, [2] M2L jobs, [3] end of step, [4] steps
 #ifdef LC_PHASE_TIMING
-#define TP_DECL long long tp_t0 = clock64();
-#define TP_MARK(slot)                                                                           \
-  do {                                                                                          \
-    const long long tp_t1 = clock64();                                                          \
-    if (lane == 0 && blockIdx.x < 4096)                                                         \
-      g_lc_ts[0][(blockIdx.x * 8 + warp) * 8 + (slot)] += (unsigned long long)(tp_t1 - tp_t0);  \
-    tp_t0 = tp_t1;                                                                              \
+#define TP_DECL                                  \
+  long long tp_t0 = clock64();                   \
+  unsigned long long tp_acc[6] = {0, 0, 0, 0, 0, 0};
+#define TP_MARK(slot)                            \
+  do {                                           \
+    const long long tp_t1 = clock64();           \
+    tp_acc[slot] += (unsigned long long)(tp_t1 - tp_t0); \
+    tp_t0 = tp_t1;                               \
   } while (0)
-#define TP_COUNT(slot, v) \
-  do { if (lane == 0 && blockIdx.x < 4096) g_lc_ts[0][(blockIdx.x * 8 + warp) * 8 + (slot)] += (v); } while (0)
+#define TP_COUNT(slot, v) (tp_acc[slot] += (v))
+#define TP_FLUSH                                                                          \
+  do {                                                                                    \
+    if (lane == 0 && blockIdx.x < 4096)                                                   \
+      for (int q = 0; q < 6; ++q) g_lc_ts[0][(blockIdx.x * 8 + warp) * 8 + q] += tp_acc[q]; \
+  } while (0)
 #else
 #define TP_DECL
 #define TP_MARK(slot) ((void)0)
 #define TP_COUNT(slot, v) ((void)0)
+#define TP_FLUSH ((void)0)
 #endif
 
 // Step 6 of one leaf for s = 32, row tiles RLO < RHI, everything unrolled at compile time:
@@ -1496,6 +1502,7 @@ __global__ void __launch_bounds__(kTileThreads, 2) lc_tile_kernel(const __grid_c
     for (int U = nls - 1; U >= -1; --U) {
       if (U >= 2) stage(tile, U - 2);
       cp_async_commit();
+      TP_MARK(5);
       const int V1 = U + 1;  // the leaf whose step 5 / step 2 run in this step
       if (warp < 4) {
         if (U >= 0 && 8 * ((warp >> 1) ? 1 : 0) < s) {
@@ -1778,6 +1785,7 @@ __global__ void __launch_bounds__(kTileThreads, 2) lc_tile_kernel(const __grid_c
       TP_MARK(3);
       TP_COUNT(4, 1);
     }
+    TP_FLUSH;
     cp_async_wait<0>();
     __syncthreads();
   }

@@ -32,5 +32,5 @@ steps = a[:, :, 4].sum(axis=0)
 print(f"n={n} batch={V} grid={grid}; cycles per leaf step, mean over CTAs")
 for w in range(8):
     st = max(steps[w], 1)
-    print(f"warp {w}: role-a {a[:, w, 0].sum() / st:7.0f}  role-b {a[:, w, 1].sum() / st:7.0f}  "
+    print(f"warp {w}: stage {a[:, w, 5].sum() / st:6.0f}  role-a {a[:, w, 0].sum() / st:7.0f}  role-b {a[:, w, 1].sum() / st:7.0f}  "
           f"m2l {a[:, w, 2].sum() / st:7.0f}  end {a[:, w, 3].sum() / st:7.0f}")
