@@ -76,7 +76,7 @@ typedef struct {
   int32_t up_subtree; /* subtree depth of the upward (leaf projection + M2M) kernel; 0 -> automatic */
   int32_t engine;   /* 0 -> automatic; 1 -> level-pipelined kernels (up / streaming / down);
                        2 -> per-tile streaming kernel (one CTA per 8-vector tile, whole Alg. 4 on chip;
-                       needs L >= 1 and s <= 32; automatic choice when there are >= 2 tiles per SM) */
+                       needs L >= 1 and s <= 32; automatic choice from about one tile per SM, or a third of that for n <= 2048) */
 } lc_plan_opts;
 
 /* Geometry and algorithmic work of a plan (per vector unless stated). */

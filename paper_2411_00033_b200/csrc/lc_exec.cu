@@ -1962,7 +1962,12 @@ lc_status configure_kernels(lc_plan* p) {
     const int64_t tsm = L >= 1 ? tile_smem_doubles(L, s) * 8 : 0;
     const bool tile_ok = L >= 1 && s <= 32 && tsm <= smax;
     if (p->engine == 2 && !tile_ok) return LC_ERR_INVALID_ARG;
-    if (p->engine == 0) p->engine = (tile_ok && ntiles8 >= 2 * int64_t(p->sm_count)) ? 2 : 1;
+    // automatic choice (tools/engine_cross.py on the B200): the per-tile pass wins once there is
+    // about one 8-vector tile per SM (e.g. n = 4096: 256 tiles 181 vs 355 us), and earlier for short
+    // vectors (n = 1024: 64 tiles 32 vs 58 us); below that the level-pipelined kernels win
+    if (p->engine == 0)
+      p->engine = (tile_ok && (ntiles8 >= int64_t(p->sm_count) || (p->n <= 2048 && 3 * ntiles8 >= int64_t(p->sm_count))))
+                      ? 2 : 1;
     if (p->engine == 2) {
       int occ = 0;
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, p->dir == 0 ? lc_tile_kernel<0> : lc_tile_kernel<1>,
