@@ -337,8 +337,13 @@ def run_gpu(args, world, rank, local):
         h2d, d2h = 2 * bytes_vec, 2 * bytes_vec
 
     cpu = None
+    cfmm = None
     if rank == 0 and not args.no_cpu_baseline:
         cpu = cpu_baseline(args.config, n, kind, budget_s=args.cpu_seconds)
+        try:
+            cfmm = cpu_fmm_baseline(n, kind, dev, budget_s=args.cpu_seconds)
+        except Exception as e:  # reported baseline only: never fail the GPU line for it
+            cfmm = {"unavailable": f"{type(e).__name__}: {e}"}
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -370,6 +375,7 @@ def run_gpu(args, world, rank, local):
         "clocks": clk,
         "round_trip_einf": {"device": rt, "host_path": rt_host},
         "cpu_baseline": cpu,
+        "cpu_fmm_baseline": cfmm,
     }
     return line
 
@@ -422,6 +428,28 @@ def cpu_baseline(config, n, kind, budget_s=15.0):
             "sample": f"{r2} uniformly sampled output rows (seed 1) of leg2cheb and of cheb2leg of vector 0 at n={n}; "
                       f"long-double compensated O(n) per row, OpenMP over rows; {dt:.1f} s",
             "seconds": dt, "full_transform_extrapolated_s": dt / done * 2 * n}
+
+
+def cpu_fmm_baseline(n, kind, dev, budget_s=10.0):
+    """The same O(N) algorithm on the host cores (cpu_fmm/, C + OpenMP, plan tables exported from the
+    GPU plans): leg2cheb then cheb2leg of vector 0, repeated within the time budget (at least once)."""
+    import cpu_fmm
+    from lc_inputs import vector
+    from paper_2411_00033_b200 import Plan
+    a = cpu_fmm.CpuFmm(Plan(n, "leg2cheb", device=dev))
+    b = cpu_fmm.CpuFmm(Plan(n, "cheb2leg", device=dev))
+    f = vector(kind, n, seed=0, v=0)
+    reps, t0 = 0, time.perf_counter()
+    while True:
+        b(a(f))
+        reps += 1
+        dt = time.perf_counter() - t0
+        if dt > budget_s / 2 or reps >= 50:
+            break
+    return {"value": 2 * n * reps / dt, "unit": UNIT, "cores": cpu_fmm.threads(),
+            "kind": "cpu O(N) FMM: the same algorithm in C + OpenMP (plan tables from the GPU plan)",
+            "sample": f"{reps} round trip(s) (leg2cheb then cheb2leg) of vector 0 at n={n}; {dt:.2f} s",
+            "seconds": dt}
 
 
 def run_reference(args, world, rank):
