@@ -1344,11 +1344,14 @@ constexpr int kTileThreads = 256;
 constexpr int kTileV = 8;                  // vectors per tile (= DMMA n)
 constexpr int kTS = kTileV * kM;           // doubles per (segment, sigma) state
 __host__ __device__ inline int tile_fst(int s) { int f = 4; while (f < s) f += 16; return f; }
+#ifndef LC_FRING
+#define LC_FRING 3  // leaf slots of the f / lambda ring (3: prefetch one leaf ahead; 4: two)
+#endif
 // T [2][32][M] | B(0) [M][M]+4 | tabA [80] | f ring [4][2][8][fst] | lambda ring [4][4s] |
 // w ring [L][3][2][8][M] | c: levels < L-1 [2][2][8][M], level L-1 [3][2][8][M] | z [2][8][2s+4]
 __host__ __device__ inline int64_t tile_smem_doubles(int L, int s) {
   const int fst = tile_fst(s);
-  return 2 * 32 * kM + (kMM + 4) + 80 + 4 * 2 * kTileV * fst + 4 * 4 * s + int64_t(L) * 3 * 2 * kTS +
+  return 2 * 32 * kM + (kMM + 4) + 80 + LC_FRING * 2 * kTileV * fst + LC_FRING * 4 * s + int64_t(L) * 3 * 2 * kTS +
          int64_t(2 * L + 1) * 2 * kTS + 2 * kTileV * (2 * s + 4);
 }
 
@@ -1427,13 +1430,13 @@ __global__ void __launch_bounds__(kTileThreads, 2) lc_tile_kernel(const __grid_c
   double* Tq = reinterpret_cast<double*>(smem);  // [2][32][M]
   double* Bq = Tq + 2 * 32 * kM;                  // B(0) [M][M]
   double* taq = Bq + kMM + 4;                     // tabA [80]
-  double* fr = taq + 80;                          // [4][2][8][fst]
-  double* lmr = fr + 4 * 2 * kTileV * fst;        // [4][4s]
-  double* wr = lmr + 4 * 4 * s;                   // [L][3][2][8][M]
+  double* fr = taq + 80;                          // [LC_FRING][2][8][fst]
+  double* lmr = fr + LC_FRING * 2 * kTileV * fst; // [LC_FRING][4s]
+  double* wr = lmr + LC_FRING * 4 * s;            // [L][3][2][8][M]
   double* cs = wr + L * 3 * 2 * kTS;              // [L-1][2][2][8][M] then [3][2][8][M]
   double* zs = cs + (2 * L + 1) * 2 * kTS;        // [2][8][2s+4]
-  auto fslot = [&](int U) { return fr + (U & 3) * 2 * kTileV * fst; };
-  auto lslot = [&](int U) { return lmr + (U & 3) * 4 * s; };
+  auto fslot = [&](int U) { return fr + ((U + LC_FRING) % LC_FRING) * 2 * kTileV * fst; };  // U >= -1
+  auto lslot = [&](int U) { return lmr + ((U + LC_FRING) % LC_FRING) * 4 * s; };
   auto wslot = [&](int g, int t) { return wr + (g * 3 + t % 3) * 2 * kTS; };
   auto cslot = [&](int g, int u) {
     return g == L - 1 ? cs + (2 * (L - 1) + u % 3) * 2 * kTS : cs + (g * 2 + (u & 1)) * 2 * kTS;
@@ -1444,7 +1447,7 @@ __global__ void __launch_bounds__(kTileThreads, 2) lc_tile_kernel(const __grid_c
   for (int i = tid; i < kMM / 2; i += kTileThreads) cp_async16(Bq + 2 * i, P.B + 2 * i);
   for (int i = tid; i < 80; i += kTileThreads) taq[i] = i < seglen ? P.tabA[i] : 0.0;
   // rows m in [s, fst) of every f slot stay zero (read by the K = 4 ceil(s/4) steps of step 1)
-  for (int i = tid; i < 4 * 2 * kTileV * fst; i += kTileThreads) fr[i] = 0.0;
+  for (int i = tid; i < LC_FRING * 2 * kTileV * fst; i += kTileThreads) fr[i] = 0.0;
   cp_async_commit();
   __syncthreads();  // the zero fill precedes every cp.async into the ring (other threads' elements)
   griddep_wait();  // the input may be produced by the preceding kernel
@@ -1493,14 +1496,15 @@ __global__ void __launch_bounds__(kTileThreads, 2) lc_tile_kernel(const __grid_c
     }
     stage(tile, nls - 1);
     cp_async_commit();
-    stage(tile, nls - 2);
+    if (LC_FRING == 4) stage(tile, nls - 2);
     cp_async_commit();
     cp_async_wait<1>();
     __syncthreads();
 
     TP_DECL
     for (int U = nls - 1; U >= -1; --U) {
-      if (U >= 2) stage(tile, U - 2);
+      // prefetch distance: two leaves with a ring of 4, one leaf (a whole step to land) with 3
+      if (LC_FRING == 4 ? U >= 2 : U >= 1) stage(tile, LC_FRING == 4 ? U - 2 : U - 1);
       cp_async_commit();
       TP_MARK(5);
       const int V1 = U + 1;  // the leaf whose step 5 / step 2 run in this step
@@ -1780,7 +1784,7 @@ __global__ void __launch_bounds__(kTileThreads, 2) lc_tile_kernel(const __grid_c
         }
       }
       TP_MARK(2);
-      cp_async_wait<1>();  // f(U-1) landed
+      if (LC_FRING == 4) cp_async_wait<1>(); else cp_async_wait<0>();  // f(U-1) landed
       __syncthreads();
       TP_MARK(3);
       TP_COUNT(4, 1);
