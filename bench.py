@@ -263,8 +263,12 @@ def run_gpu(args, world, rank, local):
                 per_kernel[d][i] += ev[i].elapsed_time(ev[i + 1]) / ksteps
     hbm, hbm_src = peaks()
     dl = pl.desc
-    names = ["lc_tile_kernel"] if kpe == 1 else (["lc_up_kernel"] if kpe == 3 else []) + ["lc_stream_kernel",
-                                                                                         "lc_down_kernel"]
+    engine = pl.kernel_info.get("engine", 1)
+    if engine == 3:
+        names = ["lc_up_kernel", "lc_range_kernel"]
+    else:
+        names = ["lc_tile_kernel"] if kpe == 1 else (["lc_up_kernel"] if kpe == 3 else []) + ["lc_stream_kernel",
+                                                                                             "lc_down_kernel"]
     # algorithmic bytes per launch (f in, z out, A_hat once, lambda once; work arrays excluded):
     # the up kernel reads f, the streaming kernel reads A_hat and lambda (and f again for the band),
     # the down kernel writes z
@@ -274,13 +278,14 @@ def run_gpu(args, world, rank, local):
         alg["lc_stream_kernel"] += 8.0 * n * V
     # the per-tile kernel (engine 2) is the whole transform: f in, z out, A_hat and lambda once
     alg["lc_tile_kernel"] = 16.0 * n * V + 8.0 * 324 * dl["nc"] + 8.0 * dl["N"]
+    alg["lc_range_kernel"] = 8.0 * n * V + 8.0 * 324 * dl["nc"] + 8.0 * dl["N"]  # f in (band), z out, A_hat, lambda
     avg_ms = {nm: 0.5 * (per_kernel[0][i] + per_kernel[1][i]) for i, nm in enumerate(names)}
-    dom = "lc_tile_kernel" if kpe == 1 else "lc_stream_kernel"  # the A_hat stream: the HBM-dominant kernel
+    dom = "lc_tile_kernel" if kpe == 1 else ("lc_range_kernel" if engine == 3 else "lc_stream_kernel")
     down_ms = avg_ms[dom]
     down_bytes = alg[dom]
     achieved = down_bytes / (down_ms * 1e-3) / 1e9
     traffic = load_traffic(args.config, dom)
-    if kpe == 1:
+    if kpe == 1 or engine == 3:
         # fp64 tensor-core bound: algorithmic flops of one transform over the kernel time, against the
         # measured DMMA peak (the higher of the two fp64 peaks, so the fraction is conservative)
         tf = dl["flops_alg"] * V / (down_ms * 1e-3) / 1e12
@@ -496,7 +501,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg2", choices=["cfg1", "cfg2", "cfg2b", "cfg3", "cfg4", "cfg5"])
     ap.add_argument("--vt", type=int, default=0)
-    ap.add_argument("--engine", type=int, default=0, help="0 automatic, 1 level-pipelined kernels, 2 per-tile kernel")
+    ap.add_argument("--engine", type=int, default=0,
+                    help="0 automatic, 1 level-pipelined kernels, 2 per-tile kernel, 3 up kernel + per-range pass")
     ap.add_argument("--subtree", type=int, default=0)
     ap.add_argument("--stage-blocks", type=int, default=0)
     ap.add_argument("--stages", type=int, default=0)

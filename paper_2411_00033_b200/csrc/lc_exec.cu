@@ -1355,6 +1355,13 @@ __host__ __device__ inline int64_t tile_smem_doubles(int L, int s) {
          int64_t(2 * L + 1) * 2 * kTS + 2 * kTileV * (2 * s + 4);
 }
 
+__host__ __device__ inline int64_t range_smem_doubles(int s) {
+  const int fst = tile_fst(s);
+  return 2 * 32 * kM + (kMM + 4) + 80 + LC_FRING * 2 * kTileV * fst + LC_FRING * 4 * s + int64_t(5) * 2 * kTS +
+         2 * kTileV * (2 * s + 4);
+}
+__host__ __device__ inline int64_t range_scratch_doubles(int L) { return int64_t(L >= 2 ? L - 2 : 0) * 2 * 2 * kTS; }
+
 struct TileParams {
   const double* in;
   double* out;
@@ -1363,8 +1370,12 @@ struct TileParams {
   const double* tabB;  // N
   const double* Tpad;  // [2][32][M]
   const double* B;     // B(0)
+  const double* wg;    // engine 3: w of every level (up kernel output), tile stride w_tile
+  double* scratch;     // engine 3: per-CTA c slots of the levels below L-2
+  int64_t w_tile;
   int64_t ld_in, ld_out, n, N, batch, ntiles;
   int layout, L, s;
+  int nranges, rlen;   // engine 3: leaf ranges per tile and their length
 };
 
 // debug build: per (CTA, warp) cycle accounting of the tile kernel in g_lc_ts[0]:
@@ -1795,6 +1806,315 @@ __global__ void __launch_bounds__(kTileThreads, 2) lc_tile_kernel(const __grid_c
   }
 }
 
+// Engine 3 (batches of long vectors, few tiles): the up kernel writes w of every level, then this
+// kernel runs the per-tile right-to-left pass over a RANGE of leaves of a tile (ranges x tiles fill
+// the GPU): steps 3-7 exactly as in lc_tile_kernel, with w read from the workspace, the step-4 chain
+// started at the range's rightmost leaf from the top level down, and the c of the levels below L-2 in
+// a per-CTA global scratch (the footprint does not grow with L).
+template <int DIR>
+__global__ void __launch_bounds__(kTileThreads, 2) lc_range_kernel(const __grid_constant__ TileParams P) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int lr = lane >> 2, lc = lane & 3;
+  const int s = P.s, L = P.L, seglen = 2 * s;
+  const int fst = tile_fst(s), zst_ = 2 * s + 4;
+  const int nls = 2 << L;  // leaf segments
+  double* Tq = reinterpret_cast<double*>(smem);  // [2][32][M]
+  double* Bq = Tq + 2 * 32 * kM;                  // B(0) [M][M]
+  double* taq = Bq + kMM + 4;                     // tabA [80]
+  double* fr = taq + 80;                          // [LC_FRING][2][8][fst]
+  double* lmr = fr + LC_FRING * 2 * kTileV * fst; // [LC_FRING][4s]
+  double* cs = lmr + LC_FRING * 4 * s;            // leaf level [3], level L-2 [2] x [2][8][M]
+  double* zs = cs + 5 * 2 * kTS;                  // [2][8][2s+4]
+  double* gc = P.scratch + int64_t(blockIdx.x) * range_scratch_doubles(L);  // levels < L-2: [L-2][2][2][8][M]
+  auto fslot = [&](int U) { return fr + ((U + LC_FRING) % LC_FRING) * 2 * kTileV * fst; };  // U >= -1
+  auto lslot = [&](int U) { return lmr + ((U + LC_FRING) % LC_FRING) * 4 * s; };
+  // w of every level comes from the up kernel (global workspace, read-only here)
+  auto wglob = [&](int64_t tile, int g, int t, int sg) {
+    return P.wg + tile * P.w_tile + (w_level_offset_units(g) + sg * nseg(g) + t) * kTS;
+  };
+  auto cslot = [&](int g, int u) {
+    return g == L - 1 ? cs + (u % 3) * 2 * kTS
+                      : (g == L - 2 ? cs + (3 + (u & 1)) * 2 * kTS : gc + (g * 2 + (u & 1)) * 2 * kTS);
+  };
+  auto zbuf = [&](int U) { return zs + (U & 1) * kTileV * zst_; };
+
+  for (int i = tid; i < 2 * 32 * kM / 2; i += kTileThreads) cp_async16(Tq + 2 * i, P.Tpad + 2 * i);
+  for (int i = tid; i < kMM / 2; i += kTileThreads) cp_async16(Bq + 2 * i, P.B + 2 * i);
+  for (int i = tid; i < 80; i += kTileThreads) taq[i] = i < seglen ? P.tabA[i] : 0.0;
+  // rows m in [s, fst) of every f slot stay zero (read by the K = 4 ceil(s/4) steps of step 1)
+  for (int i = tid; i < LC_FRING * 2 * kTileV * fst; i += kTileThreads) fr[i] = 0.0;
+  cp_async_commit();
+  __syncthreads();  // the zero fill precedes every cp.async into the ring (other threads' elements)
+  griddep_wait();  // the input may be produced by the preceding kernel
+  griddep_launch();
+
+  // stage leaf segment U of the tile: f de-interleaved by parity ([sigma][v][m]), and the lambda
+  // (tabB) window [2sU, 2sU + 4s) that the band of rows U reads; zero beyond n / N
+  auto stage = [&](int64_t tile, int U) {
+    double* fd = fslot(U);
+    const int64_t j0 = int64_t(U) * seglen;
+    if (P.layout == LC_VEC_CONTIGUOUS) {  // warp = vector, lanes along the segment
+      const int64_t gv = tile * kTileV + warp;
+      const double* src = P.in + gv * P.ld_in + j0;
+      const int64_t lim = gv < P.batch ? P.n - j0 : 0;
+      for (int x = lane; x < seglen; x += 32) {
+        const bool ok = x < lim;
+        cp_async8(fd + ((x & 1) * kTileV + warp) * fst + (x >> 1), ok ? src + x : P.in, ok ? 8u : 0u);
+      }
+    } else {  // vectors fastest
+      for (int idx = tid; idx < kTileV * seglen; idx += kTileThreads) {
+        const int x = idx >> 3, v = idx & 7;
+        const int64_t gv = tile * kTileV + v, j = j0 + x;
+        const bool ok = gv < P.batch && j < P.n;
+        cp_async8(fd + ((x & 1) * kTileV + v) * fst + (x >> 1), ok ? P.in + j * P.ld_in + gv : P.in, ok ? 8u : 0u);
+      }
+    }
+    double* ld = lslot(U);
+    for (int x = tid; x < 2 * seglen; x += kTileThreads) {
+      const bool ok = j0 + x < P.N;
+      cp_async8(ld + x, ok ? P.tabB + j0 + x : P.tabB, ok ? 8u : 0u);
+    }
+  };
+  // first level entered at leaf U (U is the rightmost leaf of its segments on levels >= gmin)
+  auto gmin_of = [&](int U) {
+    const int ones = __ffs(~U) - 1;  // trailing one bits
+    const int g = L - 1 - ones;
+    return g < 0 ? 0 : g;
+  };
+  const double inv_pi = 0.318309886183790671537767526745028724;
+
+  const int64_t nunits = P.ntiles * P.nranges;
+  for (int64_t unit = blockIdx.x; unit < nunits; unit += gridDim.x) {
+    const int64_t tile = unit / P.nranges;
+    const int Ua = int(unit - tile * P.nranges) * P.rlen;
+    const int Ub = min(nls, Ua + P.rlen) - 1;
+    // entering the range at its rightmost leaf Ub enters every level; the "step" Ub+1 only computes
+    // the M2L of Ub's rows on all levels (and stages f(Ub+1), zero past the end)
+    auto gentry = [&](int U) { return U == Ub ? 0 : gmin_of(U); };
+    stage(tile, Ub + 1);
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncthreads();
+
+    TP_DECL
+    for (int U = Ub + 1; U >= Ua - 1; --U) {
+      if (U - 1 >= Ua) stage(tile, U - 1);  // one leaf ahead (a whole step to land)
+      cp_async_commit();
+      TP_MARK(5);
+      const int V1 = U + 1;  // the leaf whose step 5 runs in this step
+      const bool inU = U >= Ua && U <= Ub;
+      if (warp < 4) {
+        if (inU && 8 * ((warp >> 1) ? 1 : 0) < s) {
+          // ---- step 6: rows i = 2sU + 2r + sigma, columns j = 2sU + 2c + sigma (c >= r, j < j_end),
+          // K[r][c] = a[c-r] b[(i+j)/2] formed per lane, G[c][v] = f_v[j] (C2L: j f_j); row tiles
+          // {0,3} or {1,2} per warp (two accumulator chains)
+          const int sg = warp & 1;
+          const int rlo = (warp >> 1) ? 1 : 0, rhi = (warp >> 1) ? 2 : 3;
+          const bool hion = 8 * rhi < s;
+          const double* fU = fslot(U) + (sg * kTileV + lr) * fst;
+          const double* fU1 = fslot(U + 1) + (sg * kTileV + lr) * fst;
+          const double* lw = lslot(U);
+          const int64_t i0 = int64_t(U) * seglen;
+          double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+          if (s == 32) {
+            const double* fa = fU + lc;
+            const double* fb = fU1 + lc;
+            const double* lamw = lw + sg + lr + lc;
+            const double* tap = taq + lc - lr;
+            if (rlo == 0)
+              band32<DIR, 0, 3>(fa, fb, lamw, tap, i0, sg, lc, lr, acc);
+            else
+              band32<DIR, 1, 2>(fa, fb, lamw, tap, i0, sg, lc, lr, acc);
+          } else if ((s & 7) == 0) {  // fast path: row tiles full, chunk boundary = segment boundary
+            const double* lamw = lw + sg + lr + lc;  // lambda[(i+j)/2 - 2sU] = lamw[8 rb + 4 kc]
+            const double* tap = taq + lc - lr;       // a[c - r] = tap[4 kc - 8 rb]
+            const int nkc = seglen >> 2, s4 = s >> 2;
+            for (int kc = 2 * rlo; kc < nkc; ++kc) {
+              const int c = 4 * kc + lc;
+              double b = kc < s4 ? fU[c] : fU1[c - s];
+              if (DIR == 1) b *= double(i0 + 2 * c + sg);
+              {
+                const int d = 4 * kc - 8 * rlo;
+                double a = tap[d] * lamw[8 * rlo + 4 * kc];
+                if (d < 8 && lc + d < lr) a = 0.0;  // c < r inside the diagonal block
+                dmma(acc[0], a, b);
+              }
+              if (hion && kc >= 2 * rhi) {
+                const int d = 4 * kc - 8 * rhi;
+                double a = tap[d] * lamw[8 * rhi + 4 * kc];
+                if (d < 8 && lc + d < lr) a = 0.0;
+                dmma(acc[1], a, b);
+              }
+            }
+          } else {  // general s: masks on rows, columns and the segment boundary
+            const int nkc = (seglen + 3) >> 2;
+            for (int kc = 2 * rlo; kc < nkc; ++kc) {
+              const int c = 4 * kc + lc;
+              double b = c < s ? fU[c] : (c < seglen ? fU1[c - s] : 0.0);
+              if (DIR == 1) b *= double(i0 + 2 * c + sg);
+#pragma unroll
+              for (int q = 0; q < 2; ++q) {
+                const int rb = q ? rhi : rlo;
+                if (8 * rb < s && kc >= 2 * rb) {
+                  const int r = 8 * rb + lr;
+                  const double lam = lw[r + c + sg];
+                  const double a = (c >= r && c < seglen && r < s) ? taq[c >= r ? c - r : 0] * lam : 0.0;
+                  dmma(acc[q], a, b);
+                }
+              }
+            }
+          }
+          double* zb = zbuf(U);
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            const int r = 8 * (q ? rhi : rlo) + lr;
+            if (r < s) {
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                const int v = 2 * lc + h;
+                double z = acc[q][h];
+                if (DIR == 1) {
+                  const int64_t ir = i0 + 2 * r + sg;
+                  z *= double(2 * ir + 1);
+                  if (ir == 0) z += fslot(U)[v * fst];  // entry (0,0) of A^{-1}C is 1 (R2)
+                }
+                zb[v * zst_ + 2 * r + sg] = z;
+              }
+            }
+          }
+        }
+        TP_MARK(0);
+        if (V1 >= Ua && V1 <= Ub && 16 * (warp >> 1) < s) {
+          // ---- step 5 of leaf V1: z[v][2m + sigma] += sum_k T(sigma)[m][k] c(L-1, V1)[sigma][v][k],
+          // row tiles {2h, 2h+1}; then C^{-1} (step 7) and the store of those rows
+          const int sg = warp & 1, mt0 = 2 * (warp >> 1);
+          const double* cc = cslot(L - 1, V1) + sg * kTS;
+          double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+          for (int kk = 0; kk < 5; ++kk) {
+            const int k = 4 * kk + lc;
+            const double bb = k < kM ? cc[lr * kM + k] : 0.0;
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+              const int m = 8 * (mt0 + q) + lr;
+              const double a = k < kM ? Tq[(sg * 32 + m) * kM + k] : 0.0;
+              dmma(acc[q], a, bb);
+            }
+          }
+          const double* zb = zbuf(V1);
+          const int64_t i0 = int64_t(V1) * seglen;
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            const int m = 8 * (mt0 + q) + lr;
+            if (m < s) {
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                const int v = 2 * lc + h;
+                const int64_t gv = tile * kTileV + v, i = i0 + 2 * m + sg;
+                double z = zb[v * zst_ + 2 * m + sg] + acc[q][h];
+                if (DIR == 0) z *= (i == 0 ? inv_pi : 2.0 * inv_pi);
+                if (gv < P.batch && i < P.n) {
+                  if (P.layout == LC_VEC_CONTIGUOUS) P.out[gv * P.ld_out + i] = z;
+                  else P.out[i * P.ld_out + gv] = z;
+                }
+              }
+            }
+          }
+        }
+      } else {
+        const int sg = warp & 1;
+        if (warp >= 6 && inU) {
+          // ---- step 4 chain (sigma) over the levels entered at U, coarse to fine
+          const int gA = gentry(U);
+          for (int g = (gA > 0 ? gA : 1); g < L; ++g) {
+            const int u = U >> (L - 1 - g);
+            const int p = u & 1;
+            const double* par = cslot(g - 1, u >> 1) + sg * kTS;
+            double* dst = cslot(g, u) + sg * kTS;
+            double acc[3][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+            for (int kk = 0; kk < 5; ++kk) {
+              const int nn = 4 * kk + lc;
+              const double bb = nn < kM ? par[lr * kM + nn] : 0.0;
+#pragma unroll
+              for (int mt = 0; mt < 3; ++mt) {
+                if (4 * kk + 3 < 8 * mt) continue;  // n < k everywhere
+                const int k = 8 * mt + lr;
+                double a = (k < kM && nn < kM) ? Bq[nn * kM + k] : 0.0;  // b_{n k}
+                if (p && ((k + nn) & 1)) a = -a;
+                dmma(acc[mt], a, bb);
+              }
+            }
+#pragma unroll
+            for (int mt = 0; mt < 3; ++mt) {
+              const int k = 8 * mt + lr;
+              if (k < kM) {
+                dst[(2 * lc) * kM + k] += acc[mt][0];
+                dst[(2 * lc + 1) * kM + k] += acc[mt][1];
+              }
+            }
+            __syncwarp();
+          }
+        }
+        TP_MARK(1);
+        // ---- step 3 for the rows the next leaf enters: job k = (level gN + k/2, sigma k&1) on warp
+        // 4, 5, 6, 7, 4, ...: c(u') = sum_r A_hat_r w(t_r), w from the up kernel's output
+        if (U - 1 >= Ua) {
+          const int gN = gentry(U - 1);
+          const int nm2l = (L - gN) * 2;
+          for (int k = warp - 4; k < nm2l; k += 4) {
+            const int g = gN + (k >> 1), sgk = k & 1;
+            const int u = (U - 1) >> (L - 1 - g);
+            double acc[3][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+            if (u < (4 << g) - 2) {
+              const int b = u >> 1, p = u & 1;
+              for (int mi = 0; mi < (p ? 1 : 2); ++mi) {
+                const int r = p ? 2 : mi;
+                const int t = u + 2 + (p ? 0 : mi);
+                const double* Am = P.A + (ahat_level_offset(g) + 3 * int64_t(b) + r) * kMM;
+                const double* W = wglob(tile, g, t, sgk);
+                double av[3][5];
+#pragma unroll
+                for (int mt = 0; mt < 3; ++mt)
+#pragma unroll
+                  for (int kk = 0; kk < 5; ++kk) {
+                    const int kx = 4 * kk + lc, mode = 8 * mt + lr;
+                    av[mt][kk] = (mode < kM && kx < kM) ? __ldg(Am + mode * kM + kx) : 0.0;
+                  }
+#pragma unroll
+                for (int kk = 0; kk < 5; ++kk) {
+                  const int kx = 4 * kk + lc;
+                  const double bb = kx < kM ? __ldg(W + lr * kM + kx) : 0.0;
+#pragma unroll
+                  for (int mt = 0; mt < 3; ++mt) dmma(acc[mt], av[mt][kk], bb);
+                }
+              }
+            }
+            double* dst = cslot(g, u) + sgk * kTS;
+#pragma unroll
+            for (int mt = 0; mt < 3; ++mt) {
+              const int mode = 8 * mt + lr;
+              if (mode < kM) {
+                dst[(2 * lc) * kM + mode] = acc[mt][0];
+                dst[(2 * lc + 1) * kM + mode] = acc[mt][1];
+              }
+            }
+          }
+        }
+      }
+      TP_MARK(2);
+      if (LC_FRING == 4) cp_async_wait<1>(); else cp_async_wait<0>();  // f(U-1) landed
+      __syncthreads();
+      TP_MARK(3);
+      TP_COUNT(4, 1);
+    }
+    TP_FLUSH;
+    cp_async_wait<0>();
+    __syncthreads();
+  }
+}
+
 // ============================================================== host side
 
 template <typename K>
@@ -1857,6 +2177,8 @@ lc_status configure_kernels(lc_plan* p) {
     if (ea == cudaSuccess) ea = set_attrs_all<64>(smax);
     if (ea == cudaSuccess) ea = set_max_dyn_smem(lc_tile_kernel<0>, smax);
     if (ea == cudaSuccess) ea = set_max_dyn_smem(lc_tile_kernel<1>, smax);
+    if (ea == cudaSuccess) ea = set_max_dyn_smem(lc_range_kernel<0>, smax);
+    if (ea == cudaSuccess) ea = set_max_dyn_smem(lc_range_kernel<1>, smax);
     if (ea == cudaSuccess) {
       double B[kMM];
       ea = cudaMemcpy(B, p->d_B, sizeof(B), cudaMemcpyDeviceToHost);
@@ -1872,6 +2194,10 @@ lc_status configure_kernels(lc_plan* p) {
 
   const int64_t budget2 = 113 * 1024;  // two CTAs per SM (228 KB minus 1 KB reserved per CTA)
   int vt = p->vt;
+  if (p->engine == 3) {  // up kernel of 8-vector tiles feeding the per-range pass
+    if (L < 1 || p->s > 32) return LC_ERR_INVALID_ARG;
+    vt = 8;
+  }
   if (vt <= 0) vt = p->batch >= 2 ? 2 : 1;
   if (vt != 1 && vt != 2 && vt != 4 && vt != 8) return LC_ERR_INVALID_ARG;
   const int64_t nleaf_total = L > 0 ? (int64_t(2) << L) : 2;  // leaf segments (L = 0: the two halves)
@@ -1966,6 +2292,26 @@ lc_status configure_kernels(lc_plan* p) {
     const int64_t tsm = L >= 1 ? tile_smem_doubles(L, s) * 8 : 0;
     const bool tile_ok = L >= 1 && s <= 32 && tsm <= smax;
     if (p->engine == 2 && !tile_ok) return LC_ERR_INVALID_ARG;
+    if (p->engine == 3) {
+      int occ = 0;
+      const size_t rsm = size_t(range_smem_doubles(s) * 8);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, p->dir == 0 ? lc_range_kernel<0> : lc_range_kernel<1>,
+                                                    kTileThreads, rsm);
+      if (occ < 1) return LC_ERR_INVALID_ARG;
+      const int64_t slots = int64_t(occ) * p->sm_count;
+      const int64_t nls = int64_t(2) << L;
+      int64_t nr = std::max<int64_t>(1, (slots + p->ntiles - 1) / p->ntiles);
+      nr = std::min(nr, nls);
+      const int64_t rlen = (nls + nr - 1) / nr;
+      nr = (nls + rlen - 1) / rlen;
+      p->range_n = int(nr);
+      p->range_len = int(rlen);
+      p->smem_tile = rsm;
+      p->tile_grid = int(std::min<int64_t>(p->ntiles * nr, slots));
+      p->ws_range_off = align_up(int64_t(p->ws_bytes), 256);
+      p->ws_bytes = size_t(p->ws_range_off + int64_t(p->tile_grid) * range_scratch_doubles(L) * 8 + 256);
+      return LC_OK;
+    }
     // automatic choice (tools/engine_cross.py on the B200): the per-tile pass wins once there is
     // about one 8-vector tile per SM (e.g. n = 4096: 256 tiles 181 vs 355 us), and earlier for short
     // vectors (n = 1024: 64 tiles 32 vs 58 us); below that the level-pipelined kernels win
@@ -2120,6 +2466,42 @@ lc_status launch_execute(const lc_plan* p, const double* in, double* out, void* 
   }
   const dim3 grid_up(unsigned(nsub), unsigned(p->ntiles));
   const dim3 grid_down(unsigned(ndown), unsigned(p->ntiles));
+  if (p->engine == 3) {
+    TileParams tp{};
+    tp.in = in; tp.out = out; tp.A = p->d_A; tp.tabA = p->d_tabA; tp.tabB = p->d_tabB; tp.Tpad = p->d_Tpad;
+    tp.B = p->d_B; tp.ld_in = p->ld_in; tp.ld_out = p->ld_out; tp.n = p->n; tp.N = p->N; tp.batch = p->batch;
+    tp.ntiles = p->ntiles; tp.layout = p->layout; tp.L = int(p->L); tp.s = int(p->s);
+    tp.wg = w; tp.w_tile = p->w_tile_doubles; tp.nranges = p->range_n; tp.rlen = p->range_len;
+    tp.scratch = reinterpret_cast<double*>(reinterpret_cast<char*>(ws) + p->ws_range_off);
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.stream = st;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int evi = 0;
+    if (ev && nev > 0) cudaEventRecord(ev[evi++], st);
+    cfg.gridDim = grid_up;
+    const bool small_up = int64_t(grid_up.x) * grid_up.y > 8 * p->sm_count && p->smem_up <= 56 * 1024;
+    cfg.blockDim = dim3(small_up ? kThreads / 2 : kThreads);
+    cfg.dynamicSmemBytes = p->smem_up;
+    cudaError_t e = cudaSuccess;
+    UpArgs<32> ua;
+    ua.p = up;
+    e = cudaLaunchKernelEx(&cfg, lc_up_kernel<8, 32>, ua);
+    if (e == cudaSuccess && ev && evi < nev) cudaEventRecord(ev[evi++], st);
+    if (e == cudaSuccess) {
+      cfg.gridDim = dim3(unsigned(p->tile_grid));
+      cfg.blockDim = dim3(kTileThreads);
+      cfg.dynamicSmemBytes = p->smem_tile;
+      e = p->dir == 0 ? cudaLaunchKernelEx(&cfg, lc_range_kernel<0>, tp) : cudaLaunchKernelEx(&cfg, lc_range_kernel<1>, tp);
+    }
+    if (e == cudaSuccess && ev && evi < nev) cudaEventRecord(ev[evi++], st);
+    if (e == cudaSuccess) e = cudaGetLastError();
+    if (prev != p->device) cudaSetDevice(prev);
+    return e == cudaSuccess ? LC_OK : record_cuda_error(e);
+  }
   const cudaError_t e = p->smax == 32 ? launch_dispatch<32>(p, up, sp, dp, grid_up, grid_down, st, ev, nev)
                                       : launch_dispatch<64>(p, up, sp, dp, grid_up, grid_down, st, ev, nev);
   if (prev != p->device) cudaSetDevice(prev);
@@ -2133,7 +2515,7 @@ extern "C" lc_status lc_plan_kernel_info(const lc_plan* p, int64_t* out, int32_t
   const int64_t up_grid = p->L > 0 ? (int64_t(4) << p->grup) * p->ntiles : 0;
   const int64_t v[] = {p->stream_grid, int64_t(p->smem_stream), int64_t(p->smem_up), p->kup, p->grup, p->kb,
                        p->bps, p->nst, p->vt, p->stream_occ, p->m2l_units, p->band_units, up_grid, p->k,
-                       int64_t(p->smem_down), p->engine, p->tile_grid, int64_t(p->smem_tile)};
+                       int64_t(p->smem_down), p->engine, p->tile_grid, int64_t(p->smem_tile), p->range_n, p->range_len};
   const int32_t nv = int32_t(sizeof(v) / sizeof(v[0]));
   int32_t i = 0;
   for (; i < nv && i < count; ++i) out[i] = v[i];
@@ -2147,7 +2529,7 @@ extern "C" lc_status lc_execute(const lc_plan* p, const double* in, double* out,
 
 extern "C" lc_status lc_execute_timed(const lc_plan* p, const double* in, double* out, void* ws, void* stream,
                                       void* const* ev, int32_t nev) {
-  if (!p || !ev || nev < (p->engine == 2 ? 2 : (p->L > 0 ? 4 : 3))) return LC_ERR_INVALID_ARG;
+  if (!p || !ev || nev < (p->engine == 2 ? 2 : (p->engine == 3 ? 3 : (p->L > 0 ? 4 : 3)))) return LC_ERR_INVALID_ARG;
   return lc::launch_execute(p, in, out, ws, (cudaStream_t)stream, reinterpret_cast<cudaEvent_t const*>(ev), nev);
 }
 

@@ -126,6 +126,8 @@ struct lc_plan {
   int engine;          // 1 = up / stream / down kernels, 2 = per-tile streaming kernel
   int tile_grid;       // CTAs of the per-tile kernel (engine 2)
   size_t smem_tile;
+  int range_n, range_len;   // engine 3: leaf ranges per tile and their length
+  int64_t ws_range_off;     // engine 3: byte offset of the per-CTA scratch in the workspace
   size_t smem_stream;
   int64_t ntiles;
   int64_t w_tile_doubles, cnt_tile_ints;

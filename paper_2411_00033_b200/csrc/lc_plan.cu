@@ -279,7 +279,7 @@ extern "C" lc_status lc_plan_create(lc_plan** out, int64_t n, lc_direction dir, 
   if (o.s_hat <= 0) o.s_hat = 32;
   if (o.M <= 0) o.M = kM;
   if (o.M != kM || o.s_hat < 2 || o.s_hat > 64) return LC_ERR_INVALID_ARG;
-  if (o.engine < 0 || o.engine > 2) return LC_ERR_INVALID_ARG;
+  if (o.engine < 0 || o.engine > 3) return LC_ERR_INVALID_ARG;
   if (o.layout != LC_VEC_CONTIGUOUS && o.layout != LC_BATCH_CONTIGUOUS) return LC_ERR_INVALID_ARG;
   const int64_t def_ld = o.layout == LC_VEC_CONTIGUOUS ? n : batch;
   if (o.ld_in == 0) o.ld_in = def_ld;
@@ -419,7 +419,7 @@ extern "C" lc_status lc_plan_describe(const lc_plan* p, lc_plan_desc* d) {
   d->plan_bytes = p->plan_bytes; d->workspace_bytes = p->ws_bytes;
   d->flops_alg = p->flops_alg; d->bytes_alg = p->bytes_alg;
   d->vt = p->vt; d->subtree = p->k; d->stage_blocks = p->bps; d->stages = p->nst;
-  d->kernels_per_execute = p->engine == 2 ? 1 : (p->L > 0 ? 3 : 2);
+  d->kernels_per_execute = p->engine == 2 ? 1 : (p->engine == 3 ? 2 : (p->L > 0 ? 3 : 2));
   return LC_OK;
 }
 

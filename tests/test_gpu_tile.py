@@ -124,3 +124,35 @@ def test_tile_engine_back_to_back_and_zero_vectors():
     assert torch.equal(z1a, z1b)
     assert torch.count_nonzero(z2) == 0
     np.testing.assert_array_equal(z1a.cpu().numpy()[3], p.execute(x1).cpu().numpy()[3])
+
+
+# engine 3: up kernel (8-vector tiles) + the per-range pass; ranges split the leaves of each tile
+# (n = 100000 -> L = 10 with 8 levels of c in the global scratch)
+@pytest.mark.parametrize("direction", ["leg2cheb", "cheb2leg"])
+@pytest.mark.parametrize("n,V", [(129, 8), (1000, 9), (4096, 8), (20000, 5), (100000, 16)])
+def test_range_engine_vs_oracle(direction, n, V):
+    dev = _dev()
+    x = batch("normal_exp1000", n, V, seed=12)
+    p = _plan(n, direction, batch=V, device=dev, engine=3)
+    assert p.kernel_info["engine"] == 3 and p.kernels_per_execute == 2
+    z = p.execute(x.to(dev)).cpu().numpy()
+    vs = range(V) if n <= 20000 else (0, V - 1)
+    for v in vs:
+        e = oracle.einf(z[v], oracle.transform_rows(direction, x[v].numpy()))
+        assert e <= GATE, (n, V, v, direction, e, p.desc)
+
+
+def test_range_engine_matches_level_pipeline():
+    dev = _dev()
+    n, V = 100000, 24
+    x = batch("normal_exp1000", n, V, seed=13).to(dev)
+    for direction in ("leg2cheb", "cheb2leg"):
+        p1 = _plan(n, direction, batch=V, device=dev, engine=1)
+        p3 = _plan(n, direction, batch=V, device=dev, engine=3)
+        z1 = torch.full_like(x, float("nan"))
+        z3 = torch.full_like(x, float("nan"))
+        p1.execute(x, out=z1)
+        p3.execute(x, out=z3)
+        torch.cuda.synchronize()
+        e = (z1 - z3).abs().max().item() / z1.abs().max().item()
+        assert e <= 1e-13, (direction, e)
