@@ -288,9 +288,13 @@ def run_gpu(args, world, rank, local):
     if kpe == 1 or engine == 3:
         # fp64 tensor-core bound: algorithmic flops of one transform over the kernel time, against the
         # measured DMMA peak (the higher of the two fp64 peaks, so the fraction is conservative)
-        tf = dl["flops_alg"] * V / (down_ms * 1e-3) / 1e12
+        fk = dl["flops_alg"]
+        if engine == 3:  # the range kernel does steps 3-7: drop step 1 and the M2M half of F_alg
+            Lq, sq, Mq = dl["L"], dl["s"], 18
+            fk -= 8.0 * ((2 ** Lq) - 1) * sq * Mq + 4.0 * (Mq * Mq + 2 * Mq) * ((2 ** Lq) - Lq - 1)
+        tf = fk * V / (down_ms * 1e-3) / 1e12
         roof = {"bound": "tensor", "kernel": dom, "achieved": tf, "peak": DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
-                "frac": tf / DMMA_PEAK_TFLOPS, "traffic": traffic, "algorithmic_flops_per_launch": dl["flops_alg"] * V,
+                "frac": tf / DMMA_PEAK_TFLOPS, "traffic": traffic, "algorithmic_flops_per_launch": fk * V,
                 "algorithmic_bytes_per_launch": down_bytes, "achieved_hbm_gbs": achieved, "avg_launch_ms": down_ms,
                 "peak_source": "measured fp64 DMMA m8n8k4 (profiles/r1_dmma_peak.txt)"}
     else:

@@ -2194,6 +2194,11 @@ lc_status configure_kernels(lc_plan* p) {
 
   const int64_t budget2 = 113 * 1024;  // two CTAs per SM (228 KB minus 1 KB reserved per CTA)
   int vt = p->vt;
+  // automatic engine 3 (tools/engine_cross3.py on the B200): long vectors in batches of 8+ (>= 16 below
+  // n = 2^18), deep enough trees for ranges of >= 64 leaves; e.g. 64 x 10^7: 42.4 -> 30.3 ms
+  if (p->engine == 0 && p->vt <= 0 && L >= 9 && p->s <= 32 && p->batch >= 8 && (p->batch >= 16 || p->n >= 262144) &&
+      ((p->batch + kTileV - 1) / kTileV) < int64_t(p->sm_count))
+    p->engine = 3;
   if (p->engine == 3) {  // up kernel of 8-vector tiles feeding the per-range pass
     if (L < 1 || p->s > 32) return LC_ERR_INVALID_ARG;
     vt = 8;
@@ -2301,7 +2306,7 @@ lc_status configure_kernels(lc_plan* p) {
       const int64_t slots = int64_t(occ) * p->sm_count;
       const int64_t nls = int64_t(2) << L;
       int64_t nr = std::max<int64_t>(1, (slots + p->ntiles - 1) / p->ntiles);
-      nr = std::min(nr, nls);
+      nr = std::max<int64_t>(1, std::min(nr, nls / 64));  // ranges of >= 64 leaves (the entry chain is L deep)
       const int64_t rlen = (nls + nr - 1) / nr;
       nr = (nls + rlen - 1) / rlen;
       p->range_n = int(nr);
