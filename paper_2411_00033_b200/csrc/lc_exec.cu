@@ -1360,6 +1360,9 @@ __host__ __device__ inline int64_t range_smem_doubles(int s) {
   return 2 * 32 * kM + (kMM + 4) + 80 + LC_FRING * 2 * kTileV * fst + LC_FRING * 4 * s + int64_t(5) * 2 * kTS +
          2 * kTileV * (2 * s + 4);
 }
+#ifndef LC_RANGE_MINB
+#define LC_RANGE_MINB 4  // CTAs per SM the range kernel's registers are bounded for (measured: 2 -> 21.3 ms, 4 -> 18.2 ms at cfg4)
+#endif
 __host__ __device__ inline int64_t range_scratch_doubles(int L) { return int64_t(L >= 2 ? L - 2 : 0) * 2 * 2 * kTS; }
 
 struct TileParams {
@@ -1812,7 +1815,7 @@ __global__ void __launch_bounds__(kTileThreads, 2) lc_tile_kernel(const __grid_c
 // started at the range's rightmost leaf from the top level down, and the c of the levels below L-2 in
 // a per-CTA global scratch (the footprint does not grow with L).
 template <int DIR>
-__global__ void __launch_bounds__(kTileThreads, 2) lc_range_kernel(const __grid_constant__ TileParams P) {
+__global__ void __launch_bounds__(kTileThreads, LC_RANGE_MINB) lc_range_kernel(const __grid_constant__ TileParams P) {
   extern __shared__ __align__(128) unsigned char smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int lr = lane >> 2, lc = lane & 3;
