@@ -1349,11 +1349,20 @@ __host__ __device__ inline int tile_fst(int s) { int f = 4; while (f < s) f += 1
 #endif
 // T [2][32][M] | B(0) [M][M]+4 | tabA [80] | f ring [4][2][8][fst] | lambda ring [4][4s] |
 // w ring [L][3][2][8][M] | c: levels < L-1 [2][2][8][M], level L-1 [3][2][8][M] | z [2][8][2s+4]
+#ifndef LC_TILE_SL
+#define LC_TILE_SL 0  // levels whose w / c stay in shared memory (0: all); the rest in a per-CTA scratch
+#endif
+#ifndef LC_TILE_MINB
+#define LC_TILE_MINB 2
+#endif
+__host__ __device__ inline int tile_gs(int L) { return (LC_TILE_SL == 0 || L <= LC_TILE_SL) ? 0 : L - LC_TILE_SL; }
 __host__ __device__ inline int64_t tile_smem_doubles(int L, int s) {
   const int fst = tile_fst(s);
-  return 2 * 32 * kM + (kMM + 4) + 80 + LC_FRING * 2 * kTileV * fst + LC_FRING * 4 * s + int64_t(L) * 3 * 2 * kTS +
-         int64_t(2 * L + 1) * 2 * kTS + 2 * kTileV * (2 * s + 4);
+  const int ns = L - tile_gs(L);  // levels in shared memory
+  return 2 * 32 * kM + (kMM + 4) + 80 + LC_FRING * 2 * kTileV * fst + LC_FRING * 4 * s + int64_t(ns) * 3 * 2 * kTS +
+         int64_t(2 * ns + 1) * 2 * kTS + 2 * kTileV * (2 * s + 4);
 }
+__host__ __device__ inline int64_t tile_scratch_doubles(int L) { return int64_t(tile_gs(L)) * 5 * 2 * kTS; }
 
 __host__ __device__ inline int64_t range_smem_doubles(int s) {
   const int fst = tile_fst(s);
@@ -1434,7 +1443,7 @@ __device__ __forceinline__ void band32(const double* __restrict__ fU, const doub
 }
 
 template <int DIR>
-__global__ void __launch_bounds__(kTileThreads, 2) lc_tile_kernel(const __grid_constant__ TileParams P) {
+__global__ void __launch_bounds__(kTileThreads, LC_TILE_MINB) lc_tile_kernel(const __grid_constant__ TileParams P) {
   extern __shared__ __align__(128) unsigned char smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int lr = lane >> 2, lc = lane & 3;
@@ -1446,14 +1455,21 @@ __global__ void __launch_bounds__(kTileThreads, 2) lc_tile_kernel(const __grid_c
   double* taq = Bq + kMM + 4;                     // tabA [80]
   double* fr = taq + 80;                          // [LC_FRING][2][8][fst]
   double* lmr = fr + LC_FRING * 2 * kTileV * fst; // [LC_FRING][4s]
-  double* wr = lmr + LC_FRING * 4 * s;            // [L][3][2][8][M]
-  double* cs = wr + L * 3 * 2 * kTS;              // [L-1][2][2][8][M] then [3][2][8][M]
-  double* zs = cs + (2 * L + 1) * 2 * kTS;        // [2][8][2s+4]
+  const int gs = tile_gs(L);                      // levels >= gs in shared memory, below in scratch
+  const int ns = L - gs;
+  double* wr = lmr + LC_FRING * 4 * s;            // [ns][3][2][8][M]
+  double* cs = wr + ns * 3 * 2 * kTS;             // levels gs..L-2: [2][2][8][M], then leaf [3][2][8][M]
+  double* zs = cs + (2 * ns + 1) * 2 * kTS;       // [2][8][2s+4]
+  double* gw = P.scratch + int64_t(blockIdx.x) * tile_scratch_doubles(L);  // [gs][3][2][8][M]
+  double* gc = gw + gs * 3 * 2 * kTS;                                       // [gs][2][2][8][M]
   auto fslot = [&](int U) { return fr + ((U + LC_FRING) % LC_FRING) * 2 * kTileV * fst; };  // U >= -1
   auto lslot = [&](int U) { return lmr + ((U + LC_FRING) % LC_FRING) * 4 * s; };
-  auto wslot = [&](int g, int t) { return wr + (g * 3 + t % 3) * 2 * kTS; };
+  auto wslot = [&](int g, int t) {
+    return g >= gs ? wr + ((g - gs) * 3 + t % 3) * 2 * kTS : gw + (g * 3 + t % 3) * 2 * kTS;
+  };
   auto cslot = [&](int g, int u) {
-    return g == L - 1 ? cs + (2 * (L - 1) + u % 3) * 2 * kTS : cs + (g * 2 + (u & 1)) * 2 * kTS;
+    return g == L - 1 ? cs + (2 * (ns - 1) + u % 3) * 2 * kTS
+                      : (g >= gs ? cs + ((g - gs) * 2 + (u & 1)) * 2 * kTS : gc + (g * 2 + (u & 1)) * 2 * kTS);
   };
   auto zbuf = [&](int U) { return zs + (U & 1) * kTileV * zst_; };
 
@@ -1503,7 +1519,8 @@ __global__ void __launch_bounds__(kTileThreads, 2) lc_tile_kernel(const __grid_c
   const double inv_pi = 0.318309886183790671537767526745028724;
 
   for (int64_t tile = blockIdx.x; tile < P.ntiles; tile += gridDim.x) {
-    for (int i = tid; i < (2 * L + 1) * 2 * kTS; i += kTileThreads) cs[i] = 0.0;  // rows without M2L stay 0
+    for (int i = tid; i < (2 * ns + 1) * 2 * kTS; i += kTileThreads) cs[i] = 0.0;  // rows without M2L stay 0
+    for (int i = tid; i < gs * 2 * 2 * kTS; i += kTileThreads) gc[i] = 0.0;
     {
       double* fz = fslot(nls);  // the segment past the end reads as zero
       for (int i = tid; i < 2 * kTileV * fst; i += kTileThreads) fz[i] = 0.0;
@@ -2335,7 +2352,7 @@ lc_status configure_kernels(lc_plan* p) {
       p->tile_grid = int(std::min<int64_t>(ntiles8, int64_t(occ) * p->sm_count));
       p->vt = kTileV;
       p->ntiles = ntiles8;
-      p->ws_bytes = 256;
+      p->ws_bytes = size_t(std::max<int64_t>(256, int64_t(p->tile_grid) * tile_scratch_doubles(L) * 8));
     }
   }
   return LC_OK;
@@ -2427,6 +2444,7 @@ lc_status launch_execute(const lc_plan* p, const double* in, double* out, void* 
     tp.in = in; tp.out = out; tp.A = p->d_A; tp.tabA = p->d_tabA; tp.tabB = p->d_tabB; tp.Tpad = p->d_Tpad;
     tp.B = p->d_B; tp.ld_in = p->ld_in; tp.ld_out = p->ld_out; tp.n = p->n; tp.N = p->N; tp.batch = p->batch;
     tp.ntiles = p->ntiles; tp.layout = p->layout; tp.L = int(p->L); tp.s = int(p->s);
+    tp.scratch = reinterpret_cast<double*>(ws);
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
