@@ -1,31 +1,25 @@
-// lc_exec.cu -- execution stage (Alg. 4, alg:fastercomplete)
-// as two sm_100a kernels per transform; both parities are processed together
-// (the same A_hat serves sigma = 0 and 1, so it is streamed once).
+// lc_exec.cu -- execution stage (Alg. 4, alg:fastercomplete) on sm_100a.
+// Both parities are processed together (the same A_hat serves sigma = 0 and 1).
+// Three engines (the plan picks one):
 //
-//   lc_up_kernel     one CTA per subtree of 2^kup leaf segments x VT vectors, one wave:
-//                    step 1 (eq:wMM, w = f^sigma T(sigma), T(sigma) read from the
-//                    kernel-parameter constant bank as uniform DFMA operands) and step 2
-//                    (eq:wtk with Alg. a.1) inside the subtree; the last
-//                    CTA of each group of 2^G sibling subtrees continues the upward pass
-//                    to level 0.  Writes w(g) of every level; raises readiness flags.
-//   lc_stream_kernel persistent, warp-specialised:
-//                    * producer lane: TMA bulk copies (cp.async.bulk + mbarrier ring,
-//                      L2 evict-first) of the level-major A_hat arena and each chunk's
-//                      w window, in the level order  [fine non-leaf levels] ->
-//                      [coarse levels] -> [leaf level L-1];
-//                    * 4 M2L warps: step 3 from the ring, c_m2l
-//                      stores, completion counters / epoch flags per chunk;
-//                    * 4 band warps: first the direct band of step 6 (Alg. 1 restricted
-//                      to j < j_end(i)), which depends only on f and lambda, then the
-//                      "down units": step 4 ("faster downward spreading")
-//                      along the ancestor chain and down a subtree, step 5 (eq:step5)
-//                      with T(sigma) from the constant bank, step 7 (C^{-1}) and the store.
-//                      A down unit needs the non-leaf levels of c_m2l (done before the
-//                      leaf level is streamed) and the leaf-level chunks over its rows,
-//                      so the downward pass overlaps the second half of the A_hat stream.
-//
-// The kernels are chained with programmatic dependent launch (griddepcontrol); the
-// streaming kernel synchronises with the up kernel through release/acquire flags.
+// Engine 1 (single vectors, small batches), three kernels chained with programmatic dependent
+// launch and release/acquire flags in the workspace:
+//   lc_up_kernel     one CTA per subtree of 2^kup leaf segments x VT vectors (about one wave):
+//                    step 1 (eq:wMM) on the fp64 tensor cores (DMMA, 8 leaves per warp item) and
+//                    step 2 (Alg. a.1) inside the subtree; the last CTA of each
+//                    group of sibling subtrees continues to level 0.  Writes w of every level.
+//   lc_stream_kernel persistent, warp-specialised: a producer lane streams the level-major A_hat
+//                    arena and the w windows with TMA bulk copies into an mbarrier ring (finest
+//                    level first); 3 M2L warps apply step 3; 4 band warps run
+//                    the direct band of step 6 (Alg. 1 restricted to j < j_end(i)) on dynamically
+//                    scheduled units.  Both take units from global counters.
+//   lc_down_kernel   one CTA per subtree: step 4 ("faster downward spreading")
+//                    along the ancestor chain and down the subtree (DMMA), step 5 (eq:step5, DMMA),
+//                    step 7 (C^{-1}) added to the band result and stored.
+// Engine 2 (batches of short vectors): lc_tile_kernel, one CTA per 8-vector tile, the whole
+//   algorithm in one right-to-left pass over the leaf segments with every intermediate on chip.
+// Engine 3 (batches of long vectors): lc_up_kernel with 8-vector tiles, then lc_range_kernel, the
+//   same pass over ranges of leaves of each tile with w read from the workspace.
 #include <algorithm>
 #include <cstdio>
 #include <cstring>
@@ -34,9 +28,6 @@
 
 namespace lc {
 
-// B(0) (App. A3) is a universal constant for M = 18: in constant memory the fully
-// unrolled triangular products take it as a uniform DFMA operand.
-__constant__ double c_B0[kMM];
 
 // ---------------------------------------------------------------- PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -103,9 +94,6 @@ __device__ __forceinline__ void named_sync(int id, int nthreads) {
 __device__ __forceinline__ void st_release(int* p, int v) {
   asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
-__device__ __forceinline__ void red_release_add(int* p, int v) {
-  asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
 __device__ __forceinline__ int ld_acquire(const int* p) {
   int v;
   asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -113,9 +101,6 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
 }
 __device__ __forceinline__ void wait_flag(const int* p) {
   while (ld_acquire(p) == 0) __nanosleep(64);
-}
-__device__ __forceinline__ void wait_geq(const int* p, int target) {  // wrap-safe "p >= target"
-  while (ld_acquire(p) - target < 0) __nanosleep(64);
 }
 
 // fp64 tensor-core MMA (DMMA m8n8k4, row.col): lane l holds A[l>>2][l&3], B[l&3][l>>2] and
@@ -144,51 +129,6 @@ __device__ __forceinline__ void lc_ts_any(int kern, int slot) {
 #define LC_TS(k, s) ((void)0)
 #define LC_TS_T(k, s) ((void)0)
 #endif
-
-// ---------------------------------------------------------------- transfer operators
-// Alg. a.1 for one parent node:
-// parent[n] = sum_{k<=n} b_nk (x0_k + (-1)^(n-k) x1_k)  (B(1) = B(0) with the odd diagonals
-// negated, App. A3).  18 register accumulators; B(0) from constant memory.
-__device__ __forceinline__ void m2m18(const double* __restrict__ x0, const double* __restrict__ x1,
-                                      double* __restrict__ out) {
-  double acc[kM];
-#pragma unroll
-  for (int n = 0; n < kM; ++n) acc[n] = 0.0;
-#pragma unroll
-  for (int k = 0; k < kM; k += 2) {
-    const double2 a2 = *reinterpret_cast<const double2*>(x0 + k);
-    const double2 b2 = *reinterpret_cast<const double2*>(x1 + k);
-    const double zp0 = a2.x + b2.x, zm0 = a2.x - b2.x, zp1 = a2.y + b2.y, zm1 = a2.y - b2.y;
-#pragma unroll
-    for (int n = k; n < kM; ++n) acc[n] = fma(c_B0[n * kM + k], ((n - k) & 1) ? zm0 : zp0, acc[n]);
-#pragma unroll
-    for (int n = k + 1; n < kM; ++n) acc[n] = fma(c_B0[n * kM + k + 1], ((n - k - 1) & 1) ? zm1 : zp1, acc[n]);
-  }
-#pragma unroll
-  for (int n = 0; n < kM; n += 2) *reinterpret_cast<double2*>(out + n) = make_double2(acc[n], acc[n + 1]);
-}
-
-// Warp-level step 4: lane l < 18 owns output mode l and keeps its column of B(0) in
-// registers; the input vector is read from shared memory by all lanes at once (broadcast).
-struct BCol {  // bcol[n] = b_{n l} (n >= l), 0 otherwise
-  double v[kM];
-};
-__device__ __forceinline__ void load_bcol(BCol& c, int l) {
-#pragma unroll
-  for (int n = 0; n < kM; ++n) c.v[n] = (l < kM && n >= l) ? c_B0[n * kM + (l < kM ? l : 0)] : 0.0;
-}
-// (B(p)^T c)_l = (-1)^{pl} sum_n b_nl (-1)^{pn} c_n   (lane l)
-__device__ __forceinline__ double l2l_warp(const BCol& cb, const double* __restrict__ c, int p, int l) {
-  double a0 = 0.0, a1 = 0.0;
-#pragma unroll
-  for (int n = 0; n < kM; n += 2) {
-    const double2 c2 = *reinterpret_cast<const double2*>(c + n);
-    a0 = fma(cb.v[n], c2.x, a0);
-    a1 = fma(cb.v[n + 1], c2.y, a1);
-  }
-  const double r = p ? a0 - a1 : a0 + a1;
-  return (p && (l & 1)) ? -r : r;
-}
 
 // ---------------------------------------------------------------- parameters
 // flags (workspace ints): [0] up main-phase arrivals, [1] fine levels of w ready,
@@ -528,7 +468,6 @@ constexpr int kBandThreads = 32 * kBandWarps;
 constexpr int kM2lThreads = 32 * kM2lWarps;
 
 __device__ __forceinline__ void band_sync() { named_sync(1, kBandThreads); }
-__device__ __forceinline__ void m2l_sync() { named_sync(2, kM2lThreads); }
 
 // M2L unit q (< nm2l) = (chunk, tile): chunk = (level g, blocks [b0, b0+nb)), nb <= cb, levels in
 // the order lvorder[]; tiles innermost so concurrent CTAs share A_hat in L2.
@@ -2199,11 +2138,6 @@ lc_status configure_kernels(lc_plan* p) {
     if (ea == cudaSuccess) ea = set_max_dyn_smem(lc_tile_kernel<1>, smax);
     if (ea == cudaSuccess) ea = set_max_dyn_smem(lc_range_kernel<0>, smax);
     if (ea == cudaSuccess) ea = set_max_dyn_smem(lc_range_kernel<1>, smax);
-    if (ea == cudaSuccess) {
-      double B[kMM];
-      ea = cudaMemcpy(B, p->d_B, sizeof(B), cudaMemcpyDeviceToHost);
-      if (ea == cudaSuccess) ea = cudaMemcpyToSymbol(c_B0, B, sizeof(B));
-    }
     if (ea != cudaSuccess) return record_cuda_error(ea);
     g_device_ready[p->device] = true;
   }
