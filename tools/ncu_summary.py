@@ -33,9 +33,11 @@ for r in rows[2:]:
         if key in h:
             i = h.index(key)
             lines.append(f"| {lab} | {r[i]} {units[i]} |")
+    scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
     try:
-        rd = float(r[h.index("dram__bytes_read.sum")]) * (1e6 if units[h.index("dram__bytes_read.sum")] == "Mbyte" else 1)
-        wr = float(r[h.index("dram__bytes_write.sum")]) * (1e6 if units[h.index("dram__bytes_write.sum")] == "Mbyte" else 1)
+        ir, iw = h.index("dram__bytes_read.sum"), h.index("dram__bytes_write.sum")
+        rd = float(r[ir]) * scale.get(units[ir], 1.0)
+        wr = float(r[iw]) * scale.get(units[iw], 1.0)
         short = name.split("<")[0].split("(")[0].replace("void ", "").replace("lc::", "").strip()
         traffic[short] = rd + wr
         lines.append(f"| DRAM read+write per launch | {rd + wr:.0f} bytes |")
