@@ -494,6 +494,10 @@ __device__ __forceinline__ void m2l_unit(int q, int ntiles, int L, int cb, const
 template <int VT, int DIR>
 __device__ __forceinline__ void band_unit(const StreamParams& P, int tile, int lr, double* ta, double* tb, double* gt,
                                           double* zst, int tp, int btid) {
+  // padding of the band tiles: one double every 2^kPadSh.  Several vectors: the lanes of a warp
+  // take rows 2 kBandR apart (one pad per 16 separates their banks); one vector: the lanes take
+  // consecutive leaf segments 2s apart (one pad per 64 keeps the segment stride odd for s = 32)
+  constexpr int kPadSh = VT == 1 ? 6 : 4;
   const int s = P.s, kb = P.kb;
   const int nleaf = 1 << kb;
   const int seglen = 2 * s;
@@ -535,7 +539,7 @@ __device__ __forceinline__ void band_unit(const StreamParams& P, int tile, int l
   } else {
   for (int x = btid; x < tcols + 2 * kBandR; x += kBandThreads) {
     const bool ok = x < tbl;
-    cp_async8(tb + x + (x >> 4), ok ? P.tabB + i0 + x : P.tabB, ok ? 8u : 0u);
+    cp_async8(tb + x + (x >> kPadSh), ok ? P.tabB + i0 + x : P.tabB, ok ? 8u : 0u);
   }
 #pragma unroll 1
   for (int v = 0; v < VT; ++v) {
@@ -547,12 +551,12 @@ __device__ __forceinline__ void band_unit(const StreamParams& P, int tile, int l
       const double* src = P.in + gv * P.ld_in + i0;
       for (int x = btid; x < tcols + 2 * kBandR; x += kBandThreads) {
         const bool ok = x < lim;
-        cp_async8(gt + v * tp + x + (x >> 4), ok ? src + x : P.in, ok ? 8u : 0u);
+        cp_async8(gt + v * tp + x + (x >> kPadSh), ok ? src + x : P.in, ok ? 8u : 0u);
       }
     } else {
       for (int x = btid; x < tcols + 2 * kBandR; x += kBandThreads) {
         const bool ok = x < lim;
-        cp_async8(gt + v * tp + x + (x >> 4), ok ? P.in + (i0 + x) * P.ld_in + gv : P.in, ok ? 8u : 0u);
+        cp_async8(gt + v * tp + x + (x >> kPadSh), ok ? P.in + (i0 + x) * P.ld_in + gv : P.in, ok ? 8u : 0u);
       }
     }
   }
@@ -654,7 +658,7 @@ __device__ __forceinline__ void band_unit(const StreamParams& P, int tile, int l
     for (int r = 0; r < kBandR; ++r) {
       acc[r] = 0.0;
       aw[r] = 0.0;
-      bw[r] = tb[(ii + r) + ((ii + r) >> 4)];
+      bw[r] = tb[(ii + r) + ((ii + r) >> kPadSh)];
     }
     const int ngrp = (cmax + 1) / kBandR;
     int c0 = 0;
@@ -664,8 +668,8 @@ __device__ __forceinline__ void band_unit(const StreamParams& P, int tile, int l
         const int c = c0 + q;
         aw[q] = ta[c];
         const int xb = ii + kBandR - 1 + c, xg = ii + 2 * c;
-        bw[(q + kBandR - 1) % kBandR] = tb[xb + (xb >> 4)];
-        double gval = gv_t[xg + (xg >> 4)];
+        bw[(q + kBandR - 1) % kBandR] = tb[xb + (xb >> kPadSh)];
+        double gval = gv_t[xg + (xg >> kPadSh)];
         if (DIR == 1) gval *= double(i + 2 * c);
 #pragma unroll
         for (int r = 0; r < kBandR; ++r) acc[r] = fma(aw[(q - r + kBandR) % kBandR] * bw[(r + q) % kBandR], gval, acc[r]);
@@ -677,8 +681,8 @@ __device__ __forceinline__ void band_unit(const StreamParams& P, int tile, int l
       if (c <= cmax) {
         aw[q] = ta[c];
         const int xb = ii + kBandR - 1 + c, xg = ii + 2 * c;
-        bw[(q + kBandR - 1) % kBandR] = tb[xb + (xb >> 4)];
-        double gval = gv_t[xg + (xg >> 4)];
+        bw[(q + kBandR - 1) % kBandR] = tb[xb + (xb >> kPadSh)];
+        double gval = gv_t[xg + (xg >> kPadSh)];
         if (DIR == 1) gval *= double(i + 2 * c);
 #pragma unroll
         for (int r = 0; r < kBandR; ++r) acc[r] = fma(aw[(q - r + kBandR) % kBandR] * bw[(r + q) % kBandR], gval, acc[r]);
