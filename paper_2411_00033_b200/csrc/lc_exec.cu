@@ -617,7 +617,7 @@ __device__ __forceinline__ void band_unit(const StreamParams& P, int tile, int l
               z *= double(2 * ir + 1);
               if (ir == 0) z += gt[v * tp8];  // entry (0,0) of A^{-1}C is 1 (reading R2)
             }
-            zst[v * rows + ii] = z;
+            zst[(v * rows + ii) + ((v * rows + ii) >> kPadSh)] = z;
           }
         }
       }
@@ -697,7 +697,7 @@ __device__ __forceinline__ void band_unit(const StreamParams& P, int tile, int l
           z *= double(2 * ir + 1);
           if (ir == 0) z += gv_t[0];  // entry (0,0) of A^{-1}C is 1 (reading R2)
         }
-        zst[v * rows + ii + 2 * r] = z;
+        zst[(v * rows + ii + 2 * r) + ((v * rows + ii + 2 * r) >> kPadSh)] = z;
       }
     }
   }
@@ -714,9 +714,10 @@ __device__ __forceinline__ void band_unit(const StreamParams& P, int tile, int l
     if (gv >= P.batch) break;
     if (P.layout == LC_VEC_CONTIGUOUS) {
       double* dst = P.out + gv * P.ld_out + i0;
-      for (int x = btid; x < olim; x += kBandThreads) dst[x] = zst[v * rows + x];
+      for (int x = btid; x < olim; x += kBandThreads) dst[x] = zst[(v * rows + x) + ((v * rows + x) >> kPadSh)];
     } else {
-      for (int x = btid; x < olim; x += kBandThreads) P.out[(i0 + x) * P.ld_out + gv] = zst[v * rows + x];
+      for (int x = btid; x < olim; x += kBandThreads)
+        P.out[(i0 + x) * P.ld_out + gv] = zst[(v * rows + x) + ((v * rows + x) >> kPadSh)];
     }
   }
   band_sync();  // tiles are reused by the next unit

@@ -74,7 +74,7 @@ __host__ __device__ inline StreamSmem stream_smem_layout(int VT, int cb, int nst
   S.ta = o;   o = align_up(o + (int64_t(2) * s + 2 * kBandR) * 8, 128);
   S.tb = o;   o = align_up(o + S.tp * 8, 128);
   S.gt = o;   o = align_up(o + int64_t(VT) * S.tp * 8, 128);
-  S.zst = o;  o = align_up(o + int64_t(VT) * nleaf * 2 * s * 8, 128);
+  S.zst = o;  o = align_up(o + (pidx(int64_t(VT) * nleaf * 2 * s) + 2) * 8, 128);  // padded like the band tiles
   S.bars = o; o = align_up(o + int64_t(2) * nst * 8, 128);
   S.total = o;
   return S;
