@@ -172,7 +172,7 @@ def run_gpu(args, world, rank, local):
     tmp = torch.empty_like(x)
     y = torch.empty_like(x)
     opts = dict(vt=args.vt, subtree=args.subtree, stage_blocks=args.stage_blocks, stages=args.stages,
-                engine=args.engine)
+                engine=args.engine, up_subtree=args.up_subtree)
     stream = torch.cuda.current_stream(dev)
     two_d = args.config == "cfg5"
     if two_d:
@@ -508,6 +508,7 @@ def main():
     ap.add_argument("--engine", type=int, default=0,
                     help="0 automatic, 1 level-pipelined kernels, 2 per-tile kernel, 3 up kernel + per-range pass")
     ap.add_argument("--subtree", type=int, default=0)
+    ap.add_argument("--up-subtree", type=int, default=0)
     ap.add_argument("--stage-blocks", type=int, default=0)
     ap.add_argument("--stages", type=int, default=0)
     ap.add_argument("--no-graph", action="store_true")
