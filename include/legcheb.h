@@ -76,7 +76,9 @@ typedef struct {
   int32_t up_subtree; /* subtree depth of the upward (leaf projection + M2M) kernel; 0 -> automatic */
   int32_t engine;   /* 0 -> automatic; 1 -> level-pipelined kernels (up / streaming / down);
                        2 -> per-tile streaming kernel (one CTA per 8-vector tile, whole Alg. 4 on chip;
-                       needs L >= 1 and s <= 32; automatic choice from about one tile per SM, or a third of that for n <= 2048) */
+                       needs L >= 1 and s <= 32; automatic choice from about one tile per SM, or a third of that for n <= 2048);
+                       3 -> up kernel of 8-vector tiles + the per-tile pass over leaf ranges (needs L >= 1, s <= 32;
+                       automatic for L >= 9 with >= 8 vectors from n = 2^18, >= 16 below, and fewer tiles than SMs) */
 } lc_plan_opts;
 
 /* Geometry and algorithmic work of a plan (per vector unless stated). */

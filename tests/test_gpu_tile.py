@@ -156,3 +156,13 @@ def test_range_engine_matches_level_pipeline():
         torch.cuda.synchronize()
         e = (z1 - z3).abs().max().item() / z1.abs().max().item()
         assert e <= 1e-13, (direction, e)
+
+
+def test_range_engine_automatic_choice():
+    dev = _dev()
+    p = _plan(100000, "leg2cheb", batch=32, device=dev)  # L = 10, 4 tiles: engine 3
+    assert p.kernel_info["engine"] == 3 and p.kernel_info["range_len"] >= 64
+    q = _plan(100000, "leg2cheb", batch=1, device=dev)  # single vector: level-pipelined kernels
+    assert q.kernel_info["engine"] == 1
+    with pytest.raises(RuntimeError):
+        _plan(100000, "leg2cheb", batch=8, device=dev, engine=4)
