@@ -1001,12 +1001,15 @@ __global__ void __launch_bounds__(kStreamThreads, 2) lc_stream_kernel(const __gr
   __syncthreads();
   LC_TS(1, 1);
   if (tid == 0) {
-    __threadfence();  // this CTA's c_m2l and band stores before its arrival
-    s_last = atomicAdd(&P.flags[4], 1) == int(gridDim.x) - 1;
+    // arrival with acquire-release semantics: this CTA's c_m2l and band stores (ordered before it by
+    // the barrier) are released, and the last arriver acquires every other CTA's, so its release of
+    // flags[12] below carries them all to the down kernel (one RMW instead of two full fences)
+    int old;
+    asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;" : "=r"(old) : "l"(&P.flags[4]) : "memory");
+    s_last = old == int(gridDim.x) - 1;
   }
   __syncthreads();
   if (s_last && tid == 0) {  // the last CTA re-arms the counters and releases the down kernel
-    __threadfence();
     P.flags[1] = 0;
     P.flags[3] = 0;
     P.flags[5] = 0;
