@@ -94,6 +94,13 @@ __device__ __forceinline__ void named_sync(int id, int nthreads) {
 __device__ __forceinline__ void st_release(int* p, int v) {
   asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+// gpu-scope acquire-release RMW: releases the CTA's prior stores (ordered before it by a barrier)
+// and acquires those released by earlier arrivers (threadfence-reduction without full fences)
+__device__ __forceinline__ int atom_add_acq_rel(int* p, int v) {
+  int old;
+  asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
 __device__ __forceinline__ int ld_acquire(const int* p) {
   int v;
   asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -384,14 +391,12 @@ __global__ void __launch_bounds__(kThreads, 2) lc_up_kernel(const __grid_constan
     }
   }
   // the fine levels (gr..L-1) of the whole batch are ready once every CTA got here
-  __threadfence();
   __syncthreads();
   LC_TS(0, 4);
   if (tid == 0) {
     const int total = int(gridDim.x * gridDim.y);
-    if (atomicAdd(&P.flags[0], 1) == total - 1) {
+    if (atom_add_acq_rel(&P.flags[0], 1) == total - 1) {
       atomicExch(&P.flags[0], 0);
-      __threadfence();
       st_release(&P.flags[1], 1);
       if (P.gr == 0) st_release(&P.flags[3], 1);
     }
@@ -407,7 +412,7 @@ __global__ void __launch_bounds__(kThreads, 2) lc_up_kernel(const __grid_constan
     __syncthreads();
     if (tid == 0) {
       int* c = P.cnt + tile * P.cnt_tile + (nseg(g) - 4) + grp;
-      const int old = atomicAdd(c, 1);
+      const int old = atom_add_acq_rel(c, 1);
       const int last = (old == (1 << ge) - 1);
       if (last) atomicExch(c, 0);  // self-reset for the next launch
       s_last = last;
@@ -440,8 +445,7 @@ __global__ void __launch_bounds__(kThreads, 2) lc_up_kernel(const __grid_constan
         for (int i = tid; i < cj2; i += blockDim.x) dst[i] = src[i];
       }
     }
-    __threadfence();
-    g -= ge;
+    g -= ge;  // the next arrival (after a barrier, acquire-release) publishes these stores
     node = grp;
     LC_TS(0, 6);
   }
@@ -449,9 +453,8 @@ __global__ void __launch_bounds__(kThreads, 2) lc_up_kernel(const __grid_constan
     __syncthreads();
     if (tid == 0) {
       const int total = 4 * int(gridDim.y);
-      if (atomicAdd(&P.flags[2], 1) == total - 1) {
+      if (atom_add_acq_rel(&P.flags[2], 1) == total - 1) {
         atomicExch(&P.flags[2], 0);
-        __threadfence();
         st_release(&P.flags[3], 1);
       }
     }
@@ -1004,9 +1007,7 @@ __global__ void __launch_bounds__(kStreamThreads, 2) lc_stream_kernel(const __gr
     // arrival with acquire-release semantics: this CTA's c_m2l and band stores (ordered before it by
     // the barrier) are released, and the last arriver acquires every other CTA's, so its release of
     // flags[12] below carries them all to the down kernel (one RMW instead of two full fences)
-    int old;
-    asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;" : "=r"(old) : "l"(&P.flags[4]) : "memory");
-    s_last = old == int(gridDim.x) - 1;
+    s_last = atom_add_acq_rel(&P.flags[4], 1) == int(gridDim.x) - 1;
   }
   __syncthreads();
   if (s_last && tid == 0) {  // the last CTA re-arms the counters and releases the down kernel
