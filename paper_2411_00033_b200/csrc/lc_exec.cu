@@ -373,15 +373,11 @@ __global__ void __launch_bounds__(kThreads, 2) lc_up_kernel(const __grid_constan
   }
   __syncthreads();
   LC_TS(0, 2);
-  // step 2 inside the subtree
-  for (int j = k; j >= 1; --j) {
-    m2m_level<VT>(Bs, tree + tree_off(j), tree + tree_off(j - 1), j - 1);
-    __syncthreads();
-  }
-  LC_TS(0, 3);
   double* wt = P.w + tile * P.w_tile;
   const int64_t VM = int64_t(VT) * kM;
-  for (int j = 0; j <= k; ++j) {
+  // each subtree level goes to the workspace as soon as it exists, so the stores drain while the
+  // next M2M levels compute (the release below then waits for little more than the last level)
+  auto write_level = [&](int j) {
     const int g = P.gr + j;
     const int cnt2 = int((int64_t(1) << j) * VM / 2);
     for (int sg = 0; sg < 2; ++sg) {
@@ -389,7 +385,15 @@ __global__ void __launch_bounds__(kThreads, 2) lc_up_kernel(const __grid_constan
       const double2* src = reinterpret_cast<const double2*>(tree + tree_off(j) + sg * (int64_t(1) << j) * VM);
       for (int i = tid; i < cnt2; i += blockDim.x) dst[i] = src[i];
     }
+  };
+  write_level(k);
+  // step 2 inside the subtree
+  for (int j = k; j >= 1; --j) {
+    m2m_level<VT>(Bs, tree + tree_off(j), tree + tree_off(j - 1), j - 1);
+    __syncthreads();
+    write_level(j - 1);
   }
+  LC_TS(0, 3);
   // the fine levels (gr..L-1) of the whole batch are ready once every CTA got here
   __syncthreads();
   LC_TS(0, 4);
