@@ -265,14 +265,14 @@ def run_gpu(args, world, rank, local):
     dl = pl.desc
     engine = pl.kernel_info.get("engine", 1)
     if engine == 3:
-        names = ["lc_up_kernel", "lc_range_kernel"]
+        names = ["lc_up3_kernel", "lc_range_kernel"]
     else:
         names = ["lc_tile_kernel"] if kpe == 1 else (["lc_up_kernel"] if kpe == 3 else []) + ["lc_stream_kernel",
                                                                                              "lc_down_kernel"]
     # algorithmic bytes per launch (f in, z out, A_hat once, lambda once; work arrays excluded):
     # the up kernel reads f, the streaming kernel reads A_hat and lambda (and f again for the band),
     # the down kernel writes z
-    alg = {"lc_up_kernel": 8.0 * n * V, "lc_stream_kernel": 8.0 * 324 * dl["nc"] + 8.0 * dl["N"],
+    alg = {"lc_up_kernel": 8.0 * n * V, "lc_up3_kernel": 8.0 * n * V, "lc_stream_kernel": 8.0 * 324 * dl["nc"] + 8.0 * dl["N"],
            "lc_down_kernel": 8.0 * n * V}
     if kpe == 2:
         alg["lc_stream_kernel"] += 8.0 * n * V

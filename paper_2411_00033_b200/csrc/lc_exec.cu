@@ -149,6 +149,9 @@ struct UpParams {
   const double* B;     // B(0) [M][M]
   int64_t ld_in, n, N, batch;
   int layout, L, s, k, gr, G, fstride, vec16;
+  int noflags;  // engine 3: the range kernel waits for the whole grid (griddepcontrol), no flags
+  int kc;       // engine 3 (lc_up3_kernel): subtrees per chunk = 2^kc
+  int64_t ntiles;
   double* w;
   int* cnt;
   int* flags;
@@ -256,37 +259,12 @@ __device__ __forceinline__ void m2m_level(const double* __restrict__ Bs, const d
   }
 }
 
-template <int VT, int SMAX>
-__global__ void __launch_bounds__(kThreads, 2) lc_up_kernel(const __grid_constant__ UpArgs<SMAX> A) {
-  extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ int s_last;
-  const UpParams& P = A.p;
-  const int s = P.s, k = P.k, fst = P.fstride;
+// stage the leaf range [R 2^k, (R+1) 2^k) of segments of vector tile `tile` into fs ([v][leaf][fst],
+// cp.async, not committed), zero padding beyond n
+template <int VT>
+__device__ __forceinline__ void up_stage(const UpParams& P, double* fs, int64_t R, int64_t tile, int nleaf, int fst) {
   const int tid = threadIdx.x;
-  const int nleaf = 1 << k;
-  const int seglen = 2 * s;
-  const int tlen = nleaf * seglen;
-  double* Ts = reinterpret_cast<double*>(smem);          // [2][SMAX][M], zero rows m >= s
-  double* Bs = Ts + 2 * SMAX * kM;                       // B(0) [M][M]
-  double* fs = reinterpret_cast<double*>(smem + kUpConstBytes);  // [v][leaf][fstride]
-  double* tree = reinterpret_cast<double*>(smem + kUpConstBytes + align_up((int64_t(VT) * nleaf * fst + 2 * SMAX) * 8, 128));
-  auto tree_off = [&](int j) { return ((1 << j) - 1) * 2 * VT * kM; };
-
-  const int64_t R = blockIdx.x;
-  const int64_t tile = blockIdx.y;
-  LC_TS(0, 0);
-  // plan constants into shared memory (broadcast operands of steps 1 and 2)
-  for (int i = tid; i < SMAX * kM; i += blockDim.x) cp_async16(Ts + 2 * i, P.Tpad + 2 * i);
-  for (int i = tid; i < kMM / 2; i += blockDim.x) cp_async16(Bs + 2 * i, P.B + 2 * i);
-  cp_async_commit();
-  griddep_wait();  // the input may be produced by the preceding kernel; w/c of the previous execution are free
-  // Trigger the dependent (streaming) launch only now: every streaming CTA then starts after the
-  // whole previous execution completed, so it can never observe flags of that execution.
-  griddep_launch();
-  if (tid == 0 && R == 0 && tile == 0) st_release(&P.flags[5], 1);  // the streaming kernel may read the input
-
-  // stage the leaf range [R 2^k, (R+1) 2^k) of segments, zero padding beyond n;
-  // segment stride fstride = 2s or 2s+2 (= 2 mod 4 doubles: conflict-free 16-byte reads below)
+  const int seglen = 2 * P.s, tlen = nleaf * seglen;
   const int64_t j0 = R * tlen;
   if (P.layout == LC_VEC_CONTIGUOUS) {
 #pragma unroll 1
@@ -320,21 +298,17 @@ __global__ void __launch_bounds__(kThreads, 2) lc_up_kernel(const __grid_constan
       cp_async8(fs + (v * nleaf + lf) * fst + x, ok ? P.in + j * P.ld_in + gv : P.in, ok ? 8u : 0u);
     }
   }
-  // zero tail read by the branch-free step 1 of the last leaf (m up to SMAX-1)
-  for (int x = tid; x < 2 * SMAX; x += blockDim.x) fs[VT * nleaf * fst + x] = 0.0;
-  if (fst > seglen)  // and the segment padding (fstride = 2s + 2 for even s)
-    for (int x = tid; x < VT * nleaf; x += blockDim.x) *reinterpret_cast<double2*>(fs + x * fst + seglen) = make_double2(0.0, 0.0);
-  cp_async_commit();
-  cp_async_wait<0>();
-  __syncthreads();
-  LC_TS(0, 1);
+}
 
+template <int VT, int SMAX>
+__device__ __forceinline__ void up_step1(const double* __restrict__ Ts, const double* __restrict__ fs, int fst,
+                                         int nleaf, int s, double* __restrict__ leaf) {
   // step 1: w(L-1)[t][k] = sum_m f[2s t + 2m + sigma] T(sigma)[m][k]   (eq:wMM), on the fp64
   // tensor cores: one warp item = (vector v, 8 leaves); A = T(sigma)^T (modes padded to 24 = 3
   // row tiles), B[m][leaf] = f[2s leaf + 2m + sigma] (one 16-byte load feeds both parities),
-  // K = SMAX rows of T (rows m >= s are zero, so the reads past a segment contribute nothing).
+  // K = 4 ceil(s/4) rows of T (rows m >= s are zero, so reads past a segment contribute nothing).
   {
-    double* leaf = tree + tree_off(k);
+    const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31, nw = blockDim.x >> 5;
     const int lr = lane >> 2, lc = lane & 3;
     const int ngrp = (nleaf + 7) >> 3;
@@ -346,8 +320,7 @@ __global__ void __launch_bounds__(kThreads, 2) lc_up_kernel(const __grid_constan
       double acc[2][3][2];
 #pragma unroll
       for (int mt = 0; mt < 3; ++mt) acc[0][mt][0] = acc[0][mt][1] = acc[1][mt][0] = acc[1][mt][1] = 0.0;
-#pragma unroll 4
-      for (int kk = 0; kk < SMAX / 4; ++kk) {
+      auto kstep = [&](int kk) {
         double2 f2 = *reinterpret_cast<const double2*>(fp + 8 * kk);  // f[2m], f[2m+1], m = 4kk + lc
         if (!okb) f2 = make_double2(0.0, 0.0);
         const double* t0 = tq + 4 * kk * kM;  // T(0)[m][8 mt + lr]
@@ -359,6 +332,16 @@ __global__ void __launch_bounds__(kThreads, 2) lc_up_kernel(const __grid_constan
           dmma(acc[0][mt], a0, f2.x);
           dmma(acc[1][mt], a1, f2.y);
         }
+      };
+      // K = 4 ceil(s/4) rows of T: the rows m >= s are zero, so short segments (s = 20 for
+      // n = 10^7) skip the all-zero K steps
+      const int nks = (s + 3) >> 2;
+      if (nks == SMAX / 4) {
+#pragma unroll
+        for (int kk = 0; kk < SMAX / 4; ++kk) kstep(kk);
+      } else {
+#pragma unroll 1
+        for (int kk = 0; kk < nks; ++kk) kstep(kk);
       }
 #pragma unroll
       for (int sg = 0; sg < 2; ++sg)
@@ -371,6 +354,50 @@ __global__ void __launch_bounds__(kThreads, 2) lc_up_kernel(const __grid_constan
           }
     }
   }
+}
+
+#ifndef LC_UP8_MINB
+#define LC_UP8_MINB 2  // resident CTAs per SM of the 8-vector up kernel (engine 3's first pass)
+#endif
+template <int VT, int SMAX>
+__global__ void __launch_bounds__(kThreads, (VT == 8 && SMAX == 32) ? LC_UP8_MINB : 2) lc_up_kernel(const __grid_constant__ UpArgs<SMAX> A) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ int s_last;
+  const UpParams& P = A.p;
+  const int s = P.s, k = P.k, fst = P.fstride;
+  const int tid = threadIdx.x;
+  const int nleaf = 1 << k;
+  const int seglen = 2 * s;
+  double* Ts = reinterpret_cast<double*>(smem);          // [2][SMAX][M], zero rows m >= s
+  double* Bs = Ts + 2 * SMAX * kM;                       // B(0) [M][M]
+  double* fs = reinterpret_cast<double*>(smem + up_const_bytes(SMAX));  // [v][leaf][fstride]
+  double* tree = reinterpret_cast<double*>(smem + up_const_bytes(SMAX) + align_up((int64_t(VT) * nleaf * fst + 2 * SMAX) * 8, 128));
+  auto tree_off = [&](int j) { return ((1 << j) - 1) * 2 * VT * kM; };
+
+  const int64_t R = blockIdx.x;
+  const int64_t tile = blockIdx.y;
+  LC_TS(0, 0);
+  // plan constants into shared memory (broadcast operands of steps 1 and 2)
+  for (int i = tid; i < SMAX * kM; i += blockDim.x) cp_async16(Ts + 2 * i, P.Tpad + 2 * i);
+  for (int i = tid; i < kMM / 2; i += blockDim.x) cp_async16(Bs + 2 * i, P.B + 2 * i);
+  cp_async_commit();
+  griddep_wait();  // the input may be produced by the preceding kernel; w/c of the previous execution are free
+  // Trigger the dependent (streaming) launch only now: every streaming CTA then starts after the
+  // whole previous execution completed, so it can never observe flags of that execution.
+  griddep_launch();
+  if (tid == 0 && R == 0 && tile == 0) st_release(&P.flags[5], 1);  // the streaming kernel may read the input
+
+  up_stage<VT>(P, fs, R, tile, nleaf, fst);
+  // zero tail read by the branch-free step 1 of the last leaf (m up to SMAX-1)
+  for (int x = tid; x < 2 * SMAX; x += blockDim.x) fs[VT * nleaf * fst + x] = 0.0;
+  if (fst > seglen)  // and the segment padding (fstride = 2s + 2 for even s)
+    for (int x = tid; x < VT * nleaf; x += blockDim.x) *reinterpret_cast<double2*>(fs + x * fst + seglen) = make_double2(0.0, 0.0);
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncthreads();
+  LC_TS(0, 1);
+
+  up_step1<VT, SMAX>(Ts, fs, fst, nleaf, s, tree + tree_off(k));
   __syncthreads();
   LC_TS(0, 2);
   double* wt = P.w + tile * P.w_tile;
@@ -397,7 +424,7 @@ __global__ void __launch_bounds__(kThreads, 2) lc_up_kernel(const __grid_constan
   // the fine levels (gr..L-1) of the whole batch are ready once every CTA got here
   __syncthreads();
   LC_TS(0, 4);
-  if (tid == 0) {
+  if (tid == 0 && !P.noflags) {
     const int total = int(gridDim.x * gridDim.y);
     if (atom_add_acq_rel(&P.flags[0], 1) == total - 1) {
       atomicExch(&P.flags[0], 0);
@@ -453,7 +480,7 @@ __global__ void __launch_bounds__(kThreads, 2) lc_up_kernel(const __grid_constan
     node = grp;
     LC_TS(0, 6);
   }
-  if (P.gr > 0) {  // this CTA produced one of the 4 level-0 nodes of its vector tile
+  if (P.gr > 0 && !P.noflags) {  // this CTA produced one of the 4 level-0 nodes of its vector tile
     __syncthreads();
     if (tid == 0) {
       const int total = 4 * int(gridDim.y);
@@ -466,6 +493,191 @@ __global__ void __launch_bounds__(kThreads, 2) lc_up_kernel(const __grid_constan
   LC_TS(0, 7);
 }
 
+
+// one M2M of a pair of siblings held apart: out[sigma][v] = B(0) left[sigma][v] + B(1) right[sigma][v]
+// (rows r = (sigma, v) of [2][VT][M], the same row-group split as m2m_level)
+template <int VT>
+__device__ __forceinline__ void m2m_pair(const double* __restrict__ Bs, const double* __restrict__ left,
+                                         const double* __restrict__ right, double* __restrict__ out) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wpr = (blockDim.x >> 5) / 3;
+  if (warp >= 3 * wpr) return;
+  const int rg = warp % 3;
+  for (int r = (warp / 3) * 32 + lane; r < 2 * VT; r += wpr * 32) {
+    const double* x0 = left + r * kM;
+    const double* x1 = right + r * kM;
+    double* o = out + r * kM;
+    if (rg == 0)
+      m2m_rows<0, 10>(Bs, x0, x1, o);
+    else if (rg == 1)
+      m2m_rows<10, 15>(Bs, x0, x1, o);
+    else
+      m2m_rows<15, 18>(Bs, x0, x1, o);
+  }
+}
+
+// Engine 3's upward pass (steps 1-2 of Alg. 4 for batches of long vectors), persistent: CTA b takes
+// chunks b, b + grid, ... of 2^kc consecutive subtrees (2^k leaf segments x 8 vectors each) and walks
+// their subtrees left to right with the f of the next subtree staged (cp.async, double buffer) while
+// the current one computes.  A subtree root that is a left child waits in shared memory for its
+// sibling; each merge (step 2) stores the parent's w at once, so the chunk root (level gr - kc) is
+// reached inside the CTA.  Above it the arrival counters of lc_up_kernel merge groups of 2^G chunk
+// roots (the last arriver continues).  No flags: the range kernel waits for the whole grid.
+__global__ void __launch_bounds__(kThreads, 2) lc_up3_kernel(const __grid_constant__ UpArgs<32> A) {
+  constexpr int VT = 8, SMAX = 32;
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ int s_last;
+  const UpParams& P = A.p;
+  const int s = P.s, k = P.k, fst = P.fstride, tid = threadIdx.x;
+  const int nleaf = 1 << k, seglen = 2 * s;
+  const int64_t VM = int64_t(VT) * kM;
+  const int64_t fbuf = align_up((int64_t(VT) * nleaf * fst + 2 * SMAX) * 8, 128) / 8;  // doubles per f buffer
+  double* Ts = reinterpret_cast<double*>(smem);  // [2][SMAX][M], zero rows m >= s
+  double* Bs = Ts + 2 * SMAX * kM;               // B(0) [M][M]
+  double* fs0 = reinterpret_cast<double*>(smem + up_const_bytes(SMAX));  // 2 x [v][leaf][fst] + zero tail
+  double* tree = fs0 + 2 * fbuf;
+  auto tree_off = [&](int j) { return ((1 << j) - 1) * 2 * VT * kM; };
+  double* pend = tree + tree_off(k + 1);  // [kc][2][VT][M]: left siblings waiting, by level
+  double* cur = pend + P.kc * 2 * VM;     // [2][2][VT][M]: merged parents (ping-pong)
+
+  for (int i = tid; i < SMAX * kM; i += blockDim.x) cp_async16(Ts + 2 * i, P.Tpad + 2 * i);
+  for (int i = tid; i < kMM / 2; i += blockDim.x) cp_async16(Bs + 2 * i, P.B + 2 * i);
+  for (int b = 0; b < 2; ++b) {  // zero tail and segment padding of both buffers (never written by cp.async)
+    double* fs = fs0 + b * fbuf;
+    for (int x = tid; x < 2 * SMAX; x += blockDim.x) fs[VT * nleaf * fst + x] = 0.0;
+    if (fst > seglen)
+      for (int x = tid; x < VT * nleaf; x += blockDim.x) *reinterpret_cast<double2*>(fs + x * fst + seglen) = make_double2(0.0, 0.0);
+  }
+  cp_async_commit();
+  griddep_wait();  // the input may be produced by the preceding kernel; w of the previous execution is free
+  griddep_launch();
+
+  const int nb = 1 << P.kc;
+  const int groot = P.gr - P.kc;                   // level of the chunk roots
+  const int64_t cpt = int64_t(4) << groot;         // chunks per tile
+  const int64_t nchunks = cpt * P.ntiles;
+  const int64_t mych = blockIdx.x < nchunks ? (nchunks - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int64_t J = mych * nb;
+  auto locate = [&](int64_t j, int64_t& tile, int64_t& R) {
+    const int64_t it = blockIdx.x + (j >> P.kc) * int64_t(gridDim.x);
+    tile = it / cpt;
+    R = (it - tile * cpt) * nb + (j & (nb - 1));
+  };
+  // VEC layout, 16-byte aligned rows: thread t stages the pair (leaf t / s, x = 2 (t % s)) of every
+  // vector (nleaf s <= 8 x 32 = 256 threads), so the addressing is computed once
+  const bool fast = P.layout == LC_VEC_CONTIGUOUS && P.vec16 && nleaf * s <= int(blockDim.x);
+  const int my_lf = tid / s, my_x = 2 * (tid - (tid / s) * s);
+  const bool my_on = tid < nleaf * s;
+  const int my_so = my_lf * fst + my_x, my_jj = my_lf * seglen + my_x;
+  auto stage = [&](double* fs, int64_t R, int64_t tile) {
+    if (!fast) {
+      up_stage<VT>(P, fs, R, tile, nleaf, fst);
+      return;
+    }
+    if (!my_on) return;
+    const int64_t j0 = R * int64_t(nleaf * seglen) + my_jj;
+    const double* src = P.in + tile * VT * P.ld_in + j0;
+#pragma unroll
+    for (int v = 0; v < VT; ++v) {
+      const int64_t rem = (tile * VT + v < P.batch) ? P.n - j0 : 0;
+      const uint32_t bytes = rem >= 2 ? 16u : (rem == 1 ? 8u : 0u);
+      cp_async16z(fs + v * nleaf * fst + my_so, bytes ? src + v * P.ld_in : P.in, bytes);
+    }
+  };
+  if (J > 0) {
+    int64_t t0, r0;
+    locate(0, t0, r0);
+    stage(fs0, r0, t0);
+  }
+  cp_async_commit();
+  for (int64_t j = 0; j < J; ++j) {
+    int64_t tile, R;
+    locate(j, tile, R);
+    if (j + 1 < J) {
+      int64_t t1, r1;
+      locate(j + 1, t1, r1);
+      stage(fs0 + ((j + 1) & 1) * fbuf, r1, t1);
+    }
+    cp_async_commit();
+    cp_async_wait<1>();  // the f of subtree j landed
+    __syncthreads();
+    up_step1<VT, SMAX>(Ts, fs0 + (j & 1) * fbuf, fst, nleaf, s, tree + tree_off(k));
+    __syncthreads();
+    double* wt = P.w + tile * P.w_tile;
+    auto store_w = [&](int g, int64_t node, int cnt, const double* src) {  // cnt nodes of level g, [sigma][cnt][v][M]
+      const int c2 = int(cnt * VM / 2);
+      const double2* sp = reinterpret_cast<const double2*>(src);
+      double2* d0 = reinterpret_cast<double2*>(wt + (w_level_offset_units(g) + node) * VM);
+      double2* d1 = reinterpret_cast<double2*>(wt + (w_level_offset_units(g) + nseg(g) + node) * VM) - c2;
+#pragma unroll 4
+      for (int i = tid; i < 2 * c2; i += blockDim.x) {
+        const double2 x2 = sp[i];
+        (i < c2 ? d0 : d1)[i] = x2;
+      }
+    };
+    store_w(P.gr + k, R << k, nleaf, tree + tree_off(k));
+    for (int lv = k; lv >= 1; --lv) {
+      m2m_level<VT>(Bs, tree + tree_off(lv), tree + tree_off(lv - 1), lv - 1);
+      __syncthreads();
+      store_w(P.gr + lv - 1, R << (lv - 1), 1 << (lv - 1), tree + tree_off(lv - 1));
+    }
+    // merge with the waiting left siblings while this node is a right child inside the chunk
+    int g = P.gr;
+    int64_t u = R;
+    const double* x = tree;  // [2][VT][M]
+    int pp = 0;
+    while (g > groot && (u & 1)) {
+      double* o = cur + pp * 2 * VM;
+      m2m_pair<VT>(Bs, pend + (g - groot - 1) * 2 * VM, x, o);
+      __syncthreads();
+      --g;
+      u >>= 1;
+      store_w(g, u, 1, o);
+      x = o;
+      pp ^= 1;
+    }
+    if (g > groot) {  // a left child: wait for the sibling
+      double* d = pend + (g - groot - 1) * 2 * VM;
+      for (int i = tid; i < 2 * VM; i += blockDim.x) d[i] = x[i];
+      __syncthreads();
+      continue;
+    }
+    // chunk root (level groot, node u) written: upward continuation across chunks, as lc_up_kernel
+    int64_t node = u;
+    while (g > 0) {
+      const int ge = min(P.G, g);
+      const int64_t grp = node >> ge;
+      __syncthreads();
+      if (tid == 0) {
+        int* c = P.cnt + tile * P.cnt_tile + (nseg(g) - 4) + grp;
+        const int old = atom_add_acq_rel(c, 1);
+        const int last = (old == (1 << ge) - 1);
+        if (last) atomicExch(c, 0);  // self-reset for the next launch
+        s_last = last;
+      }
+      __syncthreads();
+      if (!s_last) break;
+      __threadfence();
+      const int cnt2 = int((int64_t(1) << ge) * VM / 2);
+      for (int sg = 0; sg < 2; ++sg) {
+        const double2* src =
+            reinterpret_cast<const double2*>(wt + (w_level_offset_units(g) + sg * nseg(g) + (grp << ge)) * VM);
+        double2* dst = reinterpret_cast<double2*>(tree + tree_off(ge) + sg * 2 * cnt2);
+        for (int i = tid; i < cnt2; i += blockDim.x) dst[i] = __ldcg(src + i);
+      }
+      __syncthreads();
+      for (int lv = ge; lv >= 1; --lv) {
+        m2m_level<VT>(Bs, tree + tree_off(lv), tree + tree_off(lv - 1), lv - 1);
+        __syncthreads();
+      }
+      for (int lv = 0; lv < ge; ++lv) store_w(g - ge + lv, grp << lv, 1 << lv, tree + tree_off(lv));
+      g -= ge;
+      node = grp;
+    }
+    __syncthreads();  // the tree is free for the next subtree
+  }
+  cp_async_wait<0>();
+}
 
 // ============================================================== streaming kernel
 constexpr int kM2lWarps = 3;   // consumer warps applying M2L to the A_hat ring
@@ -2149,6 +2361,7 @@ lc_status configure_kernels(lc_plan* p) {
     if (ea == cudaSuccess) ea = set_attrs_all<64>(smax);
     if (ea == cudaSuccess) ea = set_max_dyn_smem(lc_tile_kernel<0>, smax);
     if (ea == cudaSuccess) ea = set_max_dyn_smem(lc_tile_kernel<1>, smax);
+    if (ea == cudaSuccess) ea = set_max_dyn_smem(lc_up3_kernel, smax);
     if (ea == cudaSuccess) ea = set_max_dyn_smem(lc_range_kernel<0>, smax);
     if (ea == cudaSuccess) ea = set_max_dyn_smem(lc_range_kernel<1>, smax);
     if (ea != cudaSuccess) return record_cuda_error(ea);
@@ -2280,6 +2493,28 @@ lc_status configure_kernels(lc_plan* p) {
       p->range_len = int(rlen);
       p->smem_tile = rsm;
       p->tile_grid = int(std::min<int64_t>(p->ntiles * nr, slots));
+      // persistent up pass: subtrees of 2^kup leaves (two CTAs per SM), chunks of 2^kc subtrees
+      {
+        int ku = std::max(0, std::min(p->kup, 3));
+        int kc = std::min(6, L - 1 - ku);
+        while (ku > 0 && up3_smem_bytes(ku, s, kc) > budget2) {
+          --ku;
+          kc = std::min(6, L - 1 - ku);
+        }
+        if (up3_smem_bytes(ku, s, kc) > smax) return LC_ERR_INVALID_ARG;
+        p->kup = ku;
+        p->grup = L - 1 - ku;
+        p->group = std::max(ku, 1);
+        p->up3_kc = kc;
+        p->smem_up = size_t(up3_smem_bytes(ku, s, kc));
+        int uocc = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&uocc, lc_up3_kernel, kThreads, p->smem_up);
+        if (uocc < 1) return LC_ERR_INVALID_ARG;
+        const int64_t nch = p->ntiles * ((int64_t(4) << p->grup) >> kc);
+        const int64_t uslots = int64_t(uocc) * p->sm_count;
+        const int64_t per = (nch + uslots - 1) / uslots;
+        p->up3_grid = (nch + per - 1) / per;
+      }
       p->ws_range_off = align_up(int64_t(p->ws_bytes), 256);
       p->ws_bytes = size_t(p->ws_range_off + int64_t(p->tile_grid) * range_scratch_doubles(L) * 8 + 256);
       return LC_OK;
@@ -2419,6 +2654,9 @@ lc_status launch_execute(const lc_plan* p, const double* in, double* out, void* 
   up.layout = p->layout; up.L = int(p->L); up.s = int(p->s); up.k = p->kup; up.gr = p->grup; up.G = p->group;
   up.fstride = up_fstride(int(p->s));
   up.vec16 = (reinterpret_cast<uintptr_t>(in) % 16 == 0) && (p->ld_in % 2 == 0) ? 1 : 0;
+  up.noflags = p->engine == 3 ? 1 : 0;
+  up.kc = p->up3_kc;
+  up.ntiles = p->ntiles;
   up.w = w; up.cnt = cnt; up.flags = flags; up.w_tile = p->w_tile_doubles; up.cnt_tile = p->cnt_tile_ints;
   StreamParams sp{};
   sp.A = p->d_A; sp.w = w; sp.c = c; sp.in = in; sp.out = out; sp.tabA = p->d_tabA; sp.tabB = p->d_tabB;
@@ -2455,14 +2693,13 @@ lc_status launch_execute(const lc_plan* p, const double* in, double* out, void* 
     cfg.numAttrs = 1;
     int evi = 0;
     if (ev && nev > 0) cudaEventRecord(ev[evi++], st);
-    cfg.gridDim = grid_up;
-    const bool small_up = int64_t(grid_up.x) * grid_up.y > 8 * p->sm_count && p->smem_up <= 56 * 1024;
-    cfg.blockDim = dim3(small_up ? kThreads / 2 : kThreads);
+    cfg.gridDim = dim3(unsigned(p->up3_grid));
+    cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = p->smem_up;
     cudaError_t e = cudaSuccess;
     UpArgs<32> ua;
     ua.p = up;
-    e = cudaLaunchKernelEx(&cfg, lc_up_kernel<8, 32>, ua);
+    e = cudaLaunchKernelEx(&cfg, lc_up3_kernel, ua);
     if (e == cudaSuccess && ev && evi < nev) cudaEventRecord(ev[evi++], st);
     if (e == cudaSuccess) {
       cfg.gridDim = dim3(unsigned(p->tile_grid));
@@ -2485,7 +2722,7 @@ lc_status launch_execute(const lc_plan* p, const double* in, double* out, void* 
 
 extern "C" lc_status lc_plan_kernel_info(const lc_plan* p, int64_t* out, int32_t count, int32_t* written) {
   if (!p || !out) return LC_ERR_INVALID_ARG;
-  const int64_t up_grid = p->L > 0 ? (int64_t(4) << p->grup) * p->ntiles : 0;
+  const int64_t up_grid = p->engine == 3 ? p->up3_grid : (p->L > 0 ? (int64_t(4) << p->grup) * p->ntiles : 0);
   const int64_t v[] = {p->stream_grid, int64_t(p->smem_stream), int64_t(p->smem_up), p->kup, p->grup, p->kb,
                        p->bps, p->nst, p->vt, p->stream_occ, p->m2l_units, p->band_units, up_grid, p->k,
                        int64_t(p->smem_down), p->engine, p->tile_grid, int64_t(p->smem_tile), p->range_n, p->range_len};

@@ -94,11 +94,11 @@ __host__ __device__ inline int64_t down_smem_bytes(int VT, int kd, int s, int L)
 // 16-byte reads of 32 consecutive leaves hit distinct bank quads
 __host__ __device__ inline int up_fstride(int s) { return (2 * s) % 4 == 2 ? 2 * s : 2 * s + 2; }
 
-constexpr int64_t kUpConstBytes = 21248;  // T(sigma) [2][<=64][M] and B(0) in shared memory, 128-byte aligned
-static_assert(kUpConstBytes >= (2 * 64 * kM + kMM) * 8 && kUpConstBytes % 128 == 0, "up-kernel constants");
+// T(sigma) [2][SMAX][M] and B(0) in shared memory, 128-byte aligned (SMAX = 32 for s <= 32, else 64)
+__host__ __device__ constexpr int64_t up_const_bytes(int smax) { return ((2 * smax * kM + kMM) * 8 + 127) / 128 * 128; }
 
 __host__ __device__ inline int64_t up_smem_bytes(int VT, int k, int s) {
-  int64_t o = kUpConstBytes;
+  int64_t o = up_const_bytes(s <= 32 ? 32 : 64);
   o = align_up(o + (int64_t(VT) * (int64_t(1) << k) * up_fstride(s) + 2 * 64) * 8, 128);  // f tile + zero tail
   o = align_up(o + ((int64_t(2) << k) - 1) * 2 * VT * kM * 8, 128);          // w tree
   o += 16;
@@ -128,6 +128,8 @@ struct lc_plan {
   size_t smem_tile;
   int range_n, range_len;   // engine 3: leaf ranges per tile and their length
   int64_t ws_range_off;     // engine 3: byte offset of the per-CTA scratch in the workspace
+  int up3_kc;               // engine 3: subtrees per chunk of the persistent up pass = 2^up3_kc
+  int64_t up3_grid;         // engine 3: CTAs of the persistent up pass
   size_t smem_stream;
   int64_t ntiles;
   int64_t w_tile_doubles, cnt_tile_ints;
@@ -155,4 +157,14 @@ lc_status record_cuda_error(cudaError_t e);
 lc_status launch_execute(const lc_plan* p, const double* in, double* out, void* ws, cudaStream_t st,
                          cudaEvent_t const* ev, int nev);
 int64_t band_nnz(int64_t N, int64_t s);
+// engine 3's persistent up pass (lc_up3_kernel, 8 vectors, s <= 32): constants, two f buffers,
+// the subtree tree, kc waiting left siblings and two merged parents
+__host__ __device__ inline int64_t up3_smem_bytes(int k, int s, int kc) {
+  int64_t o = up_const_bytes(32);
+  o += 2 * align_up((int64_t(8) * (int64_t(1) << k) * up_fstride(s) + 2 * 32) * 8, 128);
+  o += ((int64_t(2) << k) - 1) * 2 * 8 * kM * 8;
+  o += int64_t(kc + 2) * 2 * 8 * kM * 8;
+  return o + 16;
+}
+
 }  // namespace lc
