@@ -1725,10 +1725,11 @@ __global__ void __launch_bounds__(kTileThreads, LC_TILE_MINB) lc_tile_kernel(con
               band32<DIR, 0, 3>(fa, fb, lamw, tap, i0, sg, lc, lr, acc);
             else
               band32<DIR, 1, 2>(fa, fb, lamw, tap, i0, sg, lc, lr, acc);
-          } else if ((s & 7) == 0) {  // fast path: row tiles full, chunk boundary = segment boundary
+          } else if ((s & 3) == 0) {  // fast path: chunk boundary = segment boundary (rows >= s masked)
             const double* lamw = lw + sg + lr + lc;  // lambda[(i+j)/2 - 2sU] = lamw[8 rb + 4 kc]
             const double* tap = taq + lc - lr;       // a[c - r] = tap[4 kc - 8 rb]
             const int nkc = seglen >> 2, s4 = s >> 2;
+            const bool rok0 = 8 * rlo + lr < s, rok1 = 8 * rhi + lr < s;
             for (int kc = 2 * rlo; kc < nkc; ++kc) {
               const int c = 4 * kc + lc;
               double b = kc < s4 ? fU[c] : fU1[c - s];
@@ -1736,13 +1737,13 @@ __global__ void __launch_bounds__(kTileThreads, LC_TILE_MINB) lc_tile_kernel(con
               {
                 const int d = 4 * kc - 8 * rlo;
                 double a = tap[d] * lamw[8 * rlo + 4 * kc];
-                if (d < 8 && lc + d < lr) a = 0.0;  // c < r inside the diagonal block
+                if ((d < 8 && lc + d < lr) || !rok0) a = 0.0;  // c < r inside the diagonal block
                 dmma(acc[0], a, b);
               }
               if (hion && kc >= 2 * rhi) {
                 const int d = 4 * kc - 8 * rhi;
                 double a = tap[d] * lamw[8 * rhi + 4 * kc];
-                if (d < 8 && lc + d < lr) a = 0.0;
+                if ((d < 8 && lc + d < lr) || !rok1) a = 0.0;
                 dmma(acc[1], a, b);
               }
             }
@@ -2110,10 +2111,11 @@ __global__ void __launch_bounds__(kTileThreads, LC_RANGE_MINB) lc_range_kernel(c
               band32<DIR, 0, 3>(fa, fb, lamw, tap, i0, sg, lc, lr, acc);
             else
               band32<DIR, 1, 2>(fa, fb, lamw, tap, i0, sg, lc, lr, acc);
-          } else if ((s & 7) == 0) {  // fast path: row tiles full, chunk boundary = segment boundary
+          } else if ((s & 3) == 0) {  // fast path: chunk boundary = segment boundary (rows >= s masked)
             const double* lamw = lw + sg + lr + lc;  // lambda[(i+j)/2 - 2sU] = lamw[8 rb + 4 kc]
             const double* tap = taq + lc - lr;       // a[c - r] = tap[4 kc - 8 rb]
             const int nkc = seglen >> 2, s4 = s >> 2;
+            const bool rok0 = 8 * rlo + lr < s, rok1 = 8 * rhi + lr < s;
             for (int kc = 2 * rlo; kc < nkc; ++kc) {
               const int c = 4 * kc + lc;
               double b = kc < s4 ? fU[c] : fU1[c - s];
@@ -2121,13 +2123,13 @@ __global__ void __launch_bounds__(kTileThreads, LC_RANGE_MINB) lc_range_kernel(c
               {
                 const int d = 4 * kc - 8 * rlo;
                 double a = tap[d] * lamw[8 * rlo + 4 * kc];
-                if (d < 8 && lc + d < lr) a = 0.0;  // c < r inside the diagonal block
+                if ((d < 8 && lc + d < lr) || !rok0) a = 0.0;  // c < r inside the diagonal block
                 dmma(acc[0], a, b);
               }
               if (hion && kc >= 2 * rhi) {
                 const int d = 4 * kc - 8 * rhi;
                 double a = tap[d] * lamw[8 * rhi + 4 * kc];
-                if (d < 8 && lc + d < lr) a = 0.0;
+                if ((d < 8 && lc + d < lr) || !rok1) a = 0.0;
                 dmma(acc[1], a, b);
               }
             }

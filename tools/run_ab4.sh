@@ -2,7 +2,7 @@
 cp paper_2411_00033_b200/liblegcheb.so /tmp/lib_keep.so
 for v in $VARIANTS; do
   cp exp/lib_$v.so paper_2411_00033_b200/liblegcheb.so
-  timeout 300 python -m pytest tests/test_gpu_tile.py -q -x -k range 2>&1 | tail -1
+  timeout 300 python -m pytest tests/test_gpu_tile.py tests/test_gpu_engines_sweep.py -q -x 2>&1 | tail -1
   timeout 600 python bench.py --config cfg4 --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 3 > gpurun_out/ab.json 2>gpurun_out/ab.err
   python -c "
 import json; d=json.load(open('gpurun_out/ab.json'))
