@@ -1587,10 +1587,11 @@ template <int DIR, int RLO, int RHI>
 __device__ __forceinline__ void band32(const double* __restrict__ fU, const double* __restrict__ fU1,
                                        const double* __restrict__ lamw, const double* __restrict__ tap,
                                        int64_t i0, int sg, int lc, int lr, double (&acc)[2][2]) {
+  const double jb = double(i0 + 2 * lc + sg);  // C2L column weight j = jb + 8 kc (exact integers)
 #pragma unroll
   for (int kc = 2 * RLO; kc < 16; ++kc) {
     double b = kc < 8 ? fU[4 * kc] : fU1[4 * kc - 32];
-    if (DIR == 1) b *= double(i0 + 2 * (4 * kc + lc) + sg);
+    if (DIR == 1) b *= jb + double(8 * kc);
     {
       constexpr int dummy = 0;
       (void)dummy;
@@ -1730,10 +1731,11 @@ __global__ void __launch_bounds__(kTileThreads, LC_TILE_MINB) lc_tile_kernel(con
             const double* tap = taq + lc - lr;       // a[c - r] = tap[4 kc - 8 rb]
             const int nkc = seglen >> 2, s4 = s >> 2;
             const bool rok0 = 8 * rlo + lr < s, rok1 = 8 * rhi + lr < s;
-            for (int kc = 2 * rlo; kc < nkc; ++kc) {
+            double jw = double(i0 + 2 * (8 * rlo + lc) + sg);  // C2L column weight j (exact integers)
+            for (int kc = 2 * rlo; kc < nkc; ++kc, jw += 8.0) {
               const int c = 4 * kc + lc;
               double b = kc < s4 ? fU[c] : fU1[c - s];
-              if (DIR == 1) b *= double(i0 + 2 * c + sg);
+              if (DIR == 1) b *= jw;
               {
                 const int d = 4 * kc - 8 * rlo;
                 double a = tap[d] * lamw[8 * rlo + 4 * kc];
@@ -1749,10 +1751,11 @@ __global__ void __launch_bounds__(kTileThreads, LC_TILE_MINB) lc_tile_kernel(con
             }
           } else {  // general s: masks on rows, columns and the segment boundary
             const int nkc = (seglen + 3) >> 2;
-            for (int kc = 2 * rlo; kc < nkc; ++kc) {
+            double jw = double(i0 + 2 * (8 * rlo + lc) + sg);  // C2L column weight j (exact integers)
+            for (int kc = 2 * rlo; kc < nkc; ++kc, jw += 8.0) {
               const int c = 4 * kc + lc;
               double b = c < s ? fU[c] : (c < seglen ? fU1[c - s] : 0.0);
-              if (DIR == 1) b *= double(i0 + 2 * c + sg);
+              if (DIR == 1) b *= jw;
 #pragma unroll
               for (int q = 0; q < 2; ++q) {
                 const int rb = q ? rhi : rlo;
@@ -2116,10 +2119,11 @@ __global__ void __launch_bounds__(kTileThreads, LC_RANGE_MINB) lc_range_kernel(c
             const double* tap = taq + lc - lr;       // a[c - r] = tap[4 kc - 8 rb]
             const int nkc = seglen >> 2, s4 = s >> 2;
             const bool rok0 = 8 * rlo + lr < s, rok1 = 8 * rhi + lr < s;
-            for (int kc = 2 * rlo; kc < nkc; ++kc) {
+            double jw = double(i0 + 2 * (8 * rlo + lc) + sg);  // C2L column weight j (exact integers)
+            for (int kc = 2 * rlo; kc < nkc; ++kc, jw += 8.0) {
               const int c = 4 * kc + lc;
               double b = kc < s4 ? fU[c] : fU1[c - s];
-              if (DIR == 1) b *= double(i0 + 2 * c + sg);
+              if (DIR == 1) b *= jw;
               {
                 const int d = 4 * kc - 8 * rlo;
                 double a = tap[d] * lamw[8 * rlo + 4 * kc];
@@ -2135,10 +2139,11 @@ __global__ void __launch_bounds__(kTileThreads, LC_RANGE_MINB) lc_range_kernel(c
             }
           } else {  // general s: masks on rows, columns and the segment boundary
             const int nkc = (seglen + 3) >> 2;
-            for (int kc = 2 * rlo; kc < nkc; ++kc) {
+            double jw = double(i0 + 2 * (8 * rlo + lc) + sg);  // C2L column weight j (exact integers)
+            for (int kc = 2 * rlo; kc < nkc; ++kc, jw += 8.0) {
               const int c = 4 * kc + lc;
               double b = c < s ? fU[c] : (c < seglen ? fU1[c - s] : 0.0);
-              if (DIR == 1) b *= double(i0 + 2 * c + sg);
+              if (DIR == 1) b *= jw;
 #pragma unroll
               for (int q = 0; q < 2; ++q) {
                 const int rb = q ? rhi : rlo;
