@@ -639,8 +639,7 @@ __global__ void __launch_bounds__(kThreads, 2) lc_up3_kernel(const __grid_consta
     if (g > groot) {  // a left child: wait for the sibling
       double* d = pend + (g - groot - 1) * 2 * VM;
       for (int i = tid; i < 2 * VM; i += blockDim.x) d[i] = x[i];
-      __syncthreads();
-      continue;
+      continue;  // (the barrier at the top of the next subtree orders these copies before any reuse)
     }
     // chunk root (level groot, node u) written: upward continuation across chunks, as lc_up_kernel
     int64_t node = u;
@@ -674,7 +673,6 @@ __global__ void __launch_bounds__(kThreads, 2) lc_up3_kernel(const __grid_consta
       g -= ge;
       node = grp;
     }
-    __syncthreads();  // the tree is free for the next subtree
   }
   cp_async_wait<0>();
 }
