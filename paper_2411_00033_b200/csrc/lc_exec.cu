@@ -18,8 +18,9 @@
 //                    step 7 (C^{-1}) added to the band result and stored.
 // Engine 2 (batches of short vectors): lc_tile_kernel, one CTA per 8-vector tile, the whole
 //   algorithm in one right-to-left pass over the leaf segments with every intermediate on chip.
-// Engine 3 (batches of long vectors): lc_up_kernel with 8-vector tiles, then lc_range_kernel, the
-//   same pass over ranges of leaves of each tile with w read from the workspace.
+// Engine 3 (batches of long vectors): lc_up3_kernel (persistent, double-buffered steps 1-2 over chunks
+//   of 8-vector subtrees; writes w of every level), then lc_range_kernel, the same pass as engine 2
+//   over ranges of leaves of each tile with w read from the workspace.
 #include <algorithm>
 #include <cstdio>
 #include <cstring>
@@ -1992,7 +1993,7 @@ __global__ void __launch_bounds__(kTileThreads, LC_TILE_MINB) lc_tile_kernel(con
   }
 }
 
-// Engine 3 (batches of long vectors, few tiles): the up kernel writes w of every level, then this
+// Engine 3 (batches of long vectors, few tiles): lc_up3_kernel writes w of every level, then this
 // kernel runs the per-tile right-to-left pass over a RANGE of leaves of a tile (ranges x tiles fill
 // the GPU): steps 3-7 exactly as in lc_tile_kernel, with w read from the workspace, the step-4 chain
 // started at the range's rightmost leaf from the top level down, and the c of the levels below L-2 in

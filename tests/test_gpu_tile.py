@@ -166,3 +166,29 @@ def test_range_engine_automatic_choice():
     assert q.kernel_info["engine"] == 1
     with pytest.raises(RuntimeError):
         _plan(100000, "leg2cheb", batch=8, device=dev, engine=4)
+
+
+def test_range_engine_staging_paths_and_continuation():
+    # n = 300000: L = 12, s = 19 (general band path), chunk roots on level 2 -> cross-chunk continuation
+    # of the persistent up pass; V = 9: a ragged second tile; an odd ld_in forces the 8-byte staging path,
+    # the batch layout the strided one: all three must agree bit for bit
+    dev = _dev()
+    n, V = 300000, 9
+    x = batch("normal_exp1000", n, V, seed=14)
+    rows = np.unique(np.concatenate([np.arange(48), n - 1 - np.arange(48), np.random.default_rng(3).integers(0, n, 96)]))
+    for direction in ("leg2cheb", "cheb2leg"):
+        p = _plan(n, direction, batch=V, device=dev, engine=3)
+        assert p.kernel_info["engine"] == 3
+        z = p.execute(x.to(dev))
+        xin = torch.zeros(V, n + 1, dtype=torch.float64)
+        xin[:, :n] = x
+        po = _plan(n, direction, batch=V, device=dev, engine=3, ld_in=n + 1)
+        zo = po.execute(xin.to(dev))
+        pb = _plan(n, direction, batch=V, device=dev, engine=3, layout="batch")
+        zb = pb.execute(x.t().contiguous().to(dev))
+        assert torch.equal(z, zo)
+        assert torch.equal(z, zb.t().contiguous())
+        zc = z.cpu().numpy()
+        for v in (0, V - 1):
+            e = oracle.einf(zc[v][rows], oracle.transform_rows(direction, x[v].numpy(), rows))
+            assert e <= GATE, (direction, v, e)

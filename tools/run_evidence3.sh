@@ -20,4 +20,4 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpuru
 ncu --set full --clock-control none --import-source on -k regex:"lc_(up|stream|down)_kernel" -s 6 -c 3 -o gpurun_out/prof_cfg2 -f python bench.py $ARGS > gpurun_out/ncu_f2.log 2>&1; echo f2 rc=$?
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_cfg3.csv python bench.py --config cfg3 $ARGS > gpurun_out/ncu_l3.log 2>&1; echo l3 rc=$?
 ncu --set full --clock-control none --import-source on -k regex:"lc_tile_kernel" -s 2 -c 1 -o gpurun_out/prof_cfg3 -f python bench.py --config cfg3 $ARGS > gpurun_out/ncu_f3.log 2>&1; echo f3 rc=$?
-ncu --set full --clock-control none --import-source on -k regex:"lc_range_kernel" -s 1 -c 1 -o gpurun_out/prof_cfg4 -f python bench.py --config cfg4 --steps 1 --warmup 3 --no-cpu-baseline --no-graph --e2e-steps 3 > gpurun_out/ncu_f4.log 2>&1; echo f4 rc=$?
+ncu --set full --clock-control none --import-source on -k regex:"lc_(up3|range)_kernel" -s 2 -c 2 -o gpurun_out/prof_cfg4 -f python bench.py --config cfg4 --steps 1 --warmup 3 --no-cpu-baseline --no-graph --e2e-steps 3 > gpurun_out/ncu_f4.log 2>&1; echo f4 rc=$?
