@@ -101,12 +101,17 @@ class Plan:
     def kernels_per_execute(self) -> int:
         return int(self.desc["kernels_per_execute"])
 
-    def _shape(self):
-        return (self.batch, self.ld_in) if self.layout == 0 else (self.n, self.ld_in)
+    def _shape(self, ld=None):
+        ld = self.ld_in if ld is None else ld
+        return (self.batch, ld) if self.layout == 0 else (self.n, ld)
 
     def _check(self, x: torch.Tensor, what: str):
         if x.device != self.device or x.dtype != torch.float64 or not x.is_contiguous():
             raise ValueError(f"{what}: need a contiguous float64 tensor on {self.device}")
+        ld = self.ld_in if what == "input" else self.ld_out
+        rows, cols = (self.batch, self.n) if self.layout == 0 else (self.n, self.batch)
+        if x.numel() < (rows - 1) * ld + cols:  # the extent the kernels address (rows of stride ld)
+            raise ValueError(f"{what}: {x.numel()} elements, the plan addresses {(rows - 1) * ld + cols}")
 
     def new_workspace(self, stream=None) -> torch.Tensor:
         ws = torch.empty(max(1, self.workspace_bytes), dtype=torch.uint8, device=self.device)
@@ -120,7 +125,7 @@ class Plan:
         """out = transform(x) on the device; x is [batch, n] (vec layout) or [n, batch] (batch layout)."""
         self._check(x, "input")
         if out is None:
-            out = torch.empty_like(x)
+            out = torch.empty(self._shape(self.ld_out), dtype=torch.float64, device=self.device)
         self._check(out, "output")
         ws = ctypes.c_void_p(workspace.data_ptr()) if workspace is not None else ctypes.c_void_p()
         _lib.check("lc_execute", self._lib.lc_execute(self._h, ctypes.c_void_p(x.data_ptr()),
