@@ -1,5 +1,6 @@
 """Per-warp cycle accounting of the per-tile kernel (debug build liblegcheb_dbg.so): role work,
-M2L jobs, end-of-step wait, averaged over CTAs, per leaf step.  usage: python tools/tile_roles.py n batch"""
+M2L jobs, end-of-step wait, averaged over CTAs, per leaf step (engine 2, or 3 for the range kernel).
+usage: python tools/tile_roles.py n batch [engine]"""
 import ctypes
 import sys
 
@@ -13,9 +14,10 @@ from paper_2411_00033_b200 import Plan  # noqa: E402
 from lc_inputs import batch as mkbatch  # noqa: E402
 
 n, V = int(sys.argv[1]), int(sys.argv[2])
+engine = int(sys.argv[3]) if len(sys.argv) > 3 else 2
 dev = torch.device("cuda", 0)
 x = mkbatch("normal", n, V, seed=1).to(dev)
-p = Plan(n, "leg2cheb", batch=V, device=dev, engine=2)
+p = Plan(n, "leg2cheb", batch=V, device=dev, engine=engine)
 lib = _lib.load()
 lib.lc_debug_timestamps.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_ulonglong), ctypes.c_longlong]
 for _ in range(3):
