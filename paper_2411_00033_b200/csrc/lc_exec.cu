@@ -1936,47 +1936,49 @@ __global__ void __launch_bounds__(kTileThreads, LC_TILE_MINB) lc_tile_kernel(con
           }
         }
         TP_MARK(1);
-        // ---- step 3 for the rows the next leaf enters: job k = (level gN + k/2, sigma k&1) on warp
-        // 6, 7, 4, 5, 6, ...: c(u') = sum_r A_hat_r w(t_r)
-        if (U >= 1) {
-          const int gN = gmin_of(U - 1);
-          const int nm2l = (L - gN) * 2;
-          for (int k = (warp - 6) & 3; k < nm2l; k += 4) {
-            const int g = gN + (k >> 1), sgk = k & 1;
-            const int u = (U - 1) >> (L - 1 - g);
-            double acc[3][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
-            if (u < (4 << g) - 2) {
-              const int b = u >> 1, p = u & 1;
-              for (int mi = 0; mi < (p ? 1 : 2); ++mi) {
-                const int r = p ? 2 : mi;
-                const int t = u + 2 + (p ? 0 : mi);
-                const double* Am = P.A + (ahat_level_offset(g) + 3 * int64_t(b) + r) * kMM;
-                const double* W = wslot(g, t) + sgk * kTS;
-                double av[3][5];
+      }
+      // (all eight warps: the jobs past the first four go to the band warps, not back to the chain warps)
+      const int m2l_pos = warp >= 6 ? warp - 6 : (warp >= 4 ? warp - 2 : warp + 4);
+      // ---- step 3 for the rows the next leaf enters: job k = (level gN + k/2, sigma k&1) on warp
+      // 6, 7, 4, 5, 0, 1, 2, 3, 6, ...: c(u') = sum_r A_hat_r w(t_r)
+      if (U >= 1) {
+        const int gN = gmin_of(U - 1);
+        const int nm2l = (L - gN) * 2;
+        for (int k = m2l_pos; k < nm2l; k += 8) {
+          const int g = gN + (k >> 1), sgk = k & 1;
+          const int u = (U - 1) >> (L - 1 - g);
+          double acc[3][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+          if (u < (4 << g) - 2) {
+            const int b = u >> 1, p = u & 1;
+            for (int mi = 0; mi < (p ? 1 : 2); ++mi) {
+              const int r = p ? 2 : mi;
+              const int t = u + 2 + (p ? 0 : mi);
+              const double* Am = P.A + (ahat_level_offset(g) + 3 * int64_t(b) + r) * kMM;
+              const double* W = wslot(g, t) + sgk * kTS;
+              double av[3][5];
 #pragma unroll
-                for (int mt = 0; mt < 3; ++mt)
-#pragma unroll
-                  for (int kk = 0; kk < 5; ++kk) {
-                    const int kx = 4 * kk + lc, mode = 8 * mt + lr;
-                    av[mt][kk] = (mode < kM && kx < kM) ? __ldg(Am + mode * kM + kx) : 0.0;
-                  }
+              for (int mt = 0; mt < 3; ++mt)
 #pragma unroll
                 for (int kk = 0; kk < 5; ++kk) {
-                  const int kx = 4 * kk + lc;
-                  const double bb = kx < kM ? W[lr * kM + kx] : 0.0;
-#pragma unroll
-                  for (int mt = 0; mt < 3; ++mt) dmma(acc[mt], av[mt][kk], bb);
+                  const int kx = 4 * kk + lc, mode = 8 * mt + lr;
+                  av[mt][kk] = (mode < kM && kx < kM) ? __ldg(Am + mode * kM + kx) : 0.0;
                 }
+#pragma unroll
+              for (int kk = 0; kk < 5; ++kk) {
+                const int kx = 4 * kk + lc;
+                const double bb = kx < kM ? W[lr * kM + kx] : 0.0;
+#pragma unroll
+                for (int mt = 0; mt < 3; ++mt) dmma(acc[mt], av[mt][kk], bb);
               }
             }
-            double* dst = cslot(g, u) + sgk * kTS;
+          }
+          double* dst = cslot(g, u) + sgk * kTS;
 #pragma unroll
-            for (int mt = 0; mt < 3; ++mt) {
-              const int mode = 8 * mt + lr;
-              if (mode < kM) {
-                dst[(2 * lc) * kM + mode] = acc[mt][0];
-                dst[(2 * lc + 1) * kM + mode] = acc[mt][1];
-              }
+          for (int mt = 0; mt < 3; ++mt) {
+            const int mode = 8 * mt + lr;
+            if (mode < kM) {
+              dst[(2 * lc) * kM + mode] = acc[mt][0];
+              dst[(2 * lc + 1) * kM + mode] = acc[mt][1];
             }
           }
         }
@@ -2248,47 +2250,48 @@ __global__ void __launch_bounds__(kTileThreads, LC_RANGE_MINB) lc_range_kernel(c
           }
         }
         TP_MARK(1);
-        // ---- step 3 for the rows the next leaf enters: job k = (level gN + k/2, sigma k&1) on warp
-        // 4, 5, 6, 7, 4, ...: c(u') = sum_r A_hat_r w(t_r), w from the up kernel's output
-        if (U - 1 >= Ua) {
-          const int gN = gentry(U - 1);
-          const int nm2l = (L - gN) * 2;
-          for (int k = warp - 4; k < nm2l; k += 4) {
-            const int g = gN + (k >> 1), sgk = k & 1;
-            const int u = (U - 1) >> (L - 1 - g);
-            double acc[3][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
-            if (u < (4 << g) - 2) {
-              const int b = u >> 1, p = u & 1;
-              for (int mi = 0; mi < (p ? 1 : 2); ++mi) {
-                const int r = p ? 2 : mi;
-                const int t = u + 2 + (p ? 0 : mi);
-                const double* Am = P.A + (ahat_level_offset(g) + 3 * int64_t(b) + r) * kMM;
-                const double* W = wglob(tile, g, t, sgk);
-                double av[3][5];
+      }
+      // ---- step 3 for the rows the next leaf enters: job k = (level gN + k/2, sigma k&1) on warp
+      // 4, 5, 6, 7, 4, ...: c(u') = sum_r A_hat_r w(t_r), w from the up kernel's output (handing the
+      // jobs past the first four to the band warps, as lc_tile_kernel does, measured 0.6% slower here)
+      if (warp >= 4 && U - 1 >= Ua) {
+        const int gN = gentry(U - 1);
+        const int nm2l = (L - gN) * 2;
+        for (int k = warp - 4; k < nm2l; k += 4) {
+          const int g = gN + (k >> 1), sgk = k & 1;
+          const int u = (U - 1) >> (L - 1 - g);
+          double acc[3][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+          if (u < (4 << g) - 2) {
+            const int b = u >> 1, p = u & 1;
+            for (int mi = 0; mi < (p ? 1 : 2); ++mi) {
+              const int r = p ? 2 : mi;
+              const int t = u + 2 + (p ? 0 : mi);
+              const double* Am = P.A + (ahat_level_offset(g) + 3 * int64_t(b) + r) * kMM;
+              const double* W = wglob(tile, g, t, sgk);
+              double av[3][5];
 #pragma unroll
-                for (int mt = 0; mt < 3; ++mt)
-#pragma unroll
-                  for (int kk = 0; kk < 5; ++kk) {
-                    const int kx = 4 * kk + lc, mode = 8 * mt + lr;
-                    av[mt][kk] = (mode < kM && kx < kM) ? __ldg(Am + mode * kM + kx) : 0.0;
-                  }
+              for (int mt = 0; mt < 3; ++mt)
 #pragma unroll
                 for (int kk = 0; kk < 5; ++kk) {
-                  const int kx = 4 * kk + lc;
-                  const double bb = kx < kM ? __ldg(W + lr * kM + kx) : 0.0;
-#pragma unroll
-                  for (int mt = 0; mt < 3; ++mt) dmma(acc[mt], av[mt][kk], bb);
+                  const int kx = 4 * kk + lc, mode = 8 * mt + lr;
+                  av[mt][kk] = (mode < kM && kx < kM) ? __ldg(Am + mode * kM + kx) : 0.0;
                 }
+#pragma unroll
+              for (int kk = 0; kk < 5; ++kk) {
+                const int kx = 4 * kk + lc;
+                const double bb = kx < kM ? __ldg(W + lr * kM + kx) : 0.0;
+#pragma unroll
+                for (int mt = 0; mt < 3; ++mt) dmma(acc[mt], av[mt][kk], bb);
               }
             }
-            double* dst = cslot(g, u) + sgk * kTS;
+          }
+          double* dst = cslot(g, u) + sgk * kTS;
 #pragma unroll
-            for (int mt = 0; mt < 3; ++mt) {
-              const int mode = 8 * mt + lr;
-              if (mode < kM) {
-                dst[(2 * lc) * kM + mode] = acc[mt][0];
-                dst[(2 * lc + 1) * kM + mode] = acc[mt][1];
-              }
+          for (int mt = 0; mt < 3; ++mt) {
+            const int mode = 8 * mt + lr;
+            if (mode < kM) {
+              dst[(2 * lc) * kM + mode] = acc[mt][0];
+              dst[(2 * lc + 1) * kM + mode] = acc[mt][1];
             }
           }
         }
