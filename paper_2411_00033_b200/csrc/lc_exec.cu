@@ -2384,7 +2384,7 @@ lc_status configure_kernels(lc_plan* p) {
   const int64_t budget2 = 113 * 1024;  // two CTAs per SM (228 KB minus 1 KB reserved per CTA)
   int vt = p->vt;
   // automatic engine 3 (tools/engine_cross3.py on the B200): long vectors in batches of 8+ (>= 16 below
-  // n = 2^18), deep enough trees for ranges of >= 64 leaves; e.g. 64 x 10^7: 42.4 -> 30.3 ms
+  // n = 2^18), deep enough trees for ranges of >= 64 leaves; e.g. 64 x 10^7: 41.8 -> 22.9 ms per transform
   if (p->engine == 0 && p->vt <= 0 && L >= 9 && p->s <= 32 && p->batch >= 8 && (p->batch >= 16 || p->n >= 262144) &&
       ((p->batch + kTileV - 1) / kTileV) < int64_t(p->sm_count))
     p->engine = 3;
