@@ -192,3 +192,18 @@ def test_range_engine_staging_paths_and_continuation():
         for v in (0, V - 1):
             e = oracle.einf(zc[v][rows], oracle.transform_rows(direction, x[v].numpy(), rows))
             assert e <= GATE, (direction, v, e)
+
+
+def test_execute_checks_extents():
+    # input / output tensors must cover the extent the kernels address ((rows - 1) ld + cols elements)
+    dev = _dev()
+    n, V = 1000, 9
+    p = _plan(n, "leg2cheb", batch=V, device=dev, engine=2, ld_out=n + 5)
+    x = batch("normal", n, V, seed=15).to(dev)
+    with pytest.raises(ValueError):
+        p.execute(x[:, : n - 1].contiguous())
+    with pytest.raises(ValueError):
+        p.execute(x, out=torch.empty(V, n, dtype=torch.float64, device=dev))  # ld_out = n + 5
+    z = p.execute(x)  # default output allocated with ld_out
+    assert z.shape == (V, n + 5)
+    assert torch.equal(z[:, :n], _plan(n, "leg2cheb", batch=V, device=dev, engine=2).execute(x))
