@@ -1519,6 +1519,9 @@ __host__ __device__ inline int tile_fst(int s) { int f = 4; while (f < s) f += 1
 #define LC_TILE_MINB 2
 #endif
 __host__ __device__ inline int tile_gs(int L) { return (LC_TILE_SL == 0 || L <= LC_TILE_SL) ? 0 : L - LC_TILE_SL; }
+#ifndef LC_M2L_K36
+#define LC_M2L_K36 1  // the two A_hat blocks of an even M2L row as one K = 36 contraction
+#endif
 __host__ __device__ inline int64_t tile_smem_doubles(int L, int s) {
   const int fst = tile_fst(s);
   const int ns = L - tile_gs(L);  // levels in shared memory
@@ -1950,6 +1953,24 @@ __global__ void __launch_bounds__(kTileThreads, LC_TILE_MINB) lc_tile_kernel(con
           double acc[3][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
           if (u < (4 << g) - 2) {
             const int b = u >> 1, p = u & 1;
+            if (LC_M2L_K36 && p == 0) {
+              // even row: both blocks as one K = 36 contraction [A_hat_0 | A_hat_1] [w(u+2); w(u+3)]
+              // (9 K steps instead of 2 x 5 with the padding to 20)
+              const double* A0 = P.A + (ahat_level_offset(g) + 3 * int64_t(b)) * kMM;
+              const double* W0 = wslot(g, u + 2) + sgk * kTS;
+              const double* W1 = wslot(g, u + 3) + sgk * kTS;
+#pragma unroll
+              for (int kk = 0; kk < 9; ++kk) {
+                const int kx = 4 * kk + lc;
+                const int blk = kx >= kM ? 1 : 0, kc = kx - blk * kM;
+                const double bb = (blk ? W1 : W0)[lr * kM + kc];
+#pragma unroll
+                for (int mt = 0; mt < 3; ++mt) {
+                  const int mode = 8 * mt + lr;
+                  dmma(acc[mt], mode < kM ? __ldg(A0 + blk * kMM + mode * kM + kc) : 0.0, bb);
+                }
+              }
+            } else
             for (int mi = 0; mi < (p ? 1 : 2); ++mi) {
               const int r = p ? 2 : mi;
               const int t = u + 2 + (p ? 0 : mi);
@@ -2263,6 +2284,24 @@ __global__ void __launch_bounds__(kTileThreads, LC_RANGE_MINB) lc_range_kernel(c
           double acc[3][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
           if (u < (4 << g) - 2) {
             const int b = u >> 1, p = u & 1;
+            if (LC_M2L_K36 && p == 0) {
+              // even row: both blocks as one K = 36 contraction [A_hat_0 | A_hat_1] [w(u+2); w(u+3)]
+              // (9 K steps instead of 2 x 5 with the padding to 20)
+              const double* A0 = P.A + (ahat_level_offset(g) + 3 * int64_t(b)) * kMM;
+              const double* W0 = wglob(tile, g, u + 2, sgk);
+              const double* W1 = wglob(tile, g, u + 3, sgk);
+#pragma unroll
+              for (int kk = 0; kk < 9; ++kk) {
+                const int kx = 4 * kk + lc;
+                const int blk = kx >= kM ? 1 : 0, kc = kx - blk * kM;
+                const double bb = __ldg((blk ? W1 : W0) + lr * kM + kc);
+#pragma unroll
+                for (int mt = 0; mt < 3; ++mt) {
+                  const int mode = 8 * mt + lr;
+                  dmma(acc[mt], mode < kM ? __ldg(A0 + blk * kMM + mode * kM + kc) : 0.0, bb);
+                }
+              }
+            } else
             for (int mi = 0; mi < (p ? 1 : 2); ++mi) {
               const int r = p ? 2 : mi;
               const int t = u + 2 + (p ? 0 : mi);
