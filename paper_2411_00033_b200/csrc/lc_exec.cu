@@ -2533,7 +2533,7 @@ lc_status configure_kernels(lc_plan* p) {
       if (occ < 1) return LC_ERR_INVALID_ARG;
       const int64_t slots = int64_t(occ) * p->sm_count;
       const int64_t nls = int64_t(2) << L;
-      int64_t nr = std::max<int64_t>(1, (slots + p->ntiles - 1) / p->ntiles);
+      int64_t nr = std::max<int64_t>(1, slots / p->ntiles);  // units <= slots: one wave, no straggler round
       nr = std::max<int64_t>(1, std::min(nr, nls / 64));  // ranges of >= 64 leaves (the entry chain is L deep)
       const int64_t rlen = (nls + nr - 1) / nr;
       nr = (nls + rlen - 1) / rlen;

@@ -207,3 +207,14 @@ def test_execute_checks_extents():
     z = p.execute(x)  # default output allocated with ld_out
     assert z.shape == (V, n + 5)
     assert torch.equal(z[:, :n], _plan(n, "leg2cheb", batch=V, device=dev, engine=2).execute(x))
+
+
+@pytest.mark.parametrize("V", [24, 40, 48, 72])
+def test_range_engine_units_fit_one_wave(V):
+    # (tile, range) units <= CTAs: a tile count that does not divide the slot count must not leave a
+    # straggler round (was 30-40% slower, tools/range_batches.py)
+    dev = _dev()
+    p = _plan(2000000, "leg2cheb", batch=V, device=dev, engine=3)
+    ki = p.kernel_info
+    assert ki["engine"] == 3
+    assert ((V + 7) // 8) * ki["ranges"] <= ki["tile_grid"]
