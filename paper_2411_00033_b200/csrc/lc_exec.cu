@@ -1530,13 +1530,18 @@ __host__ __device__ inline int64_t tile_smem_doubles(int L, int s) {
 }
 __host__ __device__ inline int64_t tile_scratch_doubles(int L) { return int64_t(tile_gs(L)) * 5 * 2 * kTS; }
 
-__host__ __device__ inline int64_t range_smem_doubles(int s) {
+// STAGE = 1: the M2L operands of each job are staged per warp by cp.async (+30 KB; registers bounded
+// for 3 CTAs per SM), used when 3 such CTAs fit an SM (s <= 24); otherwise the direct-load variant at
+// 4 CTAs per SM (measured at cfg4, s = 20: 17.2 -> 16.7 ms; at n = 2e6, s = 31, staging would drop to
+// 2 CTAs per SM and lose 10%)
+__host__ __device__ inline int64_t range_smem_doubles(int s, int stage) {
   const int fst = tile_fst(s);
   return 2 * 32 * kM + (kMM + 4) + 80 + LC_FRING * 2 * kTileV * fst + LC_FRING * 4 * s + int64_t(5) * 2 * kTS +
-         2 * kTileV * (2 * s + 4);
+         2 * kTileV * (2 * s + 4) + (stage ? 4 * (2 * kMM + 2 * kTS) : 0);
 }
 #ifndef LC_RANGE_MINB
-#define LC_RANGE_MINB 4  // CTAs per SM the range kernel's registers are bounded for (measured: 2 -> 21.3 ms, 4 -> 18.2 ms at cfg4)
+// CTAs per SM the direct-load range kernel's registers are bounded for (cfg4: 4 -> 17.2 ms, 2 -> 19.8 ms)
+#define LC_RANGE_MINB 4
 #endif
 __host__ __device__ inline int64_t range_scratch_doubles(int L) { return int64_t(L >= 2 ? L - 2 : 0) * 2 * 2 * kTS; }
 
@@ -2021,8 +2026,8 @@ __global__ void __launch_bounds__(kTileThreads, LC_TILE_MINB) lc_tile_kernel(con
 // the GPU): steps 3-7 exactly as in lc_tile_kernel, with w read from the workspace, the step-4 chain
 // started at the range's rightmost leaf from the top level down, and the c of the levels below L-2 in
 // a per-CTA global scratch (the footprint does not grow with L).
-template <int DIR>
-__global__ void __launch_bounds__(kTileThreads, LC_RANGE_MINB) lc_range_kernel(const __grid_constant__ TileParams P) {
+template <int DIR, int STAGE>
+__global__ void __launch_bounds__(kTileThreads, STAGE ? 3 : LC_RANGE_MINB) lc_range_kernel(const __grid_constant__ TileParams P) {
   extern __shared__ __align__(128) unsigned char smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int lr = lane >> 2, lc = lane & 3;
@@ -2036,6 +2041,7 @@ __global__ void __launch_bounds__(kTileThreads, LC_RANGE_MINB) lc_range_kernel(c
   double* lmr = fr + LC_FRING * 2 * kTileV * fst; // [LC_FRING][4s]
   double* cs = lmr + LC_FRING * 4 * s;            // leaf level [3], level L-2 [2] x [2][8][M]
   double* zs = cs + 5 * 2 * kTS;                  // [2][8][2s+4]
+  double* mbuf = zs + 2 * kTileV * (2 * s + 4);    // STAGE: [4 M2L warps][2 A_hat + 2 w]
   double* gc = P.scratch + int64_t(blockIdx.x) * range_scratch_doubles(L);  // levels < L-2: [L-2][2][2][8][M]
   auto fslot = [&](int U) { return fr + ((U + LC_FRING) % LC_FRING) * 2 * kTileV * fst; };  // U >= -1
   auto lslot = [&](int U) { return lmr + ((U + LC_FRING) % LC_FRING) * 4 * s; };
@@ -2062,18 +2068,22 @@ __global__ void __launch_bounds__(kTileThreads, LC_RANGE_MINB) lc_range_kernel(c
   // stage leaf segment U of the tile: f de-interleaved by parity ([sigma][v][m]), and the lambda
   // (tabB) window [2sU, 2sU + 4s) that the band of rows U reads; zero beyond n / N
   auto stage = [&](int64_t tile, int U) {
+    if (STAGE && warp >= 4) return;  // the M2L warps' cp.async groups stay their own
     double* fd = fslot(U);
     const int64_t j0 = int64_t(U) * seglen;
+    constexpr int nstw = STAGE ? 4 : 8;  // staging warps
     if (P.layout == LC_VEC_CONTIGUOUS) {  // warp = vector, lanes along the segment
-      const int64_t gv = tile * kTileV + warp;
-      const double* src = P.in + gv * P.ld_in + j0;
-      const int64_t lim = gv < P.batch ? P.n - j0 : 0;
-      for (int x = lane; x < seglen; x += 32) {
-        const bool ok = x < lim;
-        cp_async8(fd + ((x & 1) * kTileV + warp) * fst + (x >> 1), ok ? src + x : P.in, ok ? 8u : 0u);
+      for (int vv = warp; vv < kTileV; vv += nstw) {
+        const int64_t gv = tile * kTileV + vv;
+        const double* src = P.in + gv * P.ld_in + j0;
+        const int64_t lim = gv < P.batch ? P.n - j0 : 0;
+        for (int x = lane; x < seglen; x += 32) {
+          const bool ok = x < lim;
+          cp_async8(fd + ((x & 1) * kTileV + vv) * fst + (x >> 1), ok ? src + x : P.in, ok ? 8u : 0u);
+        }
       }
     } else {  // vectors fastest
-      for (int idx = tid; idx < kTileV * seglen; idx += kTileThreads) {
+      for (int idx = tid; idx < kTileV * seglen; idx += 32 * nstw) {
         const int x = idx >> 3, v = idx & 7;
         const int64_t gv = tile * kTileV + v, j = j0 + x;
         const bool ok = gv < P.batch && j < P.n;
@@ -2081,7 +2091,7 @@ __global__ void __launch_bounds__(kTileThreads, LC_RANGE_MINB) lc_range_kernel(c
       }
     }
     double* ld = lslot(U);
-    for (int x = tid; x < 2 * seglen; x += kTileThreads) {
+    for (int x = tid; x < 2 * seglen; x += 32 * nstw) {
       const bool ok = j0 + x < P.N;
       cp_async8(ld + x, ok ? P.tabB + j0 + x : P.tabB, ok ? 8u : 0u);
     }
@@ -2282,7 +2292,38 @@ __global__ void __launch_bounds__(kTileThreads, LC_RANGE_MINB) lc_range_kernel(c
           const int g = gN + (k >> 1), sgk = k & 1;
           const int u = (U - 1) >> (L - 1 - g);
           double acc[3][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
-          if (u < (4 << g) - 2) {
+          if (STAGE && u < (4 << g) - 2) {
+            // the job's A_hat block(s) and w node(s) (contiguous) land in this warp's buffer in one round
+            const int b = u >> 1, p = u & 1, nb = p ? 1 : 2;
+            double* ab = mbuf + (warp - 4) * (2 * kMM + 2 * kTS);
+            double* wb = ab + 2 * kMM;
+            const double* As = P.A + (ahat_level_offset(g) + 3 * int64_t(b) + (p ? 2 : 0)) * kMM;
+            const double* Wsrc = wglob(tile, g, u + 2, sgk);
+            __syncwarp();
+            for (int i = lane; i < nb * (kMM / 2); i += 32) cp_async16(ab + 2 * i, As + 2 * i);
+            for (int i = lane; i < nb * (kTS / 2); i += 32) cp_async16(wb + 2 * i, Wsrc + 2 * i);
+            cp_async_commit();
+            cp_async_wait<0>();
+            __syncwarp();
+            auto kstep = [&](int kk, bool one) {
+              const int kx = 4 * kk + lc;
+              const int blk = kx >= kM ? 1 : 0, kc = kx - blk * kM;
+              const bool okk = !one || kx < kM;
+              const double bb = okk ? wb[blk * kTS + lr * kM + kc] : 0.0;
+#pragma unroll
+              for (int mt = 0; mt < 3; ++mt) {
+                const int mode = 8 * mt + lr;
+                dmma(acc[mt], (okk && mode < kM) ? ab[blk * kMM + mode * kM + kc] : 0.0, bb);
+              }
+            };
+            if (p) {
+#pragma unroll
+              for (int kk = 0; kk < 5; ++kk) kstep(kk, true);
+            } else {
+#pragma unroll
+              for (int kk = 0; kk < 9; ++kk) kstep(kk, false);
+            }
+          } else if (u < (4 << g) - 2) {
             const int b = u >> 1, p = u & 1;
             if (LC_M2L_K36 && p == 0) {
               // even row: both blocks as one K = 36 contraction [A_hat_0 | A_hat_1] [w(u+2); w(u+3)]
@@ -2410,8 +2451,10 @@ lc_status configure_kernels(lc_plan* p) {
     if (ea == cudaSuccess) ea = set_max_dyn_smem(lc_tile_kernel<0>, smax);
     if (ea == cudaSuccess) ea = set_max_dyn_smem(lc_tile_kernel<1>, smax);
     if (ea == cudaSuccess) ea = set_max_dyn_smem(lc_up3_kernel, smax);
-    if (ea == cudaSuccess) ea = set_max_dyn_smem(lc_range_kernel<0>, smax);
-    if (ea == cudaSuccess) ea = set_max_dyn_smem(lc_range_kernel<1>, smax);
+    if (ea == cudaSuccess) ea = set_max_dyn_smem(lc_range_kernel<0, 0>, smax);
+    if (ea == cudaSuccess) ea = set_max_dyn_smem(lc_range_kernel<1, 0>, smax);
+    if (ea == cudaSuccess) ea = set_max_dyn_smem(lc_range_kernel<0, 1>, smax);
+    if (ea == cudaSuccess) ea = set_max_dyn_smem(lc_range_kernel<1, 1>, smax);
     if (ea != cudaSuccess) return record_cuda_error(ea);
     g_device_ready[p->device] = true;
   }
@@ -2526,10 +2569,17 @@ lc_status configure_kernels(lc_plan* p) {
     const bool tile_ok = L >= 1 && s <= 32 && tsm <= smax;
     if (p->engine == 2 && !tile_ok) return LC_ERR_INVALID_ARG;
     if (p->engine == 3) {
+      // the staged-M2L variant where three of its CTAs fit an SM, else the direct-load one
       int occ = 0;
-      const size_t rsm = size_t(range_smem_doubles(s) * 8);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, p->dir == 0 ? lc_range_kernel<0> : lc_range_kernel<1>,
+      size_t rsm = size_t(range_smem_doubles(s, 1) * 8);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, p->dir == 0 ? lc_range_kernel<0, 1> : lc_range_kernel<1, 1>,
                                                     kTileThreads, rsm);
+      p->range_stage = occ >= 3 ? 1 : 0;
+      if (!p->range_stage) {
+        rsm = size_t(range_smem_doubles(s, 0) * 8);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, p->dir == 0 ? lc_range_kernel<0, 0> : lc_range_kernel<1, 0>,
+                                                      kTileThreads, rsm);
+      }
       if (occ < 1) return LC_ERR_INVALID_ARG;
       const int64_t slots = int64_t(occ) * p->sm_count;
       const int64_t nls = int64_t(2) << L;
@@ -2753,7 +2803,10 @@ lc_status launch_execute(const lc_plan* p, const double* in, double* out, void* 
       cfg.gridDim = dim3(unsigned(p->tile_grid));
       cfg.blockDim = dim3(kTileThreads);
       cfg.dynamicSmemBytes = p->smem_tile;
-      e = p->dir == 0 ? cudaLaunchKernelEx(&cfg, lc_range_kernel<0>, tp) : cudaLaunchKernelEx(&cfg, lc_range_kernel<1>, tp);
+      if (p->range_stage)
+        e = p->dir == 0 ? cudaLaunchKernelEx(&cfg, lc_range_kernel<0, 1>, tp) : cudaLaunchKernelEx(&cfg, lc_range_kernel<1, 1>, tp);
+      else
+        e = p->dir == 0 ? cudaLaunchKernelEx(&cfg, lc_range_kernel<0, 0>, tp) : cudaLaunchKernelEx(&cfg, lc_range_kernel<1, 0>, tp);
     }
     if (e == cudaSuccess && ev && evi < nev) cudaEventRecord(ev[evi++], st);
     if (e == cudaSuccess) e = cudaGetLastError();
