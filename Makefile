@@ -9,10 +9,11 @@ HDRS := $(PKG)/csrc/lc_internal.h include/legcheb.h
 all: $(PKG)/liblegcheb.so oracle/liboracle.so
 
 $(PKG)/liblegcheb.so: $(SRCS) $(HDRS)
+	mkdir -p build
 	$(NVCC) $(NVFLAGS) $(SRCS) -o $@ 2> build/ptxas.log || (cat build/ptxas.log; exit 1)
 
 oracle/liboracle.so: oracle/oracle.c
-	gcc -O2 -fno-fast-math -ffp-contract=off -fopenmp -shared -fPIC $< -o $@ -lm
+	gcc -O2 -fno-fast-math -ffp-contract=off -fopenmp -shared -fPIC $< -o $@ -lquadmath -lm
 
 clean:
 	rm -f $(PKG)/liblegcheb.so oracle/liboracle.so

@@ -7,11 +7,17 @@ leg2cheb followed by one cheb2leg (the round trip), i.e. one pass of the whole
 hot path in both directions.  Metric: coefficients/s = 2 n V / step time
 (n unpadded, V vectors, 2 transforms), summed over ranks.
 
-Multi-GPU (torchrun, one process per GPU, NCCL): cfg2 does not shard (one
-vector couples all leaves through the coarse levels), so N GPUs run N
-independent replicas (weak scaling).  --config cfg3/cfg4 shard the batch
-(strong scaling).  Timing: CUDA events on the launching stream inside a
-barrier + synchronize bracket, max over ranks.
+After the headline record, the batched half of the metric is measured the
+same way and attached as "batched" (default cfg3: 4096 vectors of n = 4096,
+sharded over the ranks; --batched cfg4/cfg5/none).
+
+Multi-GPU (one process per GPU, NCCL; `--gpus N` launches torchrun itself when
+WORLD_SIZE is unset): cfg2 does not shard (one vector couples all leaves
+through the coarse levels), so N GPUs run N independent replicas (weak
+scaling); cfg3/cfg4 shard the batch and cfg5 partitions rows with an
+all-to-all between the passes (strong scaling).  Timing: CUDA events on the
+launching stream inside a barrier + synchronize bracket, max over ranks;
+per-step events give the median and minimum step.
 
 --impl reference runs the CPU oracle (oracle/, long-double direct O(n^2)
 rows) on a bounded row sample of the same workload, on rank 0 only.
@@ -162,11 +168,56 @@ def make_input(kind, n, V, v0, pin):
 
 
 # --------------------------------------------------------------------------- our arm
-def run_gpu(args, world, rank, local):
+def kernel_names(pl):
+    kpe = pl.kernels_per_execute
+    engine = pl.kernel_info.get("engine", 1)
+    if engine == 3:
+        return ["lc_up3_kernel", "lc_range_kernel"], engine
+    if kpe == 1:
+        return ["lc_tile_kernel"], engine
+    return (["lc_up_kernel"] if kpe == 3 else []) + ["lc_stream_kernel", "lc_down_kernel"], engine
+
+
+def make_plans(config, n, V, dev, world, opts):
+    """The plans one step uses, with their creation times (wall, and device time of the planner)."""
     from paper_2411_00033_b200 import Plan
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    if config == "cfg5":
+        C = n // world
+        pl = Plan(n, "leg2cheb", batch=V, device=dev, **opts)
+        pc = Plan(n, "leg2cheb", batch=C, device=dev, layout="batch", **opts)
+    else:
+        pl = Plan(n, "leg2cheb", batch=V, device=dev, **opts)
+        pc = Plan(n, "cheb2leg", batch=V, device=dev, **opts)
+    wall = (time.perf_counter() - t0) * 1e3
+    plan = {"wall_ms_both": wall, "device_ms": [pl.plan_device_ms, pc.plan_device_ms],
+            "plan_bytes": [int(pl.desc["plan_bytes"]), int(pc.desc["plan_bytes"])],
+            "note": "plan creation (lambda, A_hat, tables) is outside the timed region, as in the paper"}
+    return pl, pc, plan
+
+
+def timed_replays(fn, steps, stream):
+    """fn() `steps` times with a CUDA event after each step (same stream); returns the total and the
+    per-step durations in ms."""
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
+    ev[0].record(stream)
+    for i in range(steps):
+        fn()
+        ev[i + 1].record(stream)
+    torch.cuda.synchronize()
+    per = [ev[i].elapsed_time(ev[i + 1]) for i in range(steps)]
+    return ev[0].elapsed_time(ev[steps]), per
+
+
+def measure(config, args, world, rank, local, headline=True):
+    """One JSON record (bench contract keys) for `config` on this rank set."""
     from paper_2411_00033_b200.dist import tensor_product_2d
     dev = torch.device("cuda", local)
-    n, V, kind, v0, scaling = workload(args.config, world, rank)
+    n, V, kind, v0, scaling = workload(config, world, rank)
+    two_d = config == "cfg5"
+    if two_d:
+        scaling = "strong"
     xh = make_input(kind, n, V, v0, pin=True)
     x = xh.to(dev)
     tmp = torch.empty_like(x)
@@ -174,22 +225,16 @@ def run_gpu(args, world, rank, local):
     opts = dict(vt=args.vt, subtree=args.subtree, stage_blocks=args.stage_blocks, stages=args.stages,
                 engine=args.engine, up_subtree=args.up_subtree)
     stream = torch.cuda.current_stream(dev)
-    two_d = args.config == "cfg5"
+    pl, pc, plan_info = make_plans(config, n, V, dev, world, opts)
+    C = n // world
     if two_d:
         # rows [v0, v0+V) of the n x n array on this rank; pass 1 along axis 1 (V row vectors), all-to-all,
         # pass 2 along axis 0 (n/world column vectors, batch-contiguous)
-        scaling = "strong"
-        C = n // world
-        pl = Plan(n, "leg2cheb", batch=V, device=dev, **opts)
-        pc = Plan(n, "leg2cheb", batch=C, device=dev, layout="batch", **opts)
         ycol = torch.empty((n, C), dtype=torch.float64, device=dev)
 
         def step():
             tensor_product_2d(x, row_fn=lambda a: pl.execute(a, tmp), col_fn=lambda a: pc.execute(a, ycol))
     else:
-        pl = Plan(n, "leg2cheb", batch=V, device=dev, **opts)
-        pc = Plan(n, "cheb2leg", batch=V, device=dev, **opts)
-
         def step():
             pl.execute(x, tmp)
             pc.execute(tmp, y)
@@ -217,38 +262,46 @@ def run_gpu(args, world, rank, local):
         except Exception as e:  # graph capture unavailable: eager launches
             graph = None
             print(f"[bench] graph capture failed ({e}); eager launches", file=sys.stderr)
+    run = graph.replay if graph is not None else step
 
     clocks = ClockSampler(local)
     barrier(world)
     torch.cuda.synchronize()
     clocks.start()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
     barrier(world)
     torch.cuda.synchronize()
-    e0.record(stream)
-    for _ in range(args.steps):
-        if graph is not None:
-            graph.replay()
-        else:
-            step()
-    e1.record(stream)
-    torch.cuda.synchronize()
+    ms_local, per_step = timed_replays(run, args.steps, stream)
     barrier(world)
     clk = clocks.stop()
-    ms_local = e0.elapsed_time(e1)
     ms = allreduce_max(ms_local, world)
-    coeffs = 2.0 * n * V  # per rank per step
+    coeffs = 2.0 * n * V  # per rank per step (2 transforms or 2 passes)
     total_coeffs = allreduce_sum(coeffs, world)
     value = total_coeffs * args.steps / (ms / 1e3)
+    med_ms = allreduce_max(statistics.median(per_step), world)
+    min_ms = allreduce_max(min(per_step), world)
 
     # correctness of what was timed: round trip back to the input (gate 1e-12 for n <= 1e6)
     rt = None if two_d else float((y - x).abs().max() / x.abs().max())
 
+    # ---- the 2-D passes and the all-to-all timed separately
+    passes = None
+    if two_d:
+        tm = {}
+        acc = {"pass1_ms": 0.0, "alltoall_ms": 0.0, "pass2_ms": 0.0}
+        reps = max(3, min(args.steps, 50))
+        for _ in range(reps):
+            tensor_product_2d(x, row_fn=lambda a: pl.execute(a, tmp), col_fn=lambda a: pc.execute(a, ycol),
+                              timing=tm)
+            for k in acc:
+                acc[k] += tm[k] / reps
+        passes = {k: allreduce_max(v, world) for k, v in acc.items()}
+        passes["alltoall_bytes_sent_per_rank"] = 8 * V * C * (world - 1)
+
     # ---- per-kernel durations (events around each kernel, same stream) for the roofline
     kpe = pl.kernels_per_execute
+    names, engine = kernel_names(pl)
     evs = [torch.cuda.Event(enable_timing=True) for _ in range(kpe + 1)]
-    evc = [torch.cuda.Event(enable_timing=True) for _ in range(kpe + 1)]
+    evc = [torch.cuda.Event(enable_timing=True) for _ in range(pc.kernels_per_execute + 1)]
     ksteps = max(3, min(args.steps, 200))
     per_kernel = [[0.0] * kpe, [0.0] * kpe]
     for _ in range(ksteps):
@@ -263,28 +316,23 @@ def run_gpu(args, world, rank, local):
                 per_kernel[d][i] += ev[i].elapsed_time(ev[i + 1]) / ksteps
     hbm, hbm_src = peaks()
     dl = pl.desc
-    engine = pl.kernel_info.get("engine", 1)
-    if engine == 3:
-        names = ["lc_up3_kernel", "lc_range_kernel"]
-    else:
-        names = ["lc_tile_kernel"] if kpe == 1 else (["lc_up_kernel"] if kpe == 3 else []) + ["lc_stream_kernel",
-                                                                                             "lc_down_kernel"]
     # algorithmic bytes per launch (f in, z out, A_hat once, lambda once; work arrays excluded):
     # the up kernel reads f, the streaming kernel reads A_hat and lambda (and f again for the band),
     # the down kernel writes z
-    alg = {"lc_up_kernel": 8.0 * n * V, "lc_up3_kernel": 8.0 * n * V, "lc_stream_kernel": 8.0 * 324 * dl["nc"] + 8.0 * dl["N"],
-           "lc_down_kernel": 8.0 * n * V}
-    if kpe == 2:
+    alg = {"lc_up_kernel": 8.0 * n * V, "lc_up3_kernel": 8.0 * n * V,
+           "lc_stream_kernel": 8.0 * 324 * dl["nc"] + 8.0 * dl["N"], "lc_down_kernel": 8.0 * n * V}
+    if kpe == 2 and engine == 1:
         alg["lc_stream_kernel"] += 8.0 * n * V
     # the per-tile kernel (engine 2) is the whole transform: f in, z out, A_hat and lambda once
     alg["lc_tile_kernel"] = 16.0 * n * V + 8.0 * 324 * dl["nc"] + 8.0 * dl["N"]
     alg["lc_range_kernel"] = 8.0 * n * V + 8.0 * 324 * dl["nc"] + 8.0 * dl["N"]  # f in (band), z out, A_hat, lambda
     avg_ms = {nm: 0.5 * (per_kernel[0][i] + per_kernel[1][i]) for i, nm in enumerate(names)}
     dom = "lc_tile_kernel" if kpe == 1 else ("lc_range_kernel" if engine == 3 else "lc_stream_kernel")
-    down_ms = avg_ms[dom]
-    down_bytes = alg[dom]
-    achieved = down_bytes / (down_ms * 1e-3) / 1e9
-    traffic = load_traffic(args.config, dom)
+    dom_ms = avg_ms[dom]
+    dom_bytes = alg[dom]
+    achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
+    traffic = load_traffic(config, dom)
+    fp64_peak = max(FP64_PEAK_TFLOPS, DMMA_PEAK_TFLOPS)
     if kpe == 1 or engine == 3:
         # fp64 tensor-core bound: algorithmic flops of one transform over the kernel time, against the
         # measured DMMA peak (the higher of the two fp64 peaks, so the fraction is conservative)
@@ -292,109 +340,90 @@ def run_gpu(args, world, rank, local):
         if engine == 3:  # the range kernel does steps 3-7: drop step 1 and the M2M half of F_alg
             Lq, sq, Mq = dl["L"], dl["s"], 18
             fk -= 8.0 * ((2 ** Lq) - 1) * sq * Mq + 4.0 * (Mq * Mq + 2 * Mq) * ((2 ** Lq) - Lq - 1)
-        tf = fk * V / (down_ms * 1e-3) / 1e12
+        tf = fk * V / (dom_ms * 1e-3) / 1e12
         roof = {"bound": "tensor", "kernel": dom, "achieved": tf, "peak": DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
                 "frac": tf / DMMA_PEAK_TFLOPS, "traffic": traffic, "algorithmic_flops_per_launch": fk * V,
-                "algorithmic_bytes_per_launch": down_bytes, "achieved_hbm_gbs": achieved, "avg_launch_ms": down_ms,
-                "peak_source": "measured fp64 DMMA m8n8k4 (profiles/r1_dmma_peak.txt)"}
+                "algorithmic_bytes_per_launch": dom_bytes, "achieved_hbm_gbs": achieved, "avg_launch_ms": dom_ms,
+                "peak_source": "measured fp64 DMMA m8n8k4 (profiles/r1_dmma_peak.txt); fp64 has no tcgen05 kind"}
     else:
         roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm,
                 "unit": "GB/s", "frac": achieved / hbm, "traffic": traffic,
-                "algorithmic_bytes_per_launch": down_bytes, "avg_launch_ms": down_ms,
+                "algorithmic_bytes_per_launch": dom_bytes, "avg_launch_ms": dom_ms,
                 "peak_source": hbm_src}
-    # transform-level roofline (slower of fp64 flops at the measured DFMA peak and bytes at HBM peak)
-    t_roof = max(dl["flops_alg"] * V / (FP64_PEAK_TFLOPS * 1e12), dl["bytes_alg"] / (hbm * 1e9))
+    # transform-level roofline (slower of fp64 flops at the fp64 peak -- the DMMA pipe, 37.0 TF -- and
+    # bytes at the HBM peak), per transform, against the median step
+    t_roof = max(dl["flops_alg"] * V / (fp64_peak * 1e12), dl["bytes_alg"] / (hbm * 1e9))
     t_meas = ms_local / args.steps / 2 * 1e-3
+    t_med = med_ms / 2 * 1e-3
 
-    # ---- e2e through the C ABI with HOST buffers (lc_execute_host: H2D, kernels, D2H per transform)
-    hz = torch.empty_like(xh).pin_memory()
-    hy = torch.empty_like(xh).pin_memory() if not two_d else torch.empty((n, n // world), dtype=torch.float64).pin_memory()
+    # ---- e2e through the C ABI with HOST buffers: lc_execute_host (H2D, kernels, D2H in one call) for
+    # each transform of the step, pipelined over three streams with caller-owned staging and workspaces
+    # (the call is thread- and stream-safe with distinct buffers, legcheb.h)
     e2e_steps = max(3, min(args.steps, args.e2e_steps))
+    nbuf = 3
+    streams = [torch.cuda.Stream(dev) for _ in range(nbuf)]
+    if two_d:
+        hz = [torch.empty_like(xh).pin_memory() for _ in range(nbuf)]
+        hy = [torch.empty((n, C), dtype=torch.float64).pin_memory() for _ in range(nbuf)]
+        ycols = [torch.empty((n, C), dtype=torch.float64, device=dev) for _ in range(nbuf)]
+        tmps = [torch.empty_like(x) for _ in range(nbuf)]
+    else:
+        hz = [torch.empty_like(xh).pin_memory() for _ in range(nbuf)]
+        hy = [torch.empty_like(xh).pin_memory() for _ in range(nbuf)]
+    st_l = [pl.new_host_stage() for _ in range(nbuf)]
+    st_c = [pc.new_host_stage() for _ in range(nbuf)]
+    ws_l = [pl.new_workspace(streams[b]) for b in range(nbuf)]
+    ws_c = [pc.new_workspace(streams[b]) for b in range(nbuf)]
+    torch.cuda.synchronize()
 
-    def host_step():
-        if two_d and world == 1:
-            pl.execute_host(xh, hz)
-            pc.execute_host(hz.view(n, n), hy)
-        elif two_d:
-            xd = xh.to(dev, non_blocking=True)
-            zc = tensor_product_2d(xd, row_fn=lambda a: pl.execute(a, tmp), col_fn=lambda a: pc.execute(a, ycol))
-            hy.copy_(zc, non_blocking=True)
-        else:
-            pl.execute_host(xh, hz)
-            pc.execute_host(hz, hy)
+    def host_steps(k0, k):
+        for i in range(k0, k0 + k):
+            b = i % nbuf
+            sb = streams[b]
+            if two_d and world == 1:
+                pl.execute_host(xh, hz[b], stream=sb, stage=st_l[b], workspace=ws_l[b])
+                pc.execute_host(hz[b].view(n, n), hy[b], stream=sb, stage=st_c[b], workspace=ws_c[b])
+            elif two_d:
+                with torch.cuda.stream(sb):
+                    xd = xh.to(dev, non_blocking=True)
+                    zc = tensor_product_2d(xd, row_fn=lambda a: pl.execute(a, tmps[b], workspace=ws_l[b], stream=sb),
+                                           col_fn=lambda a: pc.execute(a, ycols[b], workspace=ws_c[b], stream=sb))
+                    hy[b].copy_(zc, non_blocking=True)
+            else:
+                pl.execute_host(xh, hz[b], stream=sb, stage=st_l[b], workspace=ws_l[b])
+                pc.execute_host(hz[b], hy[b], stream=sb, stage=st_c[b], workspace=ws_c[b])
 
-    # 1-D configs: the round trip of a host vector, pipelined over three streams (the H2D of step i+1
-    # and the D2H of step i-1 overlap the two transforms of step i; double-buffered on the device)
-    s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
-    if not two_d:
-        xb = [torch.empty_like(x) for _ in range(2)]
-        tb = [torch.empty_like(x) for _ in range(2)]
-        yb = [torch.empty_like(x) for _ in range(2)]
-        hyb = [torch.empty_like(xh).pin_memory() for _ in range(2)]
-        ev_in = [torch.cuda.Event() for _ in range(2)]
-        ev_comp = [torch.cuda.Event() for _ in range(2)]
-        ev_out = [torch.cuda.Event() for _ in range(2)]
-        for b in range(2):  # mark every buffer free
-            ev_comp[b].record(stream)
-            ev_out[b].record(stream)
-
-    def pipelined(steps, h0=None, h1=None):
-        if h0 is not None:
-            h0.record(s_in)
-        for i in range(steps):
-            b = i & 1
-            s_in.wait_event(ev_comp[b])  # xb[b] consumed by step i-2
-            with torch.cuda.stream(s_in):
-                xb[b].copy_(xh, non_blocking=True)
-            ev_in[b].record(s_in)
-            stream.wait_event(ev_in[b])
-            stream.wait_event(ev_out[b])  # yb[b] read back by step i-2
-            with torch.cuda.stream(stream):
-                pl.execute(xb[b], tb[b])
-                pc.execute(tb[b], yb[b])
-            ev_comp[b].record(stream)
-            s_out.wait_event(ev_comp[b])
-            with torch.cuda.stream(s_out):
-                hyb[b].copy_(yb[b], non_blocking=True)
-            ev_out[b].record(s_out)
-        if h1 is not None:
-            h1.record(s_out)
-
+    host_steps(0, nbuf)
+    torch.cuda.synchronize()
+    barrier(world)
+    torch.cuda.synchronize()
     h0 = torch.cuda.Event(enable_timing=True)
     h1 = torch.cuda.Event(enable_timing=True)
-    if two_d:
-        for _ in range(2):
-            host_step()
-        torch.cuda.synchronize()
-        barrier(world)
-        torch.cuda.synchronize()
-        h0.record(stream)
-        for _ in range(e2e_steps):
-            host_step()
-        h1.record(stream)
-    else:
-        pipelined(2)
-        torch.cuda.synchronize()
-        barrier(world)
-        torch.cuda.synchronize()
-        pipelined(e2e_steps, h0, h1)
+    h0.record(stream)
+    for sb in streams:
+        sb.wait_event(h0)
+    host_steps(nbuf, e2e_steps)
+    for sb in streams:
+        e = torch.cuda.Event()
+        e.record(sb)
+        stream.wait_event(e)
+    h1.record(stream)
     torch.cuda.synchronize()
     barrier(world)
     e2e_ms = allreduce_max(h0.elapsed_time(h1), world)
     e2e_val = total_coeffs * e2e_steps / (e2e_ms / 1e3)
-    rt_host = None if two_d else float((hyb[(e2e_steps - 1) & 1] - xh).abs().max() / xh.abs().max())
+    last = (nbuf + e2e_steps - 1) % nbuf
+    rt_host = None if two_d else float((hy[last] - xh).abs().max() / xh.abs().max())
     bytes_vec = 8 * n * V
-    h2d = bytes_vec * (1 if (two_d and world > 1) else 2)
-    d2h = 8 * hy.numel() if two_d else 2 * bytes_vec
-    if two_d and world == 1:
+    if two_d and world > 1:
+        h2d, d2h = bytes_vec, 8 * n * C
+    else:
         h2d, d2h = 2 * bytes_vec, 2 * bytes_vec
-    if not two_d:
-        h2d, d2h = bytes_vec, bytes_vec
 
     cpu = None
     cfmm = None
-    if rank == 0 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(args.config, n, kind, budget_s=args.cpu_seconds)
+    if headline and rank == 0 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(config, n, kind, budget_s=args.cpu_seconds)
         try:
             cfmm = cpu_fmm_baseline(n, kind, dev, budget_s=args.cpu_seconds)
         except Exception as e:  # reported baseline only: never fail the GPU line for it
@@ -404,36 +433,62 @@ def run_gpu(args, world, rank, local):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": scaling,
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE.json recipe)",
-        "config": {"workload": (f"{args.config}: leg2cheb then cheb2leg (round trip) of {V} fp64 vector(s) "
+        "config": {"workload": (f"{config}: leg2cheb then cheb2leg (round trip) of {V} fp64 vector(s) "
                                 f"of n={n} per GPU") if not two_d else
                                (f"cfg5: 2-D leg2cheb of an {n}x{n} fp64 array (axis 1, all-to-all, axis 0), "
                                 f"{V} rows per GPU"), "n": n, "vectors_per_gpu": V, "N_padded": dl["N"],
                    "L": dl["L"], "s": dl["s"], "M": 18, "s_hat": 32, "transforms_per_step": 2,
                    "input_kind": kind,
                    "l2": f"no flush: per-step working set {2 * 8 * 324 * dl['nc'] / 1e6:.0f} MB of A_hat + "
-                         f"{3 * bytes_vec / 1e6:.0f} MB of vectors vs 126 MB L2" if dl["nc"] > 0 else "small",
+                         f"{3 * bytes_vec / 1e6:.0f} MB of vectors vs 126 MB L2" if dl["nc"] > 0 and
+                         2 * 8 * 324 * dl['nc'] + 3 * bytes_vec > 126e6 else
+                         ("no flush: per-step vectors " f"{3 * bytes_vec / 1e6:.0f} MB vs 126 MB L2"),
                    "graph": graph is not None, "kernel_cfg": {**{k: dl[k] for k in ("vt", "subtree", "stage_blocks",
-                                                                                    "stages")},
-                                                                 "engine": pl.kernel_info.get("engine", 1)}},
+                                                                                    "stages")}, "engine": engine}},
+        "step_ms": {"median": med_ms, "min": min_ms, "mean": ms / args.steps,
+                    "note": "per-step CUDA events between graph replays; max over ranks"},
         "roofline": roof,
         "roofline_transform": {"t_roof_us": t_roof * 1e6, "t_measured_us": t_meas * 1e6,
-                               "frac": t_roof / t_meas, "fp64_peak_tflops": FP64_PEAK_TFLOPS,
+                               "t_median_us": t_med * 1e6, "frac": t_roof / t_meas, "frac_median": t_roof / t_med,
+                               "fp64_peak_tflops": fp64_peak, "hbm_gbs": hbm,
                                "flops_alg_per_vector": dl["flops_alg"], "bytes_alg": dl["bytes_alg"]},
         "kernel_ms": {"leg2cheb": per_kernel[0], "cheb2leg": per_kernel[1], "names": names,
                       "algorithmic_bytes": [alg[nm] for nm in names],
-                      "achieved_gbs": [alg[nm] / (avg_ms[nm] * 1e-3) / 1e9 for nm in names]},
+                      "achieved_gbs": [alg[nm] / (avg_ms[nm] * 1e-3) / 1e9 for nm in names],
+                      "note": "lc_execute_timed puts an event between kernels, so they run without their PDL "
+                              "overlap: per-kernel times sum to more than the graph-replayed step"},
+        "plan": plan_info,
         "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "steps": e2e_steps, "ms_per_step": e2e_ms / e2e_steps,
-                "path": ("pinned host vector -> H2D -> leg2cheb -> cheb2leg (lc_execute) -> D2H, pipelined over "
-                         "three streams with double-buffered device arrays") if not two_d else
-                        ("lc_execute_host (C ABI, pinned host buffers) x2 per step" if world == 1
-                         else "H2D + tensor_product_2d (NCCL all-to-all) + D2H")},
-        "gpu_launches": kpe * 2 * args.steps,
+                "path": ("lc_execute_host (C ABI: pinned host buffer -> H2D -> kernels -> D2H) for leg2cheb, then "
+                         "for cheb2leg of the host result; 3 streams with caller-owned staging/workspaces")
+                        if not (two_d and world > 1) else
+                        "H2D + tensor_product_2d (NCCL all-to-all) + D2H, 3 streams"},
+        "gpu_launches": (kpe + pc.kernels_per_execute) * args.steps,
         "clocks": clk,
         "round_trip_einf": {"device": rt, "host_path": rt_host},
-        "cpu_baseline": cpu,
-        "cpu_fmm_baseline": cfmm,
     }
+    if passes is not None:
+        line["passes_ms"] = passes
+    if headline:
+        line["cpu_baseline"] = cpu
+        line["cpu_fmm_baseline"] = cfmm
+    for p in (pl, pc):
+        p.close()
+    return line
+
+
+def run_gpu(args, world, rank, local):
+    line = measure(args.config, args, world, rank, local, headline=True)
+    if args.batched != "none" and args.batched != args.config:
+        # the batched half of the metric ("at N=1e6 & batched"): cfg3 by default, sharded over the ranks
+        sub = measure(args.batched, args, world, rank, local, headline=False)
+        line["batched"] = {k: sub[k] for k in ("metric", "value", "unit", "n_gpus", "ms_per_step", "scaling",
+                                                "config", "step_ms", "roofline", "roofline_transform", "kernel_ms",
+                                                "plan", "e2e", "gpu_launches", "clocks", "round_trip_einf")
+                           if k in sub}
+        if "passes_ms" in sub:
+            line["batched"]["passes_ms"] = sub["passes_ms"]
     return line
 
 
@@ -488,25 +543,37 @@ def cpu_baseline(config, n, kind, budget_s=15.0):
 
 
 def cpu_fmm_baseline(n, kind, dev, budget_s=10.0):
-    """The same O(N) algorithm on the host cores (cpu_fmm/, C + OpenMP, plan tables exported from the
-    GPU plans): leg2cheb then cheb2leg of vector 0, repeated within the time budget (at least once)."""
+    """The same O(N) algorithm on the host (cpu_fmm/, C + OpenMP over the blocks of each step, plan tables
+    exported from the GPU plans): leg2cheb then cheb2leg of vector 0, on ONE core (the paper's setting,
+    PAPER.md:563: ~20 ms per 1e6 transform single-threaded on an M3) and on all host cores (PAPER.md:585);
+    fastest and median of the repetitions that fit the budget (the paper reports the fastest)."""
     import cpu_fmm
     from lc_inputs import vector
     from paper_2411_00033_b200 import Plan
-    a = cpu_fmm.CpuFmm(Plan(n, "leg2cheb", device=dev))
-    b = cpu_fmm.CpuFmm(Plan(n, "cheb2leg", device=dev))
+    pa, pb = Plan(n, "leg2cheb", device=dev), Plan(n, "cheb2leg", device=dev)
+    a, b = cpu_fmm.CpuFmm(pa), cpu_fmm.CpuFmm(pb)
+    pa.close()
+    pb.close()
     f = vector(kind, n, seed=0, v=0)
-    reps, t0 = 0, time.perf_counter()
-    while True:
-        b(a(f))
-        reps += 1
-        dt = time.perf_counter() - t0
-        if dt > budget_s / 2 or reps >= 50:
-            break
-    return {"value": 2 * n * reps / dt, "unit": UNIT, "cores": cpu_fmm.threads(),
-            "kind": "cpu O(N) FMM: the same algorithm in C + OpenMP (plan tables from the GPU plan)",
-            "sample": f"{reps} round trip(s) (leg2cheb then cheb2leg) of vector 0 at n={n}; {dt:.2f} s",
-            "seconds": dt}
+    cores = len(os.sched_getaffinity(0))
+    out = {"unit": UNIT, "kind": "cpu O(N) FMM: the same algorithm in C + OpenMP (plan tables from the GPU plan)"}
+    for label, t in (("one_core", 1), ("all_cores", cores)):
+        cpu_fmm.set_threads(t)
+        b(a(f))  # warm-up
+        times, t0 = [], time.perf_counter()
+        while True:
+            t1 = time.perf_counter()
+            b(a(f))
+            times.append(time.perf_counter() - t1)
+            if time.perf_counter() - t0 > budget_s / 4 or len(times) >= 50:
+                break
+        out[label] = {"value": 2 * n / min(times), "value_median": 2 * n / statistics.median(times), "cores": t,
+                      "reps": len(times), "ms_per_transform_min": min(times) / 2 * 1e3,
+                      "ms_per_transform_median": statistics.median(times) / 2 * 1e3}
+    cpu_fmm.set_threads(cores)
+    out.update(value=out["all_cores"]["value"], cores=cores,
+               sample=f"round trips (leg2cheb then cheb2leg) of vector 0 at n={n}; fastest of the repetitions")
+    return out
 
 
 def run_reference(args, world, rank):
@@ -564,9 +631,20 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-seconds", type=float, default=60.0)
     ap.add_argument("--e2e-steps", type=int, default=200)
+    ap.add_argument("--batched", default="cfg3", choices=["cfg3", "cfg4", "cfg5", "none"],
+                    help="batched sub-record measured after the headline config (the metric's 'batched' half)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # not launched by torchrun: launch one process per GPU ourselves (same flags)
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+        os.execv(sys.executable, cmd)
     if args.impl == "reference":
         # CPU oracle arm: rank 0 alone runs it; other ranks exit 0 without work (no process group needed)
         world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -576,6 +654,8 @@ def main():
             print(json.dumps(line), flush=True)
         return
     world, rank, local = dist_setup()
+    if world != args.gpus and rank == 0:
+        print(f"[bench] --gpus {args.gpus} but WORLD_SIZE={world}: measuring {world} rank(s)", file=sys.stderr)
     line = run_gpu(args, world, rank, local)
     if rank == 0 and line is not None:
         print(json.dumps(line), flush=True)

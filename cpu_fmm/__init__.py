@@ -29,12 +29,18 @@ def load():
                                         d, d, d, d, d, d, d]
         lib.cpu_fmm_execute.restype = ctypes.c_int
         lib.cpu_fmm_threads.restype = ctypes.c_int
+        lib.cpu_fmm_set_threads.argtypes = [ctypes.c_int]
+        lib.cpu_fmm_set_threads.restype = None
         _lib = lib
     return _lib
 
 
 def threads() -> int:
     return int(load().cpu_fmm_threads())
+
+
+def set_threads(t: int) -> None:
+    load().cpu_fmm_set_threads(int(t))
 
 
 class CpuFmm:

@@ -151,3 +151,13 @@ int cpu_fmm_threads(void) {
   return 1;
 #endif
 }
+
+/* thread count of the following cpu_fmm_execute calls (bench.py: 1 core and all cores) */
+void cpu_fmm_set_threads(int t) {
+#ifdef _OPENMP
+  extern void omp_set_num_threads(int);
+  omp_set_num_threads(t > 0 ? t : 1);
+#else
+  (void)t;
+#endif
+}

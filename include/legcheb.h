@@ -28,10 +28,14 @@
  *  - Nothing here throws; every function returns an lc_status.  A CUDA
  *    error detected during a call is returned as LC_ERR_CUDA; asynchronous
  *    kernel faults surface at the caller's next synchronisation.
- *  - Thread safety: a plan is immutable after lc_plan_create and may be
- *    shared by threads; concurrent lc_execute calls on one plan need
- *    distinct workspaces (a NULL workspace means the plan-owned one, which
- *    serialises calls on one stream only).
+ *  - Thread safety: a plan is immutable after lc_plan_create (its only
+ *    mutable state -- the lazily allocated lc_execute_host staging and the
+ *    per-stream record of executions used by lc_plan_destroy -- is guarded by
+ *    a per-plan mutex) and may be shared by threads.  Concurrent lc_execute /
+ *    lc_execute_host calls on one plan need distinct workspaces (and, for
+ *    lc_execute_host, distinct staging buffers); a NULL workspace or staging
+ *    means the plan-owned one, which is safe only for calls serialised on one
+ *    stream.
  */
 #ifndef LEGCHEB_H_
 #define LEGCHEB_H_
@@ -98,6 +102,7 @@ typedef struct {
   double bytes_alg;   /* algorithmic HBM bytes per execute: 16 n batch + 8 M^2 N_c + 8 N */
   int32_t vt, subtree, stage_blocks, stages; /* chosen kernel configuration */
   int32_t kernels_per_execute;               /* kernel launches per lc_execute */
+  double plan_device_ms;                     /* device time of the planning kernels at create (CUDA events) */
 } lc_plan_desc;
 
 /* Host-only geometry (no GPU needed): fills n, N, L, s, M, nc, band_nnz,
@@ -126,6 +131,10 @@ lc_status lc_workspace_init(const lc_plan* p, void* workspace, void* stream);
 
 /* Execute the transform of `batch` vectors: out = T(in), enqueue-only on
  * `stream` (a cudaStream_t; NULL = legacy default stream).
+ *   T = C^{-1} A (leg2cheb) or A^{-1} C (cheb2leg) of PAPER.md:29-32 (eq:directmv),
+ *   evaluated by Alg. 4 (alg:fastercomplete) with the plan's
+ *   hierarchy; the result equals the plain definition within the FMM's
+ *   accuracy (relative max norm <= 1e-12 for n <= 1e6, PAPER.md:527 eq:Einf).
  *   in:  device, batch vectors of n doubles in the plan's layout; unmodified.
  *   out: device, same shape; must not overlap in (LC_ERR_ALIASING).
  *   workspace: device, >= lc_workspace_bytes(p), zero-initialised once, or
@@ -139,11 +148,23 @@ lc_status lc_execute(const lc_plan* p, const double* in, double* out, void* work
 lc_status lc_execute_timed(const lc_plan* p, const double* in, double* out, void* workspace, void* stream,
                            void* const* ev, int32_t nev);
 
-/* End-to-end call with HOST buffers: copies h_in (batch vectors, layout and
- * leading dimensions of the plan) to plan-owned device staging, executes,
- * copies the result to h_out, all enqueued on stream (no host sync).  Host
- * buffers should be page-locked for asynchronous copies. */
-lc_status lc_execute_host(const lc_plan* p, const double* h_in, double* h_out, void* stream);
+/* Bytes of the device staging buffer lc_execute_host needs (input and
+ * output staging, each rounded up to 256 bytes). */
+size_t lc_host_stage_bytes(const lc_plan* p);
+
+/* End-to-end call with HOST buffers (the transform of lc_execute): copies
+ * h_in (batch vectors, layout and leading dimensions of the plan) to device
+ * staging, executes, copies the result to h_out, all enqueued on stream (no
+ * host sync; h_out is valid after the stream is synchronised).
+ *   d_stage: device, >= lc_host_stage_bytes(p), caller-owned; or NULL for the
+ *            plan-owned staging (allocated once on first use, under the plan's
+ *            mutex; calls with NULL must be serialised on one stream).
+ *   workspace: as for lc_execute (NULL = plan-owned).
+ * Host buffers should be page-locked for asynchronous copies (pageable ones
+ * make the copies synchronous).  Errors: INVALID_ARG, OUT_OF_MEMORY (staging),
+ * CUDA. */
+lc_status lc_execute_host(const lc_plan* p, const double* h_in, double* h_out, void* d_stage, void* workspace,
+                          void* stream);
 
 /* Copy plan data to host memory (synchronous; test/diagnostic use).
  * what: 0 band table B (length N: lambda_m for L2C, rho_m for C2L),
@@ -161,8 +182,13 @@ lc_status lc_plan_export(const lc_plan* p, int32_t what, double* host_out, int64
  * values written through *written (may be NULL).  Errors: INVALID_ARG on NULL p or out. */
 lc_status lc_plan_kernel_info(const lc_plan* p, int64_t* out, int32_t count, int32_t* written);
 
-/* Frees the plan's device arrays and its own workspace after synchronizing the plan's device
- * (executions still in flight may read them).  Errors: INVALID_ARG on NULL p. */
+/* Frees the plan's device arrays, its own workspace and staging.  The frees
+ * are stream-ordered after the last lc_execute / lc_execute_host of the plan
+ * on every stream it was used on (the plan records one event per stream), and
+ * the call returns when that work is done; unrelated streams are not waited
+ * for.  Executions captured into CUDA graphs are not tracked: the caller must
+ * finish such graph launches first.  Caller-owned workspaces are the caller's.
+ * Errors: INVALID_ARG on NULL p. */
 lc_status lc_plan_destroy(lc_plan* p);
 
 const char* lc_status_string(lc_status s);

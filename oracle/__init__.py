@@ -15,6 +15,8 @@ lam(n)                     lambda_k = Lambda(k), k < n
 l2c_rows(f, rows)          rows of C^{-1} A f                 PAPER.md:24-46, Alg. 1
 c2l_rows(f, rows)          rows of A^{-1} C f (eq:Lxymod rows) PAPER.md:31, 509-514
 c2l_backsub(f)             A^{-1} C f by back-substitution
+l2c_rows_q, c2l_rows_q     the same rows in __float128 with plain sums (cross-check tier of the
+                           compensated long-double sums)
 l2c(f), c2l(f)             all rows
 einf(z, zstar)             ||z - z*||_inf / ||z*||_inf        PAPER.md:527 (eq:Einf)
 """
@@ -40,7 +42,7 @@ def build(force: bool = False) -> str:
     """Compile oracle.c -> liboracle.so with gcc (no fast-math)."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
         cmd = ["gcc", "-O2", "-fno-fast-math", "-ffp-contract=off", "-fopenmp", "-shared", "-fPIC",
-               _SRC, "-o", _LIB, "-lm"]
+               _SRC, "-o", _LIB, "-lquadmath", "-lm"]
         subprocess.run(cmd, check=True)
     return _LIB
 
@@ -55,6 +57,10 @@ def _get():
         for name in ("orc_l2c_rows", "orc_c2l_rows"):
             fn = getattr(lib, name)
             fn.argtypes = [_ldp, ctypes.c_long, _lp, ctypes.c_long, _ldp, _ldp]
+            fn.restype = ctypes.c_int
+        for name in ("orc_l2c_rows_q", "orc_c2l_rows_q"):
+            fn = getattr(lib, name)
+            fn.argtypes = [_ldp, ctypes.c_long, _lp, ctypes.c_long, _ldp, ctypes.c_int]
             fn.restype = ctypes.c_int
         lib.orc_c2l_backsub.argtypes = [_ldp, ctypes.c_long, _ldp]
         lib.orc_c2l_backsub.restype = ctypes.c_int
@@ -95,6 +101,30 @@ def l2c_rows(f, rows=None, with_abs: bool = False):
 
 def c2l_rows(f, rows=None, with_abs: bool = False):
     return _rows(_get().orc_c2l_rows, f, rows, with_abs)
+
+
+def _rows_q(fn, f, rows, lam_ld):
+    f = _ld(f)
+    rows = np.ascontiguousarray(np.asarray(rows, dtype=np.int64))
+    if rows.size and (rows.min() < 0 or rows.max() >= f.shape[0]):
+        raise IndexError("row out of range")
+    out = np.empty(rows.shape[0], dtype=LD)
+    rc = fn(f.ctypes.data_as(_ldp), f.shape[0], rows.ctypes.data_as(_lp), rows.shape[0], out.ctypes.data_as(_ldp),
+            int(bool(lam_ld)))
+    if rc:
+        raise RuntimeError(f"oracle failed rc={rc}")
+    return out
+
+
+def l2c_rows_q(f, rows, lam_ld: bool = False):
+    """L2C rows in __float128 (plain sums): the cross-check tier of l2c_rows.  lam_ld: use the
+    long-double lambda (isolates the summation) instead of the quad recurrence."""
+    return _rows_q(_get().orc_l2c_rows_q, f, rows, lam_ld)
+
+
+def c2l_rows_q(f, rows, lam_ld: bool = False):
+    """C2L rows (eq:Lxymod) in __float128 (plain sums): the cross-check tier of c2l_rows."""
+    return _rows_q(_get().orc_c2l_rows_q, f, rows, lam_ld)
 
 
 def c2l_backsub(f) -> np.ndarray:

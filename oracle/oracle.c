@@ -33,6 +33,7 @@
  * (never -ffast-math: it deletes the compensation terms).
  */
 #include <math.h>
+#include <quadmath.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -141,4 +142,69 @@ int orc_transform(int dir, const long double* f, long n, long double* out) {
   int rc = dir == 0 ? orc_l2c_rows(f, n, rows, n, out, NULL) : orc_c2l_rows(f, n, rows, n, out, NULL);
   free(rows);
   return rc;
+}
+
+/* ---------------------------------------------------------------------------
+ * Cross-check tier ("oracle summation" pin): the same row
+ * definitions as orc_l2c_rows / orc_c2l_rows, evaluated in __float128
+ * (libquadmath, 113-bit significand) with plain sums -- no compensation -- so
+ * that the compensated long-double sums above can be checked at n >= 1e6.
+ * lambda by the same recurrence from sqrt(pi), either in
+ * quad (lam_ld = 0: pins the whole long-double oracle, lambda error included)
+ * or widened from the long-double recurrence (lam_ld = 1: both sides use the
+ * same lambda, isolating the summation).  Results are rounded to long double.
+ * ------------------------------------------------------------------------- */
+static __float128* orc_lambda_q(long n, int lam_ld) {
+  __float128* lam = (__float128*)malloc(sizeof(__float128) * (size_t)n);
+  if (!lam) return NULL;
+  if (lam_ld) {
+    long double* l = (long double*)malloc(sizeof(long double) * (size_t)n);
+    if (!l) { free(lam); return NULL; }
+    orc_lambda(n, l);
+    for (long i = 0; i < n; ++i) lam[i] = (__float128)l[i];
+    free(l);
+    return lam;
+  }
+  lam[0] = sqrtq(M_PIq);
+  for (long i = 1; i < n; ++i) lam[i] = lam[i - 1] * ((__float128)i - 0.5Q) / (__float128)i;
+  return lam;
+}
+
+int orc_l2c_rows_q(const long double* f, long n, const long* rows, long R, long double* out, int lam_ld) {
+  if (n <= 0) return 1;
+  __float128* lam = orc_lambda_q(n, lam_ld);
+  if (!lam) return 2;
+#pragma omp parallel for schedule(dynamic, 1)
+  for (long r = 0; r < R; ++r) {
+    long i = rows[r];
+    __float128 a = 0;
+    for (long k = 0; i + 2 * k < n; ++k) a += lam[k] * lam[i + k] * (__float128)f[i + 2 * k];
+    out[r] = (long double)((i == 0 ? 1.0Q : 2.0Q) / M_PIq * a);
+  }
+  free(lam);
+  return 0;
+}
+
+int orc_c2l_rows_q(const long double* f, long n, const long* rows, long R, long double* out, int lam_ld) {
+  if (n <= 0) return 1;
+  __float128* lam = orc_lambda_q(n, lam_ld);
+  if (!lam) return 2;
+#pragma omp parallel for schedule(dynamic, 1)
+  for (long r = 0; r < R; ++r) {
+    long i = rows[r];
+    __float128 a = 0;
+    for (long k = 0; i + 2 * k < n; ++k) {
+      __float128 e;
+      if (i == 0 && k == 0) {
+        e = 1;
+      } else {
+        __float128 x = i, y = i + 2 * k;  /* eq:Lxymod at (x, y) = (i, i+2k) */
+        e = 2 * (x + 0.5Q) * y / ((x + y) * (x + y + 1) * (x - y + 1)) * (lam[k] / lam[i + k]);
+      }
+      a += e * (__float128)f[i + 2 * k];
+    }
+    out[r] = (long double)a;
+  }
+  free(lam);
+  return 0;
 }

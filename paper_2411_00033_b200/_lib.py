@@ -29,7 +29,7 @@ class PlanDesc(ctypes.Structure):
                 ("nc", c_i64), ("direction", c_i64), ("band_nnz", c_i64), ("plan_bytes", ctypes.c_size_t),
                 ("workspace_bytes", ctypes.c_size_t), ("flops_alg", ctypes.c_double), ("bytes_alg", ctypes.c_double),
                 ("vt", c_i32), ("subtree", c_i32), ("stage_blocks", c_i32), ("stages", c_i32),
-                ("kernels_per_execute", c_i32)]
+                ("kernels_per_execute", c_i32), ("plan_device_ms", ctypes.c_double)]
 
     def as_dict(self):
         return {name: getattr(self, name) for name, _ in self._fields_}
@@ -44,7 +44,8 @@ SIGNATURES = {
     "lc_workspace_init": (c_i32, [c_vp, c_vp, c_vp]),
     "lc_execute": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_vp]),
     "lc_execute_timed": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_vp, ctypes.POINTER(c_vp), c_i32]),
-    "lc_execute_host": (c_i32, [c_vp, c_vp, c_vp, c_vp]),
+    "lc_host_stage_bytes": (ctypes.c_size_t, [c_vp]),
+    "lc_execute_host": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "lc_plan_export": (c_i32, [c_vp, c_i32, c_dp, c_i64]),
     "lc_plan_kernel_info": (c_i32, [c_vp, ctypes.POINTER(c_i64), c_i32, ctypes.POINTER(c_i32)]),
     "lc_plan_destroy": (c_i32, [c_vp]),

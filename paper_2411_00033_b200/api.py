@@ -29,9 +29,10 @@ def geometry(n: int, s_hat: int = 32) -> dict:
     return d.as_dict()
 
 
-def _stream_handle(stream) -> int:
+def _stream_handle(stream, device=None) -> int:
+    """cudaStream_t of `stream`; None -> torch's current stream of `device` (the plan's device)."""
     if stream is None:
-        stream = torch.cuda.current_stream()
+        stream = torch.cuda.current_stream(device)
     return int(stream.cuda_stream) if hasattr(stream, "cuda_stream") else int(stream)
 
 
@@ -65,6 +66,8 @@ class Plan:
         self.desc = d.as_dict()
         self.ld_in = ld_in or (self.n if self.layout == 0 else self.batch)
         self.ld_out = ld_out or (self.n if self.layout == 0 else self.batch)
+        self._ws_lock = threading.Lock()
+        self._ws_by_stream: dict = {}
 
     # -- lifetime
     def close(self):
@@ -113,11 +116,35 @@ class Plan:
         if x.numel() < (rows - 1) * ld + cols:  # the extent the kernels address (rows of stride ld)
             raise ValueError(f"{what}: {x.numel()} elements, the plan addresses {(rows - 1) * ld + cols}")
 
+    @property
+    def plan_device_ms(self) -> float:
+        """Device time of the planning kernels measured at create (CUDA events)."""
+        return float(self.desc["plan_device_ms"])
+
+    @property
+    def host_stage_bytes(self) -> int:
+        return int(self._lib.lc_host_stage_bytes(self._h))
+
     def new_workspace(self, stream=None) -> torch.Tensor:
         ws = torch.empty(max(1, self.workspace_bytes), dtype=torch.uint8, device=self.device)
-        _lib.check("lc_workspace_init", self._lib.lc_workspace_init(self._h, ctypes.c_void_p(ws.data_ptr()),
-                                                                    ctypes.c_void_p(_stream_handle(stream))))
+        _lib.check("lc_workspace_init", self._lib.lc_workspace_init(
+            self._h, ctypes.c_void_p(ws.data_ptr()), ctypes.c_void_p(_stream_handle(stream, self.device))))
         return ws
+
+    def new_host_stage(self) -> torch.Tensor:
+        """Caller-owned device staging for execute_host (lc_host_stage_bytes)."""
+        return torch.empty(max(1, self.host_stage_bytes), dtype=torch.uint8, device=self.device)
+
+    def workspace_for(self, stream=None) -> torch.Tensor:
+        """A workspace owned by this Plan object for one stream (created on first use), so that calls
+        on different streams never share the counters and flags a workspace holds (legcheb.h)."""
+        h = _stream_handle(stream, self.device)
+        with self._ws_lock:
+            ws = self._ws_by_stream.get(h)
+            if ws is None:
+                ws = self.new_workspace(stream)
+                self._ws_by_stream[h] = ws
+            return ws
 
     # -- execution
     def execute(self, x: torch.Tensor, out: torch.Tensor | None = None, workspace: torch.Tensor | None = None,
@@ -130,7 +157,7 @@ class Plan:
         ws = ctypes.c_void_p(workspace.data_ptr()) if workspace is not None else ctypes.c_void_p()
         _lib.check("lc_execute", self._lib.lc_execute(self._h, ctypes.c_void_p(x.data_ptr()),
                                                       ctypes.c_void_p(out.data_ptr()), ws,
-                                                      ctypes.c_void_p(_stream_handle(stream))))
+                                                      ctypes.c_void_p(_stream_handle(stream, self.device))))
         return out
 
     def execute_timed(self, x: torch.Tensor, out: torch.Tensor, events, stream=None) -> None:
@@ -141,16 +168,27 @@ class Plan:
         arr = (ctypes.c_void_p * len(events))(*[ctypes.c_void_p(e.cuda_event) for e in events])
         _lib.check("lc_execute_timed", self._lib.lc_execute_timed(
             self._h, ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(),
-            ctypes.c_void_p(_stream_handle(stream)), arr, len(events)))
+            ctypes.c_void_p(_stream_handle(stream, self.device)), arr, len(events)))
 
-    def execute_host(self, h_in: torch.Tensor, h_out: torch.Tensor, stream=None) -> None:
-        """End-to-end call with HOST buffers (H2D, transform, D2H enqueued on stream; no sync)."""
-        for t in (h_in, h_out):
+    def execute_host(self, h_in: torch.Tensor, h_out: torch.Tensor, stream=None, stage: torch.Tensor | None = None,
+                     workspace: torch.Tensor | None = None) -> None:
+        """End-to-end call with HOST buffers (lc_execute_host: H2D, transform, D2H enqueued on stream; no
+        sync).  stage / workspace: caller-owned device buffers (new_host_stage / new_workspace), or None
+        for the plan-owned ones (then calls must be serialised on one stream)."""
+        rows, cols = (self.batch, self.n) if self.layout == 0 else (self.n, self.batch)
+        for t, ld in ((h_in, self.ld_in), (h_out, self.ld_out)):
             if t.device.type != "cpu" or t.dtype != torch.float64 or not t.is_contiguous():
                 raise ValueError("execute_host needs contiguous float64 host tensors")
+            if t.numel() < (rows - 1) * ld + cols:
+                raise ValueError(f"execute_host: {t.numel()} elements, the plan addresses {(rows - 1) * ld + cols}")
+        if stage is not None and (stage.device != self.device or stage.numel() * stage.element_size() <
+                                  self.host_stage_bytes):
+            raise ValueError(f"stage: need {self.host_stage_bytes} bytes on {self.device}")
         _lib.check("lc_execute_host", self._lib.lc_execute_host(
             self._h, ctypes.c_void_p(h_in.data_ptr()), ctypes.c_void_p(h_out.data_ptr()),
-            ctypes.c_void_p(_stream_handle(stream))))
+            ctypes.c_void_p(stage.data_ptr() if stage is not None else None),
+            ctypes.c_void_p(workspace.data_ptr() if workspace is not None else None),
+            ctypes.c_void_p(_stream_handle(stream, self.device))))
 
     def export(self, what: str) -> np.ndarray:
         """Copy plan data to the host: tabB, tabA, ahat, B, T (tests/diagnostics)."""
@@ -183,7 +221,7 @@ def _run(x: torch.Tensor, direction) -> torch.Tensor:
         raise ValueError("expected [n] or [batch, n]")
     x2 = x2.contiguous()
     p = _cached(x2.shape[1], direction, x2.shape[0], x2.device)
-    out = p.execute(x2)
+    out = p.execute(x2, workspace=p.workspace_for())  # one workspace per stream: safe across streams/threads
     return out.reshape(-1) if squeeze else out
 
 

@@ -22,6 +22,8 @@
 //   of 8-vector subtrees; writes w of every level), then lc_range_kernel, the same pass as engine 2
 //   over ranges of leaves of each tile with w read from the workspace.
 #include <algorithm>
+#include <atomic>
+#include <mutex>
 #include <cstdio>
 #include <cstring>
 
@@ -2420,7 +2422,8 @@ static cudaError_t set_attrs_all(int smax) {
   return e;
 }
 
-static bool g_device_ready[64] = {false};
+static std::atomic<bool> g_device_ready[64];
+static std::mutex g_config_mu;  // cudaFuncSetAttribute of the kernels, once per device
 
 template <int VT>
 static int stream_occupancy(int dir, size_t smem) {
@@ -2445,7 +2448,8 @@ lc_status configure_kernels(lc_plan* p) {
   cudaError_t ea = cudaDeviceGetAttribute(&smax, cudaDevAttrMaxSharedMemoryPerBlockOptin, p->device);
   if (ea != cudaSuccess) return record_cuda_error(ea);
   if (p->device < 0 || p->device >= 64) return LC_ERR_INVALID_ARG;
-  if (!g_device_ready[p->device]) {
+  std::unique_lock<std::mutex> cfg_lock(g_config_mu);
+  if (!g_device_ready[p->device].load()) {
     ea = set_attrs_all<32>(smax);
     if (ea == cudaSuccess) ea = set_attrs_all<64>(smax);
     if (ea == cudaSuccess) ea = set_max_dyn_smem(lc_tile_kernel<0>, smax);
@@ -2456,8 +2460,9 @@ lc_status configure_kernels(lc_plan* p) {
     if (ea == cudaSuccess) ea = set_max_dyn_smem(lc_range_kernel<0, 1>, smax);
     if (ea == cudaSuccess) ea = set_max_dyn_smem(lc_range_kernel<1, 1>, smax);
     if (ea != cudaSuccess) return record_cuda_error(ea);
-    g_device_ready[p->device] = true;
+    g_device_ready[p->device].store(true);
   }
+  cfg_lock.unlock();
   smax -= 256;  // static shared memory of the kernels
   const int L = int(p->L);
   if (L > 0 && L - 1 > 62) return LC_ERR_INVALID_ARG;
@@ -2705,8 +2710,8 @@ static cudaError_t launch_dispatch(const lc_plan* p, const UpParams& up, const S
   return cudaErrorInvalidValue;
 }
 
-lc_status launch_execute(const lc_plan* p, const double* in, double* out, void* ws, cudaStream_t st,
-                         cudaEvent_t const* ev, int nev) {
+static lc_status launch_execute_impl(const lc_plan* p, const double* in, double* out, void* ws, cudaStream_t st,
+                                     cudaEvent_t const* ev, int nev) {
   if (!p || !in || !out) return LC_ERR_INVALID_ARG;
   {
     const char* a0 = reinterpret_cast<const char*>(in);
@@ -2819,6 +2824,20 @@ lc_status launch_execute(const lc_plan* p, const double* in, double* out, void* 
   return e == cudaSuccess ? LC_OK : record_cuda_error(e);
 }
 
+lc_status launch_execute(const lc_plan* p, const double* in, double* out, void* ws, cudaStream_t st,
+                         cudaEvent_t const* ev, int nev) {
+  if (!p) return LC_ERR_INVALID_ARG;
+  const lc_status rc = launch_execute_impl(p, in, out, ws, st, ev, nev);
+  if (rc == LC_OK) {
+    int prev = 0;
+    cudaGetDevice(&prev);
+    if (prev != p->device) cudaSetDevice(p->device);
+    note_execute(p, st);
+    if (prev != p->device) cudaSetDevice(prev);
+  }
+  return rc;
+}
+
 }  // namespace lc
 
 extern "C" lc_status lc_plan_kernel_info(const lc_plan* p, int64_t* out, int32_t count, int32_t* written) {
@@ -2844,36 +2863,33 @@ extern "C" lc_status lc_execute_timed(const lc_plan* p, const double* in, double
   return lc::launch_execute(p, in, out, ws, (cudaStream_t)stream, reinterpret_cast<cudaEvent_t const*>(ev), nev);
 }
 
-extern "C" lc_status lc_execute_host(const lc_plan* p_, const double* h_in, double* h_out, void* stream) {
-  lc_plan* p = const_cast<lc_plan*>(p_);
+extern "C" lc_status lc_execute_host(const lc_plan* p, const double* h_in, double* h_out, void* d_stage,
+                                     void* ws, void* stream) {
   if (!p || !h_in || !h_out) return LC_ERR_INVALID_ARG;
   const int64_t ein = lc::extent(p->layout, p->ld_in, p->n, p->batch);
   const int64_t eout = lc::extent(p->layout, p->ld_out, p->n, p->batch);
   int prev = 0;
   cudaGetDevice(&prev);
-  cudaSetDevice(p->device);
-  const size_t need = size_t(std::max(ein, eout)) * 8;
-  if (p->stage_bytes < need) {
-    cudaFree(p->d_stage_in);
-    cudaFree(p->d_stage_out);
-    p->d_stage_in = p->d_stage_out = nullptr;
-    p->stage_bytes = 0;
-    if (cudaMalloc(&p->d_stage_in, need) != cudaSuccess || cudaMalloc(&p->d_stage_out, need) != cudaSuccess) {
-      cudaSetDevice(prev);
-      return LC_ERR_OUT_OF_MEMORY;
-    }
-    p->stage_bytes = need;
+  if (prev != p->device) cudaSetDevice(p->device);
+  double* stage = static_cast<double*>(d_stage);
+  if (!stage) stage = lc::plan_stage(p);  // plan-owned, allocated once under the plan's mutex
+  if (!stage) {
+    if (prev != p->device) cudaSetDevice(prev);
+    return LC_ERR_OUT_OF_MEMORY;
   }
+  double* d_in = stage;
+  double* d_out = reinterpret_cast<double*>(reinterpret_cast<char*>(stage) + lc::align_up(ein * 8, 256));
   cudaStream_t st = (cudaStream_t)stream;
   lc_status rc = LC_OK;
-  cudaError_t e = cudaMemcpyAsync(p->d_stage_in, h_in, size_t(ein) * 8, cudaMemcpyHostToDevice, st);
+  cudaError_t e = cudaMemcpyAsync(d_in, h_in, size_t(ein) * 8, cudaMemcpyHostToDevice, st);
   if (e != cudaSuccess) rc = lc::record_cuda_error(e);
-  if (rc == LC_OK) rc = lc::launch_execute(p, p->d_stage_in, p->d_stage_out, nullptr, st, nullptr, 0);
+  if (rc == LC_OK) rc = lc::launch_execute(p, d_in, d_out, ws, st, nullptr, 0);
   if (rc == LC_OK) {
-    e = cudaMemcpyAsync(h_out, p->d_stage_out, size_t(eout) * 8, cudaMemcpyDeviceToHost, st);
+    e = cudaMemcpyAsync(h_out, d_out, size_t(eout) * 8, cudaMemcpyDeviceToHost, st);
     if (e != cudaSuccess) rc = lc::record_cuda_error(e);
+    else lc::note_execute(p, st);  // destroy also waits for the read-back of the staging
   }
-  cudaSetDevice(prev);
+  if (prev != p->device) cudaSetDevice(prev);
   return rc;
 }
 

@@ -144,9 +144,11 @@ struct lc_plan {
   double* d_Tt;     // [2][M][s]
   double* d_B;      // [M][M]
   void* d_ws;       // plan-owned workspace
-  double* d_stage_in;   // lc_execute_host staging (lazy)
-  double* d_stage_out;
-  size_t stage_bytes;
+  double* d_stage;      // plan-owned lc_execute_host staging (allocated once, on first use, under sync->mu)
+  size_t stage_bytes;   // lc_host_stage_bytes(): input staging + output staging, 256-byte aligned halves
+  cudaStream_t own;     // plan-internal non-blocking stream: planning kernels, allocations, frees
+  struct lc_plan_sync* sync;  // host-only: mutex + last-execute event per stream (lc_plan.cu)
+  double plan_ms;       // device time of the planning kernels (CUDA events on `own`)
   int64_t band_nnz;
   double flops_alg, bytes_alg;
   size_t plan_bytes;
@@ -157,6 +159,11 @@ namespace lc {
 lc_status record_cuda_error(cudaError_t e);
 lc_status launch_execute(const lc_plan* p, const double* in, double* out, void* ws, cudaStream_t st,
                          cudaEvent_t const* ev, int nev);
+// records that p was used on stream st (after the enqueued work) so lc_plan_destroy can wait for it;
+// a no-op on a capturing stream (graph launches are the caller's to finish before destroy)
+void note_execute(const lc_plan* p, cudaStream_t st);
+// the plan-owned lc_execute_host staging (allocated once, thread-safe), or nullptr on failure
+double* plan_stage(const lc_plan* p);
 int64_t band_nnz(int64_t N, int64_t s);
 // engine 3's persistent up pass (lc_up3_kernel, 8 vectors, s <= 32): constants, two f buffers,
 // the subtree tree, kc waiting left siblings and two merged parents

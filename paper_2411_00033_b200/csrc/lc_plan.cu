@@ -19,9 +19,19 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
+#include <utility>
 #include <vector>
 
 #include "lc_internal.h"
+
+// Host-side synchronisation state of a plan: a mutex for the lazily allocated lc_execute_host
+// staging and the last-execute event of every stream the plan was executed on, so that
+// lc_plan_destroy waits for the plan's own work only (never for the whole device).
+struct lc_plan_sync {
+  std::mutex mu;
+  std::vector<std::pair<cudaStream_t, cudaEvent_t>> seen;
+};
 
 namespace lc {
 
@@ -80,59 +90,125 @@ __global__ void plan_taba_kernel(double* tabA, int64_t n2s, int dir) {
   }
 }
 
-// One CTA per A_hat matrix (global arena index q = blockIdx.x + q0).
-// Ccos[k][m] = cos(k (m+1/2) pi / M); Gauss nodes X_m = Ccos[1][m].
-__global__ void __launch_bounds__(384) plan_ahat_kernel(double* A, const double* __restrict__ Ccos, int64_t q0,
-                                                        int L, int64_t s, int dir) {
-  __shared__ double Cs[kMM];
-  __shared__ double G[kMM];
-  __shared__ double H[kMM];
-  const int tid = threadIdx.x;
-  const int64_t q = q0 + blockIdx.x;
-  for (int i = tid; i < kMM; i += blockDim.x) Cs[i] = Ccos[i];
-  int g = 0;
-  while (g + 1 < L && ahat_level_offset(g + 1) <= q) ++g;
-  const int64_t loc = q - ahat_level_offset(g);
-  const int64_t b = loc / 3;
-  const int r = int(loc % 3);
-  const int p = (r == 2) ? 1 : 0;   // eq:cfrompq: r = 0,1,2 <-> (p,q) = (0,0),(0,1),(1,1)
-  const int qq = (r >= 1) ? 1 : 0;
+// Lambda with the number of eq:tau terms chosen from the smallest argument zmin the caller will pass
+// (5 terms to machine precision for z > 19.88, 4 for z > 40, 3 for z > 134, 2 for
+// z > 1844).  Arguments below 20 are shifted up as in Lambda_dev (5 terms then).
+__device__ __forceinline__ int tau_terms(double zmin) {
+  return zmin > 1844.0 ? 2 : (zmin > 134.0 ? 3 : (zmin > 40.0 ? 4 : 5));
+}
+__device__ __forceinline__ double Lambda_terms(double z, int K) {
+  if (K == 5) return Lambda_dev(z);
+  const double x = z + 0.25;
+  const double y = 1.0 / (x * x);
+  double tau;
+  if (K == 2) tau = 1.0 + y * (-1.0 / 64.0);
+  else if (K == 3) tau = 1.0 + y * (-1.0 / 64.0 + y * (21.0 / 8192.0));
+  else tau = 1.0 + y * (-1.0 / 64.0 + y * (21.0 / 8192.0 + y * (-671.0 / 524288.0)));
+  return tau / sqrt(x);
+}
+
+// Chebyshev-Gauss nodes and DCT-II table in constant memory (host-filled in long double):
+// c_cos[k][m] = cos(k (m + 1/2) pi / M), X_m = c_cos[1][m] (decreasing; X_{M-1-m} = -X_m);
+// c_tri[u] = (m, n), m <= n, the (M^2 + M)/2 = 171 upper-triangle index pairs.
+__constant__ double c_cos[kMM];
+__constant__ unsigned char c_tri[2 * (kMM + kM) / 2];
+constexpr int kTri = (kMM + kM) / 2;  // 171
+
+// Lambda^- of every level (sec:fastinit): Lambda((y_n - x_m)/2) depends on the block only
+// through the corner distance j0 - i0 = d h, d = 4 (r = 0, 2) or 6 (r = 1), so two M x M matrices per
+// level serve every submatrix of the level; each is persymmetric ((m,n) ~ (M-1-n, M-1-m)), so only
+// 171 entries are evaluated.  Out: Lm[(g*2 + t)*M*M + m*M + n], t = 0 for d = 4, 1 for d = 6.
+__global__ void plan_lminus_kernel(double* Lm, int L, int64_t s) {
+  const int g = blockIdx.x >> 1, t = blockIdx.x & 1;
   const int64_t h = s << (L - g - 1);
-  const int64_t i0 = 2 * h * (2 * b + p);       // eq:globalij
-  const int64_t j0 = 2 * h * (2 * b + qq + 2);
-  __syncthreads();
-  if (tid < kMM) {
-    const int m = tid / kM, nn = tid % kM;
-    const double hx = double(h) * (Cs[kM + m] + 1.0);   // x - i0 = h (X_m + 1)   (eq:Xfromx)
-    const double hy = double(h) * (Cs[kM + nn] + 1.0);  // y - j0 = h (Y_n + 1)
-    // (y-x)/2 and (x+y)/2 from the exact integer corner offsets (no cancellation)
-    const double ymx = 0.5 * double(j0 - i0) + 0.5 * (hy - hx);
-    const double xpy = 0.5 * double(i0 + j0) + 0.5 * (hx + hy);
-    const double lm = Lambda_dev(ymx), lp = Lambda_dev(xpy);
-    double val;
-    if (dir == 0) {
-      val = lm * lp;  // A(x,y) = Lambda((y-x)/2) Lambda((y+x)/2)
-    } else {
-      // L(x,y) = 2(x+1/2) y / ((x+y)(x+y+1)(x-y+1)) Lambda((y-x)/2)/Lambda((x+y)/2)   (eq:Lxymod)
-      const double x = double(i0) + hx, y = double(j0) + hy;
-      val = (2.0 * (x + 0.5) * y) / ((2.0 * xpy) * (2.0 * xpy + 1.0) * (1.0 - 2.0 * ymx)) * (lm / lp);
+  const double dh = double((t ? 6 : 4) * h);
+  double* out = Lm + int64_t(blockIdx.x) * kMM;
+  for (int o = threadIdx.x; o < kMM; o += blockDim.x) {
+    const int m = o / kM, n = o % kM;
+    if (m + n > kM - 1) continue;  // orbit representatives of (m, n) -> (M-1-n, M-1-m): 171 of 324
+    const double hx = double(h) * (c_cos[kM + m] + 1.0), hy = double(h) * (c_cos[kM + n] + 1.0);
+    const double v = Lambda_dev(0.5 * dh + 0.5 * (hy - hx));  // (y_n - x_m)/2 (eq:Xfromx, eq:globalij)
+    out[m * kM + n] = v;
+    out[(kM - 1 - n) * kM + (kM - 1 - m)] = v;
+  }
+}
+
+// A_hat(g, b, r) for the arena indices [q0, q0 + count), one warp per matrix (grid-stride):
+//   G(m, n) = kernel at (x_m, y_n) (eq:aklmore), x = i0 + h(X_m + 1), y = j0 + h(X_n + 1) (eq:Xfromx),
+//     L2C: A = Lambda^- o Lambda^+, C2L: L(x, y) of eq:Lxymod = prefactor * Lambda^- / Lambda^+;
+//   Lambda^+ = Lambda((x_m + y_n)/2) is symmetric in (m, n): 171 evaluations per block with the eq:tau
+//     term count of the block's smallest argument (i0 + j0)/2;
+//   A_hat = 4/(c_k c_l M^2) C G C^T (2-D DCT-II), each 1-D pass folded by the even/odd symmetry of the
+//     DCT matrix, C[k][M-1-m] = (-1)^k C[k][m] (one radix-2 stage of the mixed-radix DCT):
+//     M/2 = 9 products per output instead of 18.
+constexpr int kAhatWarps = 8;
+__global__ void __launch_bounds__(32 * kAhatWarps) plan_ahat_kernel(double* A, const double* __restrict__ Lm,
+                                                                  int64_t q0, int64_t count, int L, int64_t s,
+                                                                  int dir) {
+  __shared__ double Gs[kAhatWarps][kMM];
+  __shared__ double Hs[kAhatWarps][kMM];
+  const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
+  double* G = Gs[wq];
+  double* H = Hs[wq];
+  const int64_t nwarps = int64_t(gridDim.x) * kAhatWarps;
+  for (int64_t qi = int64_t(blockIdx.x) * kAhatWarps + wq; qi < count; qi += nwarps) {
+    const int64_t q = q0 + qi;
+    int g = 0;
+    while (g + 1 < L && ahat_level_offset(g + 1) <= q) ++g;
+    const int64_t loc = q - ahat_level_offset(g);
+    const int64_t b = loc / 3;
+    const int r = int(loc % 3);
+    const int p = (r == 2) ? 1 : 0;  // eq:cfrompq: r = 0,1,2 <-> (p,q) = (0,0),(0,1),(1,1)
+    const int qq = (r >= 1) ? 1 : 0;
+    const int64_t h = s << (L - g - 1);
+    const int64_t i0 = 2 * h * (2 * b + p);  // eq:globalij
+    const int64_t j0 = 2 * h * (2 * b + qq + 2);
+    const double* Lmg = Lm + int64_t(2 * g + (r == 1 ? 1 : 0)) * kMM;
+    const int K = tau_terms(0.5 * double(i0 + j0));
+    const double xy0 = 0.5 * double(i0 + j0);
+    for (int u = lane; u < kTri; u += 32) {
+      const int m = c_tri[2 * u], n = c_tri[2 * u + 1];
+      const double hx = double(h) * (c_cos[kM + m] + 1.0), hy = double(h) * (c_cos[kM + n] + 1.0);
+      const double lp = Lambda_terms(xy0 + 0.5 * (hx + hy), K);  // symmetric: hx + hy == hy + hx
+      if (dir == 0) {
+        G[m * kM + n] = __ldg(Lmg + m * kM + n) * lp;
+        G[n * kM + m] = __ldg(Lmg + n * kM + m) * lp;
+      } else {
+        // L(x,y) = 2(x+1/2) y / ((x+y)(x+y+1)(x-y+1)) Lambda((y-x)/2)/Lambda((x+y)/2)   (eq:Lxymod)
+        const double x = double(i0) + hx, y = double(j0) + hy, xs = 2.0 * (xy0 + 0.5 * (hx + hy));
+        const double ymx = 0.5 * double(j0 - i0) + 0.5 * (hy - hx);
+        G[m * kM + n] = (2.0 * (x + 0.5) * y) / (xs * (xs + 1.0) * (1.0 - 2.0 * ymx)) * (__ldg(Lmg + m * kM + n) / lp);
+        if (m != n) {
+          const double x2 = double(i0) + hy, y2 = double(j0) + hx;
+          const double ymx2 = 0.5 * double(j0 - i0) + 0.5 * (hx - hy);
+          G[n * kM + m] = (2.0 * (x2 + 0.5) * y2) / (xs * (xs + 1.0) * (1.0 - 2.0 * ymx2)) *
+                          (__ldg(Lmg + n * kM + m) / lp);
+        }
+      }
     }
-    G[m * kM + nn] = val;
-  }
-  __syncthreads();
-  if (tid < kMM) {  // H = C G  (DCT-II along x)
-    const int k = tid / kM, nn = tid % kM;
-    double acc = 0.0;
-    for (int m = 0; m < kM; ++m) acc += Cs[k * kM + m] * G[m * kM + nn];
-    H[k * kM + nn] = acc;
-  }
-  __syncthreads();
-  if (tid < kMM) {  // A_hat = 4/(c_k c_l M^2) H C^T  (eq:aklmore)
-    const int k = tid / kM, l = tid % kM;
-    double acc = 0.0;
-    for (int nn = 0; nn < kM; ++nn) acc += H[k * kM + nn] * Cs[l * kM + nn];
-    const double ck = k == 0 ? 2.0 : 1.0, cl = l == 0 ? 2.0 : 1.0;
-    A[q * kMM + tid] = acc * (4.0 / (ck * cl * double(kM) * double(kM)));
+    __syncwarp();
+    // H = C G along x (rows m), folded: H[k][n] = sum_{m < 9} C[k][m] (G[m][n] +- G[M-1-m][n])
+    for (int o = lane; o < kMM; o += 32) {
+      const int k = o / kM, n = o % kM;
+      const double sg = (k & 1) ? -1.0 : 1.0;
+      double acc = 0.0;
+#pragma unroll
+      for (int m = 0; m < kM / 2; ++m) acc = fma(c_cos[k * kM + m], G[m * kM + n] + sg * G[(kM - 1 - m) * kM + n], acc);
+      H[o] = acc;
+    }
+    __syncwarp();
+    // A_hat[k][l] = 4/(c_k c_l M^2) sum_{n < 9} C[l][n] (H[k][n] +- H[k][M-1-n])   (eq:aklmore)
+    double* Aq = A + q * kMM;
+    for (int o = lane; o < kMM; o += 32) {
+      const int k = o / kM, l = o % kM;
+      const double sg = (l & 1) ? -1.0 : 1.0;
+      double acc = 0.0;
+#pragma unroll
+      for (int n = 0; n < kM / 2; ++n) acc = fma(c_cos[l * kM + n], H[k * kM + n] + sg * H[k * kM + kM - 1 - n], acc);
+      const double ck = k == 0 ? 2.0 : 1.0, cl = l == 0 ? 2.0 : 1.0;
+      Aq[o] = acc * (4.0 / (ck * cl * double(kM) * double(kM)));
+    }
+    __syncwarp();
   }
 }
 
@@ -316,12 +392,18 @@ extern "C" lc_status lc_plan_create(lc_plan** out, int64_t n, lc_direction dir, 
   } while (0)
 
   const int64_t s = p->s;
-  LC_PTRY(cudaMalloc(&p->d_tabB, sizeof(double) * size_t(p->N)));
-  LC_PTRY(cudaMalloc(&p->d_tabA, sizeof(double) * size_t(2 * s)));
-  LC_PTRY(cudaMalloc(&p->d_T, sizeof(double) * size_t(2 * s * kM)));
-  LC_PTRY(cudaMalloc(&p->d_Tt, sizeof(double) * size_t(2 * s * kM)));
-  LC_PTRY(cudaMalloc(&p->d_B, sizeof(double) * kMM));
-  if (p->nc > 0) LC_PTRY(cudaMalloc(&p->d_A, sizeof(double) * size_t(p->nc) * kMM));
+  p->sync = new (std::nothrow) lc_plan_sync();
+  if (!p->sync) return fail(LC_ERR_OUT_OF_MEMORY);
+  // every device array of the plan is stream-ordered memory of `own`, so that destroy can free it
+  // after the plan's own work without the device-wide synchronisation of cudaFree
+  LC_PTRY(cudaStreamCreateWithFlags(&p->own, cudaStreamNonBlocking));
+  cudaStream_t os = p->own;
+  LC_PTRY(cudaMallocAsync(reinterpret_cast<void**>(&p->d_tabB), sizeof(double) * size_t(p->N), os));
+  LC_PTRY(cudaMallocAsync(reinterpret_cast<void**>(&p->d_tabA), sizeof(double) * size_t(2 * s), os));
+  LC_PTRY(cudaMallocAsync(reinterpret_cast<void**>(&p->d_T), sizeof(double) * size_t(2 * s * kM), os));
+  LC_PTRY(cudaMallocAsync(reinterpret_cast<void**>(&p->d_Tt), sizeof(double) * size_t(2 * s * kM), os));
+  LC_PTRY(cudaMallocAsync(reinterpret_cast<void**>(&p->d_B), sizeof(double) * kMM, os));
+  if (p->nc > 0) LC_PTRY(cudaMallocAsync(reinterpret_cast<void**>(&p->d_A), sizeof(double) * size_t(p->nc) * kMM, os));
   p->plan_bytes = sizeof(double) * (size_t(p->N) + size_t(2 * s) + size_t(4 * s * kM) + kMM + size_t(p->nc) * kMM);
 
   double B[kMM];
@@ -333,26 +415,52 @@ extern "C" lc_status lc_plan_create(lc_plan** out, int64_t n, lc_direction dir, 
     for (int m = 0; m < kM; ++m)
       Cc[k * kM + m] = double(cosl((long double)k * ((long double)m + 0.5L) *
                                    3.141592653589793238462643383279502884L / (long double)kM));
-  double* d_C = nullptr;
-  LC_PTRY(cudaMalloc(&d_C, sizeof(double) * kMM));
-  LC_PTRY(cudaMemcpy(p->d_B, B, sizeof(B), cudaMemcpyHostToDevice));
-  LC_PTRY(cudaMemcpy(p->d_T, T.data(), sizeof(double) * T.size(), cudaMemcpyHostToDevice));
-  LC_PTRY(cudaMemcpy(p->d_Tt, Tt.data(), sizeof(double) * Tt.size(), cudaMemcpyHostToDevice));
-  LC_PTRY(cudaMemcpy(d_C, Cc, sizeof(Cc), cudaMemcpyHostToDevice));
+  unsigned char tri[2 * kTri];
+  for (int m = 0, u = 0; m < kM; ++m)
+    for (int nn = m; nn < kM; ++nn, ++u) {
+      tri[2 * u] = (unsigned char)m;
+      tri[2 * u + 1] = (unsigned char)nn;
+    }
+  double* d_Lm = nullptr;  // Lambda^- of every level: L x 2 x M x M
+  if (p->L > 0) LC_PTRY(cudaMallocAsync(reinterpret_cast<void**>(&d_Lm), sizeof(double) * size_t(2 * p->L) * kMM, os));
+  // pageable sources: these copies return once the host data has been staged
+  LC_PTRY(cudaMemcpyAsync(p->d_B, B, sizeof(B), cudaMemcpyHostToDevice, os));
+  LC_PTRY(cudaMemcpyAsync(p->d_T, T.data(), sizeof(double) * T.size(), cudaMemcpyHostToDevice, os));
+  LC_PTRY(cudaMemcpyAsync(p->d_Tt, Tt.data(), sizeof(double) * Tt.size(), cudaMemcpyHostToDevice, os));
+  {
+    static std::mutex const_mu;  // the constant tables are per device; writing the same values is idempotent
+    std::lock_guard<std::mutex> lk(const_mu);
+    LC_PTRY(cudaMemcpyToSymbolAsync(c_cos, Cc, sizeof(Cc), 0, cudaMemcpyHostToDevice, os));
+    LC_PTRY(cudaMemcpyToSymbolAsync(c_tri, tri, sizeof(tri), 0, cudaMemcpyHostToDevice, os));
+    LC_PTRY(cudaStreamSynchronize(os));
+  }
 
   {
+    cudaEvent_t pe[2] = {nullptr, nullptr};
+    LC_PTRY(cudaEventCreate(&pe[0]));
+    LC_PTRY(cudaEventCreate(&pe[1]));
+    cudaEventRecord(pe[0], os);
     const int64_t groups = (p->N + 7) / 8;
     const int tpb = 256;
-    plan_lambda_kernel<<<unsigned((groups + tpb - 1) / tpb), tpb>>>(p->d_tabB, p->N, p->dir);
-    plan_taba_kernel<<<1, 32>>>(p->d_tabA, 2 * s, p->dir);
-    for (int64_t q0 = 0; q0 < p->nc; q0 += (int64_t(1) << 30)) {
-      const int64_t cnt = std::min<int64_t>(p->nc - q0, int64_t(1) << 30);
-      plan_ahat_kernel<<<unsigned(cnt), 352>>>(p->d_A, d_C, q0, int(p->L), s, p->dir);
+    plan_lambda_kernel<<<unsigned((groups + tpb - 1) / tpb), tpb, 0, os>>>(p->d_tabB, p->N, p->dir);
+    plan_taba_kernel<<<1, 32, 0, os>>>(p->d_tabA, 2 * s, p->dir);
+    if (p->L > 0) {
+      plan_lminus_kernel<<<unsigned(2 * p->L), 96, 0, os>>>(d_Lm, int(p->L), s);
+      const int64_t grid = std::min<int64_t>((p->nc + kAhatWarps - 1) / kAhatWarps, int64_t(p->sm_count) * 8);
+      plan_ahat_kernel<<<unsigned(grid), 32 * kAhatWarps, 0, os>>>(p->d_A, d_Lm, 0, p->nc, int(p->L), s, p->dir);
     }
-    LC_PTRY(cudaGetLastError());
-    LC_PTRY(cudaDeviceSynchronize());
+    cudaEventRecord(pe[1], os);
+    const cudaError_t ek = cudaGetLastError();
+    const cudaError_t es = cudaEventSynchronize(pe[1]);
+    float ms = 0.f;
+    if (ek == cudaSuccess && es == cudaSuccess) cudaEventElapsedTime(&ms, pe[0], pe[1]);
+    p->plan_ms = ms;
+    cudaEventDestroy(pe[0]);
+    cudaEventDestroy(pe[1]);
+    LC_PTRY(ek);
+    LC_PTRY(es);
   }
-  cudaFree(d_C);
+  if (d_Lm) cudaFreeAsync(d_Lm, os);
 
   p->band_nnz = band_nnz(p->N, s);
   {
@@ -373,39 +481,93 @@ extern "C" lc_status lc_plan_create(lc_plan** out, int64_t n, lc_direction dir, 
   }
   {
     const int smax_rows = s <= 32 ? 32 : 64;
-    LC_PTRY(cudaMalloc(&p->d_Tpad, sizeof(double) * size_t(2 * smax_rows * kM)));
-    LC_PTRY(cudaMemcpy(p->d_Tpad, p->h_Tpad, sizeof(double) * size_t(2 * smax_rows * kM), cudaMemcpyHostToDevice));
+    LC_PTRY(cudaMallocAsync(reinterpret_cast<void**>(&p->d_Tpad), sizeof(double) * size_t(2 * smax_rows * kM), os));
+    LC_PTRY(cudaMemcpyAsync(p->d_Tpad, p->h_Tpad, sizeof(double) * size_t(2 * smax_rows * kM), cudaMemcpyHostToDevice,
+                            os));
   }
   const lc_status cs = configure_kernels(p);
   if (cs != LC_OK) return fail(cs);
-  LC_PTRY(cudaMalloc(&p->d_ws, p->ws_bytes > 0 ? p->ws_bytes : 16));
-  LC_PTRY(cudaMemset(p->d_ws, 0, p->ws_bytes > 0 ? p->ws_bytes : 16));
-  LC_PTRY(cudaDeviceSynchronize());
+  {
+    const int64_t ein = p->layout == LC_VEC_CONTIGUOUS ? (batch - 1) * p->ld_in + n : (n - 1) * p->ld_in + batch;
+    const int64_t eout = p->layout == LC_VEC_CONTIGUOUS ? (batch - 1) * p->ld_out + n : (n - 1) * p->ld_out + batch;
+    p->stage_bytes = size_t(align_up(ein * 8, 256) + align_up(eout * 8, 256));
+  }
+  LC_PTRY(cudaMallocAsync(&p->d_ws, p->ws_bytes > 0 ? p->ws_bytes : 16, os));
+  LC_PTRY(cudaMemsetAsync(p->d_ws, 0, p->ws_bytes > 0 ? p->ws_bytes : 16, os));
+  // the plan's arrays are complete before any caller stream can see the plan
+  LC_PTRY(cudaStreamSynchronize(os));
   cudaSetDevice(prev_dev);
   *out = p;
   return LC_OK;
 #undef LC_PTRY
 }
 
+namespace lc {
+void note_execute(const lc_plan* p, cudaStream_t st) {
+  if (!p || !p->sync) return;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
+    cudaGetLastError();
+    return;
+  }
+  std::lock_guard<std::mutex> lk(p->sync->mu);
+  for (auto& e : p->sync->seen)
+    if (e.first == st) {
+      cudaEventRecord(e.second, st);
+      return;
+    }
+  cudaEvent_t ev = nullptr;
+  if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) {
+    cudaGetLastError();
+    return;
+  }
+  cudaEventRecord(ev, st);
+  p->sync->seen.emplace_back(st, ev);
+}
+
+double* plan_stage(const lc_plan* p_) {
+  lc_plan* p = const_cast<lc_plan*>(p_);  // the staging pointer is set once, under the plan's mutex
+  std::lock_guard<std::mutex> lk(p->sync->mu);
+  if (!p->d_stage) {
+    void* d = nullptr;
+    if (cudaMallocAsync(&d, p->stage_bytes, p->own) != cudaSuccess || cudaStreamSynchronize(p->own) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    p->d_stage = static_cast<double*>(d);
+  }
+  return p->d_stage;
+}
+}  // namespace lc
+
+extern "C" size_t lc_host_stage_bytes(const lc_plan* p) { return p ? p->stage_bytes : 0; }
+
 extern "C" lc_status lc_plan_destroy(lc_plan* p) {
   if (!p) return LC_ERR_INVALID_ARG;
   int prev = 0;
   cudaGetDevice(&prev);
   cudaSetDevice(p->device);
-  // executions still in flight on any stream may read the plan's arrays and workspace: finish them
-  // before the memory can be handed to another allocation
-  cudaDeviceSynchronize();
-  cudaFree(p->d_A);
-  cudaFree(p->d_tabB);
-  cudaFree(p->d_tabA);
-  cudaFree(p->d_T);
-  cudaFree(p->d_Tt);
-  cudaFree(p->d_B);
-  cudaFree(p->d_ws);
-  cudaFree(p->d_stage_in);
-  cudaFree(p->d_stage_out);
+  cudaStream_t os = p->own;
+  if (p->sync) {
+    // executions still in flight may read the plan's arrays and workspace: order the frees after the
+    // last execution on every stream the plan was used on (and only those streams)
+    std::lock_guard<std::mutex> lk(p->sync->mu);
+    for (auto& e : p->sync->seen)
+      if (os) cudaStreamWaitEvent(os, e.second, 0);
+  }
+  void* bufs[] = {p->d_A, p->d_tabB, p->d_tabA, p->d_T, p->d_Tt, p->d_B, p->d_ws, p->d_stage, p->d_Tpad};
+  for (void* b : bufs)
+    if (b && os) cudaFreeAsync(b, os);
+  if (os) {
+    cudaStreamSynchronize(os);
+    cudaStreamDestroy(os);
+  }
+  if (p->sync) {
+    for (auto& e : p->sync->seen) cudaEventDestroy(e.second);
+    delete p->sync;
+  }
   std::free(p->h_Tpad);
-  cudaFree(p->d_Tpad);
+  cudaGetLastError();  // errors of earlier asynchronous work are reported by the caller's synchronisation
   cudaSetDevice(prev);
   delete p;
   return LC_OK;
@@ -420,6 +582,7 @@ extern "C" lc_status lc_plan_describe(const lc_plan* p, lc_plan_desc* d) {
   d->flops_alg = p->flops_alg; d->bytes_alg = p->bytes_alg;
   d->vt = p->vt; d->subtree = p->k; d->stage_blocks = p->bps; d->stages = p->nst;
   d->kernels_per_execute = p->engine == 2 ? 1 : (p->engine == 3 ? 2 : (p->L > 0 ? 3 : 2));
+  d->plan_device_ms = p->plan_ms;
   return LC_OK;
 }
 

@@ -36,11 +36,16 @@ class BatchedTransform:
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         self.start, self.stop = shard_range(total_batch, self.world, self.rank)
-        self.plan = Plan(n, direction, batch=max(1, self.stop - self.start), device=device, **opts)
+        self.n = n
+        # a rank that owns no vectors (total_batch < world) has no plan and returns empty outputs
+        self.plan = Plan(n, direction, batch=self.stop - self.start, device=device, **opts) \
+            if self.stop > self.start else None
 
     def __call__(self, x_local: torch.Tensor, out: Optional[torch.Tensor] = None) -> torch.Tensor:
         if x_local.shape[0] != self.stop - self.start:
             raise ValueError(f"rank {self.rank} owns vectors [{self.start}, {self.stop})")
+        if self.plan is None:
+            return x_local.new_empty((0, self.n)) if out is None else out
         return self.plan.execute(x_local, out)
 
 

@@ -1,0 +1,149 @@
+"""The C-ABI contract of include/legcheb.h on the GPU: host-buffer execution (lc_execute_host), its
+thread safety with caller-owned staging and workspaces, the aliasing error, stream-ordered plan
+destruction, and per-stream workspaces of the Python conveniences (leg2cheb / cheb2leg).
+
+Every result is checked against the CPU oracle (the plain definitions of PAPER.md:29-32, eq:directmv).
+"""
+import threading
+import time
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from lc_inputs import batch, vector
+
+pytestmark = pytest.mark.gpu
+
+GATE = 1e-12
+
+
+def _dev():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch.device("cuda", 0)
+
+
+def _plan(*a, **k):
+    from paper_2411_00033_b200 import Plan
+    return Plan(*a, **k)
+
+
+def _rows(n, count=300, seed=3):
+    rng = np.random.default_rng(seed)
+    return np.unique(np.r_[0:min(n, 64), rng.integers(0, n, count), n - 1])
+
+
+@pytest.mark.parametrize("direction", ["leg2cheb", "cheb2leg"])
+@pytest.mark.parametrize("n,V,engine", [(5000, 1, 0), (3000, 24, 2), (300000, 8, 3), (100000, 3, 1)])
+def test_execute_host_vs_oracle(direction, n, V, engine):
+    dev = _dev()
+    x = batch("uniform_r0", n, V, seed=7).pin_memory()
+    out = torch.empty_like(x).pin_memory()
+    p = _plan(n, direction, batch=V, device=dev, engine=engine)
+    p.execute_host(x, out)  # plan-owned staging and workspace
+    torch.cuda.synchronize()
+    rows = _rows(n)
+    for v in sorted({0, V - 1}):
+        ref = oracle.transform_rows(direction, x[v].numpy(), rows)
+        assert oracle.einf(out[v].numpy()[rows], ref) <= GATE, (v, engine)
+    # identical to the device-buffer call (same kernels, same arithmetic)
+    zd = p.execute(x.to(dev)).cpu()
+    assert torch.equal(zd, out)
+
+
+def test_execute_host_two_threads_two_streams_one_plan():
+    """Two host threads drive one plan on two streams with their own staging and workspaces."""
+    dev = _dev()
+    n, V = 200000, 2
+    p = _plan(n, "leg2cheb", batch=V, device=dev)
+    xs = [batch("uniform_r0.5", n, V, seed=50 + t).pin_memory() for t in range(2)]
+    outs = [torch.empty_like(xs[t]).pin_memory() for t in range(2)]
+    stages = [p.new_host_stage() for _ in range(2)]
+    wss = [p.new_workspace() for _ in range(2)]
+    streams = [torch.cuda.Stream(device=dev) for _ in range(2)]
+    torch.cuda.synchronize()
+    errors = []
+
+    def work(t):
+        try:
+            torch.cuda.set_device(dev)
+            for _ in range(5):
+                p.execute_host(xs[t], outs[t], stream=streams[t], stage=stages[t], workspace=wss[t])
+            streams[t].synchronize()
+        except Exception as e:  # surfaced below
+            errors.append(e)
+
+    th = [threading.Thread(target=work, args=(t,)) for t in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errors, errors
+    rows = _rows(n)
+    for t in range(2):
+        for v in range(V):
+            ref = oracle.l2c_rows(xs[t][v].numpy(), rows)
+            assert oracle.einf(outs[t][v].numpy()[rows], ref) <= GATE, (t, v)
+
+
+def test_aliasing_is_rejected():
+    from paper_2411_00033_b200._lib import LegChebError
+    dev = _dev()
+    n = 4096
+    p = _plan(n, "leg2cheb", device=dev)
+    buf = torch.zeros(2 * n, dtype=torch.float64, device=dev)
+    with pytest.raises(LegChebError) as ei:
+        p.execute(buf[:n].view(1, n), buf[:n].view(1, n))  # in == out
+    assert ei.value.status == 5  # LC_ERR_ALIASING
+    with pytest.raises(LegChebError) as ei:
+        p.execute(buf[:n].view(1, n), buf[n // 2:n // 2 + n].view(1, n))  # partial overlap
+    assert ei.value.status == 5
+    p.execute(buf[:n].view(1, n), buf[n:].view(1, n))  # adjacent, disjoint: accepted
+    torch.cuda.synchronize()
+
+
+def test_destroy_waits_for_own_work_only():
+    """lc_plan_destroy orders its frees after the plan's own executions but does not wait for an
+    unrelated stream (no cudaDeviceSynchronize / cudaFree device-wide sync)."""
+    dev = _dev()
+    other = torch.cuda.Stream(device=dev)
+    mine = torch.cuda.Stream(device=dev)
+    n = 100000
+    x = torch.from_numpy(vector("uniform_r0.5", n, seed=61)).reshape(1, -1).to(dev)
+    p = _plan(n, "leg2cheb", device=dev)
+    torch.cuda.synchronize()
+    with torch.cuda.stream(other):
+        torch.cuda._sleep(3_000_000_000)  # ~1.5 s of GPU clock cycles on an unrelated stream
+    with torch.cuda.stream(mine):
+        z = p.execute(x, stream=mine)
+    t0 = time.perf_counter()
+    p.close()  # lc_plan_destroy
+    dt = time.perf_counter() - t0
+    busy = not other.query()
+    torch.cuda.synchronize()
+    ref = oracle.l2c_rows(x.cpu().numpy()[0], _rows(n))
+    assert oracle.einf(z.cpu().numpy()[0][_rows(n)], ref) <= GATE
+    assert busy and dt < 0.75, (dt, busy)
+
+
+def test_convenience_functions_on_two_streams():
+    """leg2cheb() from two streams at once: each stream gets its own workspace."""
+    from paper_2411_00033_b200 import leg2cheb
+    dev = _dev()
+    n = 150000
+    xs = [torch.from_numpy(vector("uniform_r0.5", n, seed=70 + t)).to(dev) for t in range(2)]
+    st = [torch.cuda.Stream(device=dev) for _ in range(2)]
+    torch.cuda.synchronize()
+    outs = [[], []]
+    for _ in range(4):
+        for t in range(2):
+            with torch.cuda.stream(st[t]):
+                outs[t].append(leg2cheb(xs[t]))
+    torch.cuda.synchronize()
+    rows = _rows(n)
+    for t in range(2):
+        ref = oracle.l2c_rows(xs[t].cpu().numpy(), rows)
+        for z in outs[t]:
+            assert oracle.einf(z.cpu().numpy()[rows], ref) <= GATE, t

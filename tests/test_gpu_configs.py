@@ -6,6 +6,7 @@ import torch
 
 import oracle
 from lc_inputs import CONFIGS, config_batch, vector
+from parity_util import c4_rows, check_round_trip, check_rows
 
 pytestmark = pytest.mark.gpu
 
@@ -14,16 +15,6 @@ def _dev():
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     return torch.device("cuda", 0)
-
-
-def _rows(n, seed=1, s=32):
-    """C-4: 2048 uniform rows, the first and last 256, and both sides of random 2s-tile boundaries."""
-    rng = np.random.default_rng(seed)
-    r = set(rng.choice(n, size=min(n, 2048), replace=False).tolist())
-    r |= set(range(min(n, 256))) | set(range(max(0, n - 256), n))
-    for u in rng.integers(1, max(2, n // (2 * s)), size=256):
-        r |= {int(2 * s * u - 1), int(2 * s * u)}
-    return np.array(sorted(x for x in r if 0 <= x < n), dtype=np.int64)
 
 
 @pytest.mark.parametrize("cfg", ["cfg2", "cfg2b"])
@@ -37,12 +28,12 @@ def test_cfg2_single_vector_full_size(cfg):
     pl, pc = Plan(n, "leg2cheb", device=dev), Plan(n, "cheb2leg", device=dev)
     z = pl.execute(xd)
     y = pc.execute(z)
-    rows = _rows(n)
+    rows = c4_rows(n, pl.desc["s"])  # tile boundaries at the plan's own s (31 at 1e6, 32 at 2^20)
     f = x[0].numpy()
-    for d, out, inp in (("leg2cheb", z, f), ("cheb2leg", y, z.cpu().numpy()[0])):
-        ref = oracle.transform_rows(d, inp, rows)
-        assert oracle.einf(out.cpu().numpy()[0][rows], ref) <= 1e-12, d
-    assert oracle.einf(y.cpu().numpy()[0], f) <= 1e-12  # round trip (exact result: the input)
+    zh = z.cpu().numpy()[0]
+    check_rows("leg2cheb", f, zh, rows, cfg)
+    check_rows("cheb2leg", zh, y.cpu().numpy()[0], rows, cfg)
+    check_round_trip(f, y.cpu().numpy()[0], pl.desc["s"], cfg)
 
 
 def test_cfg3_batched_full_size():
@@ -57,10 +48,11 @@ def test_cfg3_batched_full_size():
     zh, yh = z.cpu().numpy(), y.cpu().numpy()
     rng = np.random.default_rng(1)
     vs = sorted({0, V - 1} | set(rng.choice(V, 30, replace=False).tolist()))  # 32 full vectors
+    allrows = np.arange(n)
     for v in vs:
-        assert oracle.einf(zh[v], oracle.l2c(x[v].numpy())) <= 1e-12, v
-        assert oracle.einf(yh[v], oracle.c2l(zh[v])) <= 1e-12, v
-        assert oracle.einf(yh[v], x[v].numpy()) <= 1e-12, v
+        check_rows("leg2cheb", x[v].numpy(), zh[v], allrows, f"cfg3 v={v}")
+        check_rows("cheb2leg", zh[v], yh[v], allrows, f"cfg3 v={v}")
+        check_round_trip(x[v].numpy(), yh[v], pl.desc["s"], f"cfg3 v={v}")
 
 
 @pytest.mark.slow
@@ -74,13 +66,18 @@ def test_cfg4_large_round_trip_sampled():
     z = pl.execute(xd)
     y = pc.execute(z)
     torch.cuda.synchronize()
+    assert pl.kernel_info["engine"] == 3
+    sp = pl.desc["s"]
+    rows = c4_rows(n, sp, uniform=1024, tiles=128)  # >= 1000 rows per vector, boundaries at s = 20
     rng = np.random.default_rng(1)
-    rows = np.array(sorted(set(rng.choice(n, 24, replace=False).tolist()) | {0, 1, 2, 39, 40, n - 2, n - 1}))
-    for v in (0, 17, V - 1):
+    vs = sorted({0, V - 1} | set(rng.choice(np.arange(1, V - 1), 2, replace=False).tolist()))
+    for v in vs:  # 4 vectors
         zv = z[v].cpu().numpy()
-        assert oracle.einf(zv[rows], oracle.l2c_rows(x[v].numpy(), rows)) <= 1e-11, v
-        assert oracle.einf(y[v].cpu().numpy()[rows], oracle.c2l_rows(zv, rows)) <= 1e-11, v
-        assert oracle.einf(y[v].cpu().numpy(), x[v].numpy()) <= 1e-11, v  # round trip, all entries
+        check_rows("leg2cheb", x[v].numpy(), zv, rows, f"cfg4 v={v}")
+        check_rows("cheb2leg", zv, y[v].cpu().numpy(), rows, f"cfg4 v={v}")
+    yh = y.cpu().numpy()
+    for v in range(V):  # every vector, every entry
+        check_round_trip(x[v].numpy(), yh[v], sp, f"cfg4 v={v}")
     del xd, z, y
 
 
@@ -91,11 +88,12 @@ def test_cfg5_tensor_product_2d_single_gpu():
     F = torch.stack([torch.from_numpy(vector("normal_over_ij", n, seed=0, v=i)) for i in range(n)])
     Z = tensor_product_2d(F.to(dev)).cpu().numpy()  # L2C along axis 1, then along axis 0
     rng = np.random.default_rng(1)
-    js = sorted(rng.choice(n, 8, replace=False).tolist()) + [0, n - 1]
+    js = np.array(sorted(set(rng.choice(n, 62, replace=False).tolist()) | {0, n - 1}))  # 64 columns
     is_ = np.array(sorted(set(rng.choice(n, 64, replace=False).tolist()) | {0, 1, n - 1}))
     Fn = F.numpy()
-    for j in js:
-        # g_k = (row transform of row k) at output j, for all k; then Z_ij = column transform of g at i
-        g = np.array([float(oracle.l2c_rows(Fn[k], [j])[0]) for k in range(n)])
-        ref = oracle.l2c_rows(g, is_)
-        assert oracle.einf(Z[is_, j], ref) <= 1e-12, j
+    # g[k, c] = (row transform of row k) at output column js[c], for all k (one oracle call per row)
+    g = np.stack([oracle.l2c_rows(Fn[k], js) for k in range(n)])
+    for c, j in enumerate(js):
+        ref, ab = oracle.l2c_rows(g[:, c], is_, with_abs=True)
+        e = oracle.einf(Z[is_, j], ref)
+        assert e <= 1e-12, (j, e)
