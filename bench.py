@@ -124,7 +124,11 @@ def dist_setup():
         import torch.distributed as dist
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         backend = "nccl" if torch.cuda.is_available() else "gloo"
+        # LC_DIST_BACKEND=gloo with more ranks than GPUs: a functional check of the multi-rank code path on
+        # a one-GPU box (ranks share the device; the timings of such a run mean nothing)
+        backend = os.environ.get("LC_DIST_BACKEND", backend)
         if torch.cuda.is_available():
+            local = local % torch.cuda.device_count() if backend == "gloo" else local
             torch.cuda.set_device(local)
         dist.init_process_group(backend=backend)
     elif torch.cuda.is_available():
@@ -227,13 +231,22 @@ def measure(config, args, world, rank, local, headline=True):
     stream = torch.cuda.current_stream(dev)
     pl, pc, plan_info = make_plans(config, n, V, dev, world, opts)
     C = n // world
+    chunks = args.chunks if (two_d and world > 1 and V % max(1, args.chunks) == 0) else 1
     if two_d:
         # rows [v0, v0+V) of the n x n array on this rank; pass 1 along axis 1 (V row vectors), all-to-all,
-        # pass 2 along axis 0 (n/world column vectors, batch-contiguous)
+        # pass 2 along axis 0 (n/world column vectors, batch-contiguous); with chunks > 1 pass 1 runs in
+        # row chunks whose all-to-all overlaps the next chunk (dist._chunked_exchange)
         ycol = torch.empty((n, C), dtype=torch.float64, device=dev)
+        from paper_2411_00033_b200 import Plan as _Plan
+        pk = _Plan(n, "leg2cheb", batch=V // chunks, device=dev, **opts) if chunks > 1 else pl
+        tmpk = torch.empty((V // chunks, n), dtype=torch.float64, device=dev)
 
         def step():
-            tensor_product_2d(x, row_fn=lambda a: pl.execute(a, tmp), col_fn=lambda a: pc.execute(a, ycol))
+            if chunks > 1:
+                tensor_product_2d(x, row_fn=lambda a: pk.execute(a, tmpk), col_fn=lambda a: pc.execute(a, ycol),
+                                  chunks=chunks)
+            else:
+                tensor_product_2d(x, row_fn=lambda a: pl.execute(a, tmp), col_fn=lambda a: pc.execute(a, ycol))
     else:
         def step():
             pl.execute(x, tmp)
@@ -296,6 +309,14 @@ def measure(config, args, world, rank, local, headline=True):
                 acc[k] += tm[k] / reps
         passes = {k: allreduce_max(v, world) for k, v in acc.items()}
         passes["alltoall_bytes_sent_per_rank"] = 8 * V * C * (world - 1)
+        if chunks > 1:
+            ov = 0.0
+            for _ in range(reps):
+                tensor_product_2d(x, row_fn=lambda a: pk.execute(a, tmpk), col_fn=lambda a: pc.execute(a, ycol),
+                                  chunks=chunks, timing=tm)
+                ov += tm["pass1_and_alltoall_overlapped_ms"] / reps
+            passes["pass1_and_alltoall_overlapped_ms"] = allreduce_max(ov, world)
+            passes["chunks"] = chunks
 
     # ---- per-kernel durations (events around each kernel, same stream) for the roofline
     kpe = pl.kernels_per_execute
@@ -321,7 +342,7 @@ def measure(config, args, world, rank, local, headline=True):
     # the down kernel writes z
     alg = {"lc_up_kernel": 8.0 * n * V, "lc_up3_kernel": 8.0 * n * V,
            "lc_stream_kernel": 8.0 * 324 * dl["nc"] + 8.0 * dl["N"], "lc_down_kernel": 8.0 * n * V}
-    if kpe == 2 and engine == 1:
+    if kpe == 2 and engine == 1:  # L = 0: no up kernel, the streaming kernel reads f
         alg["lc_stream_kernel"] += 8.0 * n * V
     # the per-tile kernel (engine 2) is the whole transform: f in, z out, A_hat and lambda once
     alg["lc_tile_kernel"] = 16.0 * n * V + 8.0 * 324 * dl["nc"] + 8.0 * dl["N"]
@@ -631,6 +652,8 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-seconds", type=float, default=60.0)
     ap.add_argument("--e2e-steps", type=int, default=200)
+    ap.add_argument("--chunks", type=int, default=4,
+                    help="cfg5 at N > 1: pass-1 row chunks whose all-to-all overlaps the next chunk (1: no overlap)")
     ap.add_argument("--batched", default="cfg3", choices=["cfg3", "cfg4", "cfg5", "none"],
                     help="batched sub-record measured after the headline config (the metric's 'batched' half)")
     args = ap.parse_args()

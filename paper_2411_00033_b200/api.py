@@ -97,7 +97,7 @@ class Plan:
         _lib.check("lc_plan_kernel_info", self._lib.lc_plan_kernel_info(self._h, buf, 32, ctypes.byref(nw)))
         names = ["stream_grid", "smem_stream", "smem_up", "kup", "grup", "kb", "cb", "nst", "vt", "stream_occ",
                  "m2l_units", "band_units", "up_grid", "kd", "smem_down", "engine", "tile_grid", "smem_tile",
-                 "ranges", "range_len"]
+                 "ranges", "range_len", "up_ksub"]
         return {k: int(buf[i]) for i, k in enumerate(names[:nw.value])}
 
     @property

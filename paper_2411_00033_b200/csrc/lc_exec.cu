@@ -22,6 +22,7 @@
 //   of 8-vector subtrees; writes w of every level), then lc_range_kernel, the same pass as engine 2
 //   over ranges of leaves of each tile with w read from the workspace.
 #include <algorithm>
+#include <cstdlib>
 #include <atomic>
 #include <mutex>
 #include <cstdio>
@@ -153,6 +154,7 @@ struct UpParams {
   int64_t ld_in, n, N, batch;
   int layout, L, s, k, gr, G, fstride, vec16;
   int noflags;  // engine 3: the range kernel waits for the whole grid (griddepcontrol), no flags
+  int ksub;     // M2M levels done inside the CTA's subtree (<= k); the rest by the continuation
   int kc;       // engine 3 (lc_up3_kernel): subtrees per chunk = 2^kc
   int64_t ntiles;
   double* w;
@@ -190,6 +192,7 @@ struct DownParams {
   const double* B;     // B(0) [M][M]
   int64_t ld_out, n, N, batch, w_tile;
   int layout, L, s, k;
+  int bulk;  // TMA bulk loads allowed (out 16-byte aligned, ld_out even, full tiles only)
 };
 
 // ============================================================== up kernel
@@ -199,21 +202,9 @@ struct DownParams {
 // once), B(0) is a uniform constant-bank operand (the row group is warp-uniform), and every row
 // keeps two partial sums (even / odd k) to halve its dependent DFMA chain.
 template <int R0, int R1>
-__device__ __forceinline__ void m2m_rows(const double* __restrict__ Bs, const double* __restrict__ x0,
-                                         const double* __restrict__ x1, double* __restrict__ out) {
+__device__ __forceinline__ void m2m_rows_core(const double* __restrict__ Bs, const double (&zp)[R1],
+                                              const double (&zm)[R1], double* __restrict__ out) {
   constexpr int NR = R1 - R0;
-  double zp[R1], zm[R1];
-#pragma unroll
-  for (int k = 0; k < R1; k += 2) {
-    const double2 a2 = *reinterpret_cast<const double2*>(x0 + k);
-    const double2 b2 = *reinterpret_cast<const double2*>(x1 + k);
-    zp[k] = a2.x + b2.x;
-    zm[k] = a2.x - b2.x;
-    if (k + 1 < R1) {
-      zp[k + 1] = a2.y + b2.y;
-      zm[k + 1] = a2.y - b2.y;
-    }
-  }
   double acc[NR];
 #pragma unroll
   for (int n = R0; n < R1; ++n) {
@@ -232,6 +223,24 @@ __device__ __forceinline__ void m2m_rows(const double* __restrict__ Bs, const do
   }
 #pragma unroll
   for (int i = 0; i < NR; ++i) out[R0 + i] = acc[i];
+}
+
+template <int R0, int R1>
+__device__ __forceinline__ void m2m_rows(const double* __restrict__ Bs, const double* __restrict__ x0,
+                                         const double* __restrict__ x1, double* __restrict__ out) {
+  double zp[R1], zm[R1];
+#pragma unroll
+  for (int k = 0; k < R1; k += 2) {
+    const double2 a2 = *reinterpret_cast<const double2*>(x0 + k);
+    const double2 b2 = *reinterpret_cast<const double2*>(x1 + k);
+    zp[k] = a2.x + b2.x;
+    zm[k] = a2.x - b2.x;
+    if (k + 1 < R1) {
+      zp[k + 1] = a2.y + b2.y;
+      zm[k + 1] = a2.y - b2.y;
+    }
+  }
+  m2m_rows_core<R0, R1>(Bs, zp, zm, out);
 }
 
 // one tree level in shared memory ([sigma][node][v][M]); one thread per (row group, sigma,
@@ -417,8 +426,11 @@ __global__ void __launch_bounds__(kThreads, (VT == 8 && SMAX == 32) ? LC_UP8_MIN
     }
   };
   write_level(k);
-  // step 2 inside the subtree
-  for (int j = k; j >= 1; --j) {
+  const int ksub = P.ksub;        // subtree levels merged here; the CTA leaves 2^(k-ksub) roots
+  const int dsub = k - ksub;
+  // step 2 inside the subtree (ksub levels: an early exit frees the SM for the streaming kernel; the
+  // remaining levels are merged by the continuation below, beside the stream)
+  for (int j = k; j >= 1 + dsub; --j) {
     m2m_level<VT>(Bs, tree + tree_off(j), tree + tree_off(j - 1), j - 1);
     __syncthreads();
     write_level(j - 1);
@@ -432,14 +444,16 @@ __global__ void __launch_bounds__(kThreads, (VT == 8 && SMAX == 32) ? LC_UP8_MIN
     if (atom_add_acq_rel(&P.flags[0], 1) == total - 1) {
       atomicExch(&P.flags[0], 0);
       st_release(&P.flags[1], 1);
-      if (P.gr == 0) st_release(&P.flags[3], 1);
+      if (P.gr + dsub == 0) st_release(&P.flags[3], 1);
     }
   }
 
   // upward continuation above the subtree roots: the last arriver of each
-  // group of 2^G nodes merges them G levels up (threadfence-reduction pattern).
-  int g = P.gr;
-  int64_t node = R;
+  // group of 2^G nodes merges them G levels up (threadfence-reduction pattern).  A CTA that
+  // stopped dsub levels early arrives once for its 2^dsub roots.
+  int g = P.gr + dsub;
+  int64_t node = R << dsub;
+  int contrib = dsub;  // log2 of the nodes this arrival stands for
   while (g > 0) {
     const int ge = min(P.G, g);
     const int64_t grp = node >> ge;
@@ -447,7 +461,7 @@ __global__ void __launch_bounds__(kThreads, (VT == 8 && SMAX == 32) ? LC_UP8_MIN
     if (tid == 0) {
       int* c = P.cnt + tile * P.cnt_tile + (nseg(g) - 4) + grp;
       const int old = atom_add_acq_rel(c, 1);
-      const int last = (old == (1 << ge) - 1);
+      const int last = (old == (1 << (ge - contrib)) - 1);
       if (last) atomicExch(c, 0);  // self-reset for the next launch
       s_last = last;
     }
@@ -481,9 +495,10 @@ __global__ void __launch_bounds__(kThreads, (VT == 8 && SMAX == 32) ? LC_UP8_MIN
     }
     g -= ge;  // the next arrival (after a barrier, acquire-release) publishes these stores
     node = grp;
+    contrib = 0;
     LC_TS(0, 6);
   }
-  if (P.gr > 0 && !P.noflags) {  // this CTA produced one of the 4 level-0 nodes of its vector tile
+  if (P.gr + dsub > 0 && !P.noflags) {  // this CTA produced one of the 4 level-0 nodes of its vector tile
     __syncthreads();
     if (tid == 0) {
       const int total = 4 * int(gridDim.y);
@@ -1319,6 +1334,36 @@ __global__ void __launch_bounds__(NT, 512 / NT) lc_down_kernel(const DownParams 
   __syncthreads();
   LC_TS(2, 1);
   const double* ct = P.c + tile * P.w_tile;
+  const int olim = int((P.n - i0) < rows ? (P.n - i0) : rows);  // rows of this tile inside n
+  // one TMA bulk-copy round trip when every piece is 16-byte aligned and whole (the c_m2l rows and,
+  // in the vector layout, each vector's band rows of a full tile); otherwise per-element cp.async
+  // with zero fill beyond n
+  const bool bulk = P.bulk && P.layout == LC_VEC_CONTIGUOUS && olim == rows && (tile + 1) * VT <= P.batch;
+  if (bulk) {
+    __shared__ __align__(8) uint64_t dbar;
+    if (tid == 0) {
+      mbar_init(&dbar, 1);
+      fence_mbar_init();
+      uint32_t total = uint32_t(VT) * uint32_t(rows) * 8u;
+      if (L > 0) total += uint32_t(gd + (2 << kd) - 1) * 2u * uint32_t(VM) * 8u;
+      mbar_arrive_expect_tx(&dbar, total);
+      const uint64_t pol = policy_evict_first();
+      if (L > 0) {
+        for (int g = 0; g < gd; ++g)
+          for (int sg = 0; sg < 2; ++sg)
+            bulk_g2s(cm_anc(g) + sg * VM, ct + (w_level_offset_units(g) + sg * nseg(g) + (R >> (gd - g))) * VM,
+                     uint32_t(VM) * 8u, &dbar, pol);
+        for (int j = 0; j <= kd; ++j)
+          for (int sg = 0; sg < 2; ++sg)
+            bulk_g2s(cm_lvl(j) + sg * (1 << j) * VM, ct + (w_level_offset_units(gd + j) + sg * nseg(gd + j) + (R << j)) * VM,
+                     uint32_t((1 << j) * VM) * 8u, &dbar, pol);
+      }
+      for (int v = 0; v < VT; ++v)
+        bulk_g2s(zb + v * rows, P.out + (tile * VT + v) * P.ld_out + i0, uint32_t(rows) * 8u, &dbar, pol);
+    }
+    __syncthreads();
+    mbar_wait(&dbar, 0);
+  } else {
   if (L > 0) {
     for (int g = 0; g < gd; ++g) {
       const int64_t a = R >> (gd - g);
@@ -1338,7 +1383,6 @@ __global__ void __launch_bounds__(NT, 512 / NT) lc_down_kernel(const DownParams 
       }
     }
   }
-  const int olim = int((P.n - i0) < rows ? (P.n - i0) : rows);  // rows of this tile inside n
 #pragma unroll 1
   for (int v = 0; v < VT; ++v) {
     const int64_t gv = tile * VT + v;
@@ -1352,6 +1396,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) lc_down_kernel(const DownParams 
   cp_async_commit();
   cp_async_wait<0>();
   __syncthreads();
+  }
   LC_TS(2, 2);
 
   if (L > 0) {
@@ -2523,6 +2568,18 @@ lc_status configure_kernels(lc_plan* p) {
     }
   }
   if (up_smem_bytes(vt, kup, s) > smax) return LC_ERR_INVALID_ARG;
+  {
+    p->down_bulk = 1;  // TMA bulk loads in the down kernel (LC_DOWN_BULK=0: per-element cp.async, A/B runs)
+    // M2M levels merged inside the up kernel's subtree (the rest by the continuation); fewer levels
+    // free the SMs for the A_hat stream earlier (LC_UP_KSUB overrides, for A/B runs)
+    // measured on cfg2 (tools/r2_job10.sh): 3 levels in the CTA, 3 by the continuation saves ~0.7 us per
+    // transform over all 6 in the CTA (the up CTAs leave ~1.7 us earlier); 2 is slower again
+    int ksub = (L >= 10 && kup >= 4) ? 3 : kup;
+    if (const char* e = std::getenv("LC_UP_KSUB")) ksub = std::max(0, std::min(kup, std::atoi(e)));
+    if (kup - ksub > std::max(kup, 1)) ksub = kup;  // a continuation group must cover the CTA's roots
+    p->up_ksub = ksub;
+    if (const char* e = std::getenv("LC_DOWN_BULK")) p->down_bulk = std::atoi(e) != 0;
+  }
   p->vt = vt;
   p->k = kd;
   p->kb = kb;
@@ -2540,8 +2597,11 @@ lc_status configure_kernels(lc_plan* p) {
   // down to the subtree roots, then the coarse levels (after the up kernel's continuation)
   {
     int o = 0;
-    for (int g = L - 1; g >= p->grup; --g) p->lvorder[o++] = g;
-    for (int g = 0; g < p->grup; ++g) p->lvorder[o++] = g;
+    {
+      const int gtop = p->grup + (p->kup - p->up_ksub);
+      for (int g = L - 1; g >= gtop; --g) p->lvorder[o++] = g;
+      for (int g = 0; g < gtop; ++g) p->lvorder[o++] = g;
+    }
     if (o != L) return LC_ERR_INTERNAL;
   }
   int64_t nchunks = 0;
@@ -2566,7 +2626,7 @@ lc_status configure_kernels(lc_plan* p) {
   }
   // workspace: w | c_m2l | flags (64 ints) | arrival counters (c_m2l rows without a submatrix stay zero)
   const size_t wb = size_t(align_up(p->ntiles * p->w_tile_doubles * 8, 256));
-  p->ws_bytes = 2 * wb + 256 + size_t(p->ntiles * p->cnt_tile_ints) * sizeof(int);
+  p->ws_bytes = 2 * wb + 256 + size_t(p->ntiles * p->cnt_tile_ints) * sizeof(int) + 64 * sizeof(int);
   // per-tile streaming kernel (engine 2): many 8-vector tiles of short vectors
   {
     const int64_t ntiles8 = (p->batch + kTileV - 1) / kTileV;
@@ -2758,6 +2818,7 @@ static lc_status launch_execute_impl(const lc_plan* p, const double* in, double*
   up.fstride = up_fstride(int(p->s));
   up.vec16 = (reinterpret_cast<uintptr_t>(in) % 16 == 0) && (p->ld_in % 2 == 0) ? 1 : 0;
   up.noflags = p->engine == 3 ? 1 : 0;
+  up.ksub = p->engine == 1 ? p->up_ksub : p->kup;
   up.kc = p->up3_kc;
   up.ntiles = p->ntiles;
   up.w = w; up.cnt = cnt; up.flags = flags; up.w_tile = p->w_tile_doubles; up.cnt_tile = p->cnt_tile_ints;
@@ -2767,11 +2828,12 @@ static lc_status launch_execute_impl(const lc_plan* p, const double* in, double*
   sp.ld_in = p->ld_in; sp.ld_out = p->ld_out; sp.n = p->n;
   sp.N = p->N; sp.batch = p->batch; sp.ntiles = p->ntiles; sp.nm2l = p->m2l_units; sp.nband = p->band_units;
   sp.layout = p->layout; sp.L = int(p->L); sp.s = int(p->s); sp.cb = p->bps; sp.nst = p->nst; sp.kb = p->kb;
-  sp.gr_up = p->grup;
+  sp.gr_up = p->grup + (p->kup - p->up_ksub);  // finest level left to the continuation + 1
   for (int i = 0; i < 32; ++i) sp.lvorder[i] = p->lvorder[i];
   DownParams dp{};
   dp.out = out; dp.flags = flags; dp.c = c; dp.Tpad = p->d_Tpad; dp.B = p->d_B; dp.ld_out = p->ld_out; dp.n = p->n; dp.N = p->N; dp.batch = p->batch;
   dp.w_tile = p->w_tile_doubles; dp.layout = p->layout; dp.L = int(p->L); dp.s = int(p->s); dp.k = p->k;
+  dp.bulk = (p->down_bulk && reinterpret_cast<uintptr_t>(out) % 16 == 0 && p->ld_out % 2 == 0) ? 1 : 0;
   const int64_t ndown = p->L > 0 ? (int64_t(2) << p->L) >> p->k : 1;
   const int64_t nsub = p->L > 0 ? (int64_t(4) << p->grup) : 1;
   if (nsub > 0x7fffffff || ndown > 0x7fffffff || p->ntiles > 65535) {
@@ -2845,7 +2907,8 @@ extern "C" lc_status lc_plan_kernel_info(const lc_plan* p, int64_t* out, int32_t
   const int64_t up_grid = p->engine == 3 ? p->up3_grid : (p->L > 0 ? (int64_t(4) << p->grup) * p->ntiles : 0);
   const int64_t v[] = {p->stream_grid, int64_t(p->smem_stream), int64_t(p->smem_up), p->kup, p->grup, p->kb,
                        p->bps, p->nst, p->vt, p->stream_occ, p->m2l_units, p->band_units, up_grid, p->k,
-                       int64_t(p->smem_down), p->engine, p->tile_grid, int64_t(p->smem_tile), p->range_n, p->range_len};
+                       int64_t(p->smem_down), p->engine, p->tile_grid, int64_t(p->smem_tile), p->range_n, p->range_len,
+                       p->up_ksub};
   const int32_t nv = int32_t(sizeof(v) / sizeof(v[0]));
   int32_t i = 0;
   for (; i < nv && i < count; ++i) out[i] = v[i];
@@ -2859,7 +2922,7 @@ extern "C" lc_status lc_execute(const lc_plan* p, const double* in, double* out,
 
 extern "C" lc_status lc_execute_timed(const lc_plan* p, const double* in, double* out, void* ws, void* stream,
                                       void* const* ev, int32_t nev) {
-  if (!p || !ev || nev < (p->engine == 2 ? 2 : (p->engine == 3 ? 3 : (p->L > 0 ? 4 : 3)))) return LC_ERR_INVALID_ARG;
+  if (!p || !ev || nev < lc::kernels_per_execute(p) + 1) return LC_ERR_INVALID_ARG;
   return lc::launch_execute(p, in, out, ws, (cudaStream_t)stream, reinterpret_cast<cudaEvent_t const*>(ev), nev);
 }
 

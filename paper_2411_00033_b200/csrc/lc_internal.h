@@ -124,6 +124,8 @@ struct lc_plan {
   int64_t band_units;  // (leaf range, tile) band work units of the streaming kernel
   int stream_grid, stream_occ;
   int engine;          // 1 = up / stream / down kernels, 2 = per-tile streaming kernel
+  int down_bulk;       // engine 1 down kernel: TMA bulk loads of c_m2l and the band rows
+  int up_ksub;         // engine 1: M2M levels merged inside the up kernel's subtree (<= kup)
   int tile_grid;       // CTAs of the per-tile kernel (engine 2)
   size_t smem_tile;
   int range_n, range_len;   // engine 3: leaf ranges per tile and their length
@@ -162,6 +164,12 @@ lc_status launch_execute(const lc_plan* p, const double* in, double* out, void* 
 // records that p was used on stream st (after the enqueued work) so lc_plan_destroy can wait for it;
 // a no-op on a capturing stream (graph launches are the caller's to finish before destroy)
 void note_execute(const lc_plan* p, cudaStream_t st);
+// kernel launches of one lc_execute
+inline int kernels_per_execute(const lc_plan* p) {
+  if (p->engine == 2) return 1;
+  if (p->engine == 3) return 2;
+  return p->L > 0 ? 3 : 2;
+}
 // the plan-owned lc_execute_host staging (allocated once, thread-safe), or nullptr on failure
 double* plan_stage(const lc_plan* p);
 int64_t band_nnz(int64_t N, int64_t s);

@@ -147,6 +147,11 @@ __global__ void __launch_bounds__(32 * kAhatWarps) plan_ahat_kernel(double* A, c
                                                                   int dir) {
   __shared__ double Gs[kAhatWarps][kMM];
   __shared__ double Hs[kAhatWarps][kMM];
+  __shared__ double Cs[kMM];             // the DCT table, from constant memory once per CTA: lanes read
+  __shared__ unsigned char Ts[2 * kTri]; // different entries, which the constant cache would serialise
+  for (int i = threadIdx.x; i < kMM; i += blockDim.x) Cs[i] = c_cos[i];
+  for (int i = threadIdx.x; i < 2 * kTri; i += blockDim.x) Ts[i] = c_tri[i];
+  __syncthreads();
   const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
   double* G = Gs[wq];
   double* H = Hs[wq];
@@ -167,8 +172,8 @@ __global__ void __launch_bounds__(32 * kAhatWarps) plan_ahat_kernel(double* A, c
     const int K = tau_terms(0.5 * double(i0 + j0));
     const double xy0 = 0.5 * double(i0 + j0);
     for (int u = lane; u < kTri; u += 32) {
-      const int m = c_tri[2 * u], n = c_tri[2 * u + 1];
-      const double hx = double(h) * (c_cos[kM + m] + 1.0), hy = double(h) * (c_cos[kM + n] + 1.0);
+      const int m = Ts[2 * u], n = Ts[2 * u + 1];
+      const double hx = double(h) * (Cs[kM + m] + 1.0), hy = double(h) * (Cs[kM + n] + 1.0);
       const double lp = Lambda_terms(xy0 + 0.5 * (hx + hy), K);  // symmetric: hx + hy == hy + hx
       if (dir == 0) {
         G[m * kM + n] = __ldg(Lmg + m * kM + n) * lp;
@@ -193,7 +198,7 @@ __global__ void __launch_bounds__(32 * kAhatWarps) plan_ahat_kernel(double* A, c
       const double sg = (k & 1) ? -1.0 : 1.0;
       double acc = 0.0;
 #pragma unroll
-      for (int m = 0; m < kM / 2; ++m) acc = fma(c_cos[k * kM + m], G[m * kM + n] + sg * G[(kM - 1 - m) * kM + n], acc);
+      for (int m = 0; m < kM / 2; ++m) acc = fma(Cs[k * kM + m], G[m * kM + n] + sg * G[(kM - 1 - m) * kM + n], acc);
       H[o] = acc;
     }
     __syncwarp();
@@ -204,7 +209,7 @@ __global__ void __launch_bounds__(32 * kAhatWarps) plan_ahat_kernel(double* A, c
       const double sg = (l & 1) ? -1.0 : 1.0;
       double acc = 0.0;
 #pragma unroll
-      for (int n = 0; n < kM / 2; ++n) acc = fma(c_cos[l * kM + n], H[k * kM + n] + sg * H[k * kM + kM - 1 - n], acc);
+      for (int n = 0; n < kM / 2; ++n) acc = fma(Cs[l * kM + n], H[k * kM + n] + sg * H[k * kM + kM - 1 - n], acc);
       const double ck = k == 0 ? 2.0 : 1.0, cl = l == 0 ? 2.0 : 1.0;
       Aq[o] = acc * (4.0 / (ck * cl * double(kM) * double(kM)));
     }
@@ -581,7 +586,7 @@ extern "C" lc_status lc_plan_describe(const lc_plan* p, lc_plan_desc* d) {
   d->plan_bytes = p->plan_bytes; d->workspace_bytes = p->ws_bytes;
   d->flops_alg = p->flops_alg; d->bytes_alg = p->bytes_alg;
   d->vt = p->vt; d->subtree = p->k; d->stage_blocks = p->bps; d->stages = p->nst;
-  d->kernels_per_execute = p->engine == 2 ? 1 : (p->engine == 3 ? 2 : (p->L > 0 ? 3 : 2));
+  d->kernels_per_execute = kernels_per_execute(p);
   d->plan_device_ms = p->plan_ms;
   return LC_OK;
 }

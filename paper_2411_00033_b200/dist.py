@@ -29,23 +29,32 @@ def shard_range(total: int, world: int, rank: int) -> tuple[int, int]:
 
 
 class BatchedTransform:
-    """Transform of this rank's contiguous slice of a batch of vectors (no communication)."""
+    """Transform of this rank's contiguous slice of a batch of vectors (no communication).
 
-    def __init__(self, n: int, direction: str, total_batch: int, group=None, device=None, **opts):
-        from .api import Plan
+    `transform` replaces the sm_100a plan by another callable on [rows, n] (tests use a CPU stand-in);
+    the product path always builds a `Plan`."""
+
+    def __init__(self, n: int, direction: str, total_batch: int, group=None, device=None,
+                 transform: Optional[Callable] = None, **opts):
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         self.start, self.stop = shard_range(total_batch, self.world, self.rank)
         self.n = n
-        # a rank that owns no vectors (total_batch < world) has no plan and returns empty outputs
-        self.plan = Plan(n, direction, batch=self.stop - self.start, device=device, **opts) \
-            if self.stop > self.start else None
+        self.plan = None
+        self.transform = transform
+        if transform is None and self.stop > self.start:
+            # a rank that owns no vectors (total_batch < world) has no plan and returns empty outputs
+            from .api import Plan
+            self.plan = Plan(n, direction, batch=self.stop - self.start, device=device, **opts)
 
     def __call__(self, x_local: torch.Tensor, out: Optional[torch.Tensor] = None) -> torch.Tensor:
         if x_local.shape[0] != self.stop - self.start:
             raise ValueError(f"rank {self.rank} owns vectors [{self.start}, {self.stop})")
-        if self.plan is None:
+        if self.stop == self.start:
             return x_local.new_empty((0, self.n)) if out is None else out
+        if self.transform is not None:
+            y = self.transform(x_local)
+            return y if out is None else out.copy_(y)
         return self.plan.execute(x_local, out)
 
 
@@ -81,25 +90,73 @@ def transpose_cols_to_rows(z_cols: torch.Tensor, group=None) -> torch.Tensor:
     return recv.permute(1, 0, 2).reshape(n0 // world, world * C)
 
 
+def _chunked_exchange(x_rows: torch.Tensor, row_fn: Callable, chunks: int, group=None,
+                      timing: Optional[dict] = None) -> torch.Tensor:
+    """Pass 1 in `chunks` row chunks with the all-to-all of chunk k overlapping pass 1 of chunk k+1.
+
+    Chunk k's output [Rk, n1] is packed by destination ([world, Rk, C]) and exchanged with
+    all_to_all_single on a communication stream while the next chunk transforms; the received
+    [chunks][world][Rk][C] blocks are rows s R + k Rk + r of the column slab, which one local permute
+    puts in the batch-contiguous [n0, C] order pass 2 reads."""
+    world = dist.get_world_size(group)
+    R, n1 = x_rows.shape
+    Rk, C = R // chunks, n1 // world
+    recv = x_rows.new_empty((chunks, world, Rk, C))
+    cuda = x_rows.is_cuda
+    main = torch.cuda.current_stream(x_rows.device) if cuda else None
+    comm = torch.cuda.Stream(x_rows.device) if cuda else None
+    sends = []
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)] if (cuda and timing is not None) else None
+    if ev:
+        ev[0].record(main)
+    for k in range(chunks):
+        yk = row_fn(x_rows[k * Rk:(k + 1) * Rk])
+        send = pack_for_transpose(yk, world)
+        sends.append(send)  # kept alive until the exchange completes
+        if cuda:
+            done = torch.cuda.Event()
+            done.record(main)
+            with torch.cuda.stream(comm):
+                comm.wait_event(done)
+                dist.all_to_all_single(recv[k].view(-1), send.view(-1), group=group)
+        else:
+            dist.all_to_all_single(recv[k].view(-1), send.view(-1), group=group)
+    if cuda:
+        main.wait_stream(comm)
+        if ev:
+            ev[1].record(main)
+            torch.cuda.synchronize()
+            timing.update(pass1_and_alltoall_overlapped_ms=ev[0].elapsed_time(ev[1]))
+    return recv.permute(1, 0, 2, 3).reshape(world * R, C)
+
+
 def tensor_product_2d(x_rows: torch.Tensor, group=None, row_fn: Optional[Callable] = None,
                       col_fn: Optional[Callable] = None, direction: str = "leg2cheb",
-                      restore_rows: bool = False, timing: Optional[dict] = None) -> torch.Tensor:
+                      restore_rows: bool = False, timing: Optional[dict] = None, chunks: int = 1) -> torch.Tensor:
     """2-D transform of an n0 x n1 array partitioned by rows (this rank: [n0/world, n1]).
 
     Pass 1 along axis 1 on the row slab, all-to-all, pass 2 along axis 0 on the column slab
-    ([n0, n1/world], batch-contiguous).  Returns the column slab, or the row slab if restore_rows."""
+    ([n0, n1/world], batch-contiguous).  Returns the column slab, or the row slab if restore_rows.
+    chunks > 1 (world > 1): pass 1 in row chunks, each chunk's all-to-all overlapping the next
+    chunk's transform (SURVEY 8(e) "chunk pass 1 by destination ... on a comm stream")."""
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     R, n1 = x_rows.shape
     n0 = R * world
     C = n1 // world
+    if chunks < 1 or R % chunks:
+        raise ValueError("chunks must divide the rows of the slab")
     if row_fn is None or col_fn is None:
         from .api import Plan
         if row_fn is None:
-            prow = Plan(n1, direction, batch=R, device=x_rows.device)
+            prow = Plan(n1, direction, batch=R // chunks if world > 1 else R, device=x_rows.device)
             row_fn = prow.execute
         if col_fn is None:
             pcol = Plan(n0, direction, batch=C, device=x_rows.device, layout="batch")
             col_fn = pcol.execute
+    if world > 1 and chunks > 1:
+        yc = _chunked_exchange(x_rows, row_fn, chunks, group, timing)
+        z = col_fn(yc)
+        return transpose_cols_to_rows(z, group) if restore_rows else z
     ev = None
     if timing is not None and x_rows.is_cuda:
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]

@@ -69,7 +69,10 @@ def _worker(rank, world, port, n0, n1, results):
         z = tensor_product_2d(mine, None, row_fn=_oracle_rows, col_fn=_oracle_cols_batch_layout)
         zr = tensor_product_2d(mine, None, row_fn=_oracle_rows, col_fn=_oracle_cols_batch_layout,
                                restore_rows=True)
-        results[rank] = (ok_roundtrip, ok_cols, z.numpy().copy(), zr.numpy().copy())
+        # pass 1 in chunks, each chunk's all-to-all overlapping the next chunk (same result, bit for bit)
+        zc = tensor_product_2d(mine, None, row_fn=_oracle_rows, col_fn=_oracle_cols_batch_layout,
+                               chunks=R if R % 2 else 2) if R > 1 else z
+        results[rank] = (ok_roundtrip, ok_cols, z.numpy().copy(), zr.numpy().copy(), zc.numpy().copy())
     finally:
         dist.destroy_process_group()
 
@@ -90,8 +93,9 @@ def test_tensor_product_2d_gloo(world, n0, n1):
     C = n1 // world
     R = n0 // world
     for r in range(world):
-        ok_rt, ok_cols, z, zr = results[r]
+        ok_rt, ok_cols, z, zr, zc = results[r]
         assert ok_rt and ok_cols
+        assert np.array_equal(zc, z)
         assert np.max(np.abs(z - ref[:, r * C:(r + 1) * C])) <= 1e-15 * np.max(np.abs(ref))
         assert np.max(np.abs(zr - ref[r * R:(r + 1) * R])) <= 1e-15 * np.max(np.abs(ref))
 
@@ -117,3 +121,42 @@ def test_batch_sharding_gloo():
     mp.spawn(_batch_worker, args=(world, _free_port(), total, results), nprocs=world, join=True)
     assert results[0][:2] == (0, 2049) and results[1][:2] == (2049, 4097)
     assert all(results[r][2] == total and results[r][3] == float(world) for r in range(world))
+
+
+def _batched_worker(rank, world, port, n, total, results):
+    from paper_2411_00033_b200.dist import BatchedTransform
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        g = torch.Generator().manual_seed(9)
+        full = torch.randn(total, n, generator=g, dtype=torch.float64)
+        bt = BatchedTransform(n, "leg2cheb", total, transform=_oracle_rows)  # CPU stand-in for the plan
+        mine = full[bt.start:bt.stop].contiguous()
+        z = bt(mine)
+        # gather every rank's slice to rank 0 in rank order (sizes differ by at most one)
+        sizes = [torch.zeros(1, dtype=torch.int64) for _ in range(world)]
+        dist.all_gather(sizes, torch.tensor([z.shape[0]]))
+        mx = int(max(t.item() for t in sizes))
+        pad = torch.zeros(mx, n, dtype=torch.float64)
+        pad[: z.shape[0]] = z
+        parts = [torch.zeros(mx, n, dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(parts, pad)
+        if rank == 0:
+            results[0] = torch.cat([p[: int(sz.item())] for p, sz in zip(parts, sizes)]).numpy()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,total", [(2, 7), (3, 2)])
+def test_batched_transform_end_to_end_gloo(world, total):
+    """BatchedTransform end to end on CPU ranks (oracle as the per-rank transform): every vector is
+    transformed exactly once, by the rank that owns it, including ranks that own none (total < world)."""
+    import oracle
+    n = 50
+    mgr = mp.Manager()
+    results = mgr.dict()
+    mp.spawn(_batched_worker, args=(world, _free_port(), n, total, results), nprocs=world, join=True)
+    g = torch.Generator().manual_seed(9)
+    full = torch.randn(total, n, generator=g, dtype=torch.float64)
+    ref = np.stack([oracle.l2c(r.numpy()).astype(np.float64) for r in full])
+    assert np.array_equal(results[0], ref)

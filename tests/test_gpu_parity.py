@@ -201,4 +201,5 @@ def test_kernel_info_consistent():
     d = p.desc
     assert ki["vt"] == d["vt"] and ki["kd"] == d["subtree"] and ki["cb"] == d["stage_blocks"]
     assert ki["stream_grid"] <= ki["stream_occ"] * torch.cuda.get_device_properties(dev).multi_processor_count
-    assert ki["m2l_units"] > 0 and ki["band_units"] > 0 and p.kernels_per_execute == 3
+    assert ki["m2l_units"] > 0 and ki["band_units"] > 0
+    assert p.kernels_per_execute == 3 and 0 < ki["up_ksub"] <= ki["kup"]

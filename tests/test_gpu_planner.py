@@ -9,6 +9,7 @@ import pytest
 import torch
 
 import oracle
+from alg3_model import gauss_nodes, kernel
 
 pytestmark = pytest.mark.gpu
 
@@ -68,9 +69,19 @@ def _exact_lam(direction, x, y, lam):
     return float(2 * (X + np.longdouble(0.5)) * Y / ((X + Y) * (X + Y + 1) * (X - Y + 1)) * (lam[k] / lam[m]))
 
 
+# Chebyshev approximation error of M = 18 modes on a submatrix, at integer points including the block
+# edges (X, Y = -1 and near +1), relative to the block's largest entry.  Measured (round 2): L2C <= 8e-15
+# ("M = 18 is sufficient for full double precision"); C2L <= 2.3e-13 -- the kernel of
+# eq:Lxymod is less smooth near the diagonal, cf. the C2L errors of Table 1.
+APPROX = {"leg2cheb": 2e-14, "cheb2leg": 1e-12}
+
+
 @pytest.mark.parametrize("direction", ["leg2cheb", "cheb2leg"])
 @pytest.mark.parametrize("n", [4096, 1_000_000, 10_000_000])
-def test_ahat_reconstructs_exact_entries(direction, n):
+def test_ahat_pins(direction, n):
+    """(a) DCT exactness: T A_hat T^T at the Chebyshev-Gauss nodes reproduces the sampled kernel
+    (eq:aklmore is the inverse of that evaluation), with the kernel evaluated independently by mpmath;
+    (b) approximation: at integer points of the submatrix it reproduces the exact entries a_xy."""
     dev = _dev()
     p = _plan(n, direction, device=dev)
     d = p.desc
@@ -79,15 +90,24 @@ def test_ahat_reconstructs_exact_entries(direction, n):
     assert A.shape[0] == d["nc"]
     rng = np.random.default_rng(n % 1009 + (0 if direction == "leg2cheb" else 1))
     lam = oracle.lam(d["N"] + 1)
-    worst = 0.0
-    for g, b, r, q in _blocks(L, rng, per_level=4 if n > 10**6 else 6):
+    XG = gauss_nodes()
+    TG = np.stack([_cheb(X) for X in XG])  # TG[m, k] = T_k(X_m)
+    worst_nodes = worst_int = 0.0
+    for g, b, r, q in _blocks(L, rng, per_level=2 if n > 10**6 else 4):
         pp, qq = (0, 0) if r == 0 else ((0, 1) if r == 1 else (1, 1))  # eq:cfrompq
         h = s << (L - g - 1)
         i0, j0 = 2 * h * (2 * b + pp), 2 * h * (2 * b + qq + 2)  # eq:globalij
-        xs = rng.integers(i0, i0 + 2 * h, 3)
+        # (a) at the Gauss nodes x_m = i0 + h(X_m + 1), y_n = j0 + h(X_n + 1) (eq:Xfromx)
+        if g <= 2 or rng.random() < 0.5:
+            G = np.array([[kernel(direction, i0, j0, h, X, Y) for Y in XG] for X in XG])
+            e = np.max(np.abs(TG @ A[q] @ TG.T - G)) / np.max(np.abs(G))
+            worst_nodes = max(worst_nodes, e)
+            assert e < 1e-14, ("nodes", direction, n, g, b, r, e)
+        # (b) at integer points, block edges included
+        xs = np.r_[i0, i0 + 2 * h - 1, rng.integers(i0, i0 + 2 * h, 2)]
         vals, refs = [], []
         for x in xs:
-            for y in (j0 + (x - i0) % 2, j0 + 2 * h - 2 + (x - i0) % 2, int(rng.integers(j0, j0 + 2 * h))):
+            for y in (j0, j0 + 2 * h - 1, int(rng.integers(j0, j0 + 2 * h))):
                 y = int(y) + ((int(y) - int(x)) % 2)  # same parity as x (a nonzero entry of A)
                 if y >= j0 + 2 * h:
                     y -= 2
@@ -98,13 +118,13 @@ def test_ahat_reconstructs_exact_entries(direction, n):
                     assert abs(refs[-1] - _exact_oracle(direction, int(x), y)) <= 1e-15 * abs(refs[-1])
         vals, refs = np.array(vals), np.array(refs)
         err = np.max(np.abs(vals - refs)) / np.max(np.abs(refs))
-        worst = max(worst, err)
-        # M = 18 modes are "sufficient for full double precision"
-        assert err < 5e-15, (direction, n, g, b, r, err)
-    print(f"{direction} n={n}: worst block-relative reconstruction error {worst:.2e}")
+        worst_int = max(worst_int, err)
+        assert err < APPROX[direction], ("integer points", direction, n, g, b, r, err)
+    print(f"{direction} n={n}: Gauss-node reconstruction {worst_nodes:.2e}, integer points {worst_int:.2e}")
 
 
 def test_plan_time_reported():
     dev = _dev()
     p = _plan(1_000_000, "leg2cheb", device=dev)
-    assert 0.0 < p.plan_device_ms < 50.0, p.plan_device_ms
+    # the planner moves ~127 MB of A_hat for 1e6 (~20 us at HBM speed); 2 ms is a loose upper bound
+    assert 0.0 < p.plan_device_ms < 2.0, p.plan_device_ms

@@ -41,6 +41,7 @@ for _ in range(300 if n * batch < 10**7 else 5):
     y = p.execute(x)
 torch.cuda.synchronize()
 NAMES = {"up": ["start", "staged", "step1", "subtreeM2M", "written", "cont", "contdone", "exit"],
+         "upb": ["start", "lvlL-2", "lvlL-3", "merge0", "merge0done", "cont", "contdone", "end"],
          "stream": ["start", "end", "banddone", "-", "-", "-", "-", "m2ldone"],
          "down": ["start", "gdwait", "loaded", "chain", "subtree", "end", "-", "-"]}
 for rep in range(2):
@@ -50,11 +51,16 @@ for rep in range(2):
     torch.cuda.synchronize()
     buf = np.zeros(1 << 20, dtype=np.uint64)
     ts = {}
-    for kern, name in enumerate(NAMES):
+    for kern, name in enumerate(n for n in NAMES if n != "upb"):
         lib.lc_debug_timestamps(kern, buf.ctypes.data_as(ctypes.POINTER(ctypes.c_ulonglong)), buf.size)
         a = buf.reshape(-1, 8).astype(np.int64).copy()
+        if name == "up":  # lc_upb_kernel (split up pass) writes rows 100000 + CTA of the up table
+            ub = a[100000:]
+            ts["upb"] = ub[ub[:, 0] > 0]
+            a = a[:100000]
         ts[name] = a[a[:, 0] > 0]
     t0 = ts["up"][:, 0].min() if len(ts["up"]) else ts["stream"][:, 0].min()
+    ts = {k: ts[k] for k in ("up", "upb", "stream", "down") if k in ts}
     allv = np.concatenate([a[a > 0] for a in ts.values()])
     diffs = np.diff(np.unique(allv))
     print(f"=== rep {rep}: n={n} {d} batch={batch} desc vt={p.desc['vt']} subtree={p.desc['subtree']}"
