@@ -232,6 +232,12 @@ def measure(config, args, world, rank, local, headline=True):
     pl, pc, plan_info = make_plans(config, n, V, dev, world, opts)
     C = n // world
     chunks = args.chunks if (two_d and world > 1 and V % max(1, args.chunks) == 0) else 1
+    split = args.split_vector and V == 1 and world > 1 and not two_d  # NEXT-2: one vector over the ranks
+    if split:
+        from paper_2411_00033_b200.dist import SingleVectorTransform
+        scaling = "strong"
+        sl = SingleVectorTransform(n, "leg2cheb", device=dev)
+        sc = SingleVectorTransform(n, "cheb2leg", device=dev)
     if two_d:
         # rows [v0, v0+V) of the n x n array on this rank; pass 1 along axis 1 (V row vectors), all-to-all,
         # pass 2 along axis 0 (n/world column vectors, batch-contiguous); with chunks > 1 pass 1 runs in
@@ -247,6 +253,11 @@ def measure(config, args, world, rank, local, headline=True):
                                   chunks=chunks)
             else:
                 tensor_product_2d(x, row_fn=lambda a: pl.execute(a, tmp), col_fn=lambda a: pc.execute(a, ycol))
+    elif split:
+        xf = x.reshape(-1)
+
+        def step():  # every rank: its rows of leg2cheb, all-gather, its rows of cheb2leg, all-gather
+            y.copy_(sc(sl(xf)).reshape(1, -1))
     else:
         def step():
             pl.execute(x, tmp)
@@ -288,7 +299,7 @@ def measure(config, args, world, rank, local, headline=True):
     clk = clocks.stop()
     ms = allreduce_max(ms_local, world)
     coeffs = 2.0 * n * V  # per rank per step (2 transforms or 2 passes)
-    total_coeffs = allreduce_sum(coeffs, world)
+    total_coeffs = allreduce_sum(coeffs, world) if not split else coeffs  # split: one vector in total
     value = total_coeffs * args.steps / (ms / 1e3)
     med_ms = allreduce_max(statistics.median(per_step), world)
     min_ms = allreduce_max(min(per_step), world)
@@ -454,7 +465,9 @@ def measure(config, args, world, rank, local, headline=True):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": scaling,
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE.json recipe)",
-        "config": {"workload": (f"{config}: leg2cheb then cheb2leg (round trip) of {V} fp64 vector(s) "
+        "config": {"workload": (f"{config}: leg2cheb then cheb2leg (round trip) of one fp64 vector of n={n} "
+                                f"split over {world} GPUs by output rows (NEXT-2, rows all-gathered)") if split else
+                               (f"{config}: leg2cheb then cheb2leg (round trip) of {V} fp64 vector(s) "
                                 f"of n={n} per GPU") if not two_d else
                                (f"cfg5: 2-D leg2cheb of an {n}x{n} fp64 array (axis 1, all-to-all, axis 0), "
                                 f"{V} rows per GPU"), "n": n, "vectors_per_gpu": V, "N_padded": dl["N"],
@@ -652,6 +665,9 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-seconds", type=float, default=60.0)
     ap.add_argument("--e2e-steps", type=int, default=200)
+    ap.add_argument("--split-vector", action="store_true",
+                    help="cfg2/cfg2b at N > 1: one vector split over the ranks by output rows (NEXT-2) "
+                         "instead of one replica per rank")
     ap.add_argument("--chunks", type=int, default=4,
                     help="cfg5 at N > 1: pass-1 row chunks whose all-to-all overlaps the next chunk (1: no overlap)")
     ap.add_argument("--batched", default="cfg3", choices=["cfg3", "cfg4", "cfg5", "none"],

@@ -83,6 +83,13 @@ typedef struct {
                        needs L >= 1 and s <= 32; automatic choice from about one tile per SM, or a third of that for n <= 2048);
                        3 -> up kernel of 8-vector tiles + the per-tile pass over leaf ranges (needs L >= 1, s <= 32;
                        automatic for L >= 9 with >= 8 vectors from n = 2^18, >= 16 below, and fewer tiles than SMs) */
+  int32_t part_index; /* partitioned plan (NEXT-2, one long transform over several GPUs): this plan computes */
+  int32_t part_count; /* output rows [row_lo, row_hi) of part part_index of part_count (lc_partition); 0/1 -> all.
+                         The input is the whole vector (the upward pass -- leaf projection and M2M, PAPER.md:363-379
+                         -- runs whole on every part); the M2L of the rows of the part and of their ancestor
+                         segments, the band of its rows and the downward pass of its subtrees run here
+                         (eq:fgamma, eq:flevels, eq:zlevels).  Rows outside the part are not
+                         written.  Engine 1 only. */
 } lc_plan_opts;
 
 /* Geometry and algorithmic work of a plan (per vector unless stated). */
@@ -103,7 +110,14 @@ typedef struct {
   int32_t vt, subtree, stage_blocks, stages; /* chosen kernel configuration */
   int32_t kernels_per_execute;               /* kernel launches per lc_execute */
   double plan_device_ms;                     /* device time of the planning kernels at create (CUDA events) */
+  int64_t row_lo, row_hi;                    /* output rows this plan computes ([0, n) unless partitioned) */
 } lc_plan_desc;
+
+/* Host-only: output rows [*row_lo, *row_hi) of part part_index of part_count for length n (s_hat <= 0
+ * -> 32).  Parts are contiguous runs of whole groups of 64 leaf segments of 2s rows,
+ * balanced over the segments that hold outputs; a part may be empty.  Errors: INVALID_ARG. */
+lc_status lc_partition(int64_t n, int64_t s_hat, int32_t part_index, int32_t part_count, int64_t* row_lo,
+                       int64_t* row_hi);
 
 /* Host-only geometry (no GPU needed): fills n, N, L, s, M, nc, band_nnz,
  * flops_alg (batch = 1), bytes_alg (batch = 1).  s_hat <= 0 -> 32.

@@ -21,7 +21,7 @@ c_dp = ctypes.POINTER(ctypes.c_double)
 class PlanOpts(ctypes.Structure):
     _fields_ = [("s_hat", c_i64), ("M", c_i32), ("layout", c_i32), ("ld_in", c_i64), ("ld_out", c_i64),
                 ("device", c_i32), ("vt", c_i32), ("subtree", c_i32), ("stage_blocks", c_i32), ("stages", c_i32),
-                ("up_subtree", c_i32), ("engine", c_i32)]
+                ("up_subtree", c_i32), ("engine", c_i32), ("part_index", c_i32), ("part_count", c_i32)]
 
 
 class PlanDesc(ctypes.Structure):
@@ -29,7 +29,8 @@ class PlanDesc(ctypes.Structure):
                 ("nc", c_i64), ("direction", c_i64), ("band_nnz", c_i64), ("plan_bytes", ctypes.c_size_t),
                 ("workspace_bytes", ctypes.c_size_t), ("flops_alg", ctypes.c_double), ("bytes_alg", ctypes.c_double),
                 ("vt", c_i32), ("subtree", c_i32), ("stage_blocks", c_i32), ("stages", c_i32),
-                ("kernels_per_execute", c_i32), ("plan_device_ms", ctypes.c_double)]
+                ("kernels_per_execute", c_i32), ("plan_device_ms", ctypes.c_double), ("row_lo", c_i64),
+                ("row_hi", c_i64)]
 
     def as_dict(self):
         return {name: getattr(self, name) for name, _ in self._fields_}
@@ -38,6 +39,7 @@ class PlanDesc(ctypes.Structure):
 # name -> (restype, argtypes); must match include/legcheb.h (checked by tests/test_host.py)
 SIGNATURES = {
     "lc_geometry": (c_i32, [c_i64, c_i64, ctypes.POINTER(PlanDesc)]),
+    "lc_partition": (c_i32, [c_i64, c_i64, c_i32, c_i32, ctypes.POINTER(c_i64), ctypes.POINTER(c_i64)]),
     "lc_plan_create": (c_i32, [ctypes.POINTER(c_vp), c_i64, c_i32, c_i64, ctypes.POINTER(PlanOpts)]),
     "lc_plan_describe": (c_i32, [c_vp, ctypes.POINTER(PlanDesc)]),
     "lc_workspace_bytes": (ctypes.c_size_t, [c_vp]),

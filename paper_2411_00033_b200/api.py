@@ -29,6 +29,15 @@ def geometry(n: int, s_hat: int = 32) -> dict:
     return d.as_dict()
 
 
+def partition(n: int, part_index: int, part_count: int, s_hat: int = 32) -> tuple[int, int]:
+    """Output rows [lo, hi) of part part_index of part_count (lc_partition; host only): contiguous runs of
+    whole groups of leaf segments, for one long transform split over several GPUs (NEXT-2)."""
+    lo, hi = ctypes.c_int64(), ctypes.c_int64()
+    _lib.check("lc_partition", _lib.load().lc_partition(int(n), int(s_hat), int(part_index), int(part_count),
+                                                        ctypes.byref(lo), ctypes.byref(hi)))
+    return int(lo.value), int(hi.value)
+
+
 def _stream_handle(stream, device=None) -> int:
     """cudaStream_t of `stream`; None -> torch's current stream of `device` (the plan's device)."""
     if stream is None:
@@ -42,7 +51,7 @@ class Plan:
     def __init__(self, n: int, direction="leg2cheb", batch: int = 1, device=None, s_hat: int = 32,
                  layout="vec", ld_in: int = 0, ld_out: int = 0, vt: int = 0, subtree: int = 0,
                  stage_blocks: int = 0, stages: int = 0, up_subtree: int = 0,
-                 engine: int = 0):
+                 engine: int = 0, part_index: int = 0, part_count: int = 0):
         lib = _lib.load()
         if device is None:
             device = torch.cuda.current_device()
@@ -54,7 +63,7 @@ class Plan:
         opts = _lib.PlanOpts(s_hat=s_hat, M=18, layout=self.layout, ld_in=ld_in, ld_out=ld_out,
                              device=device.index if device.index is not None else -1, vt=vt, subtree=subtree,
                              stage_blocks=stage_blocks, stages=stages, up_subtree=up_subtree,
-                             engine=engine)
+                             engine=engine, part_index=part_index, part_count=part_count)
         h = ctypes.c_void_p()
         with torch.cuda.device(device):
             _lib.check("lc_plan_create", lib.lc_plan_create(ctypes.byref(h), self.n, self.direction, self.batch,

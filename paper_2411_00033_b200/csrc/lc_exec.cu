@@ -179,6 +179,9 @@ struct StreamParams {
   int64_t w_tile;  // doubles per vector tile (w and c share the layout)
   int64_t ld_in, ld_out, n, N, batch;
   int64_t ntiles, nm2l, nband;
+  int band_lo;      // first band unit (leaf range) of a partitioned plan (NEXT-2), else 0
+  int blo[32];      // first M2L block per level (partitioned plan: the rows of its leaf range), else 0
+  int nblk[32];     // M2L blocks per level (else 2^(g+1) - 1)
   int layout, L, s, cb, nst, kb, gr_up;
   int lvorder[32];  // M2L level order: position o -> level
 };
@@ -193,6 +196,7 @@ struct DownParams {
   int64_t ld_out, n, N, batch, w_tile;
   int layout, L, s, k;
   int bulk;  // TMA bulk loads allowed (out 16-byte aligned, ld_out even, full tiles only)
+  int64_t sub_lo;  // first subtree of a partitioned plan (NEXT-2), else 0
 };
 
 // ============================================================== up kernel
@@ -708,7 +712,7 @@ __device__ __forceinline__ void band_sync() { named_sync(1, kBandThreads); }
 // the order lvorder[]; tiles innermost so concurrent CTAs share A_hat in L2.
 // cstart[o] = first chunk of the o-th level of the order (shared-memory table).
 __device__ __forceinline__ void m2l_unit(int q, int ntiles, int L, int cb, const int* cstart, const int* lvord,
-                                         int& g, int& b0, int& nb, int& tile) {
+                                         const int* blo, const int* nblk, int& g, int& b0, int& nb, int& tile) {
   int ch = q;
   tile = 0;
   if (ntiles > 1) {
@@ -718,8 +722,8 @@ __device__ __forceinline__ void m2l_unit(int q, int ntiles, int L, int cb, const
   int o = 0;
   while (o + 1 < L && cstart[o + 1] <= ch) ++o;
   g = lvord[o];
-  b0 = (ch - cstart[o]) * cb;
-  const int bg = (2 << g) - 1;
+  b0 = blo[g] + (ch - cstart[o]) * cb;
+  const int bg = blo[g] + nblk[g];
   nb = (bg - b0) < cb ? (bg - b0) : cb;
 }
 
@@ -990,7 +994,7 @@ __global__ void __launch_bounds__(kStreamThreads, 2) lc_stream_kernel(const __gr
     for (int o = 0; o < P.L && o < 32; ++o) {
       cstart[o] = acc;
       const int g = P.lvorder[o];
-      acc += ((2 << g) - 1 + cb - 1) / cb;
+      acc += (P.nblk[g] + cb - 1) / cb;
     }
     for (int i = 0; i < nst; ++i) {
       mbar_init(&full[i], 1);
@@ -1010,7 +1014,7 @@ __global__ void __launch_bounds__(kStreamThreads, 2) lc_stream_kernel(const __gr
       bool fine_ok = false, coarse_ok = false;
       auto issue = [&](int q, int j, bool with_a, bool with_w) {  // M2L unit q, ring use j
         int g, nb, b0, tile;
-        m2l_unit(q, ntiles, P.L, cb, cstart, P.lvorder, g, b0, nb, tile);
+        m2l_unit(q, ntiles, P.L, cb, cstart, P.lvorder, P.blo, P.nblk, g, b0, nb, tile);
         const int slot = j % nst;
         unsigned char* base = smem + SL.ring + slot * SL.slot;
         const uint32_t abytes = uint32_t(nb) * 3 * kMM * 8;
@@ -1073,7 +1077,7 @@ __global__ void __launch_bounds__(kStreamThreads, 2) lc_stream_kernel(const __gr
       const int q = slotq[slot];
       if (q < 0) break;
       int g, nb, b0, tile;
-      m2l_unit(q, ntiles, P.L, cb, cstart, P.lvorder, g, b0, nb, tile);
+      m2l_unit(q, ntiles, P.L, cb, cstart, P.lvorder, P.blo, P.nblk, g, b0, nb, tile);
       const double* As = reinterpret_cast<const double*>(smem + SL.ring + slot * SL.slot);
       const double* wwin = reinterpret_cast<const double*>(smem + SL.ring + slot * SL.slot + a_bytes);
       double* ct = P.c + int64_t(tile) * P.w_tile + (w_level_offset_units(g) + 2 * int64_t(b0)) * VM;
@@ -1228,7 +1232,7 @@ __global__ void __launch_bounds__(kStreamThreads, 2) lc_stream_kernel(const __gr
       band_sync();
       if (u >= nband) break;
       const int tile = ntiles > 1 ? u % ntiles : 0;
-      const int lr = ntiles > 1 ? u / ntiles : u;
+      const int lr = (ntiles > 1 ? u / ntiles : u) + P.band_lo;
       band_unit<VT, DIR>(P, tile, lr, ta, tb, gt, zst, tp, btid);
     }
     LC_TS_T(1, 2);
@@ -1302,7 +1306,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) lc_down_kernel(const DownParams 
   const int VM = VT * kM;
   const int nleaf = 1 << kd;
   const int seglen = 2 * s;
-  const int64_t R = blockIdx.x;
+  const int64_t R = blockIdx.x + P.sub_lo;
   const int64_t tile = blockIdx.y;
   const int64_t U0 = R << kd;
   const int64_t i0 = U0 * seglen;
@@ -2517,7 +2521,8 @@ lc_status configure_kernels(lc_plan* p) {
   int vt = p->vt;
   // automatic engine 3 (tools/engine_cross3.py on the B200): long vectors in batches of 8+ (>= 16 below
   // n = 2^18), deep enough trees for ranges of >= 64 leaves; e.g. 64 x 10^7: 41.8 -> 22.9 ms per transform
-  if (p->engine == 0 && p->vt <= 0 && L >= 9 && p->s <= 32 && p->batch >= 8 && (p->batch >= 16 || p->n >= 262144) &&
+  if (p->engine == 0 && p->part_count <= 1 && p->vt <= 0 && L >= 9 && p->s <= 32 && p->batch >= 8 &&
+      (p->batch >= 16 || p->n >= 262144) &&
       ((p->batch + kTileV - 1) / kTileV) < int64_t(p->sm_count))
     p->engine = 3;
   if (p->engine == 3) {  // up kernel of 8-vector tiles feeding the per-range pass
@@ -2541,6 +2546,7 @@ lc_status configure_kernels(lc_plan* p) {
            down_smem_bytes(vt, kd + 1, s, L) <= budget2)
       ++kd;
     if (user_k) kd = std::min(p->k, L - 1);
+    if (p->part_count > 1) kd = std::min(kd, part_align_log2(L));  // down subtrees inside one part
   }
   if (down_smem_bytes(vt, kd, s, L) > smax) return LC_ERR_INVALID_ARG;
   // streaming kernel: band units of 2^kb leaf segments
@@ -2604,10 +2610,38 @@ lc_status configure_kernels(lc_plan* p) {
     }
     if (o != L) return LC_ERR_INTERNAL;
   }
+  // M2L blocks per level: all of them, or (a partitioned plan, NEXT-2) the row blocks of the segments
+  // that contain a leaf of the part, i.e. its own rows and their ancestors' (the down kernel's chain)
   int64_t nchunks = 0;
-  for (int g = 0; g < L; ++g) nchunks += (((int64_t(2) << g) - 1) + cb - 1) / cb;
+  for (int g = 0; g < L; ++g) {
+    const int64_t bg = (int64_t(2) << g) - 1;
+    int64_t blo = 0, nb = bg;
+    if (p->part_count > 1) {
+      const int sh = L - 1 - g;
+      if (p->part_hi > p->part_lo) {
+        const int64_t ulo = p->part_lo >> sh, uhi = (p->part_hi - 1) >> sh;
+        blo = std::min(bg, ulo >> 1);
+        nb = std::max<int64_t>(0, std::min(bg, (uhi >> 1) + 1) - blo);
+      } else {
+        nb = 0;
+      }
+    }
+    p->blo[g] = int(blo);
+    p->nblk[g] = int(nb);
+    nchunks += (nb + cb - 1) / cb;
+  }
   p->m2l_units = nchunks * p->ntiles;
-  p->band_units = (nleaf_total >> kb) * p->ntiles;
+  if (p->part_count > 1) {
+    p->band_lo = int(p->part_lo >> kb);
+    p->band_units = ((p->part_hi - p->part_lo) >> kb) * p->ntiles;
+    p->sub_lo = p->part_lo >> kd;
+    p->nsub_down = (p->part_hi - p->part_lo) >> kd;
+  } else {
+    p->band_lo = 0;
+    p->band_units = (nleaf_total >> kb) * p->ntiles;
+    p->sub_lo = 0;
+    p->nsub_down = L > 0 ? (int64_t(2) << L) >> kd : 1;
+  }
   if (p->m2l_units + p->band_units > 0x7fffffff) return LC_ERR_INVALID_ARG;
   {
     const int occ = stream_occupancy_vt(vt, p->dir, p->smem_stream);
@@ -2627,6 +2661,11 @@ lc_status configure_kernels(lc_plan* p) {
   // workspace: w | c_m2l | flags (64 ints) | arrival counters (c_m2l rows without a submatrix stay zero)
   const size_t wb = size_t(align_up(p->ntiles * p->w_tile_doubles * 8, 256));
   p->ws_bytes = 2 * wb + 256 + size_t(p->ntiles * p->cnt_tile_ints) * sizeof(int) + 64 * sizeof(int);
+  if (p->part_count > 1) {  // partitioned plans (NEXT-2) run the level-pipelined kernels
+    if (p->engine != 0 && p->engine != 1) return LC_ERR_INVALID_ARG;
+    p->engine = 1;
+    return LC_OK;
+  }
   // per-tile streaming kernel (engine 2): many 8-vector tiles of short vectors
   {
     const int64_t ntiles8 = (p->batch + kTileV - 1) / kTileV;
@@ -2829,12 +2868,22 @@ static lc_status launch_execute_impl(const lc_plan* p, const double* in, double*
   sp.N = p->N; sp.batch = p->batch; sp.ntiles = p->ntiles; sp.nm2l = p->m2l_units; sp.nband = p->band_units;
   sp.layout = p->layout; sp.L = int(p->L); sp.s = int(p->s); sp.cb = p->bps; sp.nst = p->nst; sp.kb = p->kb;
   sp.gr_up = p->grup + (p->kup - p->up_ksub);  // finest level left to the continuation + 1
-  for (int i = 0; i < 32; ++i) sp.lvorder[i] = p->lvorder[i];
+  for (int i = 0; i < 32; ++i) {
+    sp.lvorder[i] = p->lvorder[i];
+    sp.blo[i] = p->blo[i];
+    sp.nblk[i] = p->nblk[i];
+  }
+  sp.band_lo = p->band_lo;
   DownParams dp{};
   dp.out = out; dp.flags = flags; dp.c = c; dp.Tpad = p->d_Tpad; dp.B = p->d_B; dp.ld_out = p->ld_out; dp.n = p->n; dp.N = p->N; dp.batch = p->batch;
   dp.w_tile = p->w_tile_doubles; dp.layout = p->layout; dp.L = int(p->L); dp.s = int(p->s); dp.k = p->k;
   dp.bulk = (p->down_bulk && reinterpret_cast<uintptr_t>(out) % 16 == 0 && p->ld_out % 2 == 0) ? 1 : 0;
-  const int64_t ndown = p->L > 0 ? (int64_t(2) << p->L) >> p->k : 1;
+  dp.sub_lo = p->sub_lo;
+  const int64_t ndown = p->nsub_down;
+  if (p->part_count > 1 && (ndown == 0 || p->m2l_units + p->band_units == 0)) {
+    if (prev != p->device) cudaSetDevice(prev);
+    return LC_OK;  // an empty part of a partitioned plan: no rows to compute
+  }
   const int64_t nsub = p->L > 0 ? (int64_t(4) << p->grup) : 1;
   if (nsub > 0x7fffffff || ndown > 0x7fffffff || p->ntiles > 65535) {
     if (prev != p->device) cudaSetDevice(prev);

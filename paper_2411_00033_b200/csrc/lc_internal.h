@@ -35,6 +35,9 @@ struct Geometry {
   int64_t n, N, L, s, nc;
 };
 
+// log2 of the leaf-segment alignment of a part (NEXT-2): 64 leaves (or all of them for short trees)
+inline int part_align_log2(int64_t L) { return int(L + 1 < 6 ? L + 1 : 6); }
+
 // eq:numlevels; L clamped at 0 (band only) for n <= 4 s_hat.
 inline Geometry geometry(int64_t n, int64_t s_hat) {
   Geometry G{};
@@ -126,6 +129,13 @@ struct lc_plan {
   int engine;          // 1 = up / stream / down kernels, 2 = per-tile streaming kernel
   int down_bulk;       // engine 1 down kernel: TMA bulk loads of c_m2l and the band rows
   int up_ksub;         // engine 1: M2M levels merged inside the up kernel's subtree (<= kup)
+  // partitioned single-vector plan (NEXT-2): part part_index of part_count computes the output rows
+  // [row_lo, row_hi) = leaf segments [part_lo, part_hi); the up pass stays whole (replicated)
+  int part_index, part_count;
+  int64_t part_lo, part_hi, row_lo, row_hi;
+  int blo[32], nblk[32];  // M2L row blocks per level
+  int band_lo;            // first band unit
+  int64_t sub_lo, nsub_down;  // down-kernel subtrees
   int tile_grid;       // CTAs of the per-tile kernel (engine 2)
   size_t smem_tile;
   int range_n, range_len;   // engine 3: leaf ranges per tile and their length

@@ -19,6 +19,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <algorithm>
 #include <mutex>
 #include <utility>
 #include <vector>
@@ -279,6 +280,17 @@ int64_t band_nnz(int64_t N, int64_t s) {
   return tot;
 }
 
+// leaf segments [lo, hi) of part `pidx` of `pcnt`: whole groups of 2^part_align_log2(L) leaves, balanced
+// over the groups that hold outputs (rows < n); the last part runs to the end of the padded vector
+static void part_leaves(int64_t n, const Geometry& G, int pidx, int pcnt, int64_t* lo, int64_t* hi) {
+  const int64_t nls = G.L > 0 ? (int64_t(2) << G.L) : 2;
+  const int64_t align = int64_t(1) << part_align_log2(G.L);
+  const int64_t nreal = (n + 2 * G.s - 1) / (2 * G.s);
+  const int64_t nch = (nreal + align - 1) / align;
+  *lo = std::min(nls, (int64_t(pidx) * nch / pcnt) * align);
+  *hi = pidx == pcnt - 1 ? nls : std::min(nls, (int64_t(pidx + 1) * nch / pcnt) * align);
+}
+
 static void fill_work(lc_plan_desc* d, int64_t batch) {
   const double M = kM;
   const int64_t L = d->L;
@@ -324,6 +336,20 @@ const char* lc_status_string(lc_status s) {
     case LC_ERR_INTERNAL: return "internal error";
   }
   return "unknown status";
+}
+
+lc_status lc_partition(int64_t n, int64_t s_hat, int32_t part_index, int32_t part_count, int64_t* row_lo,
+                       int64_t* row_hi) {
+  if (n < 1 || !row_lo || !row_hi || part_count < 1 || part_index < 0 || part_index >= part_count)
+    return LC_ERR_INVALID_ARG;
+  if (s_hat <= 0) s_hat = 32;
+  if (s_hat < 2 || s_hat > 64) return LC_ERR_INVALID_ARG;
+  const Geometry G = geometry(n, s_hat);
+  int64_t llo = 0, lhi = 0;
+  part_leaves(n, G, part_index, part_count, &llo, &lhi);
+  *row_lo = std::min(n, llo * 2 * G.s);
+  *row_hi = std::min(n, lhi * 2 * G.s);
+  return LC_OK;
 }
 
 lc_status lc_geometry(int64_t n, int64_t s_hat, lc_plan_desc* out) {
@@ -384,6 +410,22 @@ extern "C" lc_status lc_plan_create(lc_plan** out, int64_t n, lc_direction dir, 
   p->device = dev; p->sm_count = prop.multiProcessorCount;
   p->vt = o.vt; p->k = o.subtree; p->bps = o.stage_blocks; p->nst = o.stages; p->kup = o.up_subtree;
   p->engine = o.engine;
+  if (o.part_count > 1) {
+    if (o.part_index < 0 || o.part_index >= o.part_count || G.L < 1 || (o.engine != 0 && o.engine != 1)) {
+      delete p;
+      cudaSetDevice(prev_dev);
+      return LC_ERR_INVALID_ARG;
+    }
+    p->part_index = o.part_index;
+    p->part_count = o.part_count;
+    part_leaves(n, G, o.part_index, o.part_count, &p->part_lo, &p->part_hi);
+    p->row_lo = std::min(n, p->part_lo * 2 * G.s);
+    p->row_hi = std::min(n, p->part_hi * 2 * G.s);
+  } else {
+    p->part_count = 1;
+    p->row_lo = 0;
+    p->row_hi = n;
+  }
 
   auto fail = [&](lc_status st) {
     lc_plan_destroy(p);
@@ -588,6 +630,8 @@ extern "C" lc_status lc_plan_describe(const lc_plan* p, lc_plan_desc* d) {
   d->vt = p->vt; d->subtree = p->k; d->stage_blocks = p->bps; d->stages = p->nst;
   d->kernels_per_execute = kernels_per_execute(p);
   d->plan_device_ms = p->plan_ms;
+  d->row_lo = p->row_lo;
+  d->row_hi = p->row_hi;
   return LC_OK;
 }
 

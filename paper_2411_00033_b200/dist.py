@@ -1,6 +1,6 @@
 """Multi-GPU drivers over torch.distributed (one process per GPU; NCCL over NVLink).
 
-Two partitionings:
+Three partitionings:
 
 * batch sharding (cfg3, cfg4): independent vectors are split contiguously over the ranks; every rank
   holds the full plan (replicated) and transforms its own slice -- there is no collective on the data
@@ -9,6 +9,8 @@ Two partitionings:
   axis 1 (each local row is one vector); an all-to-all transposes the row slabs into column slabs;
   pass 2 transforms along axis 0 with the batch-contiguous layout (LC_BATCH_CONTIGUOUS), so no local
   transpose is needed after the exchange (`tensor_product_2d`).
+* one long vector (NEXT-2): output rows split over the ranks (`SingleVectorTransform`), the input
+  replicated, the slices all-gathered.
 
 The per-pass transform is injectable (`row_fn`, `col_fn`) so that the index algebra can be tested on
 CPU ranks with gloo; the default is the sm_100a library through `Plan`.
@@ -56,6 +58,55 @@ class BatchedTransform:
             y = self.transform(x_local)
             return y if out is None else out.copy_(y)
         return self.plan.execute(x_local, out)
+
+
+class SingleVectorTransform:
+    """One long transform split over the ranks by output rows (NEXT-2).
+
+    Every rank holds the whole input vector (replicated; `broadcast` it first if it lives on one rank)
+    and runs a partitioned plan (lc_plan_opts.part_index / part_count): the upward pass whole, then the
+    M2L of its own rows and their ancestor segments, the band of its rows and the downward pass of its
+    subtrees -- so the A_hat stream and the band, the bulk of the work, are divided by the rank count.
+    Rank r's rows are [row_lo, row_hi) (`partition`); `gather=True` all-gathers the slices into the
+    full result on every rank (NCCL over NVLink).  `transform` replaces the plan by a callable
+    (x_full, lo, hi) -> rows lo..hi (tests use a CPU stand-in); the product path builds a `Plan`."""
+
+    def __init__(self, n: int, direction: str, group=None, device=None, transform: Optional[Callable] = None,
+                 **opts):
+        from .api import partition
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.n = n
+        self.spans = [partition(n, r, self.world) for r in range(self.world)]
+        self.row_lo, self.row_hi = self.spans[self.rank]
+        self.transform = transform
+        self.plan = None
+        if transform is None:
+            from .api import Plan
+            self.plan = Plan(n, direction, batch=1, device=device, part_index=self.rank, part_count=self.world,
+                             **opts)
+            assert (self.plan.desc["row_lo"], self.plan.desc["row_hi"]) == (self.row_lo, self.row_hi)
+
+    def __call__(self, x_full: torch.Tensor, gather: bool = True) -> torch.Tensor:
+        """x_full: the whole [n] input on this rank.  Returns the full [n] result (gather) or this
+        rank's rows [row_lo, row_hi)."""
+        if x_full.numel() != self.n:
+            raise ValueError(f"need the whole vector of {self.n} coefficients on every rank")
+        lo, hi = self.row_lo, self.row_hi
+        if self.transform is not None:
+            mine = self.transform(x_full, lo, hi)
+        else:
+            z = self.plan.execute(x_full.reshape(1, -1))  # rows outside [lo, hi) are not written
+            mine = z.reshape(-1)[lo:hi]
+        if not gather or self.world == 1:
+            return mine.clone() if gather else mine
+        width = max(b - a for a, b in self.spans)
+        send = x_full.new_zeros(width)
+        send[: hi - lo] = mine
+        recv = x_full.new_empty(self.world * width)
+        dist.all_gather_into_tensor(recv, send, group=self.group)
+        return torch.cat([recv[r * width: r * width + (b - a)] for r, (a, b) in enumerate(self.spans)])
 
 
 def pack_for_transpose(y_rows: torch.Tensor, world: int) -> torch.Tensor:

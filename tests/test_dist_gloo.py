@@ -160,3 +160,37 @@ def test_batched_transform_end_to_end_gloo(world, total):
     full = torch.randn(total, n, generator=g, dtype=torch.float64)
     ref = np.stack([oracle.l2c(r.numpy()).astype(np.float64) for r in full])
     assert np.array_equal(results[0], ref)
+
+
+def _single_vector_worker(rank, world, port, n, results):
+    from paper_2411_00033_b200.dist import SingleVectorTransform
+    import oracle
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        g = torch.Generator().manual_seed(13)
+        x = torch.randn(n, generator=g, dtype=torch.float64)  # the whole vector on every rank
+
+        def rows(xf, lo, hi):  # CPU stand-in for the partitioned plan: the oracle's rows lo..hi
+            return torch.from_numpy(oracle.l2c_rows(xf.numpy(), np.arange(lo, hi)).astype(np.float64))
+
+        t = SingleVectorTransform(n, "leg2cheb", transform=rows)
+        results[rank] = (t.row_lo, t.row_hi, t(x).numpy().copy())
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n", [(2, 3000), (3, 5000)])
+def test_single_vector_split_gloo(world, n):
+    """NEXT-2 host logic on CPU ranks: the row partition covers [0, n) once (some parts may be empty)
+    and the all-gathered slices are the whole transform on every rank."""
+    import oracle
+    mgr = mp.Manager()
+    results = mgr.dict()
+    mp.spawn(_single_vector_worker, args=(world, _free_port(), n, results), nprocs=world, join=True)
+    g = torch.Generator().manual_seed(13)
+    ref = oracle.l2c(torch.randn(n, generator=g, dtype=torch.float64).numpy()).astype(np.float64)
+    spans = sorted((results[r][0], results[r][1]) for r in range(world))
+    assert spans[0][0] == 0 and spans[-1][1] == n
+    for r in range(world):
+        assert np.array_equal(results[r][2], ref)
