@@ -392,7 +392,11 @@ def measure(config, args, world, rank, local, headline=True):
     # each transform of the step, pipelined over three streams with caller-owned staging and workspaces
     # (the call is thread- and stream-safe with distinct buffers, legcheb.h)
     e2e_steps = max(3, min(args.steps, args.e2e_steps))
-    nbuf = 3
+    # three buffer sets (staging + workspace per plan and stream) when they fit, else fewer; with one set
+    # the plan-owned staging and workspace serve (calls serialised on one stream)
+    per_set = pl.host_stage_bytes + pc.host_stage_bytes + pl.workspace_bytes + pc.workspace_bytes
+    free_b = torch.cuda.mem_get_info(dev)[0]
+    nbuf = 3 if 3 * per_set < 0.6 * free_b else (2 if 2 * per_set < 0.6 * free_b else 1)
     streams = [torch.cuda.Stream(dev) for _ in range(nbuf)]
     if two_d:
         hz = [torch.empty_like(xh).pin_memory() for _ in range(nbuf)]
@@ -402,10 +406,11 @@ def measure(config, args, world, rank, local, headline=True):
     else:
         hz = [torch.empty_like(xh).pin_memory() for _ in range(nbuf)]
         hy = [torch.empty_like(xh).pin_memory() for _ in range(nbuf)]
-    st_l = [pl.new_host_stage() for _ in range(nbuf)]
-    st_c = [pc.new_host_stage() for _ in range(nbuf)]
-    ws_l = [pl.new_workspace(streams[b]) for b in range(nbuf)]
-    ws_c = [pc.new_workspace(streams[b]) for b in range(nbuf)]
+    own = nbuf == 1
+    st_l = [None] if own else [pl.new_host_stage() for _ in range(nbuf)]
+    st_c = [None] if own else [pc.new_host_stage() for _ in range(nbuf)]
+    ws_l = [None] if own else [pl.new_workspace(streams[b]) for b in range(nbuf)]
+    ws_c = [None] if own else [pc.new_workspace(streams[b]) for b in range(nbuf)]
     torch.cuda.synchronize()
 
     def host_steps(k0, k):
@@ -495,7 +500,8 @@ def measure(config, args, world, rank, local, headline=True):
         "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "steps": e2e_steps, "ms_per_step": e2e_ms / e2e_steps,
                 "path": ("lc_execute_host (C ABI: pinned host buffer -> H2D -> kernels -> D2H) for leg2cheb, then "
-                         "for cheb2leg of the host result; 3 streams with caller-owned staging/workspaces")
+                         f"for cheb2leg of the host result; {nbuf} stream(s)" +
+                         (" with caller-owned staging/workspaces" if nbuf > 1 else ", plan-owned staging/workspace"))
                         if not (two_d and world > 1) else
                         "H2D + tensor_product_2d (NCCL all-to-all) + D2H, 3 streams"},
         "gpu_launches": (kpe + pc.kernels_per_execute) * args.steps,
