@@ -220,6 +220,8 @@ def measure(config, args, world, rank, local, headline=True):
     dev = torch.device("cuda", local)
     n, V, kind, v0, scaling = workload(config, world, rank)
     two_d = config == "cfg5"
+    if args.split_vector and V == 1 and world > 1 and not two_d:
+        v0 = 0  # one vector split over the ranks: every rank holds the same input
     if two_d:
         scaling = "strong"
     xh = make_input(kind, n, V, v0, pin=True)
