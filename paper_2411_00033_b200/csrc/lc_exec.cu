@@ -63,6 +63,15 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
       : "memory");
 }
+// 1-D TMA bulk copy shared -> global (SASS: UBLKCP), bulk-group completion
+__device__ __forceinline__ void bulk_s2g(void* gdst, const void* ssrc, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(ssrc)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit_and_wait_read() {
+  asm volatile("cp.async.bulk.commit_group;\n\tcp.async.bulk.wait_group.read 0;" ::: "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   uint32_t done = 0;
   do {
@@ -1270,19 +1279,17 @@ __global__ void __launch_bounds__(kStreamThreads, 2) lc_stream_kernel(const __gr
 // as four partial sums, so a level costs one shared-memory round trip plus a 5-deep DFMA chain.
 constexpr int kDownThreads = 256;
 
-// (B(p)^T c)_l = (-1)^{pl} sum_n b_nl (-1)^{pn} c_n   (lane l); column l of
-// B(0) from shared memory (consecutive lanes, conflict-free), c broadcast.
-__device__ __forceinline__ double l2l_lane(const double* __restrict__ Bs, const double* __restrict__ c, int p, int l) {
-  const int lc = l < kM ? l : 0;
-  double x[kM], b[kM];
+// (B(p)^T c)_l = (-1)^{pl} sum_n b_nl (-1)^{pn} c_n   (lane l), with column l of
+// B(0) in registers (the ancestor chain and the narrow subtree levels reuse it), c broadcast from
+// shared memory, four partial sums
+__device__ __forceinline__ double l2l_lane_reg(const double (&b)[kM], const double* __restrict__ c, int p, int l) {
+  double x[kM];
 #pragma unroll
   for (int n = 0; n < kM; n += 2) {
     const double2 t = *reinterpret_cast<const double2*>(c + n);
     x[n] = t.x;
     x[n + 1] = t.y;
   }
-#pragma unroll
-  for (int n = 0; n < kM; ++n) b[n] = Bs[n * kM + lc];  // b_{n l} (zero above the diagonal)
   double e0 = 0.0, e1 = 0.0, o0 = 0.0, o1 = 0.0;
 #pragma unroll
   for (int n = 0; n < kM; n += 4) {
@@ -1294,6 +1301,30 @@ __device__ __forceinline__ double l2l_lane(const double* __restrict__ Bs, const 
   const double e = e0 + e1, o = o0 + o1;
   const double r = p ? e - o : e + o;
   return (p && (l & 1)) ? -r : r;
+}
+
+// both children of one parent in one pass: with e = sum_{n even} b_nl c_n and o = sum_{n odd} b_nl c_n,
+// (B(0)^T c)_l = e + o and (B(1)^T c)_l = (-1)^l (e - o)   (B(1) = B(0) with odd diagonals negated, App. A3)
+__device__ __forceinline__ void l2l_lane_pair(const double (&b)[kM], const double* __restrict__ c, int l,
+                                              double& r0, double& r1) {
+  double x[kM];
+#pragma unroll
+  for (int n = 0; n < kM; n += 2) {
+    const double2 t = *reinterpret_cast<const double2*>(c + n);
+    x[n] = t.x;
+    x[n + 1] = t.y;
+  }
+  double e0 = 0.0, e1 = 0.0, o0 = 0.0, o1 = 0.0;
+#pragma unroll
+  for (int n = 0; n < kM; n += 4) {
+    e0 = fma(b[n], x[n], e0);
+    o0 = fma(b[n + 1], x[n + 1], o0);
+    if (n + 2 < kM) e1 = fma(b[n + 2], x[n + 2], e1);
+    if (n + 3 < kM) o1 = fma(b[n + 3], x[n + 3], o1);
+  }
+  const double e = e0 + e1, o = o0 + o1;
+  r0 = e + o;
+  r1 = (l & 1) ? o - e : e - o;
 }
 
 template <int VT, int DIR, int SMAX, int NT>
@@ -1314,8 +1345,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) lc_down_kernel(const DownParams 
   // shared memory: B(0), T(sigma), cm = ancestors [g][sigma][v][M] (g < gd), subtree level j
   // at node offset gd + 2^j - 1 ([sigma][node][v][M]); zb = [v][rows]
   double* Bsh = reinterpret_cast<double*>(smem);  // B(0) [M][M]
-  double* BTsh = Bsh + kMM + 4;                    // B(0)^T [M][M] (16-byte aligned)
-  double* Tsh = BTsh + kMM + 4;                    // T(sigma) [2][SMAX][M]
+  double* Tsh = Bsh + 2 * (kMM + 4);               // T(sigma) [2][SMAX][M] (after a spare [M][M] slot)
   double* cm = Tsh + 2 * SMAX * kM;
   double* zb = cm + (L > 0 ? (int64_t(gd) + (int64_t(2) << kd) - 1) * 2 * VM : 0);
   auto cm_anc = [&](int g) { return cm + g * 2 * VM; };
@@ -1324,7 +1354,6 @@ __global__ void __launch_bounds__(NT, 512 / NT) lc_down_kernel(const DownParams 
   // plan data first: B(0) and T(sigma) (padded to SMAX rows) into shared memory
   for (int i = tid; i < kMM / 2; i += nthr) cp_async16(Bsh + 2 * i, P.B + 2 * i);
   for (int i = tid; i < SMAX * kM; i += nthr) cp_async16(Tsh + 2 * i, P.Tpad + 2 * i);
-  for (int i = tid; i < kMM; i += nthr) BTsh[(i % kM) * kM + i / kM] = __ldg(P.B + i);
   griddep_launch();
   // c_m2l and the band result are complete once the streaming kernel's last CTA released
   // flags[12] (cheaper than waiting for the grid to retire); the last down CTA to pass re-arms it
@@ -1405,6 +1434,10 @@ __global__ void __launch_bounds__(NT, 512 / NT) lc_down_kernel(const DownParams 
 
   if (L > 0) {
     // step 4 along the ancestor chain (Horner), one warp per (sigma, v), then the subtree root
+    // column `lane` of B(0) in registers for the chain and the narrow subtree levels (b_{n l})
+    double bcol[kM];
+#pragma unroll
+    for (int n = 0; n < kM; ++n) bcol[n] = Bsh[n * kM + (lane < kM ? lane : 0)];
     if (gd > 0) {
       for (int ch = warp; ch < 2 * VT; ch += nwarps) {
         double acc = lane < kM ? cm_anc(0)[ch * kM + lane] : 0.0;
@@ -1412,7 +1445,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) lc_down_kernel(const DownParams 
         for (int g = 1; g <= gd; ++g) {
           const double own = lane < kM ? (g < gd ? cm_anc(g) : cm_lvl(0))[ch * kM + lane] : 0.0;
           const int p = int((R >> (gd - g)) & 1);
-          const double r = l2l_lane(Bsh, scr, p, lane);
+          const double r = l2l_lane_reg(bcol, scr, p, lane);
           acc = r + own;
           __syncwarp();
           scr = (g < gd ? cm_anc(g) : cm_lvl(0)) + ch * kM;
@@ -1423,57 +1456,93 @@ __global__ void __launch_bounds__(NT, 512 / NT) lc_down_kernel(const DownParams 
       __syncthreads();
     }
     LC_TS(2, 3);
-    // step 4 down the subtree, level by level.  Narrow levels: one warp per (sigma, node, v),
-    // lane = mode (short dependent chain).  Wide levels: one thread per (sigma, node, v) with
-    // all 18 outputs (the fp64 pipe is the limit there: 171 DFMA on 32 busy lanes instead of
-    // 324 lane-slots of a warp item), B(0) rows broadcast from shared memory.
-    // On the fp64 tensor cores: warp item = 8 parent columns (sigma, P, v); for child parity p,
-    // A_p[k][n] = (-1)^(p(k+n)) b_nk (rows k padded to 24, K = n padded to 20; blocks with
-    // n < k everywhere skipped), and the children 2P+p accumulate A_p c_parent.
-    for (int j = 1; j <= kd; ++j) {
-      const int nodes = 1 << j, half = nodes >> 1;
-      const double* par = cm_lvl(j - 1);
-      double* cur = cm_lvl(j);
-      const int ncol = nodes * VT;  // parent columns, both parities
-      const int lr = lane >> 2, lc = lane & 3;
-      for (int c0 = warp * 8; c0 < ncol; c0 += nwarps * 8) {
-        const int col = c0 + lr;
-        const bool okc = col < ncol;
-        const double* xp = par + (okc ? col : 0) * kM;
-        double acc[2][3][2];
-#pragma unroll
-        for (int mt = 0; mt < 3; ++mt)
-          acc[0][mt][0] = acc[0][mt][1] = acc[1][mt][0] = acc[1][mt][1] = 0.0;
-#pragma unroll
-        for (int kk = 0; kk < (kM + 3) / 4; ++kk) {
-          const int n = 4 * kk + lc;
-          const double b = (okc && n < kM) ? xp[n] : 0.0;
-#pragma unroll
-          for (int mt = 0; mt < 3; ++mt) {
-            if (4 * kk + 3 < 8 * mt) continue;  // n < k for the whole block
-            const int k = 8 * mt + lr;
-            const double a0 = (k < kM && n < kM) ? BTsh[k * kM + n] : 0.0;  // b_nk (zero for n < k)
-            const double a1 = ((k + n) & 1) ? -a0 : a0;
-            dmma(acc[0][mt], a0, b);
-            dmma(acc[1][mt], a1, b);
-          }
-        }
-#pragma unroll
-        for (int mt = 0; mt < 3; ++mt)
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int k = 8 * mt + lr, co = c0 + 2 * lc + h;
-            if (k < kM && co < ncol) {
-              const int v = co % VT, sp = co / VT;
-              const int P = sp & (half - 1), sg = sp >> (j - 1);
-              double* d0 = cur + ((sg * nodes + 2 * P) * VT + v) * kM + k;
-              d0[0] += acc[0][mt][h];
-              d0[VT * kM] += acc[1][mt][h];
+    // step 4 down the subtree, level by level, every L2L as the lane
+    // operator above (lane = child mode, the column of B(0) in registers, both children per parent).
+    {
+      // narrow levels (j <= 3, at most 4 parents per sigma): one warp per (sigma, v) runs them one after
+      // another, lane = mode, both children of a parent in one pass -- no CTA barrier between them
+      const int jn = kd < 3 ? kd : 3;
+      for (int ch = warp; ch < 2 * VT; ch += nwarps) {
+        const int sg = ch / VT, v = ch - sg * VT;
+        for (int j = 1; j <= jn; ++j) {
+          const int nodes = 1 << j;
+          const double* par = cm_lvl(j - 1);
+          double* cur = cm_lvl(j);
+          for (int Pn = 0; Pn < (nodes >> 1); ++Pn) {
+            double r0, r1;
+            l2l_lane_pair(bcol, par + ((sg * (nodes >> 1) + Pn) * VT + v) * kM, lane, r0, r1);
+            if (lane < kM) {
+              cur[((sg * nodes + 2 * Pn) * VT + v) * kM + lane] += r0;
+              cur[((sg * nodes + 2 * Pn + 1) * VT + v) * kM + lane] += r1;
             }
           }
+          __syncwarp();
+        }
       }
       __syncthreads();
+      if (jn == 3) LC_TS(2, 6);
+      // wide levels on the fp64 tensor cores: warp item = 8 parent columns (sigma, P, v); for child
+      // parity p, A_p[k][n] = (-1)^(p(k+n)) b_nk (rows k padded to 24, K = n padded to 20; blocks with
+      // n < k everywhere skipped), and the children 2P+p accumulate A_p c_parent.  The operator
+      // fragments are the same for every level and item: held in registers.
+      const int lr = lane >> 2, lc = lane & 3;
+      double af[5][3];
+#pragma unroll
+      for (int kk = 0; kk < 5; ++kk)
+#pragma unroll
+        for (int mt = 0; mt < 3; ++mt) {
+          const int n = 4 * kk + lc, k = 8 * mt + lr;
+          af[kk][mt] = (k < kM && n < kM) ? Bsh[n * kM + k] : 0.0;  // b_nk (zero for n < k)
+        }
+      for (int j = jn + 1; j <= kd; ++j) {
+        const int nodes = 1 << j, half = nodes >> 1;
+        const double* par = cm_lvl(j - 1);
+        double* cur = cm_lvl(j);
+        const int ncol = nodes * VT;  // parent columns, both parities
+        for (int c0 = warp * 8; c0 < ncol; c0 += nwarps * 8) {
+          const int col = c0 + lr;
+          const bool okc = col < ncol;
+          const double* xp = par + (okc ? col : 0) * kM;
+          double bv[5];
+#pragma unroll
+          for (int kk = 0; kk < 5; ++kk) {
+            const int n = 4 * kk + lc;
+            bv[kk] = (okc && n < kM) ? xp[n] : 0.0;
+          }
+          double acc[2][3][2];
+#pragma unroll
+          for (int mt = 0; mt < 3; ++mt)
+            acc[0][mt][0] = acc[0][mt][1] = acc[1][mt][0] = acc[1][mt][1] = 0.0;
+#pragma unroll
+          for (int kk = 0; kk < 5; ++kk) {
+#pragma unroll
+            for (int mt = 0; mt < 3; ++mt) {
+              if (4 * kk + 3 < 8 * mt) continue;  // n < k for the whole block
+              const int k = 8 * mt + lr, n = 4 * kk + lc;
+              const double a0 = af[kk][mt];
+              const double a1 = ((k + n) & 1) ? -a0 : a0;
+              dmma(acc[0][mt], a0, bv[kk]);
+              dmma(acc[1][mt], a1, bv[kk]);
+            }
+          }
+#pragma unroll
+          for (int mt = 0; mt < 3; ++mt)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int k = 8 * mt + lr, co = c0 + 2 * lc + h;
+              if (k < kM && co < ncol) {
+                const int v = co % VT, sp = co / VT;
+                const int Pn = sp & (half - 1), sg = sp >> (j - 1);
+                double* d0 = cur + ((sg * nodes + 2 * Pn) * VT + v) * kM + k;
+                d0[0] += acc[0][mt][h];
+                d0[VT * kM] += acc[1][mt][h];
+              }
+            }
+        }
+        __syncthreads();
+      }
     }
+    LC_TS(2, 7);
     LC_TS(2, 4);
     // step 5: z^sigma += c(L-1) T(sigma)^T (eq:step5) on the fp64 tensor cores: warp item =
     // (sigma, v, 8 leaves); A = T(sigma) (SMAX/8 row tiles of m, K = 18 modes padded to 20),
@@ -1514,8 +1583,24 @@ __global__ void __launch_bounds__(NT, 512 / NT) lc_down_kernel(const DownParams 
     __syncthreads();
   }
   LC_TS(2, 5);
-  // step 7: C^{-1} (L2C); coalesced store
+  // step 7: C^{-1} (L2C); coalesced store (whole aligned tiles: scaled in place, one TMA bulk store
+  // per vector)
   const double inv_pi = 0.318309886183790671537767526745028724;
+  if (bulk) {
+    for (int v = 0; v < VT; ++v)
+      for (int ii = tid; ii < rows; ii += nthr) {
+        const int64_t i = i0 + ii;
+        if (DIR == 0) zb[v * rows + ii] *= (i == 0 ? inv_pi : 2.0 * inv_pi);
+      }
+    fence_proxy_async();  // the scaled rows are visible to the bulk copy (async proxy)
+    __syncthreads();
+    if (tid == 0) {
+      for (int v = 0; v < VT; ++v)
+        bulk_s2g(P.out + (tile * VT + v) * P.ld_out + i0, zb + v * rows, uint32_t(rows) * 8u);
+      bulk_commit_and_wait_read();  // shared memory stays valid until the copies have read it
+    }
+    return;
+  }
 #pragma unroll 1
   for (int v = 0; v < VT; ++v) {
     const int64_t gv = tile * VT + v;

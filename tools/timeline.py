@@ -43,7 +43,7 @@ torch.cuda.synchronize()
 NAMES = {"up": ["start", "staged", "step1", "subtreeM2M", "written", "cont", "contdone", "exit"],
          "upb": ["start", "lvlL-2", "lvlL-3", "merge0", "merge0done", "cont", "contdone", "end"],
          "stream": ["start", "end", "banddone", "-", "-", "-", "-", "m2ldone"],
-         "down": ["start", "gdwait", "loaded", "chain", "subtree", "end", "-", "-"]}
+         "down": ["start", "gdwait", "loaded", "chain", "subtree", "end", "lvl1-3", "lvlsdone"]}
 for rep in range(2):
     lib.lc_debug_clear()
     torch.cuda.synchronize()
