@@ -238,8 +238,8 @@ def measure(config, args, world, rank, local, headline=True):
     if split:
         from paper_2411_00033_b200.dist import SingleVectorTransform
         scaling = "strong"
-        sl = SingleVectorTransform(n, "leg2cheb", device=dev)
-        sc = SingleVectorTransform(n, "cheb2leg", device=dev)
+        sl = SingleVectorTransform(n, "leg2cheb", device=dev, part_up=True)
+        sc = SingleVectorTransform(n, "cheb2leg", device=dev, part_up=True)
     if two_d:
         # rows [v0, v0+V) of the n x n array on this rank; pass 1 along axis 1 (V row vectors), all-to-all,
         # pass 2 along axis 0 (n/world column vectors, batch-contiguous); with chunks > 1 pass 1 runs in

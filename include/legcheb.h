@@ -90,6 +90,11 @@ typedef struct {
                          segments, the band of its rows and the downward pass of its subtrees run here
                          (eq:fgamma, eq:flevels, eq:zlevels).  Rows outside the part are not
                          written.  Engine 1 only. */
+  int32_t part_up;    /* partitioned plans: 1 -> the upward pass is partitioned too: each part projects and
+                         merges only its own subtrees; run with lc_execute_part: phase 0 (upward pass), then the
+                         caller exchanges the subtree roots of all parts and the w halo (2 segments per fine
+                         level) of the next part in the workspace (lc_plan_kernel_info: kup, grup, part_lo,
+                         part_hi), then phase 1 (coarse levels, M2L, band, downward pass).  0 -> replicated. */
 } lc_plan_opts;
 
 /* Geometry and algorithmic work of a plan (per vector unless stated). */
@@ -155,6 +160,15 @@ lc_status lc_workspace_init(const lc_plan* p, void* workspace, void* stream);
  *              NULL for the plan-owned workspace.
  * Outputs are the first n entries of the transform of the zero-padded input. */
 lc_status lc_execute(const lc_plan* p, const double* in, double* out, void* workspace, void* stream);
+
+/* Two-phase execution of a plan created with opts.part_up = 1 (NEXT-2): phase 0 enqueues the upward
+ * pass of the part's subtrees, phase 1 the coarse levels of step 2, the M2L, band and downward passes.
+ * Between them the caller makes w of the workspace complete for this part: all subtree roots (level
+ * grup) and, on every level g >= grup, the 2 segments following the part (from the next part).
+ * workspace must be caller-owned (its layout: DESIGN.md section 5).  Errors: INVALID_ARG (not a
+ * part_up plan, bad phase, NULL workspace), CUDA.  lc_execute rejects part_up plans. */
+lc_status lc_execute_part(const lc_plan* p, int32_t phase, const double* in, double* out, void* workspace,
+                          void* stream);
 
 /* As lc_execute, and records ev[0] before the first kernel, ev[i] after
  * kernel i (i = 1..kernels_per_execute).  ev are cudaEvent_t handles; nev

@@ -21,7 +21,8 @@ c_dp = ctypes.POINTER(ctypes.c_double)
 class PlanOpts(ctypes.Structure):
     _fields_ = [("s_hat", c_i64), ("M", c_i32), ("layout", c_i32), ("ld_in", c_i64), ("ld_out", c_i64),
                 ("device", c_i32), ("vt", c_i32), ("subtree", c_i32), ("stage_blocks", c_i32), ("stages", c_i32),
-                ("up_subtree", c_i32), ("engine", c_i32), ("part_index", c_i32), ("part_count", c_i32)]
+                ("up_subtree", c_i32), ("engine", c_i32), ("part_index", c_i32), ("part_count", c_i32),
+                ("part_up", c_i32)]
 
 
 class PlanDesc(ctypes.Structure):
@@ -45,6 +46,7 @@ SIGNATURES = {
     "lc_workspace_bytes": (ctypes.c_size_t, [c_vp]),
     "lc_workspace_init": (c_i32, [c_vp, c_vp, c_vp]),
     "lc_execute": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "lc_execute_part": (c_i32, [c_vp, c_i32, c_vp, c_vp, c_vp, c_vp]),
     "lc_execute_timed": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_vp, ctypes.POINTER(c_vp), c_i32]),
     "lc_host_stage_bytes": (ctypes.c_size_t, [c_vp]),
     "lc_execute_host": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),

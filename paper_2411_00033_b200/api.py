@@ -51,7 +51,7 @@ class Plan:
     def __init__(self, n: int, direction="leg2cheb", batch: int = 1, device=None, s_hat: int = 32,
                  layout="vec", ld_in: int = 0, ld_out: int = 0, vt: int = 0, subtree: int = 0,
                  stage_blocks: int = 0, stages: int = 0, up_subtree: int = 0,
-                 engine: int = 0, part_index: int = 0, part_count: int = 0):
+                 engine: int = 0, part_index: int = 0, part_count: int = 0, part_up: int = 0):
         lib = _lib.load()
         if device is None:
             device = torch.cuda.current_device()
@@ -63,7 +63,7 @@ class Plan:
         opts = _lib.PlanOpts(s_hat=s_hat, M=18, layout=self.layout, ld_in=ld_in, ld_out=ld_out,
                              device=device.index if device.index is not None else -1, vt=vt, subtree=subtree,
                              stage_blocks=stage_blocks, stages=stages, up_subtree=up_subtree,
-                             engine=engine, part_index=part_index, part_count=part_count)
+                             engine=engine, part_index=part_index, part_count=part_count, part_up=part_up)
         h = ctypes.c_void_p()
         with torch.cuda.device(device):
             _lib.check("lc_plan_create", lib.lc_plan_create(ctypes.byref(h), self.n, self.direction, self.batch,
@@ -106,7 +106,7 @@ class Plan:
         _lib.check("lc_plan_kernel_info", self._lib.lc_plan_kernel_info(self._h, buf, 32, ctypes.byref(nw)))
         names = ["stream_grid", "smem_stream", "smem_up", "kup", "grup", "kb", "cb", "nst", "vt", "stream_occ",
                  "m2l_units", "band_units", "up_grid", "kd", "smem_down", "engine", "tile_grid", "smem_tile",
-                 "ranges", "range_len", "up_ksub"]
+                 "ranges", "range_len", "up_ksub", "part_lo", "part_hi", "part_up"]
         return {k: int(buf[i]) for i, k in enumerate(names[:nw.value])}
 
     @property
@@ -167,6 +167,17 @@ class Plan:
         _lib.check("lc_execute", self._lib.lc_execute(self._h, ctypes.c_void_p(x.data_ptr()),
                                                       ctypes.c_void_p(out.data_ptr()), ws,
                                                       ctypes.c_void_p(_stream_handle(stream, self.device))))
+        return out
+
+    def execute_part(self, phase: int, x: torch.Tensor, out: torch.Tensor, workspace: torch.Tensor,
+                     stream=None) -> torch.Tensor:
+        """lc_execute_part: phase 0 (upward pass of the part's subtrees) or 1 (the rest), for plans with
+        part_up = 1; the caller exchanges the w roots / halo in `workspace` in between (dist.py)."""
+        self._check(x, "input")
+        self._check(out, "output")
+        _lib.check("lc_execute_part", self._lib.lc_execute_part(
+            self._h, int(phase), ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(out.data_ptr()),
+            ctypes.c_void_p(workspace.data_ptr()), ctypes.c_void_p(_stream_handle(stream, self.device))))
         return out
 
     def execute_timed(self, x: torch.Tensor, out: torch.Tensor, events, stream=None) -> None:

@@ -164,6 +164,10 @@ struct UpParams {
   int layout, L, s, k, gr, G, fstride, vec16;
   int noflags;  // engine 3: the range kernel waits for the whole grid (griddepcontrol), no flags
   int ksub;     // M2M levels done inside the CTA's subtree (<= k); the rest by the continuation
+  int64_t R0;   // first subtree (partitioned up pass, NEXT-2), else 0
+  int nocont;   // partitioned up pass: no continuation (the coarse levels follow the root exchange)
+  int phase;    // host side: -1 whole execution; partitioned up pass: 0 the up kernel, 1 coarse levels + rest
+  int contonly; // partitioned up pass, phase 1: only the continuation, from groups of the (exchanged) roots
   int kc;       // engine 3 (lc_up3_kernel): subtrees per chunk = 2^kc
   int64_t ntiles;
   double* w;
@@ -399,7 +403,7 @@ __global__ void __launch_bounds__(kThreads, (VT == 8 && SMAX == 32) ? LC_UP8_MIN
   double* tree = reinterpret_cast<double*>(smem + up_const_bytes(SMAX) + align_up((int64_t(VT) * nleaf * fst + 2 * SMAX) * 8, 128));
   auto tree_off = [&](int j) { return ((1 << j) - 1) * 2 * VT * kM; };
 
-  const int64_t R = blockIdx.x;
+  const int64_t R = blockIdx.x + P.R0;
   const int64_t tile = blockIdx.y;
   LC_TS(0, 0);
   // plan constants into shared memory (broadcast operands of steps 1 and 2)
@@ -410,8 +414,24 @@ __global__ void __launch_bounds__(kThreads, (VT == 8 && SMAX == 32) ? LC_UP8_MIN
   // Trigger the dependent (streaming) launch only now: every streaming CTA then starts after the
   // whole previous execution completed, so it can never observe flags of that execution.
   griddep_launch();
-  if (tid == 0 && R == 0 && tile == 0) st_release(&P.flags[5], 1);  // the streaming kernel may read the input
-
+  if (tid == 0 && blockIdx.x == 0 && tile == 0 && !P.contonly)
+    st_release(&P.flags[5], 1);  // the streaming kernel may read the input
+  double* wt = P.w + tile * P.w_tile;
+  const int64_t VM = int64_t(VT) * kM;
+  const int ksub = P.ksub;        // subtree levels merged here; the CTA leaves 2^(k-ksub) roots
+  const int dsub = k - ksub;
+  int g;           // the continuation starts at level g with this CTA's 2^contrib nodes from `node` on
+  int64_t node;
+  int contrib;
+  if (P.contonly) {
+    // phase 1 of a partitioned up pass: every subtree root of the vector is in w (exchanged); each
+    // CTA takes a group of them and runs the continuation
+    g = P.gr;
+    contrib = min(P.G, g);
+    node = int64_t(blockIdx.x) << contrib;
+    cp_async_wait<0>();
+    __syncthreads();
+  } else {
   up_stage<VT>(P, fs, R, tile, nleaf, fst);
   // zero tail read by the branch-free step 1 of the last leaf (m up to SMAX-1)
   for (int x = tid; x < 2 * SMAX; x += blockDim.x) fs[VT * nleaf * fst + x] = 0.0;
@@ -425,8 +445,6 @@ __global__ void __launch_bounds__(kThreads, (VT == 8 && SMAX == 32) ? LC_UP8_MIN
   up_step1<VT, SMAX>(Ts, fs, fst, nleaf, s, tree + tree_off(k));
   __syncthreads();
   LC_TS(0, 2);
-  double* wt = P.w + tile * P.w_tile;
-  const int64_t VM = int64_t(VT) * kM;
   // each subtree level goes to the workspace as soon as it exists, so the stores drain while the
   // next M2M levels compute (the release below then waits for little more than the last level)
   auto write_level = [&](int j) {
@@ -439,8 +457,6 @@ __global__ void __launch_bounds__(kThreads, (VT == 8 && SMAX == 32) ? LC_UP8_MIN
     }
   };
   write_level(k);
-  const int ksub = P.ksub;        // subtree levels merged here; the CTA leaves 2^(k-ksub) roots
-  const int dsub = k - ksub;
   // step 2 inside the subtree (ksub levels: an early exit frees the SM for the streaming kernel; the
   // remaining levels are merged by the continuation below, beside the stream)
   for (int j = k; j >= 1 + dsub; --j) {
@@ -461,12 +477,15 @@ __global__ void __launch_bounds__(kThreads, (VT == 8 && SMAX == 32) ? LC_UP8_MIN
     }
   }
 
+  if (P.nocont) return;  // partitioned up pass: the coarse levels come after the exchange of the roots
+  g = P.gr + dsub;
+  node = R << dsub;
+  contrib = dsub;
+  }
   // upward continuation above the subtree roots: the last arriver of each
   // group of 2^G nodes merges them G levels up (threadfence-reduction pattern).  A CTA that
-  // stopped dsub levels early arrives once for its 2^dsub roots.
-  int g = P.gr + dsub;
-  int64_t node = R << dsub;
-  int contrib = dsub;  // log2 of the nodes this arrival stands for
+  // stopped dsub levels early arrives once for its 2^dsub roots (contrib: log2 of the nodes an
+  // arrival stands for).
   while (g > 0) {
     const int ge = min(P.G, g);
     const int64_t grp = node >> ge;
@@ -511,7 +530,7 @@ __global__ void __launch_bounds__(kThreads, (VT == 8 && SMAX == 32) ? LC_UP8_MIN
     contrib = 0;
     LC_TS(0, 6);
   }
-  if (P.gr + dsub > 0 && !P.noflags) {  // this CTA produced one of the 4 level-0 nodes of its vector tile
+  if ((P.contonly || P.gr + dsub > 0) && !P.noflags) {  // this CTA produced one of the 4 level-0 nodes of its tile
     __syncthreads();
     if (tid == 0) {
       const int total = 4 * int(gridDim.y);
@@ -2658,6 +2677,7 @@ lc_status configure_kernels(lc_plan* p) {
       if (L >= 2) kup = std::max(kup, 1);
     }
   }
+  if (p->part_up) kup = std::max(1, std::min(kup, part_align_log2(L)));  // the parts' subtrees are whole
   if (up_smem_bytes(vt, kup, s) > smax) return LC_ERR_INVALID_ARG;
   {
     p->down_bulk = 1;  // TMA bulk loads in the down kernel (LC_DOWN_BULK=0: per-element cp.async, A/B runs)
@@ -2665,7 +2685,7 @@ lc_status configure_kernels(lc_plan* p) {
     // free the SMs for the A_hat stream earlier (LC_UP_KSUB overrides, for A/B runs)
     // measured on cfg2 (tools/r2_job10.sh): 3 levels in the CTA, 3 by the continuation saves ~0.7 us per
     // transform over all 6 in the CTA (the up CTAs leave ~1.7 us earlier); 2 is slower again
-    int ksub = (L >= 10 && kup >= 4) ? 3 : kup;
+    int ksub = (L >= 10 && kup >= 4 && !p->part_up) ? 3 : kup;
     if (const char* e = std::getenv("LC_UP_KSUB")) ksub = std::max(0, std::min(kup, std::atoi(e)));
     if (kup - ksub > std::max(kup, 1)) ksub = kup;  // a continuation group must cover the CTA's roots
     p->up_ksub = ksub;
@@ -2840,7 +2860,22 @@ static cudaError_t launch_vt(const lc_plan* p, const UpParams& up, const StreamP
   cudaError_t e = cudaSuccess;
   int evi = 0;
   if (ev && nev > 0) cudaEventRecord(ev[evi++], st);
-  if (p->L > 0) {
+  if (p->L > 0 && up.phase == 1) {
+    // partitioned up pass, after the exchange of the roots: the continuation from groups of them
+    // (stream order after the exchange, no programmatic overlap)
+    UpArgs<SMAX> ua;
+    ua.p = up;
+    ua.p.contonly = 1;
+    cudaLaunchConfig_t c1 = cfg;
+    c1.numAttrs = 0;
+    const int cg = std::min(std::max(p->kup, 1), int(p->grup));
+    c1.gridDim = dim3(unsigned(nseg(p->grup) >> cg), unsigned(p->ntiles));
+    c1.blockDim = dim3(kThreads);
+    c1.dynamicSmemBytes = p->smem_up;
+    e = cudaLaunchKernelEx(&c1, lc_up_kernel<VT, SMAX>, ua);
+    if (e != cudaSuccess) return e;
+    if (ev && evi < nev) cudaEventRecord(ev[evi++], st);
+  } else if (p->L > 0) {
     UpArgs<SMAX> ua;
     ua.p = up;
     cfg.gridDim = grid_up;
@@ -2852,6 +2887,7 @@ static cudaError_t launch_vt(const lc_plan* p, const UpParams& up, const StreamP
     e = cudaLaunchKernelEx(&cfg, lc_up_kernel<VT, SMAX>, ua);
     if (e != cudaSuccess) return e;
     if (ev && evi < nev) cudaEventRecord(ev[evi++], st);
+    if (up.phase == 0) return cudaGetLastError();  // partitioned up pass: the roots are exchanged next
   }
   cfg.gridDim = dim3(unsigned(p->stream_grid));
   cfg.blockDim = dim3(kStreamThreads);
@@ -2895,8 +2931,10 @@ static cudaError_t launch_dispatch(const lc_plan* p, const UpParams& up, const S
 }
 
 static lc_status launch_execute_impl(const lc_plan* p, const double* in, double* out, void* ws, cudaStream_t st,
-                                     cudaEvent_t const* ev, int nev) {
+                                     cudaEvent_t const* ev, int nev, int phase) {
   if (!p || !in || !out) return LC_ERR_INVALID_ARG;
+  // a plan with a partitioned up pass runs in two phases around the exchange of its subtree roots
+  if ((phase >= 0) != (p->part_up != 0)) return LC_ERR_INVALID_ARG;
   {
     const char* a0 = reinterpret_cast<const char*>(in);
     const char* a1 = a0 + 8 * extent(p->layout, p->ld_in, p->n, p->batch);
@@ -2943,6 +2981,10 @@ static lc_status launch_execute_impl(const lc_plan* p, const double* in, double*
   up.vec16 = (reinterpret_cast<uintptr_t>(in) % 16 == 0) && (p->ld_in % 2 == 0) ? 1 : 0;
   up.noflags = p->engine == 3 ? 1 : 0;
   up.ksub = p->engine == 1 ? p->up_ksub : p->kup;
+  up.R0 = p->part_up ? (p->part_lo >> p->kup) : 0;
+  up.nocont = p->part_up;
+  up.phase = phase;
+  up.contonly = 0;
   up.kc = p->up3_kc;
   up.ntiles = p->ntiles;
   up.w = w; up.cnt = cnt; up.flags = flags; up.w_tile = p->w_tile_doubles; up.cnt_tile = p->cnt_tile_ints;
@@ -2974,7 +3016,7 @@ static lc_status launch_execute_impl(const lc_plan* p, const double* in, double*
     if (prev != p->device) cudaSetDevice(prev);
     return LC_ERR_INVALID_ARG;
   }
-  const dim3 grid_up(unsigned(nsub), unsigned(p->ntiles));
+  const dim3 grid_up(unsigned(p->part_up ? ((p->part_hi - p->part_lo) >> p->kup) : nsub), unsigned(p->ntiles));
   const dim3 grid_down(unsigned(ndown), unsigned(p->ntiles));
   if (p->engine == 3) {
     TileParams tp{};
@@ -3021,9 +3063,9 @@ static lc_status launch_execute_impl(const lc_plan* p, const double* in, double*
 }
 
 lc_status launch_execute(const lc_plan* p, const double* in, double* out, void* ws, cudaStream_t st,
-                         cudaEvent_t const* ev, int nev) {
+                         cudaEvent_t const* ev, int nev, int phase) {
   if (!p) return LC_ERR_INVALID_ARG;
-  const lc_status rc = launch_execute_impl(p, in, out, ws, st, ev, nev);
+  const lc_status rc = launch_execute_impl(p, in, out, ws, st, ev, nev, phase);
   if (rc == LC_OK) {
     int prev = 0;
     cudaGetDevice(&prev);
@@ -3042,7 +3084,7 @@ extern "C" lc_status lc_plan_kernel_info(const lc_plan* p, int64_t* out, int32_t
   const int64_t v[] = {p->stream_grid, int64_t(p->smem_stream), int64_t(p->smem_up), p->kup, p->grup, p->kb,
                        p->bps, p->nst, p->vt, p->stream_occ, p->m2l_units, p->band_units, up_grid, p->k,
                        int64_t(p->smem_down), p->engine, p->tile_grid, int64_t(p->smem_tile), p->range_n, p->range_len,
-                       p->up_ksub};
+                       p->up_ksub, p->part_lo, p->part_hi, p->part_up};
   const int32_t nv = int32_t(sizeof(v) / sizeof(v[0]));
   int32_t i = 0;
   for (; i < nv && i < count; ++i) out[i] = v[i];
@@ -3051,13 +3093,19 @@ extern "C" lc_status lc_plan_kernel_info(const lc_plan* p, int64_t* out, int32_t
 }
 
 extern "C" lc_status lc_execute(const lc_plan* p, const double* in, double* out, void* ws, void* stream) {
-  return lc::launch_execute(p, in, out, ws, (cudaStream_t)stream, nullptr, 0);
+  return lc::launch_execute(p, in, out, ws, (cudaStream_t)stream, nullptr, 0, -1);
+}
+
+extern "C" lc_status lc_execute_part(const lc_plan* p, int32_t phase, const double* in, double* out, void* ws,
+                                     void* stream) {
+  if (!p || !p->part_up || (phase != 0 && phase != 1) || !ws) return LC_ERR_INVALID_ARG;
+  return lc::launch_execute(p, in, out, ws, (cudaStream_t)stream, nullptr, 0, phase);
 }
 
 extern "C" lc_status lc_execute_timed(const lc_plan* p, const double* in, double* out, void* ws, void* stream,
                                       void* const* ev, int32_t nev) {
   if (!p || !ev || nev < lc::kernels_per_execute(p) + 1) return LC_ERR_INVALID_ARG;
-  return lc::launch_execute(p, in, out, ws, (cudaStream_t)stream, reinterpret_cast<cudaEvent_t const*>(ev), nev);
+  return lc::launch_execute(p, in, out, ws, (cudaStream_t)stream, reinterpret_cast<cudaEvent_t const*>(ev), nev, -1);
 }
 
 extern "C" lc_status lc_execute_host(const lc_plan* p, const double* h_in, double* h_out, void* d_stage,
@@ -3080,7 +3128,7 @@ extern "C" lc_status lc_execute_host(const lc_plan* p, const double* h_in, doubl
   lc_status rc = LC_OK;
   cudaError_t e = cudaMemcpyAsync(d_in, h_in, size_t(ein) * 8, cudaMemcpyHostToDevice, st);
   if (e != cudaSuccess) rc = lc::record_cuda_error(e);
-  if (rc == LC_OK) rc = lc::launch_execute(p, d_in, d_out, ws, st, nullptr, 0);
+  if (rc == LC_OK) rc = lc::launch_execute(p, d_in, d_out, ws, st, nullptr, 0, -1);
   if (rc == LC_OK) {
     e = cudaMemcpyAsync(h_out, d_out, size_t(eout) * 8, cudaMemcpyDeviceToHost, st);
     if (e != cudaSuccess) rc = lc::record_cuda_error(e);

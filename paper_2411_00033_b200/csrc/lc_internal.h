@@ -132,6 +132,7 @@ struct lc_plan {
   // partitioned single-vector plan (NEXT-2): part part_index of part_count computes the output rows
   // [row_lo, row_hi) = leaf segments [part_lo, part_hi); the up pass stays whole (replicated)
   int part_index, part_count;
+  int part_up;            // the up pass partitioned too (two-phase execution around a root/halo exchange)
   int64_t part_lo, part_hi, row_lo, row_hi;
   int blo[32], nblk[32];  // M2L row blocks per level
   int band_lo;            // first band unit
@@ -170,7 +171,7 @@ namespace lc {
 // remembers the last CUDA error (thread-local) for lc_last_error(); returns LC_ERR_CUDA or OUT_OF_MEMORY
 lc_status record_cuda_error(cudaError_t e);
 lc_status launch_execute(const lc_plan* p, const double* in, double* out, void* ws, cudaStream_t st,
-                         cudaEvent_t const* ev, int nev);
+                         cudaEvent_t const* ev, int nev, int phase);
 // records that p was used on stream st (after the enqueued work) so lc_plan_destroy can wait for it;
 // a no-op on a capturing stream (graph launches are the caller's to finish before destroy)
 void note_execute(const lc_plan* p, cudaStream_t st);

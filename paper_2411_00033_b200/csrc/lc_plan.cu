@@ -281,14 +281,16 @@ int64_t band_nnz(int64_t N, int64_t s) {
 }
 
 // leaf segments [lo, hi) of part `pidx` of `pcnt`: whole groups of 2^part_align_log2(L) leaves, balanced
-// over the groups that hold outputs (rows < n); the last part runs to the end of the padded vector
+// over the groups that hold outputs (rows < n)
 static void part_leaves(int64_t n, const Geometry& G, int pidx, int pcnt, int64_t* lo, int64_t* hi) {
   const int64_t nls = G.L > 0 ? (int64_t(2) << G.L) : 2;
   const int64_t align = int64_t(1) << part_align_log2(G.L);
   const int64_t nreal = (n + 2 * G.s - 1) / (2 * G.s);
   const int64_t nch = (nreal + align - 1) / align;
   *lo = std::min(nls, (int64_t(pidx) * nch / pcnt) * align);
-  *hi = pidx == pcnt - 1 ? nls : std::min(nls, (int64_t(pidx + 1) * nch / pcnt) * align);
+  *hi = std::min(nls, (int64_t(pidx + 1) * nch / pcnt) * align);
+  // the groups past the last output row (zero padding) belong to no part: their w is 0
+  // and their rows are not returned, so no part projects, merges or evaluates them
 }
 
 static void fill_work(lc_plan_desc* d, int64_t batch) {
@@ -418,6 +420,7 @@ extern "C" lc_status lc_plan_create(lc_plan** out, int64_t n, lc_direction dir, 
     }
     p->part_index = o.part_index;
     p->part_count = o.part_count;
+    p->part_up = (o.part_up && G.L >= 2) ? 1 : 0;
     part_leaves(n, G, o.part_index, o.part_count, &p->part_lo, &p->part_hi);
     p->row_lo = std::min(n, p->part_lo * 2 * G.s);
     p->row_hi = std::min(n, p->part_hi * 2 * G.s);

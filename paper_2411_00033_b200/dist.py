@@ -60,6 +60,77 @@ class BatchedTransform:
         return self.plan.execute(x_local, out)
 
 
+class PartExchange:
+    """Index maps of the workspace exchange between the parts of a partitioned single-vector plan whose
+    upward pass is partitioned too (lc_plan_opts.part_up, lc_execute_part).
+
+    After phase 0 every part holds w of its own subtrees.  Phase 1 needs, per part, every subtree root
+    (level grup, whole vector: the coarse levels are merged from them on each part) and, on each fine
+    level g >= grup, the two segments that follow the part (the columns u+2, u+3 of its last rows,
+    eq:globalij).  Each part publishes its roots and its first two segments of every fine level; the
+    receiving side scatters what it lacks.  `send_index` (w units to pack) is the same layout on every
+    part; `recv_src` / `recv_dst` map rows of the stacked [parts, K] gather to w units of this part.
+    w unit = VM = 18 doubles of one (level, sigma, segment), tile 0 (batch 1)."""
+
+    def __init__(self, n: int, parts: int, plan_info: list[dict], me: int):
+        self.parts, self.me = parts, me
+        L = plan_info[me]["L"]
+        kup, gr = plan_info[me]["kup"], plan_info[me]["grup"]
+        self.L, self.gr = L, gr
+        unit = lambda g, sg, t: 2 * ((4 << g) - 4) + sg * (4 << g) + t  # noqa: E731
+        nseg = lambda g: 4 << g  # noqa: E731
+        spans = [(pi["part_lo"], pi["part_hi"]) for pi in plan_info]  # leaf segments
+        roots = [(lo >> kup, hi >> kup) for lo, hi in spans]
+        self.maxroots = max(b - a for a, b in roots)
+        nfine = L - gr
+        self.K = 2 * self.maxroots + nfine * 2 * 2
+
+        def send_units(r):
+            lo, hi = spans[r]
+            a, b = roots[r]
+            idx = []
+            for sg in range(2):
+                idx += [unit(gr, sg, t) for t in range(a, b)] + [0] * (self.maxroots - (b - a))
+            for g in range(gr, L):
+                lo_g = lo >> (L - 1 - g)
+                for sg in range(2):
+                    for i in range(2):
+                        t = lo_g + i
+                        idx.append(unit(g, sg, t) if (hi > lo and t < nseg(g)) else 0)
+            return idx
+
+        self.send_index = send_units(me)
+        src, dst = [], []
+        lo_me, hi_me = spans[me]
+        for r in range(parts):  # the roots of every other part
+            if r == me:
+                continue
+            a, b = roots[r]
+            for sg in range(2):
+                for k, t in enumerate(range(a, b)):
+                    src.append(r * self.K + sg * self.maxroots + k)
+                    dst.append(unit(gr, sg, t))
+        if hi_me > lo_me:  # the halo: 2 segments after the part on every fine level, from their owners
+            for g in range(gr, L):
+                sh = L - 1 - g
+                hi_g = (hi_me - 1 >> sh) + 1
+                for t in range(hi_g, min(hi_g + 2, nseg(g))):
+                    owner = next((r for r in range(parts) if spans[r][1] > spans[r][0]
+                                  and (spans[r][0] >> sh) <= t <= ((spans[r][1] - 1) >> sh)), None)
+                    if owner is None:  # zero padding past the last part: w stays 0 (never written)
+                        continue
+                    i = t - (spans[owner][0] >> sh)
+                    assert i in (0, 1), "halo segment beyond the owner's first two"
+                    for sg in range(2):
+                        src.append(owner * self.K + 2 * self.maxroots + ((g - gr) * 2 + sg) * 2 + i)
+                        dst.append(unit(g, sg, t))
+        self.recv_src, self.recv_dst = src, dst
+
+    def tensors(self, device):
+        t = lambda a: torch.tensor(a, dtype=torch.int64, device=device)  # noqa: E731
+        return t(self.send_index), t(self.recv_src), t(self.recv_dst)
+
+
 class SingleVectorTransform:
     """One long transform split over the ranks by output rows (NEXT-2).
 
@@ -72,7 +143,7 @@ class SingleVectorTransform:
     (x_full, lo, hi) -> rows lo..hi (tests use a CPU stand-in); the product path builds a `Plan`."""
 
     def __init__(self, n: int, direction: str, group=None, device=None, transform: Optional[Callable] = None,
-                 **opts):
+                 part_up: bool = False, **opts):
         from .api import partition
         self.group = group
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
@@ -82,11 +153,24 @@ class SingleVectorTransform:
         self.row_lo, self.row_hi = self.spans[self.rank]
         self.transform = transform
         self.plan = None
+        self.part_up = bool(part_up) and self.world > 1 and transform is None
         if transform is None:
             from .api import Plan
             self.plan = Plan(n, direction, batch=1, device=device, part_index=self.rank, part_count=self.world,
-                             **opts)
+                             part_up=int(self.part_up), **opts)
             assert (self.plan.desc["row_lo"], self.plan.desc["row_hi"]) == (self.row_lo, self.row_hi)
+            self.part_up = self.part_up and bool(self.plan.kernel_info["part_up"])
+            if self.part_up:
+                # every part's geometry (identical plans but for the range) for the exchange maps
+                info = dict(self.plan.kernel_info, L=self.plan.desc["L"])
+                infos = [None] * self.world
+                dist.all_gather_object(infos, {k: info[k] for k in ("L", "kup", "grup", "part_lo", "part_hi")},
+                                       group=group)
+                self.xch = PartExchange(n, self.world, infos, self.rank)
+                self.ws = self.plan.new_workspace()
+                self.w_units = self.ws.view(torch.float64)[: self.ws.numel() // 8 // 18 * 18].view(-1, 18)
+                self.send_idx, self.recv_src, self.recv_dst = self.xch.tensors(self.ws.device)
+                self.out = torch.empty((1, n), dtype=torch.float64, device=self.ws.device)
 
     def __call__(self, x_full: torch.Tensor, gather: bool = True) -> torch.Tensor:
         """x_full: the whole [n] input on this rank.  Returns the full [n] result (gather) or this
@@ -96,6 +180,15 @@ class SingleVectorTransform:
         lo, hi = self.row_lo, self.row_hi
         if self.transform is not None:
             mine = self.transform(x_full, lo, hi)
+        elif self.part_up:
+            x2 = x_full.reshape(1, -1)
+            self.plan.execute_part(0, x2, self.out, self.ws)  # upward pass of this part's subtrees
+            send = self.w_units[self.send_idx]  # roots + first two segments of every fine level
+            recv = send.new_empty((self.world * send.shape[0], 18))
+            dist.all_gather_into_tensor(recv, send, group=self.group)
+            self.w_units[self.recv_dst] = recv[self.recv_src]  # every root, the halo of the next part
+            self.plan.execute_part(1, x2, self.out, self.ws)
+            mine = self.out.reshape(-1)[lo:hi]
         else:
             z = self.plan.execute(x_full.reshape(1, -1))  # rows outside [lo, hi) are not written
             mine = z.reshape(-1)[lo:hi]

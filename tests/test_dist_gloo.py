@@ -194,3 +194,45 @@ def test_single_vector_split_gloo(world, n):
     assert spans[0][0] == 0 and spans[-1][1] == n
     for r in range(world):
         assert np.array_equal(results[r][2], ref)
+
+
+def test_part_exchange_maps_cover_what_phase_1_reads():
+    """Host logic of the partitioned upward pass (NEXT-2): after the exchange every part holds all
+    subtree roots and, on every fine level, the two segments after its range, each taken from the part
+    that owns it (checked against a synthetic w where every unit holds its own index)."""
+    from paper_2411_00033_b200.dist import PartExchange
+    for L, kup, nparts_spans in ((13, 6, [(0, 192), (192, 448), (448, 16384)]),
+                                 (10, 6, [(0, 64), (64, 128), (128, 192), (192, 2048)]),
+                                 (8, 6, [(0, 0), (0, 64), (64, 512)]),
+                                 (10, 6, [(0, 640), (640, 1920)])):  # padding groups past the last part
+        gr = L - 1 - kup
+        parts = len(nparts_spans)
+        infos = [dict(L=L, kup=kup, grup=gr, part_lo=a, part_hi=b) for a, b in nparts_spans]
+        nunits = 2 * ((4 << L) - 4)
+        unit = lambda g, sg, t: 2 * ((4 << g) - 4) + sg * (4 << g) + t  # noqa: E731
+        xs = [PartExchange(0, parts, infos, p) for p in range(parts)]
+        # w of each part after phase 0: only its own subtrees' units are valid (value = unit index)
+        ws = []
+        for p, (a, b) in enumerate(nparts_spans):
+            w = np.full(nunits, -1.0)
+            for g in range(gr, L):
+                sh = L - 1 - g
+                for sg in range(2):
+                    for t in range(a >> sh, (b >> sh) if b > a else a >> sh):
+                        w[unit(g, sg, t)] = unit(g, sg, t)
+            ws.append(w)
+        gathered = np.concatenate([ws[p][xs[p].send_index] for p in range(parts)])
+        for p, (a, b) in enumerate(nparts_spans):
+            w = ws[p].copy()
+            w[xs[p].recv_dst] = gathered[xs[p].recv_src]
+            last = max(bb for _, bb in nparts_spans)
+            for sg in range(2):  # every root (past the last part: zero padding, owned by no part)
+                for t in range(4 << gr):
+                    assert w[unit(gr, sg, t)] == (unit(gr, sg, t) if t < (last >> kup) else -1.0)
+            if b > a:  # the halo (up to the last part's end: past it w is zero padding, never written)
+                for g in range(gr, L):
+                    sh = L - 1 - g
+                    hi_g = ((b - 1) >> sh) + 1
+                    for t in range(hi_g, min(hi_g + 2, 4 << g, ((last - 1) >> sh) + 1)):
+                        for sg in range(2):
+                            assert w[unit(g, sg, t)] == unit(g, sg, t), (L, p, g, t)

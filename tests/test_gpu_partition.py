@@ -57,3 +57,48 @@ def test_partition_geometry():
             spans = [partition(n, p, parts) for p in range(parts)]
             assert spans[0][0] == 0 and spans[-1][1] == n
             assert all(spans[i][1] == spans[i + 1][0] for i in range(parts - 1))
+
+
+@pytest.mark.parametrize("direction", ["leg2cheb", "cheb2leg"])
+@pytest.mark.parametrize("n,parts", [(70001, 2), (1_000_000, 3), (1_000_000, 8), (4_000_017, 5), (10_000_000, 8),
+                                     (300_000, 7)])
+def test_partitioned_up_pass_equals_whole_plan(n, parts, direction):
+    """part_up = 1: each part runs the upward pass of its own subtrees only (lc_execute_part phase 0);
+    the subtree roots of all parts and each part's w halo are exchanged (dist.PartExchange, here as
+    local copies between the parts' workspaces in place of the all-gather); phase 1 merges the coarse
+    levels and finishes the part's rows -- equal to the whole plan bit for bit."""
+    from paper_2411_00033_b200 import Plan, partition
+    from paper_2411_00033_b200.dist import PartExchange
+    dev = _dev()
+    f = vector("normal", n, seed=78)
+    x = torch.from_numpy(f).reshape(1, -1).to(dev)
+    whole = Plan(n, direction, device=dev).execute(x)
+    plans = [Plan(n, direction, device=dev, part_index=p, part_count=parts, part_up=1) for p in range(parts)]
+    assert all(pl.kernel_info["part_up"] == 1 for pl in plans)
+    infos = [dict(pl.kernel_info, L=pl.desc["L"]) for pl in plans]
+    wss = [pl.new_workspace() for pl in plans]
+    outs = []
+    for pl, ws in zip(plans, wss):
+        o = torch.full((1, n), 0, dtype=torch.int64, device=dev)
+        o.fill_(NAN_BITS)
+        outs.append(o.view(torch.float64))
+        pl.execute_part(0, x, outs[-1], ws)
+    units = [ws.view(torch.float64)[: ws.numel() // 8 // 18 * 18].view(-1, 18) for ws in wss]
+    xs = [PartExchange(n, parts, infos, p) for p in range(parts)]
+    gathered = torch.cat([units[p][torch.tensor(xs[p].send_index, device=dev)] for p in range(parts)])
+    for p in range(parts):
+        src = torch.tensor(xs[p].recv_src, dtype=torch.int64, device=dev)
+        dst = torch.tensor(xs[p].recv_dst, dtype=torch.int64, device=dev)
+        units[p][dst] = gathered[src]
+    for pl, ws, o in zip(plans, wss, outs):
+        pl.execute_part(1, x, o, ws)
+    torch.cuda.synchronize()
+    for p in range(parts):
+        lo, hi = partition(n, p, parts)
+        ob = outs[p].view(torch.int64)[0]
+        assert bool((ob[:lo] == NAN_BITS).all()) and bool((ob[hi:] == NAN_BITS).all())
+        assert torch.equal(outs[p][0, lo:hi], whole[0, lo:hi]), (p, lo, hi)
+    # lc_execute refuses a part_up plan (it needs the exchange between its phases)
+    from paper_2411_00033_b200._lib import LegChebError
+    with pytest.raises(LegChebError):
+        plans[0].execute(x)

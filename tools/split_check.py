@@ -20,7 +20,9 @@ x = torch.from_numpy(vector("sign_over_j1", n, seed=0)).to(dev)
 pl, pc = Plan(n, "leg2cheb", device=dev), Plan(n, "cheb2leg", device=dev)
 zref = pl.execute(x.reshape(1, -1)).reshape(-1)
 yref = pc.execute(zref.reshape(1, -1)).reshape(-1)
-sl, sc = SingleVectorTransform(n, "leg2cheb", device=dev), SingleVectorTransform(n, "cheb2leg", device=dev)
+up = len(sys.argv) > 2 and sys.argv[2] == "up"  # partitioned upward pass with the root / halo exchange
+sl = SingleVectorTransform(n, "leg2cheb", device=dev, part_up=up)
+sc = SingleVectorTransform(n, "cheb2leg", device=dev, part_up=up)
 for it in range(5):
     z = sl(x)
     ez = float((z - zref).abs().max() / zref.abs().max())
