@@ -1714,6 +1714,7 @@ struct TileParams {
   int64_t ld_in, ld_out, n, N, batch, ntiles;
   int layout, L, s;
   int nranges, rlen;   // engine 3: leaf ranges per tile and their length
+  int nle;             // engine 3: leaf segments holding outputs (the ranges stop there: past n is padding)
 };
 
 // debug build: per (CTA, warp) cycle accounting of the tile kernel in g_lc_ts[0]:
@@ -2263,7 +2264,7 @@ __global__ void __launch_bounds__(kTileThreads, STAGE ? 3 : LC_RANGE_MINB) lc_ra
   for (int64_t unit = blockIdx.x; unit < nunits; unit += gridDim.x) {
     const int64_t tile = unit / P.nranges;
     const int Ua = int(unit - tile * P.nranges) * P.rlen;
-    const int Ub = min(nls, Ua + P.rlen) - 1;
+    const int Ub = min(P.nle, Ua + P.rlen) - 1;
     // entering the range at its rightmost leaf Ub enters every level; the "step" Ub+1 only computes
     // the M2L of Ub's rows on all levels (and stages f(Ub+1), zero past the end)
     auto gentry = [&](int U) { return U == Ub ? 0 : gmin_of(U); };
@@ -2791,7 +2792,10 @@ lc_status configure_kernels(lc_plan* p) {
       }
       if (occ < 1) return LC_ERR_INVALID_ARG;
       const int64_t slots = int64_t(occ) * p->sm_count;
-      const int64_t nls = int64_t(2) << L;
+      // the ranges cover the leaf segments that hold outputs: the zero padding past n has
+      // w = 0 (written by the up pass) and no rows to return, so no range walks it
+      const int64_t nls = std::min<int64_t>(int64_t(2) << L, (p->n + 2 * s - 1) / (2 * s));
+      p->range_nle = int(nls);
       int64_t nr = std::max<int64_t>(1, slots / p->ntiles);  // units <= slots: one wave, no straggler round
       nr = std::max<int64_t>(1, std::min(nr, nls / 64));  // ranges of >= 64 leaves (the entry chain is L deep)
       const int64_t rlen = (nls + nr - 1) / nr;
@@ -3024,6 +3028,7 @@ static lc_status launch_execute_impl(const lc_plan* p, const double* in, double*
     tp.B = p->d_B; tp.ld_in = p->ld_in; tp.ld_out = p->ld_out; tp.n = p->n; tp.N = p->N; tp.batch = p->batch;
     tp.ntiles = p->ntiles; tp.layout = p->layout; tp.L = int(p->L); tp.s = int(p->s);
     tp.wg = w; tp.w_tile = p->w_tile_doubles; tp.nranges = p->range_n; tp.rlen = p->range_len;
+    tp.nle = p->range_nle;
     tp.scratch = reinterpret_cast<double*>(reinterpret_cast<char*>(ws) + p->ws_range_off);
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
