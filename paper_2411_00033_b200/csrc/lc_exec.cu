@@ -2718,14 +2718,25 @@ lc_status configure_kernels(lc_plan* p) {
   }
   // M2L blocks per level: all of them, or (a partitioned plan, NEXT-2) the row blocks of the segments
   // that contain a leaf of the part, i.e. its own rows and their ancestors' (the down kernel's chain)
+  // A whole plan likewise stops at the last group of 2^max(kd, kb) leaves holding outputs: the zero
+  // padding past n has no rows to return, so its band units, down subtrees and M2L rows
+  // are skipped (its w, all zeros, is still projected by the up kernel: columns of the last rows).
+  int64_t lo_leaf = 0, hi_leaf = nleaf_total;
+  if (p->part_count > 1) {
+    lo_leaf = p->part_lo;
+    hi_leaf = p->part_hi;
+  } else if (L >= 1) {
+    const int64_t a = int64_t(1) << std::max(kd, kb);
+    hi_leaf = std::min(nleaf_total, ((p->n + 2 * s - 1) / (2 * s) + a - 1) / a * a);
+  }
   int64_t nchunks = 0;
   for (int g = 0; g < L; ++g) {
     const int64_t bg = (int64_t(2) << g) - 1;
     int64_t blo = 0, nb = bg;
-    if (p->part_count > 1) {
+    {
       const int sh = L - 1 - g;
-      if (p->part_hi > p->part_lo) {
-        const int64_t ulo = p->part_lo >> sh, uhi = (p->part_hi - 1) >> sh;
+      if (hi_leaf > lo_leaf) {
+        const int64_t ulo = lo_leaf >> sh, uhi = (hi_leaf - 1) >> sh;
         blo = std::min(bg, ulo >> 1);
         nb = std::max<int64_t>(0, std::min(bg, (uhi >> 1) + 1) - blo);
       } else {
@@ -2744,9 +2755,9 @@ lc_status configure_kernels(lc_plan* p) {
     p->nsub_down = (p->part_hi - p->part_lo) >> kd;
   } else {
     p->band_lo = 0;
-    p->band_units = (nleaf_total >> kb) * p->ntiles;
+    p->band_units = (hi_leaf >> kb) * p->ntiles;
     p->sub_lo = 0;
-    p->nsub_down = L > 0 ? (int64_t(2) << L) >> kd : 1;
+    p->nsub_down = L > 0 ? hi_leaf >> kd : 1;
   }
   if (p->m2l_units + p->band_units > 0x7fffffff) return LC_ERR_INVALID_ARG;
   {
