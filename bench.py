@@ -189,7 +189,8 @@ def make_plans(config, n, V, dev, world, opts):
     t0 = time.perf_counter()
     if config == "cfg5":
         C = n // world
-        pl = Plan(n, "leg2cheb", batch=V, device=dev, **opts)
+        # N > 1: pass 1 writes its rows packed by destination rank from the kernel epilogue (out_block)
+        pl = Plan(n, "leg2cheb", batch=V, device=dev, out_block=C if world > 1 else 0, **opts)
         pc = Plan(n, "leg2cheb", batch=C, device=dev, layout="batch", **opts)
     else:
         pl = Plan(n, "leg2cheb", batch=V, device=dev, **opts)
@@ -246,15 +247,17 @@ def measure(config, args, world, rank, local, headline=True):
         # row chunks whose all-to-all overlaps the next chunk (dist._chunked_exchange)
         ycol = torch.empty((n, C), dtype=torch.float64, device=dev)
         from paper_2411_00033_b200 import Plan as _Plan
-        pk = _Plan(n, "leg2cheb", batch=V // chunks, device=dev, **opts) if chunks > 1 else pl
+        pk = _Plan(n, "leg2cheb", batch=V // chunks, device=dev, out_block=C, **opts) if chunks > 1 else pl
+        packed = world > 1
         tmpk = torch.empty((V // chunks, n), dtype=torch.float64, device=dev)
 
         def step():
             if chunks > 1:
                 tensor_product_2d(x, row_fn=lambda a: pk.execute(a, tmpk), col_fn=lambda a: pc.execute(a, ycol),
-                                  chunks=chunks)
+                                  chunks=chunks, row_packed=packed)
             else:
-                tensor_product_2d(x, row_fn=lambda a: pl.execute(a, tmp), col_fn=lambda a: pc.execute(a, ycol))
+                tensor_product_2d(x, row_fn=lambda a: pl.execute(a, tmp), col_fn=lambda a: pc.execute(a, ycol),
+                                  row_packed=packed)
     elif split:
         xf = x.reshape(-1)
 
@@ -317,7 +320,7 @@ def measure(config, args, world, rank, local, headline=True):
         reps = max(3, min(args.steps, 50))
         for _ in range(reps):
             tensor_product_2d(x, row_fn=lambda a: pl.execute(a, tmp), col_fn=lambda a: pc.execute(a, ycol),
-                              timing=tm)
+                              timing=tm, row_packed=packed)
             for k in acc:
                 acc[k] += tm[k] / reps
         passes = {k: allreduce_max(v, world) for k, v in acc.items()}
@@ -326,7 +329,7 @@ def measure(config, args, world, rank, local, headline=True):
             ov = 0.0
             for _ in range(reps):
                 tensor_product_2d(x, row_fn=lambda a: pk.execute(a, tmpk), col_fn=lambda a: pc.execute(a, ycol),
-                                  chunks=chunks, timing=tm)
+                                  chunks=chunks, timing=tm, row_packed=packed)
                 ov += tm["pass1_and_alltoall_overlapped_ms"] / reps
             passes["pass1_and_alltoall_overlapped_ms"] = allreduce_max(ov, world)
             passes["chunks"] = chunks
@@ -426,7 +429,8 @@ def measure(config, args, world, rank, local, headline=True):
                 with torch.cuda.stream(sb):
                     xd = xh.to(dev, non_blocking=True)
                     zc = tensor_product_2d(xd, row_fn=lambda a: pl.execute(a, tmps[b], workspace=ws_l[b], stream=sb),
-                                           col_fn=lambda a: pc.execute(a, ycols[b], workspace=ws_c[b], stream=sb))
+                                           col_fn=lambda a: pc.execute(a, ycols[b], workspace=ws_c[b], stream=sb),
+                                           row_packed=True)
                     hy[b].copy_(zc, non_blocking=True)
             else:
                 pl.execute_host(xh, hz[b], stream=sb, stage=st_l[b], workspace=ws_l[b])

@@ -95,6 +95,11 @@ typedef struct {
                          caller exchanges the subtree roots of all parts and the w halo (2 segments per fine
                          level) of the next part in the workspace (lc_plan_kernel_info: kup, grup, part_lo,
                          part_hi), then phase 1 (coarse levels, M2L, band, downward pass).  0 -> replicated. */
+  int64_t out_block;  /* > 0: column-blocked output, out[(i / B) * batch * B + v * B + i % B] with B = out_block:
+                         the blocks of B output coefficients of all vectors are contiguous, i.e. the first pass of
+                         a 2-D transform over G ranks writes its rows already packed by destination rank
+                         ([G][rows][n/G], the send buffer of the all-to-all) when B = n / G.  VEC input layout,
+                         engines 2/3 (chosen automatically; INVALID_ARG where neither applies), ld_out ignored. */
 } lc_plan_opts;
 
 /* Geometry and algorithmic work of a plan (per vector unless stated). */

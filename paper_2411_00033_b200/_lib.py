@@ -22,7 +22,7 @@ class PlanOpts(ctypes.Structure):
     _fields_ = [("s_hat", c_i64), ("M", c_i32), ("layout", c_i32), ("ld_in", c_i64), ("ld_out", c_i64),
                 ("device", c_i32), ("vt", c_i32), ("subtree", c_i32), ("stage_blocks", c_i32), ("stages", c_i32),
                 ("up_subtree", c_i32), ("engine", c_i32), ("part_index", c_i32), ("part_count", c_i32),
-                ("part_up", c_i32)]
+                ("part_up", c_i32), ("out_block", c_i64)]
 
 
 class PlanDesc(ctypes.Structure):

@@ -51,7 +51,8 @@ class Plan:
     def __init__(self, n: int, direction="leg2cheb", batch: int = 1, device=None, s_hat: int = 32,
                  layout="vec", ld_in: int = 0, ld_out: int = 0, vt: int = 0, subtree: int = 0,
                  stage_blocks: int = 0, stages: int = 0, up_subtree: int = 0,
-                 engine: int = 0, part_index: int = 0, part_count: int = 0, part_up: int = 0):
+                 engine: int = 0, part_index: int = 0, part_count: int = 0, part_up: int = 0,
+                 out_block: int = 0):
         lib = _lib.load()
         if device is None:
             device = torch.cuda.current_device()
@@ -63,7 +64,8 @@ class Plan:
         opts = _lib.PlanOpts(s_hat=s_hat, M=18, layout=self.layout, ld_in=ld_in, ld_out=ld_out,
                              device=device.index if device.index is not None else -1, vt=vt, subtree=subtree,
                              stage_blocks=stage_blocks, stages=stages, up_subtree=up_subtree,
-                             engine=engine, part_index=part_index, part_count=part_count, part_up=part_up)
+                             engine=engine, part_index=part_index, part_count=part_count, part_up=part_up,
+                             out_block=out_block)
         h = ctypes.c_void_p()
         with torch.cuda.device(device):
             _lib.check("lc_plan_create", lib.lc_plan_create(ctypes.byref(h), self.n, self.direction, self.batch,
@@ -75,6 +77,7 @@ class Plan:
         self.desc = d.as_dict()
         self.ld_in = ld_in or (self.n if self.layout == 0 else self.batch)
         self.ld_out = ld_out or (self.n if self.layout == 0 else self.batch)
+        self.out_block = int(out_block)
         self._ws_lock = threading.Lock()
         self._ws_by_stream: dict = {}
 
@@ -113,7 +116,10 @@ class Plan:
     def kernels_per_execute(self) -> int:
         return int(self.desc["kernels_per_execute"])
 
-    def _shape(self, ld=None):
+    def _shape(self, ld=None, output=False):
+        if output and self.out_block:  # column-blocked: [n / B][batch][B]
+            B = self.out_block
+            return ((self.n + B - 1) // B, self.batch, B)
         ld = self.ld_in if ld is None else ld
         return (self.batch, ld) if self.layout == 0 else (self.n, ld)
 
@@ -122,8 +128,11 @@ class Plan:
             raise ValueError(f"{what}: need a contiguous float64 tensor on {self.device}")
         ld = self.ld_in if what == "input" else self.ld_out
         rows, cols = (self.batch, self.n) if self.layout == 0 else (self.n, self.batch)
-        if x.numel() < (rows - 1) * ld + cols:  # the extent the kernels address (rows of stride ld)
-            raise ValueError(f"{what}: {x.numel()} elements, the plan addresses {(rows - 1) * ld + cols}")
+        need = (rows - 1) * ld + cols  # the extent the kernels address (rows of stride ld)
+        if what == "output" and self.out_block:
+            need = -(-self.n // self.out_block) * self.batch * self.out_block
+        if x.numel() < need:
+            raise ValueError(f"{what}: {x.numel()} elements, the plan addresses {need}")
 
     @property
     def plan_device_ms(self) -> float:
@@ -161,7 +170,7 @@ class Plan:
         """out = transform(x) on the device; x is [batch, n] (vec layout) or [n, batch] (batch layout)."""
         self._check(x, "input")
         if out is None:
-            out = torch.empty(self._shape(self.ld_out), dtype=torch.float64, device=self.device)
+            out = torch.empty(self._shape(self.ld_out, output=True), dtype=torch.float64, device=self.device)
         self._check(out, "output")
         ws = ctypes.c_void_p(workspace.data_ptr()) if workspace is not None else ctypes.c_void_p()
         _lib.check("lc_execute", self._lib.lc_execute(self._h, ctypes.c_void_p(x.data_ptr()),

@@ -1715,6 +1715,7 @@ struct TileParams {
   int layout, L, s;
   int nranges, rlen;   // engine 3: leaf ranges per tile and their length
   int nle;             // engine 3: leaf segments holding outputs (the ranges stop there: past n is padding)
+  int64_t oblk;        // > 0: column-blocked output (out[(i / oblk) batch oblk + v oblk + i % oblk])
 };
 
 // debug build: per (CTA, warp) cycle accounting of the tile kernel in g_lc_ts[0]:
@@ -1981,7 +1982,8 @@ __global__ void __launch_bounds__(kTileThreads, LC_TILE_MINB) lc_tile_kernel(con
                 double z = zb[v * zst_ + 2 * m + sg] + acc[q][h];
                 if (DIR == 0) z *= (i == 0 ? inv_pi : 2.0 * inv_pi);
                 if (gv < P.batch && i < P.n) {
-                  if (P.layout == LC_VEC_CONTIGUOUS) P.out[gv * P.ld_out + i] = z;
+                  if (P.oblk) P.out[(i / P.oblk) * P.batch * P.oblk + gv * P.oblk + i % P.oblk] = z;
+                  else if (P.layout == LC_VEC_CONTIGUOUS) P.out[gv * P.ld_out + i] = z;
                   else P.out[i * P.ld_out + gv] = z;
                 }
               }
@@ -2394,7 +2396,8 @@ __global__ void __launch_bounds__(kTileThreads, STAGE ? 3 : LC_RANGE_MINB) lc_ra
                 double z = zb[v * zst_ + 2 * m + sg] + acc[q][h];
                 if (DIR == 0) z *= (i == 0 ? inv_pi : 2.0 * inv_pi);
                 if (gv < P.batch && i < P.n) {
-                  if (P.layout == LC_VEC_CONTIGUOUS) P.out[gv * P.ld_out + i] = z;
+                  if (P.oblk) P.out[(i / P.oblk) * P.batch * P.oblk + gv * P.oblk + i % P.oblk] = z;
+                  else if (P.layout == LC_VEC_CONTIGUOUS) P.out[gv * P.ld_out + i] = z;
                   else P.out[i * P.ld_out + gv] = z;
                 }
               }
@@ -2847,6 +2850,11 @@ lc_status configure_kernels(lc_plan* p) {
     if (p->engine == 0)
       p->engine = (tile_ok && (ntiles8 >= int64_t(p->sm_count) || (p->n <= 2048 && 3 * ntiles8 >= int64_t(p->sm_count))))
                       ? 2 : 1;
+    // the column-blocked output (2-D exchange packed by destination) is written by engines 2 and 3
+    if (p->out_block > 0 && p->engine == 1) {
+      if (!tile_ok) return LC_ERR_INVALID_ARG;
+      p->engine = 2;
+    }
     if (p->engine == 2) {
       int occ = 0;
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, p->dir == 0 ? lc_tile_kernel<0> : lc_tile_kernel<1>,
@@ -2954,7 +2962,8 @@ static lc_status launch_execute_impl(const lc_plan* p, const double* in, double*
     const char* a0 = reinterpret_cast<const char*>(in);
     const char* a1 = a0 + 8 * extent(p->layout, p->ld_in, p->n, p->batch);
     const char* b0 = reinterpret_cast<const char*>(out);
-    const char* b1 = b0 + 8 * extent(p->layout, p->ld_out, p->n, p->batch);
+    const char* b1 = b0 + 8 * (p->out_block ? (p->n + p->out_block - 1) / p->out_block * p->batch * p->out_block
+                                             : extent(p->layout, p->ld_out, p->n, p->batch));
     if (a0 < b1 && b0 < a1) return LC_ERR_ALIASING;
   }
   if (!ws) ws = p->d_ws;
@@ -2967,6 +2976,7 @@ static lc_status launch_execute_impl(const lc_plan* p, const double* in, double*
     tp.B = p->d_B; tp.ld_in = p->ld_in; tp.ld_out = p->ld_out; tp.n = p->n; tp.N = p->N; tp.batch = p->batch;
     tp.ntiles = p->ntiles; tp.layout = p->layout; tp.L = int(p->L); tp.s = int(p->s);
     tp.scratch = reinterpret_cast<double*>(ws);
+    tp.oblk = p->out_block;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
@@ -3040,6 +3050,7 @@ static lc_status launch_execute_impl(const lc_plan* p, const double* in, double*
     tp.ntiles = p->ntiles; tp.layout = p->layout; tp.L = int(p->L); tp.s = int(p->s);
     tp.wg = w; tp.w_tile = p->w_tile_doubles; tp.nranges = p->range_n; tp.rlen = p->range_len;
     tp.nle = p->range_nle;
+    tp.oblk = p->out_block;
     tp.scratch = reinterpret_cast<double*>(reinterpret_cast<char*>(ws) + p->ws_range_off);
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;

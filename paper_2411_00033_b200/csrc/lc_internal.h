@@ -141,6 +141,7 @@ struct lc_plan {
   size_t smem_tile;
   int range_n, range_len;   // engine 3: leaf ranges per tile and their length
   int range_nle;            // engine 3: leaf segments holding outputs (ranges stop there)
+  int64_t out_block;        // > 0: column-blocked output of width out_block (engines 2 and 3)
   int range_stage;          // engine 3: range kernel with per-warp staged M2L operands (3 CTAs per SM)
   int64_t ws_range_off;     // engine 3: byte offset of the per-CTA scratch in the workspace
   int up3_kc;               // engine 3: subtrees per chunk of the persistent up pass = 2^up3_kc

@@ -390,6 +390,8 @@ extern "C" lc_status lc_plan_create(lc_plan** out, int64_t n, lc_direction dir, 
   if (o.M != kM || o.s_hat < 2 || o.s_hat > 64) return LC_ERR_INVALID_ARG;
   if (o.engine < 0 || o.engine > 3) return LC_ERR_INVALID_ARG;
   if (o.layout != LC_VEC_CONTIGUOUS && o.layout != LC_BATCH_CONTIGUOUS) return LC_ERR_INVALID_ARG;
+  if (o.out_block < 0 || (o.out_block > 0 && (o.layout != LC_VEC_CONTIGUOUS || o.part_count > 1)))
+    return LC_ERR_INVALID_ARG;
   const int64_t def_ld = o.layout == LC_VEC_CONTIGUOUS ? n : batch;
   if (o.ld_in == 0) o.ld_in = def_ld;
   if (o.ld_out == 0) o.ld_out = def_ld;
@@ -412,6 +414,7 @@ extern "C" lc_status lc_plan_create(lc_plan** out, int64_t n, lc_direction dir, 
   p->device = dev; p->sm_count = prop.multiProcessorCount;
   p->vt = o.vt; p->k = o.subtree; p->bps = o.stage_blocks; p->nst = o.stages; p->kup = o.up_subtree;
   p->engine = o.engine;
+  p->out_block = o.out_block;
   if (o.part_count > 1) {
     if (o.part_index < 0 || o.part_index >= o.part_count || G.L < 1 || (o.engine != 0 && o.engine != 1)) {
       delete p;

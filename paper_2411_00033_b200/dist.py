@@ -235,7 +235,7 @@ def transpose_cols_to_rows(z_cols: torch.Tensor, group=None) -> torch.Tensor:
 
 
 def _chunked_exchange(x_rows: torch.Tensor, row_fn: Callable, chunks: int, group=None,
-                      timing: Optional[dict] = None) -> torch.Tensor:
+                      timing: Optional[dict] = None, row_packed: bool = False) -> torch.Tensor:
     """Pass 1 in `chunks` row chunks with the all-to-all of chunk k overlapping pass 1 of chunk k+1.
 
     Chunk k's output [Rk, n1] is packed by destination ([world, Rk, C]) and exchanged with
@@ -255,7 +255,7 @@ def _chunked_exchange(x_rows: torch.Tensor, row_fn: Callable, chunks: int, group
         ev[0].record(main)
     for k in range(chunks):
         yk = row_fn(x_rows[k * Rk:(k + 1) * Rk])
-        send = pack_for_transpose(yk, world)
+        send = yk.reshape(world, Rk, C) if row_packed else pack_for_transpose(yk, world)
         sends.append(send)  # kept alive until the exchange completes
         if cuda:
             done = torch.cuda.Event()
@@ -276,13 +276,16 @@ def _chunked_exchange(x_rows: torch.Tensor, row_fn: Callable, chunks: int, group
 
 def tensor_product_2d(x_rows: torch.Tensor, group=None, row_fn: Optional[Callable] = None,
                       col_fn: Optional[Callable] = None, direction: str = "leg2cheb",
-                      restore_rows: bool = False, timing: Optional[dict] = None, chunks: int = 1) -> torch.Tensor:
+                      restore_rows: bool = False, timing: Optional[dict] = None, chunks: int = 1,
+                      row_packed: bool = False) -> torch.Tensor:
     """2-D transform of an n0 x n1 array partitioned by rows (this rank: [n0/world, n1]).
 
     Pass 1 along axis 1 on the row slab, all-to-all, pass 2 along axis 0 on the column slab
     ([n0, n1/world], batch-contiguous).  Returns the column slab, or the row slab if restore_rows.
     chunks > 1 (world > 1): pass 1 in row chunks, each chunk's all-to-all overlapping the next
-    chunk's transform (SURVEY 8(e) "chunk pass 1 by destination ... on a comm stream")."""
+    chunk's transform (SURVEY 8(e) "chunk pass 1 by destination ... on a comm stream").
+    row_packed: row_fn already returns its rows packed by destination ([world, rows, n1/world], a plan
+    with out_block = n1/world writes them so from its kernel epilogue); the default plan does that."""
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     R, n1 = x_rows.shape
     n0 = R * world
@@ -292,13 +295,16 @@ def tensor_product_2d(x_rows: torch.Tensor, group=None, row_fn: Optional[Callabl
     if row_fn is None or col_fn is None:
         from .api import Plan
         if row_fn is None:
-            prow = Plan(n1, direction, batch=R // chunks if world > 1 else R, device=x_rows.device)
+            # world > 1: the pass-1 epilogue writes the rows packed by destination (lc_plan_opts.out_block)
+            prow = Plan(n1, direction, batch=R // chunks if world > 1 else R, device=x_rows.device,
+                        out_block=C if world > 1 else 0)
             row_fn = prow.execute
+            row_packed = world > 1
         if col_fn is None:
             pcol = Plan(n0, direction, batch=C, device=x_rows.device, layout="batch")
             col_fn = pcol.execute
     if world > 1 and chunks > 1:
-        yc = _chunked_exchange(x_rows, row_fn, chunks, group, timing)
+        yc = _chunked_exchange(x_rows, row_fn, chunks, group, timing, row_packed)
         z = col_fn(yc)
         return transpose_cols_to_rows(z, group) if restore_rows else z
     ev = None
@@ -309,7 +315,12 @@ def tensor_product_2d(x_rows: torch.Tensor, group=None, row_fn: Optional[Callabl
     if ev:
         ev[1].record()
     # one rank: the row-major [n0, n1] result already is the batch-contiguous column layout
-    yc = transpose_rows_to_cols(y, group) if world > 1 else y
+    if world > 1 and row_packed:
+        recv = torch.empty_like(y)
+        dist.all_to_all_single(recv.view(-1), y.reshape(-1), group=group)
+        yc = recv.reshape(world * R, C)
+    else:
+        yc = transpose_rows_to_cols(y, group) if world > 1 else y
     if ev:
         ev[2].record()
     z = col_fn(yc)

@@ -72,6 +72,16 @@ def _worker(rank, world, port, n0, n1, results):
         # pass 1 in chunks, each chunk's all-to-all overlapping the next chunk (same result, bit for bit)
         zc = tensor_product_2d(mine, None, row_fn=_oracle_rows, col_fn=_oracle_cols_batch_layout,
                                chunks=R if R % 2 else 2) if R > 1 else z
+        # pass 1 writing its rows packed by destination (what a plan with out_block = n1/world does)
+        C = n1 // world
+
+        def rows_packed(a):
+            return _oracle_rows(a).reshape(a.shape[0], world, C).permute(1, 0, 2).contiguous()
+
+        zp = tensor_product_2d(mine, None, row_fn=rows_packed, col_fn=_oracle_cols_batch_layout, row_packed=True)
+        zpc = tensor_product_2d(mine, None, row_fn=rows_packed, col_fn=_oracle_cols_batch_layout, row_packed=True,
+                                chunks=R if R % 2 else 2) if R > 1 else zp
+        assert torch.equal(zp, z) and torch.equal(zpc, z)
         results[rank] = (ok_roundtrip, ok_cols, z.numpy().copy(), zr.numpy().copy(), zc.numpy().copy())
     finally:
         dist.destroy_process_group()

@@ -147,3 +147,24 @@ def test_convenience_functions_on_two_streams():
         ref = oracle.l2c_rows(xs[t].cpu().numpy(), rows)
         for z in outs[t]:
             assert oracle.einf(z.cpu().numpy()[rows], ref) <= GATE, t
+
+
+@pytest.mark.parametrize("direction", ["leg2cheb", "cheb2leg"])
+@pytest.mark.parametrize("n,V,B,engine", [(8192, 24, 2048, 0), (8192, 16, 1024, 2), (5000, 9, 1250, 0),
+                                          (5000, 9, 1024, 0), (300000, 8, 37500, 3)])
+def test_column_blocked_output(direction, n, V, B, engine):
+    """lc_plan_opts.out_block (the 2-D pass-1 epilogue writing rows packed by destination rank): the
+    output [ceil(n/B)][V][B] holds exactly the vector-contiguous result, re-blocked, bit for bit."""
+    dev = _dev()
+    x = batch("normal", n, V, seed=n + B).to(dev)
+    pb = _plan(n, direction, batch=V, device=dev, engine=engine, out_block=B)
+    assert pb.kernel_info["engine"] in (2, 3)  # engine 1 (automatic for few tiles) hands over to engine 2
+    ref = _plan(n, direction, batch=V, device=dev, engine=pb.kernel_info["engine"]).execute(x)
+    nb = -(-n // B)
+    out = torch.full((nb, V, B), float("nan"), dtype=torch.float64, device=dev)
+    pb.execute(x, out)
+    torch.cuda.synchronize()
+    for k in range(nb):
+        w = min(B, n - k * B)
+        assert torch.equal(out[k, :, :w], ref[:, k * B:k * B + w]), k
+        assert bool(torch.isnan(out[k, :, w:]).all())  # past n: untouched
