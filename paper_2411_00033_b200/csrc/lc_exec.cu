@@ -47,6 +47,9 @@ __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {  // no arrival
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
@@ -1263,6 +1266,14 @@ __global__ void __launch_bounds__(kStreamThreads, 2) lc_stream_kernel(const __gr
       const int lr = (ntiles > 1 ? u / ntiles : u) + P.band_lo;
       band_unit<VT, DIR>(P, tile, lr, ta, tb, gt, zst, tp, btid);
     }
+    // this CTA's band rows are stored: an acquire-release arrival (the band warps' stores are ordered
+    // before it by the band barrier); the last CTA releases flags[14] so the down kernel can fetch the
+    // band rows while the M2L tail and the release of flags[12] are still in flight
+    band_sync();
+    if (btid == 0 && atom_add_acq_rel(&P.flags[15], 1) == int(gridDim.x) - 1) {
+      atomicExch(&P.flags[15], 0);
+      st_release(&P.flags[14], 1);
+    }
     LC_TS_T(1, 2);
   }
   __syncthreads();
@@ -1374,31 +1385,40 @@ __global__ void __launch_bounds__(NT, 512 / NT) lc_down_kernel(const DownParams 
   for (int i = tid; i < kMM / 2; i += nthr) cp_async16(Bsh + 2 * i, P.B + 2 * i);
   for (int i = tid; i < SMAX * kM; i += nthr) cp_async16(Tsh + 2 * i, P.Tpad + 2 * i);
   griddep_launch();
-  // c_m2l and the band result are complete once the streaming kernel's last CTA released
-  // flags[12] (cheaper than waiting for the grid to retire); the last down CTA to pass re-arms it
-  if (tid == 0) {
-    wait_flag(&P.flags[12]);
-    if (atomicAdd(&P.flags[13], 1) == int(gridDim.x * gridDim.y) - 1) {
-      P.flags[13] = 0;
-      P.flags[12] = 0;
-    }
-  }
-  __syncthreads();
-  LC_TS(2, 1);
   const double* ct = P.c + tile * P.w_tile;
   const int olim = int((P.n - i0) < rows ? (P.n - i0) : rows);  // rows of this tile inside n
   // one TMA bulk-copy round trip when every piece is 16-byte aligned and whole (the c_m2l rows and,
   // in the vector layout, each vector's band rows of a full tile); otherwise per-element cp.async
   // with zero fill beyond n
   const bool bulk = P.bulk && P.layout == LC_VEC_CONTIGUOUS && olim == rows && (tile + 1) * VT <= P.batch;
+  __shared__ __align__(8) uint64_t dbar;
+  if (bulk && tid == 0) {
+    // the band rows are complete once every streaming CTA's band warps arrived (flags[14]): fetch them
+    // now, while the last M2L units and the release of flags[12] are still in flight
+    mbar_init(&dbar, 1);
+    fence_mbar_init();
+    wait_flag(&P.flags[14]);
+    mbar_expect_tx(&dbar, uint32_t(VT) * uint32_t(rows) * 8u);
+    const uint64_t pol = policy_evict_first();
+    for (int v = 0; v < VT; ++v)
+      bulk_g2s(zb + v * rows, P.out + (tile * VT + v) * P.ld_out + i0, uint32_t(rows) * 8u, &dbar, pol);
+  }
+  // c_m2l (and every band row) is complete once the streaming kernel's last CTA released flags[12]
+  // (cheaper than waiting for the grid to retire); the last down CTA to pass re-arms [12] and [14]
+  if (tid == 0) {
+    wait_flag(&P.flags[12]);
+    if (atomicAdd(&P.flags[13], 1) == int(gridDim.x * gridDim.y) - 1) {
+      P.flags[13] = 0;
+      P.flags[14] = 0;
+      P.flags[12] = 0;
+    }
+  }
+  __syncthreads();
+  LC_TS(2, 1);
   if (bulk) {
-    __shared__ __align__(8) uint64_t dbar;
     if (tid == 0) {
-      mbar_init(&dbar, 1);
-      fence_mbar_init();
-      uint32_t total = uint32_t(VT) * uint32_t(rows) * 8u;
-      if (L > 0) total += uint32_t(gd + (2 << kd) - 1) * 2u * uint32_t(VM) * 8u;
-      mbar_arrive_expect_tx(&dbar, total);
+      const uint32_t total = L > 0 ? uint32_t(gd + (2 << kd) - 1) * 2u * uint32_t(VM) * 8u : 0u;
+      mbar_arrive_expect_tx(&dbar, total);  // the arrival: the phase completes with every copy
       const uint64_t pol = policy_evict_first();
       if (L > 0) {
         for (int g = 0; g < gd; ++g)
@@ -1410,8 +1430,6 @@ __global__ void __launch_bounds__(NT, 512 / NT) lc_down_kernel(const DownParams 
             bulk_g2s(cm_lvl(j) + sg * (1 << j) * VM, ct + (w_level_offset_units(gd + j) + sg * nseg(gd + j) + (R << j)) * VM,
                      uint32_t((1 << j) * VM) * 8u, &dbar, pol);
       }
-      for (int v = 0; v < VT; ++v)
-        bulk_g2s(zb + v * rows, P.out + (tile * VT + v) * P.ld_out + i0, uint32_t(rows) * 8u, &dbar, pol);
     }
     __syncthreads();
     mbar_wait(&dbar, 0);
