@@ -219,7 +219,8 @@ lc_status lc_plan_kernel_info(const lc_plan* p, int64_t* out, int32_t count, int
  * are stream-ordered after the last lc_execute / lc_execute_host of the plan
  * on every stream it was used on (the plan records one event per stream), and
  * the call returns when that work is done; unrelated streams are not waited
- * for.  Executions captured into CUDA graphs are not tracked: the caller must
+ * for (beyond 64 distinct streams it falls back to a device synchronisation).
+ * Executions captured into CUDA graphs are not tracked: the caller must
  * finish such graph launches first.  Caller-owned workspaces are the caller's.
  * Errors: INVALID_ARG on NULL p. */
 lc_status lc_plan_destroy(lc_plan* p);

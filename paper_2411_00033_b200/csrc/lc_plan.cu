@@ -32,7 +32,9 @@
 struct lc_plan_sync {
   std::mutex mu;
   std::vector<std::pair<cudaStream_t, cudaEvent_t>> seen;
+  bool overflow = false;  // more than kMaxStreams streams: destroy falls back to a device synchronisation
 };
+static constexpr size_t kMaxStreams = 64;
 
 namespace lc {
 
@@ -569,9 +571,14 @@ void note_execute(const lc_plan* p, cudaStream_t st) {
       cudaEventRecord(e.second, st);
       return;
     }
+  if (p->sync->seen.size() >= kMaxStreams) {
+    p->sync->overflow = true;
+    return;
+  }
   cudaEvent_t ev = nullptr;
   if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) {
     cudaGetLastError();
+    p->sync->overflow = true;
     return;
   }
   cudaEventRecord(ev, st);
@@ -607,6 +614,7 @@ extern "C" lc_status lc_plan_destroy(lc_plan* p) {
     std::lock_guard<std::mutex> lk(p->sync->mu);
     for (auto& e : p->sync->seen)
       if (os) cudaStreamWaitEvent(os, e.second, 0);
+    if (p->sync->overflow) cudaDeviceSynchronize();  // untracked streams: wait for everything
   }
   void* bufs[] = {p->d_A, p->d_tabB, p->d_tabA, p->d_T, p->d_Tt, p->d_B, p->d_ws, p->d_stage, p->d_Tpad};
   for (void* b : bufs)
