@@ -2209,7 +2209,6 @@ __global__ void __launch_bounds__(kTileThreads, STAGE ? 3 : LC_RANGE_MINB) lc_ra
   const int lr = lane >> 2, lc = lane & 3;
   const int s = P.s, L = P.L, seglen = 2 * s;
   const int fst = tile_fst(s), zst_ = 2 * s + 4;
-  const int nls = 2 << L;  // leaf segments
   double* Tq = reinterpret_cast<double*>(smem);  // [2][32][M]
   double* Bq = Tq + 2 * 32 * kM;                  // B(0) [M][M]
   double* taq = Bq + kMM + 4;                     // tabA [80]
