@@ -397,11 +397,13 @@ def measure(config, args, world, rank, local, headline=True):
     # each transform of the step, pipelined over three streams with caller-owned staging and workspaces
     # (the call is thread- and stream-safe with distinct buffers, legcheb.h)
     e2e_steps = max(3, min(args.steps, args.e2e_steps))
-    # three buffer sets (staging + workspace per plan and stream) when they fit, else fewer; with one set
-    # the plan-owned staging and workspace serve (calls serialised on one stream)
+    # --e2e-streams buffer sets (staging + workspace per plan and stream) when they fit, else fewer; with
+    # one set the plan-owned staging and workspace serve (calls serialised on one stream)
     per_set = pl.host_stage_bytes + pc.host_stage_bytes + pl.workspace_bytes + pc.workspace_bytes
     free_b = torch.cuda.mem_get_info(dev)[0]
-    nbuf = 3 if 3 * per_set < 0.6 * free_b else (2 if 2 * per_set < 0.6 * free_b else 1)
+    nbuf = max(1, args.e2e_streams)
+    while nbuf > 1 and nbuf * per_set >= 0.6 * free_b:
+        nbuf -= 1
     streams = [torch.cuda.Stream(dev) for _ in range(nbuf)]
     if two_d:
         hz = [torch.empty_like(xh).pin_memory() for _ in range(nbuf)]
@@ -677,6 +679,8 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-seconds", type=float, default=60.0)
     ap.add_argument("--e2e-steps", type=int, default=200)
+    ap.add_argument("--e2e-streams", type=int, default=3,
+                    help="streams (with their own staging and workspaces) the host-buffer e2e pipeline uses")
     ap.add_argument("--split-vector", action="store_true",
                     help="cfg2/cfg2b at N > 1: one vector split over the ranks by output rows (NEXT-2) "
                          "instead of one replica per rank")

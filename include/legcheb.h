@@ -94,7 +94,8 @@ typedef struct {
                          merges only its own subtrees; run with lc_execute_part: phase 0 (upward pass), then the
                          caller exchanges the subtree roots of all parts and the w halo (2 segments per fine
                          level) of the next part in the workspace (lc_plan_kernel_info: kup, grup, part_lo,
-                         part_hi), then phase 1 (coarse levels, M2L, band, downward pass).  0 -> replicated. */
+                         part_hi), then phase 1 (coarse levels, M2L, band, downward pass).  0 -> replicated.
+                         part_up needs batch = 1 (INVALID_ARG otherwise). */
   int64_t out_block;  /* > 0: column-blocked output, out[(i / B) * batch * B + v * B + i % B] with B = out_block:
                          the blocks of B output coefficients of all vectors are contiguous, i.e. the first pass of
                          a 2-D transform over G ranks writes its rows already packed by destination rank

@@ -425,6 +425,11 @@ extern "C" lc_status lc_plan_create(lc_plan** out, int64_t n, lc_direction dir, 
     }
     p->part_index = o.part_index;
     p->part_count = o.part_count;
+    if (o.part_up && batch != 1) {  // the exchange layout (PartExchange) is that of one vector
+      delete p;
+      cudaSetDevice(prev_dev);
+      return LC_ERR_INVALID_ARG;
+    }
     p->part_up = (o.part_up && G.L >= 2) ? 1 : 0;
     part_leaves(n, G, o.part_index, o.part_count, &p->part_lo, &p->part_hi);
     p->row_lo = std::min(n, p->part_lo * 2 * G.s);

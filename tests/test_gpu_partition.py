@@ -102,3 +102,21 @@ def test_partitioned_up_pass_equals_whole_plan(n, parts, direction):
     from paper_2411_00033_b200._lib import LegChebError
     with pytest.raises(LegChebError):
         plans[0].execute(x)
+
+
+@pytest.mark.parametrize("direction", ["leg2cheb", "cheb2leg"])
+def test_parts_of_a_batch(direction):
+    """Partitioned plans of several vectors (vector tiles of 2 and 4): each part's rows of every vector
+    equal the whole plan's bit for bit; a partitioned upward pass needs one vector."""
+    from paper_2411_00033_b200 import Plan, partition
+    from paper_2411_00033_b200._lib import LegChebError
+    dev = _dev()
+    for n, V, parts in ((200000, 3, 3), (1_000_000, 5, 4)):
+        x = torch.stack([torch.from_numpy(vector("normal", n, seed=90 + v)) for v in range(V)]).to(dev)
+        whole = Plan(n, direction, batch=V, device=dev, engine=1).execute(x)
+        for p in range(parts):
+            lo, hi = partition(n, p, parts)
+            z = Plan(n, direction, batch=V, device=dev, part_index=p, part_count=parts).execute(x)
+            assert torch.equal(z[:, lo:hi], whole[:, lo:hi]), (n, V, p)
+        with pytest.raises(LegChebError):
+            Plan(n, direction, batch=V, device=dev, part_index=0, part_count=parts, part_up=1)
