@@ -1699,7 +1699,7 @@ __host__ __device__ inline int64_t tile_smem_doubles(int L, int s) {
   const int fst = tile_fst(s);
   const int ns = L - tile_gs(L);  // levels in shared memory
   return 2 * 32 * kM + (kMM + 4) + 80 + LC_FRING * 2 * kTileV * fst + LC_FRING * 4 * s + int64_t(ns) * 3 * 2 * kTS +
-         int64_t(2 * ns + 1) * 2 * kTS + 2 * kTileV * (2 * s + 4);
+         int64_t(2 * ns + 1) * 2 * kTS + 2 * kTileV * (2 * s + 4) + kMM;
 }
 __host__ __device__ inline int64_t tile_scratch_doubles(int L) { return int64_t(tile_gs(L)) * 5 * 2 * kTS; }
 
@@ -1789,6 +1789,62 @@ __device__ __forceinline__ void band32(const double* __restrict__ fU, const doub
   }
 }
 
+// Step 5 of leaf V1 for row tile mt (m = 8 mt + lr) of both parities: z[v][2m + sigma] += sum_k
+// T(sigma)[m][k] c(L-1, V1)[sigma][v][k] (cc = c(L-1, V1), [sigma][v][k]), then C^{-1} (step 7) and the
+// store: a lane holds rows i0 + 2m and i0 + 2m + 1 of vectors 2 lc and 2 lc + 1, written as one 16-byte
+// store where the output layout allows it (v2ok)
+template <int DIR>
+__device__ __forceinline__ void step5_store(const TileParams& P, const double* __restrict__ Tq,
+                                            const double* __restrict__ cc, const double* __restrict__ zb, int zst,
+                                            int64_t tile, int64_t i0, int mt, int s, int lr, int lc, bool v2ok) {
+  const int m = 8 * mt + lr;
+  double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+  for (int kk = 0; kk < 5; ++kk) {
+    const int k = 4 * kk + lc;
+#pragma unroll
+    for (int sg = 0; sg < 2; ++sg) {
+      const double bb = k < kM ? cc[sg * kTS + lr * kM + k] : 0.0;
+      const double a = k < kM ? Tq[(sg * 32 + m) * kM + k] : 0.0;
+      dmma(acc[sg], a, bb);
+    }
+  }
+  if (m >= s) return;
+  const double inv_pi = 0.318309886183790671537767526745028724;
+  const int64_t i = i0 + 2 * m;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int v = 2 * lc + h;
+    const int64_t gv = tile * kTileV + v;
+    const double2 zz = *reinterpret_cast<const double2*>(zb + v * zst + 2 * m);
+    double z0 = zz.x + acc[0][h], z1 = zz.y + acc[1][h];
+    if (DIR == 0) {
+      z0 *= (i == 0 ? inv_pi : 2.0 * inv_pi);
+      z1 *= 2.0 * inv_pi;
+    }
+    if (gv >= P.batch) continue;
+    if (v2ok && i + 1 < P.n) {
+      double* o = P.oblk ? P.out + (i / P.oblk) * P.batch * P.oblk + gv * P.oblk + i % P.oblk : P.out + gv * P.ld_out + i;
+      *reinterpret_cast<double2*>(o) = make_double2(z0, z1);
+    } else {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int64_t ie = i + e;
+        const double z = e ? z1 : z0;
+        if (ie < P.n) {
+          if (P.oblk) P.out[(ie / P.oblk) * P.batch * P.oblk + gv * P.oblk + ie % P.oblk] = z;
+          else if (P.layout == LC_VEC_CONTIGUOUS) P.out[gv * P.ld_out + ie] = z;
+          else P.out[ie * P.ld_out + gv] = z;
+        }
+      }
+    }
+  }
+}
+__device__ __forceinline__ bool step5_v2ok(const TileParams& P) {
+  const bool lay = P.oblk ? (P.oblk & 1) == 0 : (P.layout == LC_VEC_CONTIGUOUS && (P.ld_out & 1) == 0);
+  return lay && (reinterpret_cast<uintptr_t>(P.out) & 15) == 0;
+}
+
 template <int DIR>
 __global__ void __launch_bounds__(kTileThreads, LC_TILE_MINB) lc_tile_kernel(const __grid_constant__ TileParams P) {
   extern __shared__ __align__(128) unsigned char smem[];
@@ -1807,6 +1863,7 @@ __global__ void __launch_bounds__(kTileThreads, LC_TILE_MINB) lc_tile_kernel(con
   double* wr = lmr + LC_FRING * 4 * s;            // [ns][3][2][8][M]
   double* cs = wr + ns * 3 * 2 * kTS;             // levels gs..L-2: [2][2][8][M], then leaf [3][2][8][M]
   double* zs = cs + (2 * ns + 1) * 2 * kTS;       // [2][8][2s+4]
+  double* Bqs = zs + 2 * kTileV * zst_;           // sign-folded B(0): (-1)^(n-k) b_nk (child 1 / parity 1)
   double* gw = P.scratch + int64_t(blockIdx.x) * tile_scratch_doubles(L);  // [gs][3][2][8][M]
   double* gc = gw + gs * 3 * 2 * kTS;                                       // [gs][2][2][8][M]
   auto fslot = [&](int U) { return fr + ((U + LC_FRING) % LC_FRING) * 2 * kTileV * fst; };  // U >= -1
@@ -1825,6 +1882,10 @@ __global__ void __launch_bounds__(kTileThreads, LC_TILE_MINB) lc_tile_kernel(con
   for (int i = tid; i < 80; i += kTileThreads) taq[i] = i < seglen ? P.tabA[i] : 0.0;
   // rows m in [s, fst) of every f slot stay zero (read by the K = 4 ceil(s/4) steps of step 1)
   for (int i = tid; i < LC_FRING * 2 * kTileV * fst; i += kTileThreads) fr[i] = 0.0;
+  for (int i = tid; i < kMM; i += kTileThreads) {
+    const double b = __ldg(P.B + i);
+    Bqs[i] = ((i / kM - i % kM) & 1) ? -b : b;
+  }
   cp_async_commit();
   __syncthreads();  // the zero fill precedes every cp.async into the ring (other threads' elements)
   griddep_wait();  // the input may be produced by the preceding kernel
@@ -1863,7 +1924,7 @@ __global__ void __launch_bounds__(kTileThreads, LC_TILE_MINB) lc_tile_kernel(con
     const int g = L - 1 - ones;
     return g < 0 ? 0 : g;
   };
-  const double inv_pi = 0.318309886183790671537767526745028724;
+  const bool v2ok = step5_v2ok(P);  // 16-byte output stores
 
   for (int64_t tile = blockIdx.x; tile < P.ntiles; tile += gridDim.x) {
     for (int i = tid; i < (2 * ns + 1) * 2 * kTS; i += kTileThreads) cs[i] = 0.0;  // rows without M2L stay 0
@@ -1970,44 +2031,8 @@ __global__ void __launch_bounds__(kTileThreads, LC_TILE_MINB) lc_tile_kernel(con
           }
         }
         TP_MARK(0);
-        if (V1 < nls && 16 * (warp >> 1) < s) {
-          // ---- step 5 of leaf V1: z[v][2m + sigma] += sum_k T(sigma)[m][k] c(L-1, V1)[sigma][v][k],
-          // row tiles {2h, 2h+1}; then C^{-1} (step 7) and the store of those rows
-          const int sg = warp & 1, mt0 = 2 * (warp >> 1);
-          const double* cc = cslot(L - 1, V1) + sg * kTS;
-          double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
-#pragma unroll
-          for (int kk = 0; kk < 5; ++kk) {
-            const int k = 4 * kk + lc;
-            const double bb = k < kM ? cc[lr * kM + k] : 0.0;
-#pragma unroll
-            for (int q = 0; q < 2; ++q) {
-              const int m = 8 * (mt0 + q) + lr;
-              const double a = k < kM ? Tq[(sg * 32 + m) * kM + k] : 0.0;
-              dmma(acc[q], a, bb);
-            }
-          }
-          const double* zb = zbuf(V1);
-          const int64_t i0 = int64_t(V1) * seglen;
-#pragma unroll
-          for (int q = 0; q < 2; ++q) {
-            const int m = 8 * (mt0 + q) + lr;
-            if (m < s) {
-#pragma unroll
-              for (int h = 0; h < 2; ++h) {
-                const int v = 2 * lc + h;
-                const int64_t gv = tile * kTileV + v, i = i0 + 2 * m + sg;
-                double z = zb[v * zst_ + 2 * m + sg] + acc[q][h];
-                if (DIR == 0) z *= (i == 0 ? inv_pi : 2.0 * inv_pi);
-                if (gv < P.batch && i < P.n) {
-                  if (P.oblk) P.out[(i / P.oblk) * P.batch * P.oblk + gv * P.oblk + i % P.oblk] = z;
-                  else if (P.layout == LC_VEC_CONTIGUOUS) P.out[gv * P.ld_out + i] = z;
-                  else P.out[i * P.ld_out + gv] = z;
-                }
-              }
-            }
-          }
-        }
+        if (V1 < nls && 8 * warp < s)  // ---- step 5 + 7 of leaf V1, row tile = warp, both parities
+          step5_store<DIR>(P, Tq, cslot(L - 1, V1), zbuf(V1), zst_, tile, int64_t(V1) * seglen, warp, s, lr, lc, v2ok);
       } else {
         const int sg = warp & 1;
         if (warp < 6) {
@@ -2068,8 +2093,7 @@ __global__ void __launch_bounds__(kTileThreads, LC_TILE_MINB) lc_tile_kernel(con
                 for (int mt = 0; mt < 3; ++mt) {
                   if (mt == 0 && (kk == 2 || kk == 3 || kk == 7 || kk == 8)) continue;  // k >= 8 > n
                   const int nn = 8 * mt + lr;
-                  double a = nn < kM ? Bq[nn * kM + kx] : 0.0;
-                  if (child && ((nn - kx) & 1)) a = -a;
+                  const double a = nn < kM ? (child ? Bqs : Bq)[nn * kM + kx] : 0.0;
                   dmma(acc[mt], a, bb);
                 }
               }
@@ -2103,8 +2127,7 @@ __global__ void __launch_bounds__(kTileThreads, LC_TILE_MINB) lc_tile_kernel(con
               for (int mt = 0; mt < 3; ++mt) {
                 if (4 * kk + 3 < 8 * mt) continue;  // n < k everywhere
                 const int k = 8 * mt + lr;
-                double a = (k < kM && nn < kM) ? Bq[nn * kM + k] : 0.0;  // b_{n k}
-                if (p && ((k + nn) & 1)) a = -a;
+                const double a = (k < kM && nn < kM) ? (p ? Bqs : Bq)[nn * kM + k] : 0.0;  // b_{n k}, sign-folded
                 dmma(acc[mt], a, bb);
               }
             }
@@ -2277,7 +2300,7 @@ __global__ void __launch_bounds__(kTileThreads, STAGE ? 3 : LC_RANGE_MINB) lc_ra
     const int g = L - 1 - ones;
     return g < 0 ? 0 : g;
   };
-  const double inv_pi = 0.318309886183790671537767526745028724;
+  const bool v2ok = step5_v2ok(P);  // 16-byte output stores
 
   const int64_t nunits = P.ntiles * P.nranges;
   for (int64_t unit = blockIdx.x; unit < nunits; unit += gridDim.x) {
@@ -2383,44 +2406,8 @@ __global__ void __launch_bounds__(kTileThreads, STAGE ? 3 : LC_RANGE_MINB) lc_ra
           }
         }
         TP_MARK(0);
-        if (V1 >= Ua && V1 <= Ub && 16 * (warp >> 1) < s) {
-          // ---- step 5 of leaf V1: z[v][2m + sigma] += sum_k T(sigma)[m][k] c(L-1, V1)[sigma][v][k],
-          // row tiles {2h, 2h+1}; then C^{-1} (step 7) and the store of those rows
-          const int sg = warp & 1, mt0 = 2 * (warp >> 1);
-          const double* cc = cslot(L - 1, V1) + sg * kTS;
-          double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
-#pragma unroll
-          for (int kk = 0; kk < 5; ++kk) {
-            const int k = 4 * kk + lc;
-            const double bb = k < kM ? cc[lr * kM + k] : 0.0;
-#pragma unroll
-            for (int q = 0; q < 2; ++q) {
-              const int m = 8 * (mt0 + q) + lr;
-              const double a = k < kM ? Tq[(sg * 32 + m) * kM + k] : 0.0;
-              dmma(acc[q], a, bb);
-            }
-          }
-          const double* zb = zbuf(V1);
-          const int64_t i0 = int64_t(V1) * seglen;
-#pragma unroll
-          for (int q = 0; q < 2; ++q) {
-            const int m = 8 * (mt0 + q) + lr;
-            if (m < s) {
-#pragma unroll
-              for (int h = 0; h < 2; ++h) {
-                const int v = 2 * lc + h;
-                const int64_t gv = tile * kTileV + v, i = i0 + 2 * m + sg;
-                double z = zb[v * zst_ + 2 * m + sg] + acc[q][h];
-                if (DIR == 0) z *= (i == 0 ? inv_pi : 2.0 * inv_pi);
-                if (gv < P.batch && i < P.n) {
-                  if (P.oblk) P.out[(i / P.oblk) * P.batch * P.oblk + gv * P.oblk + i % P.oblk] = z;
-                  else if (P.layout == LC_VEC_CONTIGUOUS) P.out[gv * P.ld_out + i] = z;
-                  else P.out[i * P.ld_out + gv] = z;
-                }
-              }
-            }
-          }
-        }
+        if (V1 >= Ua && V1 <= Ub && 8 * warp < s)  // ---- step 5 + 7 of leaf V1, row tile = warp, both parities
+          step5_store<DIR>(P, Tq, cslot(L - 1, V1), zbuf(V1), zst_, tile, int64_t(V1) * seglen, warp, s, lr, lc, v2ok);
       } else {
         const int sg = warp & 1;
         if (warp >= 6 && inU) {
