@@ -5,6 +5,10 @@ import sys
 import torch
 
 sys.path.insert(0, '.')
+import os  # noqa: E402
+from paper_2411_00033_b200 import _lib  # noqa: E402
+if os.environ.get("LC_LIB"):  # A/B builds: LC_LIB=liblegcheb_x.so
+    _lib.LIB_PATH = _lib.LIB_PATH.replace("liblegcheb.so", os.environ["LC_LIB"])
 from paper_2411_00033_b200 import Plan  # noqa: E402
 from lc_inputs import batch as mkbatch  # noqa: E402
 
