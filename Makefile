@@ -19,7 +19,7 @@ clean:
 	rm -f $(PKG)/liblegcheb.so oracle/liboracle.so
 .PHONY: all clean
 
-# phase-timestamp instrumented build (tools/phase_timing.py); not used by the product path
+# phase-timestamp instrumented build (tools/timeline.py, tile_roles.py, band_phases.py); not used by the product path
 debug: $(PKG)/liblegcheb_dbg.so
 $(PKG)/liblegcheb_dbg.so: $(SRCS) $(HDRS)
 	$(NVCC) $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -shared -DLC_PHASE_TIMING $(SRCS) -o $@
