@@ -167,7 +167,11 @@ def workload(config: str, world: int, rank: int):
 
 def make_input(kind, n, V, v0, pin):
     from lc_inputs import batch
-    out = torch.empty((V, n), dtype=torch.float64, pin_memory=pin)
+    if pin:  # page-locked host memory on huge pages (lc_host_alloc): full PCIe rate for the e2e copies
+        from paper_2411_00033_b200 import host_empty
+        out = host_empty((V, n))
+    else:
+        out = torch.empty((V, n), dtype=torch.float64)
     return batch(kind, n, V, seed=0, v0=v0, out=out)
 
 
@@ -217,6 +221,8 @@ def timed_replays(fn, steps, stream):
 
 def measure(config, args, world, rank, local, headline=True):
     """One JSON record (bench contract keys) for `config` on this rank set."""
+    from paper_2411_00033_b200 import execute_host_chain, host_empty, new_chain_stage
+    from paper_2411_00033_b200.api import chain_stage_bytes
     from paper_2411_00033_b200.dist import tensor_product_2d
     dev = torch.device("cuda", local)
     n, V, kind, v0, scaling = workload(config, world, rank)
@@ -393,41 +399,35 @@ def measure(config, args, world, rank, local, headline=True):
     t_meas = ms_local / args.steps / 2 * 1e-3
     t_med = med_ms / 2 * 1e-3
 
-    # ---- e2e through the C ABI with HOST buffers: lc_execute_host (H2D, kernels, D2H in one call) for
-    # each transform of the step, pipelined over three streams with caller-owned staging and workspaces
-    # (the call is thread- and stream-safe with distinct buffers, legcheb.h)
+    # ---- e2e through the C ABI with HOST buffers, pipelined over streams (the call is thread- and
+    # stream-safe with distinct staging and workspaces, legcheb.h)
     e2e_steps = max(3, min(args.steps, args.e2e_steps))
-    # --e2e-streams buffer sets (staging + workspace per plan and stream) when they fit, else fewer; with
-    # one set the plan-owned staging and workspace serve (calls serialised on one stream)
-    per_set = pl.host_stage_bytes + pc.host_stage_bytes + pl.workspace_bytes + pc.workspace_bytes
+    # one C-ABI call per step (lc_execute_host_chain): the step's input H2D, leg2cheb then cheb2leg (2-D:
+    # the row pass then the column pass) on the device, the result D2H; --e2e-streams buffer sets (chain
+    # staging + a workspace per plan, per stream) when they fit, else fewer
+    chain = [pl, pc]
+    per_set = chain_stage_bytes(chain) + pl.workspace_bytes + pc.workspace_bytes
     free_b = torch.cuda.mem_get_info(dev)[0]
     nbuf = max(1, args.e2e_streams)
     while nbuf > 1 and nbuf * per_set >= 0.6 * free_b:
         nbuf -= 1
     streams = [torch.cuda.Stream(dev) for _ in range(nbuf)]
-    if two_d:
-        hz = [torch.empty_like(xh).pin_memory() for _ in range(nbuf)]
-        hy = [torch.empty((n, C), dtype=torch.float64).pin_memory() for _ in range(nbuf)]
+    hy = [host_empty((n, C) if two_d else tuple(xh.shape)) for _ in range(nbuf)]
+    if two_d and world > 1:
         ycols = [torch.empty((n, C), dtype=torch.float64, device=dev) for _ in range(nbuf)]
         tmps = [torch.empty_like(x) for _ in range(nbuf)]
+        stages = [None] * nbuf
     else:
-        hz = [torch.empty_like(xh).pin_memory() for _ in range(nbuf)]
-        hy = [torch.empty_like(xh).pin_memory() for _ in range(nbuf)]
-    own = nbuf == 1
-    st_l = [None] if own else [pl.new_host_stage() for _ in range(nbuf)]
-    st_c = [None] if own else [pc.new_host_stage() for _ in range(nbuf)]
-    ws_l = [None] if own else [pl.new_workspace(streams[b]) for b in range(nbuf)]
-    ws_c = [None] if own else [pc.new_workspace(streams[b]) for b in range(nbuf)]
+        stages = [new_chain_stage(chain) for _ in range(nbuf)]
+    ws_l = [pl.new_workspace(streams[b]) for b in range(nbuf)]
+    ws_c = [pc.new_workspace(streams[b]) for b in range(nbuf)]
     torch.cuda.synchronize()
 
     def host_steps(k0, k):
         for i in range(k0, k0 + k):
             b = i % nbuf
             sb = streams[b]
-            if two_d and world == 1:
-                pl.execute_host(xh, hz[b], stream=sb, stage=st_l[b], workspace=ws_l[b])
-                pc.execute_host(hz[b].view(n, n), hy[b], stream=sb, stage=st_c[b], workspace=ws_c[b])
-            elif two_d:
+            if two_d and world > 1:
                 with torch.cuda.stream(sb):
                     xd = xh.to(dev, non_blocking=True)
                     zc = tensor_product_2d(xd, row_fn=lambda a: pl.execute(a, tmps[b], workspace=ws_l[b], stream=sb),
@@ -435,8 +435,7 @@ def measure(config, args, world, rank, local, headline=True):
                                            row_packed=True)
                     hy[b].copy_(zc, non_blocking=True)
             else:
-                pl.execute_host(xh, hz[b], stream=sb, stage=st_l[b], workspace=ws_l[b])
-                pc.execute_host(hz[b], hy[b], stream=sb, stage=st_c[b], workspace=ws_c[b])
+                execute_host_chain(chain, xh, hy[b], stages[b], stream=sb, workspaces=[ws_l[b], ws_c[b]])
 
     host_steps(0, nbuf)
     torch.cuda.synchronize()
@@ -460,10 +459,7 @@ def measure(config, args, world, rank, local, headline=True):
     last = (nbuf + e2e_steps - 1) % nbuf
     rt_host = None if two_d else float((hy[last] - xh).abs().max() / xh.abs().max())
     bytes_vec = 8 * n * V
-    if two_d and world > 1:
-        h2d, d2h = bytes_vec, 8 * n * C
-    else:
-        h2d, d2h = 2 * bytes_vec, 2 * bytes_vec
+    h2d, d2h = bytes_vec, 8 * n * C if two_d else bytes_vec
 
     cpu = None
     cfmm = None
@@ -507,11 +503,12 @@ def measure(config, args, world, rank, local, headline=True):
         "plan": plan_info,
         "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "steps": e2e_steps, "ms_per_step": e2e_ms / e2e_steps,
-                "path": ("lc_execute_host (C ABI: pinned host buffer -> H2D -> kernels -> D2H) for leg2cheb, then "
-                         f"for cheb2leg of the host result; {nbuf} stream(s)" +
-                         (" with caller-owned staging/workspaces" if nbuf > 1 else ", plan-owned staging/workspace"))
+                "path": ("lc_execute_host_chain (C ABI, one call per step: the input H2D from page-locked huge-page "
+                         "host memory (lc_host_alloc), " + ("the row pass then the column pass" if two_d else
+                                                            "leg2cheb then cheb2leg") +
+                         f" on the device, the result D2H); {nbuf} stream(s), caller-owned staging and workspaces")
                         if not (two_d and world > 1) else
-                        "H2D + tensor_product_2d (NCCL all-to-all) + D2H, 3 streams"},
+                        f"H2D + tensor_product_2d (NCCL all-to-all) + D2H, {nbuf} stream(s)"},
         "gpu_launches": (kpe + pc.kernels_per_execute) * args.steps,
         "clocks": clk,
         "round_trip_einf": {"device": rt, "host_path": rt_host},

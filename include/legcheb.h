@@ -200,6 +200,49 @@ size_t lc_host_stage_bytes(const lc_plan* p);
 lc_status lc_execute_host(const lc_plan* p, const double* h_in, double* h_out, void* d_stage, void* workspace,
                           void* stream);
 
+/* Bytes of the device staging lc_execute_host_chain needs for plans[0..nplans):
+ * two ping-pong halves, each the largest input or output extent of the plans
+ * (rounded up to 256 bytes).  0 if plans is NULL, nplans < 1 or a plan is NULL. */
+size_t lc_host_chain_stage_bytes(const lc_plan* const* plans, int nplans);
+
+/* A chain of transforms on HOST data with one copy each way: h_in (the input
+ * of plans[0]) is copied to device staging, plans[0], ..., plans[nplans-1] are
+ * executed one after another on the device (the output array of plan k, as
+ * that plan lays it out, is the input array of plan k+1), and the output of
+ * the last plan is copied to h_out; all enqueued on stream, no host sync.
+ * Examples: a round trip (leg2cheb then cheb2leg of the same n and batch), or
+ * the two passes of a 2-D tensor-product transform (a vector-layout plan over
+ * the rows, then a batch-layout plan over the columns of the same array).
+ * Applies Alg. 4 per plan, as lc_execute does.
+ *   plans: nplans >= 1 plans of one device, none with part_up; the output
+ *          extent of plan k must cover the input extent of plan k+1.
+ *   d_stage: device, >= lc_host_chain_stage_bytes(plans, nplans), caller-owned
+ *            (required).
+ *   workspaces: NULL (every plan's own workspace; calls must then be
+ *            serialised on one stream) or nplans workspaces, one per plan.
+ * Host buffers should be page-locked (lc_host_alloc).  Errors: INVALID_ARG,
+ * ALIASING, CUDA. */
+lc_status lc_execute_host_chain(const lc_plan* const* plans, int nplans, const double* h_in, double* h_out,
+                                void* d_stage, void* const* workspaces, void* stream);
+
+/* Page-locked host memory for lc_execute_host's buffers: an anonymous mapping
+ * aligned to 2 MiB, advised for transparent huge pages, touched (zeroed) and
+ * registered with cudaHostRegister.  Huge pages keep the DMA engines' address
+ * translations few: measured on this pool's B200 boxes, 8-16 MiB host-to-device
+ * copies run at 54-55 GB/s from such buffers against 12-15 GB/s from
+ * cudaHostAlloc memory (tools/h2d_sizes.py).  Where huge pages are not
+ * available the same mapping is registered with 4 KiB pages.
+ *   bytes: > 0.  *ptr receives the buffer (16-byte aligned, zero-filled).
+ * The caller owns the buffer and releases it with lc_host_free (not free or
+ * cudaFreeHost).  Errors: INVALID_ARG (bytes == 0, ptr NULL), OUT_OF_MEMORY
+ * (mapping failed), CUDA (registration failed; nothing is leaked). */
+lc_status lc_host_alloc(size_t bytes, void** ptr);
+
+/* Unregister and unmap a buffer from lc_host_alloc.  The caller makes sure no
+ * enqueued copy still uses it (e.g. synchronises the streams that do).
+ * Errors: INVALID_ARG (not a live lc_host_alloc buffer), CUDA. */
+lc_status lc_host_free(void* ptr);
+
 /* Copy plan data to host memory (synchronous; test/diagnostic use).
  * what: 0 band table B (length N: lambda_m for L2C, rho_m for C2L),
  *       1 band table A (length 2s: lambda_k for L2C, kappa_k for C2L),

@@ -50,6 +50,10 @@ SIGNATURES = {
     "lc_execute_timed": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_vp, ctypes.POINTER(c_vp), c_i32]),
     "lc_host_stage_bytes": (ctypes.c_size_t, [c_vp]),
     "lc_execute_host": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "lc_host_chain_stage_bytes": (ctypes.c_size_t, [ctypes.POINTER(c_vp), c_i32]),
+    "lc_execute_host_chain": (c_i32, [ctypes.POINTER(c_vp), c_i32, c_vp, c_vp, c_vp, ctypes.POINTER(c_vp), c_vp]),
+    "lc_host_alloc": (c_i32, [ctypes.c_size_t, ctypes.POINTER(c_vp)]),
+    "lc_host_free": (c_i32, [c_vp]),
     "lc_plan_export": (c_i32, [c_vp, c_i32, c_dp, c_i64]),
     "lc_plan_kernel_info": (c_i32, [c_vp, ctypes.POINTER(c_i64), c_i32, ctypes.POINTER(c_i32)]),
     "lc_plan_destroy": (c_i32, [c_vp]),

@@ -2937,10 +2937,6 @@ static cudaError_t launch_vt(const lc_plan* p, const UpParams& up, const StreamP
   return cudaGetLastError();
 }
 
-static int64_t extent(int layout, int64_t ld, int64_t n, int64_t batch) {
-  return layout == LC_VEC_CONTIGUOUS ? (batch - 1) * ld + n : (n - 1) * ld + batch;
-}
-
 template <int SMAX>
 static cudaError_t launch_dispatch(const lc_plan* p, const UpParams& up, const StreamParams& sp, const DownParams& dp,
                                    dim3 gu, dim3 gd, cudaStream_t st, cudaEvent_t const* ev, int nev) {
@@ -2964,10 +2960,9 @@ static lc_status launch_execute_impl(const lc_plan* p, const double* in, double*
   if ((phase >= 0) != (p->part_up != 0)) return LC_ERR_INVALID_ARG;
   {
     const char* a0 = reinterpret_cast<const char*>(in);
-    const char* a1 = a0 + 8 * extent(p->layout, p->ld_in, p->n, p->batch);
+    const char* a1 = a0 + 8 * in_extent(p);
     const char* b0 = reinterpret_cast<const char*>(out);
-    const char* b1 = b0 + 8 * (p->out_block ? (p->n + p->out_block - 1) / p->out_block * p->batch * p->out_block
-                                             : extent(p->layout, p->ld_out, p->n, p->batch));
+    const char* b1 = b0 + 8 * out_extent(p);
     if (a0 < b1 && b0 < a1) return LC_ERR_ALIASING;
   }
   if (!ws) ws = p->d_ws;
@@ -3142,8 +3137,8 @@ extern "C" lc_status lc_execute_timed(const lc_plan* p, const double* in, double
 extern "C" lc_status lc_execute_host(const lc_plan* p, const double* h_in, double* h_out, void* d_stage,
                                      void* ws, void* stream) {
   if (!p || !h_in || !h_out) return LC_ERR_INVALID_ARG;
-  const int64_t ein = lc::extent(p->layout, p->ld_in, p->n, p->batch);
-  const int64_t eout = lc::extent(p->layout, p->ld_out, p->n, p->batch);
+  const int64_t ein = lc::in_extent(p);
+  const int64_t eout = lc::out_extent(p);
   int prev = 0;
   cudaGetDevice(&prev);
   if (prev != p->device) cudaSetDevice(p->device);
@@ -3166,6 +3161,51 @@ extern "C" lc_status lc_execute_host(const lc_plan* p, const double* h_in, doubl
     else lc::note_execute(p, st);  // destroy also waits for the read-back of the staging
   }
   if (prev != p->device) cudaSetDevice(prev);
+  return rc;
+}
+
+static int64_t chain_half(const lc_plan* const* plans, int nplans) {
+  int64_t m = 0;
+  for (int k = 0; k < nplans; ++k) m = std::max(m, std::max(lc::in_extent(plans[k]), lc::out_extent(plans[k])));
+  return lc::align_up(m * 8, 256);
+}
+
+extern "C" size_t lc_host_chain_stage_bytes(const lc_plan* const* plans, int nplans) {
+  if (!plans || nplans < 1) return 0;
+  for (int k = 0; k < nplans; ++k)
+    if (!plans[k]) return 0;
+  return size_t(2 * chain_half(plans, nplans));
+}
+
+extern "C" lc_status lc_execute_host_chain(const lc_plan* const* plans, int nplans, const double* h_in, double* h_out,
+                                           void* d_stage, void* const* workspaces, void* stream) {
+  if (!plans || nplans < 1 || !h_in || !h_out || !d_stage) return LC_ERR_INVALID_ARG;
+  for (int k = 0; k < nplans; ++k) {
+    if (!plans[k] || plans[k]->device != plans[0]->device || plans[k]->part_up) return LC_ERR_INVALID_ARG;
+    if (k > 0 && lc::out_extent(plans[k - 1]) < lc::in_extent(plans[k])) return LC_ERR_INVALID_ARG;
+  }
+  const int dev = plans[0]->device;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  if (prev != dev) cudaSetDevice(dev);
+  // ping-pong staging: plan k reads buf[k & 1] and writes buf[(k + 1) & 1]
+  double* buf[2] = {static_cast<double*>(d_stage),
+                    reinterpret_cast<double*>(static_cast<char*>(d_stage) + chain_half(plans, nplans))};
+  cudaStream_t st = (cudaStream_t)stream;
+  lc_status rc = LC_OK;
+  cudaError_t e = cudaMemcpyAsync(buf[0], h_in, size_t(lc::in_extent(plans[0])) * 8, cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) rc = lc::record_cuda_error(e);
+  for (int k = 0; k < nplans && rc == LC_OK; ++k)
+    rc = lc::launch_execute(plans[k], buf[k & 1], buf[(k + 1) & 1], workspaces ? workspaces[k] : nullptr, st,
+                            nullptr, 0, -1);
+  if (rc == LC_OK) {
+    e = cudaMemcpyAsync(h_out, buf[nplans & 1], size_t(lc::out_extent(plans[nplans - 1])) * 8,
+                        cudaMemcpyDeviceToHost, st);
+    if (e != cudaSuccess) rc = lc::record_cuda_error(e);
+    else
+      for (int k = 0; k < nplans; ++k) lc::note_execute(plans[k], st);
+  }
+  if (prev != dev) cudaSetDevice(prev);
   return rc;
 }
 

@@ -170,6 +170,15 @@ struct lc_plan {
 };
 
 namespace lc {
+// elements spanned by the input / the output array of one execute (layout, leading dimensions and,
+// for the output, the column blocking of out_block plans)
+inline int64_t in_extent(const lc_plan* p) {
+  return p->layout == LC_VEC_CONTIGUOUS ? (p->batch - 1) * p->ld_in + p->n : (p->n - 1) * p->ld_in + p->batch;
+}
+inline int64_t out_extent(const lc_plan* p) {
+  if (p->out_block > 0) return (p->n + p->out_block - 1) / p->out_block * p->batch * p->out_block;
+  return p->layout == LC_VEC_CONTIGUOUS ? (p->batch - 1) * p->ld_out + p->n : (p->n - 1) * p->ld_out + p->batch;
+}
 // remembers the last CUDA error (thread-local) for lc_last_error(); returns LC_ERR_CUDA or OUT_OF_MEMORY
 lc_status record_cuda_error(cudaError_t e);
 lc_status launch_execute(const lc_plan* p, const double* in, double* out, void* ws, cudaStream_t st,

@@ -21,8 +21,11 @@
 #include <cstring>
 #include <algorithm>
 #include <mutex>
+#include <unordered_map>
 #include <utility>
 #include <vector>
+
+#include <sys/mman.h>
 
 #include "lc_internal.h"
 
@@ -548,9 +551,7 @@ extern "C" lc_status lc_plan_create(lc_plan** out, int64_t n, lc_direction dir, 
   const lc_status cs = configure_kernels(p);
   if (cs != LC_OK) return fail(cs);
   {
-    const int64_t ein = p->layout == LC_VEC_CONTIGUOUS ? (batch - 1) * p->ld_in + n : (n - 1) * p->ld_in + batch;
-    const int64_t eout = p->layout == LC_VEC_CONTIGUOUS ? (batch - 1) * p->ld_out + n : (n - 1) * p->ld_out + batch;
-    p->stage_bytes = size_t(align_up(ein * 8, 256) + align_up(eout * 8, 256));
+    p->stage_bytes = size_t(align_up(in_extent(p) * 8, 256) + align_up(out_extent(p) * 8, 256));
   }
   LC_PTRY(cudaMallocAsync(&p->d_ws, p->ws_bytes > 0 ? p->ws_bytes : 16, os));
   LC_PTRY(cudaMemsetAsync(p->d_ws, 0, p->ws_bytes > 0 ? p->ws_bytes : 16, os));
@@ -606,6 +607,59 @@ double* plan_stage(const lc_plan* p_) {
 }  // namespace lc
 
 extern "C" size_t lc_host_stage_bytes(const lc_plan* p) { return p ? p->stage_bytes : 0; }
+
+// Page-locked host buffers on transparent huge pages (legcheb.h): the mapping of every live buffer,
+// for lc_host_free
+namespace {
+struct HostMapping {
+  void* base;
+  size_t len;
+};
+std::mutex g_host_mu;
+std::unordered_map<void*, HostMapping>& host_maps() {
+  static std::unordered_map<void*, HostMapping> m;
+  return m;
+}
+}  // namespace
+
+extern "C" lc_status lc_host_alloc(size_t bytes, void** ptr) {
+  if (bytes == 0 || !ptr) return LC_ERR_INVALID_ARG;
+  *ptr = nullptr;
+  constexpr size_t kHuge = size_t(1) << 21;
+  const size_t len = (bytes + kHuge - 1) / kHuge * kHuge;
+  void* base = mmap(nullptr, len + kHuge, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+  if (base == MAP_FAILED) return LC_ERR_OUT_OF_MEMORY;
+  char* a = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(base) + kHuge - 1) & ~uintptr_t(kHuge - 1));
+#ifdef MADV_HUGEPAGE
+  madvise(a, len, MADV_HUGEPAGE);  // advisory: without THP the 4 KiB pages serve
+#endif
+  std::memset(a, 0, len);  // fault the pages in (as huge pages where granted) before registration
+  const cudaError_t e = cudaHostRegister(a, len, cudaHostRegisterDefault);
+  if (e != cudaSuccess) {
+    munmap(base, len + kHuge);
+    return lc::record_cuda_error(e);
+  }
+  {
+    std::lock_guard<std::mutex> lk(g_host_mu);
+    host_maps()[a] = HostMapping{base, len + kHuge};
+  }
+  *ptr = a;
+  return LC_OK;
+}
+
+extern "C" lc_status lc_host_free(void* ptr) {
+  HostMapping m{};
+  {
+    std::lock_guard<std::mutex> lk(g_host_mu);
+    auto it = host_maps().find(ptr);
+    if (!ptr || it == host_maps().end()) return LC_ERR_INVALID_ARG;
+    m = it->second;
+    host_maps().erase(it);
+  }
+  const cudaError_t e = cudaHostUnregister(ptr);
+  munmap(m.base, m.len);
+  return e == cudaSuccess ? LC_OK : lc::record_cuda_error(e);
+}
 
 extern "C" lc_status lc_plan_destroy(lc_plan* p) {
   if (!p) return LC_ERR_INVALID_ARG;

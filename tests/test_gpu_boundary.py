@@ -168,3 +168,112 @@ def test_column_blocked_output(direction, n, V, B, engine):
         w = min(B, n - k * B)
         assert torch.equal(out[k, :, :w], ref[:, k * B:k * B + w]), k
         assert bool(torch.isnan(out[k, :, w:]).all())  # past n: untouched
+
+
+def test_host_alloc_buffers():
+    """lc_host_alloc / lc_host_free (legcheb.h): page-locked, zero-filled, usable by lc_execute_host with
+    the same result as the device call; bad arguments are rejected; the memory is released with the
+    last view."""
+    import ctypes
+    import gc
+
+    from paper_2411_00033_b200 import _lib, host_empty
+    dev = _dev()
+    lib = _lib.load()
+    n, V = 100003, 3
+    x = host_empty((V, n))
+    assert x.is_pinned() and x.dtype == torch.float64 and x.shape == (V, n) and not bool(x.any())
+    x.copy_(batch("normal", n, V, seed=91))
+    out = host_empty((V, n))
+    p = _plan(n, "cheb2leg", batch=V, device=dev)
+    p.execute_host(x, out)
+    torch.cuda.synchronize()
+    assert torch.equal(out, p.execute(x.to(dev)).cpu())
+    # odd sizes and 1-D shapes; a view outlives its base tensor
+    y = host_empty(7)[2:5]
+    gc.collect()
+    y.fill_(1.0)
+    assert y.sum().item() == 3.0
+    # errors
+    ptr = ctypes.c_void_p()
+    assert lib.lc_host_alloc(0, ctypes.byref(ptr)) == 1  # LC_ERR_INVALID_ARG
+    assert lib.lc_host_free(ctypes.c_void_p(12345)) == 1
+    assert lib.lc_host_alloc(1 << 20, ctypes.byref(ptr)) == 0
+    assert lib.lc_host_free(ptr) == 0
+    assert lib.lc_host_free(ptr) == 1  # double free is rejected, not a crash
+
+
+def test_execute_host_column_blocked():
+    """lc_execute_host of an out_block plan copies back the whole blocked output (its extent is
+    ceil(n/B) V B, more than n V when B does not divide n)."""
+    from paper_2411_00033_b200 import host_empty
+    dev = _dev()
+    n, V, B = 5000, 9, 1024
+    x = host_empty((V, n))
+    x.copy_(batch("normal", n, V, seed=5))
+    pb = _plan(n, "leg2cheb", batch=V, device=dev, out_block=B)
+    nb = -(-n // B)
+    out = host_empty((nb, V, B))
+    out.fill_(float("nan"))
+    pb.execute_host(x, out)
+    torch.cuda.synchronize()
+    ref = pb.execute(x.to(dev)).cpu()
+    for k in range(nb):
+        w = min(B, n - k * B)
+        assert torch.equal(out[k, :, :w], ref[k, :, :w]), k
+
+
+@pytest.mark.parametrize("n,V", [(1000000, 1), (4096, 64), (70001, 3)])
+def test_execute_host_chain_round_trip(n, V):
+    """lc_execute_host_chain of [leg2cheb, cheb2leg]: one copy each way, the same bits as the two device
+    calls, on two streams with their own staging and workspaces; bad arguments are rejected."""
+    import ctypes
+
+    from paper_2411_00033_b200 import _lib, execute_host_chain, host_empty, new_chain_stage
+    dev = _dev()
+    pl = _plan(n, "leg2cheb", batch=V, device=dev)
+    pc = _plan(n, "cheb2leg", batch=V, device=dev)
+    x = host_empty((V, n))
+    x.copy_(batch("uniform_r0.5", n, V, seed=21))
+    xd = x.to(dev)
+    ref = pc.execute(pl.execute(xd)).cpu()
+    streams = [torch.cuda.Stream(device=dev) for _ in range(2)]
+    outs = [host_empty((V, n)) for _ in range(2)]
+    # (the staging and workspaces stay referenced until the streams are done: torch's caching allocator
+    # would hand memory freed on the current stream to the next allocation while the side stream runs)
+    stages = [new_chain_stage([pl, pc]) for _ in range(2)]
+    wss = [[pl.new_workspace(streams[k]), pc.new_workspace(streams[k])] for k in range(2)]
+    for k in range(2):
+        execute_host_chain([pl, pc], x, outs[k], stages[k], stream=streams[k], workspaces=wss[k])
+    torch.cuda.synchronize()
+    for k in range(2):
+        assert torch.equal(outs[k], ref), k
+    assert float((outs[0] - x).abs().max() / x.abs().max()) <= GATE
+    # errors: no staging; a chain whose next plan reads more than the previous one wrote
+    lib = _lib.load()
+    arr = (ctypes.c_void_p * 2)(pl._h, pc._h)
+    assert lib.lc_execute_host_chain(arr, 2, ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(outs[0].data_ptr()),
+                                     None, None, None) == 1
+    big = _plan(n + 1, "cheb2leg", batch=V, device=dev)
+    arr2 = (ctypes.c_void_p * 2)(pl._h, big._h)
+    st = new_chain_stage([pl, big])
+    assert lib.lc_execute_host_chain(arr2, 2, ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(outs[0].data_ptr()),
+                                     ctypes.c_void_p(st.data_ptr()), None, None) == 1
+    assert lib.lc_host_chain_stage_bytes(arr, 0) == 0
+
+
+def test_execute_host_chain_2d():
+    """The two passes of the 2-D tensor-product transform (rows on a vector-layout plan, then columns on
+    a batch-layout plan of the same array) as one host chain equal the two device passes."""
+    from paper_2411_00033_b200 import execute_host_chain, host_empty, new_chain_stage
+    dev = _dev()
+    n = 2048
+    x = host_empty((n, n))
+    x.copy_(batch("normal", n, n, seed=4))
+    pr = _plan(n, "leg2cheb", batch=n, device=dev)
+    pcol = _plan(n, "leg2cheb", batch=n, device=dev, layout="batch")
+    ref = pcol.execute(pr.execute(x.to(dev))).cpu()
+    out = host_empty((n, n))
+    execute_host_chain([pr, pcol], x, out, new_chain_stage([pr, pcol]))
+    torch.cuda.synchronize()
+    assert torch.equal(out, ref)
