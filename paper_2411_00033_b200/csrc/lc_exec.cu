@@ -212,6 +212,7 @@ struct DownParams {
   int64_t ld_out, n, N, batch, w_tile;
   int layout, L, s, k;
   int bulk;  // TMA bulk loads allowed (out 16-byte aligned, ld_out even, full tiles only)
+  int nstream;     // CTAs of the streaming kernel (their arrivals on flags[4] release the down kernel)
   int64_t sub_lo;  // first subtree of a partitioned plan (NEXT-2), else 0
 };
 
@@ -1008,7 +1009,7 @@ __global__ void __launch_bounds__(kStreamThreads, 2) lc_stream_kernel(const __gr
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ int cstart[32];
   __shared__ int slotq[8];  // M2L unit of each ring slot (-1: end of work)
-  __shared__ int s_last, s_band;
+  __shared__ int s_band;
   const StreamParams& P = A;
   const int tid = threadIdx.x;
   const int s = P.s, cb = P.cb, nst = P.nst, kb = P.kb;
@@ -1268,7 +1269,7 @@ __global__ void __launch_bounds__(kStreamThreads, 2) lc_stream_kernel(const __gr
     }
     // this CTA's band rows are stored: an acquire-release arrival (the band warps' stores are ordered
     // before it by the band barrier); the last CTA releases flags[14] so the down kernel can fetch the
-    // band rows while the M2L tail and the release of flags[12] are still in flight
+    // band rows while the M2L tail and the arrivals on flags[4] are still in flight
     band_sync();
     if (btid == 0 && atom_add_acq_rel(&P.flags[15], 1) == int(gridDim.x) - 1) {
       atomicExch(&P.flags[15], 0);
@@ -1279,20 +1280,11 @@ __global__ void __launch_bounds__(kStreamThreads, 2) lc_stream_kernel(const __gr
   __syncthreads();
   LC_TS(1, 1);
   if (tid == 0) {
-    // arrival with acquire-release semantics: this CTA's c_m2l and band stores (ordered before it by
-    // the barrier) are released, and the last arriver acquires every other CTA's, so its release of
-    // flags[12] below carries them all to the down kernel (one RMW instead of two full fences)
-    s_last = atom_add_acq_rel(&P.flags[4], 1) == int(gridDim.x) - 1;
-  }
-  __syncthreads();
-  if (s_last && tid == 0) {  // the last CTA re-arms the counters and releases the down kernel
-    P.flags[1] = 0;
-    P.flags[3] = 0;
-    P.flags[5] = 0;
-    P.flags[10] = 0;
-    P.flags[11] = 0;
-    P.flags[4] = 0;
-    st_release(&P.flags[12], 1);  // streaming complete (read by lc_down_kernel instead of a grid wait)
+    // release arrival: this CTA's c_m2l and band stores (ordered before it by the barrier) are
+    // released; the down kernel's acquire load of the complete count synchronises with every arrival
+    // (no last-arriver release: one fence per CTA on the critical path instead of two), and the down
+    // kernel re-arms the counters
+    asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(&P.flags[4]) : "memory");
   }
 }
 
@@ -1394,7 +1386,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) lc_down_kernel(const DownParams 
   __shared__ __align__(8) uint64_t dbar;
   if (bulk && tid == 0) {
     // the band rows are complete once every streaming CTA's band warps arrived (flags[14]): fetch them
-    // now, while the last M2L units and the release of flags[12] are still in flight
+    // now, while the last M2L units and the arrivals on flags[4] are still in flight
     mbar_init(&dbar, 1);
     fence_mbar_init();
     wait_flag(&P.flags[14]);
@@ -1403,14 +1395,20 @@ __global__ void __launch_bounds__(NT, 512 / NT) lc_down_kernel(const DownParams 
     for (int v = 0; v < VT; ++v)
       bulk_g2s(zb + v * rows, P.out + (tile * VT + v) * P.ld_out + i0, uint32_t(rows) * 8u, &dbar, pol);
   }
-  // c_m2l (and every band row) is complete once the streaming kernel's last CTA released flags[12]
-  // (cheaper than waiting for the grid to retire); the last down CTA to pass re-arms [12] and [14]
+  // c_m2l (and every band row) is complete once every streaming CTA arrived on flags[4] with release
+  // semantics (cheaper than waiting for the grid to retire); the last down CTA to pass re-arms the
+  // counters and readiness flags of this execution for the next one
   if (tid == 0) {
-    wait_flag(&P.flags[12]);
+    while (ld_acquire(&P.flags[4]) < P.nstream) __nanosleep(64);
     if (atomicAdd(&P.flags[13], 1) == int(gridDim.x * gridDim.y) - 1) {
       P.flags[13] = 0;
       P.flags[14] = 0;
-      P.flags[12] = 0;
+      P.flags[4] = 0;
+      P.flags[1] = 0;
+      P.flags[3] = 0;
+      P.flags[5] = 0;
+      P.flags[10] = 0;
+      P.flags[11] = 0;
     }
   }
   __syncthreads();
@@ -3029,6 +3027,7 @@ static lc_status launch_execute_impl(const lc_plan* p, const double* in, double*
   dp.out = out; dp.flags = flags; dp.c = c; dp.Tpad = p->d_Tpad; dp.B = p->d_B; dp.ld_out = p->ld_out; dp.n = p->n; dp.N = p->N; dp.batch = p->batch;
   dp.w_tile = p->w_tile_doubles; dp.layout = p->layout; dp.L = int(p->L); dp.s = int(p->s); dp.k = p->k;
   dp.bulk = (p->down_bulk && reinterpret_cast<uintptr_t>(out) % 16 == 0 && p->ld_out % 2 == 0) ? 1 : 0;
+  dp.nstream = p->stream_grid;
   dp.sub_lo = p->sub_lo;
   const int64_t ndown = p->nsub_down;
   if (p->part_count > 1 && (ndown == 0 || p->m2l_units + p->band_units == 0)) {
