@@ -200,6 +200,7 @@ struct StreamParams {
   int nblk[32];     // M2L blocks per level (else 2^(g+1) - 1)
   int layout, L, s, cb, nst, kb, gr_up;
   int lvorder[32];  // M2L level order: position o -> level
+  int nup;          // CTAs of the up kernel's main phase (their arrivals on flags[0]: fine levels ready)
 };
 using StreamArgs = StreamParams;
 
@@ -472,14 +473,9 @@ __global__ void __launch_bounds__(kThreads, (VT == 8 && SMAX == 32) ? LC_UP8_MIN
   // the fine levels (gr..L-1) of the whole batch are ready once every CTA got here
   __syncthreads();
   LC_TS(0, 4);
-  if (tid == 0 && !P.noflags) {
-    const int total = int(gridDim.x * gridDim.y);
-    if (atom_add_acq_rel(&P.flags[0], 1) == total - 1) {
-      atomicExch(&P.flags[0], 0);
-      st_release(&P.flags[1], 1);
-      if (P.gr + dsub == 0) st_release(&P.flags[3], 1);
-    }
-  }
+  // release arrival on flags[0]: the streaming kernel acquire-loads the full count (the fine levels of
+  // every CTA), so no last arriver needs a second release; the down kernel re-arms the counter
+  if (tid == 0 && !P.noflags) asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(&P.flags[0]) : "memory");
 
   if (P.nocont) return;  // partitioned up pass: the coarse levels come after the exchange of the roots
   g = P.gr + dsub;
@@ -1060,7 +1056,10 @@ __global__ void __launch_bounds__(kStreamThreads, 2) lc_stream_kernel(const __gr
           // w of level g: fine levels after the up kernel's main phase, coarse ones after its continuation
           bool& ok = g >= P.gr_up ? fine_ok : coarse_ok;
           if (!ok) {
-            wait_flag(&P.flags[g >= P.gr_up ? 1 : 3]);
+            if (g >= P.gr_up)
+              while (ld_acquire(&P.flags[0]) < P.nup) __nanosleep(64);  // every up CTA's fine levels
+            else
+              wait_flag(&P.flags[3]);
             asm volatile("fence.proxy.async.global;" ::: "memory");  // order the bulk reads after the acquire
             ok = true;
           }
@@ -1404,7 +1403,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) lc_down_kernel(const DownParams 
       P.flags[13] = 0;
       P.flags[14] = 0;
       P.flags[4] = 0;
-      P.flags[1] = 0;
+      P.flags[0] = 0;
       P.flags[3] = 0;
       P.flags[5] = 0;
       P.flags[10] = 0;
@@ -3040,6 +3039,7 @@ static lc_status launch_execute_impl(const lc_plan* p, const double* in, double*
     return LC_ERR_INVALID_ARG;
   }
   const dim3 grid_up(unsigned(p->part_up ? ((p->part_hi - p->part_lo) >> p->kup) : nsub), unsigned(p->ntiles));
+  sp.nup = int(grid_up.x * grid_up.y);  // (phase 1 of a part_up plan: the arrivals of its phase 0)
   const dim3 grid_down(unsigned(ndown), unsigned(p->ntiles));
   if (p->engine == 3) {
     TileParams tp{};
