@@ -221,7 +221,7 @@ def timed_replays(fn, steps, stream):
 
 def measure(config, args, world, rank, local, headline=True):
     """One JSON record (bench contract keys) for `config` on this rank set."""
-    from paper_2411_00033_b200 import execute_host_chain, host_empty, new_chain_stage
+    from paper_2411_00033_b200 import Plan, execute_host_chain, host_empty, new_chain_stage
     from paper_2411_00033_b200.api import chain_stage_bytes
     from paper_2411_00033_b200.dist import tensor_product_2d
     dev = torch.device("cuda", local)
@@ -405,39 +405,53 @@ def measure(config, args, world, rank, local, headline=True):
     # one C-ABI call per step (lc_execute_host_chain): the step's input H2D, leg2cheb then cheb2leg (2-D:
     # the row pass then the column pass) on the device, the result D2H; --e2e-streams buffer sets (chain
     # staging + a workspace per plan, per stream) when they fit, else fewer
-    chain = [pl, pc]
-    per_set = chain_stage_bytes(chain) + pl.workspace_bytes + pc.workspace_bytes
+    # large batches (cfg4: 5 GB per step) go in sub-batches of their own plans, so that one sub-batch's
+    # copies overlap another's transforms (the device-timed value above keeps the whole-batch plans)
+    ech = 1
+    if not two_d and V >= 16 and 8 * n * V >= (1 << 30):
+        ech = next(c for c in (8, 4, 2, 1) if V % c == 0)
+    Vc = V // ech
+    if ech > 1:
+        pl_e = Plan(n, "leg2cheb", batch=Vc, device=dev, engine=args.engine)
+        pc_e = Plan(n, "cheb2leg", batch=Vc, device=dev, engine=args.engine)
+    else:
+        pl_e, pc_e = pl, pc
+    chain = [pl_e, pc_e]
+    per_set = chain_stage_bytes(chain) + pl_e.workspace_bytes + pc_e.workspace_bytes
     free_b = torch.cuda.mem_get_info(dev)[0]
     nbuf = max(1, args.e2e_streams)
     while nbuf > 1 and nbuf * per_set >= 0.6 * free_b:
         nbuf -= 1
     streams = [torch.cuda.Stream(dev) for _ in range(nbuf)]
-    hy = [host_empty((n, C) if two_d else tuple(xh.shape)) for _ in range(nbuf)]
+    hy = [host_empty((n, C) if two_d else (Vc, n)) for _ in range(nbuf)]
     if two_d and world > 1:
         ycols = [torch.empty((n, C), dtype=torch.float64, device=dev) for _ in range(nbuf)]
         tmps = [torch.empty_like(x) for _ in range(nbuf)]
         stages = [None] * nbuf
     else:
         stages = [new_chain_stage(chain) for _ in range(nbuf)]
-    ws_l = [pl.new_workspace(streams[b]) for b in range(nbuf)]
-    ws_c = [pc.new_workspace(streams[b]) for b in range(nbuf)]
+    ws_l = [pl_e.new_workspace(streams[b]) for b in range(nbuf)]
+    ws_c = [pc_e.new_workspace(streams[b]) for b in range(nbuf)]
     torch.cuda.synchronize()
 
     def host_steps(k0, k):
         for i in range(k0, k0 + k):
-            b = i % nbuf
-            sb = streams[b]
             if two_d and world > 1:
+                b = i % nbuf
+                sb = streams[b]
                 with torch.cuda.stream(sb):
                     xd = xh.to(dev, non_blocking=True)
                     zc = tensor_product_2d(xd, row_fn=lambda a: pl.execute(a, tmps[b], workspace=ws_l[b], stream=sb),
                                            col_fn=lambda a: pc.execute(a, ycols[b], workspace=ws_c[b], stream=sb),
                                            row_packed=True)
                     hy[b].copy_(zc, non_blocking=True)
-            else:
-                execute_host_chain(chain, xh, hy[b], stages[b], stream=sb, workspaces=[ws_l[b], ws_c[b]])
+                continue
+            for c in range(ech):  # one chain call per sub-batch (one per step without sub-batches)
+                b = (i * ech + c) % nbuf
+                execute_host_chain(chain, xh[c * Vc:(c + 1) * Vc], hy[b], stages[b], stream=streams[b],
+                                   workspaces=[ws_l[b], ws_c[b]])
 
-    host_steps(0, nbuf)
+    host_steps(0, max(1, nbuf // ech))
     torch.cuda.synchronize()
     barrier(world)
     torch.cuda.synchronize()
@@ -456,8 +470,9 @@ def measure(config, args, world, rank, local, headline=True):
     barrier(world)
     e2e_ms = allreduce_max(h0.elapsed_time(h1), world)
     e2e_val = total_coeffs * e2e_steps / (e2e_ms / 1e3)
-    last = (nbuf + e2e_steps - 1) % nbuf
-    rt_host = None if two_d else float((hy[last] - xh).abs().max() / xh.abs().max())
+    qlast = (nbuf + e2e_steps) * ech - 1  # the last chain call: its buffer and sub-batch
+    rt_host = None if two_d else float((hy[qlast % nbuf] - xh[(qlast % ech) * Vc:(qlast % ech + 1) * Vc]).abs().max() /
+                                       xh.abs().max())
     bytes_vec = 8 * n * V
     h2d, d2h = bytes_vec, 8 * n * C if two_d else bytes_vec
 
@@ -503,10 +518,11 @@ def measure(config, args, world, rank, local, headline=True):
         "plan": plan_info,
         "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "steps": e2e_steps, "ms_per_step": e2e_ms / e2e_steps,
-                "path": ("lc_execute_host_chain (C ABI, one call per step: the input H2D from page-locked huge-page "
+                "path": ("lc_execute_host_chain (C ABI, one call per step or sub-batch: the input H2D from page-locked huge-page "
                          "host memory (lc_host_alloc), " + ("the row pass then the column pass" if two_d else
                                                             "leg2cheb then cheb2leg") +
-                         f" on the device, the result D2H); {nbuf} stream(s), caller-owned staging and workspaces")
+                         f" on the device, the result D2H); {nbuf} stream(s), caller-owned staging and workspaces" +
+                         (f"; {ech} sub-batches of {Vc} vectors per step, each its own call" if ech > 1 else ""))
                         if not (two_d and world > 1) else
                         f"H2D + tensor_product_2d (NCCL all-to-all) + D2H, {nbuf} stream(s)"},
         "gpu_launches": (kpe + pc.kernels_per_execute) * args.steps,
