@@ -495,7 +495,7 @@ def measure(config, args, world, rank, local, headline=True):
                                 f"of n={n} per GPU") if not two_d else
                                (f"cfg5: 2-D leg2cheb of an {n}x{n} fp64 array (axis 1, all-to-all, axis 0), "
                                 f"{V} rows per GPU"), "n": n, "vectors_per_gpu": V, "N_padded": dl["N"],
-                   "L": dl["L"], "s": dl["s"], "M": 18, "s_hat": 32, "transforms_per_step": 2,
+                   "L": dl["L"], "s": dl["s"], "M": 18, "s_hat": 40, "transforms_per_step": 2,
                    "input_kind": kind,
                    "l2": f"no flush: per-step working set {2 * 8 * 324 * dl['nc'] / 1e6:.0f} MB of A_hat + "
                          f"{3 * bytes_vec / 1e6:.0f} MB of vectors vs 126 MB L2" if dl["nc"] > 0 and

@@ -67,7 +67,7 @@ typedef enum {
 } lc_status;
 
 typedef struct {
-  int64_t s_hat;    /* preferred smallest-submatrix half size s_hat (eq:numlevels); 0 -> 32 */
+  int64_t s_hat;    /* preferred smallest-submatrix half size s_hat (eq:numlevels); 0 -> 40 */
   int32_t M;        /* Chebyshev modes per axis; only 18 is supported; 0 -> 18 */
   int32_t layout;   /* lc_layout of in/out */
   int64_t ld_in;    /* leading dimension of in  (elements); 0 -> n (VEC) or batch (BATCH) */
@@ -125,13 +125,13 @@ typedef struct {
 } lc_plan_desc;
 
 /* Host-only: output rows [*row_lo, *row_hi) of part part_index of part_count for length n (s_hat <= 0
- * -> 32).  Parts are contiguous runs of whole groups of 64 leaf segments of 2s rows,
+ * -> 40).  Parts are contiguous runs of whole groups of 64 leaf segments of 2s rows,
  * balanced over the segments that hold outputs; a part may be empty.  Errors: INVALID_ARG. */
 lc_status lc_partition(int64_t n, int64_t s_hat, int32_t part_index, int32_t part_count, int64_t* row_lo,
                        int64_t* row_hi);
 
 /* Host-only geometry (no GPU needed): fills n, N, L, s, M, nc, band_nnz,
- * flops_alg (batch = 1), bytes_alg (batch = 1).  s_hat <= 0 -> 32.
+ * flops_alg (batch = 1), bytes_alg (batch = 1).  s_hat <= 0 -> 40.
  * Errors: LC_ERR_INVALID_ARG if n < 1 or out == NULL. */
 lc_status lc_geometry(int64_t n, int64_t s_hat, lc_plan_desc* out);
 

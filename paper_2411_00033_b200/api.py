@@ -22,14 +22,14 @@ LAYOUTS = {"vec": 0, "batch": 1, 0: 0, 1: 1}
 EXPORTS = {"tabB": 0, "tabA": 1, "ahat": 2, "B": 3, "T": 4}
 
 
-def geometry(n: int, s_hat: int = 32) -> dict:
+def geometry(n: int, s_hat: int = 0) -> dict:
     """Host-only decomposition (eq:numlevels, eq:Ntot, eq:total_blocks_and_mats) and work model."""
     d = _lib.PlanDesc()
     _lib.check("lc_geometry", _lib.load().lc_geometry(int(n), int(s_hat), ctypes.byref(d)))
     return d.as_dict()
 
 
-def partition(n: int, part_index: int, part_count: int, s_hat: int = 32) -> tuple[int, int]:
+def partition(n: int, part_index: int, part_count: int, s_hat: int = 0) -> tuple[int, int]:
     """Output rows [lo, hi) of part part_index of part_count (lc_partition; host only): contiguous runs of
     whole groups of leaf segments, for one long transform split over several GPUs (NEXT-2)."""
     lo, hi = ctypes.c_int64(), ctypes.c_int64()
@@ -77,7 +77,7 @@ def _stream_handle(stream, device=None) -> int:
 class Plan:
     """A transform plan (immutable) for `batch` vectors of length n on one device."""
 
-    def __init__(self, n: int, direction="leg2cheb", batch: int = 1, device=None, s_hat: int = 32,
+    def __init__(self, n: int, direction="leg2cheb", batch: int = 1, device=None, s_hat: int = 0,
                  layout="vec", ld_in: int = 0, ld_out: int = 0, vt: int = 0, subtree: int = 0,
                  stage_blocks: int = 0, stages: int = 0, up_subtree: int = 0,
                  engine: int = 0, part_index: int = 0, part_count: int = 0, part_up: int = 0,

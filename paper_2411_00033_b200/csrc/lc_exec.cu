@@ -345,11 +345,18 @@ __device__ __forceinline__ void up_step1(const double* __restrict__ Ts, const do
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31, nw = blockDim.x >> 5;
     const int lr = lane >> 2, lc = lane & 3;
+    // a warp item fills the 8 MMA columns with lpi leaves x vpi vectors (subtrees of < 8 leaves pack
+    // several vectors per item); column col = (vector vg vpi + col / lpi, leaf lf0 + col % lpi)
+    const int llpi = nleaf >= 8 ? 3 : (nleaf >= 4 ? 2 : (nleaf >= 2 ? 1 : 0));  // log2 lpi (nleaf = 2^k)
+    const int lpi = 1 << llpi;
+    const int vpi = (8 >> llpi) < VT ? (8 >> llpi) : VT;
     const int ngrp = (nleaf + 7) >> 3;
-    for (int item = warp; item < VT * ngrp; item += nw) {
-      const int v = item / ngrp, lf0 = (item - v * ngrp) * 8;
-      const bool okb = lf0 + lr < nleaf;  // this lane's B column
-      const double* fp = fs + (v * nleaf + (okb ? lf0 + lr : 0)) * fst + 2 * lc;
+    const int nitems = (VT / vpi) * ngrp;
+    for (int item = warp; item < nitems; item += nw) {
+      const int vg = item / ngrp, lf0 = (item - vg * ngrp) * 8;
+      const int bv = vg * vpi + (lr >> llpi), blf = lf0 + (lr & (lpi - 1));
+      const bool okb = lr < lpi * vpi && blf < nleaf;  // this lane's B column
+      const double* fp = fs + (okb ? bv * nleaf + blf : 0) * fst + 2 * lc;
       const double* tq = Ts + lc * kM + lr;
       double acc[2][3][2];
 #pragma unroll
@@ -383,8 +390,9 @@ __device__ __forceinline__ void up_step1(const double* __restrict__ Ts, const do
         for (int mt = 0; mt < 3; ++mt)
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
-            const int lf = lf0 + 2 * lc + h, mode = 8 * mt + lr;
-            if (lf < nleaf && mode < kM) leaf[((sg * nleaf + lf) * VT + v) * kM + mode] = acc[sg][mt][h];
+            const int col = 2 * lc + h, mode = 8 * mt + lr;
+            const int v = vg * vpi + (col >> llpi), lf = lf0 + (col & (lpi - 1));
+            if (col < lpi * vpi && lf < nleaf && mode < kM) leaf[((sg * nleaf + lf) * VT + v) * kM + mode] = acc[sg][mt][h];
           }
     }
   }
@@ -573,8 +581,9 @@ __device__ __forceinline__ void m2m_pair(const double* __restrict__ Bs, const do
 // sibling; each merge (step 2) stores the parent's w at once, so the chunk root (level gr - kc) is
 // reached inside the CTA.  Above it the arrival counters of lc_up_kernel merge groups of 2^G chunk
 // roots (the last arriver continues).  No flags: the range kernel waits for the whole grid.
-__global__ void __launch_bounds__(kThreads, 2) lc_up3_kernel(const __grid_constant__ UpArgs<32> A) {
-  constexpr int VT = 8, SMAX = 32;
+template <int SMAX>
+__global__ void __launch_bounds__(kThreads, 2) lc_up3_kernel(const __grid_constant__ UpArgs<SMAX> A) {
+  constexpr int VT = 8;
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ int s_last;
   const UpParams& P = A.p;
@@ -613,25 +622,35 @@ __global__ void __launch_bounds__(kThreads, 2) lc_up3_kernel(const __grid_consta
     tile = it / cpt;
     R = (it - tile * cpt) * nb + (j & (nb - 1));
   };
-  // VEC layout, 16-byte aligned rows: thread t stages the pair (leaf t / s, x = 2 (t % s)) of every
-  // vector (nleaf s <= 8 x 32 = 256 threads), so the addressing is computed once
-  const bool fast = P.layout == LC_VEC_CONTIGUOUS && P.vec16 && nleaf * s <= int(blockDim.x);
-  const int my_lf = tid / s, my_x = 2 * (tid - (tid / s) * s);
-  const bool my_on = tid < nleaf * s;
-  const int my_so = my_lf * fst + my_x, my_jj = my_lf * seglen + my_x;
+  // VEC layout, 16-byte aligned rows: thread t stages the pairs (leaf q / s, x = 2 (q % s)), q = t and
+  // t + 256, of every vector (nleaf s <= 2 x 256 pairs), so the addressing is computed once
+  const bool fast = P.layout == LC_VEC_CONTIGUOUS && P.vec16 && nleaf * s <= 2 * int(blockDim.x);
+  int my_so[2], my_jj[2];
+  bool my_on[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int q = tid + h * int(blockDim.x);
+    const int lf = q / s, x = 2 * (q - lf * s);
+    my_on[h] = q < nleaf * s;
+    my_so[h] = lf * fst + x;
+    my_jj[h] = lf * seglen + x;
+  }
   auto stage = [&](double* fs, int64_t R, int64_t tile) {
     if (!fast) {
       up_stage<VT>(P, fs, R, tile, nleaf, fst);
       return;
     }
-    if (!my_on) return;
-    const int64_t j0 = R * int64_t(nleaf * seglen) + my_jj;
-    const double* src = P.in + tile * VT * P.ld_in + j0;
 #pragma unroll
-    for (int v = 0; v < VT; ++v) {
-      const int64_t rem = (tile * VT + v < P.batch) ? P.n - j0 : 0;
-      const uint32_t bytes = rem >= 2 ? 16u : (rem == 1 ? 8u : 0u);
-      cp_async16z(fs + v * nleaf * fst + my_so, bytes ? src + v * P.ld_in : P.in, bytes);
+    for (int h = 0; h < 2; ++h) {
+      if (!my_on[h]) continue;
+      const int64_t j0 = R * int64_t(nleaf * seglen) + my_jj[h];
+      const double* src = P.in + tile * VT * P.ld_in + j0;
+#pragma unroll
+      for (int v = 0; v < VT; ++v) {
+        const int64_t rem = (tile * VT + v < P.batch) ? P.n - j0 : 0;
+        const uint32_t bytes = rem >= 2 ? 16u : (rem == 1 ? 8u : 0u);
+        cp_async16z(fs + v * nleaf * fst + my_so[h], bytes ? src + v * P.ld_in : P.in, bytes);
+      }
     }
   };
   if (J > 0) {
@@ -1676,7 +1695,13 @@ __global__ void __launch_bounds__(NT, 512 / NT) lc_down_kernel(const DownParams 
 constexpr int kTileThreads = 256;
 constexpr int kTileV = 8;                  // vectors per tile (= DMMA n)
 constexpr int kTS = kTileV * kM;           // doubles per (segment, sigma) state
-__host__ __device__ inline int tile_fst(int s) { int f = 4; while (f < s) f += 16; return f; }
+// f row stride: >= s and 4 (mod 8) doubles, so the 8-byte reads [lr * fst + lc + 4 kc] of a half warp
+// (lr < 4, lc < 4) hit 16 distinct bank pairs; >= 4 ceil(s/4), the K extent of step 1
+__host__ __device__ inline int tile_fst(int s) { int f = 4; while (f < s) f += 8; return f; }
+// engines 2 and 3 take s <= kTileSMax (5 row tiles of 8); T(sigma) is staged as [2][tile_trows(s)][M]
+// with rows >= s zero (step 1 reads 4 ceil(s/4) of them)
+constexpr int kTileSMax = 40;
+__host__ __device__ inline int tile_trows(int s) { return s <= 32 ? 32 : kTileSMax; }
 #ifndef LC_FRING
 #define LC_FRING 3  // leaf slots of the f / lambda ring (3: prefetch one leaf ahead; 4: two)
 #endif
@@ -1695,7 +1720,7 @@ __host__ __device__ inline int tile_gs(int L) { return (LC_TILE_SL == 0 || L <= 
 __host__ __device__ inline int64_t tile_smem_doubles(int L, int s) {
   const int fst = tile_fst(s);
   const int ns = L - tile_gs(L);  // levels in shared memory
-  return 2 * 32 * kM + (kMM + 4) + 80 + LC_FRING * 2 * kTileV * fst + LC_FRING * 4 * s + int64_t(ns) * 3 * 2 * kTS +
+  return 2 * tile_trows(s) * kM + (kMM + 4) + 80 + LC_FRING * 2 * kTileV * fst + LC_FRING * 4 * s + int64_t(ns) * 3 * 2 * kTS +
          int64_t(2 * ns + 1) * 2 * kTS + 2 * kTileV * (2 * s + 4) + kMM;
 }
 __host__ __device__ inline int64_t tile_scratch_doubles(int L) { return int64_t(tile_gs(L)) * 5 * 2 * kTS; }
@@ -1706,7 +1731,7 @@ __host__ __device__ inline int64_t tile_scratch_doubles(int L) { return int64_t(
 // 2 CTAs per SM and lose 10%)
 __host__ __device__ inline int64_t range_smem_doubles(int s, int stage) {
   const int fst = tile_fst(s);
-  return 2 * 32 * kM + (kMM + 4) + 80 + LC_FRING * 2 * kTileV * fst + LC_FRING * 4 * s + int64_t(5) * 2 * kTS +
+  return 2 * tile_trows(s) * kM + (kMM + 4) + 80 + LC_FRING * 2 * kTileV * fst + LC_FRING * 4 * s + int64_t(5) * 2 * kTS +
          2 * kTileV * (2 * s + 4) + (stage ? 4 * (2 * kMM + 2 * kTS) : 0);
 }
 #ifndef LC_RANGE_MINB
@@ -1721,7 +1746,8 @@ struct TileParams {
   const double* A;     // A_hat arena
   const double* tabA;  // 2s
   const double* tabB;  // N
-  const double* Tpad;  // [2][32][M]
+  const double* Tpad;  // [2][tpr][M], rows >= s zero
+  int tpr;             // rows per parity of Tpad (32, or 64 for s > 32)
   const double* B;     // B(0)
   const double* wg;    // engine 3: w of every level (up kernel output), tile stride w_tile
   double* scratch;     // engine 3: per-CTA c slots of the levels below L-2
@@ -1758,6 +1784,48 @@ struct TileParams {
 #define TP_FLUSH ((void)0)
 #endif
 
+// Step 6 of one leaf for s != 32, row tiles R0, R1 (and R2 >= 0) of this warp: rows r = 8 rb + lr,
+// columns c = 4 kc + lc in [8 rb, 2s) of the segment pair (U, U+1); K[r][c] = a[c-r] lambda[(i+j)/2]
+// per lane, G[c][v] = f_v[j] (C2L: j f_j).  The k-steps are unrolled at compile time (immediate shared-
+// memory offsets; the loop ends at nkc = ceil(s/2)); only the diagonal chunks mask c < r.  Rows r >= s of
+// a partly used tile compute values that are never stored (the caller writes r < s; tiles with 8 rb >= s
+// are skipped), and columns c >= 2s have b = 0 (their a stays inside the 4s lambda window: finite).
+// fU / fU1 -> f[sigma][v = lr][0] of U / U+1, lamw -> lambda window + sigma + lr + lc, tap -> tabA + lc - lr.
+// Per warp group at s = 40: {0, 1} 38 and {2, 3, 4} 42 k-steps; at s = 31: {0, 3} 26 and {1, 2} 26.
+template <int DIR, int R0, int R1, int R2, bool ALIGNED>
+__device__ __forceinline__ void band_rows(const double* __restrict__ fU, const double* __restrict__ fU1,
+                                          const double* __restrict__ lamw, const double* __restrict__ tap,
+                                          int64_t i0, int s, int sg, int lr, int lc, double (&acc)[3][2]) {
+  constexpr int RMIN = R0 < R1 ? R0 : R1;
+  const int nkc = (2 * s + 3) >> 2;
+  const double jb = double(i0 + 2 * lc + sg);  // C2L column weight j = jb + 8 kc (exact integers)
+  // (s > 32: every listed tile holds rows, no run-time check)
+  const bool on1 = R2 >= 0 || R1 < 2 || 8 * R1 < s, on2 = R2 >= 0;
+#pragma unroll
+  for (int kc = 2 * RMIN; kc < kTileSMax / 2; ++kc) {
+    if (kc >= nkc) break;
+    const int c = 4 * kc + lc;
+    double b;
+    if (ALIGNED) {  // s = 0 (mod 4): the chunk boundary is the segment boundary, nkc = s/2 (no c >= 2s)
+      b = (4 * kc < s ? fU : fU1 - s)[c];
+    } else {
+      const double* pb = c < s ? fU + c : fU1 + (c - s);
+      b = c < 2 * s ? *pb : 0.0;
+    }
+    if (DIR == 1) b *= jb + double(8 * kc);
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      const int rb = q == 0 ? R0 : (q == 1 ? R1 : R2);
+      if (rb >= 0 && kc >= 2 * rb && (q == 0 || (q == 1 ? on1 : on2))) {
+        const int d = 4 * kc - 8 * rb;
+        double a = tap[d] * lamw[8 * rb + 4 * kc];
+        if (d < 8 && lc + d < lr) a = 0.0;
+        dmma(acc[q], a, b);
+      }
+    }
+  }
+}
+
 // Step 6 of one leaf for s = 32, row tiles RLO < RHI, everything unrolled at compile time:
 // K[r][c] = a[c-r] lambda[(i+j)/2] (per lane, one DMUL), G[c][v] = f_v[j] (C2L: j f_j).  Pointers are
 // pre-offset by the lane: fU/fU1 -> f[sigma][v = lr][lc], lamw -> lambda window + sigma + lr + lc,
@@ -1765,7 +1833,7 @@ struct TileParams {
 template <int DIR, int RLO, int RHI>
 __device__ __forceinline__ void band32(const double* __restrict__ fU, const double* __restrict__ fU1,
                                        const double* __restrict__ lamw, const double* __restrict__ tap,
-                                       int64_t i0, int sg, int lc, int lr, double (&acc)[2][2]) {
+                                       int64_t i0, int sg, int lc, int lr, double (&acc)[3][2]) {
   const double jb = double(i0 + 2 * lc + sg);  // C2L column weight j = jb + 8 kc (exact integers)
 #pragma unroll
   for (int kc = 2 * RLO; kc < 16; ++kc) {
@@ -1791,7 +1859,7 @@ __device__ __forceinline__ void band32(const double* __restrict__ fU, const doub
 // store: a lane holds rows i0 + 2m and i0 + 2m + 1 of vectors 2 lc and 2 lc + 1, written as one 16-byte
 // store where the output layout allows it (v2ok)
 template <int DIR>
-__device__ __forceinline__ void step5_store(const TileParams& P, const double* __restrict__ Tq,
+__device__ __forceinline__ void step5_store(const TileParams& P, const double* __restrict__ Tq, int tr,
                                             const double* __restrict__ cc, const double* __restrict__ zb, int zst,
                                             int64_t tile, int64_t i0, int mt, int s, int lr, int lc, bool v2ok) {
   const int m = 8 * mt + lr;
@@ -1802,7 +1870,7 @@ __device__ __forceinline__ void step5_store(const TileParams& P, const double* _
 #pragma unroll
     for (int sg = 0; sg < 2; ++sg) {
       const double bb = k < kM ? cc[sg * kTS + lr * kM + k] : 0.0;
-      const double a = k < kM ? Tq[(sg * 32 + m) * kM + k] : 0.0;
+      const double a = k < kM ? Tq[(sg * tr + m) * kM + k] : 0.0;
       dmma(acc[sg], a, bb);
     }
   }
@@ -1850,8 +1918,9 @@ __global__ void __launch_bounds__(kTileThreads, LC_TILE_MINB) lc_tile_kernel(con
   const int s = P.s, L = P.L, seglen = 2 * s;
   const int fst = tile_fst(s), zst_ = 2 * s + 4;
   const int nls = 2 << L;  // leaf segments
-  double* Tq = reinterpret_cast<double*>(smem);  // [2][32][M]
-  double* Bq = Tq + 2 * 32 * kM;                  // B(0) [M][M]
+  const int TR = tile_trows(s);
+  double* Tq = reinterpret_cast<double*>(smem);  // [2][TR][M]
+  double* Bq = Tq + 2 * TR * kM;                  // B(0) [M][M]
   double* taq = Bq + kMM + 4;                     // tabA [80]
   double* fr = taq + 80;                          // [LC_FRING][2][8][fst]
   double* lmr = fr + LC_FRING * 2 * kTileV * fst; // [LC_FRING][4s]
@@ -1874,7 +1943,10 @@ __global__ void __launch_bounds__(kTileThreads, LC_TILE_MINB) lc_tile_kernel(con
   };
   auto zbuf = [&](int U) { return zs + (U & 1) * kTileV * zst_; };
 
-  for (int i = tid; i < 2 * 32 * kM / 2; i += kTileThreads) cp_async16(Tq + 2 * i, P.Tpad + 2 * i);
+  for (int i = tid; i < TR * kM; i += kTileThreads) {  // [2][TR][M] from [2][tpr][M]: TR * M / 2 pairs per parity
+    const int sg = i >= TR * kM / 2 ? 1 : 0, j = i - sg * (TR * kM / 2);
+    cp_async16(Tq + sg * TR * kM + 2 * j, P.Tpad + int64_t(sg) * P.tpr * kM + 2 * j);
+  }
   for (int i = tid; i < kMM / 2; i += kTileThreads) cp_async16(Bq + 2 * i, P.B + 2 * i);
   for (int i = tid; i < 80; i += kTileThreads) taq[i] = i < seglen ? P.tabA[i] : 0.0;
   // rows m in [s, fst) of every f slot stay zero (read by the K = 4 ceil(s/4) steps of step 1)
@@ -1947,71 +2019,45 @@ __global__ void __launch_bounds__(kTileThreads, LC_TILE_MINB) lc_tile_kernel(con
       if (warp < 4) {
         if (U >= 0 && 8 * ((warp >> 1) ? 1 : 0) < s) {
           // ---- step 6: rows i = 2sU + 2r + sigma, columns j = 2sU + 2c + sigma (c >= r, j < j_end),
-          // K[r][c] = a[c-r] b[(i+j)/2] formed per lane, G[c][v] = f_v[j] (C2L: j f_j); row tiles
-          // {0,3} or {1,2} per warp (two accumulator chains)
+          // K[r][c] = a[c-r] b[(i+j)/2] formed per lane, G[c][v] = f_v[j] (C2L: j f_j); two or three
+          // row tiles per warp (one accumulator chain each)
           const int sg = warp & 1;
-          const int rlo = (warp >> 1) ? 1 : 0, rhi = (warp >> 1) ? 2 : 3;
-          const bool hion = 8 * rhi < s;
+          const int grp = warp >> 1;
           const double* fU = fslot(U) + (sg * kTileV + lr) * fst;
           const double* fU1 = fslot(U + 1) + (sg * kTileV + lr) * fst;
-          const double* lw = lslot(U);
+          const double* lamw = lslot(U) + sg + lr + lc;  // lambda[(i+j)/2 - 2sU] = lamw[8 rb + 4 kc]
+          const double* tap = taq + lc - lr;              // a[c - r] = tap[4 kc - 8 rb]
           const int64_t i0 = int64_t(U) * seglen;
-          double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+          // row tiles per warp group: s <= 32 {0, 3} / {1, 2}; s in (32, 40] {0, 1} / {2, 3, 4}
+          const int rq0 = s > 32 ? (grp ? 2 : 0) : (grp ? 1 : 0);
+          const int rq1 = s > 32 ? (grp ? 3 : 1) : (grp ? 2 : 3);
+          const int rq2 = (s > 32 && grp) ? 4 : 99;
+          double acc[3][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
           if (s == 32) {
-            const double* fa = fU + lc;
-            const double* fb = fU1 + lc;
-            const double* lamw = lw + sg + lr + lc;
-            const double* tap = taq + lc - lr;
-            if (rlo == 0)
-              band32<DIR, 0, 3>(fa, fb, lamw, tap, i0, sg, lc, lr, acc);
+            if (grp == 0)
+              band32<DIR, 0, 3>(fU + lc, fU1 + lc, lamw, tap, i0, sg, lc, lr, acc);
             else
-              band32<DIR, 1, 2>(fa, fb, lamw, tap, i0, sg, lc, lr, acc);
-          } else if ((s & 3) == 0) {  // fast path: chunk boundary = segment boundary (rows >= s masked)
-            const double* lamw = lw + sg + lr + lc;  // lambda[(i+j)/2 - 2sU] = lamw[8 rb + 4 kc]
-            const double* tap = taq + lc - lr;       // a[c - r] = tap[4 kc - 8 rb]
-            const int nkc = seglen >> 2, s4 = s >> 2;
-            const bool rok0 = 8 * rlo + lr < s, rok1 = 8 * rhi + lr < s;
-            double jw = double(i0 + 2 * (8 * rlo + lc) + sg);  // C2L column weight j (exact integers)
-            for (int kc = 2 * rlo; kc < nkc; ++kc, jw += 8.0) {
-              const int c = 4 * kc + lc;
-              double b = kc < s4 ? fU[c] : fU1[c - s];
-              if (DIR == 1) b *= jw;
-              {
-                const int d = 4 * kc - 8 * rlo;
-                double a = tap[d] * lamw[8 * rlo + 4 * kc];
-                if ((d < 8 && lc + d < lr) || !rok0) a = 0.0;  // c < r inside the diagonal block
-                dmma(acc[0], a, b);
-              }
-              if (hion && kc >= 2 * rhi) {
-                const int d = 4 * kc - 8 * rhi;
-                double a = tap[d] * lamw[8 * rhi + 4 * kc];
-                if ((d < 8 && lc + d < lr) || !rok1) a = 0.0;
-                dmma(acc[1], a, b);
-              }
-            }
-          } else {  // general s: masks on rows, columns and the segment boundary
-            const int nkc = (seglen + 3) >> 2;
-            double jw = double(i0 + 2 * (8 * rlo + lc) + sg);  // C2L column weight j (exact integers)
-            for (int kc = 2 * rlo; kc < nkc; ++kc, jw += 8.0) {
-              const int c = 4 * kc + lc;
-              double b = c < s ? fU[c] : (c < seglen ? fU1[c - s] : 0.0);
-              if (DIR == 1) b *= jw;
-#pragma unroll
-              for (int q = 0; q < 2; ++q) {
-                const int rb = q ? rhi : rlo;
-                if (8 * rb < s && kc >= 2 * rb) {
-                  const int r = 8 * rb + lr;
-                  const double lam = lw[r + c + sg];
-                  const double a = (c >= r && c < seglen && r < s) ? taq[c >= r ? c - r : 0] * lam : 0.0;
-                  dmma(acc[q], a, b);
-                }
-              }
-            }
+              band32<DIR, 1, 2>(fU + lc, fU1 + lc, lamw, tap, i0, sg, lc, lr, acc);
+          } else if (s > 32) {
+            if (grp == 0)
+              band_rows<DIR, 0, 1, -1, false>(fU, fU1, lamw, tap, i0, s, sg, lr, lc, acc);
+            else
+              band_rows<DIR, 2, 3, 4, false>(fU, fU1, lamw, tap, i0, s, sg, lr, lc, acc);
+          } else if ((s & 3) == 0) {
+            if (grp == 0)
+              band_rows<DIR, 0, 3, -1, true>(fU, fU1, lamw, tap, i0, s, sg, lr, lc, acc);
+            else
+              band_rows<DIR, 1, 2, -1, true>(fU, fU1, lamw, tap, i0, s, sg, lr, lc, acc);
+          } else {
+            if (grp == 0)
+              band_rows<DIR, 0, 3, -1, false>(fU, fU1, lamw, tap, i0, s, sg, lr, lc, acc);
+            else
+              band_rows<DIR, 1, 2, -1, false>(fU, fU1, lamw, tap, i0, s, sg, lr, lc, acc);
           }
           double* zb = zbuf(U);
 #pragma unroll
-          for (int q = 0; q < 2; ++q) {
-            const int r = 8 * (q ? rhi : rlo) + lr;
+          for (int q = 0; q < 3; ++q) {
+            const int r = 8 * (q == 0 ? rq0 : (q == 1 ? rq1 : rq2)) + lr;
             if (r < s) {
 #pragma unroll
               for (int h = 0; h < 2; ++h) {
@@ -2028,15 +2074,17 @@ __global__ void __launch_bounds__(kTileThreads, LC_TILE_MINB) lc_tile_kernel(con
           }
         }
         TP_MARK(0);
-        if (V1 < nls && 8 * warp < s)  // ---- step 5 + 7 of leaf V1, row tile = warp, both parities
-          step5_store<DIR>(P, Tq, cslot(L - 1, V1), zbuf(V1), zst_, tile, int64_t(V1) * seglen, warp, s, lr, lc, v2ok);
+        // ---- step 5 + 7 of leaf V1, row tile = warp (and 4 on warp 0 for s > 32), both parities
+        if (V1 < nls)
+          for (int mt = warp; 8 * mt < s; mt += 4)
+            step5_store<DIR>(P, Tq, TR, cslot(L - 1, V1), zbuf(V1), zst_, tile, int64_t(V1) * seglen, mt, s, lr, lc, v2ok);
       } else {
         const int sg = warp & 1;
         if (warp < 6) {
           if (U >= 0) {
             // ---- step 1: w(L-1, U)[sigma][v][mode] = sum_m T(sigma)[m][mode] f_v[2sU + 2m + sigma]
             const double* fv = fslot(U) + (sg * kTileV + lr) * fst;
-            const double* Tm = Tq + sg * 32 * kM;
+            const double* Tm = Tq + sg * TR * kM;
             double acc[3][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
             if (s == 32) {  // compile-time K: immediate offsets, no loop control
               const double* fq = fv + lc;
@@ -2229,8 +2277,9 @@ __global__ void __launch_bounds__(kTileThreads, STAGE ? 3 : LC_RANGE_MINB) lc_ra
   const int lr = lane >> 2, lc = lane & 3;
   const int s = P.s, L = P.L, seglen = 2 * s;
   const int fst = tile_fst(s), zst_ = 2 * s + 4;
-  double* Tq = reinterpret_cast<double*>(smem);  // [2][32][M]
-  double* Bq = Tq + 2 * 32 * kM;                  // B(0) [M][M]
+  const int TR = tile_trows(s);
+  double* Tq = reinterpret_cast<double*>(smem);  // [2][TR][M]
+  double* Bq = Tq + 2 * TR * kM;                  // B(0) [M][M]
   double* taq = Bq + kMM + 4;                     // tabA [80]
   double* fr = taq + 80;                          // [LC_FRING][2][8][fst]
   double* lmr = fr + LC_FRING * 2 * kTileV * fst; // [LC_FRING][4s]
@@ -2250,7 +2299,10 @@ __global__ void __launch_bounds__(kTileThreads, STAGE ? 3 : LC_RANGE_MINB) lc_ra
   };
   auto zbuf = [&](int U) { return zs + (U & 1) * kTileV * zst_; };
 
-  for (int i = tid; i < 2 * 32 * kM / 2; i += kTileThreads) cp_async16(Tq + 2 * i, P.Tpad + 2 * i);
+  for (int i = tid; i < TR * kM; i += kTileThreads) {  // [2][TR][M] from [2][tpr][M]: TR * M / 2 pairs per parity
+    const int sg = i >= TR * kM / 2 ? 1 : 0, j = i - sg * (TR * kM / 2);
+    cp_async16(Tq + sg * TR * kM + 2 * j, P.Tpad + int64_t(sg) * P.tpr * kM + 2 * j);
+  }
   for (int i = tid; i < kMM / 2; i += kTileThreads) cp_async16(Bq + 2 * i, P.B + 2 * i);
   for (int i = tid; i < 80; i += kTileThreads) taq[i] = i < seglen ? P.tabA[i] : 0.0;
   // rows m in [s, fst) of every f slot stay zero (read by the K = 4 ceil(s/4) steps of step 1)
@@ -2322,71 +2374,45 @@ __global__ void __launch_bounds__(kTileThreads, STAGE ? 3 : LC_RANGE_MINB) lc_ra
       if (warp < 4) {
         if (inU && 8 * ((warp >> 1) ? 1 : 0) < s) {
           // ---- step 6: rows i = 2sU + 2r + sigma, columns j = 2sU + 2c + sigma (c >= r, j < j_end),
-          // K[r][c] = a[c-r] b[(i+j)/2] formed per lane, G[c][v] = f_v[j] (C2L: j f_j); row tiles
-          // {0,3} or {1,2} per warp (two accumulator chains)
+          // K[r][c] = a[c-r] b[(i+j)/2] formed per lane, G[c][v] = f_v[j] (C2L: j f_j); two or three
+          // row tiles per warp (one accumulator chain each)
           const int sg = warp & 1;
-          const int rlo = (warp >> 1) ? 1 : 0, rhi = (warp >> 1) ? 2 : 3;
-          const bool hion = 8 * rhi < s;
+          const int grp = warp >> 1;
           const double* fU = fslot(U) + (sg * kTileV + lr) * fst;
           const double* fU1 = fslot(U + 1) + (sg * kTileV + lr) * fst;
-          const double* lw = lslot(U);
+          const double* lamw = lslot(U) + sg + lr + lc;  // lambda[(i+j)/2 - 2sU] = lamw[8 rb + 4 kc]
+          const double* tap = taq + lc - lr;              // a[c - r] = tap[4 kc - 8 rb]
           const int64_t i0 = int64_t(U) * seglen;
-          double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+          // row tiles per warp group: s <= 32 {0, 3} / {1, 2}; s in (32, 40] {0, 1} / {2, 3, 4}
+          const int rq0 = s > 32 ? (grp ? 2 : 0) : (grp ? 1 : 0);
+          const int rq1 = s > 32 ? (grp ? 3 : 1) : (grp ? 2 : 3);
+          const int rq2 = (s > 32 && grp) ? 4 : 99;
+          double acc[3][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
           if (s == 32) {
-            const double* fa = fU + lc;
-            const double* fb = fU1 + lc;
-            const double* lamw = lw + sg + lr + lc;
-            const double* tap = taq + lc - lr;
-            if (rlo == 0)
-              band32<DIR, 0, 3>(fa, fb, lamw, tap, i0, sg, lc, lr, acc);
+            if (grp == 0)
+              band32<DIR, 0, 3>(fU + lc, fU1 + lc, lamw, tap, i0, sg, lc, lr, acc);
             else
-              band32<DIR, 1, 2>(fa, fb, lamw, tap, i0, sg, lc, lr, acc);
-          } else if ((s & 3) == 0) {  // fast path: chunk boundary = segment boundary (rows >= s masked)
-            const double* lamw = lw + sg + lr + lc;  // lambda[(i+j)/2 - 2sU] = lamw[8 rb + 4 kc]
-            const double* tap = taq + lc - lr;       // a[c - r] = tap[4 kc - 8 rb]
-            const int nkc = seglen >> 2, s4 = s >> 2;
-            const bool rok0 = 8 * rlo + lr < s, rok1 = 8 * rhi + lr < s;
-            double jw = double(i0 + 2 * (8 * rlo + lc) + sg);  // C2L column weight j (exact integers)
-            for (int kc = 2 * rlo; kc < nkc; ++kc, jw += 8.0) {
-              const int c = 4 * kc + lc;
-              double b = kc < s4 ? fU[c] : fU1[c - s];
-              if (DIR == 1) b *= jw;
-              {
-                const int d = 4 * kc - 8 * rlo;
-                double a = tap[d] * lamw[8 * rlo + 4 * kc];
-                if ((d < 8 && lc + d < lr) || !rok0) a = 0.0;  // c < r inside the diagonal block
-                dmma(acc[0], a, b);
-              }
-              if (hion && kc >= 2 * rhi) {
-                const int d = 4 * kc - 8 * rhi;
-                double a = tap[d] * lamw[8 * rhi + 4 * kc];
-                if ((d < 8 && lc + d < lr) || !rok1) a = 0.0;
-                dmma(acc[1], a, b);
-              }
-            }
-          } else {  // general s: masks on rows, columns and the segment boundary
-            const int nkc = (seglen + 3) >> 2;
-            double jw = double(i0 + 2 * (8 * rlo + lc) + sg);  // C2L column weight j (exact integers)
-            for (int kc = 2 * rlo; kc < nkc; ++kc, jw += 8.0) {
-              const int c = 4 * kc + lc;
-              double b = c < s ? fU[c] : (c < seglen ? fU1[c - s] : 0.0);
-              if (DIR == 1) b *= jw;
-#pragma unroll
-              for (int q = 0; q < 2; ++q) {
-                const int rb = q ? rhi : rlo;
-                if (8 * rb < s && kc >= 2 * rb) {
-                  const int r = 8 * rb + lr;
-                  const double lam = lw[r + c + sg];
-                  const double a = (c >= r && c < seglen && r < s) ? taq[c >= r ? c - r : 0] * lam : 0.0;
-                  dmma(acc[q], a, b);
-                }
-              }
-            }
+              band32<DIR, 1, 2>(fU + lc, fU1 + lc, lamw, tap, i0, sg, lc, lr, acc);
+          } else if (s > 32) {
+            if (grp == 0)
+              band_rows<DIR, 0, 1, -1, false>(fU, fU1, lamw, tap, i0, s, sg, lr, lc, acc);
+            else
+              band_rows<DIR, 2, 3, 4, false>(fU, fU1, lamw, tap, i0, s, sg, lr, lc, acc);
+          } else if ((s & 3) == 0) {
+            if (grp == 0)
+              band_rows<DIR, 0, 3, -1, true>(fU, fU1, lamw, tap, i0, s, sg, lr, lc, acc);
+            else
+              band_rows<DIR, 1, 2, -1, true>(fU, fU1, lamw, tap, i0, s, sg, lr, lc, acc);
+          } else {
+            if (grp == 0)
+              band_rows<DIR, 0, 3, -1, false>(fU, fU1, lamw, tap, i0, s, sg, lr, lc, acc);
+            else
+              band_rows<DIR, 1, 2, -1, false>(fU, fU1, lamw, tap, i0, s, sg, lr, lc, acc);
           }
           double* zb = zbuf(U);
 #pragma unroll
-          for (int q = 0; q < 2; ++q) {
-            const int r = 8 * (q ? rhi : rlo) + lr;
+          for (int q = 0; q < 3; ++q) {
+            const int r = 8 * (q == 0 ? rq0 : (q == 1 ? rq1 : rq2)) + lr;
             if (r < s) {
 #pragma unroll
               for (int h = 0; h < 2; ++h) {
@@ -2403,10 +2429,16 @@ __global__ void __launch_bounds__(kTileThreads, STAGE ? 3 : LC_RANGE_MINB) lc_ra
           }
         }
         TP_MARK(0);
-        if (V1 >= Ua && V1 <= Ub && 8 * warp < s)  // ---- step 5 + 7 of leaf V1, row tile = warp, both parities
-          step5_store<DIR>(P, Tq, cslot(L - 1, V1), zbuf(V1), zst_, tile, int64_t(V1) * seglen, warp, s, lr, lc, v2ok);
+        // ---- step 5 + 7 of leaf V1, row tile = warp, both parities (s > 32: on warps 4 and 5, below)
+        if (s <= 32 && V1 >= Ua && V1 <= Ub && 8 * warp < s)
+          step5_store<DIR>(P, Tq, TR, cslot(L - 1, V1), zbuf(V1), zst_, tile, int64_t(V1) * seglen, warp, s, lr, lc, v2ok);
       } else {
         const int sg = warp & 1;
+        // s in (32, 40]: the band warps carry five row tiles, so step 5 + 7 of leaf V1 (its c and z
+        // slots are not written in this step) runs on warps 4 and 5: row tiles {0, 2, 4} and {1, 3}
+        if (s > 32 && warp < 6 && V1 >= Ua && V1 <= Ub)
+          for (int mt = warp - 4; 8 * mt < s; mt += 2)
+            step5_store<DIR>(P, Tq, TR, cslot(L - 1, V1), zbuf(V1), zst_, tile, int64_t(V1) * seglen, mt, s, lr, lc, v2ok);
         if (warp >= 6 && inU) {
           // ---- step 4 chain (sigma) over the levels entered at U, coarse to fine
           const int gA = gentry(U);
@@ -2448,7 +2480,9 @@ __global__ void __launch_bounds__(kTileThreads, STAGE ? 3 : LC_RANGE_MINB) lc_ra
       if (warp >= 4 && U - 1 >= Ua) {
         const int gN = gentry(U - 1);
         const int nm2l = (L - gN) * 2;
-        for (int k = warp - 4; k < nm2l; k += 4) {
+        // s > 32: jobs to warps 6, 7, 5, 4 (warps 4 and 5 carry step 5)
+        const int kpos = s > 32 ? (warp >= 6 ? warp - 6 : 7 - warp) : warp - 4;
+        for (int k = kpos; k < nm2l; k += 4) {
           const int g = gN + (k >> 1), sgk = k & 1;
           const int u = (U - 1) >> (L - 1 - g);
           double acc[3][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
@@ -2612,7 +2646,8 @@ lc_status configure_kernels(lc_plan* p) {
     if (ea == cudaSuccess) ea = set_attrs_all<64>(smax);
     if (ea == cudaSuccess) ea = set_max_dyn_smem(lc_tile_kernel<0>, smax);
     if (ea == cudaSuccess) ea = set_max_dyn_smem(lc_tile_kernel<1>, smax);
-    if (ea == cudaSuccess) ea = set_max_dyn_smem(lc_up3_kernel, smax);
+    if (ea == cudaSuccess) ea = set_max_dyn_smem(lc_up3_kernel<32>, smax);
+    if (ea == cudaSuccess) ea = set_max_dyn_smem(lc_up3_kernel<64>, smax);
     if (ea == cudaSuccess) ea = set_max_dyn_smem(lc_range_kernel<0, 0>, smax);
     if (ea == cudaSuccess) ea = set_max_dyn_smem(lc_range_kernel<1, 0>, smax);
     if (ea == cudaSuccess) ea = set_max_dyn_smem(lc_range_kernel<0, 1>, smax);
@@ -2630,12 +2665,12 @@ lc_status configure_kernels(lc_plan* p) {
   int vt = p->vt;
   // automatic engine 3 (tools/engine_cross3.py on the B200): long vectors in batches of 8+ (>= 16 below
   // n = 2^18), deep enough trees for ranges of >= 64 leaves; e.g. 64 x 10^7: 41.8 -> 22.9 ms per transform
-  if (p->engine == 0 && p->part_count <= 1 && p->vt <= 0 && L >= 9 && p->s <= 32 && p->batch >= 8 &&
+  if (p->engine == 0 && p->part_count <= 1 && p->vt <= 0 && L >= 9 && p->s <= kTileSMax && p->batch >= 8 &&
       (p->batch >= 16 || p->n >= 262144) &&
       ((p->batch + kTileV - 1) / kTileV) < int64_t(p->sm_count))
     p->engine = 3;
   if (p->engine == 3) {  // up kernel of 8-vector tiles feeding the per-range pass
-    if (L < 1 || p->s > 32) return LC_ERR_INVALID_ARG;
+    if (L < 1 || p->s > kTileSMax) return LC_ERR_INVALID_ARG;
     vt = 8;
   }
   if (vt <= 0) vt = p->batch >= 2 ? 2 : 1;
@@ -2791,7 +2826,7 @@ lc_status configure_kernels(lc_plan* p) {
   {
     const int64_t ntiles8 = (p->batch + kTileV - 1) / kTileV;
     const int64_t tsm = L >= 1 ? tile_smem_doubles(L, s) * 8 : 0;
-    const bool tile_ok = L >= 1 && s <= 32 && tsm <= smax;
+    const bool tile_ok = L >= 1 && s <= kTileSMax && tsm <= smax;
     if (p->engine == 2 && !tile_ok) return LC_ERR_INVALID_ARG;
     if (p->engine == 3) {
       // the staged-M2L variant where three of its CTAs fit an SM, else the direct-load one
@@ -2834,7 +2869,10 @@ lc_status configure_kernels(lc_plan* p) {
         p->up3_kc = kc;
         p->smem_up = size_t(up3_smem_bytes(ku, s, kc));
         int uocc = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&uocc, lc_up3_kernel, kThreads, p->smem_up);
+        if (p->smax == 32)
+          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&uocc, lc_up3_kernel<32>, kThreads, p->smem_up);
+        else
+          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&uocc, lc_up3_kernel<64>, kThreads, p->smem_up);
         if (uocc < 1) return LC_ERR_INVALID_ARG;
         const int64_t nch = p->ntiles * ((int64_t(4) << p->grup) >> kc);
         const int64_t uslots = int64_t(uocc) * p->sm_count;
@@ -2968,7 +3006,7 @@ static lc_status launch_execute_impl(const lc_plan* p, const double* in, double*
   if (prev != p->device) cudaSetDevice(p->device);
   if (p->engine == 2) {
     TileParams tp{};
-    tp.in = in; tp.out = out; tp.A = p->d_A; tp.tabA = p->d_tabA; tp.tabB = p->d_tabB; tp.Tpad = p->d_Tpad;
+    tp.in = in; tp.out = out; tp.A = p->d_A; tp.tabA = p->d_tabA; tp.tabB = p->d_tabB; tp.Tpad = p->d_Tpad; tp.tpr = p->smax;
     tp.B = p->d_B; tp.ld_in = p->ld_in; tp.ld_out = p->ld_out; tp.n = p->n; tp.N = p->N; tp.batch = p->batch;
     tp.ntiles = p->ntiles; tp.layout = p->layout; tp.L = int(p->L); tp.s = int(p->s);
     tp.scratch = reinterpret_cast<double*>(ws);
@@ -3043,7 +3081,7 @@ static lc_status launch_execute_impl(const lc_plan* p, const double* in, double*
   const dim3 grid_down(unsigned(ndown), unsigned(p->ntiles));
   if (p->engine == 3) {
     TileParams tp{};
-    tp.in = in; tp.out = out; tp.A = p->d_A; tp.tabA = p->d_tabA; tp.tabB = p->d_tabB; tp.Tpad = p->d_Tpad;
+    tp.in = in; tp.out = out; tp.A = p->d_A; tp.tabA = p->d_tabA; tp.tabB = p->d_tabB; tp.Tpad = p->d_Tpad; tp.tpr = p->smax;
     tp.B = p->d_B; tp.ld_in = p->ld_in; tp.ld_out = p->ld_out; tp.n = p->n; tp.N = p->N; tp.batch = p->batch;
     tp.ntiles = p->ntiles; tp.layout = p->layout; tp.L = int(p->L); tp.s = int(p->s);
     tp.wg = w; tp.w_tile = p->w_tile_doubles; tp.nranges = p->range_n; tp.rlen = p->range_len;
@@ -3063,9 +3101,15 @@ static lc_status launch_execute_impl(const lc_plan* p, const double* in, double*
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = p->smem_up;
     cudaError_t e = cudaSuccess;
-    UpArgs<32> ua;
-    ua.p = up;
-    e = cudaLaunchKernelEx(&cfg, lc_up3_kernel, ua);
+    if (p->smax == 32) {
+      UpArgs<32> ua;
+      ua.p = up;
+      e = cudaLaunchKernelEx(&cfg, lc_up3_kernel<32>, ua);
+    } else {
+      UpArgs<64> ua;
+      ua.p = up;
+      e = cudaLaunchKernelEx(&cfg, lc_up3_kernel<64>, ua);
+    }
     if (e == cudaSuccess && ev && evi < nev) cudaEventRecord(ev[evi++], st);
     if (e == cudaSuccess) {
       cfg.gridDim = dim3(unsigned(p->tile_grid));

@@ -38,6 +38,12 @@ struct Geometry {
 // log2 of the leaf-segment alignment of a part (NEXT-2): 64 leaves (or all of them for short trees)
 inline int part_align_log2(int64_t L) { return int(L + 1 < 6 ? L + 1 : 6); }
 
+// Default s_hat (reading R17): s = ceil(n / 2^(L+2)) then lies in [s_hat/2, s_hat] = [20, 40],
+// within a factor sqrt(2) of the flop-optimal s = 29 of eq:totalnumflopsnew for every n
+// (s_hat = 32 keeps power-of-two n at s = 32, but lets s fall to 16: n = 10^7 gets s = 20, whose M2L work
+// and A_hat bytes per coefficient are twice those of s = 39).
+constexpr int64_t kSHatDefault = 40;
+
 // eq:numlevels; L clamped at 0 (band only) for n <= 4 s_hat.
 inline Geometry geometry(int64_t n, int64_t s_hat) {
   Geometry G{};
@@ -198,8 +204,9 @@ int64_t band_nnz(int64_t N, int64_t s);
 // engine 3's persistent up pass (lc_up3_kernel, 8 vectors, s <= 32): constants, two f buffers,
 // the subtree tree, kc waiting left siblings and two merged parents
 __host__ __device__ inline int64_t up3_smem_bytes(int k, int s, int kc) {
-  int64_t o = up_const_bytes(32);
-  o += 2 * align_up((int64_t(8) * (int64_t(1) << k) * up_fstride(s) + 2 * 32) * 8, 128);
+  const int smax = s <= 32 ? 32 : 64;
+  int64_t o = up_const_bytes(smax);
+  o += 2 * align_up((int64_t(8) * (int64_t(1) << k) * up_fstride(s) + 2 * smax) * 8, 128);
   o += ((int64_t(2) << k) - 1) * 2 * 8 * kM * 8;
   o += int64_t(kc + 2) * 2 * 8 * kM * 8;
   return o + 16;

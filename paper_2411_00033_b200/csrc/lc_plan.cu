@@ -349,7 +349,7 @@ lc_status lc_partition(int64_t n, int64_t s_hat, int32_t part_index, int32_t par
                        int64_t* row_hi) {
   if (n < 1 || !row_lo || !row_hi || part_count < 1 || part_index < 0 || part_index >= part_count)
     return LC_ERR_INVALID_ARG;
-  if (s_hat <= 0) s_hat = 32;
+  if (s_hat <= 0) s_hat = kSHatDefault;
   if (s_hat < 2 || s_hat > 64) return LC_ERR_INVALID_ARG;
   const Geometry G = geometry(n, s_hat);
   int64_t llo = 0, lhi = 0;
@@ -361,7 +361,7 @@ lc_status lc_partition(int64_t n, int64_t s_hat, int32_t part_index, int32_t par
 
 lc_status lc_geometry(int64_t n, int64_t s_hat, lc_plan_desc* out) {
   if (n < 1 || out == nullptr) return LC_ERR_INVALID_ARG;
-  if (s_hat <= 0) s_hat = 32;
+  if (s_hat <= 0) s_hat = kSHatDefault;
   if (s_hat < 2 || s_hat > 64) return LC_ERR_INVALID_ARG;
   std::memset(out, 0, sizeof(*out));
   const Geometry G = geometry(n, s_hat);
@@ -390,7 +390,7 @@ extern "C" lc_status lc_plan_create(lc_plan** out, int64_t n, lc_direction dir, 
   if (dir != LC_LEG2CHEB && dir != LC_CHEB2LEG) return LC_ERR_INVALID_ARG;
   lc_plan_opts o{};
   if (opts) o = *opts;
-  if (o.s_hat <= 0) o.s_hat = 32;
+  if (o.s_hat <= 0) o.s_hat = kSHatDefault;
   if (o.M <= 0) o.M = kM;
   if (o.M != kM || o.s_hat < 2 || o.s_hat > 64) return LC_ERR_INVALID_ARG;
   if (o.engine < 0 || o.engine > 3) return LC_ERR_INVALID_ARG;

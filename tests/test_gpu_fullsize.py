@@ -32,14 +32,15 @@ def _plan(*a, **k):
     return Plan(*a, **k)
 
 
-# (n, L, s): 1e6 -> L 13, s 31; 2^20 -> L 13, s 32; 4e6+17 -> L 15, s 31; 1e7 -> L 17, s 20
+# (n, L, s) at the default s_hat = 40: 1e6 -> L 13, s 31; 2^20 -> L 13, s 32; 4e6+17 -> L 15, s 31;
+# 1e7 -> L 16, s 39 (s_hat = 32: L 17, s 20)
 @pytest.mark.parametrize("kind", ["normal", "uniform_r0.5"])
-@pytest.mark.parametrize("n", [1_000_000, 1 << 20, 4_000_017, 10_000_000])
-def test_single_vector_nondecaying(n, kind):
+@pytest.mark.parametrize("n,s_hat", [(1_000_000, 0), (1 << 20, 0), (4_000_017, 0), (10_000_000, 0), (10_000_000, 32)])
+def test_single_vector_nondecaying(n, s_hat, kind):
     dev = _dev()
     f = vector(kind, n, seed=101)
     x = torch.from_numpy(f).reshape(1, -1).to(dev)
-    pl, pc = _plan(n, "leg2cheb", device=dev), _plan(n, "cheb2leg", device=dev)
+    pl, pc = _plan(n, "leg2cheb", device=dev, s_hat=s_hat), _plan(n, "cheb2leg", device=dev, s_hat=s_hat)
     assert pl.kernel_info["engine"] == 1
     s = pl.desc["s"]
     z = pl.execute(x)
@@ -54,14 +55,14 @@ def test_single_vector_nondecaying(n, kind):
 
 
 # engine 3 (8-vector tiles: up pass + per-range pass) on long non-decaying vectors
-@pytest.mark.parametrize("n,V,kind", [(2_000_000, 16, "normal"), (10_000_000, 8, "uniform_r0.5"),
-                                      (3_000_005, 11, "normal")])
-def test_engine3_long_vectors_nondecaying(n, V, kind):
+@pytest.mark.parametrize("n,V,kind,s_hat", [(2_000_000, 16, "normal", 0), (10_000_000, 8, "uniform_r0.5", 0),
+                                             (10_000_000, 8, "normal", 32), (3_000_005, 11, "normal", 0)])
+def test_engine3_long_vectors_nondecaying(n, V, kind, s_hat):
     dev = _dev()
     xh = batch(kind, n, V, seed=202)
     x = xh.to(dev)
-    pl = _plan(n, "leg2cheb", batch=V, device=dev, engine=3)
-    pc = _plan(n, "cheb2leg", batch=V, device=dev, engine=3)
+    pl = _plan(n, "leg2cheb", batch=V, device=dev, engine=3, s_hat=s_hat)
+    pc = _plan(n, "cheb2leg", batch=V, device=dev, engine=3, s_hat=s_hat)
     assert pl.kernel_info["engine"] == 3 and pc.kernel_info["engine"] == 3
     s = pl.desc["s"]
     z = pl.execute(x)
@@ -81,19 +82,20 @@ def test_engine3_long_vectors_nondecaying(n, V, kind):
 
 
 @pytest.mark.parametrize("engine", [1, 2, 3])
-@pytest.mark.parametrize("s_hat", [16, 24, 48, 64])
+@pytest.mark.parametrize("s_hat", [16, 24, 32, 48, 64])
 def test_s_hat_variants(engine, s_hat):
     """opts.s_hat in [2, 64] changes s, L and the band blocking (SMAX = 64 instantiations for s > 32);
-    engines 2 and 3 need s <= 32 and reject larger s at plan time."""
+    engines 2 and 3 take s <= 40 (5 row tiles) and reject larger s at plan time."""
+    from paper_2411_00033_b200 import geometry
     from paper_2411_00033_b200._lib import LegChebError
     dev = _dev()
-    for n, V in ((5000, 9), (70001, 8)):
+    for n, V in ((5000, 9), (70001, 8), (600, 9)):
         xh = batch("normal", n, V, seed=s_hat + n)
         try:
             pl = _plan(n, "leg2cheb", batch=V, device=dev, engine=engine, s_hat=s_hat)
             pc = _plan(n, "cheb2leg", batch=V, device=dev, engine=engine, s_hat=s_hat)
         except LegChebError:
-            assert engine in (2, 3) and s_hat > 32
+            assert engine in (2, 3) and geometry(n, s_hat)["s"] > 40
             continue
         s = pl.desc["s"]
         assert s_hat // 2 <= s <= s_hat or pl.desc["L"] == 0
@@ -104,6 +106,38 @@ def test_s_hat_variants(engine, s_hat):
             tag = f"s_hat={s_hat} engine={engine} n={n} s={s} L={pl.desc['L']}"
             check_rows("leg2cheb", xh[v].numpy(), z[v], rows, tag)
             check_rows("cheb2leg", xh[v].numpy(), w[v], rows, tag)
+
+
+# engines 2 and 3 at s in (32, 40] (row tile 4 of the band and of step 5; T(sigma) staged with 40 rows;
+# the up pass with the 64-row T copy and subtrees of 4 leaves packing two vectors per MMA item), against
+# engine 1 and the oracle, both directions, ragged tiles and tails; s = 33 / 36 / 39 / 40
+@pytest.mark.parametrize("engine", [1, 2, 3])
+@pytest.mark.parametrize("n,V", [(2105, 9), (9215, 16), (39836, 11), (163840, 8), (1_277_951, 8)])
+def test_s_above_32(engine, n, V):
+    from paper_2411_00033_b200._lib import LegChebError
+    dev = _dev()
+    xh = batch("normal", n, V, seed=n % 1000 + V)
+    x = xh.to(dev)
+    try:
+        pl = _plan(n, "leg2cheb", batch=V, device=dev, engine=engine)
+        pc = _plan(n, "cheb2leg", batch=V, device=dev, engine=engine)
+    except LegChebError:
+        assert engine == 3 and n < 100_000  # engine 3 wants L >= 1 and ranges; small cases may be refused
+        return
+    s, L = pl.desc["s"], pl.desc["L"]
+    assert 32 < s <= 40, s
+    assert pl.kernel_info["engine"] == engine
+    z = pl.execute(x)
+    w = pc.execute(x)
+    y = pc.execute(z)
+    torch.cuda.synchronize()
+    rows = np.arange(n) if n <= 10000 else c4_rows(n, s, uniform=512, tiles=32)
+    zh, wh, yh = z.cpu().numpy(), w.cpu().numpy(), y.cpu().numpy()
+    for v in sorted({0, V // 2, V - 1}):
+        tag = f"s>32 engine={engine} n={n} V={V} v={v} s={s} L={L}"
+        check_rows("leg2cheb", xh[v].numpy(), zh[v], rows, tag)
+        check_rows("cheb2leg", xh[v].numpy(), wh[v], rows, tag)
+        check_round_trip(xh[v].numpy(), yh[v], s, tag, BLOCK_RT_SIGNED)
 
 
 def test_planted_tail_block_error_is_caught():

@@ -27,9 +27,10 @@ def _plan(*a, **k):
     return Plan(*a, **k)
 
 
-# (n, V): n = 129 -> L = 1; 1500 -> s = 24, L = 4; 3900 -> s = 31 (odd); 4096 -> L = 5, s = 32;
-# 5000 -> L = 6, s = 20; 8192 -> L = 6; 20000 -> L = 8, s = 20
-CASES = [(129, 8), (200, 13), (1000, 9), (1500, 3), (3900, 17), (4096, 8), (5000, 11), (8192, 10), (20000, 5)]
+# (n, V) at the default s_hat = 40: n = 161 -> L = 1, s = 21; 1500 -> s = 24, L = 4; 3900 -> s = 31 (odd);
+# 4096 -> L = 5, s = 32; 5000 -> L = 5, s = 40; 8192 -> L = 6; 20000 -> L = 7, s = 40; 39836 -> s = 39
+CASES = [(161, 8), (200, 13), (1000, 9), (1500, 3), (3900, 17), (4096, 8), (5000, 11), (8192, 10), (20000, 5),
+         (39836, 9)]
 
 
 @pytest.mark.parametrize("direction", ["leg2cheb", "cheb2leg"])
@@ -129,7 +130,7 @@ def test_tile_engine_back_to_back_and_zero_vectors():
 # engine 3: up kernel (8-vector tiles) + the per-range pass; ranges split the leaves of each tile
 # (n = 100000 -> L = 10 with 8 levels of c in the global scratch)
 @pytest.mark.parametrize("direction", ["leg2cheb", "cheb2leg"])
-@pytest.mark.parametrize("n,V", [(129, 8), (1000, 9), (4096, 8), (20000, 5), (100000, 16)])
+@pytest.mark.parametrize("n,V", [(161, 8), (1000, 9), (4096, 8), (20000, 5), (39836, 9), (100000, 16)])
 def test_range_engine_vs_oracle(direction, n, V):
     dev = _dev()
     x = batch("normal_exp1000", n, V, seed=12)

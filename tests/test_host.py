@@ -51,15 +51,19 @@ def test_geometry_rejects_bad_arguments():
 
 
 # ---------------------------------------------------------------- decomposition
-@pytest.mark.parametrize("n,L,s,N", [(1000, 3, 32, 1024), (1024, 3, 32, 1024), (4096, 5, 32, 4096),
-                                     (10**6, 13, 31, 1015808), (1 << 20, 13, 32, 1 << 20),
-                                     (10**7, 17, 20, 10485760), (8192, 6, 32, 8192)])
-def test_geometry_eq_numlevels(n, L, s, N):
+@pytest.mark.parametrize("s_hat,n,L,s,N", [
+    (32, 1000, 3, 32, 1024), (32, 1024, 3, 32, 1024), (32, 4096, 5, 32, 4096), (32, 10**6, 13, 31, 1015808),
+    (32, 1 << 20, 13, 32, 1 << 20), (32, 10**7, 17, 20, 10485760), (32, 8192, 6, 32, 8192),
+    # the library default s_hat = 40 (R17): the BASELINE configs keep their s but for 10^7
+    (0, 1024, 3, 32, 1024), (0, 4096, 5, 32, 4096), (0, 8192, 6, 32, 8192), (0, 10**6, 13, 31, 1015808),
+    (0, 1 << 20, 13, 32, 1 << 20), (0, 10**7, 16, 39, 10223616), (0, 640, 2, 40, 640), (40, 641, 3, 21, 672)])
+def test_geometry_eq_numlevels(s_hat, n, L, s, N):
     from paper_2411_00033_b200 import geometry
-    g = geometry(n)
+    g = geometry(n, s_hat)
     assert (g["L"], g["s"], g["N"]) == (L, s, N)
     # eq:Ntot N = s 2^(L+2);  s in [s_hat/2, s_hat]
-    assert g["N"] == g["s"] << (g["L"] + 2) and 16 <= g["s"] <= 32
+    sh = s_hat or 40
+    assert g["N"] == g["s"] << (g["L"] + 2) and sh // 2 <= g["s"] <= sh
     # eq:total_blocks_and_mats: N_b = N/2s - L - 2, N_c = 3 N_b
     assert g["nc"] == 3 * (N // (2 * s) - L - 2)
     assert g["nc"] == 3 * sum((1 << (gg + 1)) - 1 for gg in range(L))  # eq:Nb summed
@@ -84,12 +88,13 @@ def test_j_end_spec_examples():
     assert [j_end(i, 32, 4096) for i in (0, 70, 130)] == [128, 192, 256]
 
 
-@pytest.mark.parametrize("n,s_expect", [(1024, 32), (2048, 32), (4096, 32), (640, 20), (1984, 31)])
-def test_exact_cover_of_submatrices_and_band(n, s_expect):
+@pytest.mark.parametrize("n,s_hat,s_expect", [(1024, 0, 32), (2048, 0, 32), (4096, 0, 32), (640, 32, 20),
+                                               (1984, 0, 31), (1300, 0, 21), (1200, 0, 38)])
+def test_exact_cover_of_submatrices_and_band(n, s_hat, s_expect):
     # every (i, j), j >= i, is covered exactly once: by the band (j < j_end(i)) or by exactly one
     # submatrix (g, b, r) with corners eq:globalij and size 2h_g
     from paper_2411_00033_b200 import geometry
-    g = geometry(n)
+    g = geometry(n, s_hat)
     L, s, N = g["L"], g["s"], g["N"]
     assert s == s_expect
     cover = np.zeros((N, N), dtype=np.int32)

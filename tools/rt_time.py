@@ -1,6 +1,6 @@
 """Round-trip time (leg2cheb then cheb2leg) of one batch, CUDA-graph replays timed per replay with
 events (median / min over `reps`), as bench.py times its step.  A/B builds: LC_LIB=liblegcheb_x.so.
-usage: python tools/rt_time.py n [batch] [reps]"""
+usage: [LC_S_HAT=..] [LC_ENGINE=..] python tools/rt_time.py n [batch] [reps]"""
 import os
 import sys
 
@@ -18,7 +18,12 @@ V = int(sys.argv[2]) if len(sys.argv) > 2 else 1
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 200
 dev = torch.device("cuda", 0)
 x = mkbatch("normal", n, V, seed=1).to(dev)
-pl, pc = Plan(n, "leg2cheb", batch=V, device=dev), Plan(n, "cheb2leg", batch=V, device=dev)
+kw = {}
+if os.environ.get("LC_S_HAT"):
+    kw["s_hat"] = int(os.environ["LC_S_HAT"])
+if os.environ.get("LC_ENGINE"):
+    kw["engine"] = int(os.environ["LC_ENGINE"])
+pl, pc = Plan(n, "leg2cheb", batch=V, device=dev, **kw), Plan(n, "cheb2leg", batch=V, device=dev, **kw)
 tmp, y = torch.empty_like(x), torch.empty_like(x)
 s = torch.cuda.Stream(dev)
 with torch.cuda.stream(s):
@@ -37,5 +42,5 @@ for a, b in ev:
 torch.cuda.synchronize()
 ts = sorted(a.elapsed_time(b) for a, b in ev)
 err = float((y - x).abs().max() / x.abs().max())
-print(f"{os.environ.get('LC_LIB', 'liblegcheb.so')} n={n} V={V}: round trip median {1e3 * ts[reps // 2]:.1f} us "
+print(f"{os.environ.get('LC_LIB', 'liblegcheb.so')} n={n} V={V} s={pl.desc['s']} L={pl.desc['L']} engine={pl.kernel_info.get('engine')}: round trip median {1e3 * ts[reps // 2]:.1f} us "
       f"min {1e3 * ts[0]:.1f} us  (per transform {1e3 * ts[reps // 2] / 2:.1f} us)  rt err {err:.1e}")
