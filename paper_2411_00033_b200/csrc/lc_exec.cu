@@ -1702,6 +1702,11 @@ __host__ __device__ inline int tile_fst(int s) { int f = 4; while (f < s) f += 8
 // with rows >= s zero (step 1 reads 4 ceil(s/4) of them)
 constexpr int kTileSMax = 40;
 __host__ __device__ inline int tile_trows(int s) { return s <= 32 ? 32 : kTileSMax; }
+// lambda window of a leaf step: the band of rows U reads lambda[(i+j)/2] at offsets r + c + sigma from
+// 2sU, at most (s + 6) + (2s + 2) + 1 for the rows and columns the band kernels touch (band_rows: the
+// highest started row tile has 8 rb < s, columns c < 4 ceil(s/2)); 3s + 10 instead of 4s leaves room
+// for four engine-3 CTAs per SM at s = 39
+__host__ __device__ inline int tile_lw(int s) { return (3 * s + 11) & ~1; }  // even: 16-byte aligned regions follow
 #ifndef LC_FRING
 #define LC_FRING 3  // leaf slots of the f / lambda ring (3: prefetch one leaf ahead; 4: two)
 #endif
@@ -1720,7 +1725,7 @@ __host__ __device__ inline int tile_gs(int L) { return (LC_TILE_SL == 0 || L <= 
 __host__ __device__ inline int64_t tile_smem_doubles(int L, int s) {
   const int fst = tile_fst(s);
   const int ns = L - tile_gs(L);  // levels in shared memory
-  return 2 * tile_trows(s) * kM + (kMM + 4) + 80 + LC_FRING * 2 * kTileV * fst + LC_FRING * 4 * s + int64_t(ns) * 3 * 2 * kTS +
+  return 2 * tile_trows(s) * kM + (kMM + 4) + 80 + LC_FRING * 2 * kTileV * fst + LC_FRING * tile_lw(s) + int64_t(ns) * 3 * 2 * kTS +
          int64_t(2 * ns + 1) * 2 * kTS + 2 * kTileV * (2 * s + 4) + kMM;
 }
 __host__ __device__ inline int64_t tile_scratch_doubles(int L) { return int64_t(tile_gs(L)) * 5 * 2 * kTS; }
@@ -1731,7 +1736,7 @@ __host__ __device__ inline int64_t tile_scratch_doubles(int L) { return int64_t(
 // 2 CTAs per SM and lose 10%)
 __host__ __device__ inline int64_t range_smem_doubles(int s, int stage) {
   const int fst = tile_fst(s);
-  return 2 * tile_trows(s) * kM + (kMM + 4) + 80 + LC_FRING * 2 * kTileV * fst + LC_FRING * 4 * s + int64_t(5) * 2 * kTS +
+  return 2 * tile_trows(s) * kM + (kMM + 4) + 80 + LC_FRING * 2 * kTileV * fst + LC_FRING * tile_lw(s) + int64_t(5) * 2 * kTS +
          2 * kTileV * (2 * s + 4) + (stage ? 4 * (2 * kMM + 2 * kTS) : 0);
 }
 #ifndef LC_RANGE_MINB
@@ -1926,14 +1931,14 @@ __global__ void __launch_bounds__(kTileThreads, LC_TILE_MINB) lc_tile_kernel(con
   double* lmr = fr + LC_FRING * 2 * kTileV * fst; // [LC_FRING][4s]
   const int gs = tile_gs(L);                      // levels >= gs in shared memory, below in scratch
   const int ns = L - gs;
-  double* wr = lmr + LC_FRING * 4 * s;            // [ns][3][2][8][M]
+  double* wr = lmr + LC_FRING * tile_lw(s);       // [ns][3][2][8][M]
   double* cs = wr + ns * 3 * 2 * kTS;             // levels gs..L-2: [2][2][8][M], then leaf [3][2][8][M]
   double* zs = cs + (2 * ns + 1) * 2 * kTS;       // [2][8][2s+4]
   double* Bqs = zs + 2 * kTileV * zst_;           // sign-folded B(0): (-1)^(n-k) b_nk (child 1 / parity 1)
   double* gw = P.scratch + int64_t(blockIdx.x) * tile_scratch_doubles(L);  // [gs][3][2][8][M]
   double* gc = gw + gs * 3 * 2 * kTS;                                       // [gs][2][2][8][M]
   auto fslot = [&](int U) { return fr + ((U + LC_FRING) % LC_FRING) * 2 * kTileV * fst; };  // U >= -1
-  auto lslot = [&](int U) { return lmr + ((U + LC_FRING) % LC_FRING) * 4 * s; };
+  auto lslot = [&](int U) { return lmr + ((U + LC_FRING) % LC_FRING) * tile_lw(s); };
   auto wslot = [&](int g, int t) {
     return g >= gs ? wr + ((g - gs) * 3 + t % 3) * 2 * kTS : gw + (g * 3 + t % 3) * 2 * kTS;
   };
@@ -1961,7 +1966,7 @@ __global__ void __launch_bounds__(kTileThreads, LC_TILE_MINB) lc_tile_kernel(con
   griddep_launch();
 
   // stage leaf segment U of the tile: f de-interleaved by parity ([sigma][v][m]), and the lambda
-  // (tabB) window [2sU, 2sU + 4s) that the band of rows U reads; zero beyond n / N
+  // (tabB) window [2sU, 2sU + 3s + 10) that the band of rows U reads (tile_lw); zero beyond N
   auto stage = [&](int64_t tile, int U) {
     double* fd = fslot(U);
     const int64_t j0 = int64_t(U) * seglen;
@@ -1982,7 +1987,7 @@ __global__ void __launch_bounds__(kTileThreads, LC_TILE_MINB) lc_tile_kernel(con
       }
     }
     double* ld = lslot(U);
-    for (int x = tid; x < 2 * seglen; x += kTileThreads) {
+    for (int x = tid; x < tile_lw(s); x += kTileThreads) {
       const bool ok = j0 + x < P.N;
       cp_async8(ld + x, ok ? P.tabB + j0 + x : P.tabB, ok ? 8u : 0u);
     }
@@ -2283,12 +2288,12 @@ __global__ void __launch_bounds__(kTileThreads, STAGE ? 3 : LC_RANGE_MINB) lc_ra
   double* taq = Bq + kMM + 4;                     // tabA [80]
   double* fr = taq + 80;                          // [LC_FRING][2][8][fst]
   double* lmr = fr + LC_FRING * 2 * kTileV * fst; // [LC_FRING][4s]
-  double* cs = lmr + LC_FRING * 4 * s;            // leaf level [3], level L-2 [2] x [2][8][M]
+  double* cs = lmr + LC_FRING * tile_lw(s);       // leaf level [3], level L-2 [2] x [2][8][M]
   double* zs = cs + 5 * 2 * kTS;                  // [2][8][2s+4]
   double* mbuf = zs + 2 * kTileV * (2 * s + 4);    // STAGE: [4 M2L warps][2 A_hat + 2 w]
   double* gc = P.scratch + int64_t(blockIdx.x) * range_scratch_doubles(L);  // levels < L-2: [L-2][2][2][8][M]
   auto fslot = [&](int U) { return fr + ((U + LC_FRING) % LC_FRING) * 2 * kTileV * fst; };  // U >= -1
-  auto lslot = [&](int U) { return lmr + ((U + LC_FRING) % LC_FRING) * 4 * s; };
+  auto lslot = [&](int U) { return lmr + ((U + LC_FRING) % LC_FRING) * tile_lw(s); };
   // w of every level comes from the up kernel (global workspace, read-only here)
   auto wglob = [&](int64_t tile, int g, int t, int sg) {
     return P.wg + tile * P.w_tile + (w_level_offset_units(g) + sg * nseg(g) + t) * kTS;
@@ -2313,7 +2318,7 @@ __global__ void __launch_bounds__(kTileThreads, STAGE ? 3 : LC_RANGE_MINB) lc_ra
   griddep_launch();
 
   // stage leaf segment U of the tile: f de-interleaved by parity ([sigma][v][m]), and the lambda
-  // (tabB) window [2sU, 2sU + 4s) that the band of rows U reads; zero beyond n / N
+  // (tabB) window [2sU, 2sU + 3s + 10) that the band of rows U reads (tile_lw); zero beyond N
   auto stage = [&](int64_t tile, int U) {
     if (STAGE && warp >= 4) return;  // the M2L warps' cp.async groups stay their own
     double* fd = fslot(U);
@@ -2338,7 +2343,7 @@ __global__ void __launch_bounds__(kTileThreads, STAGE ? 3 : LC_RANGE_MINB) lc_ra
       }
     }
     double* ld = lslot(U);
-    for (int x = tid; x < 2 * seglen; x += 32 * nstw) {
+    for (int x = tid; x < tile_lw(s); x += 32 * nstw) {
       const bool ok = j0 + x < P.N;
       cp_async8(ld + x, ok ? P.tabB + j0 + x : P.tabB, ok ? 8u : 0u);
     }
@@ -2477,12 +2482,15 @@ __global__ void __launch_bounds__(kTileThreads, STAGE ? 3 : LC_RANGE_MINB) lc_ra
       // ---- step 3 for the rows the next leaf enters: job k = (level gN + k/2, sigma k&1) on warp
       // 4, 5, 6, 7, 4, ...: c(u') = sum_r A_hat_r w(t_r), w from the up kernel's output (handing the
       // jobs past the first four to the band warps, as lc_tile_kernel does, measured 0.6% slower here)
-      if (warp >= 4 && U - 1 >= Ua) {
+      // s > 32 (all eight warps; per-warp cycle accounting, tools/tile_roles.py): jobs to warps
+      // 5, 4 (step 5), 0, 1 (band), 6, 7 (step-4 chain), 2, 3 (the longer band group), then around again
+      if ((warp >= 4 || s > 32) && U - 1 >= Ua) {
         const int gN = gentry(U - 1);
         const int nm2l = (L - gN) * 2;
-        // s > 32: jobs to warps 6, 7, 5, 4 (warps 4 and 5 carry step 5)
-        const int kpos = s > 32 ? (warp >= 6 ? warp - 6 : 7 - warp) : warp - 4;
-        for (int k = kpos; k < nm2l; k += 4) {
+        const int kpos = s > 32 ? (warp == 5 ? 0 : warp == 4 ? 1 : warp < 2 ? warp + 2 : warp >= 6 ? warp - 2 : warp + 4)
+                                : warp - 4;
+        const int kstep = s > 32 ? 8 : 4;
+        for (int k = kpos; k < nm2l; k += kstep) {
           const int g = gN + (k >> 1), sgk = k & 1;
           const int u = (U - 1) >> (L - 1 - g);
           double acc[3][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
