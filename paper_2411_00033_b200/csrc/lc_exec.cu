@@ -1707,6 +1707,10 @@ __host__ __device__ inline int tile_trows(int s) { return s <= 32 ? 32 : kTileSM
 // highest started row tile has 8 rb < s, columns c < 4 ceil(s/2)); 3s + 10 instead of 4s leaves room
 // for four engine-3 CTAs per SM at s = 39
 __host__ __device__ inline int tile_lw(int s) { return (3 * s + 11) & ~1; }  // even: 16-byte aligned regions follow
+#ifndef LC_SKIP
+#define LC_SKIP 0  // experiment builds only (tools): skip roles of the tile / range kernels (1 band, 2 step 5,
+                   // 4 step-4 chain / step 1 + M2M, 8 M2L, 16 staging) to find the one that bounds a leaf step
+#endif
 #ifndef LC_FRING
 #define LC_FRING 3  // leaf slots of the f / lambda ring (3: prefetch one leaf ahead; 4: two)
 #endif
@@ -2017,12 +2021,12 @@ __global__ void __launch_bounds__(kTileThreads, LC_TILE_MINB) lc_tile_kernel(con
     TP_DECL
     for (int U = nls - 1; U >= -1; --U) {
       // prefetch distance: two leaves with a ring of 4, one leaf (a whole step to land) with 3
-      if (LC_FRING == 4 ? U >= 2 : U >= 1) stage(tile, LC_FRING == 4 ? U - 2 : U - 1);
+      if (!(LC_SKIP & 16) && (LC_FRING == 4 ? U >= 2 : U >= 1)) stage(tile, LC_FRING == 4 ? U - 2 : U - 1);
       cp_async_commit();
       TP_MARK(5);
       const int V1 = U + 1;  // the leaf whose step 5 / step 2 run in this step
       if (warp < 4) {
-        if (U >= 0 && 8 * ((warp >> 1) ? 1 : 0) < s) {
+        if (!(LC_SKIP & 1) && U >= 0 && 8 * ((warp >> 1) ? 1 : 0) < s) {
           // ---- step 6: rows i = 2sU + 2r + sigma, columns j = 2sU + 2c + sigma (c >= r, j < j_end),
           // K[r][c] = a[c-r] b[(i+j)/2] formed per lane, G[c][v] = f_v[j] (C2L: j f_j); two or three
           // row tiles per warp (one accumulator chain each)
@@ -2080,7 +2084,7 @@ __global__ void __launch_bounds__(kTileThreads, LC_TILE_MINB) lc_tile_kernel(con
         }
         TP_MARK(0);
         // ---- step 5 + 7 of leaf V1, row tile = warp (and 4 on warp 0 for s > 32), both parities
-        if (V1 < nls)
+        if (!(LC_SKIP & 2) && V1 < nls)
           for (int mt = warp; 8 * mt < s; mt += 4)
             step5_store<DIR>(P, Tq, TR, cslot(L - 1, V1), zbuf(V1), zst_, tile, int64_t(V1) * seglen, mt, s, lr, lc, v2ok);
       } else {
@@ -2160,7 +2164,7 @@ __global__ void __launch_bounds__(kTileThreads, LC_TILE_MINB) lc_tile_kernel(con
               u >>= 1;
             }
           }
-        } else if (U >= 0) {
+        } else if (!(LC_SKIP & 4) && U >= 0) {
           // ---- step 4 chain (sigma) over the levels entered at U, coarse to fine
           const int gA = gmin_of(U);
           for (int g = (gA > 0 ? gA : 1); g < L; ++g) {
@@ -2198,7 +2202,7 @@ __global__ void __launch_bounds__(kTileThreads, LC_TILE_MINB) lc_tile_kernel(con
       const int m2l_pos = warp >= 6 ? warp - 6 : (warp >= 4 ? warp - 2 : warp + 4);
       // ---- step 3 for the rows the next leaf enters: job k = (level gN + k/2, sigma k&1) on warp
       // 6, 7, 4, 5, 0, 1, 2, 3, 6, ...: c(u') = sum_r A_hat_r w(t_r)
-      if (U >= 1) {
+      if (!(LC_SKIP & 8) && U >= 1) {
         const int gN = gmin_of(U - 1);
         const int nm2l = (L - gN) * 2;
         for (int k = m2l_pos; k < nm2l; k += 8) {
@@ -2371,13 +2375,13 @@ __global__ void __launch_bounds__(kTileThreads, STAGE ? 3 : LC_RANGE_MINB) lc_ra
 
     TP_DECL
     for (int U = Ub + 1; U >= Ua - 1; --U) {
-      if (U - 1 >= Ua) stage(tile, U - 1);  // one leaf ahead (a whole step to land)
+      if (!(LC_SKIP & 16) && U - 1 >= Ua) stage(tile, U - 1);  // one leaf ahead (a whole step to land)
       cp_async_commit();
       TP_MARK(5);
       const int V1 = U + 1;  // the leaf whose step 5 runs in this step
       const bool inU = U >= Ua && U <= Ub;
       if (warp < 4) {
-        if (inU && 8 * ((warp >> 1) ? 1 : 0) < s) {
+        if (!(LC_SKIP & 1) && inU && 8 * ((warp >> 1) ? 1 : 0) < s) {
           // ---- step 6: rows i = 2sU + 2r + sigma, columns j = 2sU + 2c + sigma (c >= r, j < j_end),
           // K[r][c] = a[c-r] b[(i+j)/2] formed per lane, G[c][v] = f_v[j] (C2L: j f_j); two or three
           // row tiles per warp (one accumulator chain each)
@@ -2435,16 +2439,16 @@ __global__ void __launch_bounds__(kTileThreads, STAGE ? 3 : LC_RANGE_MINB) lc_ra
         }
         TP_MARK(0);
         // ---- step 5 + 7 of leaf V1, row tile = warp, both parities (s > 32: on warps 4 and 5, below)
-        if (s <= 32 && V1 >= Ua && V1 <= Ub && 8 * warp < s)
+        if (!(LC_SKIP & 2) && s <= 32 && V1 >= Ua && V1 <= Ub && 8 * warp < s)
           step5_store<DIR>(P, Tq, TR, cslot(L - 1, V1), zbuf(V1), zst_, tile, int64_t(V1) * seglen, warp, s, lr, lc, v2ok);
       } else {
         const int sg = warp & 1;
         // s in (32, 40]: the band warps carry five row tiles, so step 5 + 7 of leaf V1 (its c and z
         // slots are not written in this step) runs on warps 4 and 5: row tiles {0, 2, 4} and {1, 3}
-        if (s > 32 && warp < 6 && V1 >= Ua && V1 <= Ub)
+        if (!(LC_SKIP & 2) && s > 32 && warp < 6 && V1 >= Ua && V1 <= Ub)
           for (int mt = warp - 4; 8 * mt < s; mt += 2)
             step5_store<DIR>(P, Tq, TR, cslot(L - 1, V1), zbuf(V1), zst_, tile, int64_t(V1) * seglen, mt, s, lr, lc, v2ok);
-        if (warp >= 6 && inU) {
+        if (!(LC_SKIP & 4) && warp >= 6 && inU) {
           // ---- step 4 chain (sigma) over the levels entered at U, coarse to fine
           const int gA = gentry(U);
           for (int g = (gA > 0 ? gA : 1); g < L; ++g) {
@@ -2484,7 +2488,7 @@ __global__ void __launch_bounds__(kTileThreads, STAGE ? 3 : LC_RANGE_MINB) lc_ra
       // jobs past the first four to the band warps, as lc_tile_kernel does, measured 0.6% slower here)
       // s > 32 (all eight warps; per-warp cycle accounting, tools/tile_roles.py): jobs to warps
       // 5, 4 (step 5), 0, 1 (band), 6, 7 (step-4 chain), 2, 3 (the longer band group), then around again
-      if ((warp >= 4 || s > 32) && U - 1 >= Ua) {
+      if (!(LC_SKIP & 8) && (warp >= 4 || s > 32) && U - 1 >= Ua) {
         const int gN = gentry(U - 1);
         const int nm2l = (L - gN) * 2;
         const int kpos = s > 32 ? (warp == 5 ? 0 : warp == 4 ? 1 : warp < 2 ? warp + 2 : warp >= 6 ? warp - 2 : warp + 4)
