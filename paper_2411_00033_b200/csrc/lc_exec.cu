@@ -1702,6 +1702,10 @@ __host__ __device__ inline int tile_fst(int s) { int f = 4; while (f < s) f += 8
 // with rows >= s zero (step 1 reads 4 ceil(s/4) of them)
 constexpr int kTileSMax = 40;
 __host__ __device__ inline int tile_trows(int s) { return s <= 32 ? 32 : kTileSMax; }
+// the per-tile kernel stages T(sigma) transposed, [2][M][tile_tstride(s)] (row stride 4 or 12 mod 16
+// doubles): the A fragments of step 1 (T^T, rows = modes) and of step 5 (T, rows = positions) then hit 16
+// distinct bank pairs per half warp (the [m][M] layout's stride 18 gives 2-way conflicts on both)
+__host__ __device__ inline int tile_tstride(int s) { return s <= 32 ? 36 : 44; }
 // lambda window of a leaf step: the band of rows U reads lambda[(i+j)/2] at offsets r + c + sigma from
 // 2sU, at most (s + 6) + (2s + 2) + 1 for the rows and columns the band kernels touch (band_rows: the
 // highest started row tile has 8 rb < s, columns c < 4 ceil(s/2)); 3s + 10 instead of 4s leaves room
@@ -1729,7 +1733,7 @@ __host__ __device__ inline int tile_gs(int L) { return (LC_TILE_SL == 0 || L <= 
 __host__ __device__ inline int64_t tile_smem_doubles(int L, int s) {
   const int fst = tile_fst(s);
   const int ns = L - tile_gs(L);  // levels in shared memory
-  return 2 * tile_trows(s) * kM + (kMM + 4) + 80 + LC_FRING * 2 * kTileV * fst + LC_FRING * tile_lw(s) + int64_t(ns) * 3 * 2 * kTS +
+  return 2 * kM * tile_tstride(s) + (kMM + 4) + 80 + LC_FRING * 2 * kTileV * fst + LC_FRING * tile_lw(s) + int64_t(ns) * 3 * 2 * kTS +
          int64_t(2 * ns + 1) * 2 * kTS + 2 * kTileV * (2 * s + 4) + kMM;
 }
 __host__ __device__ inline int64_t tile_scratch_doubles(int L) { return int64_t(tile_gs(L)) * 5 * 2 * kTS; }
@@ -1867,7 +1871,7 @@ __device__ __forceinline__ void band32(const double* __restrict__ fU, const doub
 // T(sigma)[m][k] c(L-1, V1)[sigma][v][k] (cc = c(L-1, V1), [sigma][v][k]), then C^{-1} (step 7) and the
 // store: a lane holds rows i0 + 2m and i0 + 2m + 1 of vectors 2 lc and 2 lc + 1, written as one 16-byte
 // store where the output layout allows it (v2ok)
-template <int DIR>
+template <int DIR, bool TT>
 __device__ __forceinline__ void step5_store(const TileParams& P, const double* __restrict__ Tq, int tr,
                                             const double* __restrict__ cc, const double* __restrict__ zb, int zst,
                                             int64_t tile, int64_t i0, int mt, int s, int lr, int lc, bool v2ok) {
@@ -1879,7 +1883,8 @@ __device__ __forceinline__ void step5_store(const TileParams& P, const double* _
 #pragma unroll
     for (int sg = 0; sg < 2; ++sg) {
       const double bb = k < kM ? cc[sg * kTS + lr * kM + k] : 0.0;
-      const double a = k < kM ? Tq[(sg * tr + m) * kM + k] : 0.0;
+      // T(sigma)[m][k]: [2][tr][M] (TT = false) or transposed [2][M][tr] (TT = true)
+      const double a = k < kM ? (TT ? Tq[(sg * kM + k) * tr + m] : Tq[(sg * tr + m) * kM + k]) : 0.0;
       dmma(acc[sg], a, bb);
     }
   }
@@ -1927,9 +1932,9 @@ __global__ void __launch_bounds__(kTileThreads, LC_TILE_MINB) lc_tile_kernel(con
   const int s = P.s, L = P.L, seglen = 2 * s;
   const int fst = tile_fst(s), zst_ = 2 * s + 4;
   const int nls = 2 << L;  // leaf segments
-  const int TR = tile_trows(s);
-  double* Tq = reinterpret_cast<double*>(smem);  // [2][TR][M]
-  double* Bq = Tq + 2 * TR * kM;                  // B(0) [M][M]
+  const int TS = tile_tstride(s);
+  double* Tq = reinterpret_cast<double*>(smem);  // T(sigma) transposed: [2][M][TS]
+  double* Bq = Tq + 2 * kM * TS;                  // B(0) [M][M]
   double* taq = Bq + kMM + 4;                     // tabA [80]
   double* fr = taq + 80;                          // [LC_FRING][2][8][fst]
   double* lmr = fr + LC_FRING * 2 * kTileV * fst; // [LC_FRING][4s]
@@ -1952,9 +1957,9 @@ __global__ void __launch_bounds__(kTileThreads, LC_TILE_MINB) lc_tile_kernel(con
   };
   auto zbuf = [&](int U) { return zs + (U & 1) * kTileV * zst_; };
 
-  for (int i = tid; i < TR * kM; i += kTileThreads) {  // [2][TR][M] from [2][tpr][M]: TR * M / 2 pairs per parity
-    const int sg = i >= TR * kM / 2 ? 1 : 0, j = i - sg * (TR * kM / 2);
-    cp_async16(Tq + sg * TR * kM + 2 * j, P.Tpad + int64_t(sg) * P.tpr * kM + 2 * j);
+  for (int i = tid; i < 2 * kM * TS; i += kTileThreads) {  // [2][M][TS] from [2][tpr][M] (rows m >= s are zero)
+    const int sg = i / (kM * TS), r = i - sg * kM * TS, k = r / TS, m = r - k * TS;
+    Tq[i] = m < P.tpr ? __ldg(P.Tpad + (int64_t(sg) * P.tpr + m) * kM + k) : 0.0;
   }
   for (int i = tid; i < kMM / 2; i += kTileThreads) cp_async16(Bq + 2 * i, P.B + 2 * i);
   for (int i = tid; i < 80; i += kTileThreads) taq[i] = i < seglen ? P.tabA[i] : 0.0;
@@ -2086,24 +2091,24 @@ __global__ void __launch_bounds__(kTileThreads, LC_TILE_MINB) lc_tile_kernel(con
         // ---- step 5 + 7 of leaf V1, row tile = warp (and 4 on warp 0 for s > 32), both parities
         if (!(LC_SKIP & 2) && V1 < nls)
           for (int mt = warp; 8 * mt < s; mt += 4)
-            step5_store<DIR>(P, Tq, TR, cslot(L - 1, V1), zbuf(V1), zst_, tile, int64_t(V1) * seglen, mt, s, lr, lc, v2ok);
+            step5_store<DIR, true>(P, Tq, TS, cslot(L - 1, V1), zbuf(V1), zst_, tile, int64_t(V1) * seglen, mt, s, lr, lc, v2ok);
       } else {
         const int sg = warp & 1;
         if (warp < 6) {
           if (U >= 0) {
             // ---- step 1: w(L-1, U)[sigma][v][mode] = sum_m T(sigma)[m][mode] f_v[2sU + 2m + sigma]
             const double* fv = fslot(U) + (sg * kTileV + lr) * fst;
-            const double* Tm = Tq + sg * TR * kM;
+            const double* Tm = Tq + sg * kM * TS;  // T(sigma)^T: [mode][TS]
             double acc[3][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
             if (s == 32) {  // compile-time K: immediate offsets, no loop control
               const double* fq = fv + lc;
-              const double* tq = Tm + lc * kM + lr;
+              const double* tq = Tm + lr * TS + lc;
 #pragma unroll
               for (int kk = 0; kk < 8; ++kk) {
                 const double bb = fq[4 * kk];
 #pragma unroll
                 for (int mt = 0; mt < 3; ++mt)
-                  dmma(acc[mt], (mt < 2 || lr < 2) ? tq[4 * kk * kM + 8 * mt] : 0.0, bb);
+                  dmma(acc[mt], (mt < 2 || lr < 2) ? tq[8 * mt * TS + 4 * kk] : 0.0, bb);
               }
             } else {
               const int nks = (s + 3) >> 2;
@@ -2113,7 +2118,7 @@ __global__ void __launch_bounds__(kTileThreads, LC_TILE_MINB) lc_tile_kernel(con
 #pragma unroll
                 for (int mt = 0; mt < 3; ++mt) {
                   const int mode = 8 * mt + lr;
-                  dmma(acc[mt], mode < kM ? Tm[m * kM + mode] : 0.0, bb);
+                  dmma(acc[mt], mode < kM ? Tm[mode * TS + m] : 0.0, bb);
                 }
               }
             }
@@ -2440,14 +2445,14 @@ __global__ void __launch_bounds__(kTileThreads, STAGE ? 3 : LC_RANGE_MINB) lc_ra
         TP_MARK(0);
         // ---- step 5 + 7 of leaf V1, row tile = warp, both parities (s > 32: on warps 4 and 5, below)
         if (!(LC_SKIP & 2) && s <= 32 && V1 >= Ua && V1 <= Ub && 8 * warp < s)
-          step5_store<DIR>(P, Tq, TR, cslot(L - 1, V1), zbuf(V1), zst_, tile, int64_t(V1) * seglen, warp, s, lr, lc, v2ok);
+          step5_store<DIR, false>(P, Tq, TR, cslot(L - 1, V1), zbuf(V1), zst_, tile, int64_t(V1) * seglen, warp, s, lr, lc, v2ok);
       } else {
         const int sg = warp & 1;
         // s in (32, 40]: the band warps carry five row tiles, so step 5 + 7 of leaf V1 (its c and z
         // slots are not written in this step) runs on warps 4 and 5: row tiles {0, 2, 4} and {1, 3}
         if (!(LC_SKIP & 2) && s > 32 && warp < 6 && V1 >= Ua && V1 <= Ub)
           for (int mt = warp - 4; 8 * mt < s; mt += 2)
-            step5_store<DIR>(P, Tq, TR, cslot(L - 1, V1), zbuf(V1), zst_, tile, int64_t(V1) * seglen, mt, s, lr, lc, v2ok);
+            step5_store<DIR, false>(P, Tq, TR, cslot(L - 1, V1), zbuf(V1), zst_, tile, int64_t(V1) * seglen, mt, s, lr, lc, v2ok);
         if (!(LC_SKIP & 4) && warp >= 6 && inU) {
           // ---- step 4 chain (sigma) over the levels entered at U, coarse to fine
           const int gA = gentry(U);
