@@ -172,6 +172,8 @@ struct UpParams {
   int phase;    // host side: -1 whole execution; partitioned up pass: 0 the up kernel, 1 coarse levels + rest
   int contonly; // partitioned up pass, phase 1: only the continuation, from groups of the (exchanged) roots
   int kc;       // engine 3 (lc_up3_kernel): subtrees per chunk = 2^kc
+  int nbuf;     // engine 3: f buffers of the up pass (1 or 2)
+  int tpr;      // rows per parity of Tpad (32 or 64)
   int64_t ntiles;
   double* w;
   int* cnt;
@@ -591,17 +593,21 @@ __global__ void __launch_bounds__(kThreads, 2) lc_up3_kernel(const __grid_consta
   const int nleaf = 1 << k, seglen = 2 * s;
   const int64_t VM = int64_t(VT) * kM;
   const int64_t fbuf = align_up((int64_t(VT) * nleaf * fst + 2 * SMAX) * 8, 128) / 8;  // doubles per f buffer
+  const int nbuf = P.nbuf;                         // 2: double-buffered f; 1: the next f lands during M2M
   double* Ts = reinterpret_cast<double*>(smem);  // [2][SMAX][M], zero rows m >= s
   double* Bs = Ts + 2 * SMAX * kM;               // B(0) [M][M]
-  double* fs0 = reinterpret_cast<double*>(smem + up_const_bytes(SMAX));  // 2 x [v][leaf][fst] + zero tail
-  double* tree = fs0 + 2 * fbuf;
+  double* fs0 = reinterpret_cast<double*>(smem + up_const_bytes(SMAX));  // nbuf x [v][leaf][fst] + zero tail
+  double* tree = fs0 + nbuf * fbuf;
   auto tree_off = [&](int j) { return ((1 << j) - 1) * 2 * VT * kM; };
   double* pend = tree + tree_off(k + 1);  // [kc][2][VT][M]: left siblings waiting, by level
   double* cur = pend + P.kc * 2 * VM;     // [2][2][VT][M]: merged parents (ping-pong)
 
-  for (int i = tid; i < SMAX * kM; i += blockDim.x) cp_async16(Ts + 2 * i, P.Tpad + 2 * i);
+  for (int i = tid; i < SMAX * kM; i += blockDim.x) {  // [2][SMAX][M] from [2][tpr][M]: SMAX M / 2 pairs per parity
+    const int sg = i >= SMAX * kM / 2 ? 1 : 0, jj = i - sg * (SMAX * kM / 2);
+    cp_async16(Ts + sg * SMAX * kM + 2 * jj, P.Tpad + int64_t(sg) * P.tpr * kM + 2 * jj);
+  }
   for (int i = tid; i < kMM / 2; i += blockDim.x) cp_async16(Bs + 2 * i, P.B + 2 * i);
-  for (int b = 0; b < 2; ++b) {  // zero tail and segment padding of both buffers (never written by cp.async)
+  for (int b = 0; b < nbuf; ++b) {  // zero tail and segment padding of the buffers (never written by cp.async)
     double* fs = fs0 + b * fbuf;
     for (int x = tid; x < 2 * SMAX; x += blockDim.x) fs[VT * nleaf * fst + x] = 0.0;
     if (fst > seglen)
@@ -662,16 +668,22 @@ __global__ void __launch_bounds__(kThreads, 2) lc_up3_kernel(const __grid_consta
   for (int64_t j = 0; j < J; ++j) {
     int64_t tile, R;
     locate(j, tile, R);
-    if (j + 1 < J) {
+    if (nbuf == 2 && j + 1 < J) {
       int64_t t1, r1;
       locate(j + 1, t1, r1);
       stage(fs0 + ((j + 1) & 1) * fbuf, r1, t1);
     }
     cp_async_commit();
-    cp_async_wait<1>();  // the f of subtree j landed
+    if (nbuf == 2) cp_async_wait<1>(); else cp_async_wait<0>();  // the f of subtree j landed
     __syncthreads();
-    up_step1<VT, SMAX>(Ts, fs0 + (j & 1) * fbuf, fst, nleaf, s, tree + tree_off(k));
+    up_step1<VT, SMAX>(Ts, fs0 + (nbuf == 2 ? (j & 1) * fbuf : 0), fst, nleaf, s, tree + tree_off(k));
     __syncthreads();
+    if (nbuf == 1 && j + 1 < J) {  // one buffer: the next subtree's f lands during this one's M2M and stores
+      int64_t t1, r1;
+      locate(j + 1, t1, r1);
+      stage(fs0, r1, t1);
+      cp_async_commit();
+    }
     double* wt = P.w + tile * P.w_tile;
     auto store_w = [&](int g, int64_t node, int cnt, const double* src) {  // cnt nodes of level g, [sigma][cnt][v][M]
       const int c2 = int(cnt * VM / 2);
@@ -2664,7 +2676,7 @@ lc_status configure_kernels(lc_plan* p) {
     if (ea == cudaSuccess) ea = set_max_dyn_smem(lc_tile_kernel<0>, smax);
     if (ea == cudaSuccess) ea = set_max_dyn_smem(lc_tile_kernel<1>, smax);
     if (ea == cudaSuccess) ea = set_max_dyn_smem(lc_up3_kernel<32>, smax);
-    if (ea == cudaSuccess) ea = set_max_dyn_smem(lc_up3_kernel<64>, smax);
+    if (ea == cudaSuccess) ea = set_max_dyn_smem(lc_up3_kernel<40>, smax);
     if (ea == cudaSuccess) ea = set_max_dyn_smem(lc_range_kernel<0, 0>, smax);
     if (ea == cudaSuccess) ea = set_max_dyn_smem(lc_range_kernel<1, 0>, smax);
     if (ea == cudaSuccess) ea = set_max_dyn_smem(lc_range_kernel<0, 1>, smax);
@@ -2871,25 +2883,37 @@ lc_status configure_kernels(lc_plan* p) {
       p->range_len = int(rlen);
       p->smem_tile = rsm;
       p->tile_grid = int(std::min<int64_t>(p->ntiles * nr, slots));
-      // persistent up pass: subtrees of 2^kup leaves (two CTAs per SM), chunks of 2^kc subtrees
+      // persistent up pass: subtrees of 2^kup leaves (two CTAs per SM), chunks of 2^kc subtrees; the
+      // largest subtree (<= 8 leaves) that fits two CTAs per SM, double-buffered f if that fits too
+      // (s = 39: 8 leaves single-buffered, 4.18 -> ... ms at cfg4, instead of 4 leaves double-buffered)
       {
         int ku = std::max(0, std::min(p->kup, 3));
+        int nbuf = 2;
         int kc = std::min(6, L - 1 - ku);
-        while (ku > 0 && up3_smem_bytes(ku, s, kc) > budget2) {
-          --ku;
+        int force_nbuf = 0;
+        if (const char* e = std::getenv("LC_UP3_NBUF")) force_nbuf = std::atoi(e);
+        for (;;) {
           kc = std::min(6, L - 1 - ku);
+          if (force_nbuf != 1 && up3_smem_bytes(ku, s, kc, 2) <= budget2) { nbuf = 2; break; }
+          if (force_nbuf != 2 && up3_smem_bytes(ku, s, kc, 1) <= budget2) { nbuf = 1; break; }
+          if (ku == 0) { nbuf = 1; break; }
+          --ku;
         }
-        if (up3_smem_bytes(ku, s, kc) > smax) return LC_ERR_INVALID_ARG;
+        // chunks of 2^kc subtrees, but at least two chunks per SM where the tree allows (small batches
+        // of shorter vectors: 16 x 3e5 had 16 chunks for 148 SMs at kc = 6)
+        while (kc > 0 && p->ntiles * (int64_t(4) << (L - 1 - ku - kc)) < 2 * int64_t(p->sm_count)) --kc;
+        if (up3_smem_bytes(ku, s, kc, nbuf) > smax) return LC_ERR_INVALID_ARG;
         p->kup = ku;
         p->grup = L - 1 - ku;
         p->group = std::max(ku, 1);
         p->up3_kc = kc;
-        p->smem_up = size_t(up3_smem_bytes(ku, s, kc));
+        p->up3_nbuf = nbuf;
+        p->smem_up = size_t(up3_smem_bytes(ku, s, kc, nbuf));
         int uocc = 0;
-        if (p->smax == 32)
+        if (s <= 32)
           cudaOccupancyMaxActiveBlocksPerMultiprocessor(&uocc, lc_up3_kernel<32>, kThreads, p->smem_up);
         else
-          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&uocc, lc_up3_kernel<64>, kThreads, p->smem_up);
+          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&uocc, lc_up3_kernel<40>, kThreads, p->smem_up);
         if (uocc < 1) return LC_ERR_INVALID_ARG;
         const int64_t nch = p->ntiles * ((int64_t(4) << p->grup) >> kc);
         const int64_t uslots = int64_t(uocc) * p->sm_count;
@@ -3062,6 +3086,8 @@ static lc_status launch_execute_impl(const lc_plan* p, const double* in, double*
   up.phase = phase;
   up.contonly = 0;
   up.kc = p->up3_kc;
+  up.nbuf = p->up3_nbuf;
+  up.tpr = p->smax;
   up.ntiles = p->ntiles;
   up.w = w; up.cnt = cnt; up.flags = flags; up.w_tile = p->w_tile_doubles; up.cnt_tile = p->cnt_tile_ints;
   StreamParams sp{};
@@ -3118,14 +3144,14 @@ static lc_status launch_execute_impl(const lc_plan* p, const double* in, double*
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = p->smem_up;
     cudaError_t e = cudaSuccess;
-    if (p->smax == 32) {
+    if (p->s <= 32) {
       UpArgs<32> ua;
       ua.p = up;
       e = cudaLaunchKernelEx(&cfg, lc_up3_kernel<32>, ua);
     } else {
-      UpArgs<64> ua;
+      UpArgs<40> ua;
       ua.p = up;
-      e = cudaLaunchKernelEx(&cfg, lc_up3_kernel<64>, ua);
+      e = cudaLaunchKernelEx(&cfg, lc_up3_kernel<40>, ua);
     }
     if (e == cudaSuccess && ev && evi < nev) cudaEventRecord(ev[evi++], st);
     if (e == cudaSuccess) {

@@ -126,6 +126,7 @@ struct lc_plan {
   // kernel configuration
   int vt, k, gr, bps, nst, group, kup, grup, kb;
   int smax;            // 32 or 64: rows of the padded copy of T(sigma)
+  int up3_nbuf;        // engine 3: f buffers of the up pass
   int lvorder[32];     // M2L level order of the streaming kernel
   double* h_Tpad;      // host [2][smax][M] copy of T(sigma), zero rows m >= s (kernel parameter)
   double* d_Tpad;      // device copy of h_Tpad
@@ -203,10 +204,11 @@ double* plan_stage(const lc_plan* p);
 int64_t band_nnz(int64_t N, int64_t s);
 // engine 3's persistent up pass (lc_up3_kernel, 8 vectors, s <= 32): constants, two f buffers,
 // the subtree tree, kc waiting left siblings and two merged parents
-__host__ __device__ inline int64_t up3_smem_bytes(int k, int s, int kc) {
-  const int smax = s <= 32 ? 32 : 64;
+// (T(sigma) staged with 32 rows for s <= 32, else 40: engines 2 / 3 take s <= 40)
+__host__ __device__ inline int64_t up3_smem_bytes(int k, int s, int kc, int nbuf) {
+  const int smax = s <= 32 ? 32 : 40;
   int64_t o = up_const_bytes(smax);
-  o += 2 * align_up((int64_t(8) * (int64_t(1) << k) * up_fstride(s) + 2 * smax) * 8, 128);
+  o += nbuf * align_up((int64_t(8) * (int64_t(1) << k) * up_fstride(s) + 2 * smax) * 8, 128);
   o += ((int64_t(2) << k) - 1) * 2 * 8 * kM * 8;
   o += int64_t(kc + 2) * 2 * 8 * kM * 8;
   return o + 16;
