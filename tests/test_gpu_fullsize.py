@@ -164,3 +164,25 @@ def test_planted_tail_block_error_is_caught():
     assert blockwise_einf(y[v], xh[v].numpy(), 2 * s) > BLOCK_RT
     # and the untouched vectors still pass
     check_round_trip(xh[4].numpy(), y[4], s, "planted-neighbour", BLOCK_RT_SIGNED)
+
+
+# the engine-3 up pass with one f buffer (8-leaf subtrees at s > 32 when two double-buffered CTAs do not
+# fit) and with two (forced by LC_UP3_NBUF, read at plan creation): bit-identical results, oracle rows
+@pytest.mark.parametrize("n,V", [(1_277_951, 8), (400_001, 16), (2_000_000, 9)])
+def test_engine3_up_pass_buffering(n, V, monkeypatch):
+    dev = _dev()
+    xh = batch("normal", n, V, seed=31 + V)
+    x = xh.to(dev)
+    outs, infos = {}, {}
+    for nbuf in ("1", "2"):
+        monkeypatch.setenv("LC_UP3_NBUF", nbuf)
+        p = _plan(n, "leg2cheb", batch=V, device=dev, engine=3)
+        infos[nbuf] = p.kernel_info
+        outs[nbuf] = p.execute(x).cpu().numpy()
+        p.close()
+    monkeypatch.delenv("LC_UP3_NBUF")
+    assert np.array_equal(outs["1"], outs["2"])  # same arithmetic, different staging
+    s = _plan(n, "leg2cheb", batch=V, device=dev, engine=3).desc["s"]
+    rows = c4_rows(n, s, uniform=256, tiles=16)
+    for v in (0, V - 1):
+        check_rows("leg2cheb", xh[v].numpy(), outs["1"][v], rows, f"engine3 up nbuf n={n} V={V} v={v}")
