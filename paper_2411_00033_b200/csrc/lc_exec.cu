@@ -2692,11 +2692,12 @@ lc_status configure_kernels(lc_plan* p) {
 
   const int64_t budget2 = 113 * 1024;  // two CTAs per SM (228 KB minus 1 KB reserved per CTA)
   int vt = p->vt;
-  // automatic engine 3 (tools/engine_cross3.py on the B200): long vectors in batches of 8+ (>= 16 below
-  // n = 2^18), deep enough trees for ranges of >= 64 leaves; e.g. 64 x 10^7: 41.8 -> 22.9 ms per transform
+  // automatic engine 3 (tools/engine_cross_all.py on the B200, round 2): batches of 8+ long vectors with
+  // at least ~1.2e7 coefficients in all (below that the level-pipelined kernels win: 150000 x 64 engine 1
+  // 470 vs 486 us, 10^6 x 8 374 vs 461 us; above it engine 3: 10^6 x 16 518 vs 726 us, 3e6 x 8 810 vs
+  // 1588 us, 64 x 10^7 14.4 vs 36 ms), fewer 8-vector tiles than SMs (else the per-tile kernel)
   if (p->engine == 0 && p->part_count <= 1 && p->vt <= 0 && L >= 9 && p->s <= kTileSMax && p->batch >= 8 &&
-      (p->batch >= 16 || p->n >= 262144) &&
-      ((p->batch + kTileV - 1) / kTileV) < int64_t(p->sm_count))
+      p->n * p->batch >= 12000000 && ((p->batch + kTileV - 1) / kTileV) < int64_t(p->sm_count))
     p->engine = 3;
   if (p->engine == 3) {  // up kernel of 8-vector tiles feeding the per-range pass
     if (L < 1 || p->s > kTileSMax) return LC_ERR_INVALID_ARG;
