@@ -2692,12 +2692,13 @@ lc_status configure_kernels(lc_plan* p) {
 
   const int64_t budget2 = 113 * 1024;  // two CTAs per SM (228 KB minus 1 KB reserved per CTA)
   int vt = p->vt;
-  // automatic engine 3 (tools/engine_cross_all.py on the B200, round 2): batches of 8+ long vectors with
-  // at least ~1.2e7 coefficients in all (below that the level-pipelined kernels win: 150000 x 64 engine 1
-  // 470 vs 486 us, 10^6 x 8 374 vs 461 us; above it engine 3: 10^6 x 16 518 vs 726 us, 3e6 x 8 810 vs
-  // 1588 us, 64 x 10^7 14.4 vs 36 ms), fewer 8-vector tiles than SMs (else the per-tile kernel)
-  if (p->engine == 0 && p->part_count <= 1 && p->vt <= 0 && L >= 9 && p->s <= kTileSMax && p->batch >= 8 &&
-      p->n * p->batch >= 12000000 && ((p->batch + kTileV - 1) / kTileV) < int64_t(p->sm_count))
+  // automatic engine 3 (tools/engine_cross_all.py on the B200, round 2, ranges of >= 8 leaves): batches of
+  // 8+ vectors with at least ~1.6e6 coefficients in all (below, the level-pipelined kernels win: 65536 x 16
+  // engine 1 55 vs 68 us, 150000 x 8 70 vs 91 us; above, engine 3: 16384 x 128 73 vs 102 us, 10^6 x 8 267
+  // vs 374 us, 3e6 x 8 810 vs 1587 us, 64 x 10^7 14.4 vs 36 ms), fewer 8-vector tiles than SMs (else the
+  // per-tile kernel)
+  if (p->engine == 0 && p->part_count <= 1 && p->vt <= 0 && L >= 7 && p->s <= kTileSMax && p->batch >= 8 &&
+      p->n * p->batch >= 1600000 && ((p->batch + kTileV - 1) / kTileV) < int64_t(p->sm_count))
     p->engine = 3;
   if (p->engine == 3) {  // up kernel of 8-vector tiles feeding the per-range pass
     if (L < 1 || p->s > kTileSMax) return LC_ERR_INVALID_ARG;
@@ -2877,7 +2878,11 @@ lc_status configure_kernels(lc_plan* p) {
       const int64_t nls = std::min<int64_t>(int64_t(2) << L, (p->n + 2 * s - 1) / (2 * s));
       p->range_nle = int(nls);
       int64_t nr = std::max<int64_t>(1, slots / p->ntiles);  // units <= slots: one wave, no straggler round
-      nr = std::max<int64_t>(1, std::min(nr, nls / 64));  // ranges of >= 64 leaves (the entry chain is L deep)
+      // ranges of >= 8 leaves (LC_RANGE_MIN; entering a range costs the whole step-4 chain and the M2L of every
+      // level): the kernel time follows the leaf steps of one CTA, so below one wave shorter ranges win
+      int rmin = 8;
+      if (const char* e = std::getenv("LC_RANGE_MIN")) rmin = std::max(1, std::atoi(e));
+      nr = std::max<int64_t>(1, std::min<int64_t>(nr, nls / rmin));
       const int64_t rlen = (nls + nr - 1) / nr;
       nr = (nls + rlen - 1) / rlen;
       p->range_n = int(nr);

@@ -1,5 +1,5 @@
 """Time per transform of engines 1, 2, 3 (and the automatic choice) over (n, batch), CUDA events.
-usage: python tools/engine_cross_all.py"""
+usage: python tools/engine_cross_all.py [engines, e.g. 0,1,3] [n,n,...] [V,V,...]"""
 import sys
 
 import torch
@@ -9,13 +9,16 @@ from paper_2411_00033_b200 import Plan  # noqa: E402
 from paper_2411_00033_b200._lib import LegChebError  # noqa: E402
 
 dev = torch.device("cuda", 0)
-for n in (20000, 65536, 150000, 300000, 1000000, 3000000):
-    for V in (4, 8, 16, 32, 64, 128):
+ENG = [int(a) for a in sys.argv[1].split(",")] if len(sys.argv) > 1 else [0, 1, 2, 3]
+NS = [int(a) for a in sys.argv[2].split(",")] if len(sys.argv) > 2 else [20000, 65536, 150000, 300000, 1000000, 3000000]
+VS = [int(a) for a in sys.argv[3].split(",")] if len(sys.argv) > 3 else [4, 8, 16, 32, 64, 128]
+for n in NS:
+    for V in VS:
         if n * V > 2 * 10 ** 8:
             continue
         x = torch.randn(V, n, dtype=torch.float64, device=dev)
         res = {}
-        for e in (0, 1, 2, 3):
+        for e in ENG:
             try:
                 p = Plan(n, "leg2cheb", batch=V, device=dev, engine=e)
             except (LegChebError, RuntimeError):
