@@ -80,9 +80,9 @@ typedef struct {
   int32_t up_subtree; /* subtree depth of the upward (leaf projection + M2M) kernel; 0 -> automatic */
   int32_t engine;   /* 0 -> automatic; 1 -> level-pipelined kernels (up / streaming / down);
                        2 -> per-tile streaming kernel (one CTA per 8-vector tile, whole Alg. 4 on chip;
-                       needs L >= 1 and s <= 32; automatic choice from about one tile per SM, or a third of that for n <= 2048);
-                       3 -> up kernel of 8-vector tiles + the per-tile pass over leaf ranges (needs L >= 1, s <= 32;
-                       automatic for L >= 9 with >= 8 vectors from n = 2^18, >= 16 below, and fewer tiles than SMs) */
+                       needs L >= 1 and s <= 40; automatic choice from about one tile per SM, or a third of that for n <= 2048);
+                       3 -> up kernel of 8-vector tiles + the per-tile pass over leaf ranges (needs L >= 1, s <= 40;
+                       automatic for L >= 7 with >= 8 vectors and >= 1.6e6 coefficients in all, and fewer tiles than SMs) */
   int32_t part_index; /* partitioned plan (NEXT-2, one long transform over several GPUs): this plan computes */
   int32_t part_count; /* output rows [row_lo, row_hi) of part part_index of part_count (lc_partition); 0/1 -> all.
                          The input is the whole vector (the upward pass -- leaf projection and M2M, PAPER.md:363-379
@@ -254,8 +254,9 @@ lc_status lc_plan_export(const lc_plan* p, int32_t what, double* host_out, int64
 /* Kernel configuration chosen for the plan (diagnostic; host only, no device work).
  * out[0..] = stream_grid, smem_stream, smem_up, kup (up-kernel subtree depth), grup,
  * kb (band/down unit depth), cb (blocks per A_hat stage), nst (stages), vt, stream CTAs per
- * SM, m2l_units, band_units, up_grid (CTAs), kd (down-kernel subtree depth), smem_down, engine (1 or 2),
- * tile_grid and smem_tile (per-tile kernel, engine 2).  count = capacity of out; returns the number of
+ * SM, m2l_units, band_units, up_grid (CTAs), kd (down-kernel subtree depth), smem_down, engine (1, 2 or 3),
+ * tile_grid and smem_tile (per-tile kernel, engine 2; range kernel, engine 3), ranges and range_len
+ * (engine 3), up_ksub, part_lo, part_hi, part_up.  count = capacity of out; returns the number of
  * values written through *written (may be NULL).  Errors: INVALID_ARG on NULL p or out. */
 lc_status lc_plan_kernel_info(const lc_plan* p, int64_t* out, int32_t count, int32_t* written);
 
