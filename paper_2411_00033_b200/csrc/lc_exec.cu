@@ -219,6 +219,9 @@ struct DownParams {
   int64_t sub_lo;  // first subtree of a partitioned plan (NEXT-2), else 0
 };
 
+#ifndef LC_UP3_SKIP
+#define LC_UP3_SKIP 0  // experiment builds only: skip parts of the engine-3 up pass (1 w stores, 2 subtree M2M, 4 step 1)
+#endif
 // ============================================================== up kernel
 // Alg. a.1, rows [R0, R1) of one parent:
 // parent[n] = sum_{k<=n} b_nk (x0_k + (-1)^(n-k) x1_k)   (B(1) = B(0) with the odd diagonals
@@ -676,7 +679,7 @@ __global__ void __launch_bounds__(kThreads, 2) lc_up3_kernel(const __grid_consta
     cp_async_commit();
     if (nbuf == 2) cp_async_wait<1>(); else cp_async_wait<0>();  // the f of subtree j landed
     __syncthreads();
-    up_step1<VT, SMAX>(Ts, fs0 + (nbuf == 2 ? (j & 1) * fbuf : 0), fst, nleaf, s, tree + tree_off(k));
+    if (!(LC_UP3_SKIP & 4)) up_step1<VT, SMAX>(Ts, fs0 + (nbuf == 2 ? (j & 1) * fbuf : 0), fst, nleaf, s, tree + tree_off(k));
     __syncthreads();
     if (nbuf == 1 && j + 1 < J) {  // one buffer: the next subtree's f lands during this one's M2M and stores
       int64_t t1, r1;
@@ -686,6 +689,7 @@ __global__ void __launch_bounds__(kThreads, 2) lc_up3_kernel(const __grid_consta
     }
     double* wt = P.w + tile * P.w_tile;
     auto store_w = [&](int g, int64_t node, int cnt, const double* src) {  // cnt nodes of level g, [sigma][cnt][v][M]
+      if (LC_UP3_SKIP & 1) return;
       const int c2 = int(cnt * VM / 2);
       const double2* sp = reinterpret_cast<const double2*>(src);
       double2* d0 = reinterpret_cast<double2*>(wt + (w_level_offset_units(g) + node) * VM);
@@ -698,7 +702,7 @@ __global__ void __launch_bounds__(kThreads, 2) lc_up3_kernel(const __grid_consta
     };
     store_w(P.gr + k, R << k, nleaf, tree + tree_off(k));
     for (int lv = k; lv >= 1; --lv) {
-      m2m_level<VT>(Bs, tree + tree_off(lv), tree + tree_off(lv - 1), lv - 1);
+      if (!(LC_UP3_SKIP & 2)) m2m_level<VT>(Bs, tree + tree_off(lv), tree + tree_off(lv - 1), lv - 1);
       __syncthreads();
       store_w(P.gr + lv - 1, R << (lv - 1), 1 << (lv - 1), tree + tree_off(lv - 1));
     }
