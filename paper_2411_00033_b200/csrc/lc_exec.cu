@@ -1890,7 +1890,8 @@ __device__ __forceinline__ void band32(const double* __restrict__ fU, const doub
 template <int DIR, bool TT>
 __device__ __forceinline__ void step5_store(const TileParams& P, const double* __restrict__ Tq, int tr,
                                             const double* __restrict__ cc, const double* __restrict__ zb, int zst,
-                                            int64_t tile, int64_t i0, int mt, int s, int lr, int lc, bool v2ok) {
+                                            int64_t tile, int64_t i0, int mt, int s, int lr, int lc, bool v2ok,
+                                            double* ob0 = nullptr, double* ob1 = nullptr) {
   const int m = 8 * mt + lr;
   double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
 #pragma unroll
@@ -1918,7 +1919,9 @@ __device__ __forceinline__ void step5_store(const TileParams& P, const double* _
       z1 *= 2.0 * inv_pi;
     }
     if (gv >= P.batch) continue;
-    if (v2ok && i + 1 < P.n) {
+    if (ob0 && i + 1 < P.n) {  // hoisted row pointers of the lane's two vectors (vector layout, 16-byte stores)
+      *reinterpret_cast<double2*>((h ? ob1 : ob0) + i) = make_double2(z0, z1);
+    } else if (v2ok && i + 1 < P.n) {
       double* o = P.oblk ? P.out + (i / P.oblk) * P.batch * P.oblk + gv * P.oblk + i % P.oblk : P.out + gv * P.ld_out + i;
       *reinterpret_cast<double2*>(o) = make_double2(z0, z1);
     } else {
@@ -2026,6 +2029,10 @@ __global__ void __launch_bounds__(kTileThreads, LC_TILE_MINB) lc_tile_kernel(con
   const bool v2ok = step5_v2ok(P);  // 16-byte output stores
 
   for (int64_t tile = blockIdx.x; tile < P.ntiles; tile += gridDim.x) {
+    // the lane's two output rows (vectors 2 lc, 2 lc + 1) for step 7's 16-byte stores
+    const bool hoist = v2ok && !P.oblk && P.layout == LC_VEC_CONTIGUOUS;
+    double* const ob0 = hoist ? P.out + (tile * kTileV + 2 * lc) * P.ld_out : nullptr;
+    double* const ob1 = hoist ? P.out + (tile * kTileV + 2 * lc + 1) * P.ld_out : nullptr;
     for (int i = tid; i < (2 * ns + 1) * 2 * kTS; i += kTileThreads) cs[i] = 0.0;  // rows without M2L stay 0
     for (int i = tid; i < gs * 2 * 2 * kTS; i += kTileThreads) gc[i] = 0.0;
     {
@@ -2107,7 +2114,8 @@ __global__ void __launch_bounds__(kTileThreads, LC_TILE_MINB) lc_tile_kernel(con
         // ---- step 5 + 7 of leaf V1, row tile = warp (and 4 on warp 0 for s > 32), both parities
         if (!(LC_SKIP & 2) && V1 < nls)
           for (int mt = warp; 8 * mt < s; mt += 4)
-            step5_store<DIR, true>(P, Tq, TS, cslot(L - 1, V1), zbuf(V1), zst_, tile, int64_t(V1) * seglen, mt, s, lr, lc, v2ok);
+            step5_store<DIR, true>(P, Tq, TS, cslot(L - 1, V1), zbuf(V1), zst_, tile, int64_t(V1) * seglen, mt, s, lr, lc, v2ok,
+                                   ob0, ob1);
       } else {
         const int sg = warp & 1;
         if (warp < 6) {
