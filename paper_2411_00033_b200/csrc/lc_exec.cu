@@ -2394,6 +2394,9 @@ __global__ void __launch_bounds__(kTileThreads, STAGE ? 3 : LC_RANGE_MINB) lc_ra
     const int64_t tile = unit / P.nranges;
     const int Ua = int(unit - tile * P.nranges) * P.rlen;
     const int Ub = min(P.nle, Ua + P.rlen) - 1;
+    const bool hoist = v2ok && !P.oblk && P.layout == LC_VEC_CONTIGUOUS;  // step 7's row pointers per lane
+    double* const ob0 = hoist ? P.out + (tile * kTileV + 2 * lc) * P.ld_out : nullptr;
+    double* const ob1 = hoist ? P.out + (tile * kTileV + 2 * lc + 1) * P.ld_out : nullptr;
     // entering the range at its rightmost leaf Ub enters every level; the "step" Ub+1 only computes
     // the M2L of Ub's rows on all levels (and stages f(Ub+1), zero past the end)
     auto gentry = [&](int U) { return U == Ub ? 0 : gmin_of(U); };
@@ -2469,14 +2472,16 @@ __global__ void __launch_bounds__(kTileThreads, STAGE ? 3 : LC_RANGE_MINB) lc_ra
         TP_MARK(0);
         // ---- step 5 + 7 of leaf V1, row tile = warp, both parities (s > 32: on warps 4 and 5, below)
         if (!(LC_SKIP & 2) && s <= 32 && V1 >= Ua && V1 <= Ub && 8 * warp < s)
-          step5_store<DIR, false>(P, Tq, TR, cslot(L - 1, V1), zbuf(V1), zst_, tile, int64_t(V1) * seglen, warp, s, lr, lc, v2ok);
+          step5_store<DIR, false>(P, Tq, TR, cslot(L - 1, V1), zbuf(V1), zst_, tile, int64_t(V1) * seglen, warp, s, lr, lc, v2ok,
+                                  ob0, ob1);
       } else {
         const int sg = warp & 1;
         // s in (32, 40]: the band warps carry five row tiles, so step 5 + 7 of leaf V1 (its c and z
         // slots are not written in this step) runs on warps 4 and 5: row tiles {0, 2, 4} and {1, 3}
         if (!(LC_SKIP & 2) && s > 32 && warp < 6 && V1 >= Ua && V1 <= Ub)
           for (int mt = warp - 4; 8 * mt < s; mt += 2)
-            step5_store<DIR, false>(P, Tq, TR, cslot(L - 1, V1), zbuf(V1), zst_, tile, int64_t(V1) * seglen, mt, s, lr, lc, v2ok);
+            step5_store<DIR, false>(P, Tq, TR, cslot(L - 1, V1), zbuf(V1), zst_, tile, int64_t(V1) * seglen, mt, s, lr, lc, v2ok,
+                                    ob0, ob1);
         if (!(LC_SKIP & 4) && warp >= 6 && inU) {
           // ---- step 4 chain (sigma) over the levels entered at U, coarse to fine
           const int gA = gentry(U);
