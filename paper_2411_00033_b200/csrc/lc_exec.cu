@@ -1334,6 +1334,9 @@ __global__ void __launch_bounds__(kStreamThreads, 2) lc_stream_kernel(const __gr
 // Operator inputs are loaded into registers before the arithmetic and every dot product runs
 // as four partial sums, so a level costs one shared-memory round trip plus a 5-deep DFMA chain.
 constexpr int kDownThreads = 256;
+#ifndef LC_DOWN_NARROW_SPLIT
+#define LC_DOWN_NARROW_SPLIT 1  // narrow subtree levels split over (sigma, v, parent) warps when 2 VT < warps
+#endif
 
 // (B(p)^T c)_l = (-1)^{pl} sum_n b_nl (-1)^{pn} c_n   (lane l), with column l of
 // B(0) in registers (the ancestor chain and the narrow subtree levels reuse it), c broadcast from
@@ -1531,6 +1534,27 @@ __global__ void __launch_bounds__(NT, 512 / NT) lc_down_kernel(const DownParams 
       // narrow levels (j <= 3, at most 4 parents per sigma): one warp per (sigma, v) runs them one after
       // another, lane = mode, both children of a parent in one pass -- no CTA barrier between them
       const int jn = kd < 3 ? kd : 3;
+      if (LC_DOWN_NARROW_SPLIT && 2 * VT < nwarps) {
+        // few vectors (2 VT chains < warps): one warp per (sigma, v, parent) and a CTA barrier per level,
+        // so the 1 + 2 + 4 parents of a chain are not walked by one warp while the others wait (same
+        // arithmetic per element)
+        for (int j = 1; j <= jn; ++j) {
+          const int nodes = 1 << j, half = nodes >> 1;
+          const double* par = cm_lvl(j - 1);
+          double* cur = cm_lvl(j);
+          for (int it = warp; it < 2 * VT * half; it += nwarps) {
+            const int ch = it / half, Pn = it - ch * half;
+            const int sg = ch / VT, v = ch - sg * VT;
+            double r0, r1;
+            l2l_lane_pair(bcol, par + ((sg * half + Pn) * VT + v) * kM, lane, r0, r1);
+            if (lane < kM) {
+              cur[((sg * nodes + 2 * Pn) * VT + v) * kM + lane] += r0;
+              cur[((sg * nodes + 2 * Pn + 1) * VT + v) * kM + lane] += r1;
+            }
+          }
+          __syncthreads();
+        }
+      } else
       for (int ch = warp; ch < 2 * VT; ch += nwarps) {
         const int sg = ch / VT, v = ch - sg * VT;
         for (int j = 1; j <= jn; ++j) {
