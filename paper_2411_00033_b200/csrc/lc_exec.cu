@@ -1337,6 +1337,9 @@ constexpr int kDownThreads = 256;
 #ifndef LC_DOWN_NARROW_SPLIT
 #define LC_DOWN_NARROW_SPLIT 1  // narrow subtree levels split over (sigma, v, parent) warps when 2 VT < warps
 #endif
+#ifndef LC_DOWN_NARROW_JS
+#define LC_DOWN_NARROW_JS 4  // subtree levels run as lane operators when split (the rest on DMMA; 3: +0.25 us, 5: +2 us at 10^6)
+#endif
 
 // (B(p)^T c)_l = (-1)^{pl} sum_n b_nl (-1)^{pn} c_n   (lane l), with column l of
 // B(0) in registers (the ancestor chain and the narrow subtree levels reuse it), c broadcast from
@@ -1533,8 +1536,9 @@ __global__ void __launch_bounds__(NT, 512 / NT) lc_down_kernel(const DownParams 
     {
       // narrow levels (j <= 3, at most 4 parents per sigma): one warp per (sigma, v) runs them one after
       // another, lane = mode, both children of a parent in one pass -- no CTA barrier between them
-      const int jn = kd < 3 ? kd : 3;
-      if (LC_DOWN_NARROW_SPLIT && 2 * VT < nwarps) {
+      const bool split = LC_DOWN_NARROW_SPLIT && 2 * VT < nwarps;
+      const int jn = min(kd, split ? LC_DOWN_NARROW_JS : 3);
+      if (split) {
         // few vectors (2 VT chains < warps): one warp per (sigma, v, parent) and a CTA barrier per level,
         // so the 1 + 2 + 4 parents of a chain are not walked by one warp while the others wait (same
         // arithmetic per element)
