@@ -1337,6 +1337,9 @@ constexpr int kDownThreads = 256;
 #ifndef LC_DOWN_NARROW_SPLIT
 #define LC_DOWN_NARROW_SPLIT 1  // narrow subtree levels split over (sigma, v, parent) warps when 2 VT < warps
 #endif
+#ifndef LC_DOWN_PAR_ISSUE
+#define LC_DOWN_PAR_ISSUE 1  // bulk path: the c_m2l copies issued by the lanes of warp 0 (one copy each)
+#endif
 #ifndef LC_DOWN_NARROW_JS
 #define LC_DOWN_NARROW_JS 4  // subtree levels run as lane operators when split (the rest on DMMA; 3: +0.25 us, 5: +2 us at 10^6)
 #endif
@@ -1454,7 +1457,28 @@ __global__ void __launch_bounds__(NT, 512 / NT) lc_down_kernel(const DownParams 
   __syncthreads();
   LC_TS(2, 1);
   if (bulk) {
-    if (tid == 0) {
+    if (LC_DOWN_PAR_ISSUE && warp == 0) {
+      // the arrival with the byte count first, then one bulk copy per lane (c_m2l of the gd ancestors and
+      // of the kd + 1 subtree levels, both parities): issued in parallel instead of by one thread
+      const uint32_t total = L > 0 ? uint32_t(gd + (2 << kd) - 1) * 2u * uint32_t(VM) * 8u : 0u;
+      if (lane == 0) mbar_arrive_expect_tx(&dbar, total);  // the phase completes with every copy
+      __syncwarp();
+      if (L > 0) {
+        const uint64_t pol = policy_evict_first();
+        for (int c = lane; c < 2 * (gd + kd + 1); c += 32) {
+          const int sg = c & 1;
+          if (c < 2 * gd) {
+            const int g = c >> 1;
+            bulk_g2s(cm_anc(g) + sg * VM, ct + (w_level_offset_units(g) + sg * nseg(g) + (R >> (gd - g))) * VM,
+                     uint32_t(VM) * 8u, &dbar, pol);
+          } else {
+            const int j = (c >> 1) - gd;
+            bulk_g2s(cm_lvl(j) + sg * (1 << j) * VM, ct + (w_level_offset_units(gd + j) + sg * nseg(gd + j) + (R << j)) * VM,
+                     uint32_t((1 << j) * VM) * 8u, &dbar, pol);
+          }
+        }
+      }
+    } else if (!LC_DOWN_PAR_ISSUE && tid == 0) {
       const uint32_t total = L > 0 ? uint32_t(gd + (2 << kd) - 1) * 2u * uint32_t(VM) * 8u : 0u;
       mbar_arrive_expect_tx(&dbar, total);  // the arrival: the phase completes with every copy
       const uint64_t pol = policy_evict_first();
