@@ -270,6 +270,41 @@ __device__ __forceinline__ void m2m_rows(const double* __restrict__ Bs, const do
   m2m_rows_core<R0, R1>(Bs, zp, zm, out);
 }
 
+// m2m_rows for one vector per item (VT = 1): a warp's items lie 36 doubles apart, so the 16-byte chunk
+// c of every lane's x falls into the bank groups 2P + c (mod 8), half of them; lanes of odd quads load
+// the chunks of each pair (c, c ^ 1) in swapped order, so that each load of a warp covers all eight
+// groups (no 2-way conflicts), and the pair is swapped back in registers (same arithmetic)
+#ifndef LC_M2M_ROT
+#define LC_M2M_ROT 1
+#endif
+template <int R0, int R1>
+__device__ __forceinline__ void m2m_rows_rot(const double* __restrict__ Bs, const double* __restrict__ x0,
+                                             const double* __restrict__ x1, double* __restrict__ out, bool odd) {
+  constexpr int NC = (R1 + 1) / 2;
+  double2 ta[NC], tb[NC];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    const int cp = (c ^ 1) < NC ? (c ^ 1) : c;
+    const int cl = odd ? cp : c;
+    ta[c] = *reinterpret_cast<const double2*>(x0 + 2 * cl);
+    tb[c] = *reinterpret_cast<const double2*>(x1 + 2 * cl);
+  }
+  double zp[R1], zm[R1];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    const int cp = (c ^ 1) < NC ? (c ^ 1) : c;
+    const double2 a2 = odd ? ta[cp] : ta[c];
+    const double2 b2 = odd ? tb[cp] : tb[c];
+    zp[2 * c] = a2.x + b2.x;
+    zm[2 * c] = a2.x - b2.x;
+    if (2 * c + 1 < R1) {
+      zp[2 * c + 1] = a2.y + b2.y;
+      zm[2 * c + 1] = a2.y - b2.y;
+    }
+  }
+  m2m_rows_core<R0, R1>(Bs, zp, zm, out);
+}
+
 // one tree level in shared memory ([sigma][node][v][M]); one thread per (row group, sigma,
 // parent, v), each warp on a single row group: [0,10), [10,15), [15,18) carry 55, 65 and 51
 // DFMA.  Six of the eight warps work; a level is one round for up to 64 (sigma, parent, v).
@@ -289,7 +324,15 @@ __device__ __forceinline__ void m2m_level(const double* __restrict__ Bs, const d
     const int sg = sp >> lp;
     const double* x0 = ch + ((sg * 2 * np + 2 * P) * VT + v) * kM;
     double* o = pa + r * kM;
-    if (rg == 0)
+    if (VT == 1 && LC_M2M_ROT && per >= 32) {  // whole warps of items (narrow levels: no conflicts to remove)
+      const bool odd = (lane >> 2) & 1;
+      if (rg == 0)
+        m2m_rows_rot<0, 10>(Bs, x0, x0 + VT * kM, o, odd);
+      else if (rg == 1)
+        m2m_rows_rot<10, 15>(Bs, x0, x0 + VT * kM, o, odd);
+      else
+        m2m_rows_rot<15, 18>(Bs, x0, x0 + VT * kM, o, odd);
+    } else if (rg == 0)
       m2m_rows<0, 10>(Bs, x0, x0 + VT * kM, o);
     else if (rg == 1)
       m2m_rows<10, 15>(Bs, x0, x0 + VT * kM, o);
