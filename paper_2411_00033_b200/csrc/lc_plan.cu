@@ -20,6 +20,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <algorithm>
+#include <chrono>
 #include <mutex>
 #include <unordered_map>
 #include <utility>
@@ -272,16 +273,20 @@ static void build_T(int64_t s, std::vector<double>& T, std::vector<double>& Tt) 
 }
 
 int64_t band_nnz(int64_t N, int64_t s) {
-  // nonzeros (i, i+2k) of A with i <= j < j_end(i) = min(N, 2s(floor(i/2s)+2))
-  int64_t tot = 0;
+  // nonzeros (i, i+2k) of A with i <= j < j_end(i) = min(N, 2s(floor(i/2s)+2)).  Every segment u whose
+  // window ends inside the matrix (2s(u+2) <= N) has the same count, so only one of them and the last
+  // (at most two) segments are summed row by row: O(s) instead of O(N) on the host.
   const int64_t seg = 2 * s;
-  for (int64_t u = 0; u * seg < N; ++u) {
+  auto seg_sum = [&](int64_t u) {
+    int64_t tot = 0;
     const int64_t je = std::min<int64_t>(N, seg * (u + 2));
-    for (int64_t r = 0; r < seg && u * seg + r < N; ++r) {
-      const int64_t i = u * seg + r;
-      tot += (je - i + 1) / 2;
-    }
-  }
+    for (int64_t r = 0; r < seg && u * seg + r < N; ++r) tot += (je - (u * seg + r) + 1) / 2;
+    return tot;
+  };
+  const int64_t nu = (N + seg - 1) / seg;
+  const int64_t nfull = std::max<int64_t>(0, N / seg - 1);
+  int64_t tot = nfull > 0 ? nfull * seg_sum(0) : 0;
+  for (int64_t u = nfull; u < nu; ++u) tot += seg_sum(u);
   return tot;
 }
 
@@ -385,6 +390,7 @@ lc_status configure_kernels(lc_plan* p);  // lc_exec.cu
 
 extern "C" lc_status lc_plan_create(lc_plan** out, int64_t n, lc_direction dir, int64_t batch,
                                     const lc_plan_opts* opts) {
+  const auto t_create = std::chrono::steady_clock::now();
   if (out == nullptr || n < 1 || batch < 1) return LC_ERR_INVALID_ARG;
   *out = nullptr;
   if (dir != LC_LEG2CHEB && dir != LC_CHEB2LEG) return LC_ERR_INVALID_ARG;
@@ -404,19 +410,29 @@ extern "C" lc_status lc_plan_create(lc_plan** out, int64_t n, lc_direction dir, 
 
   int dev = o.device;
   if (dev < 0) LC_CUDA_TRY(cudaGetDevice(&dev));
-  cudaDeviceProp prop;
-  LC_CUDA_TRY(cudaGetDeviceProperties(&prop, dev));
-  if (prop.major != 10) return LC_ERR_UNSUPPORTED_DEVICE;
+  // two attribute queries (microseconds) instead of cudaGetDeviceProperties (it fills the whole structure)
+  int cc_major = 0, sm_count = 0;
+  LC_CUDA_TRY(cudaDeviceGetAttribute(&cc_major, cudaDevAttrComputeCapabilityMajor, dev));
+  LC_CUDA_TRY(cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, dev));
+  if (cc_major != 10) return LC_ERR_UNSUPPORTED_DEVICE;
   int prev_dev = 0;
   LC_CUDA_TRY(cudaGetDevice(&prev_dev));
   LC_CUDA_TRY(cudaSetDevice(dev));
 
+  // LC_PLAN_TRACE=1: host wall time of the stages of plan creation on stderr (tools/plan_wall.py)
+  static const bool trace = std::getenv("LC_PLAN_TRACE") != nullptr;
+  auto mark = [&](const char* what) {
+    if (trace)
+      std::fprintf(stderr, "lc_plan_create %-12s %8.3f ms\n", what,
+                   std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_create).count());
+  };
+  mark("device");
   lc_plan* p = new lc_plan();
   std::memset(p, 0, sizeof(*p));
   const Geometry G = geometry(n, o.s_hat);
   p->n = n; p->N = G.N; p->L = G.L; p->s = G.s; p->M = kM; p->batch = batch; p->nc = G.nc;
   p->dir = int(dir); p->layout = o.layout; p->ld_in = o.ld_in; p->ld_out = o.ld_out;
-  p->device = dev; p->sm_count = prop.multiProcessorCount;
+  p->device = dev; p->sm_count = sm_count;
   p->vt = o.vt; p->k = o.subtree; p->bps = o.stage_blocks; p->nst = o.stages; p->kup = o.up_subtree;
   p->engine = o.engine;
   p->out_block = o.out_block;
@@ -469,6 +485,7 @@ extern "C" lc_status lc_plan_create(lc_plan** out, int64_t n, lc_direction dir, 
   if (p->nc > 0) LC_PTRY(cudaMallocAsync(reinterpret_cast<void**>(&p->d_A), sizeof(double) * size_t(p->nc) * kMM, os));
   p->plan_bytes = sizeof(double) * (size_t(p->N) + size_t(2 * s) + size_t(4 * s * kM) + kMM + size_t(p->nc) * kMM);
 
+  mark("malloc");
   double B[kMM];
   build_B0(B);
   std::vector<double> T, Tt;
@@ -484,6 +501,7 @@ extern "C" lc_status lc_plan_create(lc_plan** out, int64_t n, lc_direction dir, 
       tri[2 * u] = (unsigned char)m;
       tri[2 * u + 1] = (unsigned char)nn;
     }
+  mark("host tables");
   double* d_Lm = nullptr;  // Lambda^- of every level: L x 2 x M x M
   if (p->L > 0) LC_PTRY(cudaMallocAsync(reinterpret_cast<void**>(&d_Lm), sizeof(double) * size_t(2 * p->L) * kMM, os));
   // pageable sources: these copies return once the host data has been staged
@@ -498,6 +516,7 @@ extern "C" lc_status lc_plan_create(lc_plan** out, int64_t n, lc_direction dir, 
     LC_PTRY(cudaStreamSynchronize(os));
   }
 
+  mark("copies");
   {
     cudaEvent_t pe[2] = {nullptr, nullptr};
     LC_PTRY(cudaEventCreate(&pe[0]));
@@ -524,6 +543,7 @@ extern "C" lc_status lc_plan_create(lc_plan** out, int64_t n, lc_direction dir, 
     LC_PTRY(es);
   }
   if (d_Lm) cudaFreeAsync(d_Lm, os);
+  mark("kernels");
 
   p->band_nnz = band_nnz(p->N, s);
   {
@@ -548,8 +568,10 @@ extern "C" lc_status lc_plan_create(lc_plan** out, int64_t n, lc_direction dir, 
     LC_PTRY(cudaMemcpyAsync(p->d_Tpad, p->h_Tpad, sizeof(double) * size_t(2 * smax_rows * kM), cudaMemcpyHostToDevice,
                             os));
   }
+  mark("Tpad");
   const lc_status cs = configure_kernels(p);
   if (cs != LC_OK) return fail(cs);
+  mark("configure");
   {
     p->stage_bytes = size_t(align_up(in_extent(p) * 8, 256) + align_up(out_extent(p) * 8, 256));
   }
@@ -557,6 +579,7 @@ extern "C" lc_status lc_plan_create(lc_plan** out, int64_t n, lc_direction dir, 
   LC_PTRY(cudaMemsetAsync(p->d_ws, 0, p->ws_bytes > 0 ? p->ws_bytes : 16, os));
   // the plan's arrays are complete before any caller stream can see the plan
   LC_PTRY(cudaStreamSynchronize(os));
+  mark("workspace");
   cudaSetDevice(prev_dev);
   *out = p;
   return LC_OK;

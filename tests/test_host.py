@@ -115,10 +115,12 @@ def test_band_nnz_is_about_1p5_sN():
     for n in (4096, 1 << 16, 10**6):
         g = geometry(n)
         assert abs(g["band_nnz"] / (1.5 * g["s"] * g["N"]) - 1) < 0.05
-    g = geometry(4096)
-    N, s = g["N"], g["s"]
-    brute = sum((j_end(i, s, N) - i + 1) // 2 for i in range(N))
-    assert g["band_nnz"] == brute
+    # exact against brute force over every row (the library sums one interior segment and the last two)
+    for n, s_hat in ((4096, 0), (1, 0), (37, 0), (130, 16), (1000, 24), (5001, 64), (65537, 0), (30000, 48)):
+        g = geometry(n, s_hat)
+        N, s = g["N"], g["s"]
+        brute = sum((j_end(i, s, N) - i + 1) // 2 for i in range(N))
+        assert g["band_nnz"] == brute, (n, s_hat)
 
 
 def test_flop_model_lemma2():
