@@ -94,7 +94,7 @@ def blockwise_einf(y: np.ndarray, x: np.ndarray, block: int) -> float:
 # that is wrong at 1e-10 of its own scale (tests/test_gpu_fullsize.py plants one at 1e-9).
 BLOCK_RT = 1e-10
 BLOCK_RT_SIGNED = 1e-13  # inputs with random signs
-DIAG_MEASURED = 2.5e-14  # largest per-row diagnostic seen (tools/fuzz_parity.py, 1360 cases; the suite: 1.4e-14, C2L, s_hat = 24, n = 70001)
+DIAG_MEASURED = 2.6e-14  # largest per-row diagnostic seen (tools/fuzz_parity.py, 3360 cases; the suite: 1.4e-14, C2L, s_hat = 24, n = 70001)
 
 
 def check_round_trip(x: np.ndarray, y: np.ndarray, s: int, tag: str = "", block_bound: float = BLOCK_RT):

@@ -1,6 +1,6 @@
 """Seeded fuzz of the three engines with non-decaying inputs (tools/fuzz_parity.py): random n, batch, direction,
 layout and s_hat; the oracle on C-4 rows at the plan's own s with the per-row diagnostic, and the engines against
-each other per 2s-block.  The test runs 32 cases; 1360 cases (seeds 7, 11 and 23, n up to 3e6) are recorded in
+each other per 2s-block.  The test runs 32 cases; 3360 cases (seeds 7, 11, 23 and 101, n up to 3e6) are recorded in
 profiles/r2_fuzz_parity.txt."""
 import os
 import subprocess
